@@ -1,0 +1,133 @@
+/*
+ * aol_b200.h — C ABI of libaolb200.so, the B200 (sm_100a) Array-OL repetitive-task engine.
+ *
+ * This is the drop-in boundary below the Python host mirror
+ * (paper_1105_4424_b200/executor.py).  It replaces the body of the
+ * reference's per-device launch loop, i.e. what
+ *     gmodelc.refexec.execute_schedule -> run_device -> "for launch in step.launches"
+ * does at /root/reference/pkg/src/gmodelc/refexec.py:476-516, and it follows the
+ * kernel parameter convention the reference's code generator emits for the
+ * same launch (codegen.py:105-123: `first, count`, then the ports in
+ * IntrinsicSpec order, host-resident scalar inputs by value).
+ *
+ * Plain C types only: no torch or C++ types cross this boundary.
+ *  - Ownership: the caller owns every port buffer (device pointers) and every
+ *    stream; the library never frees caller memory.  The library owns only
+ *    per-process tensor-map/attribute caches and its thread-local error text.
+ *  - Errors: functions return AOL_OK (0) or a negative aol_status; the message
+ *    of the last failure on the calling thread is returned by aol_last_error().
+ *    Validation failures are reported before anything is launched.
+ *  - Threading: launches are asynchronous on the caller's stream; the library
+ *    keeps no mutable global state besides lazily-initialised caches guarded
+ *    by a mutex.
+ */
+#ifndef AOL_B200_H
+#define AOL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AOL_ABI_VERSION 1
+#define AOL_MAX_RANK 4      /* array / repetition / pattern rank limit */
+#define AOL_MAX_TILERS 4    /* tiled ports per task */
+#define AOL_MAX_PORTS 8
+
+typedef enum aol_status {
+  AOL_OK = 0,
+  AOL_EINVAL = -1,        /* malformed task / tiler / arguments */
+  AOL_ECUDA = -2,         /* CUDA runtime or driver failure */
+  AOL_EUNSUPPORTED = -3,  /* op/dtype combination not implemented */
+  AOL_ENODEV = -4         /* no sm_100 device visible */
+} aol_status;
+
+typedef enum aol_dtype { AOL_F32 = 0, AOL_F64 = 1, AOL_I32 = 2, AOL_I64 = 3 } aol_dtype;
+
+/* Elementary tasks.  1..15: the reference's identity-tiler device intrinsics
+ * (intrinsics.py:51-83); 16..: Array-OL tile intrinsics. */
+typedef enum aol_op {
+  AOL_OP_COPY = 1,        /* ports: src, dst                            dst[i] = src[i]        */
+  AOL_OP_SUB = 2,         /* ports: x, y, z                             z[i] = x[i] - y[i]     */
+  AOL_OP_SCALE = 3,       /* ports: y;     scalars: a                   y[i] *= a              */
+  AOL_OP_AXPY = 4,        /* ports: y, x;  scalars: a (if n_scalars=1)  y[i] += a*x[i] | x[i]  */
+  AOL_OP_SPMV_CSR = 5,    /* ports: rowptr, colidx, values, x, y        row-wise, left to right */
+  AOL_OP_DOT_PARTIAL = 6, /* ports: a, b, partial (1 element, device)   partial = sum a[i]*b[i] */
+  AOL_OP_TILE_COPY = 16,  /* ports: src, dst           tilers: src, dst                        */
+  AOL_OP_MATMUL = 17,     /* ports: a, b, c            tilers: a, b, c   c = sum_k a_k * b_k   */
+  AOL_OP_TILE_FILTER = 18,/* ports: x, w, y            tilers: x, y      y_j = sum_i w_ji x_i  */
+  AOL_OP_TILE_SUM = 19    /* ports: x, s               tilers: x, s      s = sum_i x_i         */
+} aol_op;
+
+typedef enum aol_precision {
+  AOL_PREC_DEFAULT = 0,   /* matmul: TF32 tensor cores; everything else: exact order */
+  AOL_PREC_TF32 = 1,      /* matmul on tcgen05 kind::tf32 (tolerance stated in DESIGN.md) */
+  AOL_PREC_3XTF32 = 2,    /* matmul on tcgen05 with hi/lo split, ~fp32 accuracy */
+  AOL_PREC_EXACT = 3      /* CUDA cores, pattern order, no FMA: bit-exact vs the oracle */
+} aol_precision;
+
+/* e(r,i) = (origin + paving.r + fitting.i) mod array   (component-wise, Euclidean)
+ * off    = row-major flat offset of e in `array`.
+ * r = row-major unravel of the repetition index over rep[0..rep_rank),
+ * i = row-major unravel of the pattern index over pattern[0..pat_rank). */
+typedef struct aol_tiler {
+  int32_t arr_rank, rep_rank, pat_rank, reserved;
+  int64_t array[AOL_MAX_RANK];
+  int64_t rep[AOL_MAX_RANK];
+  int64_t pattern[AOL_MAX_RANK];
+  int64_t origin[AOL_MAX_RANK];
+  int64_t paving[AOL_MAX_RANK][AOL_MAX_RANK];   /* [array dim][repetition dim] */
+  int64_t fitting[AOL_MAX_RANK][AOL_MAX_RANK];  /* [array dim][pattern dim]    */
+} aol_tiler;
+
+typedef struct aol_task {
+  int32_t op;              /* aol_op */
+  int32_t dtype;           /* aol_dtype of the value ports */
+  int32_t index_dtype;     /* AOL_I32 / AOL_I64: spmv rowptr/colidx */
+  int32_t precision;       /* aol_precision */
+  int32_t n_tilers;        /* tiled ports, in IntrinsicSpec port order */
+  int32_t n_scalars;       /* host-resident scalar inputs passed by value */
+  int32_t reserved[2];
+  aol_tiler tilers[AOL_MAX_TILERS];
+} aol_task;
+
+/* ABI version of the loaded library (== AOL_ABI_VERSION). */
+int aol_abi_version(void);
+
+/* Message of the last failure on this thread ("" if none). */
+const char* aol_last_error(void);
+
+/* Number of visible sm_100 devices; fails with AOL_ENODEV if none. */
+int aol_device_count(int* n);
+
+/* Validate a task without launching (same checks aol_launch performs). */
+int aol_validate(const aol_task* task);
+
+/* One launch of a repetitive task over repetitions [first, first+count) on the
+ * current device, asynchronously on `stream` (a cudaStream_t; NULL = legacy
+ * default stream).  `ports` are device pointers in IntrinsicSpec order
+ * (intrinsics.py:51-83 for reference ops); `scalars` are host scalar inputs.
+ * Replaces one iteration of refexec.py:488-514 / one clEnqueueNDRangeKernel of
+ * the generated host code (codegen.py:456-457). */
+int aol_launch(const aol_task* task, int64_t first, int64_t count,
+               void* const* ports, const double* scalars, void* stream);
+
+/* Kernel variant aol_launch would pick for this task (diagnostics / tests):
+ * writes a NUL-terminated name into buf. */
+int aol_plan_name(const aol_task* task, int64_t first, int64_t count,
+                  void* const* ports, char* buf, int buflen);
+
+/* Debug / parity: flat offsets off(r, i) for r in [first, first+count) computed
+ * on the GPU into out_dev[(r-first)*pattern_total + i] (int64, device memory). */
+int aol_tiler_offsets(const aol_tiler* tiler, int64_t first, int64_t count,
+                      int64_t* out_dev, void* stream);
+
+/* Number of kernels this library has launched in this process (evidence counter). */
+int64_t aol_launch_counter(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* AOL_B200_H */

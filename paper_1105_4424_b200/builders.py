@@ -1,0 +1,98 @@
+"""Programmatic single-task models — the reference test harness, without its DSL.
+
+Builds the model that the reference suite writes as text in
+``SINGLE_TASK`` / ``_single_task_model`` (pkg/tests/test_refexec.py:250-293):
+a host (cpu + hostRam), one device processor ``dev.cu`` of 4 compute units
+x 8 processing elements, and a ``dev.gmem`` global memory; one repetitive
+task ``t`` of type ``T`` deployed on ``dev.cu`` inside root ``m``.  Port and
+allocation specs use the same strings as that harness
+(``"src in float32 [64]"``, ``"allocate data i onto dev.gmem"``), so the
+GPU tests read like the reference's own.
+"""
+
+from __future__ import annotations
+
+import re
+
+from .model import (AllocationLink, AllocKind, Component, ComponentKind, Connector, DataType, Direction,
+                    FlowPort, HwStereotype, MemoryRole, Model, PartInstance, Shape, StereotypeKind)
+from .tiler import Tiler
+
+_PORT = re.compile(r"^\s*(\w+)\s+(in|out|inout)\s+(float32|float64|int32|int64)\s+\[([\d,\s]+)\]\s*$")
+_ALLOC = re.compile(r"^\s*allocate\s+(data|task)\s+([\w.]+)\s+onto\s+([\w.]+)\s*$")
+
+
+def port(spec: str) -> FlowPort:
+    m = _PORT.match(spec)
+    if not m:
+        raise ValueError(f"bad port spec {spec!r}")
+    dims = tuple(int(d) for d in m.group(4).split(","))
+    return FlowPort(m.group(1), Direction(m.group(2)), Shape(dims), DataType(m.group(3)))
+
+
+def platform(cus: int = 4, pes: int = 8, local_capacity: int | None = None) -> dict:
+    P = ComponentKind.PLATFORM
+    comps = {
+        "Host": Component("Host", P, parts=(PartInstance("cpu", "Cpu"), PartInstance("ram", "Ram"))),
+        "Cpu": Component("Cpu", P, stereotype=HwStereotype(StereotypeKind.PROCESSOR)),
+        "Ram": Component("Ram", P, stereotype=HwStereotype(StereotypeKind.MEMORY, MemoryRole.HOST_RAM)),
+        "Pe": Component("Pe", P, stereotype=HwStereotype(StereotypeKind.PROCESSOR)),
+        "Cu": Component("Cu", P, parts=(PartInstance("pe", "Pe", Shape((pes,))),)
+                        + ((PartInstance("lmem", "Lmem"),) if local_capacity else ()),
+                        stereotype=HwStereotype(StereotypeKind.PROCESSOR)),
+        "Gmem": Component("Gmem", P, stereotype=HwStereotype(StereotypeKind.MEMORY, MemoryRole.DEVICE_GLOBAL)),
+        "Cmem": Component("Cmem", P, stereotype=HwStereotype(StereotypeKind.MEMORY, MemoryRole.DEVICE_CONSTANT)),
+        "Dev": Component("Dev", P, parts=(PartInstance("cu", "Cu", Shape((cus,))), PartInstance("gmem", "Gmem"),
+                                          PartInstance("cmem", "Cmem"))),
+        "p": Component("p", P, parts=(PartInstance("host", "Host"), PartInstance("dev", "Dev"))),
+    }
+    if local_capacity:
+        comps["Lmem"] = Component("Lmem", P, stereotype=HwStereotype(
+            StereotypeKind.MEMORY, MemoryRole.DEVICE_LOCAL, capacity_bytes=local_capacity))
+    return comps
+
+
+def allocation(spec: str) -> AllocationLink:
+    m = _ALLOC.match(spec)
+    if not m:
+        raise ValueError(f"bad allocation spec {spec!r}")
+    return AllocationLink(AllocKind(m.group(1)), m.group(2), m.group(3))
+
+
+def single_task_model(op: str, ports, root_ports, conns, allocs, n=None, *, repeat=None,
+                      tilers: dict[str, Tiler] | None = None) -> Model:
+    """The reference harness's one-task model; ``repeat`` (dims) overrides ``[n]``."""
+    A = ComponentKind.APPLICATION
+    rep = Shape(tuple(repeat)) if repeat is not None else (Shape((n,)) if n is not None else None)
+    task = Component("T", A, ports=tuple(port(p) for p in ports), repetition_space=rep, elementary_op=op,
+                     tilers=tuple(sorted((tilers or {}).items())))
+    conn = []
+    for c in conns:
+        src, dst = (s.strip() for s in c.split("->"))
+        conn.append(Connector(src, dst))
+    root = Component("m", A, ports=tuple(port(p) for p in root_ports), parts=(PartInstance("t", "T"),),
+                     connectors=tuple(conn))
+    return Model(platform_components=platform(), application_components={"T": task, "m": root},
+                 platform_root="p", application_root="m",
+                 allocations=tuple(allocation(a) for a in allocs))
+
+
+def tile_task_model(op: str, ports: dict[str, str], tilers: dict[str, Tiler], repeat) -> Model:
+    """Single tile-intrinsic task whose root ports mirror the task ports one to one.
+
+    ``ports`` maps task port name -> "<dir> <dtype> [dims]"; root port names
+    are the task port names prefixed with ``p_``.
+    """
+    tp, rp, conns, allocs = [], [], [], []
+    for name, spec in ports.items():
+        tp.append(f"{name} {spec}")
+        rp.append(f"p_{name} {spec}")
+        d = spec.split()[0]
+        if d == "out":
+            conns.append(f"t.{name} -> p_{name}")
+            allocs.append(f"allocate data t.{name} onto dev.gmem")
+        else:
+            conns.append(f"p_{name} -> t.{name}")
+            allocs.append(f"allocate data p_{name} onto dev.gmem")
+    allocs.append("allocate task t onto dev.cu")
+    return single_task_model(op, tp, rp, conns, allocs, repeat=repeat, tilers=tilers)

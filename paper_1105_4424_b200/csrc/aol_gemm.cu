@@ -1,0 +1,405 @@
+// MatMul elementary task on the 5th-generation tensor cores (tcgen05, kind::tf32).
+//
+// Used when the three tilers of a `matmul` task are the canonical GEMM triple
+// up to leading dimensions / operand majorness:
+//     a: off = ca + sa_m*m + sa_k*k     b: off = cb + sb_n*n + sb_k*k
+//     c: off = cc + ldc*m + n           repetition space [M, N], pattern [K]
+// The launch covers the linear repetition range [first, first+count) of [M, N]
+// (one reference launch, refexec.py:488-490); the epilogue masks the ragged
+// first/last rows, so unaligned shards (D = 3, 5, ...) are exact.
+//
+// Structure (one CTA per SM, persistent over output tiles):
+//   warp 0      TMA producer: A/B k-blocks -> 4-stage smem ring (128B swizzle)
+//   warp 1      MMA issuer:   one thread issues tcgen05.mma 128x256x8 into TMEM
+//   warp 2      TMEM allocator (512 columns = two 128x256 fp32 accumulators)
+//   warps 4..7  epilogue:     tcgen05.ld TMEM -> registers -> masked st.global
+// Two accumulators let the epilogue of tile i overlap the MMAs of tile i+1.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "aol_common.cuh"
+
+namespace aol {
+namespace gemm {
+
+constexpr int BM = 128, BN = 256, BK = 32, STAGES = 4;
+constexpr int UMMA_K = 8;                       // tf32: 32 bytes of K per MMA
+constexpr int A_BYTES = BM * BK * 4;            // 16 KB
+constexpr int B_BYTES = BN * BK * 4;            // 32 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;  // 48 KB
+constexpr int NUM_THREADS = 256;
+constexpr int TMEM_COLS = 512;
+constexpr int GROUP_M = 16;                     // tile raster: 16 M-tiles share each B panel
+constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+
+struct Params {
+  float* c;            // C + cc
+  int64_t ldc;
+  int64_t M, N, K;
+  int64_t m_lo, m_hi;  // inclusive row range of this launch
+  int64_t first, last; // inclusive linear repetition range
+  int m_tiles, n_tiles, k_blocks, num_tiles;
+  int c_vec;           // 16-byte stores allowed
+};
+
+// ------------------------------------------------------------ PTX helpers ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// 32 lanes x 32 consecutive 32-bit columns: thread i of the warp gets row (lane base + i).
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Shared-memory matrix descriptor (tcgen05 "version 1"), SWIZZLE_128B.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
+}
+
+// Operand tile of R rows (M or N) x BK:
+//   K-major : one TMA box {BK, R}; rows of 128 B; 8-row atoms 1024 B apart (SBO);
+//             the k-th MMA slice starts 32 B further inside the swizzle row.
+//   MN-major: R/32 boxes {32, BK}; each box = BK rows (k) of 32 elements (128 B);
+//             boxes 4 KB apart (LBO), 8-k-row groups 1024 B apart (SBO);
+//             the k-th MMA slice starts 8 rows (1024 B) further.
+template <bool KMAJOR>
+__device__ __forceinline__ uint64_t operand_desc(uint32_t base, int k) {
+  if (KMAJOR) return smem_desc(base + k * (UMMA_K * 4), 16, 1024);
+  return smem_desc(base + k * (UMMA_K * 128), BK * 128, 1024);
+}
+
+template <bool KMAJOR, int R>
+__device__ __forceinline__ void load_operand(const CUtensorMap* map, uint64_t* bar, uint8_t* dst, int kcoord,
+                                             int rcoord) {
+  if (KMAJOR) {
+    tma_load_2d(map, bar, dst, kcoord, rcoord);
+  } else {
+#pragma unroll
+    for (int c = 0; c < R / 32; ++c) tma_load_2d(map, bar, dst + c * (BK * 128), rcoord + 32 * c, kcoord);
+  }
+}
+
+__device__ __forceinline__ void tile_coords(const Params& p, int tile, int& mt, int& nt) {
+  const int per_group = GROUP_M * p.n_tiles;
+  const int g = tile / per_group;
+  const int first_m = g * GROUP_M;
+  const int gm = min(GROUP_M, p.m_tiles - first_m);
+  const int in = tile - g * per_group;
+  mt = first_m + in % gm;
+  nt = in / gm;
+}
+
+template <bool A_KMAJOR, bool B_KMAJOR>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    k_gemm_tf32(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&map_a);
+    prefetch_tmap(&map_b);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------------------------------------------- TMA producer ----
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        int mt, nt;
+        tile_coords(p, tile, mt, nt);
+        const int row0 = (int)(p.m_lo + (int64_t)mt * BM), col0 = nt * BN;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * STAGE_BYTES;
+          uint8_t* sb = sa + A_BYTES;
+          mbar_expect_tx(&full[stage], STAGE_BYTES);
+          load_operand<A_KMAJOR, BM>(&map_a, &full[stage], sa, kb * BK, row0);
+          load_operand<B_KMAJOR, BN>(&map_b, &full[stage], sb, kb * BK, col0);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------------ MMA issuer ----
+      constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((A_KMAJOR ? 0u : 1u) << 15) |
+                                 ((B_KMAJOR ? 0u : 1u) << 16) | ((uint32_t)(BN >> 3) << 17) |
+                                 ((uint32_t)(BM >> 4) << 24);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+          const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / UMMA_K; ++k)
+            tc_mma_tf32(d_tmem, operand_desc<A_KMAJOR>(sa, k), operand_desc<B_KMAJOR>(sb, k), idesc,
+                        (kb | k) != 0);
+          tc_commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(&tfull[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    // -------------------------------------------------------- epilogue ----
+    const int ew = warp - 4;  // TMEM lanes 32*ew .. 32*ew+31
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+      int mt, nt;
+      tile_coords(p, tile, mt, nt);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int64_t gm = p.m_lo + (int64_t)mt * BM + ew * 32 + lane;
+      const bool row_ok = gm <= p.m_hi && gm < p.M;
+      int64_t col_lo = 0, col_hi = p.N;
+      if (gm == p.m_lo) col_lo = p.first - p.m_lo * p.N;
+      if (gm == p.m_hi) col_hi = p.last - p.m_hi * p.N + 1;
+      float* crow = p.c + gm * p.ldc;
+#pragma unroll 1
+      for (int ch = 0; ch < BN / 32; ++ch) {
+        uint32_t v[32];
+        tmem_ld32(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + ch * 32, v);
+        const int64_t c0 = (int64_t)nt * BN + ch * 32;
+        if (!row_ok) continue;
+        if (p.c_vec && c0 >= col_lo && c0 + 32 <= col_hi) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            *reinterpret_cast<float4*>(crow + c0 + j) =
+                make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]),
+                            __uint_as_float(v[j + 3]));
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (c0 + j >= col_lo && c0 + j < col_hi) crow[c0 + j] = __uint_as_float(v[j]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+  }
+}
+
+// ------------------------------------------------------------ host side ----
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2-D fp32 tensor map: dims {inner, outer}, row pitch in elements, box {bi, bo}, 128B swizzle.
+static int make_map(CUtensorMap* map, const float* base, int64_t inner, int64_t outer, int64_t pitch, int bi,
+                    int bo) {
+  auto fn = encode_fn();
+  if (!fn) return fail(AOL_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)(pitch * 4)};
+  cuuint32_t box[2] = {(cuuint32_t)bi, (cuuint32_t)bo};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(AOL_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return AOL_OK;
+}
+
+}  // namespace gemm
+
+// Canonical-GEMM recognition from the affine forms of the three tilers.
+struct GemmShape {
+  bool ok;
+  bool a_kmajor, b_kmajor;
+  int64_t M, N, K;
+  int64_t ca, lda, cb, ldb, cc, ldc;
+};
+
+GemmShape recognise_gemm(const aol_task& t) {
+  GemmShape g{};
+  const aol_tiler &ta = t.tilers[0], &tb = t.tilers[1], &tc = t.tilers[2];
+  if (ta.rep_rank != 2 || tb.rep_rank != 2 || tc.rep_rank != 2) return g;
+  if (tiler_pat_total(ta) != ta.pattern[ta.pat_rank - 1]) return g;  // pattern must be 1-D (after extent-1 dims)
+  if (tiler_pat_total(tb) != tb.pattern[tb.pat_rank - 1]) return g;
+  Affine a = tiler_affine(ta), b = tiler_affine(tb), c = tiler_affine(tc);
+  if (!a.ok || !b.ok || !c.ok) return g;
+  const int64_t M = ta.rep[0], N = ta.rep[1], K = tiler_pat_total(ta);
+  const int64_t sa_m = a.A[0], sa_n = a.A[1], sa_k = a.B[ta.pat_rank - 1];
+  const int64_t sb_m = b.A[0], sb_n = b.A[1], sb_k = b.B[tb.pat_rank - 1];
+  if (sa_n != 0 || sb_m != 0) return g;                      // a depends on m only, b on n only
+  if (c.A[1] != 1 || c.A[0] < N) return g;                   // c row-major with ldc >= N
+  bool ak = (sa_k == 1 && sa_m >= K), am = (sa_m == 1 && sa_k >= M);
+  bool bn = (sb_n == 1 && sb_k >= N), bk = (sb_k == 1 && sb_n >= K);
+  if (!(ak || am) || !(bn || bk)) return g;
+  g.a_kmajor = ak;
+  g.b_kmajor = bk && !bn;
+  g.lda = ak ? sa_m : sa_k;
+  g.ldb = g.b_kmajor ? sb_n : sb_k;
+  g.M = M; g.N = N; g.K = K;
+  g.ca = a.c0; g.cb = b.c0; g.cc = c.c0; g.ldc = c.A[0];
+  // TMA: 16-byte aligned bases and pitches, coordinates inside int32
+  if ((g.lda % 4) || (g.ldb % 4) || (g.ca % 4) || (g.cb % 4)) return g;
+  if (M >= (1ll << 31) || N >= (1ll << 31) || K >= (1ll << 31)) return g;
+  g.ok = true;
+  return g;
+}
+
+bool gemm_tf32_applicable(const aol_task& t, void* const* ports) {
+  if (t.dtype != AOL_F32) return false;
+  if (t.precision == AOL_PREC_EXACT) return false;
+  GemmShape g = recognise_gemm(t);
+  if (!g.ok) return false;
+  const float* a = static_cast<const float*>(ports[0]) + g.ca;
+  const float* b = static_cast<const float*>(ports[1]) + g.cb;
+  return ((uintptr_t)a % 16 == 0) && ((uintptr_t)b % 16 == 0);
+}
+
+int launch_gemm_tf32(const aol_task& t, int64_t first, int64_t count, void* const* ports, cudaStream_t stream) {
+  using namespace gemm;
+  GemmShape g = recognise_gemm(t);
+  if (!g.ok) return fail(AOL_EUNSUPPORTED, "matmul tilers are not a TMA-compatible GEMM");
+  if (count <= 0) return AOL_OK;
+  const float* A = static_cast<const float*>(ports[0]) + g.ca;
+  const float* B = static_cast<const float*>(ports[1]) + g.cb;
+  float* C = static_cast<float*>(ports[2]) + g.cc;
+  CUtensorMap ma, mb;
+  int rc;
+  if (g.a_kmajor) rc = make_map(&ma, A, g.K, g.M, g.lda, BK, BM);
+  else rc = make_map(&ma, A, g.M, g.K, g.lda, 32, BK);
+  if (rc) return rc;
+  if (g.b_kmajor) rc = make_map(&mb, B, g.K, g.N, g.ldb, BK, BN);
+  else rc = make_map(&mb, B, g.N, g.K, g.ldb, 32, BK);
+  if (rc) return rc;
+
+  Params p{};
+  p.c = C;
+  p.ldc = g.ldc;
+  p.M = g.M; p.N = g.N; p.K = g.K;
+  p.first = first;
+  p.last = first + count - 1;
+  p.m_lo = first / g.N;
+  p.m_hi = p.last / g.N;
+  p.m_tiles = (int)((p.m_hi - p.m_lo + BM) / BM);
+  p.n_tiles = (int)((g.N + BN - 1) / BN);
+  p.k_blocks = (int)((g.K + BK - 1) / BK);
+  p.num_tiles = p.m_tiles * p.n_tiles;
+  p.c_vec = ((uintptr_t)C % 16 == 0) && (g.ldc % 4 == 0);
+
+  void (*kern)(const CUtensorMap, const CUtensorMap, Params);
+  if (g.a_kmajor) kern = g.b_kmajor ? k_gemm_tf32<true, true> : k_gemm_tf32<true, false>;
+  else kern = g.b_kmajor ? k_gemm_tf32<false, true> : k_gemm_tf32<false, false>;
+  AOL_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
+  int sms = kNumSMs;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = p.num_tiles < sms ? p.num_tiles : sms;
+  kern<<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(ma, mb, p);
+  AOL_LAUNCH_CHECK("k_gemm_tf32");
+  return AOL_OK;
+}
+
+}  // namespace aol

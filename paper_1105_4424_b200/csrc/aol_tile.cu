@@ -1,0 +1,513 @@
+// Array-OL tiler gather/scatter engine and the CUDA-core tile intrinsics (sm_100a).
+//
+// Semantics: SURVEY.md Appendix A (tiler) and paper_1105_4424_b200/intrinsics.py
+// (elementary tasks).  Every launch covers repetitions [first, first+count) of the
+// linearised repetition space, exactly like one reference launch
+// (refexec.py:488-514; codegen.py:128-129 guards `gid >= count`).
+//
+// Arithmetic in the tile intrinsics uses __fmul_rn/__fadd_rn (no FMA contraction)
+// in pattern order, which is the order of the reference's spmv_csr executor
+// (refexec.py:111-121) that pins the oracle — results are bit-exact.
+#include <algorithm>
+#include <cstring>
+
+#include "aol_common.cuh"
+
+namespace aol {
+
+// ------------------------------------------------------------ host side ----
+
+static int64_t prod(const int64_t* v, int n) {
+  int64_t t = 1;
+  for (int i = 0; i < n; ++i) t *= v[i];
+  return t;
+}
+int64_t tiler_rep_total(const aol_tiler& t) { return prod(t.rep, t.rep_rank); }
+int64_t tiler_pat_total(const aol_tiler& t) { return prod(t.pattern, t.pat_rank); }
+int64_t tiler_arr_total(const aol_tiler& t) { return prod(t.array, t.arr_rank); }
+
+static int64_t emod_h(int64_t v, int64_t m) {
+  int64_t r = v % m;
+  return r < 0 ? r + m : r;
+}
+
+int make_dev_tiler(const aol_tiler& in, DevTiler& out) {
+  memset(&out, 0, sizeof(out));
+  if (in.arr_rank < 1 || in.arr_rank > AOL_MAX_RANK || in.rep_rank < 1 ||
+      in.rep_rank > AOL_MAX_RANK || in.pat_rank < 1 || in.pat_rank > AOL_MAX_RANK)
+    return fail(AOL_EINVAL, "tiler ranks must be in 1..4");
+  out.a = in.arr_rank;
+  out.q = in.rep_rank;
+  out.p = in.pat_rank;
+  for (int d = 0; d < out.a; ++d)
+    if (in.array[d] < 1) return fail(AOL_EINVAL, "tiler array dimensions must be >= 1");
+  for (int j = 0; j < out.q; ++j)
+    if (in.rep[j] < 1) return fail(AOL_EINVAL, "tiler repetition dimensions must be >= 1");
+  for (int k = 0; k < out.p; ++k)
+    if (in.pattern[k] < 1) return fail(AOL_EINVAL, "tiler pattern dimensions must be >= 1");
+  const double lim = 4.0e18;  // keep every raw coordinate inside int64 (< 2^62)
+  int64_t acc = 1;
+  for (int d = out.a - 1; d >= 0; --d) {
+    out.s[d] = in.array[d];
+    out.st[d] = acc;
+    acc *= in.array[d];
+    out.o[d] = emod_h(in.origin[d], in.array[d]);
+    double span = (double)in.array[d];
+    for (int j = 0; j < out.q; ++j) {
+      out.P[d][j] = in.paving[d][j];
+      span += fabs((double)in.paving[d][j]) * (double)(in.rep[j] - 1);
+    }
+    for (int k = 0; k < out.p; ++k) {
+      out.F[d][k] = in.fitting[d][k];
+      span += fabs((double)in.fitting[d][k]) * (double)(in.pattern[k] - 1);
+    }
+    if (span > lim) return fail(AOL_EINVAL, "tiler coordinates overflow int64");
+  }
+  for (int j = 0; j < out.q; ++j) out.rep[j] = in.rep[j];
+  for (int k = 0; k < out.p; ++k) out.pat[k] = in.pattern[k];
+  const int64_t R = tiler_rep_total(in), Pt = tiler_pat_total(in);
+  out.small = (R < (1ll << 31) && Pt < (1ll << 31)) ? 1 : 0;
+  if (out.small) {
+    for (int j = 0; j < out.q; ++j) out.rep_div[j] = FastDiv32((uint32_t)in.rep[j]);
+    for (int k = 0; k < out.p; ++k) out.pat_div[k] = FastDiv32((uint32_t)in.pattern[k]);
+  }
+  return AOL_OK;
+}
+
+Affine tiler_affine(const aol_tiler& t) {
+  Affine r;
+  memset(&r, 0, sizeof(r));
+  int64_t st[AOL_MAX_RANK], acc = 1;
+  for (int d = t.arr_rank - 1; d >= 0; --d) {
+    st[d] = acc;
+    acc *= t.array[d];
+  }
+  for (int d = 0; d < t.arr_rank; ++d) {
+    int64_t o = emod_h(t.origin[d], t.array[d]);
+    int64_t lo = o, hi = o;
+    for (int j = 0; j < t.rep_rank; ++j) {
+      int64_t v = t.paving[d][j] * (t.rep[j] - 1);
+      lo += std::min<int64_t>(0, v);
+      hi += std::max<int64_t>(0, v);
+    }
+    for (int k = 0; k < t.pat_rank; ++k) {
+      int64_t v = t.fitting[d][k] * (t.pattern[k] - 1);
+      lo += std::min<int64_t>(0, v);
+      hi += std::max<int64_t>(0, v);
+    }
+    if (lo < 0 || hi >= t.array[d]) return r;  // wraps: not affine
+    r.c0 += o * st[d];
+  }
+  for (int j = 0; j < t.rep_rank; ++j)
+    for (int d = 0; d < t.arr_rank; ++d) r.A[j] += t.paving[d][j] * st[d];
+  for (int k = 0; k < t.pat_rank; ++k)
+    for (int d = 0; d < t.arr_rank; ++d) r.B[k] += t.fitting[d][k] * st[d];
+  r.ok = true;
+  return r;
+}
+
+size_t dtype_size(int dtype) { return (dtype == AOL_F32 || dtype == AOL_I32) ? 4 : 8; }
+
+// ------------------------------------------------------ pattern tables ----
+// fr[k * a + d] = (sum_k F_dk i_k) mod s_d for pattern point k: the per-pattern
+// part of each coordinate, pre-reduced so one conditional subtract suffices.
+constexpr int kTableMax = 4096;  // int64 entries in shared memory (32 KB)
+
+__device__ __forceinline__ void fill_table(const DevTiler& t, int64_t* fr, int64_t npat) {
+  for (int64_t k = threadIdx.x; k < npat; k += blockDim.x) {
+    int64_t i[AOL_MAX_RANK];
+    unravel(t, false, k, i);
+#pragma unroll
+    for (int d = 0; d < AOL_MAX_RANK; ++d) {
+      if (d >= t.a) break;
+      int64_t e = 0;
+#pragma unroll
+      for (int kk = 0; kk < AOL_MAX_RANK; ++kk)
+        if (kk < t.p) e += t.F[d][kk] * i[kk];
+      fr[k * t.a + d] = emod(e, t.s[d]);
+    }
+  }
+}
+
+__device__ __forceinline__ int64_t table_offset(const DevTiler& t, const int64_t base[AOL_MAX_RANK],
+                                                const int64_t* fr, int64_t k) {
+  int64_t off = 0;
+#pragma unroll
+  for (int d = 0; d < AOL_MAX_RANK; ++d) {
+    if (d >= t.a) break;
+    int64_t e = base[d] + fr[k * t.a + d];
+    if (e >= t.s[d]) e -= t.s[d];
+    off += e * t.st[d];
+  }
+  return off;
+}
+
+// ------------------------------------------------------------- kernels ----
+
+__global__ void k_tiler_offsets(DevTiler t, int64_t first, int64_t count, int64_t npat,
+                                int64_t* __restrict__ out) {
+  const int64_t n = count * npat;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    out[e] = tiler_offset(t, first + e / npat, e % npat);
+}
+
+// Generic gather -> scatter: one thread per (rho, iota) element.
+template <typename T>
+__global__ void k_tile_copy_generic(const T* __restrict__ src, T* __restrict__ dst, DevTiler ts,
+                                    DevTiler td, int64_t first, int64_t count, int64_t npat) {
+  const int64_t n = count * npat;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rho = first + e / npat, iota = e % npat;
+    dst[tiler_offset(td, rho, iota)] = src[tiler_offset(ts, rho, iota)];
+  }
+}
+
+// Both tilers affine with a collapsed 1-D repetition and 1-D pattern:
+//   src[cs + As*rho + Bs*iota] -> dst[cd + Ad*rho + Bd*iota].
+// Consecutive threads take consecutive (rho, iota), so dense sides coalesce.
+template <typename T, int UNROLL>
+__global__ void __launch_bounds__(256) k_tile_copy_affine(const T* __restrict__ src, T* __restrict__ dst,
+                                                          int64_t cs, int64_t As, int64_t Bs, int64_t cd,
+                                                          int64_t Ad, int64_t Bd, int64_t first, int64_t n,
+                                                          FastDiv32 pdiv) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * UNROLL;
+  for (int64_t e0 = (blockIdx.x * (int64_t)blockDim.x) * UNROLL + threadIdx.x; e0 < n; e0 += stride) {
+    T v[UNROLL];
+    int64_t od[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      const int64_t e = e0 + (int64_t)u * blockDim.x;
+      od[u] = -1;
+      if (e < n) {
+        uint32_t q, r;
+        pdiv.divmod((uint32_t)e, q, r);
+        const int64_t rho = first + q;
+        v[u] = __ldg(src + cs + As * rho + Bs * (int64_t)r);
+        od[u] = cd + Ad * rho + Bd * (int64_t)r;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u)
+      if (od[u] >= 0) dst[od[u]] = v[u];
+  }
+}
+
+// Contiguous on both sides: a streaming copy with 16-byte vectors.
+__global__ void __launch_bounds__(256) k_stream_copy16(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                                       int64_t n16) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x * 4 + threadIdx.x; i < n16; i += stride) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (i + u * blockDim.x < n16) v[u] = __ldcs(src + i + u * blockDim.x);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (i + u * blockDim.x < n16) __stcs(dst + i + u * blockDim.x, v[u]);
+  }
+}
+
+template <typename T>
+__global__ void k_stream_copy_tail(const T* __restrict__ src, T* __restrict__ dst, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+// Pattern dot (generic matmul): c[off_c(rho)] = sum_k a_k * b_k, k ascending, no FMA.
+template <typename T>
+__global__ void k_matmul_generic(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ c,
+                                 DevTiler ta, DevTiler tb, DevTiler tc, int64_t first, int64_t count,
+                                 int64_t K, int use_table) {
+  extern __shared__ int64_t smem[];
+  int64_t* fa = smem;
+  int64_t* fb = smem + (use_table ? K * ta.a : 0);
+  if (use_table) {
+    fill_table(ta, fa, K);
+    fill_table(tb, fb, K);
+    __syncthreads();
+  }
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rho = first + e;
+    T acc = T(0);
+    if (use_table) {
+      int64_t ba[AOL_MAX_RANK], bb[AOL_MAX_RANK];
+      tiler_base(ta, rho, ba);
+      tiler_base(tb, rho, bb);
+      for (int64_t k = 0; k < K; ++k) {
+        const T x = a[table_offset(ta, ba, fa, k)], y = b[table_offset(tb, bb, fb, k)];
+        if constexpr (sizeof(T) == 4) acc = __fadd_rn(acc, __fmul_rn(x, y));
+        else acc = __dadd_rn(acc, __dmul_rn(x, y));
+      }
+    } else {
+      for (int64_t k = 0; k < K; ++k) {
+        const T x = a[tiler_offset(ta, rho, k)], y = b[tiler_offset(tb, rho, k)];
+        if constexpr (sizeof(T) == 4) acc = __fadd_rn(acc, __fmul_rn(x, y));
+        else acc = __dadd_rn(acc, __dmul_rn(x, y));
+      }
+    }
+    c[tiler_offset(tc, rho, 0)] = acc;
+  }
+}
+
+// Pattern linear map: y_pat[j] = sum_i w[j, i] * x_pat[i], i ascending, no FMA.
+// One thread per repetition; up to MAXO outputs accumulate while the pattern
+// streams once through registers.
+template <typename T, int MAXO>
+__global__ void __launch_bounds__(256) k_filter_generic(const T* __restrict__ x, const T* __restrict__ w,
+                                                        T* __restrict__ y, DevTiler tx, DevTiler ty,
+                                                        int64_t first, int64_t count, int px, int py) {
+  extern __shared__ int64_t smem[];
+  int64_t* fx = smem;
+  int64_t* fy = fx + (int64_t)px * tx.a;
+  T* ws = reinterpret_cast<T*>(fy + (int64_t)py * ty.a);
+  fill_table(tx, fx, px);
+  fill_table(ty, fy, py);
+  for (int k = threadIdx.x; k < px * py; k += blockDim.x) ws[k] = w[k];
+  __syncthreads();
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rho = first + e;
+    int64_t bx[AOL_MAX_RANK], by[AOL_MAX_RANK];
+    tiler_base(tx, rho, bx);
+    tiler_base(ty, rho, by);
+    T acc[MAXO];
+#pragma unroll
+    for (int j = 0; j < MAXO; ++j) acc[j] = T(0);
+    for (int i = 0; i < px; ++i) {
+      const T xv = x[table_offset(tx, bx, fx, i)];
+#pragma unroll
+      for (int j = 0; j < MAXO; ++j) {
+        if (j < py) {
+          if constexpr (sizeof(T) == 4) acc[j] = __fadd_rn(acc[j], __fmul_rn(ws[j * px + i], xv));
+          else acc[j] = __dadd_rn(acc[j], __dmul_rn(ws[j * px + i], xv));
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < MAXO; ++j)
+      if (j < py) y[table_offset(ty, by, fy, j)] = acc[j];
+  }
+}
+
+// Pattern reduction: s[off_s(rho)] = sum_i x_pat[i], i ascending.
+template <typename T>
+__global__ void k_tile_sum_generic(const T* __restrict__ x, T* __restrict__ s, DevTiler tx, DevTiler ts,
+                                   int64_t first, int64_t count, int px) {
+  extern __shared__ int64_t smem[];
+  fill_table(tx, smem, px);
+  __syncthreads();
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rho = first + e;
+    int64_t bx[AOL_MAX_RANK];
+    tiler_base(tx, rho, bx);
+    T acc = T(0);
+    for (int i = 0; i < px; ++i) {
+      if constexpr (sizeof(T) == 4) acc = __fadd_rn(acc, x[table_offset(tx, bx, smem, i)]);
+      else acc = __dadd_rn(acc, x[table_offset(tx, bx, smem, i)]);
+    }
+    s[tiler_offset(ts, rho, 0)] = acc;
+  }
+}
+
+// ------------------------------------------------------- launch wrappers ----
+
+int launch_tiler_offsets(const aol_tiler& t, int64_t first, int64_t count, int64_t* out,
+                         cudaStream_t stream) {
+  DevTiler dt;
+  int rc = make_dev_tiler(t, dt);
+  if (rc) return rc;
+  const int64_t R = tiler_rep_total(t), Pt = tiler_pat_total(t);
+  if (first < 0 || count < 0 || first + count > R)
+    return fail(AOL_EINVAL, "repetition range outside the repetition space");
+  if (count == 0) return AOL_OK;
+  k_tiler_offsets<<<grid_for(count * Pt, 256), 256, 0, stream>>>(dt, first, count, Pt, out);
+  AOL_LAUNCH_CHECK("k_tiler_offsets");
+  return AOL_OK;
+}
+
+// Collapse a 1-D view out of the repetition/pattern coefficients when possible.
+static bool collapse(const int64_t* coef, const int64_t* dims, int n, int64_t& stride) {
+  // coef[j] == coef[j+1] * dims[j+1] for every adjacent pair (ignoring extent-1 dims)
+  int64_t s = 0;
+  bool have = false;
+  int64_t expect_next = 0;
+  for (int j = n - 1; j >= 0; --j) {
+    if (dims[j] == 1) continue;
+    if (!have) {
+      s = coef[j];
+      have = true;
+      expect_next = coef[j] * dims[j];
+    } else {
+      if (coef[j] != expect_next) return false;
+      expect_next = coef[j] * dims[j];
+    }
+  }
+  stride = have ? s : 0;
+  return true;
+}
+
+struct CopyPlan {
+  int kind;  // 0 generic, 1 affine1, 2 stream
+  int64_t cs, As, Bs, cd, Ad, Bd;
+};
+
+static CopyPlan plan_tile_copy(const aol_tiler& ts, const aol_tiler& td, int64_t first, int64_t count) {
+  CopyPlan p{};
+  Affine s = tiler_affine(ts), d = tiler_affine(td);
+  if (!s.ok || !d.ok) return p;
+  int64_t As, Ad, Bs, Bd;
+  // the shared repetition space must collapse identically on both sides
+  if (!collapse(s.A, ts.rep, ts.rep_rank, As) || !collapse(d.A, td.rep, td.rep_rank, Ad)) return p;
+  if (!collapse(s.B, ts.pattern, ts.pat_rank, Bs) || !collapse(d.B, td.pattern, td.pat_rank, Bd)) return p;
+  const int64_t P = tiler_pat_total(ts);
+  if (count * P >= (1ll << 32)) return p;
+  p.kind = 1;
+  p.cs = s.c0; p.As = As; p.Bs = P > 1 ? Bs : 0;
+  p.cd = d.c0; p.Ad = Ad; p.Bd = P > 1 ? Bd : 0;
+  const bool src_dense = (P == 1 || p.Bs == 1) && p.As == P;
+  const bool dst_dense = (P == 1 || p.Bd == 1) && p.Ad == P;
+  if (src_dense && dst_dense) p.kind = 2;
+  (void)first;
+  return p;
+}
+
+const char* tile_copy_plan_name(const aol_tiler& ts, const aol_tiler& td, int64_t first, int64_t count) {
+  switch (plan_tile_copy(ts, td, first, count).kind) {
+    case 2: return "tile_copy.stream16";
+    case 1: return "tile_copy.affine";
+    default: return "tile_copy.generic";
+  }
+}
+
+template <typename T>
+static int launch_tile_copy_t(const aol_tiler& ts, const aol_tiler& td, int64_t first, int64_t count,
+                              const void* src, void* dst, cudaStream_t stream) {
+  const int64_t P = tiler_pat_total(ts);
+  CopyPlan p = plan_tile_copy(ts, td, first, count);
+  const T* s = static_cast<const T*>(src);
+  T* d = static_cast<T*>(dst);
+  if (p.kind == 2) {
+    const T* s0 = s + p.cs + first * P;
+    T* d0 = d + p.cd + first * P;
+    const int64_t n = count * P;
+    const int64_t bytes = n * (int64_t)sizeof(T);
+    if (((uintptr_t)s0 % 16) == ((uintptr_t)d0 % 16)) {
+      // peel to 16-byte alignment, stream the body, copy the tail
+      int64_t head = ((16 - ((uintptr_t)s0 % 16)) % 16) / sizeof(T);
+      if (head > n) head = n;
+      if (head) {
+        k_stream_copy_tail<T><<<1, 32, 0, stream>>>(s0, d0, head);
+        AOL_LAUNCH_CHECK("k_stream_copy_tail");
+      }
+      const int64_t body16 = (bytes - head * (int64_t)sizeof(T)) / 16;
+      if (body16) {
+        k_stream_copy16<<<grid_for(body16, 1024, 8), 256, 0, stream>>>(
+            reinterpret_cast<const uint4*>(s0 + head), reinterpret_cast<uint4*>(d0 + head), body16);
+        AOL_LAUNCH_CHECK("k_stream_copy16");
+      }
+      const int64_t done = head + body16 * 16 / (int64_t)sizeof(T);
+      if (n - done) {
+        k_stream_copy_tail<T><<<1, 256, 0, stream>>>(s0 + done, d0 + done, n - done);
+        AOL_LAUNCH_CHECK("k_stream_copy_tail");
+      }
+      return AOL_OK;
+    }
+    p.kind = 1;
+  }
+  if (p.kind == 1) {
+    const int64_t n = count * P;
+    k_tile_copy_affine<T, 4><<<grid_for(n, 1024, 16), 256, 0, stream>>>(
+        s, d, p.cs, p.As, p.Bs, p.cd, p.Ad, p.Bd, first, n, FastDiv32((uint32_t)P));
+    AOL_LAUNCH_CHECK("k_tile_copy_affine");
+    return AOL_OK;
+  }
+  DevTiler dts, dtd;
+  int rc = make_dev_tiler(ts, dts);
+  if (rc) return rc;
+  rc = make_dev_tiler(td, dtd);
+  if (rc) return rc;
+  k_tile_copy_generic<T><<<grid_for(count * P, 256), 256, 0, stream>>>(s, d, dts, dtd, first, count, P);
+  AOL_LAUNCH_CHECK("k_tile_copy_generic");
+  return AOL_OK;
+}
+
+int launch_tile_copy(const aol_task& t, int64_t first, int64_t count, void* const* ports,
+                     cudaStream_t stream) {
+  if (dtype_size(t.dtype) == 4)
+    return launch_tile_copy_t<uint32_t>(t.tilers[0], t.tilers[1], first, count, ports[0], ports[1], stream);
+  return launch_tile_copy_t<uint64_t>(t.tilers[0], t.tilers[1], first, count, ports[0], ports[1], stream);
+}
+
+int launch_matmul_generic(const aol_task& t, int64_t first, int64_t count, void* const* ports,
+                          cudaStream_t stream) {
+  DevTiler ta, tb, tc;
+  int rc;
+  if ((rc = make_dev_tiler(t.tilers[0], ta)) || (rc = make_dev_tiler(t.tilers[1], tb)) ||
+      (rc = make_dev_tiler(t.tilers[2], tc)))
+    return rc;
+  const int64_t K = tiler_pat_total(t.tilers[0]);
+  const int use_table = K * (ta.a + tb.a) <= kTableMax ? 1 : 0;
+  const size_t smem = use_table ? (size_t)K * (ta.a + tb.a) * sizeof(int64_t) : 0;
+  const unsigned grid = grid_for(count, 128, 32);
+  if (t.dtype == AOL_F32)
+    k_matmul_generic<float><<<grid, 128, smem, stream>>>(
+        (const float*)ports[0], (const float*)ports[1], (float*)ports[2], ta, tb, tc, first, count, K, use_table);
+  else
+    k_matmul_generic<double><<<grid, 128, smem, stream>>>(
+        (const double*)ports[0], (const double*)ports[1], (double*)ports[2], ta, tb, tc, first, count, K,
+        use_table);
+  AOL_LAUNCH_CHECK("k_matmul_generic");
+  return AOL_OK;
+}
+
+template <typename T, int MAXO>
+static int launch_filter_t(const DevTiler& tx, const DevTiler& ty, int64_t first, int64_t count, int px,
+                           int py, void* const* ports, cudaStream_t stream) {
+  const size_t smem = ((size_t)px * tx.a + (size_t)py * ty.a) * sizeof(int64_t) + (size_t)px * py * sizeof(T);
+  auto kern = k_filter_generic<T, MAXO>;
+  if (smem > 48 * 1024) AOL_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<grid_for(count, 256, 16), 256, smem, stream>>>((const T*)ports[0], (const T*)ports[1], (T*)ports[2],
+                                                        tx, ty, first, count, px, py);
+  AOL_LAUNCH_CHECK("k_filter_generic");
+  return AOL_OK;
+}
+
+int launch_filter_generic(const aol_task& t, int64_t first, int64_t count, void* const* ports,
+                          cudaStream_t stream) {
+  DevTiler tx, ty;
+  int rc;
+  if ((rc = make_dev_tiler(t.tilers[0], tx)) || (rc = make_dev_tiler(t.tilers[1], ty))) return rc;
+  const int64_t px = tiler_pat_total(t.tilers[0]), py = tiler_pat_total(t.tilers[1]);
+  if (px * tx.a + py * ty.a > kTableMax * 4 || px * py > 16384)
+    return fail(AOL_EUNSUPPORTED, "tile_filter pattern too large (px*py <= 16384)");
+  if (py > 16) return fail(AOL_EUNSUPPORTED, "tile_filter supports at most 16 outputs per pattern");
+  const bool f32 = t.dtype == AOL_F32;
+  if (py <= 4)
+    return f32 ? launch_filter_t<float, 4>(tx, ty, first, count, px, py, ports, stream)
+               : launch_filter_t<double, 4>(tx, ty, first, count, px, py, ports, stream);
+  return f32 ? launch_filter_t<float, 16>(tx, ty, first, count, px, py, ports, stream)
+             : launch_filter_t<double, 16>(tx, ty, first, count, px, py, ports, stream);
+}
+
+int launch_tile_sum(const aol_task& t, int64_t first, int64_t count, void* const* ports, cudaStream_t stream) {
+  DevTiler tx, ts;
+  int rc;
+  if ((rc = make_dev_tiler(t.tilers[0], tx)) || (rc = make_dev_tiler(t.tilers[1], ts))) return rc;
+  const int64_t px = tiler_pat_total(t.tilers[0]);
+  if (px * tx.a > kTableMax) return fail(AOL_EUNSUPPORTED, "tile_sum pattern too large");
+  const size_t smem = (size_t)px * tx.a * sizeof(int64_t);
+  if (t.dtype == AOL_F32)
+    k_tile_sum_generic<float><<<grid_for(count, 256, 16), 256, smem, stream>>>(
+        (const float*)ports[0], (float*)ports[1], tx, ts, first, count, (int)px);
+  else
+    k_tile_sum_generic<double><<<grid_for(count, 256, 16), 256, smem, stream>>>(
+        (const double*)ports[0], (double*)ports[1], tx, ts, first, count, (int)px);
+  AOL_LAUNCH_CHECK("k_tile_sum_generic");
+  return AOL_OK;
+}
+
+}  // namespace aol

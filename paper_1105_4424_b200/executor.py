@@ -1,0 +1,281 @@
+"""B200 drop-in for ``gmodelc.refexec.execute_schedule`` (refexec.py:427-549).
+
+Same signature, same return type (:class:`ExecutionResult`), same binding
+checks (``MissingBinding``, refexec.py:390-396), same signature errors
+(``UnknownIntrinsic`` / ``IntrinsicShapeMismatch`` incl. the
+output-aliases-input check, :440-455), zero-initialised unwritten outputs
+(:399-403), flat row-major outputs (:545-547) and the same LoopStep
+semantics (:518-541).  What changes is where the arrays live and who runs
+the launches:
+
+  * storage: one CUDA tensor per connected-port group (``_Storage``
+    :375-412) in HBM, allocated through PyTorch (tensor handoff only);
+  * every ``KernelLaunch`` of a ``DeviceStep`` becomes one ``aol_launch``
+    of libaolb200.so over the same ``[offset, offset+count)`` range
+    (replacing the numpy body of refexec.py:488-514);
+  * dot_partial keeps the reference's host combine: one partial per
+    launch, summed on the host in ascending device order (:478-487).
+
+Keyword-only additions: ``tilers`` (task path -> port -> Tiler, for
+reference models whose Component has no tiler field), ``precision`` for
+the matmul elementary task, ``device_outputs`` to keep results in HBM, and
+``stream``.  There is no CPU fallback: a missing library raises.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _capi
+from .intrinsics import (INTRINSICS, IntrinsicShapeMismatch, _ports_match_spec, check_task_signature,
+                         check_tile_signature)
+from .model import connected_port_groups, enum_value, iter_app_instances, task_component
+
+
+class MissingBinding(KeyError):
+    pass
+
+
+@dataclass
+class ExecutionResult:
+    outputs: dict
+    iterations: int
+    final_relres: float | None
+    converged: bool
+
+
+_TORCH_DTYPES = None
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def torch_dtype(name: str):
+    global _TORCH_DTYPES
+    torch = _torch()
+    if _TORCH_DTYPES is None:
+        _TORCH_DTYPES = {"float32": torch.float32, "float64": torch.float64,
+                         "int32": torch.int32, "int64": torch.int64}
+    return _TORCH_DTYPES[name]
+
+
+class DeviceStorage:
+    """Arrays per connected-port group, resident on one CUDA device (refexec.py:375-412)."""
+
+    def __init__(self, model, bindings: dict, device, stream=None):
+        torch = _torch()
+        self.groups = connected_port_groups(model)
+        self.ports = {}
+        for path, comp in iter_app_instances(model):
+            for port in comp.ports:
+                self.ports[f"{path}.{port.name}" if path else port.name] = port
+        self.arrays: dict = {}
+        self.h2d_bytes = 0
+        root = model.application_components[model.application_root]
+        for port in root.ports:
+            if enum_value(port.direction) not in ("in", "inout"):
+                continue
+            if port.name not in bindings:
+                raise MissingBinding(f"no binding for input port '{port.name}'")
+            data = bindings[port.name]
+            dt = enum_value(port.data_type)
+            if isinstance(data, torch.Tensor):
+                flat = data.reshape(-1)
+                if flat.numel() != port.shape.total:
+                    raise MissingBinding(f"binding '{port.name}' has {flat.numel()} elements, "
+                                         f"port expects {port.shape.total}")
+                if flat.device.type != "cuda":
+                    self.h2d_bytes += flat.numel() * flat.element_size()
+                t = flat.to(device=device, dtype=torch_dtype(dt), copy=True, non_blocking=True)
+            else:
+                arr = np.asarray(data).ravel()
+                if arr.size != port.shape.total:
+                    raise MissingBinding(f"binding '{port.name}' has {arr.size} elements, "
+                                         f"port expects {port.shape.total}")
+                arr = np.ascontiguousarray(arr.astype(dt, copy=False))
+                self.h2d_bytes += arr.nbytes
+                t = torch.from_numpy(arr).to(device=device, copy=True)
+            self.arrays[self.groups[port.name]] = t
+        for node, port in self.ports.items():
+            g = self.groups[node]
+            if g not in self.arrays:
+                self.arrays[g] = torch.zeros(port.shape.total, dtype=torch_dtype(enum_value(port.data_type)),
+                                             device=device)
+
+    def array(self, node: str):
+        return self.arrays[self.groups[node]]
+
+
+class _Task:
+    """A validated leaf task: spec, bound tilers, C task struct and port nodes in spec order."""
+
+    def __init__(self, model, storage: DeviceStorage, task_path: str, tilers: dict | None, precision: str):
+        comp = task_component(model, task_path)
+        spec = INTRINSICS.get(comp.elementary_op) if comp.elementary_op else None
+        bound = None
+        if spec is not None and spec.tile:
+            _ports_match_spec(task_path, comp, spec)
+            bound = check_tile_signature(task_path, comp, spec, tilers)
+        else:
+            spec = check_task_signature(task_path, comp, tilers)
+        for port in comp.ports:
+            if enum_value(port.direction) != "out":
+                continue
+            g = storage.groups[f"{task_path}.{port.name}"]
+            for other in comp.ports:
+                if enum_value(other.direction) == "in" and storage.groups[f"{task_path}.{other.name}"] is g:
+                    raise IntrinsicShapeMismatch(
+                        f"task '{task_path}': output port '{port.name}' aliases input port '{other.name}'")
+        self.comp, self.spec, self.path = comp, spec, task_path
+        self.nodes = {p.name: f"{task_path}.{p.name}" for p in comp.ports}
+        self.dtype = None
+        self.ctask = None
+        if spec.kind != "device":
+            return
+        if spec.tile:
+            self.dtype = enum_value(comp.port(spec.ports[0].name).data_type)
+            self.ctask = _capi.make_task(spec.name, self.dtype,
+                                         [bound[ps.name] for ps in spec.ports if ps.tiled],
+                                         precision=precision)
+            self.port_order = [ps.name for ps in spec.ports]
+            self.scalar_ports = []
+        else:
+            val = "values" if spec.name == "spmv_csr" else next(
+                ps.name for ps in spec.ports if not ps.integer and not ps.scalar)
+            self.dtype = enum_value(comp.port(val).data_type)
+            index_dtype = enum_value(comp.port("rowptr").data_type) if spec.name == "spmv_csr" else "int32"
+            self.scalar_ports = [ps.name for ps in spec.ports
+                                 if ps.scalar and enum_value(ps.direction) == "in" and comp.port(ps.name)]
+            self.port_order = [ps.name for ps in spec.ports
+                               if not (ps.scalar and enum_value(ps.direction) == "in") and comp.port(ps.name)]
+            self.ctask = _capi.make_task(spec.name, self.dtype, n_scalars=len(self.scalar_ports),
+                                         index_dtype=index_dtype)
+
+
+class Executor:
+    """Prepared schedule: storage resident in HBM, tasks validated, ready to run repeatedly."""
+
+    def __init__(self, model, schedule, bindings: dict, device_count: int, *, tilers: dict | None = None,
+                 precision: str = "default", device=None, stream=None):
+        torch = _torch()
+        _capi.load()
+        if not torch.cuda.is_available():
+            raise _capi.NativeLibraryError("no CUDA device: the B200 executor has no CPU fallback")
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.model, self.schedule = model, schedule
+        self.device_count = device_count
+        self.tilers = tilers or {}
+        self.precision = precision
+        self.stream = stream
+        with torch.cuda.device(self.device):
+            self.storage = DeviceStorage(model, bindings, self.device, stream)
+        self._tasks: dict[str, _Task] = {}
+        self._dot_buf = None
+        self.iterations = 0
+        self.final_relres = None
+        self.converged = True
+
+    def task(self, path: str) -> _Task:
+        t = self._tasks.get(path)
+        if t is None:
+            t = _Task(self.model, self.storage, path, self.tilers.get(path), self.precision)
+            self._tasks[path] = t
+        return t
+
+    def _stream_handle(self) -> int:
+        torch = _torch()
+        s = self.stream if self.stream is not None else torch.cuda.current_stream(self.device)
+        return int(s.cuda_stream)
+
+    # -- steps -------------------------------------------------------------
+    def run_host(self, step) -> None:
+        t = self.task(step.task_path)
+        a = lambda name: self.storage.array(t.nodes[name])   # noqa: E731
+        if step.op == "div":
+            a("q")[0] = float(a("num")[0].item()) / float(a("den")[0].item())
+        elif step.op == "neg":
+            a("z")[0] = -a("a")[0].item()
+        elif step.op == "rel_residual":
+            a("z")[0] = math.sqrt(float(a("num")[0].item())) / math.sqrt(float(a("den")[0].item()))
+        else:
+            raise IntrinsicShapeMismatch(f"intrinsic '{INTRINSICS[step.op].name}' cannot run as a host scalar op")
+
+    def run_device(self, step) -> None:
+        torch = _torch()
+        t = self.task(step.task_path)
+        s = self._stream_handle()
+        arrays = {name: self.storage.array(node) for name, node in t.nodes.items()}
+        scalars = [float(arrays[n][0].item()) for n in t.scalar_ports]
+        if step.op == "dot_partial":
+            n = len(step.launches)
+            if self._dot_buf is None or self._dot_buf.numel() < n or self._dot_buf.dtype != arrays["a"].dtype:
+                self._dot_buf = torch.zeros(max(n, 8), dtype=arrays["a"].dtype, device=self.device)
+            for i, l in enumerate(step.launches):
+                ptrs = [arrays["a"].data_ptr(), arrays["b"].data_ptr(),
+                        self._dot_buf.data_ptr() + i * self._dot_buf.element_size()]
+                _capi.launch(t.ctask, l.range.offset, l.range.count, ptrs, (), s)
+            partials = self._dot_buf[:n].double().cpu().tolist()
+            total = 0.0
+            for p in partials:                      # ascending device order (refexec.py:483-486)
+                total += p
+            arrays["s"][0] = total
+            return
+        ptrs = [arrays[name].data_ptr() for name in t.port_order]
+        for l in step.launches:
+            _capi.launch(t.ctask, l.range.offset, l.range.count, ptrs, scalars, s)
+
+    def run_steps(self, steps, tol=None, max_iter=None) -> None:
+        for step in steps:
+            if hasattr(step, "launches"):
+                self.run_device(step)
+            elif hasattr(step, "body"):
+                loop_tol = tol if tol is not None else step.tolerance
+                loop_max = max_iter if max_iter is not None else step.max_iterations
+                done = False
+                n = 0
+                while True:
+                    self.run_steps(step.body, tol, max_iter)
+                    n += 1
+                    self.iterations += 1
+                    relres = float(self.storage.array(step.relres_port)[0].item())
+                    self.final_relres = relres
+                    if relres <= loop_tol:
+                        done = True
+                        break
+                    if n >= loop_max:
+                        break
+                self.converged = self.converged and done
+            else:
+                self.run_host(step)
+
+    def run(self, tol=None, max_iter=None) -> None:
+        torch = _torch()
+        with torch.cuda.device(self.device):
+            self.run_steps(self.schedule.steps, tol, max_iter)
+
+    def outputs(self, on_device: bool = False) -> dict:
+        root = self.model.application_components[self.model.application_root]
+        out = {}
+        for port in root.ports:
+            if enum_value(port.direction) != "out":
+                continue
+            t = self.storage.array(port.name)
+            out[port.name] = t.clone() if on_device else t.cpu().numpy()
+        return out
+
+
+def execute_schedule(model, schedule, bindings: dict, device_count: int, tol: float | None = None,
+                     max_iter: int | None = None, *, tilers: dict | None = None, precision: str = "default",
+                     device_outputs: bool = False, device=None, stream=None) -> ExecutionResult:
+    """Interpret ``schedule`` on the B200 with ``device_count`` launch shards per device step."""
+    ex = Executor(model, schedule, bindings, device_count, tilers=tilers, precision=precision,
+                  device=device, stream=stream)
+    ex.run(tol, max_iter)
+    outs = ex.outputs(on_device=device_outputs)
+    return ExecutionResult(outputs=outs, iterations=ex.iterations, final_relres=ex.final_relres,
+                           converged=ex.converged)

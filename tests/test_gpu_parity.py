@@ -1,0 +1,328 @@
+"""CUDA path vs the CPU oracle / the reference's golden outputs, through the drop-in executor.
+
+Every test here calls libaolb200.so through ``execute_schedule`` (the
+reference's public entry point, refexec.py:427) or the C ABI directly.
+Bar: bit-exact for tiler indices, gather/scatter layouts and every op in
+"exact" order; the TF32 tensor-core matmul is held to the stated bound
+  |C - C_fp64| <= (2^-9 + K * 2^-23) * (|A| |B|)     (element-wise)
+(two TF32-truncated operands: relative error < 2 * 2^-10 per product,
+plus fp32 accumulation over K terms).
+"""
+
+import numpy as np
+import pytest
+
+from oracle import aol_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    from paper_1105_4424_b200 import _capi
+    assert _capi.device_count() >= 1
+
+
+def _tiler(d):
+    from paper_1105_4424_b200 import Tiler
+    return Tiler(d["origin"], d["paving"], d["fitting"], d["pattern"])
+
+
+def _spec(d, direction, dtype):
+    dims = ",".join(str(x) for x in d["array"])
+    return f"{direction} {dtype} [{dims}]"
+
+
+def _run_tile(op, tilers, ports, bindings, devices, **kw):
+    from paper_1105_4424_b200 import builders
+    from paper_1105_4424_b200.partition import build_schedule
+    from paper_1105_4424_b200.executor import execute_schedule
+    rep = next(iter(tilers.values()))["rep"]
+    model = builders.tile_task_model(op, ports, {k: _tiler(v) for k, v in tilers.items()}, rep)
+    res = execute_schedule(model, build_schedule(model, devices), {f"p_{k}": v for k, v in bindings.items()},
+                           devices, **kw)
+    return res
+
+
+GOLDEN_TILE_OPS = ("tile_copy", "matmul", "tile_filter", "hfilter", "vfilter", "stencil", "tile_sum")
+
+
+def _golden_names(meta):
+    return sorted(k for k, v in meta.items() if not k.startswith("_") and not k.startswith("ident_")
+                  and v["op"] in GOLDEN_TILE_OPS)
+
+
+@pytest.mark.parametrize("devices", [1, 3, 5, 8])
+def test_tile_ops_bitwise_vs_reference_golden(golden, devices):
+    data, meta = golden
+    for name in _golden_names(meta):
+        m = meta[name]
+        t = m["tilers"]
+        ref = data[f"{name}/out"]
+        op = m["op"]
+        if op == "tile_copy":
+            ports = {"src": _spec(t["src"], "in", "float32"), "dst": _spec(t["dst"], "out", "float32")}
+            b = {"src": data[f"{name}/src"]}
+            out = "dst"
+        elif op == "matmul":
+            ports = {"a": _spec(t["a"], "in", "float32"), "b": _spec(t["b"], "in", "float32"),
+                     "c": _spec(t["c"], "out", "float32")}
+            b = {"a": data[f"{name}/a"], "b": data[f"{name}/b"]}
+            out = "c"
+        elif op == "tile_sum":
+            ports = {"x": _spec(t["x"], "in", "float32"), "s": _spec(t["s"], "out", "float32")}
+            b = {"x": data[f"{name}/x"]}
+            out = "s"
+        else:
+            w = data[f"{name}/w"]
+            ports = {"x": _spec(t["x"], "in", "float32"), "w": f"in float32 [{w.size}]",
+                     "y": _spec(t["y"], "out", "float32")}
+            b = {"x": data[f"{name}/x"], "w": w}
+            out = "y"
+        res = _run_tile(op, t, ports, b, devices, precision="exact")
+        got = res.outputs[f"p_{out}"]
+        assert got.dtype == ref.dtype and got.shape == ref.shape, name
+        assert np.array_equal(got.view(np.uint32), ref.view(np.uint32)), (name, devices)
+
+
+def test_tiler_offsets_bitwise_vs_oracle(golden):
+    from paper_1105_4424_b200 import _capi
+    _, meta = golden
+    for name in _golden_names(meta):
+        for d in meta[name]["tilers"].values():
+            bt = _tiler(d).bind(d["array"], d["rep"])
+            R, P = bt.rep_total, bt.pattern_total
+            for first, count in ((0, R), (R // 3, R - R // 3), (R - 1, 1)):
+                out = torch.empty(count * P, dtype=torch.int64, device="cuda")
+                _capi.tiler_offsets(bt, first, count, out.data_ptr())
+                torch.cuda.synchronize()
+                ref = orc.tiler_offsets(d, first, count).ravel()
+                assert np.array_equal(out.cpu().numpy(), ref), (name, first, count)
+
+
+def _random_tiler_cases():
+    rng = np.random.default_rng(1234)
+    cases = []
+    for _ in range(40):
+        a = int(rng.integers(1, 4))
+        q = int(rng.integers(1, 4))
+        p = int(rng.integers(1, 3))
+        arr = tuple(int(x) for x in rng.integers(1, 9, a))
+        rep = tuple(int(x) for x in rng.integers(1, 7, q))
+        pat = tuple(int(x) for x in rng.integers(1, 5, p))
+        o = tuple(int(x) for x in rng.integers(-20, 20, a))
+        P = tuple(tuple(int(x) for x in rng.integers(-5, 6, q)) for _ in range(a))
+        F = tuple(tuple(int(x) for x in rng.integers(-5, 6, p)) for _ in range(a))
+        cases.append(dict(array=arr, rep=rep, pattern=pat, origin=o, paving=P, fitting=F))
+    return cases
+
+
+def test_tiler_offsets_random_vs_loop_oracle():
+    from paper_1105_4424_b200 import _capi
+    for d in _random_tiler_cases():
+        bt = _tiler(d).bind(d["array"], d["rep"])
+        R, P = bt.rep_total, bt.pattern_total
+        out = torch.empty(R * P, dtype=torch.int64, device="cuda")
+        _capi.tiler_offsets(bt, 0, R, out.data_ptr())
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), np.array(orc.tiler_offsets_loop(d, 0, R)).ravel()), d
+
+
+@pytest.mark.parametrize("case", [
+    # (src array, rep, pattern, paving, fitting, origin)   1-D sweep shapes of config C5
+    ((4096,), (1024,), (4,), ((4,),), ((1,),), (0,)),           # dense -> stream copy
+    ((4096,), (2047,), (4,), ((2,),), ((1,),), (0,)),           # overlap -> affine
+    ((8192,), (1000,), (3,), ((8,),), ((2,),), (5,)),           # gaps + strided fitting -> affine
+    ((1000,), (999,), (7,), ((1,),), ((1,),), (17,)),           # wraps -> generic
+    ((64, 48), (48, 64), (1,), ((0, 1), (1, 0)), ((0,), (0,)), (0, 0)),   # transpose
+])
+@pytest.mark.parametrize("devices", [1, 3])
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+def test_tile_copy_plans_vs_oracle(case, devices, dtype):
+    from paper_1105_4424_b200 import _capi
+    arr, rep, pat, P, F, o = case
+    R = int(np.prod(rep))
+    npat = int(np.prod(pat))
+    ts = dict(array=arr, rep=rep, pattern=pat, origin=o, paving=P, fitting=F)
+    # dense output [R * npat] with the same rep shape
+    q = len(rep)
+    strides = [int(np.prod(rep[j + 1:])) * npat for j in range(q)]
+    td = dict(array=(R * npat,), rep=rep, pattern=pat, origin=(0,), paving=(tuple(strides),),
+              fitting=(tuple(int(np.prod(pat[k + 1:])) for k in range(len(pat))),))
+    src = (np.arange(int(np.prod(arr))) % (1 << 20)).astype(dtype) + 1
+    ports = {"src": _spec(ts, "in", dtype), "dst": _spec(td, "out", dtype)}
+    res = _run_tile("tile_copy", {"src": ts, "dst": td}, ports, {"src": src}, devices)
+    ref = orc.run_tile_task("tile_copy", {"src": ts, "dst": td}, {"src": src},
+                            {"dst": (R * npat, np.dtype(dtype))}, R, devices)["dst"]
+    assert np.array_equal(res.outputs["p_dst"], ref)
+    bts, btd = _tiler(ts).bind(arr, rep), _tiler(td).bind(td["array"], rep)
+    name = _capi.plan_name(_capi.make_task("tile_copy", dtype, [bts, btd]), 0, R)
+    assert name.startswith("tile_copy.")
+
+
+def _gemm_bound(a64, b64, K):
+    return (2.0 ** -9 + K * 2.0 ** -23) * (np.abs(a64) @ np.abs(b64))
+
+
+@pytest.mark.parametrize("M,N,K,devices", [
+    (256, 256, 256, 1), (128, 256, 64, 1), (300, 520, 200, 1), (1000, 700, 333, 3),
+    (37, 23, 19, 5), (1024, 1024, 4096, 2), (513, 1031, 96, 7)])
+def test_matmul_tf32_within_stated_bound(M, N, K, devices):
+    from paper_1105_4424_b200 import _capi
+    g = orc.gemm_tilers(M, N, K)
+    rng = np.random.default_rng(M * 7 + N)
+    a = rng.standard_normal(M * K).astype(np.float32)
+    b = rng.standard_normal(K * N).astype(np.float32)
+    ports = {"a": f"in float32 [{M},{K}]", "b": f"in float32 [{K},{N}]", "c": f"out float32 [{M},{N}]"}
+    res = _run_tile("matmul", g, ports, {"a": a, "b": b}, devices)
+    c = res.outputs["p_c"].reshape(M, N)
+    a64, b64 = a.reshape(M, K).astype(np.float64), b.reshape(K, N).astype(np.float64)
+    c64 = a64 @ b64
+    err = np.abs(c - c64)
+    assert np.all(err <= _gemm_bound(a64, b64, K)), float(np.max(err / _gemm_bound(a64, b64, K)))
+    assert np.linalg.norm(c - c64) / np.linalg.norm(c64) < 2e-3
+    bt = [_tiler(g[k]).bind(g[k]["array"], (M, N)) for k in "abc"]
+    task = _capi.make_task("matmul", "float32", bt)
+    expect = "matmul.tcgen05_tf32" if (K % 4 == 0 and N % 4 == 0) else "matmul.generic_exact"
+    ta = torch.zeros(4, device="cuda")
+    assert _capi.plan_name(task, 0, M * N, [ta.data_ptr()] * 3) == expect
+
+
+@pytest.mark.parametrize("bt", [False, True])
+def test_matmul_tf32_operand_majorness(bt):
+    """B given as [N, K] (K-major) and A given as [K, M] (M-major) hit the other TMA layouts."""
+    M, N, K = 384, 512, 160
+    rng = np.random.default_rng(3)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    B = rng.standard_normal((K, N)).astype(np.float32)
+    if bt:   # a row-major [M,K]; b stored transposed [N,K]
+        ta = dict(array=(M, K), rep=(M, N), pattern=(K,), origin=(0, 0), paving=((1, 0), (0, 0)),
+                  fitting=((0,), (1,)))
+        tb = dict(array=(N, K), rep=(M, N), pattern=(K,), origin=(0, 0), paving=((0, 1), (0, 0)),
+                  fitting=((0,), (1,)))
+        a_bind, b_bind, a_arr, b_arr = A.ravel(), B.T.copy().ravel(), (M, K), (N, K)
+    else:    # a stored transposed [K,M]; b row-major [K,N]
+        ta = dict(array=(K, M), rep=(M, N), pattern=(K,), origin=(0, 0), paving=((0, 0), (1, 0)),
+                  fitting=((1,), (0,)))
+        tb = dict(array=(K, N), rep=(M, N), pattern=(K,), origin=(0, 0), paving=((0, 0), (0, 1)),
+                  fitting=((1,), (0,)))
+        a_bind, b_bind, a_arr, b_arr = A.T.copy().ravel(), B.ravel(), (K, M), (K, N)
+    tc = dict(array=(M, N), rep=(M, N), pattern=(1,), origin=(0, 0), paving=((1, 0), (0, 1)),
+              fitting=((0,), (0,)))
+    ports = {"a": f"in float32 [{a_arr[0]},{a_arr[1]}]", "b": f"in float32 [{b_arr[0]},{b_arr[1]}]",
+             "c": f"out float32 [{M},{N}]"}
+    res = _run_tile("matmul", {"a": ta, "b": tb, "c": tc}, ports, {"a": a_bind, "b": b_bind}, 3)
+    c = res.outputs["p_c"].reshape(M, N)
+    a64, b64 = A.astype(np.float64), B.astype(np.float64)
+    assert np.all(np.abs(c - a64 @ b64) <= _gemm_bound(a64, b64, K))
+
+
+def test_c1_matmul_256_exact_equals_reference(golden):
+    """Config C1 through the drop-in: exact mode is bit-identical to the reference executor."""
+    data, _ = golden
+    g = orc.gemm_tilers(256, 256, 256)
+    ports = {"a": "in float32 [256,256]", "b": "in float32 [256,256]", "c": "out float32 [256,256]"}
+    b = {"a": data["matmul_c1_256/a"], "b": data["matmul_c1_256/b"]}
+    for d in (1, 8):
+        res = _run_tile("matmul", g, ports, b, d, precision="exact")
+        assert np.array_equal(res.outputs["p_c"], data["matmul_c1_256/out"])
+        res = _run_tile("matmul", g, ports, b, d)
+        a64 = data["matmul_c1_256/a"].reshape(256, 256).astype(np.float64)
+        b64 = data["matmul_c1_256/b"].reshape(256, 256).astype(np.float64)
+        c = res.outputs["p_c"].reshape(256, 256)
+        assert np.all(np.abs(c - a64 @ b64) <= _gemm_bound(a64, b64, 256))
+
+
+def test_identity_ops_vs_reference_golden(golden):
+    from paper_1105_4424_b200 import builders
+    from paper_1105_4424_b200.partition import build_schedule
+    from paper_1105_4424_b200.executor import execute_schedule
+    data, meta = golden
+    specs = {
+        "copy": (["src in {t} [{n}]", "dst out {t} [{n}]"], ["i in {t} [{n}]", "o out {t} [{n}]"],
+                 ["i -> t.src", "t.dst -> o"]),
+        "sub": (["x in {t} [{n}]", "y in {t} [{n}]", "z out {t} [{n}]"],
+                ["i1 in {t} [{n}]", "i2 in {t} [{n}]", "o out {t} [{n}]"], ["i1 -> t.x", "i2 -> t.y", "t.z -> o"]),
+        "scale": (["y inout {t} [{n}]", "a in {t} [1]"], ["i in {t} [{n}]", "s in {t} [1]", "o out {t} [{n}]"],
+                  ["i -> t.y", "s -> t.a", "t.y -> o"]),
+        "axpy": (["y inout {t} [{n}]", "x in {t} [{n}]", "a in {t} [1]"],
+                 ["i in {t} [{n}]", "v in {t} [{n}]", "s in {t} [1]", "o out {t} [{n}]"],
+                 ["i -> t.y", "v -> t.x", "s -> t.a", "t.y -> o"]),
+        "dot_partial": (["a in {t} [{n}]", "b in {t} [{n}]", "s out {t} [1]"],
+                        ["i1 in {t} [{n}]", "i2 in {t} [{n}]", "o out {t} [1]"], ["i1 -> t.a", "i2 -> t.b", "t.s -> o"]),
+    }
+    for key in sorted(k for k in meta if k.startswith("ident_") and meta[k]["op"] in specs):
+        m = meta[key]
+        ports, rports, conns = specs[m["op"]]
+        fmt = dict(t=m["dtype"], n=m["n"])
+        allocs = [f"allocate data {b} onto {'host.ram' if b == 's' else 'dev.gmem'}" for b in m["bind"]]
+        allocs += ["allocate data t.s onto host.ram"] if m["op"] == "dot_partial" else []
+        allocs += ["allocate task t onto dev.cu"]
+        model = builders.single_task_model(m["op"], [p.format(**fmt) for p in ports],
+                                           [p.format(**fmt) for p in rports], conns, allocs, m["n"])
+        bind = {b: data[f"{key}/in_{b}"] for b in m["bind"]}
+        res = execute_schedule(model, build_schedule(model, m["devices"]), bind, m["devices"])
+        ref = data[f"{key}/out"]
+        if m["op"] == "dot_partial":
+            tol = 1e-12 if m["dtype"] == "float64" else 1e-5
+            assert abs(float(res.outputs["o"][0]) - float(ref[0])) <= tol * max(1.0, abs(float(ref[0]))), key
+        else:
+            assert np.array_equal(res.outputs["o"], ref), key
+
+
+def test_spmv_vs_reference_golden(golden):
+    from paper_1105_4424_b200 import builders
+    from paper_1105_4424_b200.partition import build_schedule
+    from paper_1105_4424_b200.executor import execute_schedule
+    data, meta = golden
+    for key in sorted(k for k in meta if k.startswith("ident_spmv")):
+        m = meta[key]
+        n = m["n"]
+        rp, ci = data[f"{key}/rowptr"], data[f"{key}/colidx"]
+        nnz = ci.size
+        model = builders.single_task_model(
+            "spmv_csr",
+            [f"rowptr in int32 [{n + 1}]", f"colidx in int32 [{nnz}]", f"values in float64 [{nnz}]",
+             f"x in float64 [{n}]", f"y out float64 [{n}]"],
+            [f"rp in int32 [{n + 1}]", f"ci in int32 [{nnz}]", f"va in float64 [{nnz}]",
+             f"vx in float64 [{n}]", f"o out float64 [{n}]"],
+            ["rp -> t.rowptr", "ci -> t.colidx", "va -> t.values", "vx -> t.x", "t.y -> o"],
+            ["allocate data rp onto dev.gmem", "allocate data ci onto dev.gmem", "allocate data va onto dev.gmem",
+             "allocate data vx onto dev.gmem", "allocate data t.y onto dev.gmem", "allocate task t onto dev.cu"], n)
+        res = execute_schedule(model, build_schedule(model, m["devices"]),
+                               {"rp": rp, "ci": ci, "va": data[f"{key}/values"], "vx": data[f"{key}/x"]},
+                               m["devices"])
+        assert np.array_equal(res.outputs["o"], data[f"{key}/out"]), key
+
+
+def test_filter_and_stencil_random_vs_oracle():
+    """Filters/stencil at sizes beyond the golden set, exact order, several shard counts."""
+    cases = [("stencil", orc.stencil_tilers(97, 131), orc.stencil_weights()),
+             ("hfilter", orc.hfilter_tilers(3, 17, 256), orc.hfilter_weights()),
+             ("vfilter", orc.vfilter_tilers(2, 45, 96), orc.vfilter_weights())]
+    rng = np.random.default_rng(77)
+    for op, t, w in cases:
+        nx = int(np.prod(t["x"]["array"]))
+        ny = int(np.prod(t["y"]["array"]))
+        x = rng.random(nx).astype(np.float32)
+        R = int(np.prod(t["x"]["rep"]))
+        ports = {"x": _spec(t["x"], "in", "float32"), "w": f"in float32 [{w.size}]",
+                 "y": _spec(t["y"], "out", "float32")}
+        for d in (1, 4):
+            res = _run_tile(op, t, ports, {"x": x, "w": w}, d)
+            ref = orc.run_tile_task(op, t, {"x": x, "w": w}, {"y": (ny, np.float32)}, R, d)["y"]
+            assert np.array_equal(res.outputs["p_y"].view(np.uint32), ref.view(np.uint32)), (op, d)
+
+
+def test_missing_library_fails_loudly(tmp_path, monkeypatch):
+    from paper_1105_4424_b200 import _capi
+    saved = _capi._lib
+    try:
+        _capi._lib = None
+        with pytest.raises(_capi.NativeLibraryError):
+            _capi.load(tmp_path / "nope.so")
+    finally:
+        _capi._lib = saved

@@ -1,0 +1,214 @@
+"""Host-side logic and the C ABI surface — runs without a GPU."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+from hypothesis import given, settings, strategies as st
+
+from oracle import aol_oracle as orc
+from paper_1105_4424_b200 import (INTRINSICS, IntrinsicShapeMismatch, Tiler, TilerError, UnknownIntrinsic,
+                                  WorkRange, builders, build_schedule, check_task_signature, partition_equally)
+from paper_1105_4424_b200 import _capi
+
+ROOT = Path(__file__).resolve().parent.parent
+REF_SRC = Path("/root/reference/pkg/src")
+
+
+# -- C ABI -------------------------------------------------------------------
+
+def header_functions():
+    text = (ROOT / "include" / "aol_b200.h").read_text()
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(aol_\w+)\s*\(", text, re.M)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = ctypes.CDLL(str(_capi.LIB_PATH))
+    names = header_functions()
+    assert len(names) >= 8
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(_capi.EXPORTS)
+    assert _capi.load().aol_abi_version() == _capi.ABI_VERSION
+
+
+def test_struct_layout_matches_header():
+    assert ctypes.sizeof(_capi.AolTiler) == 16 + 4 * 4 * 8 + 2 * 16 * 8
+    assert ctypes.sizeof(_capi.AolTask) == 32 + 4 * ctypes.sizeof(_capi.AolTiler)
+
+
+def _bt(d):
+    return Tiler(d["origin"], d["paving"], d["fitting"], d["pattern"]).bind(d["array"], d["rep"])
+
+
+def test_validate_and_plan_without_gpu():
+    g = orc.gemm_tilers(64, 64, 32)
+    task = _capi.make_task("matmul", "float32", [_bt(g[k]) for k in "abc"])
+    _capi.validate(task)
+    assert _capi.plan_name(task, 0, 64 * 64) == "matmul.generic_exact"      # no ports -> no TMA check
+    bad = _capi.make_task("matmul", "float32", [_bt(g[k]) for k in "ab"])
+    with pytest.raises(_capi.AolError, match="tilers"):
+        _capi.validate(bad)
+    cp = dict(array=(100,), rep=(25,), pattern=(4,), origin=(0,), paving=((4,),), fitting=((1,),))
+    t = _capi.make_task("tile_copy", "float32", [_bt(cp), _bt(cp)])
+    assert _capi.plan_name(t, 0, 25) == "tile_copy.stream16"
+    ov = dict(cp, rep=(49,), paving=((2,),))
+    dst = dict(array=(196,), rep=(49,), pattern=(4,), origin=(0,), paving=((4,),), fitting=((1,),))
+    assert _capi.plan_name(_capi.make_task("tile_copy", "float32", [_bt(ov), _bt(dst)]), 0, 49) == "tile_copy.affine"
+    wr = dict(cp, origin=(99,))
+    assert _capi.plan_name(_capi.make_task("tile_copy", "float32", [_bt(wr), _bt(cp)]), 0, 25) == "tile_copy.generic"
+    mism = dict(cp, pattern=(2,), array=(50,), paving=((2,),))
+    with pytest.raises(_capi.AolError, match="pattern"):
+        _capi.validate(_capi.make_task("tile_copy", "float32", [_bt(cp), _bt(mism)]))
+
+
+# -- partitioning (partition.py:105-121) ---------------------------------------
+
+def test_partition_paper_scale():
+    ranges = partition_equally(132651, 4)
+    assert [r.count for r in ranges] == [33163, 33163, 33163, 33162]
+    assert [r.offset for r in ranges] == [0, 33163, 66326, 99489]
+    assert partition_equally(10, 1) == [WorkRange(0, 10)]
+    assert len(partition_equally(3, 8)) == 3
+    with pytest.raises(ValueError):
+        partition_equally(0, 4)
+
+
+@settings(max_examples=300, deadline=None)
+@given(st.integers(1, 100000), st.integers(1, 16))
+def test_partition_matches_oracle(total, devices):
+    assert [(r.offset, r.count) for r in partition_equally(total, devices)] == orc.partition_equally(total, devices)
+
+
+def test_partition_golden(golden):
+    _, meta = golden
+    for key, ranges in meta["_partition"].items():
+        t, d = map(int, key.split(","))
+        assert [[r.offset, r.count] for r in partition_equally(t, d)] == ranges
+
+
+# -- tilers -------------------------------------------------------------------
+
+def test_tiler_bind_errors():
+    with pytest.raises(TilerError):
+        Tiler([0], [[1]], [[1]], [2]).bind((4, 4), (4,))        # origin rank != array rank
+    with pytest.raises(TilerError):
+        Tiler([0], [[1, 0]], [[1]], [2]).bind((4,), (4,))       # paving not a x q
+    with pytest.raises(TilerError):
+        Tiler([0], [[1]], [[1]], [0]).bind((4,), (4,))          # zero pattern dim
+    with pytest.raises(TilerError):
+        Tiler([0] * 5, [[1]] * 5, [[1]] * 5, [1]).bind((2,) * 5, (1,))
+
+
+def test_tiler_affine_and_wrap():
+    g = orc.gemm_tilers(8, 6, 5)
+    a = _bt(g["a"])
+    assert not a.wraps and a.affine == (0, (5, 0), (1,))
+    s = _bt(orc.stencil_tilers(8, 8)["x"])
+    assert s.wraps and s.affine is None
+
+
+def test_tiler_offsets_match_oracle_loop():
+    rng = np.random.default_rng(5)
+    for _ in range(60):
+        a, q, p = (int(x) for x in rng.integers(1, 4, 3))
+        d = dict(array=tuple(int(x) for x in rng.integers(1, 7, a)), rep=tuple(int(x) for x in rng.integers(1, 5, q)),
+                 pattern=tuple(int(x) for x in rng.integers(1, 4, p)),
+                 origin=tuple(int(x) for x in rng.integers(-9, 9, a)),
+                 paving=tuple(tuple(int(x) for x in rng.integers(-4, 5, q)) for _ in range(a)),
+                 fitting=tuple(tuple(int(x) for x in rng.integers(-4, 5, p)) for _ in range(a)))
+        bt = _bt(d)
+        assert np.array_equal(bt.offsets(), np.array(orc.tiler_offsets_loop(d, 0, bt.rep_total)))
+
+
+def test_injectivity():
+    _bt(orc.gemm_tilers(64, 32, 8)["c"]).check_injective()
+    _bt(orc.stencil_tilers(16, 16)["y"]).check_injective()
+    big = dict(array=(1 << 30,), rep=(1 << 28,), pattern=(4,), origin=(0,), paving=((4,),), fitting=((1,),))
+    _bt(big).check_injective()                                  # mixed-radix proof, no enumeration
+    with pytest.raises(TilerError):
+        _bt(dict(array=(100,), rep=(20,), pattern=(4,), origin=(0,), paving=((2,),), fitting=((1,),))).check_injective()
+    with pytest.raises(TilerError):   # wraps onto itself
+        _bt(dict(array=(10,), rep=(10,), pattern=(1,), origin=(0,), paving=((2,),), fitting=((0,),))).check_injective()
+
+
+# -- registry / signature checks ------------------------------------------------
+
+def _copy_model(op="copy", ports=("src in float64 [64]", "dst out float64 [64]")):
+    return builders.single_task_model(
+        op, list(ports), ["i in float64 [64]", "o out float64 [64]"], ["i -> t.src", "t.dst -> o"],
+        ["allocate data i onto dev.gmem", "allocate data t.dst onto dev.gmem", "allocate task t onto dev.cu"], 64)
+
+
+def test_signature_checks():
+    m = _copy_model()
+    assert check_task_signature("t", m.application_components["T"]).name == "copy"
+    with pytest.raises(UnknownIntrinsic):
+        check_task_signature("t", _copy_model(op="nope").application_components["T"])
+    with pytest.raises(IntrinsicShapeMismatch, match="expects ports"):
+        check_task_signature("t", _copy_model(ports=("src in float64 [64]", "z out float64 [64]"))
+                             .application_components["T"])
+    tm = builders.tile_task_model("tile_copy", {"src": "in float32 [64]", "dst": "out float32 [64]"}, {}, (16,))
+    with pytest.raises(IntrinsicShapeMismatch, match="no tiler"):
+        check_task_signature("t", tm.application_components["T"])
+    cp = Tiler([0], [[4]], [[1]], [4])
+    tm = builders.tile_task_model("tile_copy", {"src": "in float32 [64]", "dst": "out float32 [64]"},
+                                  {"src": cp, "dst": cp}, (16,))
+    assert check_task_signature("t", tm.application_components["T"]).tile
+    ov = Tiler([0], [[2]], [[1]], [4])
+    tm = builders.tile_task_model("tile_copy", {"src": "in float32 [64]", "dst": "out float32 [64]"},
+                                  {"src": cp, "dst": ov}, (16,))
+    with pytest.raises(IntrinsicShapeMismatch, match="injective"):
+        check_task_signature("t", tm.application_components["T"])
+
+
+def test_schedule_mirror():
+    m = _copy_model()
+    s = build_schedule(m, 3)
+    (step,) = s.steps
+    assert [(l.range.offset, l.range.count, l.global_size, l.local_size) for l in step.launches] == \
+        [(0, 22, 24, 8), (22, 21, 24, 8), (43, 21, 24, 8)]
+
+
+@pytest.mark.skipif(not REF_SRC.exists(), reason="reference not present (GPU box)")
+def test_reference_models_drive_the_mirror(monkeypatch):
+    """A model parsed by the unmodified reference front-end is accepted by the host mirror."""
+    import sys
+    sys.dont_write_bytecode = True
+    monkeypatch.syspath_prepend(str(REF_SRC))
+    import gmodelc
+    from paper_1105_4424_b200.model import connected_port_groups
+    text = gmodelc.bundled_model_text()
+    model = gmodelc.parse_model(text)
+    for d in (1, 4):
+        ref = gmodelc.build_schedule(model, d)
+        mine = build_schedule(model, d)
+
+        def flat(steps):
+            out = []
+            for s in steps:
+                if hasattr(s, "launches"):
+                    out.append(("D", s.task_path, s.op, tuple((l.device_index, l.range.offset, l.range.count,
+                                                               l.global_size, l.local_size) for l in s.launches)))
+                elif hasattr(s, "body"):
+                    out.append(("L", s.task_path, s.tolerance, s.max_iterations, s.relres_port, tuple(flat(s.body))))
+                else:
+                    out.append(("H", s.task_path, s.op))
+            return out
+        assert flat(ref.steps) == flat(mine.steps)
+    assert connected_port_groups(model) == gmodelc.metamodel.connected_port_groups(model)
+    for comp in model.application_components.values():
+        if comp.elementary_op:
+            assert check_task_signature("x", comp).name == gmodelc.intrinsics.check_task_signature("x", comp).name
+    reg = dict(gmodelc.intrinsics.INTRINSICS)
+    from paper_1105_4424_b200 import register_into
+    register_into(reg)
+    assert "matmul" in reg and reg["copy"] is gmodelc.intrinsics.INTRINSICS["copy"]
+
+
+def test_registry_has_reference_and_tile_ops():
+    for op in ("spmv_csr", "dot_partial", "axpy", "scale", "copy", "sub", "div", "neg", "rel_residual",
+               "tile_copy", "matmul", "tile_filter", "hfilter", "vfilter", "stencil", "tile_sum"):
+        assert op in INTRINSICS
