@@ -17,6 +17,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "aol_common.cuh"
@@ -42,6 +43,7 @@ struct Params {
   int64_t first, last; // inclusive linear repetition range
   int m_tiles, n_tiles, k_blocks, num_tiles;
   int c_vec;           // 16-byte stores allowed
+  uint32_t* dbg;       // debug: first smem stage (48 KB) is copied here when non-null
 };
 
 // ------------------------------------------------------------ PTX helpers ----
@@ -106,22 +108,23 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// Shared-memory matrix descriptor (tcgen05 "version 1"), SWIZZLE_128B.
-__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+// Shared-memory matrix descriptor (tcgen05 "version 1").  layout: 2 = SWIZZLE_128B,
+// 1 = SWIZZLE_128B_BASE32B (128B swizzle with 32-byte atoms, the only MN-major tf32 layout).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
   return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
-         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | ((uint64_t)layout << 61);
 }
 
 // Operand tile of R rows (M or N) x BK:
 //   K-major : one TMA box {BK, R}; rows of 128 B; 8-row atoms 1024 B apart (SBO);
 //             the k-th MMA slice starts 32 B further inside the swizzle row.
-//   MN-major: R/32 boxes {32, BK}; each box = BK rows (k) of 32 elements (128 B);
-//             boxes 4 KB apart (LBO), 8-k-row groups 1024 B apart (SBO);
-//             the k-th MMA slice starts 8 rows (1024 B) further.
+//   MN-major: R/32 boxes {32, BK} with the 128B/32B-atom swizzle; each box = BK rows
+//             (k) of 32 elements (128 B); boxes 4 KB apart (LBO), 4-k-row atoms
+//             512 B apart (SBO); the k-th MMA slice starts 8 rows (1024 B) further.
 template <bool KMAJOR>
 __device__ __forceinline__ uint64_t operand_desc(uint32_t base, int k) {
-  if (KMAJOR) return smem_desc(base + k * (UMMA_K * 4), 16, 1024);
-  return smem_desc(base + k * (UMMA_K * 128), BK * 128, 1024);
+  if (KMAJOR) return smem_desc(base + k * (UMMA_K * 4), 16, 1024, 2);
+  return smem_desc(base + k * (UMMA_K * 128), BK * 128, 512, 1);
 }
 
 template <bool KMAJOR, int R>
@@ -218,6 +221,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
+          if (p.dbg && tile == (int)blockIdx.x && kb == 0 && blockIdx.x == 0) {
+            const uint32_t* src = reinterpret_cast<const uint32_t*>(smem + stage * STAGE_BYTES);
+            for (int i = 0; i < STAGE_BYTES / 4; ++i) p.dbg[i] = src[i];
+          }
           const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
           const uint32_t sb = sa + A_BYTES;
 #pragma unroll
@@ -295,7 +302,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // 2-D fp32 tensor map: dims {inner, outer}, row pitch in elements, box {bi, bo}, 128B swizzle.
 static int make_map(CUtensorMap* map, const float* base, int64_t inner, int64_t outer, int64_t pitch, int bi,
-                    int bo) {
+                    int bo, bool kmajor) {
   auto fn = encode_fn();
   if (!fn) return fail(AOL_ECUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
@@ -303,7 +310,9 @@ static int make_map(CUtensorMap* map, const float* base, int64_t inner, int64_t 
   cuuint32_t box[2] = {(cuuint32_t)bi, (cuuint32_t)bo};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  kmajor ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(AOL_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
   return AOL_OK;
@@ -368,11 +377,11 @@ int launch_gemm_tf32(const aol_task& t, int64_t first, int64_t count, void* cons
   float* C = static_cast<float*>(ports[2]) + g.cc;
   CUtensorMap ma, mb;
   int rc;
-  if (g.a_kmajor) rc = make_map(&ma, A, g.K, g.M, g.lda, BK, BM);
-  else rc = make_map(&ma, A, g.M, g.K, g.lda, 32, BK);
+  if (g.a_kmajor) rc = make_map(&ma, A, g.K, g.M, g.lda, BK, BM, true);
+  else rc = make_map(&ma, A, g.M, g.K, g.lda, 32, BK, false);
   if (rc) return rc;
-  if (g.b_kmajor) rc = make_map(&mb, B, g.K, g.N, g.ldb, BK, BN);
-  else rc = make_map(&mb, B, g.N, g.K, g.ldb, 32, BK);
+  if (g.b_kmajor) rc = make_map(&mb, B, g.K, g.N, g.ldb, BK, BN, true);
+  else rc = make_map(&mb, B, g.N, g.K, g.ldb, 32, BK, false);
   if (rc) return rc;
 
   Params p{};
@@ -388,6 +397,7 @@ int launch_gemm_tf32(const aol_task& t, int64_t first, int64_t count, void* cons
   p.k_blocks = (int)((g.K + BK - 1) / BK);
   p.num_tiles = p.m_tiles * p.n_tiles;
   p.c_vec = ((uintptr_t)C % 16 == 0) && (g.ldc % 4 == 0);
+  if (const char* dbg = getenv("AOL_GEMM_DBG")) p.dbg = reinterpret_cast<uint32_t*>(strtoull(dbg, nullptr, 10));
 
   void (*kern)(const CUtensorMap, const CUtensorMap, Params);
   if (g.a_kmajor) kern = g.b_kmajor ? k_gemm_tf32<true, true> : k_gemm_tf32<true, false>;
