@@ -105,3 +105,36 @@ def test_identity_ops_match_reference(golden):
             assert abs(arrays["s"][0] - ref[0]) <= 1e-12 * max(1.0, abs(ref[0])) * (1e5 if dt == "float32" else 1)
         else:
             assert np.array_equal(arrays[outn], ref), key
+
+
+def test_c_oracle_matches_numpy_oracle_and_reference(golden):
+    """The C restatement (bench CPU baseline, big checks) agrees bit for bit with the pinned numpy oracle."""
+    from oracle import c_oracle as co
+    data, meta = golden
+    for name in _cases(meta, {"tile_copy", "matmul", "tile_filter", "hfilter", "vfilter", "stencil"}):
+        m = meta[name]
+        t = m["tilers"]
+        ref = data[f"{name}/out"]
+        for tl in t.values():
+            R = int(np.prod(tl["rep"]))
+            assert np.array_equal(co.tiler_offsets(tl, 0, R), orc.tiler_offsets(tl, 0, R))
+        out = np.zeros_like(ref)
+        if m["op"] == "tile_copy":
+            R = int(np.prod(t["src"]["rep"]))
+            co.tile_copy(data[f"{name}/src"], out, t["src"], t["dst"], 0, R)
+        elif m["op"] == "matmul":
+            R = int(np.prod(t["c"]["rep"]))
+            co.matmul(data[f"{name}/a"], data[f"{name}/b"], out, t["a"], t["b"], t["c"], 0, R)
+        else:
+            R = int(np.prod(t["x"]["rep"]))
+            co.tile_filter(data[f"{name}/x"], data[f"{name}/w"], out, t["x"], t["y"], 0, R)
+        assert np.array_equal(out.view(np.uint32), ref.view(np.uint32)), name
+    a = data["matmul_c1_256/a"]
+    b = data["matmul_c1_256/b"]
+    c = np.zeros(256 * 256, np.float32)
+    co.gemm_rows(a, b, c, 256, 256, 0, 256)
+    assert np.array_equal(c, data["matmul_c1_256/out"])
+    x = data["stencil_32x48/x"]
+    y = np.zeros_like(x)
+    co.stencil_rows(x, data["stencil_32x48/w"], y, 32, 48, 0, 32)
+    assert np.array_equal(y, data["stencil_32x48/out"])
