@@ -74,6 +74,10 @@ class Clocks:
                  "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
+            return
+        deadline = time.time() + 8.0            # wait for the first sample before timing
+        while time.time() < deadline and Path(self.path).stat().st_size == 0:
+            time.sleep(0.05)
 
     def stop(self) -> dict:
         if self.proc is None:
@@ -121,8 +125,9 @@ def profile_traffic(key: str):
     return None
 
 
-def tf32_peak(torch, device) -> float | None:
-    """cuBLAS TF32 8192^3 best-of-10 TFLOP/s (the measurement recipe MEASURED_PEAKS uses for bf16)."""
+def tf32_peak(torch, device, sustain_s: float = 4.0):
+    """cuBLAS TF32 8192^3 TFLOP/s: best of 10 (burst) and back to back for ``sustain_s`` seconds
+    (sustained, under the power cap) — the recipe MEASURED_PEAKS.json uses for bf16."""
     try:
         torch.backends.cuda.matmul.allow_tf32 = True
         n = 8192
@@ -139,9 +144,20 @@ def tf32_peak(torch, device) -> float | None:
             e.record()
             e.synchronize()
             best = min(best, s.elapsed_time(e))
+        burst = 2 * n ** 3 / (best * 1e-3) / 1e12
+        sustained = None
+        if sustain_s > 0:
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = max(1, int(sustain_s / (best * 1e-3)))
+            s.record()
+            for _ in range(reps):
+                torch.matmul(a, b)
+            e.record()
+            e.synchronize()
+            sustained = 2 * n ** 3 * reps / (s.elapsed_time(e) * 1e-3) / 1e12
         del a, b
         torch.cuda.empty_cache()
-        return 2 * n ** 3 / (best * 1e-3) / 1e12
+        return burst, sustained
     finally:
         torch.backends.cuda.matmul.allow_tf32 = False
 
@@ -188,15 +204,17 @@ class MatmulWorkload:
         gen = torch.Generator().manual_seed(7)
         self.ha = torch.randn(self.M * self.K, generator=gen).pin_memory()
         self.hb = torch.randn(self.K * self.N, generator=gen).pin_memory()
+        self.hc = torch.empty(self.M * self.N).pin_memory()
         self.e2e_bytes = (self.ha.numel() * 4 + self.hb.numel() * 4, self.M * self.N * 4)
 
     def e2e_step(self):
         from paper_1105_4424_b200.executor import execute_schedule
-        res = execute_schedule(self.model, self.schedule, {"p_a": self.ha, "p_b": self.hb}, 1)
+        res = execute_schedule(self.model, self.schedule, {"p_a": self.ha, "p_b": self.hb}, 1,
+                               out={"p_c": self.hc})
         return res.outputs["p_c"]
 
     def e2e_free(self):
-        del self.ha, self.hb
+        del self.ha, self.hb, self.hc
 
     # CPU oracle on a bounded sample of rows
     def cpu_sample(self, seconds: float = 8.0):
@@ -294,32 +312,39 @@ def run_gpu(args):
     e2e = None
     if not args.no_e2e:
         wl.e2e_setup()
-        for _ in range(max(1, min(args.warmup, 2))):
+        for _ in range(3):
             wl.e2e_step()
         torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()
-        for _ in range(args.steps):
+        for _ in range(args.e2e_steps):
             wl.e2e_step()
         torch.cuda.synchronize()
         el = allmax(time.perf_counter() - t0)
         wl.e2e_free()
-        e2e = {"value": wl.units_per_step * world * args.steps / el, "unit": wl.unit,
+        e2e = {"value": wl.units_per_step * world * args.e2e_steps / el, "unit": wl.unit,
                "h2d_bytes_per_step": wl.e2e_bytes[0] * world, "d2h_bytes_per_step": wl.e2e_bytes[1] * world,
-               "ms_per_step": el * 1e3 / args.steps,
-               "path": "paper_1105_4424_b200.executor.execute_schedule, pinned host bindings -> numpy outputs"}
+               "ms_per_step": el * 1e3 / args.e2e_steps, "steps": args.e2e_steps,
+               "path": "paper_1105_4424_b200.executor.execute_schedule, pinned host bindings and pinned out= buffers"}
 
     peaks = measured_peaks()
     out = None
     if rank == 0:
         achieved = wl.units_per_step / (kernel_ms * 1e-3)
         if wl.bound == "tensor":
-            tf32 = None if args.no_peak else tf32_peak(torch, device)
-            peak = tf32 if tf32 else peaks.get("bf16_tflops", 1590.0) / 2
-            peak_src = ("cuBLAS TF32 8192^3 best of 10, measured in this run" if tf32 else
-                        "half of MEASURED_PEAKS bf16_tflops (no TF32 measurement)")
+            burst, sustained = (None, None) if args.no_peak else tf32_peak(torch, device)
+            long_region = total_ms > 250.0
+            if sustained and long_region:
+                peak, peak_src = sustained, ("cuBLAS TF32 8192^3 back to back for 4 s (sustained, power-capped), "
+                                             "measured in this run; the timed region is a long step")
+            elif burst:
+                peak, peak_src = burst, "cuBLAS TF32 8192^3 best of 10 (burst), measured in this run"
+            else:
+                peak, peak_src = peaks.get("bf16_tflops", 1590.0) / 2, "half of MEASURED_PEAKS bf16_tflops"
             roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                     "frac": achieved / peak, "traffic": profile_traffic(wl.name), "peak_source": peak_src,
+                    "tf32_cublas_burst": burst, "tf32_cublas_sustained": sustained,
+                    "frac_of_burst": achieved / burst if burst else None,
                     "bf16_peak_measured": peaks.get("bf16_tflops"),
                     "frac_of_bf16_peak": achieved / peaks["bf16_tflops"] if peaks.get("bf16_tflops") else None,
                     "kernel_ms": kernel_ms, "algorithmic": wl.algorithmic}
@@ -386,7 +411,8 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="matmul", choices=sorted(WORKLOADS))

@@ -258,24 +258,44 @@ class Executor:
         with torch.cuda.device(self.device):
             self.run_steps(self.schedule.steps, tol, max_iter)
 
-    def outputs(self, on_device: bool = False) -> dict:
+    def outputs(self, on_device: bool = False, out: dict | None = None) -> dict:
+        """Root out-port arrays, flat row-major (refexec.py:545-547).
+
+        ``out`` maps port name -> caller-owned host buffer (numpy array or
+        pinned torch tensor) that receives the result instead of a fresh array.
+        """
+        torch = _torch()
         root = self.model.application_components[self.model.application_root]
-        out = {}
+        res = {}
+        pending = False
         for port in root.ports:
             if enum_value(port.direction) != "out":
                 continue
             t = self.storage.array(port.name)
-            out[port.name] = t.clone() if on_device else t.cpu().numpy()
-        return out
+            if out is not None and port.name in out:
+                dst = out[port.name]
+                host = torch.from_numpy(dst) if isinstance(dst, np.ndarray) else dst
+                if host.numel() != t.numel():
+                    raise MissingBinding(f"output buffer '{port.name}' has {host.numel()} elements, "
+                                         f"port has {t.numel()}")
+                host.view(-1).copy_(t, non_blocking=True)
+                pending = True
+                res[port.name] = dst
+            else:
+                res[port.name] = t.clone() if on_device else t.cpu().numpy()
+        if pending:
+            torch.cuda.current_stream(self.device).synchronize()
+        return res
 
 
 def execute_schedule(model, schedule, bindings: dict, device_count: int, tol: float | None = None,
                      max_iter: int | None = None, *, tilers: dict | None = None, precision: str = "default",
-                     device_outputs: bool = False, device=None, stream=None) -> ExecutionResult:
+                     device_outputs: bool = False, out: dict | None = None, device=None,
+                     stream=None) -> ExecutionResult:
     """Interpret ``schedule`` on the B200 with ``device_count`` launch shards per device step."""
     ex = Executor(model, schedule, bindings, device_count, tilers=tilers, precision=precision,
                   device=device, stream=stream)
     ex.run(tol, max_iter)
-    outs = ex.outputs(on_device=device_outputs)
+    outs = ex.outputs(on_device=device_outputs, out=out)
     return ExecutionResult(outputs=outs, iterations=ex.iterations, final_relres=ex.final_relres,
                            converged=ex.converged)
