@@ -164,57 +164,84 @@ def tf32_peak(torch, device, sustain_s: float = 4.0):
 
 # --------------------------------------------------------------- workloads --
 
-class MatmulWorkload:
+def _tiler(d):
+    from paper_1105_4424_b200 import Tiler
+    return Tiler(d["origin"], d["paving"], d["fitting"], d["pattern"])
+
+
+def _spec(d, direction):
+    return f"{direction} float32 [{','.join(str(x) for x in d['array'])}]"
+
+
+class Workload:
+    """One repetitive-task schedule prepared in HBM; step() = one pass over one batch."""
+
+    name = "?"
+    unit = "GB/s"
+    bound = "hbm"
+
+    def _prepare(self, torch, device, model, schedule, dev_bindings: dict, host_specs: dict, outputs: dict):
+        from paper_1105_4424_b200.executor import Executor
+        self.torch, self.device = torch, device
+        self.model, self.schedule = model, schedule
+        self.ex = Executor(model, schedule, dev_bindings, 1)
+        self.host_specs, self.out_sizes = host_specs, outputs
+
+    def step(self):
+        self.ex.run()
+
+    def e2e_setup(self):
+        torch = self.torch
+        gen = torch.Generator().manual_seed(7)
+        self.hin = {k: (torch.rand(n, generator=gen) if kind == "rand" else torch.from_numpy(kind)).pin_memory()
+                    for k, (n, kind) in self.host_specs.items()}
+        self.hout = {k: torch.empty(n).pin_memory() for k, n in self.out_sizes.items()}
+        self.e2e_bytes = (sum(t.numel() * 4 for t in self.hin.values()),
+                          sum(t.numel() * 4 for t in self.hout.values()))
+
+    def e2e_step(self):
+        from paper_1105_4424_b200.executor import execute_schedule
+        return execute_schedule(self.model, self.schedule, self.hin, 1, out=self.hout).outputs
+
+    def e2e_free(self):
+        del self.hin, self.hout
+
+
+class MatmulWorkload(Workload):
     name = "matmul"
     unit = "TFLOP/s"
     bound = "tensor"
 
     def __init__(self, torch, device, rank, world, M=8192, N=8192, K=8192):
         from oracle import aol_oracle as orc
-        from paper_1105_4424_b200 import Tiler, builders
-        from paper_1105_4424_b200.executor import Executor
+        from paper_1105_4424_b200 import builders
         from paper_1105_4424_b200.partition import build_schedule, partition_equally
-        self.torch, self.device = torch, device
         self.M, self.N, self.K = M, N, K
         # weak scaling: the job's repetition space is [M*world, N]; this rank's contiguous
         # shard is M whole rows, executed as a local task over its input hull.
         shard = partition_equally(M * world * N, world)[rank]
         assert shard.count == M * N and shard.offset == rank * M * N
         g = orc.gemm_tilers(M, N, K)
-        self.tilers = {k: Tiler(v["origin"], v["paving"], v["fitting"], v["pattern"]) for k, v in g.items()}
-        self.model = builders.tile_task_model(
+        model = builders.tile_task_model(
             "matmul", {"a": f"in float32 [{M},{K}]", "b": f"in float32 [{K},{N}]", "c": f"out float32 [{M},{N}]"},
-            self.tilers, (M, N))
-        self.schedule = build_schedule(self.model, 1)
+            {k: _tiler(v) for k, v in g.items()}, (M, N))
         gen = torch.Generator(device=device).manual_seed(2 + rank)
         a = torch.randn(M * K, device=device, generator=gen)
         b = torch.randn(K * N, device=device, generator=torch.Generator(device=device).manual_seed(3))
-        self.ex = Executor(self.model, self.schedule, {"p_a": a, "p_b": b}, 1)
+        self._prepare(torch, device, model, build_schedule(model, 1), {"p_a": a, "p_b": b}, {}, {"p_c": M * N})
         del a, b
         self.units_per_step = 2.0 * M * N * K / 1e12          # TFLOP
         self.algorithmic = {"flop_per_launch": 2 * M * N * K, "per_unit": "2 FLOP per (m, n, k)"}
         self.workload = f"matmul {M}x{N}x{K} fp32 (TF32 tcgen05), rep space [{M}x{world},{N}] sharded by rows"
+        self.l2 = "inputs (768 MiB/rank) exceed the 126 MB L2"
 
-    def step(self):
-        self.ex.run()
-
-    # e2e through the public API with pinned host bindings
     def e2e_setup(self):
         torch = self.torch
         gen = torch.Generator().manual_seed(7)
-        self.ha = torch.randn(self.M * self.K, generator=gen).pin_memory()
-        self.hb = torch.randn(self.K * self.N, generator=gen).pin_memory()
-        self.hc = torch.empty(self.M * self.N).pin_memory()
-        self.e2e_bytes = (self.ha.numel() * 4 + self.hb.numel() * 4, self.M * self.N * 4)
-
-    def e2e_step(self):
-        from paper_1105_4424_b200.executor import execute_schedule
-        res = execute_schedule(self.model, self.schedule, {"p_a": self.ha, "p_b": self.hb}, 1,
-                               out={"p_c": self.hc})
-        return res.outputs["p_c"]
-
-    def e2e_free(self):
-        del self.ha, self.hb, self.hc
+        self.hin = {"p_a": torch.randn(self.M * self.K, generator=gen).pin_memory(),
+                    "p_b": torch.randn(self.K * self.N, generator=gen).pin_memory()}
+        self.hout = {"p_c": torch.empty(self.M * self.N).pin_memory()}
+        self.e2e_bytes = ((self.M * self.K + self.K * self.N) * 4, self.M * self.N * 4)
 
     # CPU oracle on a bounded sample of rows
     def cpu_sample(self, seconds: float = 8.0):
@@ -240,7 +267,220 @@ class MatmulWorkload:
                           f"k-ascending fp32, OpenMP {thr} threads, {dt:.2f} s"}
 
 
-WORKLOADS = {"matmul": MatmulWorkload}
+class StencilWorkload(Workload):
+    """Config C4: 3x3 toroidal stencil on a 16384^2 fp32 torus per rank (N independent tori)."""
+
+    name = "stencil"
+
+    def __init__(self, torch, device, rank, world, n=16384):
+        from oracle import aol_oracle as orc
+        from paper_1105_4424_b200 import builders
+        from paper_1105_4424_b200.partition import build_schedule
+        self.n = n
+        t = orc.stencil_tilers(n, n)
+        w = orc.stencil_weights()
+        model = builders.tile_task_model(
+            "stencil", {"x": _spec(t["x"], "in"), "w": "in float32 [9]", "y": _spec(t["y"], "out")},
+            {k: _tiler(v) for k, v in t.items()}, (n, n))
+        gen = torch.Generator(device=device).manual_seed(5 + rank)
+        x = torch.randn(n * n, device=device, generator=gen)
+        self._prepare(torch, device, model, build_schedule(model, 1),
+                      {"p_x": x, "p_w": torch.from_numpy(w).to(device)},
+                      {"p_x": (n * n, "rand"), "p_w": (9, w)}, {"p_y": n * n})
+        del x
+        self.units_per_step = 2.0 * n * n * 4 / 1e9            # GB (read x once, write y once)
+        self.algorithmic = {"bytes_per_launch": 2 * n * n * 4, "per_unit": "4 B read + 4 B written per element"}
+        self.workload = f"toroidal 3x3 stencil {n}x{n} fp32, origin (-1,-1), weights [1,2,1]^T[1,2,1]/16"
+        self.l2 = "inputs (1 GiB/rank) exceed the 126 MB L2"
+
+    def cpu_sample(self, seconds: float = 8.0):
+        from oracle import c_oracle as co
+        n = self.n
+        x = np.random.default_rng(5).standard_normal(n * n, dtype=np.float32)
+        y = np.zeros_like(x)
+        w = __import__("oracle.aol_oracle", fromlist=["x"]).stencil_weights()
+        t0 = time.perf_counter()
+        co.stencil_rows(x, w, y, n, n, 0, 256)
+        dt = time.perf_counter() - t0
+        rows = int(min(n, max(256, 256 * seconds / max(dt, 1e-3))))
+        t0 = time.perf_counter()
+        co.stencil_rows(x, w, y, n, n, 0, rows)
+        dt = time.perf_counter() - t0
+        return {"value": 2.0 * rows * n * 4 / dt / 1e9, "unit": "GB/s", "cores": co.threads(), "kind": "port",
+                "sample": f"{rows} of {n} rows, oracle/aol_oracle.c stencil, {dt:.2f} s"}
+
+
+class DownscalerWorkload(Workload):
+    """Config C3: H filter (13 taps, paving 8 -> 3 outputs) then V filter (14 taps, paving 9 -> 4 outputs)."""
+
+    name = "downscaler"
+
+    def __init__(self, torch, device, rank, world, frames=256, H=2160, W=3840):
+        from oracle import aol_oracle as orc
+        from paper_1105_4424_b200 import builders
+        from paper_1105_4424_b200.partition import build_schedule
+        th = orc.hfilter_tilers(frames, H, W)
+        Wo = th["y"]["array"][2]
+        tv = orc.vfilter_tilers(frames, H, Wo)
+        Ho = tv["y"]["array"][1]
+        wh, wv = orc.hfilter_weights(), orc.vfilter_weights()
+        model = builders.chain_model(
+            [("h", "hfilter", {"x": _spec(th["x"], "in"), "w": f"in float32 [{wh.size}]",
+                               "y": _spec(th["y"], "out")}, {k: _tiler(v) for k, v in th.items()},
+              th["x"]["rep"]),
+             ("v", "vfilter", {"x": _spec(tv["x"], "in"), "w": f"in float32 [{wv.size}]",
+                               "y": _spec(tv["y"], "out")}, {k: _tiler(v) for k, v in tv.items()},
+              tv["x"]["rep"])],
+            {"x": _spec(th["x"], "in"), "wh": f"in float32 [{wh.size}]", "wv": f"in float32 [{wv.size}]"},
+            {"y": _spec(tv["y"], "out")},
+            [("x", "h.x"), ("wh", "h.w"), ("h.y", "v.x"), ("wv", "v.w"), ("v.y", "y")])
+        nx = frames * H * W
+        gen = torch.Generator(device=device).manual_seed(4 + rank)
+        x = torch.rand(nx, device=device, generator=gen)
+        self._prepare(torch, device, model, build_schedule(model, 1),
+                      {"x": x, "wh": torch.from_numpy(wh).to(device), "wv": torch.from_numpy(wv).to(device)},
+                      {"x": (nx, "rand"), "wh": (wh.size, wh), "wv": (wv.size, wv)}, {"y": frames * Ho * Wo})
+        del x
+        hbytes = (nx + frames * H * Wo) * 4
+        vbytes = (frames * H * Wo + frames * Ho * Wo) * 4
+        self.units_per_step = (hbytes + vbytes) / 1e9
+        self.algorithmic = {"bytes_per_step": hbytes + vbytes, "h_bytes": hbytes, "v_bytes": vbytes,
+                            "per_unit": "each array element read once / written once per filter"}
+        self.workload = (f"downscaler {frames}x{H}x{W} fp32: hfilter 13->3 paving 8, then vfilter 14->4 paving 9 "
+                         f"(two repetitive tasks, unfused)")
+        self.l2 = "inputs (8.5 GB/rank) exceed the 126 MB L2"
+        self.dims = (frames, H, W, Wo, Ho)
+
+    def cpu_sample(self, seconds: float = 8.0):
+        from oracle import aol_oracle as orc
+        from oracle import c_oracle as co
+        _, H, W, Wo, Ho = self.dims
+        f = 2
+        th, tv = orc.hfilter_tilers(f, H, W), orc.vfilter_tilers(f, H, Wo)
+        x = np.random.default_rng(4).random(f * H * W, dtype=np.float32)
+        mid = np.zeros(f * H * Wo, np.float32)
+        y = np.zeros(f * Ho * Wo, np.float32)
+        t0 = time.perf_counter()
+        co.tile_filter(x, orc.hfilter_weights(), mid, th["x"], th["y"], 0, int(np.prod(th["x"]["rep"])))
+        co.tile_filter(mid, orc.vfilter_weights(), y, tv["x"], tv["y"], 0, int(np.prod(tv["x"]["rep"])))
+        dt = time.perf_counter() - t0
+        b = ((f * H * W + f * H * Wo) + (f * H * Wo + f * Ho * Wo)) * 4
+        return {"value": b / dt / 1e9, "unit": "GB/s", "cores": co.threads(), "kind": "port",
+                "sample": f"{f} frames through both filters, oracle/aol_oracle.c, {dt:.2f} s"}
+
+
+class SweepWorkload(Workload):
+    """Config C5: tile_copy sweep over pattern m, paving (dense / overlap / gaps), fitting and T.
+
+    step() runs the largest point; the per-point table is measured separately (measure_points)."""
+
+    name = "sweep"
+
+    POINTS_M = (1, 2, 4, 8, 16, 32, 64)
+
+    def __init__(self, torch, device, rank, world, max_out_bytes=8 << 30):
+        self.torch, self.device = torch, device
+        self.max_out = max_out_bytes
+        self.points = []
+        for m in self.POINTS_M:
+            for kind in ("dense", "overlap", "gaps", "strided"):
+                if kind in ("overlap", "strided") and m == 1:
+                    continue
+                for T in (10 ** 3, 10 ** 5, 10 ** 7, 10 ** 8, 10 ** 9):
+                    if T * m * 4 > self.max_out:
+                        continue
+                    self.points.append((m, kind, T))
+        big = [p for p in self.points if p[2] >= 10 ** 7]
+        self.main = max(big, key=lambda p: p[2] * p[0])
+        self.task = self._make(*self.main)
+        self.units_per_step = self.task["bytes"] / 1e9
+        self.algorithmic = {"bytes_per_launch": self.task["bytes"],
+                            "per_unit": "distinct input elements read + output elements written, x 4 B"}
+        self.workload = f"tile_copy sweep; step = pattern {self.main[0]} {self.main[1]} T={self.main[2]:.0e}"
+        self.l2 = "sweep points with T*m >= 1e7 exceed the L2"
+
+    def _make(self, m, kind, T):
+        from paper_1105_4424_b200 import Tiler, _capi
+        torch = self.torch
+        p = {"dense": m, "overlap": max(1, m // 2), "gaps": 2 * m, "strided": m * 2}[kind]
+        f = 2 if kind == "strided" else 1
+        span = (T - 1) * p + (m - 1) * f + 1
+        distinct = span if (kind == "overlap") else T * m
+        src = Tiler((0,), ((p,),), ((f,),), (m,)).bind((span,), (T,))
+        dst = Tiler((0,), ((m,),), ((1,),), (m,)).bind((T * m,), (T,))
+        x = torch.empty(span, device=self.device).uniform_()
+        y = torch.empty(T * m, device=self.device)
+        task = _capi.make_task("tile_copy", "float32", [src, dst])
+        ptrs = [x.data_ptr(), y.data_ptr()]
+        return {"x": x, "y": y, "task": task, "ptrs": ptrs, "T": T, "bytes": (distinct + T * m) * 4,
+                "plan": _capi.plan_name(task, 0, T, ptrs)}
+
+    def step(self):
+        from paper_1105_4424_b200 import _capi
+        t = self.task
+        _capi.launch(t["task"], 0, t["T"], t["ptrs"], (), int(self.torch.cuda.current_stream().cuda_stream))
+
+    def measure_points(self, steps=10, warmup=3):
+        torch = self.torch
+        rows = []
+        for m, kind, T in self.points:
+            t = self._make(m, kind, T)
+            from paper_1105_4424_b200 import _capi
+            st = int(torch.cuda.current_stream().cuda_stream)
+            for _ in range(warmup):
+                _capi.launch(t["task"], 0, T, t["ptrs"], (), st)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(steps):
+                _capi.launch(t["task"], 0, T, t["ptrs"], (), st)
+            e1.record()
+            e1.synchronize()
+            ms = e0.elapsed_time(e1) / steps
+            rows.append({"m": m, "paving": kind, "T": T, "plan": t["plan"], "ms": ms,
+                         "GBps": t["bytes"] / (ms * 1e-3) / 1e9})
+            del t
+            torch.cuda.empty_cache()
+        return rows
+
+    def e2e_setup(self):
+        torch = self.torch
+        t = self.task
+        self.hx = torch.empty(t["x"].numel()).uniform_().pin_memory()
+        self.hy = torch.empty(t["y"].numel()).pin_memory()
+        self.e2e_bytes = (self.hx.numel() * 4, self.hy.numel() * 4)
+
+    def e2e_step(self):
+        from paper_1105_4424_b200 import _capi
+        t = self.task
+        t["x"].copy_(self.hx, non_blocking=True)
+        _capi.launch(t["task"], 0, t["T"], t["ptrs"], (), int(self.torch.cuda.current_stream().cuda_stream))
+        self.hy.copy_(t["y"], non_blocking=True)
+        self.torch.cuda.current_stream().synchronize()
+
+    def e2e_free(self):
+        del self.hx, self.hy
+
+    def cpu_sample(self, seconds: float = 8.0):
+        from oracle import c_oracle as co
+        m, kind, T = self.main
+        p = {"dense": m, "overlap": max(1, m // 2), "gaps": 2 * m, "strided": m * 2}[kind]
+        f = 2 if kind == "strided" else 1
+        Ts = min(T, 2_000_000)
+        span = (Ts - 1) * p + (m - 1) * f + 1
+        ts = dict(array=(span,), rep=(Ts,), pattern=(m,), origin=(0,), paving=((p,),), fitting=((f,),))
+        td = dict(array=(Ts * m,), rep=(Ts,), pattern=(m,), origin=(0,), paving=((m,),), fitting=((1,),))
+        x = np.random.default_rng(0).random(span, dtype=np.float32)
+        y = np.zeros(Ts * m, np.float32)
+        t0 = time.perf_counter()
+        co.tile_copy(x, y, ts, td, 0, Ts)
+        dt = time.perf_counter() - t0
+        distinct = span if kind == "overlap" else Ts * m
+        return {"value": (distinct + Ts * m) * 4 / dt / 1e9, "unit": "GB/s", "cores": co.threads(), "kind": "port",
+                "sample": f"T={Ts} repetitions of the main point, oracle/aol_oracle.c tile_copy, {dt:.2f} s"}
+
+
+WORKLOADS = {"matmul": MatmulWorkload, "stencil": StencilWorkload, "downscaler": DownscalerWorkload,
+             "sweep": SweepWorkload}
 
 
 # ---------------------------------------------------------------- the arms --
@@ -355,14 +595,18 @@ def run_gpu(args):
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650",
                     "kernel_ms": kernel_ms, "algorithmic": wl.algorithmic}
         cpu = None if args.no_cpu else wl.cpu_sample(args.cpu_seconds)
+        extra = {}
+        if wl.name == "sweep" and not args.no_points:
+            extra["sweep_points"] = wl.measure_points()
         out = {
             "metric": METRIC, "value": value, "unit": wl.unit, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32" if wl.bound == "hbm" else "tf32 (fp32 in/out)",
             "data": "synthetic (torch.randn, seeded)",
-            "config": {"workload": wl.workload, "l2": "inputs (768 MiB/rank) exceed the 126 MB L2",
+            "config": {"workload": wl.workload, "l2": wl.l2,
                        "parallelism": f"repetition space sharded by contiguous blocks over {world} rank(s)"},
             "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "clocks": clk,
+            **extra,
         }
         print(json.dumps(out), flush=True)
     if world > 1:
@@ -420,6 +664,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-peak", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
+    ap.add_argument("--no-points", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         log("note: warmup < 3 is below the timing rules; using 3")

@@ -96,3 +96,36 @@ def tile_task_model(op: str, ports: dict[str, str], tilers: dict[str, Tiler], re
             allocs.append(f"allocate data p_{name} onto dev.gmem")
     allocs.append("allocate task t onto dev.cu")
     return single_task_model(op, tp, rp, conns, allocs, repeat=repeat, tilers=tilers)
+
+
+def chain_model(stages: list[tuple[str, str, dict[str, str], dict[str, Tiler], tuple]], root_in: dict[str, str],
+                root_out: dict[str, str], links: list[tuple[str, str]]) -> Model:
+    """Several repetitive tasks wired by connectors (one storage group per connected port set).
+
+    ``stages``: (part name, op, {port: "<dir> <dtype> [dims]"}, tilers, repeat);
+    ``root_in`` / ``root_out``: root port name -> spec; ``links``: (source, target)
+    endpoints in the reference connector syntax ("x", "h.x", "h.y" ...).  Every
+    root input and every task output is allocated onto dev.gmem and every task
+    onto dev.cu (the device-processor geometry of the reference harness).
+    """
+    A = ComponentKind.APPLICATION
+    comps = {}
+    parts = []
+    allocs = []
+    for part, op, ports, tilers, rep in stages:
+        tname = part.capitalize() + "T"
+        comps[tname] = Component(tname, A, ports=tuple(port(f"{n} {s}") for n, s in ports.items()),
+                                 repetition_space=Shape(tuple(rep)), elementary_op=op,
+                                 tilers=tuple(sorted(tilers.items())))
+        parts.append(PartInstance(part, tname))
+        for n, s in ports.items():
+            if s.split()[0] == "out":
+                allocs.append(AllocationLink(AllocKind.DATA, f"{part}.{n}", "dev.gmem"))
+        allocs.append(AllocationLink(AllocKind.TASK, part, "dev.cu"))
+    rports = tuple(port(f"{n} {s}") for n, s in {**root_in, **root_out}.items())
+    for n in root_in:
+        allocs.insert(0, AllocationLink(AllocKind.DATA, n, "dev.gmem"))
+    comps["m"] = Component("m", A, ports=rports, parts=tuple(parts),
+                           connectors=tuple(Connector(a, b) for a, b in links))
+    return Model(platform_components=platform(), application_components=comps, platform_root="p",
+                 application_root="m", allocations=tuple(allocs))

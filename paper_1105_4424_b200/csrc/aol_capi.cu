@@ -28,6 +28,7 @@ int launch_tile_copy(const aol_task& t, int64_t first, int64_t count, void* cons
 const char* tile_copy_plan_name(const aol_tiler& ts, const aol_tiler& td, int64_t first, int64_t count);
 int launch_matmul_generic(const aol_task& t, int64_t first, int64_t count, void* const* ports, cudaStream_t s);
 int launch_filter_generic(const aol_task& t, int64_t first, int64_t count, void* const* ports, cudaStream_t s);
+const char* filter_plan_name(const aol_task& t);
 int launch_tile_sum(const aol_task& t, int64_t first, int64_t count, void* const* ports, cudaStream_t s);
 int launch_identity(const aol_task& t, int64_t first, int64_t count, void* const* ports, const double* scalars,
                     cudaStream_t s);
@@ -81,7 +82,7 @@ static const char* plan_name(const aol_task* t, int64_t first, int64_t count, vo
     case AOL_OP_TILE_COPY: return tile_copy_plan_name(t->tilers[0], t->tilers[1], first, count);
     case AOL_OP_MATMUL:
       return (ports && gemm_tf32_applicable(*t, ports)) ? "matmul.tcgen05_tf32" : "matmul.generic_exact";
-    case AOL_OP_TILE_FILTER: return "tile_filter.generic";
+    case AOL_OP_TILE_FILTER: return filter_plan_name(*t);
     case AOL_OP_TILE_SUM: return "tile_sum.generic";
     default: return "identity";
   }

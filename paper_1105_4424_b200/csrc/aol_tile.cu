@@ -252,43 +252,137 @@ __global__ void k_matmul_generic(const T* __restrict__ a, const T* __restrict__ 
   }
 }
 
+// Raw (unreduced) base coordinates b_d = o_d + P_d . r for one repetition.
+__device__ __forceinline__ void tiler_base_raw(const DevTiler& t, int64_t rho, int64_t b[AOL_MAX_RANK]) {
+  int64_t r[AOL_MAX_RANK];
+  unravel(t, true, rho, r);
+#pragma unroll
+  for (int d = 0; d < AOL_MAX_RANK; ++d) {
+    b[d] = 0;
+    if (d >= t.a) continue;
+    int64_t e = t.o[d];
+#pragma unroll
+    for (int j = 0; j < AOL_MAX_RANK; ++j)
+      if (j < t.q) e += t.P[d][j] * r[j];
+    b[d] = e;
+  }
+}
+
+// Per-dimension extent of the pattern: raw offsets F_d . i lie in [lo_d, hi_d].
+struct PatSpan {
+  int64_t lo[AOL_MAX_RANK], hi[AOL_MAX_RANK];
+};
+
+__device__ __forceinline__ bool wrap_free(const DevTiler& t, const PatSpan& sp, const int64_t b[AOL_MAX_RANK],
+                                          int64_t& off) {
+  bool ok = true;
+  off = 0;
+#pragma unroll
+  for (int d = 0; d < AOL_MAX_RANK; ++d) {
+    if (d >= t.a) break;
+    ok = ok && (b[d] + sp.lo[d] >= 0) && (b[d] + sp.hi[d] < t.s[d]);
+    off += b[d] * t.st[d];
+  }
+  return ok;
+}
+
+// raw flat pattern offsets: foff[k] = sum_d (F_d . i_k) * st_d   (valid when the window does not wrap)
+__device__ __forceinline__ void fill_raw_offsets(const DevTiler& t, int64_t* foff, int64_t npat) {
+  for (int64_t k = threadIdx.x; k < npat; k += blockDim.x) {
+    int64_t i[AOL_MAX_RANK];
+    unravel(t, false, k, i);
+    int64_t o = 0;
+#pragma unroll
+    for (int d = 0; d < AOL_MAX_RANK; ++d) {
+      if (d >= t.a) break;
+      int64_t e = 0;
+#pragma unroll
+      for (int kk = 0; kk < AOL_MAX_RANK; ++kk)
+        if (kk < t.p) e += t.F[d][kk] * i[kk];
+      o += e * t.st[d];
+    }
+    foff[k] = o;
+  }
+}
+
 // Pattern linear map: y_pat[j] = sum_i w[j, i] * x_pat[i], i ascending, no FMA.
-// One thread per repetition; up to MAXO outputs accumulate while the pattern
-// streams once through registers.
-template <typename T, int MAXO>
+// One thread per repetition.  Fast path (window does not wrap): flat offsets
+// base + foff[i] with no modulo at all; the x window is read with float4 when
+// it is contiguous and 16-byte aligned (XVEC).  Wrapping windows take the
+// reduced-table path (one Euclidean mod per dimension per repetition).
+template <typename T, int MAXO, bool XVEC>
 __global__ void __launch_bounds__(256) k_filter_generic(const T* __restrict__ x, const T* __restrict__ w,
-                                                        T* __restrict__ y, DevTiler tx, DevTiler ty,
-                                                        int64_t first, int64_t count, int px, int py) {
+                                                        T* __restrict__ y, DevTiler tx, DevTiler ty, PatSpan sx,
+                                                        PatSpan sy, int64_t first, int64_t count, int px, int py,
+                                                        int64_t nx) {
   extern __shared__ int64_t smem[];
-  int64_t* fx = smem;
+  int64_t* fx = smem;                                   // reduced tables (wrap path)
   int64_t* fy = fx + (int64_t)px * tx.a;
-  T* ws = reinterpret_cast<T*>(fy + (int64_t)py * ty.a);
+  int64_t* ox = fy + (int64_t)py * ty.a;                // raw flat offsets (fast path)
+  int64_t* oy = ox + px;
+  T* ws = reinterpret_cast<T*>(oy + py);
   fill_table(tx, fx, px);
   fill_table(ty, fy, py);
+  fill_raw_offsets(tx, ox, px);
+  fill_raw_offsets(ty, oy, py);
   for (int k = threadIdx.x; k < px * py; k += blockDim.x) ws[k] = w[k];
   __syncthreads();
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t rho = first + e;
     int64_t bx[AOL_MAX_RANK], by[AOL_MAX_RANK];
-    tiler_base(tx, rho, bx);
-    tiler_base(ty, rho, by);
+    tiler_base_raw(tx, rho, bx);
+    tiler_base_raw(ty, rho, by);
+    int64_t xoff, yoff;
+    const bool xfree = wrap_free(tx, sx, bx, xoff);
+    const bool yfree = wrap_free(ty, sy, by, yoff);
+    if (!xfree) {
+#pragma unroll
+      for (int d = 0; d < AOL_MAX_RANK; ++d)
+        if (d < tx.a) bx[d] = emod(bx[d], tx.s[d]);
+    }
     T acc[MAXO];
 #pragma unroll
     for (int j = 0; j < MAXO; ++j) acc[j] = T(0);
-    for (int i = 0; i < px; ++i) {
-      const T xv = x[table_offset(tx, bx, fx, i)];
+    if (XVEC && xfree && (xoff & 3) == 0 && xoff + 16 <= nx) {
+      float xv[16];
 #pragma unroll
-      for (int j = 0; j < MAXO; ++j) {
-        if (j < py) {
-          if constexpr (sizeof(T) == 4) acc[j] = __fadd_rn(acc[j], __fmul_rn(ws[j * px + i], xv));
-          else acc[j] = __dadd_rn(acc[j], __dmul_rn(ws[j * px + i], xv));
+      for (int q = 0; q < 4; ++q) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(x) + (xoff >> 2) + q);
+        xv[4 * q] = v.x; xv[4 * q + 1] = v.y; xv[4 * q + 2] = v.z; xv[4 * q + 3] = v.w;
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        if (i < px) {
+#pragma unroll
+          for (int j = 0; j < MAXO; ++j)
+            if (j < py) acc[j] = __fadd_rn(acc[j], __fmul_rn(ws[j * px + i], xv[i]));
+        }
+      }
+    } else {
+      for (int i = 0; i < px; ++i) {
+        const T xv = xfree ? __ldg(x + xoff + ox[i]) : __ldg(x + table_offset(tx, bx, fx, i));
+#pragma unroll
+        for (int j = 0; j < MAXO; ++j) {
+          if (j < py) {
+            if constexpr (sizeof(T) == 4) acc[j] = __fadd_rn(acc[j], __fmul_rn(ws[j * px + i], xv));
+            else acc[j] = __dadd_rn(acc[j], __dmul_rn(ws[j * px + i], xv));
+          }
         }
       }
     }
+    if (yfree) {
 #pragma unroll
-    for (int j = 0; j < MAXO; ++j)
-      if (j < py) y[table_offset(ty, by, fy, j)] = acc[j];
+      for (int j = 0; j < MAXO; ++j)
+        if (j < py) y[yoff + oy[j]] = acc[j];
+    } else {
+#pragma unroll
+      for (int d = 0; d < AOL_MAX_RANK; ++d)
+        if (d < ty.a) by[d] = emod(by[d], ty.s[d]);
+#pragma unroll
+      for (int j = 0; j < MAXO; ++j)
+        if (j < py) y[table_offset(ty, by, fy, j)] = acc[j];
+    }
   }
 }
 
@@ -464,33 +558,79 @@ int launch_matmul_generic(const aol_task& t, int64_t first, int64_t count, void*
   return AOL_OK;
 }
 
-template <typename T, int MAXO>
-static int launch_filter_t(const DevTiler& tx, const DevTiler& ty, int64_t first, int64_t count, int px,
-                           int py, void* const* ports, cudaStream_t stream) {
-  const size_t smem = ((size_t)px * tx.a + (size_t)py * ty.a) * sizeof(int64_t) + (size_t)px * py * sizeof(T);
-  auto kern = k_filter_generic<T, MAXO>;
-  if (smem > 48 * 1024) AOL_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<grid_for(count, 256, 16), 256, smem, stream>>>((const T*)ports[0], (const T*)ports[1], (T*)ports[2],
-                                                        tx, ty, first, count, px, py);
+static PatSpan pattern_span(const aol_tiler& t) {
+  PatSpan sp;
+  memset(&sp, 0, sizeof(sp));
+  for (int d = 0; d < t.arr_rank; ++d)
+    for (int k = 0; k < t.pat_rank; ++k) {
+      const int64_t v = t.fitting[d][k] * (t.pattern[k] - 1);
+      sp.lo[d] += std::min<int64_t>(0, v);
+      sp.hi[d] += std::max<int64_t>(0, v);
+    }
+  return sp;
+}
+
+// x pattern is a contiguous run: raw offsets foff[i] == i (1-D along the last dim, unit fitting)
+static bool contiguous_pattern(const aol_tiler& t) {
+  int64_t st[AOL_MAX_RANK], acc = 1;
+  for (int d = t.arr_rank - 1; d >= 0; --d) { st[d] = acc; acc *= t.array[d]; }
+  int64_t expect = 1;
+  for (int k = t.pat_rank - 1; k >= 0; --k) {
+    if (t.pattern[k] == 1) continue;
+    int64_t c = 0;
+    for (int d = 0; d < t.arr_rank; ++d) c += t.fitting[d][k] * st[d];
+    if (c != expect) return false;
+    expect *= t.pattern[k];
+  }
+  return true;
+}
+
+template <typename T, int MAXO, bool XVEC>
+static int launch_filter_t(const aol_task& t, const DevTiler& tx, const DevTiler& ty, int64_t first, int64_t count,
+                           int px, int py, void* const* ports, cudaStream_t stream) {
+  const size_t smem = ((size_t)px * tx.a + (size_t)py * ty.a + px + py) * sizeof(int64_t) +
+                      (size_t)px * py * sizeof(T);
+  auto kern = k_filter_generic<T, MAXO, XVEC>;
+  if (smem > 48 * 1024)
+    AOL_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t nx = tiler_arr_total(t.tilers[0]);
+  kern<<<grid_for(count, 256, 16), 256, smem, stream>>>((const T*)ports[0], (const T*)ports[1], (T*)ports[2], tx,
+                                                        ty, pattern_span(t.tilers[0]), pattern_span(t.tilers[1]),
+                                                        first, count, px, py, nx);
   AOL_LAUNCH_CHECK("k_filter_generic");
   return AOL_OK;
 }
 
+bool stencil_box_applicable(const aol_task& t, int& KH, int& KW);
+int launch_stencil_box(const aol_task& t, int64_t first, int64_t count, void* const* ports, cudaStream_t s);
+
+const char* filter_plan_name(const aol_task& t) {
+  int kh, kw;
+  if (stencil_box_applicable(t, kh, kw)) return "tile_filter.stencil_box";
+  const int64_t px = tiler_pat_total(t.tilers[0]), py = tiler_pat_total(t.tilers[1]);
+  if (t.dtype == AOL_F32 && px <= 16 && py <= 4 && contiguous_pattern(t.tilers[0])) return "tile_filter.window_vec";
+  return "tile_filter.generic";
+}
+
 int launch_filter_generic(const aol_task& t, int64_t first, int64_t count, void* const* ports,
                           cudaStream_t stream) {
+  int kh, kw;
+  if (stencil_box_applicable(t, kh, kw)) return launch_stencil_box(t, first, count, ports, stream);
   DevTiler tx, ty;
   int rc;
   if ((rc = make_dev_tiler(t.tilers[0], tx)) || (rc = make_dev_tiler(t.tilers[1], ty))) return rc;
   const int64_t px = tiler_pat_total(t.tilers[0]), py = tiler_pat_total(t.tilers[1]);
-  if (px * tx.a + py * ty.a > kTableMax * 4 || px * py > 16384)
+  if (px * tx.a + py * ty.a + px + py > kTableMax * 4 || px * py > 16384)
     return fail(AOL_EUNSUPPORTED, "tile_filter pattern too large (px*py <= 16384)");
   if (py > 16) return fail(AOL_EUNSUPPORTED, "tile_filter supports at most 16 outputs per pattern");
   const bool f32 = t.dtype == AOL_F32;
+  if (f32 && px <= 16 && py <= 4 && contiguous_pattern(t.tilers[0]))
+    return launch_filter_t<float, 4, true>(t, tx, ty, first, count, (int)px, (int)py, ports, stream);
   if (py <= 4)
-    return f32 ? launch_filter_t<float, 4>(tx, ty, first, count, px, py, ports, stream)
-               : launch_filter_t<double, 4>(tx, ty, first, count, px, py, ports, stream);
-  return f32 ? launch_filter_t<float, 16>(tx, ty, first, count, px, py, ports, stream)
-             : launch_filter_t<double, 16>(tx, ty, first, count, px, py, ports, stream);
+    return f32 ? launch_filter_t<float, 4, false>(t, tx, ty, first, count, (int)px, (int)py, ports, stream)
+               : launch_filter_t<double, 4, false>(t, tx, ty, first, count, (int)px, (int)py, ports, stream);
+  return f32 ? launch_filter_t<float, 16, false>(t, tx, ty, first, count, (int)px, (int)py, ports, stream)
+             : launch_filter_t<double, 16, false>(t, tx, ty, first, count, (int)px, (int)py, ports, stream);
 }
 
 int launch_tile_sum(const aol_task& t, int64_t first, int64_t count, void* const* ports, cudaStream_t stream) {
