@@ -193,7 +193,7 @@ class Workload:
     def e2e_setup(self):
         torch = self.torch
         gen = torch.Generator().manual_seed(7)
-        self.hin = {k: (torch.rand(n, generator=gen) if kind == "rand" else torch.from_numpy(kind)).pin_memory()
+        self.hin = {k: (torch.rand(n, generator=gen) if isinstance(kind, str) else torch.from_numpy(kind)).pin_memory()
                     for k, (n, kind) in self.host_specs.items()}
         self.hout = {k: torch.empty(n).pin_memory() for k, n in self.out_sizes.items()}
         self.e2e_bytes = (sum(t.numel() * 4 for t in self.hin.values()),

@@ -41,35 +41,35 @@ __global__ void __launch_bounds__(ST_TX* ST_TY) k_stencil_box(const float* __res
   for (int i = 0; i < ST_RPT; ++i)
 #pragma unroll
     for (int j = 0; j < ST_CPT; ++j) acc[i][j] = 0.0f;
+  // load the whole (ST_RPT + KH - 1) x (ST_CPT + 2) input block first: every load is
+  // independent, so a thread keeps ~3*(ST_RPT+KH-1) requests in flight
+  float v[ST_RPT + KH - 1][ST_CPT + 2];
 #pragma unroll
   for (int rr = 0; rr < ST_RPT + KH - 1; ++rr) {
-    const int row = (int)(((int64_t)r0 + orow + rr) % H);
+    int row = r0 + orow + rr;
+    if (row >= H) row -= H;
+    if (row >= H) row %= H;
     const float* xr = x + (int64_t)row * W;
-    float v[ST_CPT + 2];
-    v[0] = __ldg(xr + cl);
+    v[rr][0] = __ldg(xr + cl);
     if (vec) {
       const float4 q = __ldg(reinterpret_cast<const float4*>(xr + cin));
-      v[1] = q.x; v[2] = q.y; v[3] = q.z; v[4] = q.w;
+      v[rr][1] = q.x; v[rr][2] = q.y; v[rr][3] = q.z; v[rr][4] = q.w;
     } else {
 #pragma unroll
-      for (int j = 0; j < ST_CPT; ++j) v[1 + j] = __ldg(xr + (cin + j) % W);
+      for (int j = 0; j < ST_CPT; ++j) v[rr][1 + j] = __ldg(xr + (cin + j) % W);
     }
-    v[ST_CPT + 1] = __ldg(xr + cr);
-    // this input row contributes tap-row di = rr - i to output row i
+    v[rr][ST_CPT + 1] = __ldg(xr + cr);
+  }
 #pragma unroll
-    for (int i = 0; i < ST_RPT; ++i) {
-      const int di = rr - i;
-      if (di < 0 || di >= KH) continue;
+  for (int i = 0; i < ST_RPT; ++i)
 #pragma unroll
-      for (int j = 0; j < ST_CPT; ++j) {
+    for (int di = 0; di < KH; ++di)
+#pragma unroll
+      for (int j = 0; j < ST_CPT; ++j)
 #pragma unroll
         for (int dj = 0; dj < KW; ++dj)
-          acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(ws[di * KW + dj], v[j + dj]));
-      }
-    }
-  }
-  // NB: accumulation order per output is di-major, dj-minor because rr increases
-  // monotonically and, for a fixed output row i, di = rr - i increases with rr.
+          acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(ws[di * KW + dj], v[i + di][j + dj]));
+  // accumulation order per output: di-major, dj-minor = the pattern's row-major order
 #pragma unroll
   for (int i = 0; i < ST_RPT; ++i) {
     const int r = r0 + i;

@@ -603,10 +603,20 @@ static int launch_filter_t(const aol_task& t, const DevTiler& tx, const DevTiler
 
 bool stencil_box_applicable(const aol_task& t, int& KH, int& KW);
 int launch_stencil_box(const aol_task& t, int64_t first, int64_t count, void* const* ports, cudaStream_t s);
+struct LineGeom;
+bool line_filter_geometry(const aol_task& t, LineGeom& g);
+const char* line_filter_variant(const LineGeom& g);
+int launch_line_filter(const aol_task& t, const LineGeom& g, int64_t first, int64_t count, void* const* ports,
+                       cudaStream_t s);
+// opaque storage for a LineGeom (defined in aol_linefilter.cu)
+struct alignas(16) LineGeomBuf { unsigned char b[256]; };
 
 const char* filter_plan_name(const aol_task& t) {
   int kh, kw;
   if (stencil_box_applicable(t, kh, kw)) return "tile_filter.stencil_box";
+  LineGeomBuf gb;
+  if (line_filter_geometry(t, *reinterpret_cast<LineGeom*>(&gb)))
+    return line_filter_variant(*reinterpret_cast<LineGeom*>(&gb));
   const int64_t px = tiler_pat_total(t.tilers[0]), py = tiler_pat_total(t.tilers[1]);
   if (t.dtype == AOL_F32 && px <= 16 && py <= 4 && contiguous_pattern(t.tilers[0])) return "tile_filter.window_vec";
   return "tile_filter.generic";
@@ -616,6 +626,9 @@ int launch_filter_generic(const aol_task& t, int64_t first, int64_t count, void*
                           cudaStream_t stream) {
   int kh, kw;
   if (stencil_box_applicable(t, kh, kw)) return launch_stencil_box(t, first, count, ports, stream);
+  LineGeomBuf gb;
+  if (line_filter_geometry(t, *reinterpret_cast<LineGeom*>(&gb)))
+    return launch_line_filter(t, *reinterpret_cast<LineGeom*>(&gb), first, count, ports, stream);
   DevTiler tx, ty;
   int rc;
   if ((rc = make_dev_tiler(t.tilers[0], tx)) || (rc = make_dev_tiler(t.tilers[1], ty))) return rc;

@@ -326,3 +326,63 @@ def test_missing_library_fails_loudly(tmp_path, monkeypatch):
             _capi.load(tmp_path / "nope.so")
     finally:
         _capi._lib = saved
+
+
+def _filter_case(op, t, w, x, devices):
+    ny = int(np.prod(t["y"]["array"]))
+    R = int(np.prod(t["x"]["rep"]))
+    ports = {"x": _spec(t["x"], "in", "float32"), "w": f"in float32 [{w.size}]",
+             "y": _spec(t["y"], "out", "float32")}
+    res = _run_tile(op, t, ports, {"x": x, "w": w}, devices)
+    ref = orc.run_tile_task(op, t, {"x": x, "w": w}, {"y": (ny, np.float32)}, R, devices)["y"]
+    return res.outputs["p_y"], ref
+
+
+def _plan(op_tilers, dtype="float32"):
+    from paper_1105_4424_b200 import _capi
+    bts = [_tiler(d).bind(d["array"], d["rep"]) for d in op_tilers]
+    return _capi.plan_name(_capi.make_task("tile_filter", dtype, bts), 0, bts[0].rep_total)
+
+
+@pytest.mark.parametrize("H,W,origin,kh,devices", [
+    (256, 512, None, 3, 1), (256, 512, None, 3, 3), (130, 260, (0, 0), 3, 2), (64, 128, (5, 7), 3, 5),
+    (96, 64, None, 5, 4), (33, 44, (32, 43), 3, 1)])
+def test_stencil_box_kernel_vs_oracle(H, W, origin, kh, devices):
+    t = orc.stencil_tilers(H, W)
+    if origin is not None:
+        t["x"] = dict(t["x"], origin=origin)
+    if kh == 5:
+        t["x"] = dict(t["x"], pattern=(5, 3), origin=(H - 2, W - 1))
+        w = np.arange(1, 16, dtype=np.float32) / 64
+    else:
+        w = orc.stencil_weights()
+    assert _plan([t["x"], t["y"]]) == "tile_filter.stencil_box"
+    x = np.random.default_rng(H + W).standard_normal(H * W).astype(np.float32)
+    got, ref = _filter_case("stencil", t, w, x, devices)
+    assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
+
+
+@pytest.mark.parametrize("kind,dims,devices", [
+    ("h", (2, 5, 384), 1), ("h", (3, 7, 96), 3), ("v", (2, 45, 64), 1), ("v", (3, 27, 40), 4),
+    ("h_shift", (2, 3, 128), 2), ("v_generic", (2, 40, 24), 3)])
+def test_line_filter_kernel_vs_oracle(kind, dims, devices):
+    F, H, W = dims
+    if kind.startswith("h"):
+        t = orc.hfilter_tilers(F, H, W)
+        w = orc.hfilter_weights()
+        if kind == "h_shift":
+            t["x"] = dict(t["x"], origin=(0, 0, W - 2))       # window starts 2 left: wraps at the row start
+        expect = "tile_filter.line_13x3"
+    else:
+        if kind == "v_generic":
+            t = orc.vfilter_tilers(F, H, W, taps=6, step=4, outs=2)
+            w = orc.vfilter_weights(6, 2)
+            expect = "tile_filter.line"
+        else:
+            t = orc.vfilter_tilers(F, H, W)
+            w = orc.vfilter_weights()
+            expect = "tile_filter.line_14x4"
+    assert _plan([t["x"], t["y"]]) == expect
+    x = np.random.default_rng(F * H * W).random(int(np.prod(t["x"]["array"]))).astype(np.float32)
+    got, ref = _filter_case("tile_filter", t, w, x, devices)
+    assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
