@@ -1,0 +1,253 @@
+"""Multi-GPU execution: one process per GPU, contiguous repetition shards, no data-path collective.
+
+The reference simulates D devices in one process: launch d covers
+``partition_equally(T, D)[d]`` (partition.py:105-121, refexec.py:488) and
+devices share nothing except host-ordered dot reductions (refexec.py:5-7,
+:478-487).  Here device d *is* rank d of a ``torch.distributed`` group:
+
+  * rank r executes only the KernelLaunch whose ``device_index == r``;
+  * an output array that a later step (or the caller) needs whole is made
+    whole by exchanging each rank's **packed output-pattern stream**: the
+    rank gathers its own patterns in rho order through the output tiler
+    (a ``tile_copy`` into a dense [count, P] buffer), the streams are
+    all-gathered (NCCL over NVLink on GPUs, gloo on CPU), and every rank
+    scatters the other ranks' streams back through the same tiler.  No
+    indices travel, and unequal shard sizes (differing by one repetition)
+    need no padding in the payload;
+  * dot_partial partials are all-gathered and summed in ascending device
+    order, exactly the reference's combine.
+
+The pack / unpack / launch primitives are injected, so the same exchange
+logic is exercised on CPU (gloo, world size 2, with the oracle as the
+launcher) in tests/test_distributed.py and on B200 with libaolb200.so.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable
+
+from .partition import WorkRange, partition_equally
+from .tiler import BoundTiler
+
+
+@dataclass(frozen=True)
+class Shard:
+    rank: int
+    world: int
+    ranges: tuple[WorkRange, ...]
+
+    @property
+    def mine(self) -> WorkRange | None:
+        return self.ranges[self.rank] if self.rank < len(self.ranges) else None
+
+
+def shard(total: int, rank: int, world: int) -> Shard:
+    """Rank ``rank``'s contiguous block of a repetition space of ``total`` points."""
+    return Shard(rank, world, tuple(partition_equally(total, world)))
+
+
+def input_hull(bt: BoundTiler, first: int, count: int) -> tuple[int, int]:
+    """[lo, hi) flat-offset range of the array that repetitions [first, first+count) read.
+
+    Exact bounding range for non-wrapping tilers (each repetition row of the
+    covered box is affine); the whole array for toroidal tilers.  A rank
+    needs only this slice of the input resident.
+    """
+    if count <= 0:
+        return (0, 0)
+    aff = bt.affine
+    if aff is None:
+        return (0, bt.array_total)
+    c0, rc, pc = aff
+    # unravel first/last repetition; the covered set lies inside the box spanned by the
+    # outermost differing coordinate (full extent for inner dims)
+    import numpy as np
+    r_lo = np.unravel_index(first, bt.rep)
+    r_hi = np.unravel_index(first + count - 1, bt.rep)
+    lo_box, hi_box = [], []
+    differ = False
+    for j, ext in enumerate(bt.rep):
+        if differ:
+            lo_box.append(0)
+            hi_box.append(ext - 1)
+        else:
+            lo_box.append(int(r_lo[j]))
+            hi_box.append(int(r_hi[j]))
+            if r_lo[j] != r_hi[j]:
+                differ = True
+    lo = c0
+    hi = c0
+    for c, a, b in zip(rc, lo_box, hi_box):
+        lo += min(c * a, c * b)
+        hi += max(c * a, c * b)
+    for c, ext in zip(pc, bt.tiler.pattern):
+        lo += min(0, c * (ext - 1))
+        hi += max(0, c * (ext - 1))
+    return (int(lo), int(hi) + 1)
+
+
+class Exchange:
+    """Variable-size all-gather of packed pattern streams over a torch.distributed group."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def all_gather_v(self, local, counts: list[int]):
+        """``local`` is this rank's flat stream (counts[rank] elements); returns every rank's stream."""
+        import torch
+        n = max(counts)
+        buf = torch.zeros(n, dtype=local.dtype, device=local.device)
+        buf[:local.numel()] = local
+        out = [torch.empty(n, dtype=local.dtype, device=local.device) for _ in range(self.world)]
+        self.dist.all_gather(out, buf, group=self.group)
+        return [o[:c] for o, c in zip(out, counts)]
+
+    def all_gather_scalars(self, value: float) -> list[float]:
+        import torch
+        dev = "cuda" if self.dist.get_backend(self.group) == "nccl" else "cpu"
+        t = torch.tensor([value], dtype=torch.float64, device=dev)
+        out = [torch.empty(1, dtype=torch.float64, device=dev) for _ in range(self.world)]
+        self.dist.all_gather(out, t, group=self.group)
+        return [float(o.item()) for o in out]
+
+
+def gather_output(array, bt: BoundTiler, sh: Shard, ex: Exchange,
+                  pack: Callable, unpack: Callable) -> None:
+    """Make ``array`` (written by this rank on its shard) whole on every rank.
+
+    ``pack(array, bt, first, count) -> flat stream`` and
+    ``unpack(array, bt, first, count, stream)`` move patterns through the
+    output tiler in rho order (tile_copy kernels on GPU, the oracle on CPU).
+    """
+    P = bt.pattern_total
+    counts = [r.count * P for r in sh.ranges] + [0] * (sh.world - len(sh.ranges))
+    mine = sh.mine
+    local = pack(array, bt, mine.offset, mine.count) if mine else None
+    if local is None:
+        import torch
+        local = torch.zeros(0, dtype=array.dtype, device=array.device)
+    streams = ex.all_gather_v(local, counts)
+    for r, rng in enumerate(sh.ranges):
+        if r != sh.rank:
+            unpack(array, bt, rng.offset, rng.count, streams[r])
+
+
+def combine_partials(ex: Exchange, partial: float) -> float:
+    """dot_partial combine: partials summed in ascending device order (refexec.py:483-486)."""
+    total = 0.0
+    for p in ex.all_gather_scalars(partial):
+        total += p
+    return total
+
+
+# -- CUDA pack / unpack through libaolb200 tile_copy -----------------------------
+
+def cuda_pack(array, bt: BoundTiler, first: int, count: int):
+    """Gather this rank's output patterns (rho order) into a dense stream with one tile_copy launch."""
+    import torch
+    from . import _capi
+    from .tiler import Tiler
+    P = bt.pattern_total
+    out = torch.empty(count * P, dtype=array.dtype, device=array.device)
+    # dense side indexed by (rho - first): origin -first*P on a [count*P] array would wrap, so
+    # address the dense buffer as a window [first*P, ...) of a virtual array of R*P elements
+    R = bt.rep_total
+    dense = Tiler((0,), (tuple(int(__import__("numpy").prod(bt.rep[j + 1:])) * P for j in range(len(bt.rep))),),
+                  ((1,),), (P,)).bind((R * P,), bt.rep)
+    task = _capi.make_task("tile_copy", str(array.dtype).replace("torch.", ""), [bt, dense])
+    base = out.data_ptr() - first * P * out.element_size()
+    _capi.launch(task, first, count, [array.data_ptr(), base], (),
+                 int(torch.cuda.current_stream(array.device).cuda_stream))
+    return out
+
+
+def cuda_unpack(array, bt: BoundTiler, first: int, count: int, stream) -> None:
+    """Scatter another rank's dense pattern stream back through the output tiler."""
+    import numpy as np
+    import torch
+    from . import _capi
+    from .tiler import Tiler
+    P = bt.pattern_total
+    R = bt.rep_total
+    dense = Tiler((0,), (tuple(int(np.prod(bt.rep[j + 1:])) * P for j in range(len(bt.rep))),),
+                  ((1,),), (P,)).bind((R * P,), bt.rep)
+    task = _capi.make_task("tile_copy", str(array.dtype).replace("torch.", ""), [dense, bt])
+    base = stream.data_ptr() - first * P * stream.element_size()
+    _capi.launch(task, first, count, [base, array.data_ptr()], (),
+                 int(torch.cuda.current_stream(array.device).cuda_stream))
+
+
+# -- distributed drop-in ----------------------------------------------------------
+
+def _written_ports(task) -> list[str]:
+    return [ps.name for ps in task.spec.ports if ps.direction in ("out", "inout") and task.comp.port(ps.name)]
+
+
+def _port_tiler(ex, task, name: str) -> BoundTiler:
+    """Output tiler of a port: the task's tiler for tile ops, the identity tiler for reference ops."""
+    from .model import enum_value
+    from .tiler import Tiler
+    tl = dict(getattr(task.comp, "tilers", ()) or ())
+    tl.update(ex.tilers.get(task.path, {}) or {})
+    port = task.comp.port(name)
+    rep = task.comp.repetition_space.dims if task.comp.repetition_space is not None else (1,)
+    if name in tl:
+        return tl[name].bind(port.shape.dims, rep)
+    n = port.shape.total
+    T = 1
+    for d in rep:
+        T *= int(d)
+    if T == n:
+        return Tiler((0,), ((1,),), ((0,),), (1,)).bind((n,), (T,))
+    # repetition total 1 with a longer vector: only element 0 is touched (refexec probe)
+    return Tiler((0,), ((0,),), ((0,),), (1,)).bind((n,), (T,))
+
+
+def make_distributed_executor(model, schedule, bindings: dict, *, group=None, **kw):
+    """Executor for rank ``dist.get_rank(group)`` of a schedule built with device_count == world size."""
+    from .executor import Executor, _capi
+
+    class DistributedExecutor(Executor):
+        def __init__(self):
+            import torch.distributed as dist
+            self.xch = Exchange(group)
+            super().__init__(model, schedule, bindings, self.xch.world, **kw)
+            self.rank, self.world = self.xch.rank, self.xch.world
+
+        def run_device(self, step) -> None:
+            import torch
+            t = self.task(step.task_path)
+            if len(step.launches) > self.world:
+                raise ValueError(f"step '{step.task_path}' has {len(step.launches)} launches for "
+                                 f"{self.world} ranks: build the schedule with device_count == world size")
+            s = self._stream_handle()
+            arrays = {name: self.storage.array(node) for name, node in t.nodes.items()}
+            mine = [l for l in step.launches if l.device_index == self.rank]
+            if step.op == "dot_partial":
+                part = 0.0
+                if mine:
+                    buf = torch.zeros(1, dtype=arrays["a"].dtype, device=self.device)
+                    l = mine[0]
+                    _capi.launch(t.ctask, l.range.offset, l.range.count,
+                                 [arrays["a"].data_ptr(), arrays["b"].data_ptr(), buf.data_ptr()], (), s)
+                    part = float(buf.double().item())
+                arrays["s"][0] = combine_partials(self.xch, part)
+                return
+            scalars = [float(arrays[n][0].item()) for n in t.scalar_ports]
+            ptrs = [arrays[name].data_ptr() for name in t.port_order]
+            for l in mine:
+                _capi.launch(t.ctask, l.range.offset, l.range.count, ptrs, scalars, s)
+            total = sum(l.range.count for l in step.launches)
+            sh = Shard(self.rank, self.world, tuple(l.range for l in step.launches))
+            for name in _written_ports(t):
+                bt = _port_tiler(self, t, name)
+                if bt.rep_total != total:
+                    continue
+                gather_output(arrays[name], bt, sh, self.xch, cuda_pack, cuda_unpack)
+
+    return DistributedExecutor()

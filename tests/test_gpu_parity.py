@@ -386,3 +386,65 @@ def test_line_filter_kernel_vs_oracle(kind, dims, devices):
     x = np.random.default_rng(F * H * W).random(int(np.prod(t["x"]["array"]))).astype(np.float32)
     got, ref = _filter_case("tile_filter", t, w, x, devices)
     assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
+
+
+@pytest.mark.parametrize("name", ["copy_box_torus", "hfilter_2x4x64", "matmul_small_d3", "stencil_32x48"])
+def test_cuda_pack_unpack_roundtrip(golden, name):
+    """The multi-GPU exchange primitives: pack a shard's output patterns, unpack them elsewhere."""
+    from paper_1105_4424_b200.distributed import cuda_pack, cuda_unpack, shard
+    _, meta = golden
+    tl = meta[name]["tilers"]
+    d = tl["dst"] if "dst" in tl else (tl["c"] if "c" in tl else tl["y"])
+    bt = _tiler(d).bind(d["array"], d["rep"])
+    n = bt.array_total
+    src = torch.arange(1, n + 1, dtype=torch.float32, device="cuda")
+    for D in (2, 3):
+        for r in shard(bt.rep_total, 0, D).ranges:
+            stream = cuda_pack(src, bt, r.offset, r.count)
+            offs = orc.tiler_offsets(d, r.offset, r.count).ravel()
+            assert np.array_equal(stream.cpu().numpy(), src.cpu().numpy()[offs])
+            dst = torch.zeros(n, dtype=torch.float32, device="cuda")
+            cuda_unpack(dst, bt, r.offset, r.count, stream)
+            want = np.zeros(n, np.float32)
+            want[offs] = src.cpu().numpy()[offs]
+            assert np.array_equal(dst.cpu().numpy(), want)
+
+
+def test_distributed_executor_world1_nccl():
+    """The rank-local executor (world size 1 over NCCL) runs the two-stage downscaler chain like the plain one."""
+    import os
+    import torch.distributed as dist
+    from paper_1105_4424_b200 import builders
+    from paper_1105_4424_b200.distributed import make_distributed_executor
+    from paper_1105_4424_b200.executor import execute_schedule
+    from paper_1105_4424_b200.partition import build_schedule
+    th = orc.hfilter_tilers(2, 18, 64)
+    tv = orc.vfilter_tilers(2, 18, 24)
+    wh, wv = orc.hfilter_weights(), orc.vfilter_weights()
+    spec = lambda d, io: _spec(d, io, "float32")   # noqa: E731
+    model = builders.chain_model(
+        [("h", "hfilter", {"x": spec(th["x"], "in"), "w": f"in float32 [{wh.size}]", "y": spec(th["y"], "out")},
+          {k: _tiler(v) for k, v in th.items()}, th["x"]["rep"]),
+         ("v", "vfilter", {"x": spec(tv["x"], "in"), "w": f"in float32 [{wv.size}]", "y": spec(tv["y"], "out")},
+          {k: _tiler(v) for k, v in tv.items()}, tv["x"]["rep"])],
+        {"x": spec(th["x"], "in"), "wh": f"in float32 [{wh.size}]", "wv": f"in float32 [{wv.size}]"},
+        {"y": spec(tv["y"], "out")},
+        [("x", "h.x"), ("wh", "h.w"), ("h.y", "v.x"), ("wv", "v.w"), ("v.y", "y")])
+    x = np.random.default_rng(8).random(2 * 18 * 64).astype(np.float32)
+    bind = {"x": x, "wh": wh, "wv": wv}
+    ref = execute_schedule(model, build_schedule(model, 1), bind, 1).outputs["y"]
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29571")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        ex = make_distributed_executor(model, build_schedule(model, 1), bind)
+        ex.run()
+        got = ex.outputs()["y"]
+    finally:
+        dist.destroy_process_group()
+    assert np.array_equal(got, ref)
+    mid = orc.run_tile_task("hfilter", th, {"x": x, "w": wh}, {"y": (2 * 18 * 24, np.float32)},
+                            int(np.prod(th["x"]["rep"])), 1)["y"]
+    want = orc.run_tile_task("vfilter", tv, {"x": mid, "w": wv}, {"y": (2 * 8 * 24, np.float32)},
+                             int(np.prod(tv["x"]["rep"])), 1)["y"]
+    assert np.array_equal(got, want)
