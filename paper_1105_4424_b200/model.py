@@ -343,3 +343,54 @@ def task_component(model, task_path: str):
         part = comp.part(seg)
         comp = comps[part.type_ref]
     return comp
+
+
+# -- JSON round trip (lets models built by the reference front-end travel without the DSL) ----
+
+def model_to_dict(model) -> dict:
+    """Plain-data form of a (mirror or reference) Model; inverse of :func:`model_from_dict`."""
+    def shape(s):
+        return None if s is None else [int(d) for d in s.dims]
+
+    def comp(c):
+        st = c.stereotype
+        return {
+            "name": c.name, "kind": enum_value(c.kind),
+            "ports": [[p.name, enum_value(p.direction), shape(p.shape), enum_value(p.data_type)] for p in c.ports],
+            "parts": [[p.name, p.type_ref, shape(p.shaped)] for p in c.parts],
+            "connectors": [[k.source, k.target] for k in c.connectors],
+            "stereotype": None if st is None else [enum_value(st.kind), enum_value(st.memory_role),
+                                                   st.capacity_bytes, st.frequency_mhz],
+            "repetition_space": shape(c.repetition_space),
+            "elementary_op": c.elementary_op,
+            "until": None if c.until is None else [c.until.port, c.until.tolerance],
+        }
+    return {
+        "platform_components": [comp(c) for c in model.platform_components.values()],
+        "application_components": [comp(c) for c in model.application_components.values()],
+        "platform_root": model.platform_root, "application_root": model.application_root,
+        "allocations": [[enum_value(a.kind), a.source_path, a.target_path] for a in model.allocations],
+    }
+
+
+def model_from_dict(d: dict) -> Model:
+    def shape(v):
+        return None if v is None else Shape(tuple(int(x) for x in v))
+
+    def comp(c):
+        st = c["stereotype"]
+        return Component(
+            name=c["name"], kind=ComponentKind(c["kind"]),
+            ports=tuple(FlowPort(n, Direction(di), shape(s), DataType(t)) for n, di, s, t in c["ports"]),
+            parts=tuple(PartInstance(n, t, shape(s)) for n, t, s in c["parts"]),
+            connectors=tuple(Connector(a, b) for a, b in c["connectors"]),
+            stereotype=None if st is None else HwStereotype(StereotypeKind(st[0]),
+                                                            None if st[1] is None else MemoryRole(st[1]),
+                                                            st[2], st[3]),
+            repetition_space=shape(c["repetition_space"]), elementary_op=c["elementary_op"],
+            until=None if c["until"] is None else UntilCondition(c["until"][0], float(c["until"][1])))
+    return Model(
+        platform_components={c["name"]: comp(c) for c in d["platform_components"]},
+        application_components={c["name"]: comp(c) for c in d["application_components"]},
+        platform_root=d["platform_root"], application_root=d["application_root"],
+        allocations=tuple(AllocationLink(AllocKind(k), s, t) for k, s, t in d["allocations"]))

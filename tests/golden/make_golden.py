@@ -289,9 +289,30 @@ def make_identity_cases(store, meta):
         meta[key] = dict(op="spmv_csr", dtype="float64", devices=d, n=A.n)
 
 
+def make_cg_case(store, meta):
+    """The paper's case study: CG on poisson_2d(20) through the unmodified executor at D = 1, 2, 4."""
+    from gmodelc.refexec import instantiate_for_matrix
+    from paper_1105_4424_b200.model import model_to_dict
+    model = gmodelc.parse_model(gmodelc.bundled_model_text())
+    A = poisson_2d(20)
+    sized = instantiate_for_matrix(model, A.n, A.nnz)
+    assert gmodelc.validate_conformance(sized) == []
+    b = np.ones(A.n)
+    bind = {"rowptr": A.row_ptr, "colidx": A.col_idx, "values": A.values, "b": b}
+    for k, v in bind.items():
+        store[f"cg_k20/{k}"] = v
+    meta["cg_k20"] = {"op": "cg", "model": model_to_dict(sized), "runs": {}}
+    for d in (1, 2, 4):
+        res = execute_schedule(sized, build_schedule(sized, d), dict(bind), d)
+        store[f"cg_k20/x_d{d}"] = res.outputs["x"]
+        meta["cg_k20"]["runs"][str(d)] = {"iterations": res.iterations, "final_relres": res.final_relres,
+                                          "converged": res.converged}
+
+
 def main():
     store: dict[str, np.ndarray] = {}
     meta: dict[str, dict] = {}
+    make_cg_case(store, meta)
     for i, (name, (ts, td)) in enumerate(COPY_CASES.items()):
         meta[name] = make_copy_case(name, ts, td, (1, 3, 5)[i % 3], store)
 

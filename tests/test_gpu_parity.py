@@ -448,3 +448,23 @@ def test_distributed_executor_world1_nccl():
     want = orc.run_tile_task("vfilter", tv, {"x": mid, "w": wv}, {"y": (2 * 8 * 24, np.float32)},
                              int(np.prod(tv["x"]["rep"])), 1)["y"]
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("devices", [1, 2, 4])
+def test_cg_case_study_through_the_drop_in(golden, devices):
+    """The paper's case study (CG on poisson_2d(20), the bundled cg.gmodel resized by the reference)
+    through execute_schedule on the B200: same iteration count as the reference executor at every D,
+    solution within 1e-10 (the reference's own cross-D criterion, tests/test_refexec.py:237-247)."""
+    from paper_1105_4424_b200.executor import execute_schedule
+    from paper_1105_4424_b200.model import model_from_dict
+    from paper_1105_4424_b200.partition import build_schedule
+    data, meta = golden
+    m = meta["cg_k20"]
+    model = model_from_dict(m["model"])
+    bind = {k: data[f"cg_k20/{k}"] for k in ("rowptr", "colidx", "values", "b")}
+    res = execute_schedule(model, build_schedule(model, devices), bind, devices)
+    ref = m["runs"][str(devices)]
+    assert res.iterations == ref["iterations"] and res.converged
+    x_ref = data[f"cg_k20/x_d{devices}"]
+    assert np.max(np.abs(res.outputs["x"] - x_ref)) / np.max(np.abs(x_ref)) <= 1e-10
+    assert abs(res.final_relres - ref["final_relres"]) <= 1e-3 * ref["final_relres"]

@@ -212,3 +212,13 @@ def test_registry_has_reference_and_tile_ops():
     for op in ("spmv_csr", "dot_partial", "axpy", "scale", "copy", "sub", "div", "neg", "rel_residual",
                "tile_copy", "matmul", "tile_filter", "hfilter", "vfilter", "stencil", "tile_sum"):
         assert op in INTRINSICS
+
+
+def test_model_json_roundtrip(golden):
+    from paper_1105_4424_b200.model import model_from_dict, model_to_dict
+    _, meta = golden
+    d = meta["cg_k20"]["model"]
+    m = model_from_dict(d)
+    assert model_to_dict(m) == d
+    s = build_schedule(m, 4)
+    assert len(s.steps) == 4 and hasattr(s.steps[-1], "body") and len(s.steps[-1].body) == 12
