@@ -95,7 +95,7 @@ bool line_filter_geometry(const aol_task& t, LineGeom& g) {
   return true;
 }
 
-template <int PX, int PY>
+template <int PX, int PY, typename IDX>
 __global__ void __launch_bounds__(256) k_line_filter(const float* __restrict__ x, const float* __restrict__ w,
                                                      float* __restrict__ y, LineGeom g, int64_t first,
                                                      int64_t count) {
@@ -106,45 +106,59 @@ __global__ void __launch_bounds__(256) k_line_filter(const float* __restrict__ x
   __shared__ float ws[32 * 8];
   for (int k = threadIdx.x; k < px * py; k += blockDim.x) ws[k] = w[k];
   __syncthreads();
+  const IDX inner = (IDX)g.inner;
+  const IDX SxI = (IDX)(g.Sx * g.inner), SyI = (IDX)(g.Sy * g.inner);
+  const IDX Sx = (IDX)g.Sx;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t rho = first + e;
-    int64_t i, l, o;
+    IDX i, l, o;
     if (g.small) {
       uint32_t q, r, q2, r2;
       g.div_inner.divmod((uint32_t)rho, q, r);
       g.div_nl.divmod(q, q2, r2);
-      i = r; l = r2; o = q2;
+      i = (IDX)r; l = (IDX)r2; o = (IDX)q2;
     } else {
-      i = rho % g.inner;
+      i = (IDX)(rho % g.inner);
       const int64_t q = rho / g.inner;
-      l = q % g.NL;
-      o = q / g.NL;
+      l = (IDX)(q % g.NL);
+      o = (IDX)(q / g.NL);
     }
-    int64_t row = l * g.sx + g.ox;
-    if (row >= g.Sx) row %= g.Sx;
-    const float* xb = x + o * g.Sx * g.inner + i;
+    IDX row = l * (IDX)g.sx + (IDX)g.ox;
+    if (row >= Sx) row %= Sx;
+    const float* xb = x + (o * SxI + i);
     float xv[MAXP];
-    if (g.inner == 1 && row + 16 <= g.Sx && MAXP <= 16 && (((uintptr_t)(xb + row)) & 15) == 0) {
-      const float4* p = reinterpret_cast<const float4*>(xb + row);
+    if (row + (IDX)px <= Sx) {                       // window does not wrap
+      if (g.inner == 1 && MAXP <= 16 && row + 16 <= Sx && ((((uintptr_t)(xb + row)) & 15) == 0)) {
+        const float4* p = reinterpret_cast<const float4*>(xb + row);
 #pragma unroll
-      for (int q = 0; q < (MAXP + 3) / 4; ++q) {
-        const float4 v = __ldg(p + q);
-        if (4 * q < MAXP) xv[4 * q] = v.x;
-        if (4 * q + 1 < MAXP) xv[4 * q + 1] = v.y;
-        if (4 * q + 2 < MAXP) xv[4 * q + 2] = v.z;
-        if (4 * q + 3 < MAXP) xv[4 * q + 3] = v.w;
+        for (int q = 0; q < (MAXP + 3) / 4; ++q) {
+          const float4 v = __ldg(p + q);
+          if (4 * q < MAXP) xv[4 * q] = v.x;
+          if (4 * q + 1 < MAXP) xv[4 * q + 1] = v.y;
+          if (4 * q + 2 < MAXP) xv[4 * q + 2] = v.z;
+          if (4 * q + 3 < MAXP) xv[4 * q + 3] = v.w;
+        }
+      } else {
+        const float* xp = xb + row * inner;
+#pragma unroll
+        for (int t = 0; t < MAXP; ++t) {
+          if (t < px) {
+            xv[t] = __ldg(xp);
+            xp += inner;
+          }
+        }
       }
-    } else {
+    } else {                                          // wraps around the line: rare
 #pragma unroll
       for (int t = 0; t < MAXP; ++t) {
         if (t < px) {
-          xv[t] = __ldg(xb + row * g.inner);
-          if (++row == g.Sx) row = 0;
+          xv[t] = __ldg(xb + row * inner);
+          if (++row == Sx) row = 0;
         }
       }
     }
-    float* yb = y + o * g.Sy * g.inner + (l * g.sy + g.oy) * g.inner + i;
+    float* yp = y + (o * SyI + (l * (IDX)g.sy + (IDX)g.oy) * inner + i);
 #pragma unroll
     for (int j = 0; j < MAXO; ++j) {
       if (j < py) {
@@ -152,7 +166,8 @@ __global__ void __launch_bounds__(256) k_line_filter(const float* __restrict__ x
 #pragma unroll
         for (int t = 0; t < MAXP; ++t)
           if (t < px) acc = __fadd_rn(acc, __fmul_rn(ws[j * px + t], xv[t]));
-        yb[j * g.inner] = acc;
+        *yp = acc;
+        yp += inner;
       }
     }
   }
@@ -172,12 +187,18 @@ int launch_line_filter(const aol_task& t, const LineGeom& g, int64_t first, int6
   const float* w = static_cast<const float*>(ports[1]);
   float* y = static_cast<float*>(ports[2]);
   const unsigned grid = grid_for(count, 256, 8);
-  if (g.px == 13 && g.py == 3)
-    k_line_filter<13, 3><<<grid, 256, 0, s>>>(x, w, y, g, first, count);
-  else if (g.px == 14 && g.py == 4)
-    k_line_filter<14, 4><<<grid, 256, 0, s>>>(x, w, y, g, first, count);
-  else
-    k_line_filter<0, 0><<<grid, 256, 0, s>>>(x, w, y, g, first, count);
+  // 32-bit offsets whenever both arrays fit (every in-range offset < 2^32)
+  const bool idx32 = g.outer * g.Sx * g.inner < (1ll << 32) && g.outer * g.Sy * g.inner < (1ll << 32);
+  if (idx32) {
+    if (g.px == 13 && g.py == 3)
+      k_line_filter<13, 3, uint32_t><<<grid, 256, 0, s>>>(x, w, y, g, first, count);
+    else if (g.px == 14 && g.py == 4)
+      k_line_filter<14, 4, uint32_t><<<grid, 256, 0, s>>>(x, w, y, g, first, count);
+    else
+      k_line_filter<0, 0, uint32_t><<<grid, 256, 0, s>>>(x, w, y, g, first, count);
+  } else {
+    k_line_filter<0, 0, int64_t><<<grid, 256, 0, s>>>(x, w, y, g, first, count);
+  }
   AOL_LAUNCH_CHECK("k_line_filter");
   (void)t;
   return AOL_OK;

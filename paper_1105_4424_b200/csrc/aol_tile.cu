@@ -194,6 +194,55 @@ __global__ void __launch_bounds__(256) k_tile_copy_affine(const T* __restrict__ 
   }
 }
 
+// Affine copy, V consecutive pattern elements per thread (P % V == 0, destination
+// contiguous within a pattern and V-aligned).  The source is read as one V-vector
+// when the pattern is contiguous (SRC_VEC), else as V strided scalars.
+template <typename T> struct Vec2;
+template <> struct Vec2<uint32_t> { using t2 = uint2; using t4 = uint4; };
+template <> struct Vec2<uint64_t> { using t2 = ulonglong2; using t4 = ulonglong2; };
+
+template <typename T, int V, bool SRC_VEC>
+__global__ void __launch_bounds__(256) k_tile_copy_vec(const T* __restrict__ src, T* __restrict__ dst, int64_t cs,
+                                                       int64_t As, int64_t Bs, int64_t cd, int64_t Ad,
+                                                       int64_t first, int64_t ngroups, FastDiv32 pdiv) {
+  using V2 = typename Vec2<T>::t2;
+  using V4 = typename Vec2<T>::t4;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ngroups;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t q, r;
+    pdiv.divmod((uint32_t)(g * V), q, r);
+    const int64_t rho = first + q;
+    const int64_t so = cs + As * rho + Bs * (int64_t)r;
+    const int64_t doff = cd + Ad * rho + (int64_t)r;
+    T v[V];
+    if (SRC_VEC) {
+      if constexpr (V == 4 && sizeof(T) == 4) {
+        const V4 t = __ldg(reinterpret_cast<const V4*>(src + so));
+        v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+      } else if constexpr (V == 2) {
+        const V2 t = __ldg(reinterpret_cast<const V2*>(src + so));
+        v[0] = t.x; v[1] = t.y;
+      } else {
+#pragma unroll
+        for (int u = 0; u < V; ++u) v[u] = __ldg(src + so + u);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < V; ++u) v[u] = __ldg(src + so + Bs * u);
+    }
+    if constexpr (V == 4 && sizeof(T) == 4) {
+      V4 t; t.x = v[0]; t.y = v[1]; t.z = v[2]; t.w = v[3];
+      *reinterpret_cast<V4*>(dst + doff) = t;
+    } else if constexpr (V == 2) {
+      V2 t; t.x = v[0]; t.y = v[1];
+      *reinterpret_cast<V2*>(dst + doff) = t;
+    } else {
+#pragma unroll
+      for (int u = 0; u < V; ++u) dst[doff + u] = v[u];
+    }
+  }
+}
+
 // Contiguous on both sides: a streaming copy with 16-byte vectors.
 __global__ void __launch_bounds__(256) k_stream_copy16(const uint4* __restrict__ src, uint4* __restrict__ dst,
                                                        int64_t n16) {
@@ -445,8 +494,10 @@ static bool collapse(const int64_t* coef, const int64_t* dims, int n, int64_t& s
 }
 
 struct CopyPlan {
-  int kind;  // 0 generic, 1 affine1, 2 stream
+  int kind;  // 0 generic, 1 affine1, 2 stream, 3 vector (V elements / thread)
   int64_t cs, As, Bs, cd, Ad, Bd;
+  int V;
+  bool src_vec;
 };
 
 static CopyPlan plan_tile_copy(const aol_tiler& ts, const aol_tiler& td, int64_t first, int64_t count) {
@@ -464,13 +515,31 @@ static CopyPlan plan_tile_copy(const aol_tiler& ts, const aol_tiler& td, int64_t
   p.cd = d.c0; p.Ad = Ad; p.Bd = P > 1 ? Bd : 0;
   const bool src_dense = (P == 1 || p.Bs == 1) && p.As == P;
   const bool dst_dense = (P == 1 || p.Bd == 1) && p.Ad == P;
-  if (src_dense && dst_dense) p.kind = 2;
+  if (src_dense && dst_dense) {
+    p.kind = 2;
+    return p;
+  }
+  // vector path: destination contiguous within the pattern, V | P, V-aligned offsets
+  // prefer the widest V that also vectorises the source; else the widest store-only V
+  for (int pass = 0; pass < 2 && p.kind != 3; ++pass) {
+    for (int V = 4; V >= 2; V /= 2) {
+      if (P % V || (P > 1 && p.Bd != 1) || p.cd % V || p.Ad % V) continue;
+      const bool sv = (P == 1 || p.Bs == 1) && p.cs % V == 0 && p.As % V == 0;
+      if (pass == 0 && !sv) continue;
+      p.V = V;
+      p.src_vec = sv;
+      p.kind = 3;
+      break;
+    }
+  }
   (void)first;
   return p;
 }
 
 const char* tile_copy_plan_name(const aol_tiler& ts, const aol_tiler& td, int64_t first, int64_t count) {
-  switch (plan_tile_copy(ts, td, first, count).kind) {
+  const CopyPlan pl = plan_tile_copy(ts, td, first, count);
+  switch (pl.kind) {
+    case 3: return pl.src_vec ? "tile_copy.vec" : "tile_copy.vec_store";
     case 2: return "tile_copy.stream16";
     case 1: return "tile_copy.affine";
     default: return "tile_copy.generic";
@@ -508,6 +577,25 @@ static int launch_tile_copy_t(const aol_tiler& ts, const aol_tiler& td, int64_t 
         k_stream_copy_tail<T><<<1, 256, 0, stream>>>(s0 + done, d0 + done, n - done);
         AOL_LAUNCH_CHECK("k_stream_copy_tail");
       }
+      return AOL_OK;
+    }
+    p.kind = 1;
+  }
+  if (p.kind == 3) {
+    int V = p.V;
+    if (sizeof(T) == 8 && V > 2) V = 2;                 // 16-byte vectors
+    const uintptr_t sa = (uintptr_t)s, da = (uintptr_t)d;
+    const size_t vb = (size_t)V * sizeof(T);
+    if (da % vb == 0 && (!p.src_vec || sa % vb == 0)) {
+      const int64_t groups = count * P / V;
+      const unsigned grid = grid_for(groups, 1024, 16);
+      const FastDiv32 pd((uint32_t)P);
+#define AOL_VEC_LAUNCH(VV, SV)                                                                               \
+  k_tile_copy_vec<T, VV, SV><<<grid, 256, 0, stream>>>(s, d, p.cs, p.As, p.Bs, p.cd, p.Ad, first, groups, pd)
+      if (V == 4) { if (p.src_vec) AOL_VEC_LAUNCH(4, true); else AOL_VEC_LAUNCH(4, false); }
+      else { if (p.src_vec) AOL_VEC_LAUNCH(2, true); else AOL_VEC_LAUNCH(2, false); }
+#undef AOL_VEC_LAUNCH
+      AOL_LAUNCH_CHECK("k_tile_copy_vec");
       return AOL_OK;
     }
     p.kind = 1;

@@ -138,6 +138,10 @@ def test_tiler_offsets_random_vs_loop_oracle():
     ((8192,), (1000,), (3,), ((8,),), ((2,),), (5,)),           # gaps + strided fitting -> affine
     ((1000,), (999,), (7,), ((1,),), ((1,),), (17,)),           # wraps -> generic
     ((64, 48), (48, 64), (1,), ((0, 1), (1, 0)), ((0,), (0,)), (0, 0)),   # transpose
+    ((16384,), (1000,), (8,), ((16,),), ((1,),), (4,)),         # gaps -> vec (V=4 loads)
+    ((4096,), (1023,), (4,), ((2,),), ((1,),), (2,)),           # overlap -> vec (V=2 loads)
+    ((8192,), (1000,), (4,), ((8,),), ((2,),), (0,)),           # strided fitting -> vec_store
+    ((8192,), (999,), (6,), ((7,),), ((1,),), (1,)),            # odd stride -> vec (V=2) or affine
 ])
 @pytest.mark.parametrize("devices", [1, 3])
 @pytest.mark.parametrize("dtype", ["float32", "float64"])

@@ -56,7 +56,13 @@ def test_validate_and_plan_without_gpu():
     assert _capi.plan_name(t, 0, 25) == "tile_copy.stream16"
     ov = dict(cp, rep=(49,), paving=((2,),))
     dst = dict(array=(196,), rep=(49,), pattern=(4,), origin=(0,), paving=((4,),), fitting=((1,),))
-    assert _capi.plan_name(_capi.make_task("tile_copy", "float32", [_bt(ov), _bt(dst)]), 0, 49) == "tile_copy.affine"
+    assert _capi.plan_name(_capi.make_task("tile_copy", "float32", [_bt(ov), _bt(dst)]), 0, 49) == "tile_copy.vec"
+    st = dict(cp, rep=(24,), paving=((4,),), fitting=((2,),))
+    dst2 = dict(dst, array=(96,), rep=(24,))
+    assert _capi.plan_name(_capi.make_task("tile_copy", "float32", [_bt(st), _bt(dst2)]), 0, 24) == "tile_copy.vec_store"
+    od = dict(cp, array=(75,), rep=(25,), pattern=(3,), paving=((3,),), fitting=((1,),))
+    odd = dict(od, origin=(0,), array=(80,), paving=((3,),), fitting=((1,),))
+    assert _capi.plan_name(_capi.make_task("tile_copy", "float32", [_bt(dict(od, paving=((2,),), array=(60,))), _bt(odd)]), 0, 25) == "tile_copy.affine"
     wr = dict(cp, origin=(99,))
     assert _capi.plan_name(_capi.make_task("tile_copy", "float32", [_bt(wr), _bt(cp)]), 0, 25) == "tile_copy.generic"
     mism = dict(cp, pattern=(2,), array=(50,), paving=((2,),))
