@@ -18,8 +18,10 @@ the launches:
 
 Keyword-only additions: ``tilers`` (task path -> port -> Tiler, for
 reference models whose Component has no tiler field), ``precision`` for
-the matmul elementary task, ``device_outputs`` to keep results in HBM, and
-``stream``.  There is no CPU fallback: a missing library raises.
+the matmul elementary task, ``device_outputs`` to keep results in HBM,
+``out`` (caller-owned host buffers), ``pipeline`` (chunked H2D / compute /
+D2H overlap for one-step schedules bound to host memory) and ``stream``.
+There is no CPU fallback: a missing library raises.
 """
 
 from __future__ import annotations
@@ -37,6 +39,12 @@ from .model import connected_port_groups, enum_value, iter_app_instances, task_c
 
 class MissingBinding(KeyError):
     pass
+
+
+def partition_equally_local(total: int, parts: int) -> list[tuple[int, int]]:
+    """(offset, count) sub-chunks of [0, total) — the partition.py:105-121 rule, reused for pipelining."""
+    from .partition import partition_equally
+    return [(r.offset, r.count) for r in partition_equally(total, parts)] if total > 0 else []
 
 
 @dataclass
@@ -67,8 +75,11 @@ def torch_dtype(name: str):
 class DeviceStorage:
     """Arrays per connected-port group, resident on one CUDA device (refexec.py:375-412)."""
 
-    def __init__(self, model, bindings: dict, device, stream=None):
+    def __init__(self, model, bindings: dict, device, stream=None, defer: bool = False):
+        """``defer``: allocate device arrays for host bindings but do not copy them; the
+        streamed path uploads each chunk's input hull itself (``self.host`` keeps the sources)."""
         torch = _torch()
+        self.host: dict = {}
         self.groups = connected_port_groups(model)
         self.ports = {}
         for path, comp in iter_app_instances(model):
@@ -91,7 +102,11 @@ class DeviceStorage:
                                          f"port expects {port.shape.total}")
                 if flat.device.type != "cuda":
                     self.h2d_bytes += flat.numel() * flat.element_size()
-                t = flat.to(device=device, dtype=torch_dtype(dt), copy=True, non_blocking=True)
+                if defer and flat.device.type != "cuda" and flat.dtype == torch_dtype(dt):
+                    self.host[self.groups[port.name]] = flat
+                    t = torch.empty(flat.numel(), dtype=flat.dtype, device=device)
+                else:
+                    t = flat.to(device=device, dtype=torch_dtype(dt), copy=True, non_blocking=True)
             else:
                 arr = np.asarray(data).ravel()
                 if arr.size != port.shape.total:
@@ -99,7 +114,11 @@ class DeviceStorage:
                                          f"port expects {port.shape.total}")
                 arr = np.ascontiguousarray(arr.astype(dt, copy=False))
                 self.h2d_bytes += arr.nbytes
-                t = torch.from_numpy(arr).to(device=device, copy=True)
+                if defer:
+                    self.host[self.groups[port.name]] = torch.from_numpy(arr)
+                    t = torch.empty(arr.size, dtype=torch_dtype(dt), device=device)
+                else:
+                    t = torch.from_numpy(arr).to(device=device, copy=True)
             self.arrays[self.groups[port.name]] = t
         for node, port in self.ports.items():
             g = self.groups[node]
@@ -161,7 +180,7 @@ class Executor:
     """Prepared schedule: storage resident in HBM, tasks validated, ready to run repeatedly."""
 
     def __init__(self, model, schedule, bindings: dict, device_count: int, *, tilers: dict | None = None,
-                 precision: str = "default", device=None, stream=None):
+                 precision: str = "default", device=None, stream=None, pipeline: int = 0):
         torch = _torch()
         _capi.load()
         if not torch.cuda.is_available():
@@ -172,8 +191,10 @@ class Executor:
         self.tilers = tilers or {}
         self.precision = precision
         self.stream = stream
+        steps = [st for st in schedule.steps]
+        self.pipeline = pipeline if (pipeline > 1 and len(steps) == 1 and hasattr(steps[0], "launches")) else 0
         with torch.cuda.device(self.device):
-            self.storage = DeviceStorage(model, bindings, self.device, stream)
+            self.storage = DeviceStorage(model, bindings, self.device, stream, defer=bool(self.pipeline))
         self._tasks: dict[str, _Task] = {}
         self._dot_buf = None
         self.iterations = 0
@@ -228,6 +249,117 @@ class Executor:
         ptrs = [arrays[name].data_ptr() for name in t.port_order]
         for l in step.launches:
             _capi.launch(t.ctask, l.range.offset, l.range.count, ptrs, scalars, s)
+
+    # -- streamed execution from host memory -----------------------------------
+    def _port_bound(self, t: _Task, name: str):
+        from .distributed import _port_tiler
+        return _port_tiler(self, t, name)
+
+    def run_streamed(self, out: dict | None = None) -> dict:
+        """Run a one-step schedule chunk by chunk straight from host memory.
+
+        Each launch range is split into ``pipeline`` contiguous chunks.  For
+        chunk c: the part of every input's hull (distributed.input_hull) not
+        yet resident is copied H2D on a copy stream; the chunk launches on the
+        compute stream once its inputs landed; its output hull is copied D2H
+        on a third stream.  PCIe upload, tensor-core compute and download of
+        consecutive chunks overlap.  Returns the root outputs (host).
+        """
+        from .distributed import input_hull
+        torch = _torch()
+        step = self.schedule.steps[0]
+        t = self.task(step.task_path)
+        comp = torch.cuda.current_stream(self.device) if self.stream is None else self.stream
+        cin = torch.cuda.Stream(self.device)
+        cout = torch.cuda.Stream(self.device)
+        st = self.storage
+        arrays = {name: st.array(node) for name, node in t.nodes.items()}
+        in_ports = [ps.name for ps in t.spec.ports if enum_value(ps.direction) in ("in", "inout")
+                    and t.comp.port(ps.name) and st.groups[t.nodes[ps.name]] in st.host]
+        out_ports = [ps.name for ps in t.spec.ports if enum_value(ps.direction) in ("out", "inout")
+                     and t.comp.port(ps.name)]
+        # whole-array inputs (filter coefficients, scalars) go up first; tiled / identity
+        # vector inputs stream chunk by chunk through their hulls
+        whole = [n for n in in_ports if (t.spec.tile and not t.spec.port_spec(n).tiled)
+                 or t.spec.port_spec(n).scalar]
+        in_ports = [n for n in in_ports if n not in whole]
+        bound = {n: self._port_bound(t, n) for n in in_ports + out_ports}
+        uploaded = {n: [0, 0] for n in in_ports}
+        root = self.model.application_components[self.model.application_root]
+        root_out = {p.name: st.array(p.name) for p in root.ports if enum_value(p.direction) == "out"}
+        hosts = {}
+        for name, dev in root_out.items():
+            if out is not None and name in out:
+                h = out[name]
+                hosts[name] = torch.from_numpy(h) if isinstance(h, np.ndarray) else h.view(-1)
+            else:
+                hosts[name] = torch.empty(dev.numel(), dtype=dev.dtype, pin_memory=True)
+        out_group = {n: st.groups[t.nodes[n]] for n in out_ports}
+        root_of = {st.groups[n]: n for n in root_out}
+        covered = {n: [] for n in out_ports}
+        ptrs = [arrays[name].data_ptr() for name in t.port_order]
+        with torch.cuda.stream(cin):
+            for n in whole:
+                arrays[n].copy_(st.host[st.groups[t.nodes[n]]], non_blocking=True)
+        comp.wait_stream(cin)
+        scal = []
+        for n in t.scalar_ports:
+            g = st.groups[t.nodes[n]]
+            scal.append(float(st.host[g][0]) if g in st.host else float(arrays[n][0].item()))
+        chunks = []
+        for l in step.launches:
+            for r in partition_equally_local(l.range.count, self.pipeline):
+                chunks.append((l.range.offset + r[0], r[1]))
+
+        def upload(name, lo, hi):
+            g = st.groups[t.nodes[name]]
+            if hi > lo:
+                arrays[name][lo:hi].copy_(st.host[g][lo:hi], non_blocking=True)
+
+        for first, count in chunks:
+            with torch.cuda.stream(cin):
+                for n in in_ports:
+                    lo, hi = input_hull(bound[n], first, count) if n in bound else (0, arrays[n].numel())
+                    u = uploaded[n]
+                    if u[1] == u[0]:
+                        upload(n, lo, hi)
+                        u[0], u[1] = lo, hi
+                    else:
+                        if lo < u[0]:
+                            upload(n, lo, u[0])
+                            u[0] = lo
+                        if hi > u[1]:
+                            upload(n, u[1], hi)
+                            u[1] = hi
+                ev_in = torch.cuda.Event()
+                ev_in.record(cin)
+            comp.wait_event(ev_in)
+            _capi.launch(t.ctask, first, count, ptrs, scal, int(comp.cuda_stream))
+            ev_done = torch.cuda.Event()
+            ev_done.record(comp)
+            cout.wait_event(ev_done)
+            with torch.cuda.stream(cout):
+                for n in out_ports:
+                    rn = root_of.get(out_group[n])
+                    if rn is None:
+                        continue
+                    lo, hi = input_hull(bound[n], first, count)
+                    hosts[rn][lo:hi].copy_(root_out[rn][lo:hi], non_blocking=True)
+                    covered[n].append((lo, hi))
+        # elements no chunk wrote keep the zero initialisation (refexec.py:399-403)
+        with torch.cuda.stream(cout):
+            for n in out_ports:
+                rn = root_of.get(out_group[n])
+                if rn is None:
+                    continue
+                pos = 0
+                for lo, hi in sorted(covered[n]) + [(root_out[rn].numel(), root_out[rn].numel())]:
+                    if lo > pos:
+                        hosts[rn][pos:lo].copy_(root_out[rn][pos:lo], non_blocking=True)
+                    pos = max(pos, hi)
+        cout.synchronize()
+        comp.synchronize()
+        return {n: (out[n] if out is not None and n in out else h.numpy()) for n, h in hosts.items()}
 
     def run_steps(self, steps, tol=None, max_iter=None) -> None:
         for step in steps:
@@ -291,11 +423,16 @@ class Executor:
 def execute_schedule(model, schedule, bindings: dict, device_count: int, tol: float | None = None,
                      max_iter: int | None = None, *, tilers: dict | None = None, precision: str = "default",
                      device_outputs: bool = False, out: dict | None = None, device=None,
-                     stream=None) -> ExecutionResult:
+                     stream=None, pipeline: int = 0) -> ExecutionResult:
     """Interpret ``schedule`` on the B200 with ``device_count`` launch shards per device step."""
     ex = Executor(model, schedule, bindings, device_count, tilers=tilers, precision=precision,
-                  device=device, stream=stream)
-    ex.run(tol, max_iter)
-    outs = ex.outputs(on_device=device_outputs, out=out)
+                  device=device, stream=stream, pipeline=0 if device_outputs else pipeline)
+    if ex.pipeline:
+        torch = _torch()
+        with torch.cuda.device(ex.device):
+            outs = ex.run_streamed(out)
+    else:
+        ex.run(tol, max_iter)
+        outs = ex.outputs(on_device=device_outputs, out=out)
     return ExecutionResult(outputs=outs, iterations=ex.iterations, final_relres=ex.final_relres,
                            converged=ex.converged)

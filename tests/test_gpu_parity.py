@@ -472,3 +472,46 @@ def test_cg_case_study_through_the_drop_in(golden, devices):
     x_ref = data[f"cg_k20/x_d{devices}"]
     assert np.max(np.abs(res.outputs["x"] - x_ref)) / np.max(np.abs(x_ref)) <= 1e-10
     assert abs(res.final_relres - ref["final_relres"]) <= 1e-3 * ref["final_relres"]
+
+
+@pytest.mark.parametrize("case", ["matmul", "stencil", "hfilter", "copy_gaps", "axpy"])
+@pytest.mark.parametrize("chunks", [2, 7])
+def test_streamed_execution_equals_plain(case, chunks):
+    """pipeline=k (chunked H2D / launch / D2H on three streams) returns exactly the plain result."""
+    from paper_1105_4424_b200 import builders
+    from paper_1105_4424_b200.executor import execute_schedule
+    from paper_1105_4424_b200.partition import build_schedule
+    rng = np.random.default_rng(chunks)
+    if case == "matmul":
+        M, N, K = 300, 264, 96
+        t = orc.gemm_tilers(M, N, K)
+        ports = {"a": f"in float32 [{M},{K}]", "b": f"in float32 [{K},{N}]", "c": f"out float32 [{M},{N}]"}
+        bind = {"p_a": rng.standard_normal(M * K).astype(np.float32),
+                "p_b": rng.standard_normal(K * N).astype(np.float32)}
+        model = builders.tile_task_model("matmul", ports, {k: _tiler(v) for k, v in t.items()}, (M, N))
+    elif case in ("stencil", "hfilter"):
+        t = orc.stencil_tilers(64, 96) if case == "stencil" else orc.hfilter_tilers(3, 5, 128)
+        w = orc.stencil_weights() if case == "stencil" else orc.hfilter_weights()
+        ports = {"x": _spec(t["x"], "in", "float32"), "w": f"in float32 [{w.size}]",
+                 "y": _spec(t["y"], "out", "float32")}
+        bind = {"p_x": rng.random(int(np.prod(t["x"]["array"]))).astype(np.float32), "p_w": w}
+        model = builders.tile_task_model(case, ports, {k: _tiler(v) for k, v in t.items()}, t["x"]["rep"])
+    elif case == "copy_gaps":
+        t = {"src": dict(array=(4000,), rep=(300,), pattern=(4,), origin=(3,), paving=((12,),), fitting=((1,),)),
+             "dst": dict(array=(2000,), rep=(300,), pattern=(4,), origin=(0,), paving=((6,),), fitting=((1,),))}
+        ports = {"src": "in float32 [4000]", "dst": "out float32 [2000]"}
+        bind = {"p_src": rng.random(4000).astype(np.float32)}
+        model = builders.tile_task_model("tile_copy", ports, {k: _tiler(v) for k, v in t.items()}, (300,))
+    else:
+        model = builders.single_task_model(
+            "axpy", ["y inout float64 [999]", "x in float64 [999]", "a in float64 [1]"],
+            ["i in float64 [999]", "v in float64 [999]", "s in float64 [1]", "o out float64 [999]"],
+            ["i -> t.y", "v -> t.x", "s -> t.a", "t.y -> o"],
+            ["allocate data i onto dev.gmem", "allocate data v onto dev.gmem", "allocate data s onto host.ram",
+             "allocate task t onto dev.cu"], 999)
+        bind = {"i": rng.standard_normal(999), "v": rng.standard_normal(999), "s": np.array([0.75])}
+    sched = build_schedule(model, 3)
+    plain = execute_schedule(model, sched, bind, 3).outputs
+    streamed = execute_schedule(model, sched, bind, 3, pipeline=chunks).outputs
+    for k in plain:
+        assert np.array_equal(plain[k], streamed[k]), k
