@@ -129,3 +129,35 @@ def chain_model(stages: list[tuple[str, str, dict[str, str], dict[str, Tiler], t
                            connectors=tuple(Connector(a, b) for a, b in links))
     return Model(platform_components=platform(), application_components=comps, platform_root="p",
                  application_root="m", allocations=tuple(allocs))
+
+
+def b200_platform(n_sm: int = 148, lanes: int = 128, smem_bytes: int = 227 * 1024,
+                  hbm_bytes: int = 183_359 * 1024 * 1024, cmem_bytes: int = 64 * 1024) -> dict:
+    """A MARTE platform model of one B200, in the reference's vocabulary.
+
+    host (cpu + hostRam) | gpu.sm : Sm shaped [148] with lane : Lane shaped [128] (the PE
+    multiplicity that derive_launch_config reads as the work-group size, partition.py:124-154),
+    a deviceLocal shared memory of 227 KB per SM and a devicePrivate register file; gpu.hbm
+    (deviceGlobal, 180 GB) and gpu.cmem (deviceConstant, 64 KB).
+    """
+    P = ComponentKind.PLATFORM
+    return {
+        "Host": Component("Host", P, parts=(PartInstance("cpu", "Cpu"), PartInstance("ram", "Ram"))),
+        "Cpu": Component("Cpu", P, stereotype=HwStereotype(StereotypeKind.PROCESSOR)),
+        "Ram": Component("Ram", P, stereotype=HwStereotype(StereotypeKind.MEMORY, MemoryRole.HOST_RAM)),
+        "Lane": Component("Lane", P, stereotype=HwStereotype(StereotypeKind.PROCESSOR)),
+        "Smem": Component("Smem", P, stereotype=HwStereotype(StereotypeKind.MEMORY, MemoryRole.DEVICE_LOCAL,
+                                                              capacity_bytes=smem_bytes)),
+        "Rf": Component("Rf", P, stereotype=HwStereotype(StereotypeKind.MEMORY, MemoryRole.DEVICE_PRIVATE,
+                                                          capacity_bytes=256 * 1024)),
+        "Sm": Component("Sm", P, parts=(PartInstance("lane", "Lane", Shape((lanes,))), PartInstance("smem", "Smem"),
+                                        PartInstance("rf", "Rf")),
+                        stereotype=HwStereotype(StereotypeKind.PROCESSOR, frequency_mhz=1965)),
+        "Hbm": Component("Hbm", P, stereotype=HwStereotype(StereotypeKind.MEMORY, MemoryRole.DEVICE_GLOBAL,
+                                                            capacity_bytes=hbm_bytes)),
+        "Cmem": Component("Cmem", P, stereotype=HwStereotype(StereotypeKind.MEMORY, MemoryRole.DEVICE_CONSTANT,
+                                                              capacity_bytes=cmem_bytes)),
+        "B200": Component("B200", P, parts=(PartInstance("sm", "Sm", Shape((n_sm,))), PartInstance("hbm", "Hbm"),
+                                            PartInstance("cmem", "Cmem"))),
+        "p": Component("p", P, parts=(PartInstance("host", "Host"), PartInstance("gpu", "B200"))),
+    }

@@ -187,6 +187,9 @@ class Executor:
             raise _capi.NativeLibraryError("no CUDA device: the B200 executor has no CPU fallback")
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self.model, self.schedule = model, schedule
+        # MARTE memory allocation -> B200 placement; CapacityExceeded before anything is launched
+        from .placement import plan_placement
+        self.placement = plan_placement(model)
         self.device_count = device_count
         self.tilers = tilers or {}
         self.precision = precision
@@ -200,6 +203,18 @@ class Executor:
         self.iterations = 0
         self.final_relres = None
         self.converged = True
+
+    def placement_report(self) -> str:
+        """Placement of every data allocation plus the staging each device task's kernel uses."""
+        from .placement import emit_placement_report, kernel_staging
+        lines = [emit_placement_report(self.placement)]
+        for step in self.schedule.device_steps():
+            t = self.task(step.task_path)
+            l = step.launches[0]
+            ptrs = [self.storage.array(t.nodes[n]).data_ptr() for n in t.port_order]
+            name = _capi.plan_name(t.ctask, l.range.offset, l.range.count, ptrs)
+            lines.append(f"task {step.task_path} ({step.op}): kernel {name}: {kernel_staging(name)}\n")
+        return "".join(lines)
 
     def task(self, path: str) -> _Task:
         t = self._tasks.get(path)

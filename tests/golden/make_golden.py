@@ -302,6 +302,10 @@ def make_cg_case(store, meta):
     for k, v in bind.items():
         store[f"cg_k20/{k}"] = v
     meta["cg_k20"] = {"op": "cg", "model": model_to_dict(sized), "runs": {}}
+    from gmodelc.memmap import build_memory_maps, emit_memory_map_report
+    meta["cg_k20"]["memmap_report"] = emit_memory_map_report(build_memory_maps(sized))
+    meta["cg_bundled"] = {"op": "memmap", "model": model_to_dict(model),
+                          "memmap_report": emit_memory_map_report(build_memory_maps(model))}
     for d in (1, 2, 4):
         res = execute_schedule(sized, build_schedule(sized, d), dict(bind), d)
         store[f"cg_k20/x_d{d}"] = res.outputs["x"]

@@ -515,3 +515,17 @@ def test_streamed_execution_equals_plain(case, chunks):
     streamed = execute_schedule(model, sched, bind, 3, pipeline=chunks).outputs
     for k in plain:
         assert np.array_equal(plain[k], streamed[k]), k
+
+
+def test_placement_report_names_kernels():
+    from paper_1105_4424_b200 import builders
+    from paper_1105_4424_b200.executor import Executor
+    from paper_1105_4424_b200.partition import build_schedule
+    g = orc.gemm_tilers(256, 256, 64)
+    model = builders.tile_task_model(
+        "matmul", {"a": "in float32 [256,64]", "b": "in float32 [64,256]", "c": "out float32 [256,256]"},
+        {k: _tiler(v) for k, v in g.items()}, (256, 256))
+    ex = Executor(model, build_schedule(model, 1), {"p_a": np.ones(256 * 64, np.float32),
+                                                    "p_b": np.ones(64 * 256, np.float32)}, 1)
+    rep = ex.placement_report()
+    assert "matmul.tcgen05_tf32" in rep and "TMEM" in rep and "-> hbm" in rep
