@@ -285,6 +285,221 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
+// =============================================================================
+// 2-CTA variant (cta_group::2): a cluster of two CTAs on a TPC computes a 256x256
+// tile.  Each CTA TMA-loads its 128 rows of A and its 128 columns of B into its own
+// smem (6-stage ring, 32 KB/stage) and signals the leader's full barrier; the
+// leader's single thread issues tcgen05.mma.cta_group::2 M=256 N=256, which reads
+// both CTAs' operands; each CTA's TMEM holds its 128 rows x 256 fp32 columns.
+// Per-SM operand traffic is 2/3 of the 1-CTA 128x256 kernel's.
+// =============================================================================
+namespace pair {
+
+constexpr int BM = 256, BN = 256, STAGES = 6;
+constexpr int HALF_M = 128, HALF_N = 128;
+constexpr int A_BYTES = HALF_M * BK * 4;           // 16 KB
+constexpr int B_BYTES = HALF_N * BK * 4;           // 16 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;     // 32 KB per CTA
+constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;        // shared::cluster address of the same offset in CTA 0
+constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 1024 + 256;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint32_t leader_bar, void* dst, int x,
+                                                 int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(leader_bar)
+      : "memory");
+}
+__device__ __forceinline__ void mma_tf32_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, {%5, %5, %5, %5, %5, %5, %5, %5}, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(0u)
+      : "memory");
+}
+__device__ __forceinline__ void commit_pair_multicast(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void arrive_leader(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & PEER_MASK) : "memory");
+}
+
+template <bool KMAJOR, int R>
+__device__ __forceinline__ void load_operand_pair(const CUtensorMap* map, uint32_t leader_bar, uint8_t* dst,
+                                                  int kcoord, int rcoord) {
+  if (KMAJOR) {
+    tma_load_2d_pair(map, leader_bar, dst, kcoord, rcoord);
+  } else {
+#pragma unroll
+    for (int c = 0; c < R / 32; ++c) tma_load_2d_pair(map, leader_bar, dst + c * (BK * 128), rcoord + 32 * c, kcoord);
+  }
+}
+
+__device__ __forceinline__ void tile_coords_pair(const Params& p, int tile, int& mt, int& nt) {
+  const int per_group = GROUP_M * p.n_tiles;
+  const int g = tile / per_group;
+  const int first_m = g * GROUP_M;
+  const int gm = min(GROUP_M, p.m_tiles - first_m);
+  const int in = tile - g * per_group;
+  mt = first_m + in % gm;
+  nt = in / gm;
+}
+
+template <bool A_KMAJOR, bool B_KMAJOR>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    k_gemm_tf32_pair(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int pair_id = blockIdx.x >> 1, num_pairs = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&map_a);
+    prefetch_tmap(&map_b);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 2 * 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------- TMA producer (both CTAs) ----
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = pair_id; tile < p.num_tiles; tile += num_pairs) {
+        int mt, nt;
+        tile_coords_pair(p, tile, mt, nt);
+        const int row0 = (int)(p.m_lo + (int64_t)mt * BM) + (int)rank * HALF_M;
+        const int col0 = nt * BN + (int)rank * HALF_N;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * STAGE_BYTES;
+          uint8_t* sb = sa + A_BYTES;
+          const uint32_t lbar = smem_u32(&full[stage]) & PEER_MASK;
+          if (rank == 0) mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);
+          load_operand_pair<A_KMAJOR, HALF_M>(&map_a, lbar, sa, kb * BK, row0);
+          load_operand_pair<B_KMAJOR, HALF_N>(&map_b, lbar, sb, kb * BK, col0);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // ---------------------------------------------------- MMA issuer (leader) ----
+      constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((A_KMAJOR ? 0u : 1u) << 15) |
+                                 ((B_KMAJOR ? 0u : 1u) << 16) | ((uint32_t)(BN >> 3) << 17) |
+                                 ((uint32_t)(BM >> 4) << 24);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = pair_id; tile < p.num_tiles; tile += num_pairs) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+          const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / UMMA_K; ++k)
+            mma_tf32_pair(d_tmem, operand_desc<A_KMAJOR>(sa, k), operand_desc<B_KMAJOR>(sb, k), idesc,
+                          (kb | k) != 0);
+          commit_pair_multicast(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        commit_pair_multicast(&tfull[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    // -------------------------------------------------------- epilogue (both CTAs) ----
+    const int ew = warp - 4;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = pair_id; tile < p.num_tiles; tile += num_pairs) {
+      int mt, nt;
+      tile_coords_pair(p, tile, mt, nt);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int64_t gm = p.m_lo + (int64_t)mt * BM + rank * HALF_M + ew * 32 + lane;
+      const bool row_ok = gm <= p.m_hi && gm < p.M;
+      int64_t col_lo = 0, col_hi = p.N;
+      if (gm == p.m_lo) col_lo = p.first - p.m_lo * p.N;
+      if (gm == p.m_hi) col_hi = p.last - p.m_hi * p.N + 1;
+      float* crow = p.c + gm * p.ldc;
+#pragma unroll 1
+      for (int ch = 0; ch < BN / 32; ++ch) {
+        uint32_t v[32];
+        tmem_ld32(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + ch * 32, v);
+        const int64_t c0 = (int64_t)nt * BN + ch * 32;
+        if (!row_ok) continue;
+        if (p.c_vec && c0 >= col_lo && c0 + 32 <= col_hi) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            *reinterpret_cast<float4*>(crow + c0 + j) =
+                make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]),
+                            __uint_as_float(v[j + 3]));
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (c0 + j >= col_lo && c0 + j < col_hi) crow[c0 + j] = __uint_as_float(v[j]);
+        }
+      }
+      tc_fence_before();
+      arrive_leader(&tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+  }
+}
+
+}  // namespace pair
+
 // ------------------------------------------------------------ host side ----
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -399,6 +614,45 @@ int launch_gemm_tf32(const aol_task& t, int64_t first, int64_t count, void* cons
   p.c_vec = ((uintptr_t)C % 16 == 0) && (g.ldc % 4 == 0);
   if (const char* dbg = getenv("AOL_GEMM_DBG")) p.dbg = reinterpret_cast<uint32_t*>(strtoull(dbg, nullptr, 10));
 
+  static const bool force_1sm = getenv("AOL_GEMM_1SM") != nullptr;
+  if (!force_1sm) {
+    // 2-CTA path: re-encode B with 128-column boxes (each CTA loads half the tile's N)
+    CUtensorMap mb2;
+    if (g.b_kmajor) rc = make_map(&mb2, B, g.K, g.N, g.ldb, BK, pair::HALF_N, true);
+    else rc = make_map(&mb2, B, g.N, g.K, g.ldb, 32, BK, false);
+    if (rc) return rc;
+    CUtensorMap ma2;
+    if (g.a_kmajor) rc = make_map(&ma2, A, g.K, g.M, g.lda, BK, pair::HALF_M, true);
+    else rc = make_map(&ma2, A, g.M, g.K, g.lda, 32, BK, false);
+    if (rc) return rc;
+    Params pp = p;
+    pp.m_tiles = (int)((p.m_hi - p.m_lo + pair::BM) / pair::BM);
+    pp.n_tiles = (int)((g.N + pair::BN - 1) / pair::BN);
+    pp.num_tiles = pp.m_tiles * pp.n_tiles;
+    void (*k2)(const CUtensorMap, const CUtensorMap, Params);
+    if (g.a_kmajor) k2 = g.b_kmajor ? pair::k_gemm_tf32_pair<true, true> : pair::k_gemm_tf32_pair<true, false>;
+    else k2 = g.b_kmajor ? pair::k_gemm_tf32_pair<false, true> : pair::k_gemm_tf32_pair<false, false>;
+    AOL_CUDA_CHECK(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pair::SMEM_BYTES));
+    int sms2 = kNumSMs;
+    int dev2 = 0;
+    if (cudaGetDevice(&dev2) == cudaSuccess) cudaDeviceGetAttribute(&sms2, cudaDevAttrMultiProcessorCount, dev2);
+    const int pairs = pp.num_tiles < sms2 / 2 ? pp.num_tiles : sms2 / 2;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * pairs);
+    cfg.blockDim = dim3(NUM_THREADS);
+    cfg.dynamicSmemBytes = pair::SMEM_BYTES;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    AOL_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k2, ma2, mb2, pp));
+    AOL_LAUNCH_CHECK("k_gemm_tf32_pair");
+    return AOL_OK;
+  }
   void (*kern)(const CUtensorMap, const CUtensorMap, Params);
   if (g.a_kmajor) kern = g.b_kmajor ? k_gemm_tf32<true, true> : k_gemm_tf32<true, false>;
   else kern = g.b_kmajor ? k_gemm_tf32<false, true> : k_gemm_tf32<false, false>;
