@@ -81,7 +81,9 @@ static const char* plan_name(const aol_task* t, int64_t first, int64_t count, vo
   switch (t->op) {
     case AOL_OP_TILE_COPY: return tile_copy_plan_name(t->tilers[0], t->tilers[1], first, count);
     case AOL_OP_MATMUL:
-      return (ports && gemm_tf32_applicable(*t, ports)) ? "matmul.tcgen05_tf32" : "matmul.generic_exact";
+      if (ports && gemm_tf32_applicable(*t, ports))
+        return t->precision == AOL_PREC_3XTF32 ? "matmul.tcgen05_3xtf32" : "matmul.tcgen05_tf32";
+      return "matmul.generic_exact";
     case AOL_OP_TILE_FILTER: return filter_plan_name(*t);
     case AOL_OP_TILE_SUM: return "tile_sum.generic";
     default: return "identity";

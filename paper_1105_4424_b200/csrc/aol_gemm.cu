@@ -582,14 +582,77 @@ bool gemm_tf32_applicable(const aol_task& t, void* const* ports) {
   return ((uintptr_t)a % 16 == 0) && ((uintptr_t)b % 16 == 0);
 }
 
+// Split x into tf32 hi (low 13 mantissa bits cleared) and lo = x - hi (exact).
+__global__ void __launch_bounds__(256) k_split_a(const float* __restrict__ A, float* __restrict__ Ap, int64_t rows,
+                                                 int64_t K, int64_t sm, int64_t sk, int64_t row0, int64_t pitch) {
+  // Ap = [Ahi | Ahi | Alo], row-major [rows, 3K]
+  const int64_t n = rows * K;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / K, k = e - r * K;
+    const float x = A[(row0 + r) * sm + k * sk];
+    const float hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+    const float lo = __fsub_rn(x, hi);
+    float* row = Ap + r * pitch;
+    row[k] = hi;
+    row[K + k] = hi;
+    row[2 * K + k] = lo;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_split_b(const float* __restrict__ B, float* __restrict__ Bp, int64_t K,
+                                                 int64_t N, int64_t sk, int64_t sn, int64_t pitch) {
+  // Bp = [Bhi ; Blo ; Bhi], row-major [3K, N]
+  const int64_t n = K * N;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = e / N, c = e - k * N;
+    const float x = B[k * sk + c * sn];
+    const float hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+    Bp[k * pitch + c] = hi;
+    Bp[(K + k) * pitch + c] = __fsub_rn(x, hi);
+    Bp[(2 * K + k) * pitch + c] = hi;
+  }
+}
+
+static int gemm_core(const float* A, const float* B, float* C, const GemmShape& g, int64_t first, int64_t count,
+                     cudaStream_t stream);
+
 int launch_gemm_tf32(const aol_task& t, int64_t first, int64_t count, void* const* ports, cudaStream_t stream) {
-  using namespace gemm;
   GemmShape g = recognise_gemm(t);
   if (!g.ok) return fail(AOL_EUNSUPPORTED, "matmul tilers are not a TMA-compatible GEMM");
   if (count <= 0) return AOL_OK;
   const float* A = static_cast<const float*>(ports[0]) + g.ca;
   const float* B = static_cast<const float*>(ports[1]) + g.cb;
   float* C = static_cast<float*>(ports[2]) + g.cc;
+  if (t.precision != AOL_PREC_3XTF32) return gemm_core(A, B, C, g, first, count, stream);
+  // 3xTF32: C = Ahi.Bhi + Ahi.Blo + Alo.Bhi as ONE tensor-core GEMM over K' = 3K of the
+  // K-concatenated operands [Ahi|Ahi|Alo] . [Bhi;Blo;Bhi] (fp32 accumulation in TMEM).
+  const int64_t m_lo = first / g.N, m_hi = (first + count - 1) / g.N, rows = m_hi - m_lo + 1;
+  const int64_t lda3 = (3 * g.K + 3) / 4 * 4, ldb3 = (g.N + 3) / 4 * 4;   // 16-byte TMA pitches
+  float *Ap = nullptr, *Bp = nullptr;
+  AOL_CUDA_CHECK(cudaMallocAsync((void**)&Ap, (size_t)rows * lda3 * sizeof(float), stream));
+  AOL_CUDA_CHECK(cudaMallocAsync((void**)&Bp, (size_t)3 * g.K * ldb3 * sizeof(float), stream));
+  const int64_t sa_m = g.a_kmajor ? g.lda : 1, sa_k = g.a_kmajor ? 1 : g.lda;
+  const int64_t sb_k = g.b_kmajor ? 1 : g.ldb, sb_n = g.b_kmajor ? g.ldb : 1;
+  k_split_a<<<grid_for(rows * g.K, 256, 16), 256, 0, stream>>>(A, Ap, rows, g.K, sa_m, sa_k, m_lo, lda3);
+  AOL_LAUNCH_CHECK("k_split_a");
+  k_split_b<<<grid_for(g.K * g.N, 256, 16), 256, 0, stream>>>(B, Bp, g.K, g.N, sb_k, sb_n, ldb3);
+  AOL_LAUNCH_CHECK("k_split_b");
+  GemmShape g3 = g;
+  g3.a_kmajor = true;
+  g3.b_kmajor = false;
+  g3.M = rows;
+  g3.K = 3 * g.K;
+  g3.lda = lda3;
+  g3.ldb = ldb3;
+  int rc = gemm_core(Ap, Bp, C + m_lo * g.ldc, g3, first - m_lo * g.N, count, stream);
+  cudaFreeAsync(Ap, stream);
+  cudaFreeAsync(Bp, stream);
+  return rc;
+}
+
+static int gemm_core(const float* A, const float* B, float* C, const GemmShape& g, int64_t first, int64_t count,
+                     cudaStream_t stream) {
+  using namespace gemm;
   CUtensorMap ma, mb;
   int rc;
   if (g.a_kmajor) rc = make_map(&ma, A, g.K, g.M, g.lda, BK, BM, true);

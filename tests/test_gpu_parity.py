@@ -529,3 +529,34 @@ def test_placement_report_names_kernels():
                                                     "p_b": np.ones(64 * 256, np.float32)}, 1)
     rep = ex.placement_report()
     assert "matmul.tcgen05_tf32" in rep and "TMEM" in rep and "-> hbm" in rep
+
+
+@pytest.mark.parametrize("M,N,K,devices,bt", [(256, 256, 256, 1, False), (300, 520, 200, 3, False),
+                                              (1024, 768, 2048, 2, True), (129, 130, 131, 1, False)])
+def test_matmul_3xtf32_fp32_accuracy(M, N, K, devices, bt):
+    """precision='3xtf32': hi/lo split, three TF32 products on the tensor cores -> fp32-level accuracy.
+    Stated bound: |C - C64| <= (2^-19 + 3K * 2^-24) (|A||B|), and normwise error < 5e-6."""
+    from paper_1105_4424_b200 import _capi
+    rng = np.random.default_rng(M + K)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    B = rng.standard_normal((K, N)).astype(np.float32)
+    g = orc.gemm_tilers(M, N, K)
+    if bt:
+        g["b"] = dict(array=(N, K), rep=(M, N), pattern=(K,), origin=(0, 0), paving=((0, 1), (0, 0)),
+                      fitting=((0,), (1,)))
+        b_bind, b_spec = B.T.copy().ravel(), f"in float32 [{N},{K}]"
+    else:
+        b_bind, b_spec = B.ravel(), f"in float32 [{K},{N}]"
+    ports = {"a": f"in float32 [{M},{K}]", "b": b_spec, "c": f"out float32 [{M},{N}]"}
+    res = _run_tile("matmul", g, ports, {"a": A.ravel(), "b": b_bind}, devices, precision="3xtf32")
+    c = res.outputs["p_c"].reshape(M, N)
+    a64, b64 = A.astype(np.float64), B.astype(np.float64)
+    c64 = a64 @ b64
+    bound = (2.0 ** -19 + 3 * K * 2.0 ** -24) * (np.abs(a64) @ np.abs(b64))
+    assert np.all(np.abs(c - c64) <= bound)
+    assert np.linalg.norm(c - c64) / np.linalg.norm(c64) < 5e-6
+    bts = [_tiler(g[k]).bind(g[k]["array"], (M, N)) for k in "abc"]
+    t = torch.zeros(4, device="cuda")
+    if K % 4 == 0 and (bt or N % 4 == 0):
+        assert _capi.plan_name(_capi.make_task("matmul", "float32", bts, precision="3xtf32"), 0, M * N,
+                               [t.data_ptr()] * 3) == "matmul.tcgen05_3xtf32"
