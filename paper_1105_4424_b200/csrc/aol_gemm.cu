@@ -585,7 +585,8 @@ bool gemm_tf32_applicable(const aol_task& t, void* const* ports) {
 // Split x into tf32 hi (low 13 mantissa bits cleared) and lo = x - hi (exact).
 __global__ void __launch_bounds__(256) k_split_a(const float* __restrict__ A, float* __restrict__ Ap, int64_t rows,
                                                  int64_t K, int64_t sm, int64_t sk, int64_t row0, int64_t pitch) {
-  // Ap = [Ahi | Ahi | Alo], row-major [rows, 3K]
+  // Ap = [Alo | Ahi | Ahi], row-major [rows, 3K]: the small correction products accumulate
+  // first, so they are not rounded away against the large Ahi.Bhi running sum
   const int64_t n = rows * K;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = e / K, k = e - r * K;
@@ -593,9 +594,9 @@ __global__ void __launch_bounds__(256) k_split_a(const float* __restrict__ A, fl
     const float hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
     const float lo = __fsub_rn(x, hi);
     float* row = Ap + r * pitch;
-    row[k] = hi;
+    row[k] = lo;
     row[K + k] = hi;
-    row[2 * K + k] = lo;
+    row[2 * K + k] = hi;
   }
 }
 
@@ -624,8 +625,8 @@ int launch_gemm_tf32(const aol_task& t, int64_t first, int64_t count, void* cons
   const float* B = static_cast<const float*>(ports[1]) + g.cb;
   float* C = static_cast<float*>(ports[2]) + g.cc;
   if (t.precision != AOL_PREC_3XTF32) return gemm_core(A, B, C, g, first, count, stream);
-  // 3xTF32: C = Ahi.Bhi + Ahi.Blo + Alo.Bhi as ONE tensor-core GEMM over K' = 3K of the
-  // K-concatenated operands [Ahi|Ahi|Alo] . [Bhi;Blo;Bhi] (fp32 accumulation in TMEM).
+  // 3xTF32: C = Alo.Bhi + Ahi.Blo + Ahi.Bhi as ONE tensor-core GEMM over K' = 3K of the
+  // K-concatenated operands [Alo|Ahi|Ahi] . [Bhi;Blo;Bhi] (fp32 accumulation in TMEM).
   const int64_t m_lo = first / g.N, m_hi = (first + count - 1) / g.N, rows = m_hi - m_lo + 1;
   const int64_t lda3 = (3 * g.K + 3) / 4 * 4, ldb3 = (g.N + 3) / 4 * 4;   // 16-byte TMA pitches
   float *Ap = nullptr, *Bp = nullptr;
