@@ -126,6 +126,18 @@ int aol_tiler_offsets(const aol_tiler* tiler, int64_t first, int64_t count,
 /* Number of kernels this library has launched in this process (evidence counter). */
 int64_t aol_launch_counter(void);
 
+/* Task fusion: run `consumer` over its repetitions [first, first+count) computing
+ * the part of `producer`'s output it reads on the fly, in shared memory, instead of
+ * reading a materialised intermediate array (bit-identical results; the
+ * intermediate is not written).  The executor calls it for two consecutive
+ * DeviceSteps whose connecting port group only they use; returns
+ * AOL_EUNSUPPORTED (nothing launched) when the pair is not fusable — currently a
+ * horizontal 13->3 line filter feeding a vertical 14->4 line filter, the Array-OL
+ * downscaler.  No reference counterpart (the reference runs steps one by one,
+ * refexec.py:518-541). */
+int aol_launch_fused2(const aol_task* producer, const aol_task* consumer, int64_t first, int64_t count,
+                      void* const* producer_ports, void* const* consumer_ports, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -27,7 +27,7 @@ OP = {"copy": 1, "sub": 2, "scale": 3, "axpy": 4, "spmv_csr": 5, "dot_partial": 
 PRECISION = {"default": 0, "tf32": 1, "3xtf32": 2, "exact": 3}
 
 EXPORTS = ("aol_abi_version", "aol_last_error", "aol_device_count", "aol_validate", "aol_launch",
-           "aol_plan_name", "aol_tiler_offsets", "aol_launch_counter")
+           "aol_plan_name", "aol_tiler_offsets", "aol_launch_counter", "aol_launch_fused2")
 
 
 class NativeLibraryError(RuntimeError):
@@ -114,6 +114,8 @@ def load(path: Path | str | None = None) -> C.CDLL:
                                   C.c_char_p, C.c_int]
     lib.aol_tiler_offsets.argtypes = [C.POINTER(AolTiler), C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]
     lib.aol_launch_counter.restype = C.c_int64
+    lib.aol_launch_fused2.argtypes = [C.POINTER(AolTask), C.POINTER(AolTask), C.c_int64, C.c_int64,
+                                      C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_void_p]
     if lib.aol_abi_version() != ABI_VERSION:
         raise NativeLibraryError(f"{p}: ABI {lib.aol_abi_version()} != expected {ABI_VERSION}")
     _lib = lib
@@ -156,6 +158,17 @@ def tiler_offsets(bt: BoundTiler, first: int, count: int, out_ptr: int, stream: 
     t = pack_tiler(bt)
     check(load().aol_tiler_offsets(C.byref(t), int(first), int(count), C.c_void_p(int(out_ptr)),
                                    C.c_void_p(int(stream))))
+
+
+def launch_fused2(producer: AolTask, consumer: AolTask, first: int, count: int, pports: list[int],
+                  cports: list[int], stream: int = 0) -> bool:
+    """True when the fused kernel ran; False when the pair is not fusable (nothing launched)."""
+    rc = load().aol_launch_fused2(C.byref(producer), C.byref(consumer), int(first), int(count), _ptrs(pports),
+                                  _ptrs(cports), C.c_void_p(int(stream)))
+    if rc == AOL_EUNSUPPORTED:
+        return False
+    check(rc)
+    return True
 
 
 def launch_counter() -> int:

@@ -33,6 +33,8 @@ int launch_tile_sum(const aol_task& t, int64_t first, int64_t count, void* const
 int launch_identity(const aol_task& t, int64_t first, int64_t count, void* const* ports, const double* scalars,
                     cudaStream_t s);
 bool gemm_tf32_applicable(const aol_task& t, void* const* ports);
+int launch_fused_line_filters(const aol_task& th, const aol_task& tv, int64_t first, int64_t count,
+                              void* const* ph, void* const* pv, cudaStream_t s);
 int launch_gemm_tf32(const aol_task& t, int64_t first, int64_t count, void* const* ports, cudaStream_t s);
 
 static int tilers_needed(int op) {
@@ -152,5 +154,19 @@ int aol_tiler_offsets(const aol_tiler* tiler, int64_t first, int64_t count, int6
 }
 
 int64_t aol_launch_counter(void) { return g_launches.load(); }
+
+int aol_launch_fused2(const aol_task* producer, const aol_task* consumer, int64_t first, int64_t count,
+                      void* const* producer_ports, void* const* consumer_ports, void* stream) {
+  int rc = validate(producer);
+  if (rc) return rc;
+  if ((rc = validate(consumer))) return rc;
+  if (producer->op != AOL_OP_TILE_FILTER || consumer->op != AOL_OP_TILE_FILTER)
+    return fail(AOL_EUNSUPPORTED, "fusion is implemented for tile_filter -> tile_filter chains");
+  if (first < 0 || count < 0 || first + count > task_rep_total(consumer))
+    return fail(AOL_EINVAL, "repetition range outside the consumer's repetition space");
+  if (!producer_ports || !consumer_ports) return fail(AOL_EINVAL, "null port array");
+  return launch_fused_line_filters(*producer, *consumer, first, count, producer_ports, consumer_ports,
+                                   static_cast<cudaStream_t>(stream));
+}
 
 }  // extern "C"

@@ -205,3 +205,152 @@ int launch_line_filter(const aol_task& t, const LineGeom& g, int64_t first, int6
 }
 
 }  // namespace aol
+
+namespace aol {
+
+// -----------------------------------------------------------------------------
+// Task fusion: a horizontal line filter (inner == 1) feeding a vertical line filter
+// through an intermediate array that only the second task reads — the Array-OL
+// downscaler (config C3).  The fused kernel computes, per tile of the consumer's
+// repetition space, the intermediate rows the tile needs into shared memory (same
+// tap order, same __fmul_rn/__fadd_rn, so the values are bit-identical to the
+// unfused intermediate) and applies the consumer filter from shared memory.  The
+// intermediate never touches HBM: x is read once (+ (px_v - sx_v)/(TV*sx_v) halo
+// rows) and y written once.
+// -----------------------------------------------------------------------------
+constexpr int FZ_TV = 8;       // consumer line repetitions per tile
+constexpr int FZ_HR = 32;      // producer repetitions per intermediate row per tile
+constexpr int FZ_THREADS = 256;
+
+struct FusedGeom {
+  LineGeom h, v;
+  int64_t R;                   // rows of the intermediate (= v.Sx)
+  int64_t Wm;                  // columns of the intermediate (= h.Sy = v.inner)
+  int64_t W;                   // x line length (= h.Sx)
+  int NR;                      // intermediate rows per tile
+  int TI;                      // intermediate columns per tile (FZ_HR * h.sy)
+  int64_t tiles_i, tiles_l;
+};
+
+bool fused_line_geometry(const aol_task& th, const aol_task& tv, FusedGeom& f) {
+  if (!line_filter_geometry(th, f.h) || !line_filter_geometry(tv, f.v)) return false;
+  const LineGeom &h = f.h, &v = f.v;
+  if (h.inner != 1 || v.inner != h.Sy || h.outer != v.outer * v.Sx) return false;
+  // the producer writes every intermediate element exactly once (dense, no origin)
+  if (h.oy != 0 || h.sy != h.py || h.NL * h.sy != h.Sy) return false;
+  if (h.px > 16 || v.px > 16 || h.py > 8 || v.py > 8) return false;
+  // the intermediate array of the producer's output tiler must be the consumer's x array
+  const aol_tiler &hy = th.tilers[1], &vx = tv.tilers[0];
+  if (hy.arr_rank != vx.arr_rank) return false;
+  for (int d = 0; d < hy.arr_rank; ++d)
+    if (hy.array[d] != vx.array[d]) return false;
+  f.R = v.Sx;
+  f.Wm = h.Sy;
+  f.W = h.Sx;
+  f.NR = (int)((FZ_TV - 1) * v.sx + v.px);
+  f.TI = FZ_HR * (int)h.sy;
+  if ((int64_t)f.NR * f.TI * 4 > 96 * 1024) return false;
+  f.tiles_i = (f.Wm + f.TI - 1) / f.TI;
+  f.tiles_l = (v.NL + FZ_TV - 1) / FZ_TV;
+  return f.R * f.W * v.outer < (1ll << 32);   // 32-bit x offsets
+}
+
+template <int PXH, int PYH, int PXV, int PYV>
+__global__ void __launch_bounds__(FZ_THREADS) k_fused_line_filters(const float* __restrict__ x,
+                                                                   const float* __restrict__ wh,
+                                                                   const float* __restrict__ wv,
+                                                                   float* __restrict__ y, FusedGeom g, int64_t first,
+                                                                   int64_t last, int64_t tile0, int64_t ntiles) {
+  extern __shared__ float sm[];
+  float* mt = sm;                                   // [NR][TI] intermediate tile
+  __shared__ float swh[PXH * PYH], swv[PXV * PYV];
+  for (int k = threadIdx.x; k < PXH * PYH; k += blockDim.x) swh[k] = wh[k];
+  for (int k = threadIdx.x; k < PXV * PYV; k += blockDim.x) swv[k] = wv[k];
+  const LineGeom &h = g.h, &v = g.v;
+  for (int64_t tt = tile0 + blockIdx.x; tt < tile0 + ntiles; tt += gridDim.x) {
+    const int64_t ib = tt % g.tiles_i;
+    const int64_t q = tt / g.tiles_i;
+    const int64_t lb = q % g.tiles_l;
+    const int64_t fr = q / g.tiles_l;               // frame (consumer outer index)
+    const int64_t lv0 = lb * FZ_TV;
+    const int64_t i0 = ib * g.TI;
+    const int64_t lh0 = i0 / h.sy;
+    __syncthreads();                                // weights ready / previous tile consumed
+    // phase 1: intermediate rows r_k = (lv0*sxv + oxv + k) mod R, columns [i0, i0+TI)
+    for (int item = threadIdx.x; item < g.NR * FZ_HR; item += blockDim.x) {
+      const int k = item / FZ_HR, hh = item - k * FZ_HR;
+      const int64_t lh = lh0 + hh;
+      if (lh >= h.NL) continue;
+      const int64_t r = (lv0 * v.sx + v.ox + k) % g.R;
+      const uint32_t xrow = (uint32_t)((fr * g.R + r) * g.W);
+      int64_t col = lh * h.sx + h.ox;
+      if (col >= g.W) col %= g.W;
+      float xv[16];
+      if (col + 16 <= g.W && ((xrow + col) & 3) == 0) {
+        const float4* p = reinterpret_cast<const float4*>(x + xrow + col);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float4 t4 = __ldg(p + u);
+          xv[4 * u] = t4.x; xv[4 * u + 1] = t4.y; xv[4 * u + 2] = t4.z; xv[4 * u + 3] = t4.w;
+        }
+      } else {
+        int64_t c = col;
+#pragma unroll
+        for (int t = 0; t < PXH; ++t) {
+          xv[t] = __ldg(x + xrow + c);
+          if (++c == g.W) c = 0;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < PYH; ++j) {
+        float acc = 0.0f;
+#pragma unroll
+        for (int t = 0; t < PXH; ++t) acc = __fadd_rn(acc, __fmul_rn(swh[j * PXH + t], xv[t]));
+        mt[k * g.TI + hh * PYH + j] = acc;
+      }
+    }
+    __syncthreads();
+    // phase 2: consumer repetitions (fr, lv, i) of this tile
+    for (int item = threadIdx.x; item < FZ_TV * g.TI; item += blockDim.x) {
+      const int l = item / g.TI, c = item - l * g.TI;
+      const int64_t lv = lv0 + l, i = i0 + c;
+      if (lv >= v.NL || i >= g.Wm) continue;
+      const int64_t rho = (fr * v.NL + lv) * g.Wm + i;
+      if (rho < first || rho > last) continue;
+      float* yp = y + (fr * v.Sy + lv * v.sy + v.oy) * g.Wm + i;
+      const float* mp = mt + (l * v.sx) * g.TI + c;
+#pragma unroll
+      for (int j = 0; j < PYV; ++j) {
+        float acc = 0.0f;
+#pragma unroll
+        for (int t = 0; t < PXV; ++t) acc = __fadd_rn(acc, __fmul_rn(swv[j * PXV + t], mp[t * g.TI]));
+        yp[j * g.Wm] = acc;
+      }
+    }
+  }
+}
+
+int launch_fused_line_filters(const aol_task& th, const aol_task& tv, int64_t first, int64_t count,
+                              void* const* ph, void* const* pv, cudaStream_t s) {
+  FusedGeom g;
+  if (!fused_line_geometry(th, tv, g)) return fail(AOL_EUNSUPPORTED, "task pair is not a fusable line-filter chain");
+  if (!(g.h.px == 13 && g.h.py == 3 && g.v.px == 14 && g.v.py == 4))
+    return fail(AOL_EUNSUPPORTED, "fused line filters are instantiated for 13x3 -> 14x4");
+  if (count <= 0) return AOL_OK;
+  const int64_t last = first + count - 1;
+  const int64_t per_frame = g.v.NL * g.Wm;
+  const int64_t f_lo = first / per_frame, f_hi = last / per_frame;
+  const int64_t tiles_per_frame = g.tiles_i * g.tiles_l;
+  const int64_t tile0 = f_lo * tiles_per_frame, ntiles = (f_hi - f_lo + 1) * tiles_per_frame;
+  const size_t smem = (size_t)g.NR * g.TI * sizeof(float);
+  auto kern = k_fused_line_filters<13, 3, 14, 4>;
+  if (smem > 48 * 1024) AOL_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t grid = ntiles < (int64_t)kNumSMs * 8 ? ntiles : (int64_t)kNumSMs * 8;
+  kern<<<(unsigned)grid, FZ_THREADS, smem, s>>>(static_cast<const float*>(ph[0]), static_cast<const float*>(ph[1]),
+                                                static_cast<const float*>(pv[1]), static_cast<float*>(pv[2]), g, first,
+                                                last, tile0, ntiles);
+  AOL_LAUNCH_CHECK("k_fused_line_filters");
+  return AOL_OK;
+}
+
+}  // namespace aol

@@ -216,6 +216,7 @@ def make_distributed_executor(model, schedule, bindings: dict, *, group=None, **
         def __init__(self):
             import torch.distributed as dist
             self.xch = Exchange(group)
+            kw.setdefault("fuse", False)     # fused chains skip the intermediate exchange
             super().__init__(model, schedule, bindings, self.xch.world, **kw)
             self.rank, self.world = self.xch.rank, self.xch.world
 

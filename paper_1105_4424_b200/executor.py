@@ -180,7 +180,7 @@ class Executor:
     """Prepared schedule: storage resident in HBM, tasks validated, ready to run repeatedly."""
 
     def __init__(self, model, schedule, bindings: dict, device_count: int, *, tilers: dict | None = None,
-                 precision: str = "default", device=None, stream=None, pipeline: int = 0):
+                 precision: str = "default", device=None, stream=None, pipeline: int = 0, fuse: bool = True):
         torch = _torch()
         _capi.load()
         if not torch.cuda.is_available():
@@ -199,6 +199,9 @@ class Executor:
         with torch.cuda.device(self.device):
             self.storage = DeviceStorage(model, bindings, self.device, stream, defer=bool(self.pipeline))
         self._tasks: dict[str, _Task] = {}
+        self.fuse = fuse
+        self._fusable: dict[tuple, bool] = {}
+        self.fused_launches = 0
         self._dot_buf = None
         self.iterations = 0
         self.final_relres = None
@@ -376,8 +379,47 @@ class Executor:
         comp.synchronize()
         return {n: (out[n] if out is not None and n in out else h.numpy()) for n, h in hosts.items()}
 
+    # -- task fusion ---------------------------------------------------------------
+    def _fusion_candidate(self, s1, s2) -> bool:
+        """s1's filter output feeds s2's filter input through a group nobody else touches."""
+        from .intrinsics import FILTER_OPS
+        key = (s1.task_path, s2.task_path)
+        if key in self._fusable:
+            return self._fusable[key]
+        ok = False
+        if self.fuse and s1.op in FILTER_OPS and s2.op in FILTER_OPS:
+            st = self.storage
+            g = st.groups.get(f"{s1.task_path}.y")
+            ok = g is not None and g is st.groups.get(f"{s2.task_path}.x") and \
+                set(g) == {f"{s1.task_path}.y", f"{s2.task_path}.x"}
+        self._fusable[key] = ok
+        return ok
+
+    def _run_fused(self, s1, s2) -> bool:
+        t1, t2 = self.task(s1.task_path), self.task(s2.task_path)
+        a1 = [self.storage.array(t1.nodes[n]).data_ptr() for n in t1.port_order]
+        a2 = [self.storage.array(t2.nodes[n]).data_ptr() for n in t2.port_order]
+        st = self._stream_handle()
+        for i, l in enumerate(s2.launches):
+            if not _capi.launch_fused2(t1.ctask, t2.ctask, l.range.offset, l.range.count, a1, a2, st):
+                if i == 0:
+                    self._fusable[(s1.task_path, s2.task_path)] = False
+                    return False
+                raise RuntimeError("fusion became unsupported mid-step")
+            self.fused_launches += 1
+        return True
+
     def run_steps(self, steps, tol=None, max_iter=None) -> None:
-        for step in steps:
+        steps = list(steps)
+        i = 0
+        while i < len(steps):
+            step = steps[i]
+            nxt = steps[i + 1] if i + 1 < len(steps) else None
+            if (hasattr(step, "launches") and nxt is not None and hasattr(nxt, "launches")
+                    and self._fusion_candidate(step, nxt) and self._run_fused(step, nxt)):
+                i += 2
+                continue
+            i += 1
             if hasattr(step, "launches"):
                 self.run_device(step)
             elif hasattr(step, "body"):
@@ -438,10 +480,10 @@ class Executor:
 def execute_schedule(model, schedule, bindings: dict, device_count: int, tol: float | None = None,
                      max_iter: int | None = None, *, tilers: dict | None = None, precision: str = "default",
                      device_outputs: bool = False, out: dict | None = None, device=None,
-                     stream=None, pipeline: int = 0) -> ExecutionResult:
+                     stream=None, pipeline: int = 0, fuse: bool = True) -> ExecutionResult:
     """Interpret ``schedule`` on the B200 with ``device_count`` launch shards per device step."""
     ex = Executor(model, schedule, bindings, device_count, tilers=tilers, precision=precision,
-                  device=device, stream=stream, pipeline=0 if device_outputs else pipeline)
+                  device=device, stream=stream, pipeline=0 if device_outputs else pipeline, fuse=fuse)
     if ex.pipeline:
         torch = _torch()
         with torch.cuda.device(ex.device):

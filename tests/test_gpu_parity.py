@@ -561,3 +561,48 @@ def test_matmul_3xtf32_fp32_accuracy(M, N, K, devices, bt):
     if K % 4 == 0 and (bt or N % 4 == 0):
         assert _capi.plan_name(_capi.make_task("matmul", "float32", bts, precision="3xtf32"), 0, M * N,
                                [t.data_ptr()] * 3) == "matmul.tcgen05_3xtf32"
+
+
+def _downscaler_model(F, H, W):
+    from paper_1105_4424_b200 import builders
+    th = orc.hfilter_tilers(F, H, W)
+    Wo = th["y"]["array"][2]
+    tv = orc.vfilter_tilers(F, H, Wo)
+    wh, wv = orc.hfilter_weights(), orc.vfilter_weights()
+    spec = lambda d, io: _spec(d, io, "float32")   # noqa: E731
+    model = builders.chain_model(
+        [("h", "hfilter", {"x": spec(th["x"], "in"), "w": f"in float32 [{wh.size}]", "y": spec(th["y"], "out")},
+          {k: _tiler(v) for k, v in th.items()}, th["x"]["rep"]),
+         ("v", "vfilter", {"x": spec(tv["x"], "in"), "w": f"in float32 [{wv.size}]", "y": spec(tv["y"], "out")},
+          {k: _tiler(v) for k, v in tv.items()}, tv["x"]["rep"])],
+        {"x": spec(th["x"], "in"), "wh": f"in float32 [{wh.size}]", "wv": f"in float32 [{wv.size}]"},
+        {"y": spec(tv["y"], "out")},
+        [("x", "h.x"), ("wh", "h.w"), ("h.y", "v.x"), ("wv", "v.w"), ("v.y", "y")])
+    return model, th, tv, wh, wv
+
+
+@pytest.mark.parametrize("F,H,W,devices", [(2, 18, 64, 1), (3, 45, 256, 3), (1, 27, 776, 2), (2, 99, 384, 5)])
+def test_fused_downscaler_bitwise(F, H, W, devices):
+    """H->V task fusion (intermediate kept in shared memory) equals the unfused chain and the oracle bit for bit."""
+    from paper_1105_4424_b200.executor import Executor
+    from paper_1105_4424_b200.partition import build_schedule
+    model, th, tv, wh, wv = _downscaler_model(F, H, W)
+    x = np.random.default_rng(F * H + W).random(F * H * W).astype(np.float32)
+    bind = {"x": x, "wh": wh, "wv": wv}
+    sched = build_schedule(model, devices)
+    ex = Executor(model, sched, bind, devices)
+    ex.run()
+    fused = ex.outputs()["y"]
+    assert ex.fused_launches == len(sched.steps[1].launches)
+    ex2 = Executor(model, sched, bind, devices, fuse=False)
+    ex2.run()
+    assert ex2.fused_launches == 0
+    plain = ex2.outputs()["y"]
+    assert np.array_equal(fused.view(np.uint32), plain.view(np.uint32))
+    Wo = th["y"]["array"][2]
+    mid = orc.run_tile_task("hfilter", th, {"x": x, "w": wh}, {"y": (F * H * Wo, np.float32)},
+                            int(np.prod(th["x"]["rep"])), 1)["y"]
+    ny = int(np.prod(tv["y"]["array"]))
+    want = orc.run_tile_task("vfilter", tv, {"x": mid, "w": wv}, {"y": (ny, np.float32)},
+                             int(np.prod(tv["x"]["rep"])), 1)["y"]
+    assert np.array_equal(fused.view(np.uint32), want.view(np.uint32))
