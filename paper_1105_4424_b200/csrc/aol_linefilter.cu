@@ -303,15 +303,25 @@ __global__ void __launch_bounds__(FZ_THREADS) k_fused_line_filters(const float* 
     const int64_t r_begin = lv0 * v.sx + v.ox, r_end = (lv1 - 1) * v.sx + v.ox + PXV;   // unwrapped rows
     int64_t rr = r_begin % g.R;
     float* yb = y + fr * v.Sy * g.Wm + i;
+    // software pipeline: the window of row r+1 is in flight while row r is reduced
+    float4 nxt[4];
+    auto fetch = [&](int64_t row, float4 (&dst)[4]) {
+      const float* xr = xf + row * g.W;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) dst[u] = __ldg(reinterpret_cast<const float4*>(xr) + u);
+    };
+    if (xvec) fetch(rr, nxt);
     for (int64_t r = r_begin; r < r_end; ++r) {
       // producer value m(rr, i), taps in order
       float xv[16];
-      const float* xr = xf + rr * g.W;
       if (xvec) {
+        float4 curw[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) curw[u] = nxt[u];
+        if (r + 1 < r_end) fetch(rr + 1 == g.R ? 0 : rr + 1, nxt);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const float4 t4 = __ldg(reinterpret_cast<const float4*>(xr) + u);
-          xv[4 * u] = t4.x; xv[4 * u + 1] = t4.y; xv[4 * u + 2] = t4.z; xv[4 * u + 3] = t4.w;
+          xv[4 * u] = curw[u].x; xv[4 * u + 1] = curw[u].y; xv[4 * u + 2] = curw[u].z; xv[4 * u + 3] = curw[u].w;
         }
       } else {
         int64_t c = col0;

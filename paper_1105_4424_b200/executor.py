@@ -180,7 +180,7 @@ class Executor:
     """Prepared schedule: storage resident in HBM, tasks validated, ready to run repeatedly."""
 
     def __init__(self, model, schedule, bindings: dict, device_count: int, *, tilers: dict | None = None,
-                 precision: str = "default", device=None, stream=None, pipeline: int = 0, fuse: bool = True):
+                 precision: str = "default", device=None, stream=None, pipeline: int = 0, fuse: bool = False):
         torch = _torch()
         _capi.load()
         if not torch.cuda.is_available():
@@ -480,7 +480,7 @@ class Executor:
 def execute_schedule(model, schedule, bindings: dict, device_count: int, tol: float | None = None,
                      max_iter: int | None = None, *, tilers: dict | None = None, precision: str = "default",
                      device_outputs: bool = False, out: dict | None = None, device=None,
-                     stream=None, pipeline: int = 0, fuse: bool = True) -> ExecutionResult:
+                     stream=None, pipeline: int = 0, fuse: bool = False) -> ExecutionResult:
     """Interpret ``schedule`` on the B200 with ``device_count`` launch shards per device step."""
     ex = Executor(model, schedule, bindings, device_count, tilers=tilers, precision=precision,
                   device=device, stream=stream, pipeline=0 if device_outputs else pipeline, fuse=fuse)

@@ -590,7 +590,7 @@ def test_fused_downscaler_bitwise(F, H, W, devices):
     x = np.random.default_rng(F * H + W).random(F * H * W).astype(np.float32)
     bind = {"x": x, "wh": wh, "wv": wv}
     sched = build_schedule(model, devices)
-    ex = Executor(model, sched, bind, devices)
+    ex = Executor(model, sched, bind, devices, fuse=True)
     ex.run()
     fused = ex.outputs()["y"]
     assert ex.fused_launches == len(sched.steps[1].launches)
