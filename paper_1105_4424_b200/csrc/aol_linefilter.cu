@@ -173,10 +173,59 @@ __global__ void __launch_bounds__(256) k_line_filter(const float* __restrict__ x
   }
 }
 
+// Vertical strips (inner > 1): one thread computes REPS consecutive line repetitions of one
+// (outer, inner) column.  Their windows overlap (px > sx), so the (REPS-1)*sx + px rows are
+// loaded once into registers; every output is still summed over its own taps in order.
+template <int PX, int PY, int SX, int REPS>
+__global__ void __launch_bounds__(256) k_line_filter_vstrip(const float* __restrict__ x, const float* __restrict__ w,
+                                                            float* __restrict__ y, LineGeom g, int64_t first,
+                                                            int64_t last, int64_t o_lo, int64_t ngroups) {
+  constexpr int NRW = (REPS - 1) * SX + PX;
+  __shared__ float ws[PX * PY];
+  for (int k = threadIdx.x; k < PX * PY; k += blockDim.x) ws[k] = w[k];
+  __syncthreads();
+  const uint32_t inner = (uint32_t)g.inner;
+  const int64_t NLG = (g.NL + REPS - 1) / REPS;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ngroups;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % g.inner;
+    const int64_t q = e / g.inner;
+    const int64_t lg = q % NLG, o = o_lo + q / NLG;
+    const int64_t l0 = lg * REPS;
+    const int64_t rho0 = (o * g.NL + l0) * g.inner + i;
+    const int64_t rhoN = (o * g.NL + min(l0 + REPS, g.NL) - 1) * g.inner + i;
+    if (rhoN < first || rho0 > last) continue;
+    uint32_t row = (uint32_t)((l0 * SX + g.ox) % g.Sx);
+    const float* xb = x + (uint64_t)o * (uint64_t)(g.Sx * g.inner) + i;
+    float xw[NRW];
+#pragma unroll
+    for (int t = 0; t < NRW; ++t) {
+      xw[t] = __ldg(xb + (uint64_t)row * inner);
+      if (++row == (uint32_t)g.Sx) row = 0;
+    }
+    float* yb = y + (uint64_t)o * (uint64_t)(g.Sy * g.inner) + i;
+#pragma unroll
+    for (int u = 0; u < REPS; ++u) {
+      const int64_t l = l0 + u;
+      const int64_t rho = rho0 + (int64_t)u * g.inner;
+      if (l >= g.NL || rho < first || rho > last) continue;
+      float* yp = yb + (uint64_t)(l * g.sy + g.oy) * inner;
+#pragma unroll
+      for (int j = 0; j < PY; ++j) {
+        float acc = 0.0f;
+#pragma unroll
+        for (int t = 0; t < PX; ++t) acc = __fadd_rn(acc, __fmul_rn(ws[j * PX + t], xw[u * SX + t]));
+        yp[(uint64_t)j * inner] = acc;
+      }
+    }
+  }
+}
+
 static_assert(sizeof(LineGeom) <= 256, "LineGeomBuf in aol_tile.cu must hold a LineGeom");
 
 const char* line_filter_variant(const LineGeom& g) {
   if (g.px == 13 && g.py == 3) return "tile_filter.line_13x3";
+  if (g.px == 14 && g.py == 4 && g.inner > 1 && g.sx == 9) return "tile_filter.line_14x4_vstrip";
   if (g.px == 14 && g.py == 4) return "tile_filter.line_14x4";
   return "tile_filter.line";
 }
@@ -189,6 +238,18 @@ int launch_line_filter(const aol_task& t, const LineGeom& g, int64_t first, int6
   const unsigned grid = grid_for(count, 256, 8);
   // 32-bit offsets whenever both arrays fit (every in-range offset < 2^32)
   const bool idx32 = g.outer * g.Sx * g.inner < (1ll << 32) && g.outer * g.Sy * g.inner < (1ll << 32);
+  if (idx32 && g.inner > 1 && g.px == 14 && g.py == 4 && g.sx == 9 && g.Sx * g.inner < (1ll << 32)) {
+    constexpr int REPS = 4;
+    const int64_t last = first + count - 1;
+    const int64_t NLG = (g.NL + REPS - 1) / REPS;
+    // repetition groups intersecting [first, last]
+    const int64_t o_lo = first / (g.NL * g.inner), o_hi = last / (g.NL * g.inner);
+    const int64_t ngroups = (o_hi - o_lo + 1) * NLG * g.inner;
+    k_line_filter_vstrip<14, 4, 9, REPS><<<grid_for(ngroups, 256, 8), 256, 0, s>>>(x, w, y, g, first, last, o_lo,
+                                                                                    ngroups);
+    AOL_LAUNCH_CHECK("k_line_filter_vstrip");
+    return AOL_OK;
+  }
   if (idx32) {
     if (g.px == 13 && g.py == 3)
       k_line_filter<13, 3, uint32_t><<<grid, 256, 0, s>>>(x, w, y, g, first, count);

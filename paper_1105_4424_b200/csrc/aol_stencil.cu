@@ -15,8 +15,8 @@
 
 namespace aol {
 
-constexpr int ST_TX = 32, ST_TY = 8;       // threads
-constexpr int ST_RPT = 4, ST_CPT = 4;      // outputs per thread: rows, cols
+constexpr int ST_TX = 32, ST_TY = 4;       // threads
+constexpr int ST_RPT = 8, ST_CPT = 4;      // outputs per thread: rows, cols
 constexpr int ST_ROWS = ST_TY * ST_RPT;    // 32 output rows per CTA
 constexpr int ST_COLS = ST_TX * ST_CPT;    // 128 output cols per CTA
 

@@ -385,7 +385,7 @@ def test_line_filter_kernel_vs_oracle(kind, dims, devices):
         else:
             t = orc.vfilter_tilers(F, H, W)
             w = orc.vfilter_weights()
-            expect = "tile_filter.line_14x4"
+            expect = "tile_filter.line_14x4_vstrip"
     assert _plan([t["x"], t["y"]]) == expect
     x = np.random.default_rng(F * H * W).random(int(np.prod(t["x"]["array"]))).astype(np.float32)
     got, ref = _filter_case("tile_filter", t, w, x, devices)
