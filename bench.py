@@ -490,8 +490,118 @@ class SweepWorkload(Workload):
                 "sample": f"T={Ts} repetitions of the main point, oracle/aol_oracle.c tile_copy, {dt:.2f} s"}
 
 
+def _poisson_2d(k: int):
+    """Five-point Poisson CSR (rows sorted), the reference's generator restated (refexec.py:330-347)."""
+    n = k * k
+    idx = np.arange(n, dtype=np.int64)
+    gi, gj = idx // k, idx % k
+    rows, cols, vals = [idx], [idx], [np.full(n, 4.0)]
+    for di, dj in ((-1, 0), (1, 0), (0, -1), (0, 1)):
+        ok = (gi + di >= 0) & (gi + di < k) & (gj + dj >= 0) & (gj + dj < k)
+        rows.append(idx[ok])
+        cols.append((gi[ok] + di) * k + gj[ok] + dj)
+        vals.append(np.full(int(ok.sum()), -1.0))
+    r, c, v = np.concatenate(rows), np.concatenate(cols), np.concatenate(vals)
+    order = np.lexsort((c, r))
+    r, c, v = r[order], c[order], v[order]
+    rowptr = np.zeros(n + 1, np.int32)
+    np.cumsum(np.bincount(r, minlength=n), out=rowptr[1:])
+    return n, rowptr, c.astype(np.int32), v
+
+
+def _resize_model_dict(d: dict, n_old: int, nnz_old: int, n: int, nnz: int) -> dict:
+    """instantiate_for_matrix (refexec.py:552-596) restated on the plain-data model."""
+    import copy
+    d = copy.deepcopy(d)
+
+    def m(x):
+        return nnz if x == nnz_old else n if x == n_old else n + 1 if x == n_old + 1 else x
+    for c in d["application_components"]:
+        for p in c["ports"]:
+            if p[2] is not None:
+                p[2] = [m(v) for v in p[2]]
+        if c["repetition_space"] is not None:
+            c["repetition_space"] = [m(v) for v in c["repetition_space"]]
+    return d
+
+
+class CGWorkload(Workload):
+    """Row f1 / the paper's case study: CG (cg.gmodel, resized) on a 2-D Poisson matrix, n ~ 132k.
+
+    One step = one full solve to relres <= 1e-10 through execute_schedule's interpreter
+    (LoopStep, host scalar ops, dot partials combined in device order).  Reported like
+    the paper's Table 1: GFLOP/s over the solve."""
+
+    name = "cg"
+    unit = "GFLOP/s"
+
+    def __init__(self, torch, device, rank, world, k=364):
+        from paper_1105_4424_b200.executor import Executor
+        from paper_1105_4424_b200.model import model_from_dict
+        from paper_1105_4424_b200.partition import build_schedule
+        meta = json.loads((ROOT / "tests" / "golden" / "reference_golden.json").read_text())
+        base = meta["cg_k20"]["model"]
+        n, rowptr, colidx, vals = _poisson_2d(k)
+        self.n, self.nnz = n, int(rowptr[-1])
+        self.model = model_from_dict(_resize_model_dict(base, 400, 1920, n, self.nnz))
+        self.schedule = build_schedule(self.model, 1)
+        self.bind = {"rowptr": rowptr, "colidx": colidx, "values": vals, "b": np.ones(n)}
+        self.torch, self.device = torch, device
+        ex = Executor(self.model, self.schedule, self.bind, 1)
+        ex.run()
+        torch.cuda.synchronize()
+        self.iters = ex.iterations
+        self.flop = self.iters * (2 * self.nnz + 12 * n) + 2 * n
+        self.units_per_step = self.flop / 1e9
+        self.algorithmic = {"flop_per_solve": self.flop, "iterations": self.iters,
+                            "per_unit": "per iteration 2*nnz (spmv) + 3 dots + 3 vector updates (12n)"}
+        self.workload = f"CG (bundled cg.gmodel resized) poisson_2d({k}): n={n}, nnz={self.nnz}, {self.iters} iterations"
+        self.l2 = "vectors (1 MB) fit in L2: the solve is launch- and host-sync-bound"
+        self.ex = None
+
+    def step(self):
+        from paper_1105_4424_b200.executor import Executor
+        ex = Executor(self.model, self.schedule, self.bind, 1)
+        ex.run()
+
+    def e2e_setup(self):
+        self.e2e_bytes = (sum(v.nbytes for v in self.bind.values()), self.n * 8)
+
+    def e2e_step(self):
+        from paper_1105_4424_b200.executor import execute_schedule
+        return execute_schedule(self.model, self.schedule, self.bind, 1).outputs
+
+    def e2e_free(self):
+        pass
+
+    def cpu_sample(self, seconds: float = 8.0):
+        from oracle import aol_oracle as orc
+        n = self.n
+        rp, ci, va = self.bind["rowptr"], self.bind["colidx"], self.bind["values"]
+        x = np.zeros(n)
+        r = np.ones(n)
+        p = r.copy()
+        rr = float(np.dot(r, r))
+        t0 = time.perf_counter()
+        it = 0
+        while it < 10:
+            ap = np.zeros(n)
+            orc.spmv_rows(rp, ci, va, p, ap, 0, n)
+            alpha = rr / float(np.dot(p, ap))
+            x += alpha * p
+            r += (-alpha) * ap
+            rrn = float(np.dot(r, r))
+            p *= rrn / rr
+            p += r
+            rr = rrn
+            it += 1
+        dt = (time.perf_counter() - t0) / it
+        return {"value": (2 * self.nnz + 12 * n) / dt / 1e9, "unit": "GFLOP/s", "cores": 1, "kind": "port",
+                "sample": f"10 CG iterations with the oracle's level-synchronous spmv (numpy), {dt * 1e3:.1f} ms/iter"}
+
+
 WORKLOADS = {"matmul": MatmulWorkload, "stencil": StencilWorkload, "downscaler": DownscalerWorkload,
-             "sweep": SweepWorkload}
+             "sweep": SweepWorkload, "cg": CGWorkload}
 
 
 # ---------------------------------------------------------------- the arms --
