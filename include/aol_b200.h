@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define AOL_ABI_VERSION 1
+#define AOL_ABI_VERSION 2
 #define AOL_MAX_RANK 4      /* array / repetition / pattern rank limit */
 #define AOL_MAX_TILERS 4    /* tiled ports per task */
 #define AOL_MAX_PORTS 8
@@ -54,11 +54,21 @@ typedef enum aol_op {
   AOL_OP_AXPY = 4,        /* ports: y, x;  scalars: a (if n_scalars=1)  y[i] += a*x[i] | x[i]  */
   AOL_OP_SPMV_CSR = 5,    /* ports: rowptr, colidx, values, x, y        row-wise, left to right */
   AOL_OP_DOT_PARTIAL = 6, /* ports: a, b, partial (1 element, device)   partial = sum a[i]*b[i] */
+  AOL_OP_SCALAR_DIV = 7,  /* ports: num, den, q (1 element each)        q = num / den  (host op div) */
+  AOL_OP_SCALAR_NEG = 8,  /* ports: a, z                                z = -a         (host op neg) */
+  AOL_OP_REL_RESIDUAL = 9,/* ports: num, den, z                         z = sqrt(num)/sqrt(den)      */
+  AOL_OP_PARTIALS_SUM = 10,/* ports: partials (count elements), s       s = ((p0 + p1) + p2) ... fp64,
+                              ascending device order (refexec.py:483-486); first must be 0 */
   AOL_OP_TILE_COPY = 16,  /* ports: src, dst           tilers: src, dst                        */
   AOL_OP_MATMUL = 17,     /* ports: a, b, c            tilers: a, b, c   c = sum_k a_k * b_k   */
   AOL_OP_TILE_FILTER = 18,/* ports: x, w, y            tilers: x, y      y_j = sum_i w_ji x_i  */
   AOL_OP_TILE_SUM = 19    /* ports: x, s               tilers: x, s      s = sum_i x_i         */
 } aol_op;
+
+/* flags: scalar inputs (scale/axpy `a`) are read from a device pointer appended after
+ * the vector ports instead of `scalars` — lets a whole loop body run without host
+ * round trips (CUDA-graph capture of LoopStep bodies). */
+#define AOL_FLAG_DEVICE_SCALARS 1
 
 typedef enum aol_precision {
   AOL_PREC_DEFAULT = 0,   /* matmul: TF32 tensor cores; everything else: exact order */
@@ -88,7 +98,8 @@ typedef struct aol_task {
   int32_t precision;       /* aol_precision */
   int32_t n_tilers;        /* tiled ports, in IntrinsicSpec port order */
   int32_t n_scalars;       /* host-resident scalar inputs passed by value */
-  int32_t reserved[2];
+  int32_t flags;           /* AOL_FLAG_* */
+  int32_t reserved;
   aol_tiler tilers[AOL_MAX_TILERS];
 } aol_task;
 

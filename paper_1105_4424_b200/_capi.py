@@ -16,12 +16,14 @@ import numpy as np
 from .tiler import MAX_RANK, BoundTiler
 
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libaolb200.so"
-ABI_VERSION = 1
+ABI_VERSION = 2
+FLAG_DEVICE_SCALARS = 1
 MAX_TILERS = 4
 
 AOL_OK, AOL_EINVAL, AOL_ECUDA, AOL_EUNSUPPORTED, AOL_ENODEV = 0, -1, -2, -3, -4
 DTYPE = {"float32": 0, "float64": 1, "int32": 2, "int64": 3}
 OP = {"copy": 1, "sub": 2, "scale": 3, "axpy": 4, "spmv_csr": 5, "dot_partial": 6,
+      "div": 7, "neg": 8, "rel_residual": 9, "partials_sum": 10,
       "tile_copy": 16, "matmul": 17, "tile_filter": 18, "hfilter": 18, "vfilter": 18,
       "stencil": 18, "tile_sum": 19}
 PRECISION = {"default": 0, "tf32": 1, "3xtf32": 2, "exact": 3}
@@ -52,7 +54,7 @@ class AolTiler(C.Structure):
 class AolTask(C.Structure):
     _fields_ = [("op", C.c_int32), ("dtype", C.c_int32), ("index_dtype", C.c_int32),
                 ("precision", C.c_int32), ("n_tilers", C.c_int32), ("n_scalars", C.c_int32),
-                ("reserved", C.c_int32 * 2), ("tilers", AolTiler * MAX_TILERS)]
+                ("flags", C.c_int32), ("reserved", C.c_int32), ("tilers", AolTiler * MAX_TILERS)]
 
 
 def pack_tiler(bt: BoundTiler) -> AolTiler:
@@ -74,8 +76,9 @@ def pack_tiler(bt: BoundTiler) -> AolTiler:
 
 
 def make_task(op: str, dtype: str, tilers: list[BoundTiler] = (), precision: str = "default",
-              n_scalars: int = 0, index_dtype: str = "int32") -> AolTask:
+              n_scalars: int = 0, index_dtype: str = "int32", flags: int = 0) -> AolTask:
     task = AolTask()
+    task.flags = flags
     task.op = OP[op]
     task.dtype = DTYPE[dtype]
     task.index_dtype = DTYPE[index_dtype]

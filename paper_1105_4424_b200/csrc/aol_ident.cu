@@ -32,12 +32,15 @@ __global__ void k_sub(const T* __restrict__ x, const T* __restrict__ y, T* __res
 }
 
 template <typename T>
-__global__ void k_scale(T* __restrict__ y, T a, int64_t first, int64_t count) {
+__global__ void k_scale(T* __restrict__ y, T a, const T* __restrict__ a_dev, int64_t first, int64_t count) {
+  if (a_dev) a = *a_dev;
   GRID_STRIDE(i, first, count) y[i] = mul_rn(y[i], a);
 }
 
 template <typename T>
-__global__ void k_axpy(T* __restrict__ y, const T* __restrict__ x, T a, int has_a, int64_t first, int64_t count) {
+__global__ void k_axpy(T* __restrict__ y, const T* __restrict__ x, T a, const T* __restrict__ a_dev, int has_a,
+                       int64_t first, int64_t count) {
+  if (a_dev) a = *a_dev;
   if (has_a) {
     GRID_STRIDE(i, first, count) y[i] = add_rn(y[i], mul_rn(a, x[i]));
   } else {
@@ -112,10 +115,32 @@ static double* dot_scratch(int dev) {
   return bufs[dev];
 }
 
+// Host scalar ops of the reference (refexec.py:462-474) as one-thread device kernels, so a
+// loop body runs without host round trips.  IEEE division / sqrt are correctly rounded in
+// CUDA (no fast-math), as in Python, so the results are bit-identical.
+template <typename T>
+__global__ void k_scalar_div(const T* num, const T* den, T* q) {
+  q[0] = (T)((double)num[0] / (double)den[0]);
+}
+template <typename T>
+__global__ void k_scalar_neg(const T* a, T* z) { z[0] = -a[0]; }
+template <typename T>
+__global__ void k_rel_residual(const T* num, const T* den, T* z) {
+  z[0] = (T)(sqrt((double)num[0]) / sqrt((double)den[0]));
+}
+// dot_partial combine: total = 0.0; total += p for p in partials (refexec.py:483-486)
+template <typename T>
+__global__ void k_partials_sum(const T* p, int n, T* s) {
+  double total = 0.0;
+  for (int i = 0; i < n; ++i) total = __dadd_rn(total, (double)p[i]);
+  s[0] = (T)total;
+}
+
 template <typename T>
 static int launch_ident_t(const aol_task& t, int64_t first, int64_t count, void* const* ports,
                           const double* scalars, cudaStream_t s) {
   const unsigned g = grid_for(count, 1024, 16);
+  const bool dev_scalars = (t.flags & AOL_FLAG_DEVICE_SCALARS) != 0;
   switch (t.op) {
     case AOL_OP_COPY:
       k_copy<T><<<g, 256, 0, s>>>((const T*)ports[0], (T*)ports[1], first, count);
@@ -123,13 +148,30 @@ static int launch_ident_t(const aol_task& t, int64_t first, int64_t count, void*
     case AOL_OP_SUB:
       k_sub<T><<<g, 256, 0, s>>>((const T*)ports[0], (const T*)ports[1], (T*)ports[2], first, count);
       break;
-    case AOL_OP_SCALE:
-      if (t.n_scalars < 1 || !scalars) return fail(AOL_EINVAL, "scale needs scalar a");
-      k_scale<T><<<g, 256, 0, s>>>((T*)ports[0], (T)scalars[0], first, count);
+    case AOL_OP_SCALE: {
+      const T* a_dev = dev_scalars ? (const T*)ports[1] : nullptr;
+      if (!a_dev && (t.n_scalars < 1 || !scalars)) return fail(AOL_EINVAL, "scale needs scalar a");
+      k_scale<T><<<g, 256, 0, s>>>((T*)ports[0], a_dev ? T(0) : (T)scalars[0], a_dev, first, count);
       break;
-    case AOL_OP_AXPY:
-      k_axpy<T><<<g, 256, 0, s>>>((T*)ports[0], (const T*)ports[1], t.n_scalars > 0 ? (T)scalars[0] : T(0),
+    }
+    case AOL_OP_AXPY: {
+      const T* a_dev = (dev_scalars && t.n_scalars > 0) ? (const T*)ports[2] : nullptr;
+      k_axpy<T><<<g, 256, 0, s>>>((T*)ports[0], (const T*)ports[1],
+                                  (t.n_scalars > 0 && !a_dev) ? (T)scalars[0] : T(0), a_dev,
                                   t.n_scalars > 0 ? 1 : 0, first, count);
+      break;
+    }
+    case AOL_OP_SCALAR_DIV:
+      k_scalar_div<T><<<1, 1, 0, s>>>((const T*)ports[0], (const T*)ports[1], (T*)ports[2]);
+      break;
+    case AOL_OP_SCALAR_NEG:
+      k_scalar_neg<T><<<1, 1, 0, s>>>((const T*)ports[0], (T*)ports[1]);
+      break;
+    case AOL_OP_REL_RESIDUAL:
+      k_rel_residual<T><<<1, 1, 0, s>>>((const T*)ports[0], (const T*)ports[1], (T*)ports[2]);
+      break;
+    case AOL_OP_PARTIALS_SUM:
+      k_partials_sum<T><<<1, 1, 0, s>>>((const T*)ports[0], (int)count, (T*)ports[1]);
       break;
     case AOL_OP_SPMV_CSR: {
       const unsigned gs = grid_for(count, 256, 32);

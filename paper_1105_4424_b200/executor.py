@@ -180,7 +180,8 @@ class Executor:
     """Prepared schedule: storage resident in HBM, tasks validated, ready to run repeatedly."""
 
     def __init__(self, model, schedule, bindings: dict, device_count: int, *, tilers: dict | None = None,
-                 precision: str = "default", device=None, stream=None, pipeline: int = 0, fuse: bool = False):
+                 precision: str = "default", device=None, stream=None, pipeline: int = 0, fuse: bool = False,
+                 graphs: bool = False):
         torch = _torch()
         _capi.load()
         if not torch.cuda.is_available():
@@ -200,6 +201,11 @@ class Executor:
             self.storage = DeviceStorage(model, bindings, self.device, stream, defer=bool(self.pipeline))
         self._tasks: dict[str, _Task] = {}
         self.fuse = fuse
+        self.graphs = graphs
+        self._graphs: dict[str, object] = {}
+        self._gbufs: dict[str, object] = {}
+        self._dev_tasks: dict[str, object] = {}
+        self.graph_replays = 0
         self._fusable: dict[tuple, bool] = {}
         self.fused_launches = 0
         self._dot_buf = None
@@ -379,6 +385,74 @@ class Executor:
         comp.synchronize()
         return {n: (out[n] if out is not None and n in out else h.numpy()) for n, h in hosts.items()}
 
+    # -- CUDA-graph loop bodies -----------------------------------------------------
+    _GRAPH_HOST_OPS = ("div", "neg", "rel_residual")
+
+    def _graphable(self, body) -> bool:
+        for st in body:
+            if hasattr(st, "body"):
+                return False
+            if not hasattr(st, "launches") and st.op not in self._GRAPH_HOST_OPS:
+                return False
+        return True
+
+    def _dev_task(self, step):
+        """Device-resident variant of a step's task: host scalar ops as kernels, scalar inputs by pointer."""
+        d = self._dev_tasks.get(step.task_path)
+        if d is None:
+            t = self.task(step.task_path)
+            if not hasattr(step, "launches"):
+                dt = enum_value(t.comp.ports[0].data_type)
+                d = (_capi.make_task(step.op, dt), [ps.name for ps in t.spec.ports])
+            elif step.op in ("scale", "axpy") and t.scalar_ports:
+                d = (_capi.make_task(step.op, t.dtype, n_scalars=len(t.scalar_ports),
+                                     flags=_capi.FLAG_DEVICE_SCALARS), t.port_order + t.scalar_ports)
+            else:
+                d = (t.ctask, t.port_order)
+            self._dev_tasks[step.task_path] = d
+        return d
+
+    def _run_body_device(self, body) -> None:
+        """Enqueue one loop iteration with no host round trip (capturable)."""
+        torch = _torch()
+        s = self._stream_handle()
+        for step in body:
+            t = self.task(step.task_path)
+            arrays = {name: self.storage.array(node) for name, node in t.nodes.items()}
+            if step.op == "dot_partial":
+                buf = self._gbufs[step.task_path]
+                for i, l in enumerate(step.launches):
+                    _capi.launch(t.ctask, l.range.offset, l.range.count,
+                                 [arrays["a"].data_ptr(), arrays["b"].data_ptr(),
+                                  buf.data_ptr() + i * buf.element_size()], (), s)
+                ctask = _capi.make_task("partials_sum", t.dtype)
+                _capi.launch(ctask, 0, len(step.launches), [buf.data_ptr(), arrays["s"].data_ptr()], (), s)
+                continue
+            ctask, names = self._dev_task(step)
+            ptrs = [arrays[n].data_ptr() for n in names]
+            if not hasattr(step, "launches"):
+                _capi.launch(ctask, 0, 1, ptrs, (), s)
+                continue
+            for l in step.launches:
+                _capi.launch(ctask, l.range.offset, l.range.count, ptrs, (), s)
+
+    def _loop_graph(self, step):
+        torch = _torch()
+        g = self._graphs.get(step.task_path)
+        if g is None:
+            for st in step.body:
+                if getattr(st, "op", None) == "dot_partial":
+                    t = self.task(st.task_path)
+                    self._gbufs[st.task_path] = torch.zeros(max(8, len(st.launches)),
+                                                            dtype=torch_dtype(t.dtype), device=self.device)
+                self._dev_task(st) if not (getattr(st, "op", None) == "dot_partial") else None
+            torch.cuda.synchronize(self.device)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._run_body_device(step.body)
+            self._graphs[step.task_path] = g
+        return g
+
     # -- task fusion ---------------------------------------------------------------
     def _fusion_candidate(self, s1, s2) -> bool:
         """s1's filter output feeds s2's filter input through a group nobody else touches."""
@@ -427,8 +501,13 @@ class Executor:
                 loop_max = max_iter if max_iter is not None else step.max_iterations
                 done = False
                 n = 0
+                graph = self._loop_graph(step) if (self.graphs and self._graphable(step.body)) else None
                 while True:
-                    self.run_steps(step.body, tol, max_iter)
+                    if graph is not None:
+                        graph.replay()
+                        self.graph_replays += 1
+                    else:
+                        self.run_steps(step.body, tol, max_iter)
                     n += 1
                     self.iterations += 1
                     relres = float(self.storage.array(step.relres_port)[0].item())
@@ -480,10 +559,11 @@ class Executor:
 def execute_schedule(model, schedule, bindings: dict, device_count: int, tol: float | None = None,
                      max_iter: int | None = None, *, tilers: dict | None = None, precision: str = "default",
                      device_outputs: bool = False, out: dict | None = None, device=None,
-                     stream=None, pipeline: int = 0, fuse: bool = False) -> ExecutionResult:
+                     stream=None, pipeline: int = 0, fuse: bool = False, graphs: bool = False) -> ExecutionResult:
     """Interpret ``schedule`` on the B200 with ``device_count`` launch shards per device step."""
     ex = Executor(model, schedule, bindings, device_count, tilers=tilers, precision=precision,
-                  device=device, stream=stream, pipeline=0 if device_outputs else pipeline, fuse=fuse)
+                  device=device, stream=stream, pipeline=0 if device_outputs else pipeline, fuse=fuse,
+                  graphs=graphs)
     if ex.pipeline:
         torch = _torch()
         with torch.cuda.device(ex.device):

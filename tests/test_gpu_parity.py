@@ -606,3 +606,24 @@ def test_fused_downscaler_bitwise(F, H, W, devices):
     want = orc.run_tile_task("vfilter", tv, {"x": mid, "w": wv}, {"y": (ny, np.float32)},
                              int(np.prod(tv["x"]["rep"])), 1)["y"]
     assert np.array_equal(fused.view(np.uint32), want.view(np.uint32))
+
+
+@pytest.mark.parametrize("devices", [1, 4])
+def test_cg_graph_mode_equals_eager(golden, devices):
+    """LoopStep body captured once as a CUDA graph (device scalar ops, ordered partial sums):
+    bit-identical to the eager interpreter, and to the reference's iteration count."""
+    from paper_1105_4424_b200.executor import Executor
+    from paper_1105_4424_b200.model import model_from_dict
+    from paper_1105_4424_b200.partition import build_schedule
+    data, meta = golden
+    m = meta["cg_k20"]
+    model = model_from_dict(m["model"])
+    bind = {k: data[f"cg_k20/{k}"] for k in ("rowptr", "colidx", "values", "b")}
+    sched = build_schedule(model, devices)
+    eager = Executor(model, sched, bind, devices)
+    eager.run()
+    gr = Executor(model, sched, bind, devices, graphs=True)
+    gr.run()
+    assert gr.graph_replays == gr.iterations == eager.iterations == m["runs"][str(devices)]["iterations"]
+    assert np.array_equal(gr.outputs()["x"], eager.outputs()["x"])
+    assert gr.final_relres == eager.final_relres
