@@ -555,13 +555,16 @@ class CGWorkload(Workload):
         self.units_per_step = self.flop / 1e9
         self.algorithmic = {"flop_per_solve": self.flop, "iterations": self.iters,
                             "per_unit": "per iteration 2*nnz (spmv) + 3 dots + 3 vector updates (12n)"}
-        self.workload = f"CG (bundled cg.gmodel resized) poisson_2d({k}): n={n}, nnz={self.nnz}, {self.iters} iterations"
+        self.workload = (f"CG (bundled cg.gmodel resized) poisson_2d({k}): n={n}, nnz={self.nnz}, {self.iters} "
+                         f"iterations; loop body replayed as one CUDA graph per iteration (setup + capture timed)")
         self.l2 = "vectors (1 MB) fit in L2: the solve is launch- and host-sync-bound"
         self.ex = None
 
+    graphs = True
+
     def step(self):
         from paper_1105_4424_b200.executor import Executor
-        ex = Executor(self.model, self.schedule, self.bind, 1)
+        ex = Executor(self.model, self.schedule, self.bind, 1, graphs=self.graphs)
         ex.run()
 
     def e2e_setup(self):
@@ -569,7 +572,7 @@ class CGWorkload(Workload):
 
     def e2e_step(self):
         from paper_1105_4424_b200.executor import execute_schedule
-        return execute_schedule(self.model, self.schedule, self.bind, 1).outputs
+        return execute_schedule(self.model, self.schedule, self.bind, 1, graphs=self.graphs).outputs
 
     def e2e_free(self):
         pass
