@@ -43,6 +43,7 @@ struct Params {
   int64_t first, last; // inclusive linear repetition range
   int m_tiles, n_tiles, k_blocks, num_tiles;
   int c_vec;           // 16-byte stores allowed
+  int group_m;         // tile raster: M-tiles per group sharing each B panel
   uint32_t* dbg;       // debug: first smem stage (48 KB) is copied here when non-null
 };
 
@@ -351,10 +352,10 @@ __device__ __forceinline__ void load_operand_pair(const CUtensorMap* map, uint32
 }
 
 __device__ __forceinline__ void tile_coords_pair(const Params& p, int tile, int& mt, int& nt) {
-  const int per_group = GROUP_M * p.n_tiles;
+  const int per_group = p.group_m * p.n_tiles;
   const int g = tile / per_group;
-  const int first_m = g * GROUP_M;
-  const int gm = min(GROUP_M, p.m_tiles - first_m);
+  const int first_m = g * p.group_m;
+  const int gm = min(p.group_m, p.m_tiles - first_m);
   const int in = tile - g * per_group;
   mt = first_m + in % gm;
   nt = in / gm;
@@ -690,6 +691,8 @@ static int gemm_core(const float* A, const float* B, float* C, const GemmShape& 
     else rc = make_map(&ma2, A, g.M, g.K, g.lda, 32, BK, false);
     if (rc) return rc;
     Params pp = p;
+    static const int gm_env = getenv("AOL_GEMM_GROUP_M") ? atoi(getenv("AOL_GEMM_GROUP_M")) : 0;
+    pp.group_m = gm_env > 0 ? gm_env : 8;
     pp.m_tiles = (int)((p.m_hi - p.m_lo + pair::BM) / pair::BM);
     pp.n_tiles = (int)((g.N + pair::BN - 1) / pair::BN);
     pp.num_tiles = pp.m_tiles * pp.n_tiles;
