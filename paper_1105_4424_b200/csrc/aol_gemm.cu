@@ -44,7 +44,6 @@ struct Params {
   int m_tiles, n_tiles, k_blocks, num_tiles;
   int c_vec;           // 16-byte stores allowed
   int group_m;         // tile raster: M-tiles per group sharing each B panel
-  uint32_t* dbg;       // debug: first smem stage (48 KB) is copied here when non-null
 };
 
 // ------------------------------------------------------------ PTX helpers ----
@@ -222,10 +221,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          if (p.dbg && tile == (int)blockIdx.x && kb == 0 && blockIdx.x == 0) {
-            const uint32_t* src = reinterpret_cast<const uint32_t*>(smem + stage * STAGE_BYTES);
-            for (int i = 0; i < STAGE_BYTES / 4; ++i) p.dbg[i] = src[i];
-          }
           const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
           const uint32_t sb = sa + A_BYTES;
 #pragma unroll
@@ -677,7 +672,6 @@ static int gemm_core(const float* A, const float* B, float* C, const GemmShape& 
   p.k_blocks = (int)((g.K + BK - 1) / BK);
   p.num_tiles = p.m_tiles * p.n_tiles;
   p.c_vec = ((uintptr_t)C % 16 == 0) && (g.ldc % 4 == 0);
-  if (const char* dbg = getenv("AOL_GEMM_DBG")) p.dbg = reinterpret_cast<uint32_t*>(strtoull(dbg, nullptr, 10));
 
   static const bool force_1sm = getenv("AOL_GEMM_1SM") != nullptr;
   if (!force_1sm) {

@@ -627,3 +627,65 @@ def test_cg_graph_mode_equals_eager(golden, devices):
     assert gr.graph_replays == gr.iterations == eager.iterations == m["runs"][str(devices)]["iterations"]
     assert np.array_equal(gr.outputs()["x"], eager.outputs()["x"])
     assert gr.final_relres == eager.final_relres
+
+
+def _rand_tiler(rng, arr=None, rep=None, pat=None):
+    a = len(arr) if arr else int(rng.integers(1, 4))
+    arr = arr or tuple(int(x) for x in rng.integers(2, 12, a))
+    q = len(rep) if rep else int(rng.integers(1, 4))
+    rep = rep or tuple(int(x) for x in rng.integers(1, 7, q))
+    p = len(pat) if pat else int(rng.integers(1, 3))
+    pat = pat or tuple(int(x) for x in rng.integers(1, 5, p))
+    return dict(array=arr, rep=rep, pattern=pat, origin=tuple(int(x) for x in rng.integers(-30, 30, a)),
+                paving=tuple(tuple(int(x) for x in rng.integers(-6, 7, q)) for _ in range(a)),
+                fitting=tuple(tuple(int(x) for x in rng.integers(-4, 5, p)) for _ in range(a)))
+
+
+def _dense_out(rep, pat):
+    R, P = int(np.prod(rep)), int(np.prod(pat))
+    q = len(rep)
+    return dict(array=(R * P,), rep=rep, pattern=pat, origin=(0,),
+                paving=(tuple(int(np.prod(rep[j + 1:])) * P for j in range(q)),),
+                fitting=(tuple(int(np.prod(pat[k + 1:])) for k in range(len(pat))),))
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_tilers_all_tile_ops_vs_oracle(seed):
+    """Random gather tilers (toroidal, negative strides, ranks 1-3) through every tile intrinsic."""
+    rng = np.random.default_rng(1000 + seed)
+    for _ in range(6):
+        tx = _rand_tiler(rng)
+        rep, pat = tx["rep"], tx["pattern"]
+        R, P = int(np.prod(rep)), int(np.prod(pat))
+        nx = int(np.prod(tx["array"]))
+        x = (rng.random(nx) * 4).astype(np.float32)
+        d = int(rng.integers(1, 5))
+        # tile_copy
+        td = _dense_out(rep, pat)
+        ports = {"src": _spec(tx, "in", "float32"), "dst": _spec(td, "out", "float32")}
+        got = _run_tile("tile_copy", {"src": tx, "dst": td}, ports, {"src": x}, d).outputs["p_dst"]
+        ref = orc.run_tile_task("tile_copy", {"src": tx, "dst": td}, {"src": x}, {"dst": (R * P, np.float32)}, R, d)
+        assert np.array_equal(got, ref["dst"]), ("copy", tx)
+        # tile_filter with 1..3 outputs per pattern
+        py = int(rng.integers(1, 4))
+        ty = _dense_out(rep, (py,))
+        w = rng.standard_normal(py * P).astype(np.float32)
+        ports = {"x": _spec(tx, "in", "float32"), "w": f"in float32 [{w.size}]", "y": _spec(ty, "out", "float32")}
+        got = _run_tile("tile_filter", {"x": tx, "y": ty}, ports, {"x": x, "w": w}, d).outputs["p_y"]
+        ref = orc.run_tile_task("tile_filter", {"x": tx, "y": ty}, {"x": x, "w": w}, {"y": (R * py, np.float32)}, R, d)
+        assert np.array_equal(got.view(np.uint32), ref["y"].view(np.uint32)), ("filter", tx)
+        # tile_sum
+        ts = _dense_out(rep, (1,))
+        ports = {"x": _spec(tx, "in", "float32"), "s": _spec(ts, "out", "float32")}
+        got = _run_tile("tile_sum", {"x": tx, "s": ts}, ports, {"x": x}, d).outputs["p_s"]
+        ref = orc.run_tile_task("tile_sum", {"x": tx, "s": ts}, {"x": x}, {"s": (R, np.float32)}, R, d)
+        assert np.array_equal(got.view(np.uint32), ref["s"].view(np.uint32)), ("sum", tx)
+        # matmul (generic path): a second random tiler over the same repetition space and pattern
+        tb = _rand_tiler(rng, rep=rep, pat=pat)
+        nb = int(np.prod(tb["array"]))
+        b = (rng.random(nb) * 4).astype(np.float32)
+        tc = _dense_out(rep, (1,))
+        ports = {"a": _spec(tx, "in", "float32"), "b": _spec(tb, "in", "float32"), "c": _spec(tc, "out", "float32")}
+        got = _run_tile("matmul", {"a": tx, "b": tb, "c": tc}, ports, {"a": x, "b": b}, d).outputs["p_c"]
+        ref = orc.run_tile_task("matmul", {"a": tx, "b": tb, "c": tc}, {"a": x, "b": b}, {"c": (R, np.float32)}, R, d)
+        assert np.array_equal(got.view(np.uint32), ref["c"].view(np.uint32)), ("matmul", tx, tb)

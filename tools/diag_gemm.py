@@ -40,12 +40,3 @@ out["a3"], out["b3"], out["c3"] = A3, B3, run(A3, B3)
 np.savez("gpurun_out/diag_gemm.npz", **out)
 print("saved")
 
-# smem stage dump of the first k-block
-import os
-dbg = torch.zeros(48 * 1024 // 4, dtype=torch.int32, device="cuda")
-os.environ["AOL_GEMM_DBG"] = str(dbg.data_ptr())
-out["c4"] = run(A1, B1)
-out["dbg"] = dbg.cpu().numpy().view(np.float32)
-out["a1"], out["b1"] = A1, B1
-np.savez("gpurun_out/diag_gemm.npz", **out)
-print("saved dbg")
