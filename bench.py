@@ -394,8 +394,8 @@ class SweepWorkload(Workload):
         self.max_out = max_out_bytes
         self.points = []
         for m in self.POINTS_M:
-            for kind in ("dense", "overlap", "gaps", "strided"):
-                if kind in ("overlap", "strided") and m == 1:
+            for kind in ("dense", "overlap", "gaps", "strided", "rowstride"):
+                if kind in ("overlap", "strided", "rowstride") and m == 1:
                     continue
                 for T in (10 ** 3, 10 ** 5, 10 ** 7, 10 ** 8, 10 ** 9):
                     if T * m * 4 > self.max_out:
@@ -413,11 +413,16 @@ class SweepWorkload(Workload):
     def _make(self, m, kind, T):
         from paper_1105_4424_b200 import Tiler, _capi
         torch = self.torch
-        p = {"dense": m, "overlap": max(1, m // 2), "gaps": 2 * m, "strided": m * 2}[kind]
-        f = 2 if kind == "strided" else 1
-        span = (T - 1) * p + (m - 1) * f + 1
-        distinct = span if (kind == "overlap") else T * m
-        src = Tiler((0,), ((p,),), ((f,),), (m,)).bind((span,), (T,))
+        if kind == "rowstride":
+            # array [m, T] row-major: repetition r walks a row, pattern i walks down a column
+            span, distinct = m * T, m * T
+            src = Tiler((0, 0), ((0,), (1,)), ((1,), (0,)), (m,)).bind((m, T), (T,))
+        else:
+            p = {"dense": m, "overlap": max(1, m // 2), "gaps": 2 * m, "strided": m * 2}[kind]
+            f = 2 if kind == "strided" else 1
+            span = (T - 1) * p + (m - 1) * f + 1
+            distinct = span if (kind == "overlap") else T * m
+            src = Tiler((0,), ((p,),), ((f,),), (m,)).bind((span,), (T,))
         dst = Tiler((0,), ((m,),), ((1,),), (m,)).bind((T * m,), (T,))
         x = torch.empty(span, device=self.device).uniform_()
         y = torch.empty(T * m, device=self.device)

@@ -14,6 +14,7 @@
 // run read with float4 when aligned and not wrapping.  inner > 1 (vertical filter,
 // e.g. 14 taps paving 9): consecutive threads take consecutive i, so every tap is a
 // coalesced row read and every output a coalesced row write.
+#include <cstdlib>
 #include <cstring>
 
 #include "aol_common.cuh"
@@ -177,7 +178,7 @@ __global__ void __launch_bounds__(256) k_line_filter(const float* __restrict__ x
 // (outer, inner) column.  Their windows overlap (px > sx), so the (REPS-1)*sx + px rows are
 // loaded once into registers; every output is still summed over its own taps in order.
 template <int PX, int PY, int SX, int REPS>
-__global__ void __launch_bounds__(256) k_line_filter_vstrip(const float* __restrict__ x, const float* __restrict__ w,
+__global__ void __launch_bounds__(256, (REPS <= 2 ? 4 : 3)) k_line_filter_vstrip(const float* __restrict__ x, const float* __restrict__ w,
                                                             float* __restrict__ y, LineGeom g, int64_t first,
                                                             int64_t last, int64_t o_lo, int64_t ngroups) {
   constexpr int NRW = (REPS - 1) * SX + PX;
@@ -239,14 +240,20 @@ int launch_line_filter(const aol_task& t, const LineGeom& g, int64_t first, int6
   // 32-bit offsets whenever both arrays fit (every in-range offset < 2^32)
   const bool idx32 = g.outer * g.Sx * g.inner < (1ll << 32) && g.outer * g.Sy * g.inner < (1ll << 32);
   if (idx32 && g.inner > 1 && g.px == 14 && g.py == 4 && g.sx == 9 && g.Sx * g.inner < (1ll << 32)) {
-    constexpr int REPS = 4;
+    static const int reps_env = getenv("AOL_VSTRIP_REPS") ? atoi(getenv("AOL_VSTRIP_REPS")) : 0;
+    const int REPS = reps_env >= 2 && reps_env <= 4 ? reps_env : 4;
     const int64_t last = first + count - 1;
     const int64_t NLG = (g.NL + REPS - 1) / REPS;
     // repetition groups intersecting [first, last]
     const int64_t o_lo = first / (g.NL * g.inner), o_hi = last / (g.NL * g.inner);
     const int64_t ngroups = (o_hi - o_lo + 1) * NLG * g.inner;
-    k_line_filter_vstrip<14, 4, 9, REPS><<<grid_for(ngroups, 256, 8), 256, 0, s>>>(x, w, y, g, first, last, o_lo,
-                                                                                    ngroups);
+    const unsigned grid = grid_for(ngroups, 256, 8);
+    if (REPS == 2)
+      k_line_filter_vstrip<14, 4, 9, 2><<<grid, 256, 0, s>>>(x, w, y, g, first, last, o_lo, ngroups);
+    else if (REPS == 3)
+      k_line_filter_vstrip<14, 4, 9, 3><<<grid, 256, 0, s>>>(x, w, y, g, first, last, o_lo, ngroups);
+    else
+      k_line_filter_vstrip<14, 4, 9, 4><<<grid, 256, 0, s>>>(x, w, y, g, first, last, o_lo, ngroups);
     AOL_LAUNCH_CHECK("k_line_filter_vstrip");
     return AOL_OK;
   }

@@ -243,6 +243,36 @@ __global__ void __launch_bounds__(256) k_tile_copy_vec(const T* __restrict__ src
   }
 }
 
+// "Row-stride" gathers: consecutive repetitions are adjacent in the source (As == 1) while
+// the pattern elements are far apart (one array row, Bs >= 32); the destination is the dense
+// pattern stream.  A 32x32 (repetition x pattern) tile goes through padded shared memory so
+// both the source reads (along repetitions) and the destination writes (along the stream)
+// are coalesced — the classic transpose.
+template <typename T>
+__global__ void __launch_bounds__(256) k_tile_copy_transpose(const T* __restrict__ src, T* __restrict__ dst,
+                                                             int64_t cs, int64_t Bs, int64_t cd, int64_t P,
+                                                             int64_t first, int64_t count) {
+  __shared__ T tile[32][33];
+  const int64_t nrb = (count + 31) / 32, npb = (P + 31) / 32;
+  for (int64_t b = blockIdx.x; b < nrb * npb; b += gridDim.x) {
+    const int64_t rb = b / npb, pb = b - rb * npb;
+    const int64_t r0 = first + rb * 32, p0 = pb * 32;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int pl = threadIdx.y + 8 * k;
+      const int64_t rho = r0 + threadIdx.x, iota = p0 + pl;
+      if (rho < first + count && iota < P) tile[pl][threadIdx.x] = __ldg(src + cs + rho + Bs * iota);
+    }
+    __syncthreads();
+    const int64_t pw = P - p0 < 32 ? P - p0 : 32, rw = first + count - r0 < 32 ? first + count - r0 : 32;
+    for (int k = threadIdx.y * 32 + threadIdx.x; k < pw * rw; k += 256) {
+      const int rl = (int)(k / pw), pl = (int)(k - rl * pw);
+      dst[cd + (r0 + rl) * P + p0 + pl] = tile[pl][rl];
+    }
+  }
+}
+
 // Contiguous on both sides: a streaming copy with 16-byte vectors.
 __global__ void __launch_bounds__(256) k_stream_copy16(const uint4* __restrict__ src, uint4* __restrict__ dst,
                                                        int64_t n16) {
@@ -494,7 +524,7 @@ static bool collapse(const int64_t* coef, const int64_t* dims, int n, int64_t& s
 }
 
 struct CopyPlan {
-  int kind;  // 0 generic, 1 affine1, 2 stream, 3 vector (V elements / thread)
+  int kind;  // 0 generic, 1 affine1, 2 stream, 3 vector (V elements / thread), 4 transpose
   int64_t cs, As, Bs, cd, Ad, Bd;
   int V;
   bool src_vec;
@@ -519,6 +549,11 @@ static CopyPlan plan_tile_copy(const aol_tiler& ts, const aol_tiler& td, int64_t
     p.kind = 2;
     return p;
   }
+  // row-stride gather into a dense stream: transpose through shared memory
+  if (p.As == 1 && P > 1 && (p.Bs >= 32 || p.Bs <= -32) && p.Ad == P && p.Bd == 1) {
+    p.kind = 4;
+    return p;
+  }
   // vector path: destination contiguous within the pattern, V | P, V-aligned offsets
   // prefer the widest V that also vectorises the source; else the widest store-only V
   for (int pass = 0; pass < 2 && p.kind != 3; ++pass) {
@@ -539,6 +574,7 @@ static CopyPlan plan_tile_copy(const aol_tiler& ts, const aol_tiler& td, int64_t
 const char* tile_copy_plan_name(const aol_tiler& ts, const aol_tiler& td, int64_t first, int64_t count) {
   const CopyPlan pl = plan_tile_copy(ts, td, first, count);
   switch (pl.kind) {
+    case 4: return "tile_copy.transpose";
     case 3: return pl.src_vec ? "tile_copy.vec" : "tile_copy.vec_store";
     case 2: return "tile_copy.stream16";
     case 1: return "tile_copy.affine";
@@ -580,6 +616,13 @@ static int launch_tile_copy_t(const aol_tiler& ts, const aol_tiler& td, int64_t 
       return AOL_OK;
     }
     p.kind = 1;
+  }
+  if (p.kind == 4) {
+    const int64_t tiles = ((count + 31) / 32) * ((P + 31) / 32);
+    k_tile_copy_transpose<T><<<(unsigned)std::min<int64_t>(tiles, (int64_t)kNumSMs * 16), dim3(32, 8), 0, stream>>>(
+        s, d, p.cs, p.Bs, p.cd, P, first, count);
+    AOL_LAUNCH_CHECK("k_tile_copy_transpose");
+    return AOL_OK;
   }
   if (p.kind == 3) {
     int V = p.V;

@@ -142,6 +142,8 @@ def test_tiler_offsets_random_vs_loop_oracle():
     ((4096,), (1023,), (4,), ((2,),), ((1,),), (2,)),           # overlap -> vec (V=2 loads)
     ((8192,), (1000,), (4,), ((8,),), ((2,),), (0,)),           # strided fitting -> vec_store
     ((8192,), (999,), (6,), ((7,),), ((1,),), (1,)),            # odd stride -> vec (V=2) or affine
+    ((40, 1000), (1000,), (40,), ((0,), (1,)), ((1,), (0,)), (0, 0)),   # row stride -> transpose
+    ((7, 3000), (2999,), (7,), ((0,), (1,)), ((1,), (0,)), (0, 1)),     # row stride, ragged -> transpose
 ])
 @pytest.mark.parametrize("devices", [1, 3])
 @pytest.mark.parametrize("dtype", ["float32", "float64"])
