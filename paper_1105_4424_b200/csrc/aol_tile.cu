@@ -251,24 +251,29 @@ __global__ void __launch_bounds__(256) k_tile_copy_vec(const T* __restrict__ src
 template <typename T>
 __global__ void __launch_bounds__(256) k_tile_copy_transpose(const T* __restrict__ src, T* __restrict__ dst,
                                                              int64_t cs, int64_t Bs, int64_t cd, int64_t P,
-                                                             int64_t first, int64_t count) {
-  __shared__ T tile[32][33];
-  const int64_t nrb = (count + 31) / 32, npb = (P + 31) / 32;
+                                                             int64_t first, int64_t count, int pc, int rshift,
+                                                             FastDiv32 pcdiv) {
+  // tile = (1 << rshift) repetitions x pc pattern elements (pc <= 32, pc * 2^rshift <= 1024+)
+  __shared__ T tile[1024 + 64];
+  const int rt = 1 << rshift;
+  const int pitch = rt + 1;
+  const int64_t nrb = (count + rt - 1) / rt, npb = (P + pc - 1) / pc;
   for (int64_t b = blockIdx.x; b < nrb * npb; b += gridDim.x) {
     const int64_t rb = b / npb, pb = b - rb * npb;
-    const int64_t r0 = first + rb * 32, p0 = pb * 32;
+    const int64_t r0 = first + rb * rt, p0 = pb * pc;
+    const int pw = (int)(P - p0 < pc ? P - p0 : pc);
+    const int rw = (int)(first + count - r0 < rt ? first + count - r0 : rt);
     __syncthreads();
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int pl = threadIdx.y + 8 * k;
-      const int64_t rho = r0 + threadIdx.x, iota = p0 + pl;
-      if (rho < first + count && iota < P) tile[pl][threadIdx.x] = __ldg(src + cs + rho + Bs * iota);
+    for (int k = threadIdx.x; k < pc * rt; k += blockDim.x) {      // coalesced along repetitions
+      const int pl = k >> rshift, rl = k & (rt - 1);
+      if (pl < pw && rl < rw) tile[pl * pitch + rl] = __ldg(src + cs + (r0 + rl) + Bs * (p0 + pl));
     }
     __syncthreads();
-    const int64_t pw = P - p0 < 32 ? P - p0 : 32, rw = first + count - r0 < 32 ? first + count - r0 : 32;
-    for (int k = threadIdx.y * 32 + threadIdx.x; k < pw * rw; k += 256) {
-      const int rl = (int)(k / pw), pl = (int)(k - rl * pw);
-      dst[cd + (r0 + rl) * P + p0 + pl] = tile[pl][rl];
+    for (int k = threadIdx.x; k < pw * rw; k += blockDim.x) {      // coalesced along the dense stream
+      uint32_t rl, pl;
+      if (pw == pc) pcdiv.divmod((uint32_t)k, rl, pl);
+      else { rl = (uint32_t)(k / pw); pl = (uint32_t)(k - rl * pw); }
+      dst[cd + (r0 + rl) * P + p0 + pl] = tile[pl * pitch + rl];
     }
   }
 }
@@ -618,9 +623,14 @@ static int launch_tile_copy_t(const aol_tiler& ts, const aol_tiler& td, int64_t 
     p.kind = 1;
   }
   if (p.kind == 4) {
-    const int64_t tiles = ((count + 31) / 32) * ((P + 31) / 32);
-    k_tile_copy_transpose<T><<<(unsigned)std::min<int64_t>(tiles, (int64_t)kNumSMs * 16), dim3(32, 8), 0, stream>>>(
-        s, d, p.cs, p.Bs, p.cd, P, first, count);
+    const int pc = (int)std::min<int64_t>(P, 32);
+    int pc2 = 1;
+    while (pc2 < pc) pc2 <<= 1;
+    int rshift = 0;
+    while ((1 << (rshift + 1)) * pc2 <= 1024) ++rshift;      // tile: 2^rshift x pc <= 1024 elements
+    const int64_t tiles = ((count + (1 << rshift) - 1) >> rshift) * ((P + pc - 1) / pc);
+    k_tile_copy_transpose<T><<<(unsigned)std::min<int64_t>(tiles, (int64_t)kNumSMs * 16), 256, 0, stream>>>(
+        s, d, p.cs, p.Bs, p.cd, P, first, count, pc, rshift, FastDiv32((uint32_t)pc));
     AOL_LAUNCH_CHECK("k_tile_copy_transpose");
     return AOL_OK;
   }
