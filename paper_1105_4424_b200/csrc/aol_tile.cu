@@ -253,8 +253,9 @@ __global__ void __launch_bounds__(256) k_tile_copy_transpose(const T* __restrict
                                                              int64_t cs, int64_t Bs, int64_t cd, int64_t P,
                                                              int64_t first, int64_t count, int pc, int rshift,
                                                              FastDiv32 pcdiv) {
-  // tile = (1 << rshift) repetitions x pc pattern elements (pc <= 32, pc * 2^rshift <= 1024+)
-  __shared__ T tile[1024 + 64];
+  // tile = (1 << rshift) repetitions x pc pattern elements (pc <= 32, pc * 2^rshift <= 4096)
+  constexpr int PER = 16;                          // elements per thread per tile, loaded before storing
+  __shared__ T tile[4096 + 128];
   const int rt = 1 << rshift;
   const int pitch = rt + 1;
   const int64_t nrb = (count + rt - 1) / rt, npb = (P + pc - 1) / pc;
@@ -263,10 +264,19 @@ __global__ void __launch_bounds__(256) k_tile_copy_transpose(const T* __restrict
     const int64_t r0 = first + rb * rt, p0 = pb * pc;
     const int pw = (int)(P - p0 < pc ? P - p0 : pc);
     const int rw = (int)(first + count - r0 < rt ? first + count - r0 : rt);
-    __syncthreads();
-    for (int k = threadIdx.x; k < pc * rt; k += blockDim.x) {      // coalesced along repetitions
+    T v[PER];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {                                // coalesced along repetitions
+      const int k = threadIdx.x + u * 256;
       const int pl = k >> rshift, rl = k & (rt - 1);
-      if (pl < pw && rl < rw) tile[pl * pitch + rl] = __ldg(src + cs + (r0 + rl) + Bs * (p0 + pl));
+      if (k < pc * rt && pl < pw && rl < rw) v[u] = __ldg(src + cs + (r0 + rl) + Bs * (p0 + pl));
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int k = threadIdx.x + u * 256;
+      const int pl = k >> rshift, rl = k & (rt - 1);
+      if (k < pc * rt && pl < pw && rl < rw) tile[pl * pitch + rl] = v[u];
     }
     __syncthreads();
     for (int k = threadIdx.x; k < pw * rw; k += blockDim.x) {      // coalesced along the dense stream
@@ -627,7 +637,7 @@ static int launch_tile_copy_t(const aol_tiler& ts, const aol_tiler& td, int64_t 
     int pc2 = 1;
     while (pc2 < pc) pc2 <<= 1;
     int rshift = 0;
-    while ((1 << (rshift + 1)) * pc2 <= 1024) ++rshift;      // tile: 2^rshift x pc <= 1024 elements
+    while ((1 << (rshift + 1)) * pc2 <= 4096) ++rshift;      // tile: 2^rshift x pc <= 4096 elements
     const int64_t tiles = ((count + (1 << rshift) - 1) >> rshift) * ((P + pc - 1) / pc);
     k_tile_copy_transpose<T><<<(unsigned)std::min<int64_t>(tiles, (int64_t)kNumSMs * 16), 256, 0, stream>>>(
         s, d, p.cs, p.Bs, p.cd, P, first, count, pc, rshift, FastDiv32((uint32_t)pc));
