@@ -691,3 +691,69 @@ def test_random_tilers_all_tile_ops_vs_oracle(seed):
         got = _run_tile("matmul", {"a": tx, "b": tb, "c": tc}, ports, {"a": x, "b": b}, d).outputs["p_c"]
         ref = orc.run_tile_task("matmul", {"a": tx, "b": tb, "c": tc}, {"a": x, "b": b}, {"c": (R, np.float32)}, R, d)
         assert np.array_equal(got.view(np.uint32), ref["c"].view(np.uint32)), ("matmul", tx, tb)
+
+
+def _cg_model_and_bind(golden):
+    from paper_1105_4424_b200.model import model_from_dict
+    data, meta = golden
+    model = model_from_dict(meta["cg_k20"]["model"])
+    bind = {k: data[f"cg_k20/{k}"] for k in ("rowptr", "colidx", "values", "b")}
+    return model, bind
+
+
+def test_missing_and_missized_bindings(golden):
+    """tests/test_refexec.py:392-405 through the drop-in: MissingBinding before anything runs."""
+    from paper_1105_4424_b200.executor import MissingBinding, execute_schedule
+    from paper_1105_4424_b200.partition import build_schedule
+    model, bind = _cg_model_and_bind(golden)
+    b2 = dict(bind)
+    del b2["b"]
+    with pytest.raises(MissingBinding):
+        execute_schedule(model, build_schedule(model, 1), b2, 1)
+    b3 = dict(bind, b=np.ones(3))
+    with pytest.raises(MissingBinding):
+        execute_schedule(model, build_schedule(model, 1), b3, 1)
+
+
+def test_max_iter_override_stops_early(golden):
+    """tests/test_refexec.py:410-414: max_iter=3 -> 3 iterations, not converged."""
+    from paper_1105_4424_b200.executor import execute_schedule
+    from paper_1105_4424_b200.partition import build_schedule
+    model, bind = _cg_model_and_bind(golden)
+    for graphs in (False, True):
+        res = execute_schedule(model, build_schedule(model, 1), bind, 1, max_iter=3, graphs=graphs)
+        assert res.iterations == 3 and not res.converged
+
+
+def test_signature_mismatch_and_aliasing():
+    """tests/test_refexec.py:399-407 (wrong port name) and the output-aliases-input check (refexec.py:444-453)."""
+    from paper_1105_4424_b200 import IntrinsicShapeMismatch, builders
+    from paper_1105_4424_b200.executor import execute_schedule
+    from paper_1105_4424_b200.partition import build_schedule
+    model = builders.single_task_model(
+        "scale", ["y inout float64 [64]", "b in float64 [1]"],
+        ["i in float64 [64]", "s in float64 [1]", "o out float64 [64]"],
+        ["i -> t.y", "s -> t.b", "t.y -> o"],
+        ["allocate data i onto dev.gmem", "allocate data s onto host.ram", "allocate task t onto dev.cu"], 64)
+    with pytest.raises(IntrinsicShapeMismatch):
+        execute_schedule(model, build_schedule(model, 1), {"i": np.ones(64), "s": np.ones(1)}, 1)
+    # copy whose dst is connected back to its own src group
+    alias = builders.single_task_model(
+        "copy", ["src in float64 [8]", "dst out float64 [8]"], ["i in float64 [8]"],
+        ["i -> t.src", "t.dst -> t.src"],
+        ["allocate data i onto dev.gmem", "allocate task t onto dev.cu"], 8)
+    with pytest.raises(IntrinsicShapeMismatch, match="aliases"):
+        execute_schedule(alias, build_schedule(alias, 1), {"i": np.ones(8)}, 1)
+
+
+def test_no_repeat_touches_element_zero_only():
+    """SURVEY App. B probe: with no `repeat` the repetition space is 1 -> only element 0 is written."""
+    from paper_1105_4424_b200 import builders
+    from paper_1105_4424_b200.executor import execute_schedule
+    from paper_1105_4424_b200.partition import build_schedule
+    model = builders.single_task_model(
+        "copy", ["src in float32 [8]", "dst out float32 [8]"], ["i in float32 [8]", "o out float32 [8]"],
+        ["i -> t.src", "t.dst -> o"], ["allocate data i onto dev.gmem", "allocate data t.dst onto dev.gmem",
+                                       "allocate task t onto dev.cu"], None)
+    res = execute_schedule(model, build_schedule(model, 3), {"i": np.arange(1, 9, dtype=np.float32)}, 3)
+    assert res.outputs["o"].tolist() == [1, 0, 0, 0, 0, 0, 0, 0]
