@@ -248,43 +248,84 @@ __global__ void __launch_bounds__(256) k_tile_copy_vec(const T* __restrict__ src
 // pattern stream.  A 32x32 (repetition x pattern) tile goes through padded shared memory so
 // both the source reads (along repetitions) and the destination writes (along the stream)
 // are coalesced — the classic transpose.
-template <typename T>
+template <typename T, bool VEC>
 __global__ void __launch_bounds__(256) k_tile_copy_transpose(const T* __restrict__ src, T* __restrict__ dst,
                                                              int64_t cs, int64_t Bs, int64_t cd, int64_t P,
                                                              int64_t first, int64_t count, int pc, int rshift,
-                                                             FastDiv32 pcdiv) {
-  // tile = (1 << rshift) repetitions x pc pattern elements (pc <= 32, pc * 2^rshift <= 4096)
-  constexpr int PER = 16;                          // elements per thread per tile, loaded before storing
-  __shared__ T tile[4096 + 128];
+                                                             FastDiv32 pcdiv, int pitch) {
+  // tile = (1 << rshift) repetitions x pc pattern elements (pc <= 32, <= 4096 elements).
+  // pitch == 32/pc (mod 32): a warp's 32 accesses in either phase fall in 32 distinct banks.
+  constexpr int PER = VEC ? 4 : 16;                // loads per thread per tile (vectors or scalars)
+  constexpr int W = VEC ? 4 : 1;                   // elements per access
+  __shared__ T tile[4096 + 32 * 33];
   const int rt = 1 << rshift;
-  const int pitch = rt + 1;
   const int64_t nrb = (count + rt - 1) / rt, npb = (P + pc - 1) / pc;
   for (int64_t b = blockIdx.x; b < nrb * npb; b += gridDim.x) {
     const int64_t rb = b / npb, pb = b - rb * npb;
     const int64_t r0 = first + rb * rt, p0 = pb * pc;
     const int pw = (int)(P - p0 < pc ? P - p0 : pc);
     const int rw = (int)(first + count - r0 < rt ? first + count - r0 : rt);
-    T v[PER];
+    const bool full = VEC && pw == pc && rw == rt;
+    T v[PER * W];
 #pragma unroll
     for (int u = 0; u < PER; ++u) {                                // coalesced along repetitions
-      const int k = threadIdx.x + u * 256;
+      const int k = (threadIdx.x + u * 256) * W;
       const int pl = k >> rshift, rl = k & (rt - 1);
-      if (k < pc * rt && pl < pw && rl < rw) v[u] = __ldg(src + cs + (r0 + rl) + Bs * (p0 + pl));
+      if (k < pc * rt) {
+        const T* sp = src + cs + (r0 + rl) + Bs * (p0 + pl);
+        if (full) {
+          if constexpr (sizeof(T) == 4) {
+            const uint4 q = __ldg(reinterpret_cast<const uint4*>(sp));
+            v[u * W] = q.x; v[u * W + 1] = q.y; v[u * W + 2] = q.z; v[u * W + 3] = q.w;
+          } else {
+#pragma unroll
+            for (int e = 0; e < W; ++e) v[u * W + e] = __ldg(sp + e);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < W; ++e)
+            if (pl < pw && rl + e < rw) v[u * W + e] = __ldg(sp + e);
+        }
+      }
     }
     __syncthreads();
 #pragma unroll
     for (int u = 0; u < PER; ++u) {
-      const int k = threadIdx.x + u * 256;
+      const int k = (threadIdx.x + u * 256) * W;
       const int pl = k >> rshift, rl = k & (rt - 1);
-      if (k < pc * rt && pl < pw && rl < rw) tile[pl * pitch + rl] = v[u];
+      if (k < pc * rt) {
+#pragma unroll
+        for (int e = 0; e < W; ++e)
+          if (pl < pw && rl + e < rw) tile[pl * pitch + rl + e] = v[u * W + e];
+      }
     }
     __syncthreads();
-    for (int k = threadIdx.x; k < pw * rw; k += blockDim.x) {      // coalesced along the dense stream
-      uint32_t rl, pl;
-      if (pw == pc) pcdiv.divmod((uint32_t)k, rl, pl);
-      else { rl = (uint32_t)(k / pw); pl = (uint32_t)(k - rl * pw); }
-      dst[cd + (r0 + rl) * P + p0 + pl] = tile[pl * pitch + rl];
+    if (full) {                                                    // 16-byte stores along the stream
+      for (int k = threadIdx.x * 4; k < pw * rw; k += 256 * 4) {
+        T o[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          uint32_t rl, pl;
+          pcdiv.divmod((uint32_t)(k + e), rl, pl);
+          o[e] = tile[pl * pitch + rl];
+        }
+        T* dp = dst + cd + r0 * P + k;
+        if constexpr (sizeof(T) == 4) {
+          *reinterpret_cast<uint4*>(dp) = make_uint4(o[0], o[1], o[2], o[3]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) dp[e] = o[e];
+        }
+      }
+    } else {
+      for (int k = threadIdx.x; k < pw * rw; k += blockDim.x) {    // coalesced along the dense stream
+        uint32_t rl, pl;
+        if (pw == pc) pcdiv.divmod((uint32_t)k, rl, pl);
+        else { rl = (uint32_t)(k / pw); pl = (uint32_t)(k - rl * pw); }
+        dst[cd + (r0 + rl) * P + p0 + pl] = tile[pl * pitch + rl];
+      }
     }
+    __syncthreads();
   }
 }
 
@@ -639,8 +680,17 @@ static int launch_tile_copy_t(const aol_tiler& ts, const aol_tiler& td, int64_t 
     int rshift = 0;
     while ((1 << (rshift + 1)) * pc2 <= 4096) ++rshift;      // tile: 2^rshift x pc <= 4096 elements
     const int64_t tiles = ((count + (1 << rshift) - 1) >> rshift) * ((P + pc - 1) / pc);
-    k_tile_copy_transpose<T><<<(unsigned)std::min<int64_t>(tiles, (int64_t)kNumSMs * 16), 256, 0, stream>>>(
-        s, d, p.cs, p.Bs, p.cd, P, first, count, pc, rshift, FastDiv32((uint32_t)pc));
+    const int pitch = (1 << rshift) + 32 / pc2;
+    // 16-byte accesses on both sides when every tile row / stream chunk is aligned
+    const bool vec = sizeof(T) == 4 && pc == P && (1 << rshift) >= 4 && p.cs % 4 == 0 && p.Bs % 4 == 0 &&
+                     first % 4 == 0 && p.cd % 4 == 0 && ((uintptr_t)s % 16) == 0 && ((uintptr_t)d % 16) == 0;
+    const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)kNumSMs * 16);
+    if (vec)
+      k_tile_copy_transpose<T, true><<<grid, 256, 0, stream>>>(s, d, p.cs, p.Bs, p.cd, P, first, count, pc, rshift,
+                                                               FastDiv32((uint32_t)pc), pitch);
+    else
+      k_tile_copy_transpose<T, false><<<grid, 256, 0, stream>>>(s, d, p.cs, p.Bs, p.cd, P, first, count, pc, rshift,
+                                                                FastDiv32((uint32_t)pc), pitch);
     AOL_LAUNCH_CHECK("k_tile_copy_transpose");
     return AOL_OK;
   }

@@ -144,6 +144,8 @@ def test_tiler_offsets_random_vs_loop_oracle():
     ((8192,), (999,), (6,), ((7,),), ((1,),), (1,)),            # odd stride -> vec (V=2) or affine
     ((40, 1000), (1000,), (40,), ((0,), (1,)), ((1,), (0,)), (0, 0)),   # row stride -> transpose
     ((7, 3000), (2999,), (7,), ((0,), (1,)), ((1,), (0,)), (0, 1)),     # row stride, ragged -> transpose
+    ((8, 4096), (4096,), (8,), ((0,), (1,)), ((1,), (0,)), (0, 0)),     # row stride, aligned -> vector transpose
+    ((64, 1024), (1024,), (64,), ((0,), (1,)), ((1,), (0,)), (0, 0)),   # two pattern chunks
 ])
 @pytest.mark.parametrize("devices", [1, 3])
 @pytest.mark.parametrize("dtype", ["float32", "float64"])
