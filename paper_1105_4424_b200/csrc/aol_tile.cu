@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(256) k_tile_copy_transpose(const T* __restrict
                                                              int64_t cs, int64_t Bs, int64_t cd, int64_t P,
                                                              int64_t first, int64_t count, int pc, int rshift,
                                                              FastDiv32 pcdiv, int pitch) {
-  // tile = (1 << rshift) repetitions x pc pattern elements (pc <= 32, <= 4096 elements).
+  // tile = (1 << rshift) repetitions x pc pattern elements (pc <= 64, <= 4096 elements).
   // pitch == 32/pc (mod 32): a warp's 32 accesses in either phase fall in 32 distinct banks.
   constexpr int PER = VEC ? 4 : 16;                // loads per thread per tile (vectors or scalars)
   constexpr int W = VEC ? 4 : 1;                   // elements per access
@@ -674,13 +674,13 @@ static int launch_tile_copy_t(const aol_tiler& ts, const aol_tiler& td, int64_t 
     p.kind = 1;
   }
   if (p.kind == 4) {
-    const int pc = (int)std::min<int64_t>(P, 32);
+    const int pc = (int)std::min<int64_t>(P, 64);
     int pc2 = 1;
     while (pc2 < pc) pc2 <<= 1;
     int rshift = 0;
     while ((1 << (rshift + 1)) * pc2 <= 4096) ++rshift;      // tile: 2^rshift x pc <= 4096 elements
     const int64_t tiles = ((count + (1 << rshift) - 1) >> rshift) * ((P + pc - 1) / pc);
-    const int pitch = (1 << rshift) + 32 / pc2;
+    const int pitch = (1 << rshift) + (pc2 >= 32 ? 1 : 32 / pc2);
     // 16-byte accesses on both sides when every tile row / stream chunk is aligned
     const bool vec = sizeof(T) == 4 && pc == P && (1 << rshift) >= 4 && p.cs % 4 == 0 && p.Bs % 4 == 0 &&
                      first % 4 == 0 && p.cd % 4 == 0 && ((uintptr_t)s % 16) == 0 && ((uintptr_t)d % 16) == 0;
