@@ -222,92 +222,9 @@ __global__ void __launch_bounds__(256, (REPS <= 2 ? 4 : 3)) k_line_filter_vstrip
   }
 }
 
-// Horizontal windows with paving SX (inner == 1): each lane loads only its own SX-float
-// segment (coalesced 16-byte loads, the warp reads one contiguous run) and takes the
-// remaining PX - SX taps from the next lane with __shfl_down_sync.  Lanes whose neighbour
-// is not the next repetition of the same line (row end, warp end, wrap) load the tail
-// themselves.  Same taps, same order: bit-identical to k_line_filter.
-template <int PX, int PY, int SX>
-__global__ void __launch_bounds__(256) k_line_filter_hshfl(const float* __restrict__ x, const float* __restrict__ w,
-                                                           float* __restrict__ y, LineGeom g, int64_t first,
-                                                           int64_t count) {
-  static_assert(SX % 4 == 0 && PX > SX && PX - SX <= SX, "segment + one neighbour must cover the window");
-  constexpr int TAIL = PX - SX;
-  __shared__ float ws[PX * PY];
-  for (int k = threadIdx.x; k < PX * PY; k += blockDim.x) ws[k] = w[k];
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const uint32_t Sx = (uint32_t)g.Sx, Sy = (uint32_t)g.Sy;
-  // warp-uniform loop over groups of 32 consecutive repetitions
-  const int64_t warps_total = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  for (int64_t base = wid * 32; base < count; base += warps_total * 32) {
-    const int64_t e = base + lane;
-    const bool active = e < count;
-    const int64_t rho = first + (active ? e : count - 1);
-    uint32_t l, o;
-    {
-      uint32_t q, r;
-      g.div_nl.divmod((uint32_t)rho, q, r);      // inner == 1: rho = o * NL + l
-      l = r;
-      o = q;
-    }
-    uint32_t col = l * (uint32_t)g.sx + (uint32_t)g.ox;
-    if (col >= Sx) col %= Sx;
-    const float* xr = x + (uint64_t)o * Sx;
-    float xv[PX];
-    const bool seg_ok = col + SX <= Sx && ((col & 3) == 0);
-    if (seg_ok) {
-#pragma unroll
-      for (int q = 0; q < SX / 4; ++q) {
-        const float4 v4 = __ldg(reinterpret_cast<const float4*>(xr + col) + q);
-        xv[4 * q] = v4.x; xv[4 * q + 1] = v4.y; xv[4 * q + 2] = v4.z; xv[4 * q + 3] = v4.w;
-      }
-    } else {
-      uint32_t c = col;
-#pragma unroll
-      for (int t = 0; t < SX; ++t) {
-        xv[t] = __ldg(xr + c);
-        if (++c == Sx) c = 0;
-      }
-    }
-    // the next lane holds repetition rho+1; it continues this window iff it is the next
-    // repetition on the same line and its segment starts exactly SX floats further
-    const uint32_t ncol = __shfl_down_sync(0xffffffffu, col, 1);
-    const uint32_t no = __shfl_down_sync(0xffffffffu, o, 1);
-    const bool nseg = __shfl_down_sync(0xffffffffu, seg_ok ? 1 : 0, 1);
-    const bool from_next = lane < 31 && no == o && ncol == col + SX && nseg && g.sx == SX;
-#pragma unroll
-    for (int t = 0; t < TAIL; ++t) {
-      const float v = __shfl_down_sync(0xffffffffu, xv[t], 1);
-      xv[SX + t] = v;
-    }
-    if (!from_next) {
-      uint32_t c = col + SX;
-      if (c >= Sx) c -= Sx;
-#pragma unroll
-      for (int t = 0; t < TAIL; ++t) {
-        xv[SX + t] = __ldg(xr + c);
-        if (++c == Sx) c = 0;
-      }
-    }
-    if (active) {
-      float* yp = y + (uint64_t)o * Sy + (l * (uint32_t)g.sy + (uint32_t)g.oy);
-#pragma unroll
-      for (int j = 0; j < PY; ++j) {
-        float acc = 0.0f;
-#pragma unroll
-        for (int t = 0; t < PX; ++t) acc = __fadd_rn(acc, __fmul_rn(ws[j * PX + t], xv[t]));
-        yp[j] = acc;
-      }
-    }
-  }
-}
-
 static_assert(sizeof(LineGeom) <= 256, "LineGeomBuf in aol_tile.cu must hold a LineGeom");
 
 const char* line_filter_variant(const LineGeom& g) {
-  if (g.px == 13 && g.py == 3 && g.inner == 1 && g.sx == 8) return "tile_filter.line_13x3_shfl";
   if (g.px == 13 && g.py == 3) return "tile_filter.line_13x3";
   if (g.px == 14 && g.py == 4 && g.inner > 1 && g.sx == 9) return "tile_filter.line_14x4_vstrip";
   if (g.px == 14 && g.py == 4) return "tile_filter.line_14x4";
@@ -338,12 +255,6 @@ int launch_line_filter(const aol_task& t, const LineGeom& g, int64_t first, int6
     else
       k_line_filter_vstrip<14, 4, 9, 4><<<grid, 256, 0, s>>>(x, w, y, g, first, last, o_lo, ngroups);
     AOL_LAUNCH_CHECK("k_line_filter_vstrip");
-    return AOL_OK;
-  }
-  if (idx32 && g.inner == 1 && g.px == 13 && g.py == 3 && g.sx == 8 && g.small && g.NL < (1ll << 31) &&
-      g.outer * g.NL < (1ll << 32) && !getenv("AOL_NO_HSHFL")) {
-    k_line_filter_hshfl<13, 3, 8><<<grid_for(count, 256, 8), 256, 0, s>>>(x, w, y, g, first, count);
-    AOL_LAUNCH_CHECK("k_line_filter_hshfl");
     return AOL_OK;
   }
   if (idx32) {

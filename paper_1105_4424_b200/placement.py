@@ -215,8 +215,6 @@ KERNEL_STAGING = {
     "tile_copy.generic": "HBM -> registers -> HBM (full index function)",
     "tile_filter.stencil_box": "coefficients: smem broadcast; (4+KH-1) x 6 input window: registers; outputs float4",
     "tile_filter.line_13x3": "coefficients: smem broadcast; 13-tap window: registers (float4 loads); outputs HBM",
-    "tile_filter.line_13x3_shfl": "coefficients: smem broadcast; each lane's 8-float segment: registers (coalesced "
-                                  "float4), 5-tap tail from the next lane by warp shuffle",
     "tile_filter.line_14x4": "coefficients: smem broadcast; 14-tap window: registers (coalesced row taps)",
     "tile_filter.line_14x4_vstrip": "coefficients: smem broadcast; 4 overlapping 14-tap windows (41 rows): registers "
                                     "(coalesced row taps)",

@@ -380,7 +380,7 @@ def test_line_filter_kernel_vs_oracle(kind, dims, devices):
         w = orc.hfilter_weights()
         if kind == "h_shift":
             t["x"] = dict(t["x"], origin=(0, 0, W - 2))       # window starts 2 left: wraps at the row start
-        expect = "tile_filter.line_13x3_shfl"
+        expect = "tile_filter.line_13x3"
     else:
         if kind == "v_generic":
             t = orc.vfilter_tilers(F, H, W, taps=6, step=4, outs=2)
