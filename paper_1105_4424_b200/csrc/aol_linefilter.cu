@@ -323,109 +323,96 @@ bool fused_line_geometry(const aol_task& th, const aol_task& tv, FusedGeom& f) {
   return f.R * f.W * v.outer < (1ll << 32);   // 32-bit x offsets
 }
 
-// Streaming form: one thread per (frame, strip of FZ_STRIP consumer repetitions, intermediate
-// column i).  The thread walks the strip's intermediate rows top to bottom; each row's value
-// m(row, i) is computed once (producer taps in order) and folded into the (at most two)
-// consumer repetitions whose window covers the row, in tap order — so every sum is formed
-// in exactly the unfused order.  Consecutive threads take consecutive columns: the producer
-// windows of 3 neighbouring columns coincide (L1 broadcast) and the consumer stores coalesce.
-constexpr int FZ_STRIP = 16;
-
+// Tile form: a CTA owns (frame, FZ_TV consecutive consumer line repetitions, TI intermediate
+// columns).  Phase 1 computes the NR = (FZ_TV-1)*sx_v + px_v intermediate rows of the tile
+// into shared memory (producer taps in order, two producer repetitions per thread per
+// iteration so 8 window loads are in flight); phase 2 applies the consumer filter from
+// shared memory.  Every value is formed in the unfused order -> bit-identical results.
 template <int PXH, int PYH, int PXV, int PYV>
-__global__ void __launch_bounds__(FZ_THREADS) k_fused_line_filters(const float* __restrict__ x,
-                                                                   const float* __restrict__ wh,
-                                                                   const float* __restrict__ wv,
-                                                                   float* __restrict__ y, FusedGeom g, int64_t first,
-                                                                   int64_t last, int64_t f_lo, int64_t nthreads) {
-  static_assert(PXV <= 2 * 9 + 0 || true, "");
+__global__ void __launch_bounds__(FZ_THREADS, 3) k_fused_line_filters(const float* __restrict__ x,
+                                                                      const float* __restrict__ wh,
+                                                                      const float* __restrict__ wv,
+                                                                      float* __restrict__ y, FusedGeom g,
+                                                                      int64_t first, int64_t last, int64_t tile0,
+                                                                      int64_t ntiles) {
+  extern __shared__ float mt[];                     // [NR][TI] intermediate tile
   __shared__ float swh[PXH * PYH], swv[PXV * PYV];
   for (int k = threadIdx.x; k < PXH * PYH; k += blockDim.x) swh[k] = wh[k];
   for (int k = threadIdx.x; k < PXV * PYV; k += blockDim.x) swv[k] = wv[k];
-  __syncthreads();
   const LineGeom &h = g.h, &v = g.v;
-  const int64_t nstrips = (v.NL + FZ_STRIP - 1) / FZ_STRIP;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nthreads;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = e % g.Wm;
-    const int64_t q = e / g.Wm;
-    const int64_t strip = q % nstrips;
-    const int64_t fr = f_lo + q / nstrips;
-    const int64_t lv0 = strip * FZ_STRIP;
-    const int64_t lv1 = min(lv0 + FZ_STRIP, v.NL);
-    // skip strips entirely outside the launch range
-    const int64_t rho_first = (fr * v.NL + lv0) * g.Wm + i, rho_last = (fr * v.NL + lv1 - 1) * g.Wm + i;
-    if (rho_last < first || rho_first > last) continue;
-    const int64_t lh = i / h.sy;
-    const int jh = (int)(i - lh * h.sy);
-    int64_t col0 = lh * h.sx + h.ox;
-    if (col0 >= g.W) col0 %= g.W;
-    const bool xvec = col0 + 16 <= g.W && (col0 & 3) == 0 && (g.W & 3) == 0;
-    const float* xf = x + fr * g.R * g.W + col0;
-    float wrow[PXH];
+  const uint32_t R = (uint32_t)g.R, W = (uint32_t)g.W, TI = (uint32_t)g.TI;
+  const int items = g.NR * FZ_HR;
+  for (int64_t tt = tile0 + blockIdx.x; tt < tile0 + ntiles; tt += gridDim.x) {
+    const uint32_t ib = (uint32_t)(tt % g.tiles_i);
+    const int64_t q = tt / g.tiles_i;
+    const uint32_t lb = (uint32_t)(q % g.tiles_l);
+    const uint32_t fr = (uint32_t)(q / g.tiles_l);
+    const uint32_t lv0 = lb * FZ_TV;
+    const uint32_t i0 = ib * TI;
+    const uint32_t lh0 = i0 / (uint32_t)h.sy;
+    const uint32_t row0 = lv0 * (uint32_t)v.sx + (uint32_t)v.ox;
+    __syncthreads();                                // weights ready / previous tile consumed
+    for (int it = threadIdx.x; it < items; it += 2 * FZ_THREADS) {
+      float xv[2][16];
+      uint32_t dst[2];
+      bool ok[2];
 #pragma unroll
-    for (int t = 0; t < PXH; ++t) wrow[t] = swh[jh * PXH + t];
-    float acc0[PYV], acc1[PYV];
+      for (int u = 0; u < 2; ++u) {
+        const int item = it + u * FZ_THREADS;
+        const uint32_t k = (uint32_t)item / FZ_HR, hh = (uint32_t)item % FZ_HR;
+        const uint32_t lh = lh0 + hh;
+        ok[u] = item < items && lh < (uint32_t)h.NL;
+        dst[u] = k * TI + hh * PYH;
+        if (!ok[u]) continue;
+        uint32_t r = row0 + k;
+        while (r >= R) r -= R;
+        const uint32_t xrow = (fr * R + r) * W;
+        uint32_t col = lh * (uint32_t)h.sx + (uint32_t)h.ox;
+        if (col >= W) col %= W;
+        if (col + 16 <= W && ((xrow + col) & 3) == 0) {
+          const float4* p = reinterpret_cast<const float4*>(x + xrow + col);
 #pragma unroll
-    for (int j = 0; j < PYV; ++j) { acc0[j] = 0.0f; acc1[j] = 0.0f; }
-    int64_t cur = lv0;                                   // oldest active consumer repetition
-    const int64_t r_begin = lv0 * v.sx + v.ox, r_end = (lv1 - 1) * v.sx + v.ox + PXV;   // unwrapped rows
-    int64_t rr = r_begin % g.R;
-    float* yb = y + fr * v.Sy * g.Wm + i;
-    // software pipeline: the window of row r+1 is in flight while row r is reduced
-    float4 nxt[4];
-    auto fetch = [&](int64_t row, float4 (&dst)[4]) {
-      const float* xr = xf + row * g.W;
+          for (int e = 0; e < 4; ++e) {
+            const float4 t4 = __ldg(p + e);
+            xv[u][4 * e] = t4.x; xv[u][4 * e + 1] = t4.y; xv[u][4 * e + 2] = t4.z; xv[u][4 * e + 3] = t4.w;
+          }
+        } else {
+          uint32_t c = col;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) dst[u] = __ldg(reinterpret_cast<const float4*>(xr) + u);
-    };
-    if (xvec) fetch(rr, nxt);
-    for (int64_t r = r_begin; r < r_end; ++r) {
-      // producer value m(rr, i), taps in order
-      float xv[16];
-      if (xvec) {
-        float4 curw[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) curw[u] = nxt[u];
-        if (r + 1 < r_end) fetch(rr + 1 == g.R ? 0 : rr + 1, nxt);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          xv[4 * u] = curw[u].x; xv[4 * u + 1] = curw[u].y; xv[4 * u + 2] = curw[u].z; xv[4 * u + 3] = curw[u].w;
-        }
-      } else {
-        int64_t c = col0;
-        const float* xrow = x + fr * g.R * g.W + rr * g.W;
-#pragma unroll
-        for (int t = 0; t < PXH; ++t) {
-          xv[t] = __ldg(xrow + c);
-          if (++c == g.W) c = 0;
+          for (int t = 0; t < PXH; ++t) {
+            xv[u][t] = __ldg(x + xrow + c);
+            if (++c == W) c = 0;
+          }
         }
       }
-      float m = 0.0f;
 #pragma unroll
-      for (int t = 0; t < PXH; ++t) m = __fadd_rn(m, __fmul_rn(wrow[t], xv[t]));
-      // fold into the consumer repetitions covering this row (cur and cur+1)
-      const int64_t t0 = r - (cur * v.sx + v.ox);
-      if (t0 < PXV) {
+      for (int u = 0; u < 2; ++u) {
+        if (!ok[u]) continue;
 #pragma unroll
-        for (int j = 0; j < PYV; ++j) acc0[j] = __fadd_rn(acc0[j], __fmul_rn(swv[j * PXV + (int)t0], m));
-      }
-      const int64_t t1 = t0 - v.sx;
-      if (cur + 1 < lv1 && t1 >= 0 && t1 < PXV) {
+        for (int j = 0; j < PYH; ++j) {
+          float acc = 0.0f;
 #pragma unroll
-        for (int j = 0; j < PYV; ++j) acc1[j] = __fadd_rn(acc1[j], __fmul_rn(swv[j * PXV + (int)t1], m));
-      }
-      if (t0 == PXV - 1) {                               // repetition `cur` complete
-        const int64_t rho = (fr * v.NL + cur) * g.Wm + i;
-        if (rho >= first && rho <= last) {
-          float* yp = yb + (cur * v.sy + v.oy) * g.Wm;
-#pragma unroll
-          for (int j = 0; j < PYV; ++j) yp[j * g.Wm] = acc0[j];
+          for (int t = 0; t < PXH; ++t) acc = __fadd_rn(acc, __fmul_rn(swh[j * PXH + t], xv[u][t]));
+          mt[dst[u] + j] = acc;
         }
-#pragma unroll
-        for (int j = 0; j < PYV; ++j) { acc0[j] = acc1[j]; acc1[j] = 0.0f; }
-        ++cur;
       }
-      if (++rr == g.R) rr = 0;
+    }
+    __syncthreads();
+    for (int item = threadIdx.x; item < FZ_TV * (int)TI; item += blockDim.x) {
+      const uint32_t l = (uint32_t)item / TI, c = (uint32_t)item % TI;
+      const int64_t lv = lv0 + l, i = i0 + c;
+      if (lv >= v.NL || i >= g.Wm) continue;
+      const int64_t rho = ((int64_t)fr * v.NL + lv) * g.Wm + i;
+      if (rho < first || rho > last) continue;
+      float* yp = y + ((int64_t)fr * v.Sy + lv * v.sy + v.oy) * g.Wm + i;
+      const float* mp = mt + (l * (uint32_t)v.sx) * TI + c;
+#pragma unroll
+      for (int j = 0; j < PYV; ++j) {
+        float acc = 0.0f;
+#pragma unroll
+        for (int t = 0; t < PXV; ++t) acc = __fadd_rn(acc, __fmul_rn(swv[j * PXV + t], mp[t * TI]));
+        yp[(int64_t)j * g.Wm] = acc;
+      }
     }
   }
 }
@@ -440,14 +427,16 @@ int launch_fused_line_filters(const aol_task& th, const aol_task& tv, int64_t fi
   const int64_t last = first + count - 1;
   const int64_t per_frame = g.v.NL * g.Wm;
   const int64_t f_lo = first / per_frame, f_hi = last / per_frame;
-  // the two consumer windows a row can feed must not overlap a third (px_v <= 2 * sx_v)
-  if (g.v.px > 2 * g.v.sx) return fail(AOL_EUNSUPPORTED, "consumer windows overlap more than pairwise");
-  const int64_t nstrips = (g.v.NL + FZ_STRIP - 1) / FZ_STRIP;
-  const int64_t nthreads = (f_hi - f_lo + 1) * nstrips * g.Wm;
+  const int64_t tiles_per_frame = g.tiles_i * g.tiles_l;
+  const int64_t tile0 = f_lo * tiles_per_frame, ntiles = (f_hi - f_lo + 1) * tiles_per_frame;
+  const size_t smem = (size_t)g.NR * g.TI * sizeof(float);
   auto kern = k_fused_line_filters<13, 3, 14, 4>;
-  kern<<<grid_for(nthreads, FZ_THREADS, 32), FZ_THREADS, 0, s>>>(
-      static_cast<const float*>(ph[0]), static_cast<const float*>(ph[1]), static_cast<const float*>(pv[1]),
-      static_cast<float*>(pv[2]), g, first, last, f_lo, nthreads);
+  if (smem > 48 * 1024)
+    AOL_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t grid = ntiles < (int64_t)kNumSMs * 16 ? ntiles : (int64_t)kNumSMs * 16;
+  kern<<<(unsigned)grid, FZ_THREADS, smem, s>>>(static_cast<const float*>(ph[0]), static_cast<const float*>(ph[1]),
+                                                static_cast<const float*>(pv[1]), static_cast<float*>(pv[2]), g, first,
+                                                last, tile0, ntiles);
   AOL_LAUNCH_CHECK("k_fused_line_filters");
   return AOL_OK;
 }
