@@ -180,11 +180,13 @@ class Workload:
     unit = "GB/s"
     bound = "hbm"
 
+    fuse = False
+
     def _prepare(self, torch, device, model, schedule, dev_bindings: dict, host_specs: dict, outputs: dict):
         from paper_1105_4424_b200.executor import Executor
         self.torch, self.device = torch, device
         self.model, self.schedule = model, schedule
-        self.ex = Executor(model, schedule, dev_bindings, 1)
+        self.ex = Executor(model, schedule, dev_bindings, 1, fuse=Workload.fuse)
         self.host_specs, self.out_sizes = host_specs, outputs
 
     def step(self):
@@ -795,10 +797,12 @@ def main():
     ap.add_argument("--no-peak", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-points", action="store_true")
+    ap.add_argument("--fuse", action="store_true", help="enable task fusion (downscaler H->V)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         log("note: warmup < 3 is below the timing rules; using 3")
         args.warmup = 3
+    Workload.fuse = args.fuse
     if args.impl == "reference":
         run_reference(args)
     else:
