@@ -201,7 +201,7 @@ class Workload:
         self.e2e_bytes = (sum(t.numel() * 4 for t in self.hin.values()),
                           sum(t.numel() * 4 for t in self.hout.values()))
 
-    pipeline = 8
+    pipeline = int(os.environ.get("AOL_E2E_PIPELINE", "8"))
 
     def e2e_step(self):
         from paper_1105_4424_b200.executor import execute_schedule

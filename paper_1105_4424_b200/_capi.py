@@ -11,8 +11,6 @@ import ctypes as C
 import os
 from pathlib import Path
 
-import numpy as np
-
 from .tiler import MAX_RANK, BoundTiler
 
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libaolb200.so"
@@ -177,6 +175,3 @@ def launch_fused2(producer: AolTask, consumer: AolTask, first: int, count: int, 
 def launch_counter() -> int:
     return int(load().aol_launch_counter())
 
-
-def numpy_dtype(name: str):
-    return np.dtype(name)

@@ -440,12 +440,13 @@ class Executor:
         torch = _torch()
         g = self._graphs.get(step.task_path)
         if g is None:
-            for st in step.body:
+            for st in step.body:                   # everything allocated before capture
                 if getattr(st, "op", None) == "dot_partial":
                     t = self.task(st.task_path)
                     self._gbufs[st.task_path] = torch.zeros(max(8, len(st.launches)),
                                                             dtype=torch_dtype(t.dtype), device=self.device)
-                self._dev_task(st) if not (getattr(st, "op", None) == "dot_partial") else None
+                else:
+                    self._dev_task(st)
             torch.cuda.synchronize(self.device)
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
