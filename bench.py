@@ -610,8 +610,62 @@ class CGWorkload(Workload):
                 "sample": f"10 CG iterations with the oracle's level-synchronous spmv (numpy), {dt * 1e3:.1f} ms/iter"}
 
 
+class C1Workload(Workload):
+    """Config C1: the paper-case-study MatMul 256x256 fp32 repetitive task, one full
+    execute_schedule call per step (host numpy bindings -> numpy outputs, like the reference
+    executor is called).  Launch/overhead-bound: reported, not a roofline target."""
+
+    name = "c1"
+    unit = "TFLOP/s"
+    bound = "tensor"
+
+    def __init__(self, torch, device, rank, world, n=256):
+        from oracle import aol_oracle as orc
+        from paper_1105_4424_b200 import builders
+        from paper_1105_4424_b200.partition import build_schedule
+        self.torch, self.device, self.n = torch, device, n
+        g = orc.gemm_tilers(n, n, n)
+        self.model = builders.tile_task_model(
+            "matmul", {"a": f"in float32 [{n},{n}]", "b": f"in float32 [{n},{n}]", "c": f"out float32 [{n},{n}]"},
+            {k: _tiler(v) for k, v in g.items()}, (n, n))
+        self.schedule = build_schedule(self.model, 1)
+        rng = np.random.default_rng(0)
+        self.bind = {"p_a": rng.standard_normal(n * n, dtype=np.float32),
+                     "p_b": rng.standard_normal(n * n, dtype=np.float32)}
+        self.units_per_step = 2.0 * n ** 3 / 1e12
+        self.algorithmic = {"flop_per_launch": 2 * n ** 3, "per_unit": "2 FLOP per (m, n, k)"}
+        self.workload = f"C1 matmul {n}x{n}x{n} fp32 via execute_schedule (host numpy in/out, TF32 tcgen05)"
+        self.l2 = "small: L2-resident, launch- and API-overhead-bound"
+
+    def step(self):
+        from paper_1105_4424_b200.executor import execute_schedule
+        execute_schedule(self.model, self.schedule, self.bind, 1)
+
+    def e2e_setup(self):
+        self.e2e_bytes = (2 * self.n * self.n * 4, self.n * self.n * 4)
+
+    def e2e_step(self):
+        self.step()
+
+    def e2e_free(self):
+        pass
+
+    def cpu_sample(self, seconds: float = 8.0):
+        from oracle import c_oracle as co
+        n = self.n
+        c = np.zeros(n * n, np.float32)
+        reps, t0 = 0, time.perf_counter()
+        while time.perf_counter() - t0 < min(seconds, 2.0):
+            co.gemm_rows(self.bind["p_a"], self.bind["p_b"], c, n, n, 0, n)
+            reps += 1
+        dt = (time.perf_counter() - t0) / reps
+        return {"value": 2.0 * n ** 3 / dt / 1e12, "unit": "TFLOP/s", "cores": co.threads(), "kind": "port",
+                "sample": f"full 256^3 product, oracle/aol_oracle.c, {dt * 1e3:.2f} ms per product "
+                          f"(the reference executor's Kronecker-spmv route took 0.60-0.72 s here, SURVEY App. B)"}
+
+
 WORKLOADS = {"matmul": MatmulWorkload, "stencil": StencilWorkload, "downscaler": DownscalerWorkload,
-             "sweep": SweepWorkload, "cg": CGWorkload}
+             "sweep": SweepWorkload, "cg": CGWorkload, "c1": C1Workload}
 
 
 # ---------------------------------------------------------------- the arms --
