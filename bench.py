@@ -563,7 +563,7 @@ class CGWorkload(Workload):
         self.algorithmic = {"flop_per_solve": self.flop, "iterations": self.iters,
                             "per_unit": "per iteration 2*nnz (spmv) + 3 dots + 3 vector updates (12n)"}
         self.workload = (f"CG (bundled cg.gmodel resized) poisson_2d({k}): n={n}, nnz={self.nnz}, {self.iters} "
-                         f"iterations; loop body replayed as one CUDA graph per iteration (setup + capture timed)")
+                         f"iterations; the whole LoopStep as ONE CUDA graph with a device-side conditional WHILE node (setup + capture timed)")
         self.l2 = "vectors (1 MB) fit in L2: the solve is launch- and host-sync-bound"
         self.ex = None
 

@@ -149,6 +149,21 @@ int64_t aol_launch_counter(void);
 int aol_launch_fused2(const aol_task* producer, const aol_task* consumer, int64_t first, int64_t count,
                       void* const* producer_ports, void* const* consumer_ports, void* stream);
 
+/* Device-side LoopStep (refexec.py:525-541): one CUDA graph holding a conditional WHILE
+ * node.  aol_loop_begin starts capturing `stream` (a non-default cudaStream_t) into the
+ * node's body; the caller then enqueues one loop iteration with aol_launch on that stream
+ * (device-resident scalars, AOL_FLAG_DEVICE_SCALARS, AOL_OP_SCALAR_*, AOL_OP_PARTIALS_SUM);
+ * aol_loop_end appends the check (iterations += 1; stop when *relres_dev <= tol or after
+ * max_iter iterations) and instantiates.  aol_loop_run executes the whole loop with no host
+ * round trip per iteration and returns the bookkeeping of ExecutionResult (refexec.py:367-372).
+ * No reference counterpart beyond the interpreter loop itself. */
+typedef struct aol_loop aol_loop;
+int aol_loop_begin(void* stream, const void* relres_dev, int relres_dtype, double tol, int64_t max_iter,
+                   aol_loop** loop);
+int aol_loop_end(aol_loop* loop);
+int aol_loop_run(aol_loop* loop, void* stream, int64_t* iterations, double* final_relres, int* converged);
+int aol_loop_destroy(aol_loop* loop);
+
 #ifdef __cplusplus
 }
 #endif

@@ -27,7 +27,8 @@ OP = {"copy": 1, "sub": 2, "scale": 3, "axpy": 4, "spmv_csr": 5, "dot_partial": 
 PRECISION = {"default": 0, "tf32": 1, "3xtf32": 2, "exact": 3}
 
 EXPORTS = ("aol_abi_version", "aol_last_error", "aol_device_count", "aol_validate", "aol_launch",
-           "aol_plan_name", "aol_tiler_offsets", "aol_launch_counter", "aol_launch_fused2")
+           "aol_plan_name", "aol_tiler_offsets", "aol_launch_counter", "aol_launch_fused2", "aol_loop_begin",
+           "aol_loop_end", "aol_loop_run", "aol_loop_destroy")
 
 
 class NativeLibraryError(RuntimeError):
@@ -117,6 +118,11 @@ def load(path: Path | str | None = None) -> C.CDLL:
     lib.aol_launch_counter.restype = C.c_int64
     lib.aol_launch_fused2.argtypes = [C.POINTER(AolTask), C.POINTER(AolTask), C.c_int64, C.c_int64,
                                       C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_void_p]
+    lib.aol_loop_begin.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_int64, C.POINTER(C.c_void_p)]
+    lib.aol_loop_end.argtypes = [C.c_void_p]
+    lib.aol_loop_run.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_double),
+                                 C.POINTER(C.c_int)]
+    lib.aol_loop_destroy.argtypes = [C.c_void_p]
     if lib.aol_abi_version() != ABI_VERSION:
         raise NativeLibraryError(f"{p}: ABI {lib.aol_abi_version()} != expected {ABI_VERSION}")
     _lib = lib
@@ -170,6 +176,29 @@ def launch_fused2(producer: AolTask, consumer: AolTask, first: int, count: int, 
         return False
     check(rc)
     return True
+
+
+def loop_begin(stream: int, relres_ptr: int, dtype: str, tol: float, max_iter: int) -> int:
+    """Start capturing one LoopStep body on `stream` into a device-side WHILE loop; returns a handle."""
+    h = C.c_void_p()
+    check(load().aol_loop_begin(C.c_void_p(int(stream)), C.c_void_p(int(relres_ptr)), DTYPE[dtype], float(tol),
+                                int(max_iter), C.byref(h)))
+    return h.value
+
+
+def loop_end(handle: int) -> None:
+    check(load().aol_loop_end(C.c_void_p(handle)))
+
+
+def loop_run(handle: int, stream: int) -> tuple[int, float, bool]:
+    it, rr, cv = C.c_int64(), C.c_double(), C.c_int()
+    check(load().aol_loop_run(C.c_void_p(handle), C.c_void_p(int(stream)), C.byref(it), C.byref(rr), C.byref(cv)))
+    return it.value, rr.value, bool(cv.value)
+
+
+def loop_destroy(handle: int) -> None:
+    if handle:
+        load().aol_loop_destroy(C.c_void_p(handle))
 
 
 def launch_counter() -> int:

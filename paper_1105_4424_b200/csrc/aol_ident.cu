@@ -136,6 +136,12 @@ __global__ void k_partials_sum(const T* p, int n, T* s) {
   s[0] = (T)total;
 }
 
+double* dot_scratch_for_current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  return dot_scratch(dev);
+}
+
 template <typename T>
 static int launch_ident_t(const aol_task& t, int64_t first, int64_t count, void* const* ports,
                           const double* scalars, cudaStream_t s) {

@@ -202,10 +202,10 @@ class Executor:
         self._tasks: dict[str, _Task] = {}
         self.fuse = fuse
         self.graphs = graphs
-        self._graphs: dict[str, object] = {}
+        self._loops: dict[tuple, tuple] = {}
         self._gbufs: dict[str, object] = {}
         self._dev_tasks: dict[str, object] = {}
-        self.graph_replays = 0
+        self.device_loops = 0
         self._fusable: dict[tuple, bool] = {}
         self.fused_launches = 0
         self._dot_buf = None
@@ -436,10 +436,12 @@ class Executor:
             for l in step.launches:
                 _capi.launch(ctask, l.range.offset, l.range.count, ptrs, (), s)
 
-    def _loop_graph(self, step):
+    def _loop_device(self, step, tol: float, max_iter: int):
+        """Run a LoopStep as one device-side CUDA graph (conditional WHILE node, aol_loop_*)."""
         torch = _torch()
-        g = self._graphs.get(step.task_path)
-        if g is None:
+        key = (step.task_path, tol, max_iter)
+        entry = self._loops.get(key)
+        if entry is None:
             for st in step.body:                   # everything allocated before capture
                 if getattr(st, "op", None) == "dot_partial":
                     t = self.task(st.task_path)
@@ -447,12 +449,34 @@ class Executor:
                                                             dtype=torch_dtype(t.dtype), device=self.device)
                 else:
                     self._dev_task(st)
+            stream = torch.cuda.Stream(self.device)          # captures need a non-default stream
+            relres = self.storage.array(step.relres_port)
             torch.cuda.synchronize(self.device)
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                self._run_body_device(step.body)
-            self._graphs[step.task_path] = g
-        return g
+            handle = None
+            with torch.cuda.stream(stream):
+                handle = _capi.loop_begin(stream.cuda_stream, relres.data_ptr(),
+                                          str(relres.dtype).replace("torch.", ""), tol, max(1, int(max_iter)))
+                try:
+                    self._run_body_device(step.body)
+                finally:
+                    try:
+                        _capi.loop_end(handle)
+                    except Exception:
+                        _capi.loop_destroy(handle)
+                        raise
+            entry = (handle, stream)
+            self._loops[key] = entry
+        handle, stream = entry
+        stream.wait_stream(torch.cuda.current_stream(self.device))
+        self.device_loops += 1
+        return _capi.loop_run(handle, stream.cuda_stream)
+
+    def __del__(self):
+        for handle, _ in getattr(self, "_loops", {}).values():
+            try:
+                _capi.loop_destroy(handle)
+            except Exception:
+                pass
 
     # -- task fusion ---------------------------------------------------------------
     def _fusion_candidate(self, s1, s2) -> bool:
@@ -502,13 +526,14 @@ class Executor:
                 loop_max = max_iter if max_iter is not None else step.max_iterations
                 done = False
                 n = 0
-                graph = self._loop_graph(step) if (self.graphs and self._graphable(step.body)) else None
+                if self.graphs and self._graphable(step.body):
+                    n, relres, done = self._loop_device(step, loop_tol, loop_max)
+                    self.iterations += n
+                    self.final_relres = relres
+                    self.converged = self.converged and done
+                    continue
                 while True:
-                    if graph is not None:
-                        graph.replay()
-                        self.graph_replays += 1
-                    else:
-                        self.run_steps(step.body, tol, max_iter)
+                    self.run_steps(step.body, tol, max_iter)
                     n += 1
                     self.iterations += 1
                     relres = float(self.storage.array(step.relres_port)[0].item())

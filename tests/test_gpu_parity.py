@@ -614,8 +614,8 @@ def test_fused_downscaler_bitwise(F, H, W, devices):
 
 @pytest.mark.parametrize("devices", [1, 4])
 def test_cg_graph_mode_equals_eager(golden, devices):
-    """LoopStep body captured once as a CUDA graph (device scalar ops, ordered partial sums):
-    bit-identical to the eager interpreter, and to the reference's iteration count."""
+    """LoopStep as ONE device-side CUDA graph (conditional WHILE node; device scalar ops, ordered
+    partial sums): bit-identical to the eager interpreter, and to the reference's iteration count."""
     from paper_1105_4424_b200.executor import Executor
     from paper_1105_4424_b200.model import model_from_dict
     from paper_1105_4424_b200.partition import build_schedule
@@ -628,7 +628,8 @@ def test_cg_graph_mode_equals_eager(golden, devices):
     eager.run()
     gr = Executor(model, sched, bind, devices, graphs=True)
     gr.run()
-    assert gr.graph_replays == gr.iterations == eager.iterations == m["runs"][str(devices)]["iterations"]
+    assert gr.device_loops == 1
+    assert gr.iterations == eager.iterations == m["runs"][str(devices)]["iterations"]
     assert np.array_equal(gr.outputs()["x"], eager.outputs()["x"])
     assert gr.final_relres == eager.final_relres
 
