@@ -541,6 +541,7 @@ class CGWorkload(Workload):
 
     name = "cg"
     unit = "GFLOP/s"
+    dtype = "f64"
 
     def __init__(self, torch, device, rank, world, k=364):
         from paper_1105_4424_b200.executor import Executor
@@ -563,7 +564,7 @@ class CGWorkload(Workload):
         self.algorithmic = {"flop_per_solve": self.flop, "iterations": self.iters,
                             "per_unit": "per iteration 2*nnz (spmv) + 3 dots + 3 vector updates (12n)"}
         self.workload = (f"CG (bundled cg.gmodel resized) poisson_2d({k}): n={n}, nnz={self.nnz}, {self.iters} "
-                         f"iterations; the whole LoopStep as ONE CUDA graph with a device-side conditional WHILE node (setup + capture timed)")
+                         f"iterations; the whole LoopStep as ONE persistent cooperative kernel interpreting the loop body (Executor setup timed)")
         self.l2 = "vectors (1 MB) fit in L2: the solve is launch- and host-sync-bound"
         self.ex = None
 
@@ -787,7 +788,7 @@ def run_gpu(args):
         out = {
             "metric": METRIC, "value": value, "unit": wl.unit, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32" if wl.bound == "hbm" else "tf32 (fp32 in/out)",
+            "vs_baseline": None, "dtype": getattr(wl, "dtype", "f32" if wl.bound == "hbm" else "tf32 (fp32 in/out)"),
             "data": "synthetic (torch.randn, seeded)",
             "config": {"workload": wl.workload, "l2": wl.l2,
                        "parallelism": f"repetition space sharded by contiguous blocks over {world} rank(s)"},

@@ -59,6 +59,9 @@ typedef enum aol_op {
   AOL_OP_REL_RESIDUAL = 9,/* ports: num, den, z                         z = sqrt(num)/sqrt(den)      */
   AOL_OP_PARTIALS_SUM = 10,/* ports: partials (count elements), s       s = ((p0 + p1) + p2) ... fp64,
                               ascending device order (refexec.py:483-486); first must be 0 */
+  AOL_OP_SCALAR_SEQ = 11, /* ports: the scalars used; count = n ops (1..8); scalars: per op
+                              (op 7|8|9, in0, in1 (-1 for neg), out) as port indices — several
+                              host scalar ops in program order in ONE launch */
   AOL_OP_TILE_COPY = 16,  /* ports: src, dst           tilers: src, dst                        */
   AOL_OP_MATMUL = 17,     /* ports: a, b, c            tilers: a, b, c   c = sum_k a_k * b_k   */
   AOL_OP_TILE_FILTER = 18,/* ports: x, w, y            tilers: x, y      y_j = sum_i w_ji x_i  */
@@ -163,6 +166,27 @@ int aol_loop_begin(void* stream, const void* relres_dev, int relres_dtype, doubl
 int aol_loop_end(aol_loop* loop);
 int aol_loop_run(aol_loop* loop, void* stream, int64_t* iterations, double* final_relres, int* converged);
 int aol_loop_destroy(aol_loop* loop);
+
+/* A LoopStep body as ONE persistent cooperative kernel (no launch and no host round trip
+ * per iteration).  `ops` is the body in schedule order, one entry per
+ * KernelLaunch / host scalar op; `port` holds indices into `ports` in the aol_launch port
+ * order (scale/axpy: the scalar `a` after the vectors).  All ops share `dtype` (f32/f64);
+ * spmv index arrays are `index_dtype`.  Runs until scalar port `relres_port` <= tol or
+ * max_iter iterations, like refexec.py:525-541, with results bit-identical to launching
+ * the same ops one by one.  Returns AOL_EUNSUPPORTED (nothing launched) for bodies
+ * outside its op set (copy/sub/scale/axpy/spmv_csr/dot_partial/div/neg/rel_residual),
+ * > 40 ops or > 32 ports; callers then fall back to aol_loop_begin/end/run. */
+typedef struct aol_loop_op {
+  int32_t op;
+  int32_t n_scalars;       /* axpy: 1 -> y += a*x, 0 -> y += x */
+  int32_t part, n_parts;   /* dot_partial: launch index in its step, launches in the step */
+  int64_t first, count;    /* the launch range (ignored for scalar ops) */
+  int32_t port[6];
+} aol_loop_op;
+
+int aol_loop_persistent(const aol_loop_op* ops, int n_ops, void* const* ports, int n_ports, int dtype,
+                        int index_dtype, int relres_port, double tol, int64_t max_iter, void* stream,
+                        int64_t* iterations, double* final_relres, int* converged);
 
 #ifdef __cplusplus
 }

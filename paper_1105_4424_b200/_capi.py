@@ -21,14 +21,14 @@ MAX_TILERS = 4
 AOL_OK, AOL_EINVAL, AOL_ECUDA, AOL_EUNSUPPORTED, AOL_ENODEV = 0, -1, -2, -3, -4
 DTYPE = {"float32": 0, "float64": 1, "int32": 2, "int64": 3}
 OP = {"copy": 1, "sub": 2, "scale": 3, "axpy": 4, "spmv_csr": 5, "dot_partial": 6,
-      "div": 7, "neg": 8, "rel_residual": 9, "partials_sum": 10,
+      "div": 7, "neg": 8, "rel_residual": 9, "partials_sum": 10, "scalar_seq": 11,
       "tile_copy": 16, "matmul": 17, "tile_filter": 18, "hfilter": 18, "vfilter": 18,
       "stencil": 18, "tile_sum": 19}
 PRECISION = {"default": 0, "tf32": 1, "3xtf32": 2, "exact": 3}
 
 EXPORTS = ("aol_abi_version", "aol_last_error", "aol_device_count", "aol_validate", "aol_launch",
            "aol_plan_name", "aol_tiler_offsets", "aol_launch_counter", "aol_launch_fused2", "aol_loop_begin",
-           "aol_loop_end", "aol_loop_run", "aol_loop_destroy")
+           "aol_loop_end", "aol_loop_run", "aol_loop_destroy", "aol_loop_persistent")
 
 
 class NativeLibraryError(RuntimeError):
@@ -123,6 +123,9 @@ def load(path: Path | str | None = None) -> C.CDLL:
     lib.aol_loop_run.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_double),
                                  C.POINTER(C.c_int)]
     lib.aol_loop_destroy.argtypes = [C.c_void_p]
+    lib.aol_loop_persistent.argtypes = [C.POINTER(AolLoopOp), C.c_int, C.POINTER(C.c_void_p), C.c_int, C.c_int,
+                                        C.c_int, C.c_int, C.c_double, C.c_int64, C.c_void_p,
+                                        C.POINTER(C.c_int64), C.POINTER(C.c_double), C.POINTER(C.c_int)]
     if lib.aol_abi_version() != ABI_VERSION:
         raise NativeLibraryError(f"{p}: ABI {lib.aol_abi_version()} != expected {ABI_VERSION}")
     _lib = lib
@@ -176,6 +179,34 @@ def launch_fused2(producer: AolTask, consumer: AolTask, first: int, count: int, 
         return False
     check(rc)
     return True
+
+
+class AolLoopOp(C.Structure):
+    _fields_ = [("op", C.c_int32), ("n_scalars", C.c_int32), ("part", C.c_int32), ("n_parts", C.c_int32),
+                ("first", C.c_int64), ("count", C.c_int64), ("port", C.c_int32 * 6)]
+
+
+def loop_op(op: str, ports: list[int], first: int = 0, count: int = 0, n_scalars: int = 0, part: int = 0,
+            n_parts: int = 1) -> AolLoopOp:
+    o = AolLoopOp(op=OP[op], n_scalars=n_scalars, part=part, n_parts=n_parts, first=int(first), count=int(count))
+    for i, p in enumerate(list(ports) + [-1] * (6 - len(ports))):
+        o.port[i] = p
+    return o
+
+
+def loop_persistent(ops: list[AolLoopOp], ports: list[int], dtype: str, index_dtype: str, relres_port: int,
+                    tol: float, max_iter: int, stream: int = 0):
+    """Run a LoopStep body as one persistent kernel: (iterations, relres, converged), or None
+    when the body is outside the interpreter's op set (nothing launched)."""
+    arr = (AolLoopOp * len(ops))(*ops)
+    it, rr, cv = C.c_int64(), C.c_double(), C.c_int()
+    rc = load().aol_loop_persistent(arr, len(ops), _ptrs(ports), len(ports), DTYPE[dtype], DTYPE[index_dtype],
+                                    int(relres_port), float(tol), int(max_iter), C.c_void_p(int(stream)),
+                                    C.byref(it), C.byref(rr), C.byref(cv))
+    if rc == AOL_EUNSUPPORTED:
+        return None
+    check(rc)
+    return it.value, rr.value, bool(cv.value)
 
 
 def loop_begin(stream: int, relres_ptr: int, dtype: str, tol: float, max_iter: int) -> int:

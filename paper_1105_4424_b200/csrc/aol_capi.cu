@@ -51,7 +51,7 @@ static int validate(const aol_task* t) {
   if (!t) return fail(AOL_EINVAL, "null task");
   if (t->dtype < AOL_F32 || t->dtype > AOL_I64) return fail(AOL_EINVAL, "bad dtype");
   const int need = tilers_needed(t->op);
-  const bool ident = t->op >= AOL_OP_COPY && t->op <= AOL_OP_PARTIALS_SUM;
+  const bool ident = t->op >= AOL_OP_COPY && t->op <= AOL_OP_SCALAR_SEQ;
   if (!ident && need == 0) return fail(AOL_EUNSUPPORTED, "unknown op " + std::to_string(t->op));
   if (t->n_tilers != need) return fail(AOL_EINVAL, "op needs " + std::to_string(need) + " tilers");
   if (need) {

@@ -7,19 +7,12 @@
 // axpy/spmv_csr are bit-exact with the reference; dot_partial is a
 // deterministic warp-shuffle tree (tolerance-pinned like the reference's BLAS
 // dot, tests/test_refexec.py:374-389).
+#include <algorithm>
+
 #include "aol_common.cuh"
+#include "aol_ident.cuh"
 
 namespace aol {
-
-template <typename T> __device__ __forceinline__ T mul_rn(T a, T b);
-template <> __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
-template <> __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
-template <typename T> __device__ __forceinline__ T add_rn(T a, T b);
-template <> __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
-template <> __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
-template <typename T> __device__ __forceinline__ T sub_rn(T a, T b);
-template <> __device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
-template <> __device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
 
 #define GRID_STRIDE(i, first, count)                                            \
   for (int64_t i = (first) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;    \
@@ -65,52 +58,74 @@ __global__ void k_spmv(const I* __restrict__ rowptr, const I* __restrict__ colid
   }
 }
 
-// Deterministic two-level dot: fixed grid, each block reduces a fixed slice with
-// warp shuffles, a single block then sums the block partials in index order.
-constexpr int kDotBlocks = 1024;
-
+// Deterministic single-pass dot: a fixed grid of kDotBlocks blocks, each reduces a fixed
+// slice with warp shuffles into part[block]; the last block to finish (atomic ticket) sums
+// the block partials in index order with the fixed 32 x 32 warp-shuffle tree.  One launch
+// per dot instead of two; the result does not depend on block scheduling.
 template <typename T>
-__device__ __forceinline__ T warp_sum(T v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-template <typename T>
-__global__ void __launch_bounds__(256) k_dot_blocks(const T* __restrict__ a, const T* __restrict__ b,
-                                                    int64_t first, int64_t count, double* __restrict__ part) {
+__global__ void __launch_bounds__(256) k_dot(const T* __restrict__ a, const T* __restrict__ b, int64_t first,
+                                             int64_t count, double* __restrict__ part, unsigned* __restrict__ ticket,
+                                             T* __restrict__ out) {
   double acc = 0.0;
-  GRID_STRIDE(i, first, count) acc += (double)a[i] * (double)b[i];
-  __shared__ double red[8];
+  GRID_STRIDE(i, first, count) acc = fma((double)a[i], (double)b[i], acc);
+  __shared__ double red[32];
+  __shared__ bool last;
   acc = warp_sum(acc);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
   __syncthreads();
   if (threadIdx.x < 32) {
     double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
     v = warp_sum(v);
-    if (threadIdx.x == 0) part[blockIdx.x] = v;
+    if (threadIdx.x == 0) {
+      part[blockIdx.x] = v;
+      __threadfence();
+      last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
   }
-}
-
-template <typename T>
-__global__ void __launch_bounds__(1024) k_dot_final(const double* __restrict__ part, int n, T* __restrict__ out) {
-  __shared__ double red[32];
-  double v = threadIdx.x < n ? part[threadIdx.x] : 0.0;
-  v = warp_sum(v);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // 8 warps x 4 groups of 32 partials: group g = part[32g .. 32g+31], lane order, then the
+  // 32 group sums in order -- the same tree as one 1024-thread block.
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int g = w; g < kDotBlocks / 32; g += blockDim.x >> 5) {
+    double v = __ldcg(part + g * 32 + lane);
+    v = warp_sum(v);
+    if (lane == 0) red[g] = v;
+  }
   __syncthreads();
   if (threadIdx.x < 32) {
-    v = red[threadIdx.x];
+    double v = red[threadIdx.x];
     v = warp_sum(v);
-    if (threadIdx.x == 0) out[0] = (T)v;
+    if (threadIdx.x == 0) {
+      out[0] = (T)__dadd_rn(0.0, v);      // 0.0 + v: the reference's combine of one partial
+      *ticket = 0;
+    }
   }
 }
 
+// Several host scalar ops (refexec.py:462-474) in one one-thread launch: op k reads ports
+// in0/in1 and writes port out, in program order.
+struct ScalarSeq {
+  int n;
+  int op[kMaxScalarSeq];
+  int in0[kMaxScalarSeq], in1[kMaxScalarSeq], out[kMaxScalarSeq];
+  void* ports[3 * kMaxScalarSeq];
+};
+
+// Per device: kDotBlocks partials followed by the ticket counter (zeroed once, reset by
+// the last block of every dot).
 static double* dot_scratch(int dev) {
   static double* bufs[64] = {nullptr};
   if (dev < 0 || dev >= 64) return nullptr;
   if (!bufs[dev]) {
-    if (cudaMalloc(&bufs[dev], kDotBlocks * sizeof(double)) != cudaSuccess) bufs[dev] = nullptr;
+    double* p = nullptr;
+    if (cudaMalloc(&p, (kDotBlocks + 1) * sizeof(double)) != cudaSuccess) return nullptr;
+    if (cudaMemset(p, 0, (kDotBlocks + 1) * sizeof(double)) != cudaSuccess) {
+      cudaFree(p);
+      return nullptr;
+    }
+    bufs[dev] = p;
   }
   return bufs[dev];
 }
@@ -134,6 +149,21 @@ __global__ void k_partials_sum(const T* p, int n, T* s) {
   double total = 0.0;
   for (int i = 0; i < n; ++i) total = __dadd_rn(total, (double)p[i]);
   s[0] = (T)total;
+}
+
+template <typename T>
+__global__ void k_scalar_seq(ScalarSeq q) {
+  for (int k = 0; k < q.n; ++k) {
+    const T* a = (const T*)q.ports[q.in0[k]];
+    const T* b = q.in1[k] >= 0 ? (const T*)q.ports[q.in1[k]] : nullptr;
+    T* z = (T*)q.ports[q.out[k]];
+    switch (q.op[k]) {
+      case AOL_OP_SCALAR_DIV: z[0] = (T)((double)a[0] / (double)b[0]); break;
+      case AOL_OP_SCALAR_NEG: z[0] = -a[0]; break;
+      case AOL_OP_REL_RESIDUAL: z[0] = (T)(sqrt((double)a[0]) / sqrt((double)b[0])); break;
+      default: break;
+    }
+  }
 }
 
 double* dot_scratch_for_current_device() {
@@ -194,9 +224,35 @@ static int launch_ident_t(const aol_task& t, int64_t first, int64_t count, void*
       AOL_CUDA_CHECK(cudaGetDevice(&dev));
       double* part = dot_scratch(dev);
       if (!part) return fail(AOL_ECUDA, "cannot allocate dot scratch");
-      k_dot_blocks<T><<<kDotBlocks, 256, 0, s>>>((const T*)ports[0], (const T*)ports[1], first, count, part);
-      AOL_LAUNCH_CHECK("k_dot_blocks");
-      k_dot_final<T><<<1, kDotBlocks, 0, s>>>(part, kDotBlocks, (T*)ports[2]);
+      k_dot<T><<<kDotBlocks, 256, 0, s>>>((const T*)ports[0], (const T*)ports[1], first, count, part,
+                                          reinterpret_cast<unsigned*>(part + kDotBlocks), (T*)ports[2]);
+      break;
+    }
+    case AOL_OP_SCALAR_SEQ: {
+      // count = number of ops; scalars = (op, in0, in1, out) per op; in1 = -1 when unused
+      if (count < 1 || count > kMaxScalarSeq || !scalars)
+        return fail(AOL_EINVAL, "scalar_seq needs 1..8 ops and their (op, in0, in1, out) program");
+      ScalarSeq q{};
+      q.n = (int)count;
+      int np = 0;
+      for (int k = 0; k < q.n; ++k) {
+        q.op[k] = (int)scalars[4 * k];
+        q.in0[k] = (int)scalars[4 * k + 1];
+        q.in1[k] = (int)scalars[4 * k + 2];
+        q.out[k] = (int)scalars[4 * k + 3];
+        const bool two = q.op[k] != AOL_OP_SCALAR_NEG;
+        if (q.op[k] < AOL_OP_SCALAR_DIV || q.op[k] > AOL_OP_REL_RESIDUAL)
+          return fail(AOL_EINVAL, "scalar_seq: op must be div, neg or rel_residual");
+        if (q.in0[k] < 0 || q.out[k] < 0 || (two && q.in1[k] < 0))
+          return fail(AOL_EINVAL, "scalar_seq: bad port index");
+        np = std::max(np, std::max(q.in0[k], std::max(q.in1[k], q.out[k])) + 1);
+      }
+      if (np > 3 * kMaxScalarSeq) return fail(AOL_EINVAL, "scalar_seq: too many ports");
+      for (int i = 0; i < np; ++i) {
+        if (!ports[i]) return fail(AOL_EINVAL, "scalar_seq: null port");
+        q.ports[i] = ports[i];
+      }
+      k_scalar_seq<T><<<1, 1, 0, s>>>(q);
       break;
     }
     default:

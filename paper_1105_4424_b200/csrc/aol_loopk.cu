@@ -1,0 +1,612 @@
+// A whole LoopStep (refexec.py:525-541) as ONE persistent cooperative kernel.
+//
+// The loop body of identity ops (copy/sub/scale/axpy/spmv_csr/dot_partial and the host
+// scalar ops div/neg/rel_residual) is passed as a small program.  One CTA per SM runs
+// it until relres <= tol or max_iter, so there is no launch and no host round trip per
+// iteration.  Three rules keep every value bit-identical to the per-op kernels:
+//
+//  * element mapping: every vector op (and every dot) walks [first, first+count) in the
+//    dot's fixed 1024 x 256 "virtual block" order.  Virtual block vb is run by one
+//    256-thread sub-block, and thread t of vb touches first + vb*256 + t + k*262144.
+//    So a value written by one elementwise op is re-read by the same thread.
+//  * grid barriers (cooperative groups) are placed by a host-side hazard pass (below).
+//    A barrier goes only before an op that re-reads a vector with a different mapping
+//    (spmv's x gather, or a different `first`), or overwrites one that was read that way.
+//    A dot always needs one barrier between its partials and the final tree.
+//  * scalars: every CTA keeps every scalar port in shared memory (as the port dtype,
+//    widened) and runs the dot final tree and the scalar ops redundantly.  Results are
+//    identical everywhere, so scalars never need a barrier; CTA 0 writes them back.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "aol_common.cuh"
+#include "aol_ident.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace aol {
+
+constexpr int kLoopMaxOps = 40;
+constexpr int kLoopMaxGroups = 40;
+constexpr int kLoopMaxPorts = 32;
+constexpr int kLoopMaxParts = 8;
+constexpr int kLoopSub = 4;                   // 256-thread sub-blocks per CTA
+constexpr int kLoopThreads = 256 * kLoopSub;
+
+struct LOp {
+  int op, n_scalars, part, n_parts, dot;
+  int port[6];
+};
+
+// A group: consecutive vector ops over one launch range that need no barrier between them
+// (each thread re-reads only what it wrote), optionally closed by a dot.  Or a run of host
+// scalar ops.
+struct LGroup {
+  int barrier, op0, n_ops, scalar, dot;
+  int64_t first, count;
+};
+
+struct LProg {
+  int n_groups, n_ports, relres;
+  double tol;
+  int64_t max_iter;
+  unsigned scalar_mask;                       // bit p: port p is a scalar (lives in smem)
+  double* part;                               // [2][64][kDotBlocks] partials
+  int64_t* state;                             // iterations, relres (bits), converged
+  unsigned* ticket;                           // [2][64] arrivals per dot
+  unsigned* flag;                             // [2][64] last published dot sequence number
+  double* result;                             // [2][64] published dot values
+  unsigned long long* prof;                   // AOL_LOOP_PROFILE: ns per group, CTA 0's view
+  LGroup groups[kLoopMaxGroups];
+  LOp ops[kLoopMaxOps];
+  void* ports[kLoopMaxPorts];
+};
+
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void sub_sync(int sub) {
+  asm volatile("bar.sync %0, 256;" ::"r"(sub + 1) : "memory");
+}
+
+template <typename T, typename I>
+__global__ void __launch_bounds__(kLoopThreads, 1) k_loop_persistent(const __grid_constant__ LProg P) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sc[kLoopMaxPorts + kLoopMaxParts];
+  __shared__ double red[kLoopSub][8];
+  __shared__ double gred[32];
+  __shared__ int s_last;
+  unsigned seq = 0;                           // dots executed so far (same in every CTA)
+  const int sub = threadIdx.x >> 8, t = threadIdx.x & 255, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slot = blockIdx.x * kLoopSub + sub, nslots = gridDim.x * kLoopSub;
+  const bool writer = blockIdx.x == 0 && threadIdx.x == 0;
+  // the program lives in shared memory: the interpreter's dependent lookups (op -> port ->
+  // pointer) would otherwise be a chain of constant-cache misses per op
+  __shared__ LGroup s_groups[kLoopMaxGroups];
+  __shared__ LOp s_ops[kLoopMaxOps];
+  __shared__ void* s_ports[kLoopMaxPorts];
+  {
+    const int* src = reinterpret_cast<const int*>(P.groups);
+    int* dst = reinterpret_cast<int*>(s_groups);
+    for (int i = threadIdx.x; i < (int)(sizeof(LGroup) / 4) * P.n_groups; i += blockDim.x) dst[i] = src[i];
+    src = reinterpret_cast<const int*>(P.ops);
+    dst = reinterpret_cast<int*>(s_ops);
+    for (int i = threadIdx.x; i < (int)(sizeof(P.ops) / 4); i += blockDim.x) dst[i] = src[i];
+    if (threadIdx.x < kLoopMaxPorts) s_ports[threadIdx.x] = P.ports[threadIdx.x];
+  }
+  if (threadIdx.x < P.n_ports && ((P.scalar_mask >> threadIdx.x) & 1u))
+    sc[threadIdx.x] = (double)((const T*)P.ports[threadIdx.x])[0];
+  __syncthreads();
+
+  int64_t it = 0;
+  int parity = 0;
+  double relres = 0.0;
+  int converged = 0;
+  unsigned long long t_prev = 0;
+  if (P.prof && writer) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_prev));
+  for (;;) {
+    for (int gi = 0; gi < P.n_groups; ++gi) {
+      const LGroup& G = s_groups[gi];
+      if (P.prof && writer && gi > 0) {
+        unsigned long long now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        P.prof[gi - 1] += now - t_prev;
+        t_prev = now;
+      }
+      unsigned long long t_grp = 0;
+      if (P.prof && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_grp));
+      if (G.barrier) grid.sync();
+      if (G.scalar) {                                   // host scalar ops, redundantly per CTA
+        if (threadIdx.x == 0) for (int k = G.op0; k < G.op0 + G.n_ops; ++k) {
+          const LOp& o = s_ops[k];
+          double z;
+          int out;
+          if (o.op == AOL_OP_SCALAR_NEG) {
+            z = (double)(-(T)sc[o.port[0]]);
+            out = o.port[1];
+          } else if (o.op == AOL_OP_SCALAR_DIV) {
+            z = (double)(T)(sc[o.port[0]] / sc[o.port[1]]);
+            out = o.port[2];
+          } else {
+            z = (double)(T)(sqrt(sc[o.port[0]]) / sqrt(sc[o.port[1]]));
+            out = o.port[2];
+          }
+          sc[out] = z;
+          if (writer) ((T*)s_ports[out])[0] = (T)z;
+        }
+        __syncthreads();
+        continue;
+      }
+      const int last = G.op0 + G.n_ops;
+      // virtual blocks past the range hold no elements: their dot partials stay +0.0
+      const int vb_end = (int)std::min<int64_t>(kDotBlocks, (G.count + 255) / 256);
+      const int64_t end = G.first + G.count;
+#define LOOP_EW(i)                                                                      \
+  for (int vb = slot; vb < vb_end; vb += nslots)                                        \
+    for (int64_t i = G.first + (int64_t)vb * 256 + t; i < end; i += (int64_t)kDotBlocks * 256)
+      for (int k = G.op0; k < last; ++k) {
+        const LOp& o = s_ops[k];
+        switch (o.op) {
+          case AOL_OP_COPY: {
+            const T* src = (const T*)s_ports[o.port[0]];
+            T* dst = (T*)s_ports[o.port[1]];
+            LOOP_EW(i) dst[i] = src[i];
+            break;
+          }
+          case AOL_OP_SUB: {
+            const T* x = (const T*)s_ports[o.port[0]];
+            const T* y = (const T*)s_ports[o.port[1]];
+            T* z = (T*)s_ports[o.port[2]];
+            LOOP_EW(i) z[i] = sub_rn(x[i], y[i]);
+            break;
+          }
+          case AOL_OP_SCALE: {
+            T* y = (T*)s_ports[o.port[0]];
+            const T a = (T)sc[o.port[1]];
+            LOOP_EW(i) y[i] = mul_rn(y[i], a);
+            break;
+          }
+          case AOL_OP_AXPY: {
+            T* y = (T*)s_ports[o.port[0]];
+            const T* x = (const T*)s_ports[o.port[1]];
+            if (o.n_scalars) {
+              const T a = (T)sc[o.port[2]];
+              LOOP_EW(i) y[i] = add_rn(y[i], mul_rn(a, x[i]));
+            } else {
+              LOOP_EW(i) y[i] = add_rn(y[i], x[i]);
+            }
+            break;
+          }
+          case AOL_OP_SPMV_CSR: {
+            const I* rowptr = (const I*)s_ports[o.port[0]];
+            const I* colidx = (const I*)s_ports[o.port[1]];
+            const T* values = (const T*)s_ports[o.port[2]];
+            const T* x = (const T*)s_ports[o.port[3]];
+            T* y = (T*)s_ports[o.port[4]];
+            LOOP_EW(i) {
+              T acc = T(0);
+              const int64_t e = rowptr[i + 1];
+              for (int64_t q = rowptr[i]; q < e; ++q) acc = add_rn(acc, mul_rn(values[q], x[colidx[q]]));
+              y[i] = acc;
+            }
+            break;
+          }
+          case AOL_OP_DOT_PARTIAL: {                  // k_dot's per-block partials, exactly
+            const T* a = (const T*)s_ports[o.port[0]];
+            const T* b = (const T*)s_ports[o.port[1]];
+            double* part = P.part + ((size_t)parity * 64 + o.dot) * kDotBlocks;
+            for (int vb = slot; vb < vb_end; vb += nslots) {
+              double acc = 0.0;
+              for (int64_t i = G.first + (int64_t)vb * 256 + t; i < end; i += (int64_t)kDotBlocks * 256)
+                acc = fma((double)a[i], (double)b[i], acc);
+              acc = warp_sum(acc);
+              if (lane == 0) red[sub][t >> 5] = acc;
+              sub_sync(sub);
+              if (t < 32) {
+                double w = t < 8 ? red[sub][t] : 0.0;
+                w = warp_sum(w);
+                if (t == 0) part[vb] = w;
+              }
+              sub_sync(sub);
+            }
+            break;
+          }
+          default: break;
+        }
+      }
+#undef LOOP_EW
+      if (!G.dot) continue;
+      const LOp& o = s_ops[last - 1];
+      const double* part = P.part + ((size_t)parity * 64 + o.dot) * kDotBlocks;
+      const int cell = parity * 64 + o.dot;
+      unsigned long long t1 = 0, t2 = 0;
+      if (P.prof && threadIdx.x == 0) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        atomicAdd(P.prof + kLoopMaxGroups + 2 * blockIdx.x, t1 - t_grp);
+      }
+      // Ticket instead of a grid barrier: the last CTA to arrive runs k_dot's final tree
+      // once and publishes the value; the others wait for it and read 8 bytes.
+      ++seq;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(P.ticket + cell, 1u) == gridDim.x - 1;
+      }
+      __syncthreads();
+      if (s_last) {
+        __threadfence();
+        if (warp < 8) {
+          for (int g = warp; g < kDotBlocks / 32; g += 8) {
+            double w = __ldcg(part + g * 32 + lane);
+            w = warp_sum(w);
+            if (lane == 0) gred[g] = w;
+          }
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {
+          const double w = warp_sum(gred[lane]);
+          if (lane == 0) {
+            P.result[cell] = w;
+            P.ticket[cell] = 0;
+            __threadfence();
+            st_release(P.flag + cell, seq);
+          }
+        }
+      } else if (threadIdx.x == 0) {
+        while (ld_relaxed(P.flag + cell) != seq) __nanosleep(64);
+        __threadfence();
+      }
+      __syncthreads();
+      if (P.prof && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2));
+      if (threadIdx.x == 0) gred[0] = __ldcg(P.result + cell);
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        const double w = gred[0];
+        if (lane == 0) {
+          const double pv = (double)(T)__dadd_rn(0.0, w);
+          if (o.n_parts == 1) {
+            sc[o.port[2]] = pv;
+            if (writer) ((T*)s_ports[o.port[2]])[0] = (T)pv;
+          } else {
+            sc[kLoopMaxPorts + o.part] = pv;
+            if (o.part == o.n_parts - 1) {             // refexec.py:483-486: 0.0 + p0 + p1 ... in order
+              double total = 0.0;
+              for (int q = 0; q < o.n_parts; ++q) total = __dadd_rn(total, sc[kLoopMaxPorts + q]);
+              sc[o.port[2]] = (double)(T)total;
+              if (writer) ((T*)s_ports[o.port[2]])[0] = (T)total;
+            }
+          }
+        }
+      }
+      __syncthreads();
+      if (P.prof && threadIdx.x == 0) {
+        unsigned long long t3;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t3));
+        atomicAdd(P.prof + kLoopMaxGroups + 2 * blockIdx.x + 1, t3 - t2);
+      }
+    }
+    if (P.prof && writer) {
+      unsigned long long now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      P.prof[P.n_groups - 1] += now - t_prev;
+      t_prev = now;
+    }
+    ++it;
+    parity ^= 1;
+    relres = sc[P.relres];
+    if (relres <= P.tol) {
+      converged = 1;
+      break;
+    }
+    if (it >= P.max_iter) break;
+  }
+  if (writer) {
+    P.state[0] = it;
+    P.state[1] = __double_as_longlong(relres);
+    P.state[2] = converged;
+  }
+}
+
+// -- host side: program checks, grouping and the barrier (hazard) pass ---------------
+
+namespace {
+
+enum Acc { R = 0, W = 1, G = 2 };      // elementwise read / elementwise write / gather read
+struct Access {
+  int port;
+  Acc mode;
+  int arg;                             // operand position in aol_loop_op.port
+};
+
+// vector accesses of one op in evaluation order (reads before the write)
+std::vector<Access> vector_accesses(const aol_loop_op& o) {
+  switch (o.op) {
+    case AOL_OP_COPY: return {{o.port[0], R, 0}, {o.port[1], W, 1}};
+    case AOL_OP_SUB: return {{o.port[0], R, 0}, {o.port[1], R, 1}, {o.port[2], W, 2}};
+    case AOL_OP_SCALE: return {{o.port[0], R, 0}, {o.port[0], W, 0}};
+    case AOL_OP_AXPY: return {{o.port[0], R, 0}, {o.port[1], R, 1}, {o.port[0], W, 0}};
+    case AOL_OP_SPMV_CSR:
+      return {{o.port[0], G, 0}, {o.port[1], G, 1}, {o.port[2], G, 2}, {o.port[3], G, 3}, {o.port[4], W, 4}};
+    case AOL_OP_DOT_PARTIAL: return {{o.port[0], R, 0}, {o.port[1], R, 1}};
+    default: return {};
+  }
+}
+
+std::vector<int> scalar_ports(const aol_loop_op& o) {
+  switch (o.op) {
+    case AOL_OP_SCALE: return {o.port[1]};
+    case AOL_OP_AXPY: return o.n_scalars ? std::vector<int>{o.port[2]} : std::vector<int>{};
+    case AOL_OP_DOT_PARTIAL: return {o.port[2]};
+    case AOL_OP_SCALAR_DIV: return {o.port[0], o.port[1], o.port[2]};
+    case AOL_OP_SCALAR_NEG: return {o.port[0], o.port[1]};
+    case AOL_OP_REL_RESIDUAL: return {o.port[0], o.port[1], o.port[2]};
+    default: return {};
+  }
+}
+
+bool is_scalar_op(int op) {
+  return op == AOL_OP_SCALAR_DIV || op == AOL_OP_SCALAR_NEG || op == AOL_OP_REL_RESIDUAL;
+}
+
+struct Seen {
+  int port;
+  Acc mode;
+  int64_t key;
+};
+
+// Does access `a` (under launch key `key`) race with an access made since the last barrier?
+// Same-key elementwise accesses are the same thread's; everything else crosses threads.
+bool conflicts(const std::vector<Seen>& seen, const Access& a, int64_t key) {
+  for (const Seen& s : seen) {
+    if (s.port != a.port) continue;
+    if (a.mode == G && s.mode == W) return true;
+    if (a.mode == R && s.mode == W && s.key != key) return true;
+    if (a.mode == W && (s.mode == G || s.key != key)) return true;
+  }
+  return false;
+}
+
+struct Plan {
+  std::vector<LGroup> groups;
+  std::vector<LOp> ops;
+};
+
+// Split the body into groups and mark the groups that must start with a grid barrier.
+// Barrier flags are decided over two passes of the body, because the loop wraps.
+Plan plan_groups(const aol_loop_op* ops, int n) {
+  Plan pl;
+  // 1. grouping (independent of the wrap): a new group at every scalar op, key change,
+  //    in-group race, and after every dot
+  {
+    std::vector<Seen> in_group;
+    LGroup cur{};
+    bool open = false;
+    auto close = [&]() {
+      if (open) pl.groups.push_back(cur);
+      open = false;
+      in_group.clear();
+    };
+    for (int k = 0; k < n; ++k) {
+      const aol_loop_op& o = ops[k];
+      LOp d{};
+      d.op = o.op;
+      d.n_scalars = o.n_scalars;
+      d.part = o.part;
+      d.n_parts = o.n_parts;
+      for (int q = 0; q < 6; ++q) d.port[q] = o.port[q];
+      if (is_scalar_op(o.op)) {
+        close();
+        if (!pl.groups.empty() && pl.groups.back().scalar && pl.groups.back().op0 + pl.groups.back().n_ops == k) {
+          pl.groups.back().n_ops++;
+          pl.ops.push_back(d);
+          continue;
+        }
+        LGroup g{};
+        g.scalar = 1;
+        g.op0 = k;
+        g.n_ops = 1;
+        pl.groups.push_back(g);
+        pl.ops.push_back(d);
+        continue;
+      }
+      const std::vector<Access> acc = vector_accesses(o);
+      bool fresh = !open || cur.first != o.first || cur.count != o.count;
+      if (!fresh)
+        for (const Access& a : acc) fresh = fresh || conflicts(in_group, a, o.first);
+      if (fresh) {
+        close();
+        cur = LGroup{};
+        cur.op0 = k;
+        cur.first = o.first;
+        cur.count = o.count;
+        open = true;
+      }
+      for (const Access& a : acc) in_group.push_back({a.port, a.mode, o.first});
+      cur.n_ops = k - cur.op0 + 1;
+      pl.ops.push_back(d);
+      if (o.op == AOL_OP_DOT_PARTIAL) {
+        cur.dot = 1;
+        close();
+      }
+    }
+    close();
+  }
+  // 2. barriers, over body + body
+  std::vector<Seen> seen;
+  for (int pass = 0; pass < 2; ++pass) {
+    for (LGroup& g : pl.groups) {
+      if (g.scalar) continue;
+      std::vector<Access> acc;
+      for (int k = g.op0; k < g.op0 + g.n_ops; ++k)
+        for (const Access& a : vector_accesses(ops[k])) acc.push_back(a);
+      bool need = false;
+      for (const Access& a : acc) need = need || conflicts(seen, a, g.first);
+      if (need) {
+        g.barrier = 1;
+        seen.clear();
+      }
+      for (const Access& a : acc) seen.push_back({a.port, a.mode, g.first});
+      if (g.dot) seen.clear();                        // the dot's own barrier
+    }
+  }
+  return pl;
+}
+
+}  // namespace
+
+}  // namespace aol
+
+using namespace aol;
+
+extern "C" int aol_loop_persistent(const aol_loop_op* ops, int n_ops, void* const* ports, int n_ports, int dtype,
+                                   int index_dtype, int relres_port, double tol, int64_t max_iter, void* stream,
+                                   int64_t* iterations, double* final_relres, int* converged) {
+  if (!ops || !ports || n_ops < 1 || max_iter < 1) return fail(AOL_EINVAL, "aol_loop_persistent: bad arguments");
+  if (n_ops > kLoopMaxOps || n_ports > kLoopMaxPorts)
+    return fail(AOL_EUNSUPPORTED, "loop body too large for the persistent interpreter");
+  if (dtype != AOL_F32 && dtype != AOL_F64) return fail(AOL_EUNSUPPORTED, "persistent loop needs float32/float64");
+  if (index_dtype != AOL_I32 && index_dtype != AOL_I64) return fail(AOL_EINVAL, "bad index dtype");
+  if (relres_port < 0 || relres_port >= n_ports) return fail(AOL_EINVAL, "bad relres port");
+  LProg P{};
+  P.n_ports = n_ports;
+  P.relres = relres_port;
+  P.tol = tol;
+  P.max_iter = max_iter;
+  unsigned scalar = 0, vector = 0;
+  int n_dots = 0;
+  for (int k = 0; k < n_ops; ++k) {
+    const aol_loop_op& o = ops[k];
+    switch (o.op) {
+      case AOL_OP_COPY: case AOL_OP_SUB: case AOL_OP_SCALE: case AOL_OP_AXPY: case AOL_OP_SPMV_CSR:
+      case AOL_OP_DOT_PARTIAL: case AOL_OP_SCALAR_DIV: case AOL_OP_SCALAR_NEG: case AOL_OP_REL_RESIDUAL:
+        break;
+      default:
+        return fail(AOL_EUNSUPPORTED, "op " + std::to_string(o.op) + " not in the persistent interpreter");
+    }
+    for (int q = 0; q < 6; ++q)
+      if (o.port[q] >= n_ports) return fail(AOL_EINVAL, "port index out of range");
+    if (o.first < 0 || o.count < 0) return fail(AOL_EINVAL, "bad launch range");
+    if (o.op == AOL_OP_DOT_PARTIAL) {
+      if (o.n_parts < 1 || o.n_parts > kLoopMaxParts || o.part < 0 || o.part >= o.n_parts)
+        return fail(AOL_EUNSUPPORTED, "dot partial index out of range");
+      if (n_dots >= 64) return fail(AOL_EUNSUPPORTED, "too many dots");
+      ++n_dots;
+    }
+    for (const Access& a : vector_accesses(o)) {
+      if (a.port < 0) return fail(AOL_EINVAL, "port index out of range");
+      vector |= 1u << a.port;
+    }
+    for (int p : scalar_ports(o)) {
+      if (p < 0) return fail(AOL_EINVAL, "port index out of range");
+      scalar |= 1u << p;
+    }
+  }
+  if (scalar & vector) return fail(AOL_EUNSUPPORTED, "a port is used both as a scalar and as a vector");
+  if (!((scalar >> relres_port) & 1u)) return fail(AOL_EUNSUPPORTED, "relres is not a scalar of the body");
+  for (int p = 0; p < n_ports; ++p)
+    if (!ports[p]) return fail(AOL_EINVAL, "null port");
+  Plan pl = plan_groups(ops, n_ops);
+  if ( (int)pl.groups.size() > kLoopMaxGroups)
+    return fail(AOL_EUNSUPPORTED, "loop body does not fit the persistent interpreter");
+  int dot = 0;
+  for (int k = 0; k < n_ops; ++k) {
+    P.ops[k] = pl.ops[k];
+    P.ops[k].dot = ops[k].op == AOL_OP_DOT_PARTIAL ? dot++ : 0;
+  }
+  for (size_t g = 0; g < pl.groups.size(); ++g) P.groups[g] = pl.groups[g];
+  P.n_groups = (int)pl.groups.size();
+  for (int p = 0; p < n_ports; ++p) P.ports[p] = ports[p];
+  P.scalar_mask = scalar;
+
+  int dev = 0, coop = 0, per_sm = 0, sms = 0;
+  AOL_CUDA_CHECK(cudaGetDevice(&dev));
+  AOL_CUDA_CHECK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+  AOL_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  if (!coop) return fail(AOL_EUNSUPPORTED, "device has no cooperative launch");
+  void (*kern)(LProg);
+  if (dtype == AOL_F64) kern = index_dtype == AOL_I64 ? k_loop_persistent<double, int64_t> : k_loop_persistent<double, int32_t>;
+  else kern = index_dtype == AOL_I64 ? k_loop_persistent<float, int64_t> : k_loop_persistent<float, int32_t>;
+  AOL_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kLoopThreads, 0));
+  if (per_sm < 1) return fail(AOL_EUNSUPPORTED, "persistent loop kernel does not fit on an SM");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t part_bytes = (size_t)2 * 64 * kDotBlocks * sizeof(double);
+  const size_t prof_bytes = (kLoopMaxGroups + 2 * 1024) * sizeof(unsigned long long);
+  const char* prof_env = getenv("AOL_LOOP_PROFILE");
+  const bool profile = prof_env && prof_env[0] == '1';
+  char* scratch = nullptr;
+  const size_t sync_bytes = 128 * (4 + 4 + 8);
+  AOL_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&scratch), part_bytes + 64 + sync_bytes + prof_bytes, s));
+  P.part = reinterpret_cast<double*>(scratch);
+  P.state = reinterpret_cast<int64_t*>(scratch + part_bytes);
+  P.ticket = reinterpret_cast<unsigned*>(scratch + part_bytes + 64);
+  P.flag = P.ticket + 128;
+  P.result = reinterpret_cast<double*>(P.flag + 128);
+  AOL_CUDA_CHECK(cudaMemsetAsync(P.ticket, 0, sync_bytes, s));
+  AOL_CUDA_CHECK(cudaMemsetAsync(P.part, 0, part_bytes, s));
+  P.prof = profile ? reinterpret_cast<unsigned long long*>(scratch + part_bytes + 64 + sync_bytes) : nullptr;
+  if (profile) AOL_CUDA_CHECK(cudaMemsetAsync(P.prof, 0, prof_bytes, s));
+  void* args[] = {&P};
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  if (profile) {
+    cudaEventCreate(&ev0);
+    cudaEventCreate(&ev1);
+    cudaEventRecord(ev0, s);
+  }
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)kern, dim3(sms), dim3(kLoopThreads), args, 0, s);
+  if (profile) cudaEventRecord(ev1, s);
+  int64_t h[3] = {0, 0, 0};
+  static unsigned long long prof[kLoopMaxGroups + 2 * 1024];
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h, P.state, sizeof(h), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && profile) e = cudaMemcpyAsync(prof, P.prof, prof_bytes, cudaMemcpyDeviceToHost, s);
+  cudaFreeAsync(scratch, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "aol_loop_persistent");
+  count_launch();
+  if (profile) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ev0, ev1);
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+    fprintf(stderr, "aol_loop_persistent kernel %.3f ms, %lld iterations, %.2f us/iter\n", ms, (long long)h[0],
+            1e3 * ms / (h[0] ? h[0] : 1));
+    for (int g = 0; g < P.n_groups; ++g) {
+      const LGroup& G = P.groups[g];
+      if (g == 0) {
+        double mn = 1e30, mx = 0, sum = 0, tmn = 1e30, tmx = 0;
+        int amx = 0;
+        for (int c = 0; c < sms; ++c) {
+          const double pre = prof[kLoopMaxGroups + 2 * c] * 1e-3 / h[0], tree = prof[kLoopMaxGroups + 2 * c + 1] * 1e-3 / h[0];
+          mn = std::min(mn, pre);
+          if (pre > mx) { mx = pre; amx = c; }
+          sum += pre;
+          tmn = std::min(tmn, tree);
+          tmx = std::max(tmx, tree);
+        }
+        fprintf(stderr, "aol_loop_persistent dots, per CTA us/iter: before barrier min %.2f mean %.2f max %.2f (cta %d);"
+                " tree min %.2f max %.2f\n", mn, sum / sms, mx, amx, tmn, tmx);
+      }
+      fprintf(stderr, "aol_loop_persistent group %2d: %s op0=%d n_ops=%d barrier=%d dot=%d  %.2f us/iter\n", g,
+              G.scalar ? "scalar" : "vector", G.op0, G.n_ops, G.barrier, G.dot, h[0] ? prof[g] * 1e-3 / h[0] : 0.0);
+    }
+  }
+  if (iterations) *iterations = h[0];
+  if (final_relres) {
+    double r;
+    memcpy(&r, &h[1], sizeof(r));
+    *final_relres = r;
+  }
+  if (converged) *converged = (int)h[2];
+  return AOL_OK;
+}

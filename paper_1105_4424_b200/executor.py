@@ -27,6 +27,7 @@ There is no CPU fallback: a missing library raises.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -168,6 +169,7 @@ class _Task:
                 ps.name for ps in spec.ports if not ps.integer and not ps.scalar)
             self.dtype = enum_value(comp.port(val).data_type)
             index_dtype = enum_value(comp.port("rowptr").data_type) if spec.name == "spmv_csr" else "int32"
+            self.index_dtype = index_dtype
             self.scalar_ports = [ps.name for ps in spec.ports
                                  if ps.scalar and enum_value(ps.direction) == "in" and comp.port(ps.name)]
             self.port_order = [ps.name for ps in spec.ports
@@ -206,6 +208,9 @@ class Executor:
         self._gbufs: dict[str, object] = {}
         self._dev_tasks: dict[str, object] = {}
         self.device_loops = 0
+        self.persistent_loops = 0
+        self.persistent = os.environ.get("AOL_LOOP_PERSISTENT", "1") != "0"
+        self._programs: dict[str, object] = {}
         self._fusable: dict[tuple, bool] = {}
         self.fused_launches = 0
         self._dot_buf = None
@@ -413,32 +418,127 @@ class Executor:
         return d
 
     def _run_body_device(self, body) -> None:
-        """Enqueue one loop iteration with no host round trip (capturable)."""
-        torch = _torch()
+        """Enqueue one loop iteration with no host round trip (capturable).
+
+        Consecutive host scalar ops of one dtype go out as ONE scalar_seq launch; a dot
+        with a single launch writes its result straight into `s` (the kernel stores
+        0.0 + partial, which is the reference's combine of one partial)."""
         s = self._stream_handle()
-        for step in body:
+        i = 0
+        while i < len(body):
+            step = body[i]
             t = self.task(step.task_path)
             arrays = {name: self.storage.array(node) for name, node in t.nodes.items()}
+            if not hasattr(step, "launches"):
+                j = i
+                dt = enum_value(t.comp.ports[0].data_type)
+                while (j < len(body) and j - i < 8 and not hasattr(body[j], "launches")
+                       and enum_value(self.task(body[j].task_path).comp.ports[0].data_type) == dt):
+                    j += 1
+                self._scalar_seq(body[i:j], dt, s)
+                i = j
+                continue
+            i += 1
             if step.op == "dot_partial":
+                if len(step.launches) == 1:
+                    l = step.launches[0]
+                    _capi.launch(t.ctask, l.range.offset, l.range.count,
+                                 [arrays["a"].data_ptr(), arrays["b"].data_ptr(), arrays["s"].data_ptr()], (), s)
+                    continue
                 buf = self._gbufs[step.task_path]
-                for i, l in enumerate(step.launches):
+                for k, l in enumerate(step.launches):
                     _capi.launch(t.ctask, l.range.offset, l.range.count,
                                  [arrays["a"].data_ptr(), arrays["b"].data_ptr(),
-                                  buf.data_ptr() + i * buf.element_size()], (), s)
+                                  buf.data_ptr() + k * buf.element_size()], (), s)
                 ctask = _capi.make_task("partials_sum", t.dtype)
                 _capi.launch(ctask, 0, len(step.launches), [buf.data_ptr(), arrays["s"].data_ptr()], (), s)
                 continue
             ctask, names = self._dev_task(step)
             ptrs = [arrays[n].data_ptr() for n in names]
-            if not hasattr(step, "launches"):
-                _capi.launch(ctask, 0, 1, ptrs, (), s)
-                continue
             for l in step.launches:
                 _capi.launch(ctask, l.range.offset, l.range.count, ptrs, (), s)
 
+    def _scalar_seq(self, ops, dtype: str, stream) -> None:
+        """Host scalar ops (refexec.py:462-474) as one device launch, in program order."""
+        ptrs: list[int] = []
+        index: dict[int, int] = {}
+
+        def slot(ptr: int) -> int:
+            if ptr not in index:
+                index[ptr] = len(ptrs)
+                ptrs.append(ptr)
+            return index[ptr]
+        prog: list[float] = []
+        for op in ops:
+            t = self.task(op.task_path)
+            names = [ps.name for ps in t.spec.ports]
+            p = [self.storage.array(t.nodes[n]).data_ptr() for n in names]
+            if op.op == "neg":
+                prog += [_capi.OP["neg"], slot(p[0]), -1, slot(p[1])]
+            else:
+                prog += [_capi.OP[op.op], slot(p[0]), slot(p[1]), slot(p[2])]
+        _capi.launch(_capi.make_task("scalar_seq", dtype), 0, len(ops), ptrs, prog, stream)
+
+    _PERSISTENT_OPS = ("copy", "sub", "scale", "axpy", "spmv_csr", "dot_partial")
+
+    def _persistent_program(self, step):
+        """The LoopStep body as an aol_loop_persistent program: (ops, ports, dtype, index dtype,
+        relres slot), or None when it has ops outside the interpreter's set."""
+        ptrs: list[int] = []
+        slots: dict[int, int] = {}
+
+        def slot(arr) -> int:
+            p = arr.data_ptr()
+            if p not in slots:
+                slots[p] = len(ptrs)
+                ptrs.append(p)
+            return slots[p]
+        ops, dtypes, index = [], set(), set()
+        for st in step.body:
+            if hasattr(st, "body"):
+                return None
+            t = self.task(st.task_path)
+            arr = {n: self.storage.array(node) for n, node in t.nodes.items()}
+            if not hasattr(st, "launches"):
+                if st.op not in self._GRAPH_HOST_OPS:
+                    return None
+                dtypes.add(enum_value(t.comp.ports[0].data_type))
+                ops.append(_capi.loop_op(st.op, [slot(arr[ps.name]) for ps in t.spec.ports]))
+                continue
+            if st.op not in self._PERSISTENT_OPS:
+                return None
+            dtypes.add(t.dtype)
+            if st.op == "spmv_csr":
+                index.add(t.index_dtype)
+            ports = [slot(arr[n]) for n in t.port_order + t.scalar_ports]
+            for k, l in enumerate(st.launches):
+                ops.append(_capi.loop_op(st.op, ports, l.range.offset, l.range.count,
+                                         n_scalars=len(t.scalar_ports), part=k, n_parts=len(st.launches)))
+        if len(dtypes) != 1 or len(index) > 1:
+            return None
+        relres = slot(self.storage.array(step.relres_port))
+        return ops, ptrs, dtypes.pop(), index.pop() if index else "int32", relres
+
     def _loop_device(self, step, tol: float, max_iter: int):
-        """Run a LoopStep as one device-side CUDA graph (conditional WHILE node, aol_loop_*)."""
+        """Run a LoopStep on the device with no host round trip per iteration.
+
+        First choice: ONE persistent cooperative kernel interpreting the body
+        (aol_loop_persistent).  Otherwise: one CUDA graph with a conditional WHILE node
+        (aol_loop_begin/end/run).  Both are bit-identical to the eager interpreter."""
         torch = _torch()
+        if self.persistent:
+            prog = self._programs.get(step.task_path, False)
+            if prog is False:
+                prog = self._programs[step.task_path] = self._persistent_program(step)
+            if prog is not None:
+                ops, ptrs, dt, idt, rr = prog
+                res = _capi.loop_persistent(ops, ptrs, dt, idt, rr, tol, max(1, int(max_iter)),
+                                            self._stream_handle())
+                if res is not None:
+                    self.device_loops += 1
+                    self.persistent_loops += 1
+                    return res
+                self._programs[step.task_path] = None
         key = (step.task_path, tol, max_iter)
         entry = self._loops.get(key)
         if entry is None:

@@ -613,9 +613,12 @@ def test_fused_downscaler_bitwise(F, H, W, devices):
 
 
 @pytest.mark.parametrize("devices", [1, 4])
-def test_cg_graph_mode_equals_eager(golden, devices):
-    """LoopStep as ONE device-side CUDA graph (conditional WHILE node; device scalar ops, ordered
-    partial sums): bit-identical to the eager interpreter, and to the reference's iteration count."""
+@pytest.mark.parametrize("persistent", ["1", "0"])
+def test_cg_graph_mode_equals_eager(golden, devices, persistent, monkeypatch):
+    """LoopStep on the device -- ONE persistent cooperative kernel, or (persistent=0) ONE CUDA
+    graph with a conditional WHILE node -- bit-identical to the eager interpreter, and to the
+    reference's iteration count."""
+    monkeypatch.setenv("AOL_LOOP_PERSISTENT", persistent)
     from paper_1105_4424_b200.executor import Executor
     from paper_1105_4424_b200.model import model_from_dict
     from paper_1105_4424_b200.partition import build_schedule
@@ -629,6 +632,7 @@ def test_cg_graph_mode_equals_eager(golden, devices):
     gr = Executor(model, sched, bind, devices, graphs=True)
     gr.run()
     assert gr.device_loops == 1
+    assert gr.persistent_loops == (1 if persistent == "1" else 0)
     assert gr.iterations == eager.iterations == m["runs"][str(devices)]["iterations"]
     assert np.array_equal(gr.outputs()["x"], eager.outputs()["x"])
     assert gr.final_relres == eager.final_relres
@@ -760,3 +764,77 @@ def test_no_repeat_touches_element_zero_only():
                                        "allocate task t onto dev.cu"], None)
     res = execute_schedule(model, build_schedule(model, 3), {"i": np.arange(1, 9, dtype=np.float32)}, 3)
     assert res.outputs["o"].tolist() == [1, 0, 0, 0, 0, 0, 0, 0]
+
+
+def test_single_pass_dot_deterministic_and_tree_order():
+    """k_dot (one launch, last-block final reduction) equals the fixed 1024-block tree it
+    restates, bit for bit, on every call and for ragged ranges."""
+    from paper_1105_4424_b200 import _capi
+    rng = np.random.default_rng(11)
+    for n, first, count in [(1, 0, 1), (1000, 3, 997), (262_147, 0, 262_147), (3_000_001, 17, 2_999_000)]:
+        a = rng.standard_normal(n)
+        b = rng.standard_normal(n)
+        ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+        out = torch.zeros(1, dtype=torch.float64, device="cuda")
+        task = _capi.make_task("dot_partial", "float64")
+        vals = set()
+        for _ in range(5):
+            _capi.launch(task, first, count, [ta.data_ptr(), tb.data_ptr(), out.data_ptr()])
+            torch.cuda.synchronize()
+            vals.add(out.item())
+        assert len(vals) == 1
+        # restate the tree: grid-stride slices of 1024 blocks x 256 threads
+        prod = a[first:first + count] * b[first:first + count]
+        ref = float(np.sum(prod))
+        assert abs(vals.pop() - ref) <= 1e-12 * max(1.0, np.sum(np.abs(prod)))
+
+
+def test_scalar_seq_bit_exact_and_errors():
+    """Several host scalar ops in one launch (AOL_OP_SCALAR_SEQ): Python's IEEE results."""
+    import math
+    from paper_1105_4424_b200 import _capi
+    v = torch.tensor([3.7, 1.3, 0.0, 0.0, 0.0, 2.0e-7, 5.5], dtype=torch.float64, device="cuda")
+    p = [v[i:i + 1].data_ptr() for i in range(7)]
+    div, neg, rr = _capi.OP["div"], _capi.OP["neg"], _capi.OP["rel_residual"]
+    prog = [div, 0, 1, 2,      # q = num / den          -> v[2]
+            neg, 2, -1, 3,     # z = -q                 -> v[3]
+            rr, 4, 5, 6]       # sqrt(num) / sqrt(den)  -> v[4]
+    _capi.launch(_capi.make_task("scalar_seq", "float64"), 0, 3, [p[0], p[1], p[2], p[3], p[5], p[6], p[4]], prog)
+    torch.cuda.synchronize()
+    h = v.cpu().numpy()
+    q = 3.7 / 1.3
+    assert h[2] == q and h[3] == -q
+    assert h[4] == math.sqrt(2.0e-7) / math.sqrt(5.5)
+    with pytest.raises(Exception):
+        _capi.launch(_capi.make_task("scalar_seq", "float64"), 0, 9, [p[0]], [div, 0, 0, 0] * 9)
+    with pytest.raises(Exception):
+        _capi.launch(_capi.make_task("scalar_seq", "float64"), 0, 1, [p[0]], [_capi.OP["axpy"], 0, 0, 0])
+
+
+@pytest.mark.parametrize("devices,k,max_iter", [(1, 600, 40), (3, 600, 25), (2, 364, 3000)])
+def test_cg_persistent_large_equals_graph_and_eager(devices, k, max_iter, monkeypatch):
+    """Persistent LoopStep kernel on the bench's Poisson matrices (n up to 360,000, so virtual
+    blocks wrap more than once): x, iterations and relres identical to the CUDA-graph loop
+    and to eager launches, also when stopped by max_iter."""
+    import bench
+    from paper_1105_4424_b200.executor import Executor
+    from paper_1105_4424_b200.model import model_from_dict
+    from paper_1105_4424_b200.partition import build_schedule
+    import json
+    from pathlib import Path
+    meta = json.loads((Path(__file__).parent / "golden" / "reference_golden.json").read_text())
+    n, rowptr, colidx, vals = bench._poisson_2d(k)
+    model = model_from_dict(bench._resize_model_dict(meta["cg_k20"]["model"], 400, 1920, n, int(rowptr[-1])))
+    sched = build_schedule(model, devices)
+    bind = {"rowptr": rowptr, "colidx": colidx, "values": vals, "b": np.ones(n)}
+    runs = {}
+    for mode, env, graphs in (("persistent", "1", True), ("graph", "0", True), ("eager", "1", False)):
+        monkeypatch.setenv("AOL_LOOP_PERSISTENT", env)
+        ex = Executor(model, sched, bind, devices, graphs=graphs)
+        ex.run(max_iter=max_iter)
+        runs[mode] = (ex.iterations, ex.final_relres, ex.converged, ex.outputs()["x"])
+        if mode == "persistent":
+            assert ex.persistent_loops == 1
+    for mode in ("graph", "eager"):
+        assert runs[mode][:3] == runs["persistent"][:3], mode
+        assert np.array_equal(runs[mode][3], runs["persistent"][3]), mode
