@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "aol_async.cuh"
 #include "aol_common.cuh"
 
 namespace aol {
@@ -417,6 +418,231 @@ __global__ void __launch_bounds__(FZ_THREADS, 3) k_fused_line_filters(const floa
   }
 }
 
+// -----------------------------------------------------------------------------
+// Streaming form (the default when the geometry allows): a persistent CTA per SM owns a
+// contiguous run of consumer line repetitions.  One producer warp streams whole x rows
+// (W floats + a 32-byte wrap halo = x[row][0..7]) into an NST-stage shared-memory ring
+// with cp.async.bulk, completion on mbarriers.  Each consumer thread owns one producer
+// repetition lh of the row (window x[8lh .. 8lh+12]), computes its PYH intermediate values
+// for the row and folds them straight into register accumulators of the consumer filter
+// for its PYH columns -- "current" rep (tap t = s mod SXV) and "previous" rep (tap
+// t + SXV while t < PXV - SXV).  Rows arrive in tap order, so every output is the unfused
+// sum in the unfused order (bit-identical), and the intermediate never exists anywhere.
+// x is read once (+ (PXV - SXV) rows per CTA run and per frame), y written once.
+// -----------------------------------------------------------------------------
+constexpr int FS_NST = 8;
+
+// (a0, a1) += (p0, p1) with one packed add (each lane IEEE round-to-nearest, like
+// __fadd_rn).  The products stay scalar __fmul_rn: ptxas contracts a packed mul.rn.f32x2
+// feeding a packed add into FFMA2 (one rounding), which would break bit-exactness.
+__device__ __forceinline__ void add2_rn(float& a0, float& a1, float p0, float p1) {
+  asm("{\n\t.reg .b64 ra, rp;\n\tmov.b64 ra, {%0, %1};\n\tmov.b64 rp, {%2, %3};\n\t"
+      "add.rn.f32x2 ra, ra, rp;\n\tmov.b64 {%0, %1}, ra;\n\t}"
+      : "+f"(a0), "+f"(a1)
+      : "f"(p0), "f"(p1));
+}
+
+struct StreamGeom {
+  int64_t F, R, W;               // x: [F, R, W]
+  int64_t NLh, NLv, Wm, Sy;      // producer reps per row, consumer reps per frame, y row length, y rows
+  int64_t first, last;           // consumer repetition range (rho, inclusive)
+};
+
+template <int PXH, int SXH, int PYH, int PXV, int SXV, int PYV>
+__global__ void __launch_bounds__(512, 1) k_fused_stream(const float* __restrict__ x, const float* __restrict__ wh,
+                                                          const float* __restrict__ wv, float* __restrict__ y,
+                                                          StreamGeom g, int n_consumer_warps) {
+  static_assert(PXV > SXV && PXV - SXV <= SXV, "consumer windows overlap by less than one paving step");
+  extern __shared__ __align__(128) unsigned char fs_smem[];
+  const int RS = (int)g.W + 8;                                   // floats per stage (row + halo)
+  float* stages = reinterpret_cast<float*>(fs_smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(fs_smem + (size_t)FS_NST * RS * 4);
+  uint64_t* empty = full + FS_NST;
+  __shared__ float swv[PXV * PYV];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int k = threadIdx.x; k < PXV * PYV; k += blockDim.x) swv[k] = wv[k];
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < FS_NST; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, n_consumer_warps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // this CTA's consumer repetitions [v0, v1) in (frame * NLv + lv) units
+  const int64_t v_lo = g.first / g.Wm, v_hi = g.last / g.Wm + 1;
+  const int64_t nv = v_hi - v_lo;
+  const int64_t v0 = v_lo + nv * blockIdx.x / gridDim.x, v1 = v_lo + nv * (blockIdx.x + 1) / gridDim.x;
+  const uint32_t row_bytes = (uint32_t)g.W * 4;
+
+  if (warp == n_consumer_warps) {                                 // producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t v = v0; v < v1;) {
+        const int64_t f = v / g.NLv, ra = v % g.NLv;
+        const int64_t rb = (v1 - f * g.NLv < g.NLv) ? v1 - f * g.NLv : g.NLv;
+        const int64_t nrows = (rb - ra) * SXV + (PXV - SXV);
+        for (int64_t sidx = 0; sidx < nrows; ++sidx) {
+          const int64_t row = (ra * SXV + sidx) % g.R;
+          const float* src = x + (f * g.R + row) * g.W;
+          mbar_wait(empty + stage, phase ^ 1);
+          mbar_expect_tx(full + stage, row_bytes + 32);
+          float* dst = stages + (size_t)stage * RS;
+          bulk_load(dst, src, row_bytes, full + stage);
+          bulk_load(dst + g.W, src, 32, full + stage);          // wrap halo: x[row][0..7]
+          if (++stage == FS_NST) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        v = f * g.NLv + rb;
+      }
+    }
+    return;
+  }
+
+  // consumers: thread lh owns producer repetition lh (threads past NLh compute on a clamped
+  // window and never store)
+  const int lh = threadIdx.x;
+  const bool active = lh < g.NLh;
+  const uint32_t win = (uint32_t)(SXH * (active ? lh : 0)) * 4;   // window byte offset in a row
+  float whr[PYH][PXH];
+#pragma unroll
+  for (int j = 0; j < PYH; ++j)
+#pragma unroll
+    for (int t = 0; t < PXH; ++t) whr[j][t] = wh[j * PXH + t];
+  const uint32_t stage0 = smem_u32(stages);
+  const uint32_t stage_bytes = (uint32_t)RS * 4;
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int64_t v = v0; v < v1;) {
+    const int64_t f = v / g.NLv, ra = v % g.NLv;
+    const int64_t rb = (v1 - f * g.NLv < g.NLv) ? v1 - f * g.NLv : g.NLv;
+    const int nrep = (int)(rb - ra);
+    // this frame segment's outputs lie wholly inside [first, last]?
+    const bool whole = (f * g.NLv + ra) * g.Wm >= g.first && (f * g.NLv + rb) * g.Wm - 1 <= g.last;
+    float cur[PYH][PYV], prev[PYH][PYV];
+    for (int u = 0; u <= nrep; ++u) {               // u == nrep: the tail rows of rep nrep-1 only
+#pragma unroll
+      for (int t = 0; t < SXV; ++t) {
+        if (u == nrep && t >= PXV - SXV) break;
+        mbar_wait(full + stage, phase);
+        float xw[16];
+        {
+          const uint32_t a = stage0 + (uint32_t)stage * stage_bytes + win;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            float4 q;
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(q.x), "=f"(q.y), "=f"(q.z), "=f"(q.w)
+                         : "r"(a + 16 * e));
+            xw[4 * e] = q.x; xw[4 * e + 1] = q.y; xw[4 * e + 2] = q.z; xw[4 * e + 3] = q.w;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + stage);
+        if (++stage == FS_NST) {
+          stage = 0;
+          phase ^= 1;
+        }
+        if (t == 0) {                               // rep u starts, rep u-1 continues
+#pragma unroll
+          for (int c = 0; c < PYH; ++c)
+#pragma unroll
+            for (int j = 0; j < PYV; ++j) {
+              prev[c][j] = cur[c][j];
+              cur[c][j] = 0.0f;
+            }
+        }
+        float hv[PYH];                              // the producer's outputs, unfused order
+#pragma unroll
+        for (int c = 0; c < PYH; ++c) hv[c] = 0.0f;
+#pragma unroll
+        for (int k = 0; k < PXH; ++k) {
+#pragma unroll
+          for (int c = 0; c + 1 < PYH; c += 2)
+            add2_rn(hv[c], hv[c + 1], __fmul_rn(whr[c][k], xw[k]), __fmul_rn(whr[c + 1][k], xw[k]));
+          if (PYH % 2) hv[PYH - 1] = __fadd_rn(hv[PYH - 1], __fmul_rn(whr[PYH - 1][k], xw[k]));
+        }
+        static_assert(PYV % 2 == 0, "consumer outputs are accumulated in pairs");
+        if (u < nrep) {
+#pragma unroll
+          for (int j = 0; j < PYV; j += 2) {
+            const float w0 = swv[j * PXV + t], w1 = swv[(j + 1) * PXV + t];
+#pragma unroll
+            for (int c = 0; c < PYH; ++c) add2_rn(cur[c][j], cur[c][j + 1], __fmul_rn(w0, hv[c]), __fmul_rn(w1, hv[c]));
+          }
+        }
+        if (t < PXV - SXV && u >= 1) {
+#pragma unroll
+          for (int j = 0; j < PYV; j += 2) {
+            const float w0 = swv[j * PXV + t + SXV], w1 = swv[(j + 1) * PXV + t + SXV];
+#pragma unroll
+            for (int c = 0; c < PYH; ++c)
+              add2_rn(prev[c][j], prev[c][j + 1], __fmul_rn(w0, hv[c]), __fmul_rn(w1, hv[c]));
+          }
+          if (t == PXV - SXV - 1 && active) {       // rep u-1 complete: store it
+            const int64_t lv = ra + u - 1;
+            float* yp = y + (f * g.Sy + lv * PYV) * g.Wm + (int64_t)lh * PYH;
+            if (whole) {
+#pragma unroll
+              for (int j = 0; j < PYV; ++j)
+#pragma unroll
+                for (int c = 0; c < PYH; ++c) yp[(int64_t)j * g.Wm + c] = prev[c][j];
+            } else {
+              const int64_t rho0 = (f * g.NLv + lv) * g.Wm + (int64_t)lh * PYH;
+#pragma unroll
+              for (int j = 0; j < PYV; ++j)
+#pragma unroll
+                for (int c = 0; c < PYH; ++c)
+                  if (rho0 + c >= g.first && rho0 + c <= g.last) yp[(int64_t)j * g.Wm + c] = prev[c][j];
+            }
+          }
+        }
+      }
+    }
+    v = f * g.NLv + rb;
+  }
+}
+
+static int launch_fused_stream(const FusedGeom& fg, int64_t first, int64_t count, const float* x, const float* wh,
+                               const float* wv, float* y, cudaStream_t s) {
+  const LineGeom &h = fg.h, &v = fg.v;
+  StreamGeom g;
+  g.F = v.outer;
+  g.R = fg.R;
+  g.W = fg.W;
+  g.NLh = h.NL;
+  g.NLv = v.NL;
+  g.Wm = fg.Wm;
+  g.Sy = v.Sy;
+  g.first = first;
+  g.last = first + count - 1;
+  const int cw = (int)((h.NL + 31) / 32);
+  const size_t smem = (size_t)FS_NST * (g.W + 8) * 4 + 2 * FS_NST * sizeof(uint64_t);
+  auto kern = k_fused_stream<13, 8, 3, 14, 9, 4>;
+  AOL_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int dev = 0, sms = 0;
+  AOL_CUDA_CHECK(cudaGetDevice(&dev));
+  AOL_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int64_t nv = g.last / g.Wm - g.first / g.Wm + 1;
+  const int grid = (int)(nv < sms ? nv : sms);
+  kern<<<grid, (cw + 1) * 32, smem, s>>>(x, wh, wv, y, g, cw);
+  AOL_LAUNCH_CHECK("k_fused_stream");
+  return AOL_OK;
+}
+
+// streaming form applies: 13x3 paving 8 -> 14x4 paving 9, full rows, no origins, x rows
+// 16-byte aligned and a ring of FS_NST rows fitting in shared memory
+static bool fused_stream_ok(const FusedGeom& fg) {
+  const LineGeom &h = fg.h, &v = fg.v;
+  if (getenv("AOL_FUSED_TILE")) return false;
+  return h.px == 13 && h.sx == 8 && h.py == 3 && h.sy == 3 && h.ox == 0 && h.NL * h.sx == fg.W &&
+         v.px == 14 && v.sx == 9 && v.py == 4 && v.sy == 4 && v.ox == 0 && v.oy == 0 && fg.W % 4 == 0 &&
+         h.NL <= 15 * 32 && (size_t)FS_NST * (fg.W + 8) * 4 + 256 <= 200 * 1024;
+}
+
 int launch_fused_line_filters(const aol_task& th, const aol_task& tv, int64_t first, int64_t count,
                               void* const* ph, void* const* pv, cudaStream_t s) {
   FusedGeom g;
@@ -424,6 +650,9 @@ int launch_fused_line_filters(const aol_task& th, const aol_task& tv, int64_t fi
   if (!(g.h.px == 13 && g.h.py == 3 && g.v.px == 14 && g.v.py == 4))
     return fail(AOL_EUNSUPPORTED, "fused line filters are instantiated for 13x3 -> 14x4");
   if (count <= 0) return AOL_OK;
+  if (fused_stream_ok(g))
+    return launch_fused_stream(g, first, count, static_cast<const float*>(ph[0]), static_cast<const float*>(ph[1]),
+                               static_cast<const float*>(pv[1]), static_cast<float*>(pv[2]), s);
   const int64_t last = first + count - 1;
   const int64_t per_frame = g.v.NL * g.Wm;
   const int64_t f_lo = first / per_frame, f_hi = last / per_frame;

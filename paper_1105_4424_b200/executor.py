@@ -182,7 +182,7 @@ class Executor:
     """Prepared schedule: storage resident in HBM, tasks validated, ready to run repeatedly."""
 
     def __init__(self, model, schedule, bindings: dict, device_count: int, *, tilers: dict | None = None,
-                 precision: str = "default", device=None, stream=None, pipeline: int = 0, fuse: bool = False,
+                 precision: str = "default", device=None, stream=None, pipeline: int = 0, fuse: bool = True,
                  graphs: bool = False):
         torch = _torch()
         _capi.load()
@@ -685,7 +685,7 @@ class Executor:
 def execute_schedule(model, schedule, bindings: dict, device_count: int, tol: float | None = None,
                      max_iter: int | None = None, *, tilers: dict | None = None, precision: str = "default",
                      device_outputs: bool = False, out: dict | None = None, device=None,
-                     stream=None, pipeline: int = 0, fuse: bool = False, graphs: bool = False) -> ExecutionResult:
+                     stream=None, pipeline: int = 0, fuse: bool = True, graphs: bool = False) -> ExecutionResult:
     """Interpret ``schedule`` on the B200 with ``device_count`` launch shards per device step."""
     ex = Executor(model, schedule, bindings, device_count, tilers=tilers, precision=precision,
                   device=device, stream=stream, pipeline=0 if device_outputs else pipeline, fuse=fuse,

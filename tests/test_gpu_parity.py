@@ -585,9 +585,14 @@ def _downscaler_model(F, H, W):
     return model, th, tv, wh, wv
 
 
-@pytest.mark.parametrize("F,H,W,devices", [(2, 18, 64, 1), (3, 45, 256, 3), (1, 27, 776, 2), (2, 99, 384, 5)])
-def test_fused_downscaler_bitwise(F, H, W, devices):
-    """H->V task fusion (intermediate kept in shared memory) equals the unfused chain and the oracle bit for bit."""
+@pytest.mark.parametrize("form", ["stream", "tile"])
+@pytest.mark.parametrize("F,H,W,devices", [(2, 18, 64, 1), (3, 45, 256, 3), (1, 27, 776, 2), (2, 99, 384, 5),
+                                           (3, 2160 // 40, 3840, 7)])
+def test_fused_downscaler_bitwise(F, H, W, devices, form, monkeypatch):
+    """H->V task fusion (the intermediate never reaches HBM; streaming and tile kernels) equals the
+    unfused chain and the oracle bit for bit, also for launch ranges that split rows."""
+    if form == "tile":
+        monkeypatch.setenv("AOL_FUSED_TILE", "1")
     from paper_1105_4424_b200.executor import Executor
     from paper_1105_4424_b200.partition import build_schedule
     model, th, tv, wh, wv = _downscaler_model(F, H, W)
