@@ -11,6 +11,8 @@
 // (4+KH-1) input rows once as float4 (+ KW-1 neighbour columns), so each input
 // element is fetched ~1.1 times from L1 instead of KH*KW times.  Rows wrap by a
 // per-row modulo computed once; columns wrap only in the two neighbour loads.
+#include <cstdlib>
+
 #include "aol_common.cuh"
 
 namespace aol {
@@ -86,6 +88,78 @@ __global__ void __launch_bounds__(ST_TX* ST_TY) k_stencil_box(const float* __res
   }
 }
 
+// (a0, a1) += (p0, p1), one packed IEEE round-to-nearest add per lane (products stay
+// scalar __fmul_rn: ptxas would contract a packed mul into the packed add).
+__device__ __forceinline__ void st_add2(float& a0, float& a1, float p0, float p1) {
+  asm("{\n\t.reg .b64 ra, rp;\n\tmov.b64 ra, {%0, %1};\n\tmov.b64 rp, {%2, %3};\n\t"
+      "add.rn.f32x2 ra, ra, rp;\n\tmov.b64 {%0, %1}, ra;\n\t}"
+      : "+f"(a0), "+f"(a1)
+      : "f"(p0), "f"(p1));
+}
+
+// Fast form (the common case: W % 4 == 0 and the window centre column of every float4 is
+// 16-byte aligned): a thread owns 4 columns and slides a KH-row register window down
+// SV_RPT output rows -- each input row is loaded once per strip (float4 + two neighbour
+// scalars), the KH-1 halo rows once per SV_RPT rows.  Same tap order as k_stencil_box.
+constexpr int SV_TX = 128, SV_RPT = 16;
+
+template <int KH>
+__global__ void __launch_bounds__(SV_TX) k_stencil_slide(const float* __restrict__ x, const float* __restrict__ w,
+                                                         float* __restrict__ y, int H, int W, int orow, int ocol,
+                                                         int rows, int64_t first, int64_t last) {
+  float wr[KH * 3];
+#pragma unroll
+  for (int k = 0; k < KH * 3; ++k) wr[k] = __ldg(w + k);
+  const int c0 = (blockIdx.x * SV_TX + threadIdx.x) * 4;
+  const int r0 = blockIdx.y * SV_RPT;
+  if (c0 >= W || r0 >= rows) return;
+  int cin = c0 + ocol + 1;                              // window centre of column c0 (dj = 1)
+  if (cin >= W) cin -= W;
+  const int cl = cin == 0 ? W - 1 : cin - 1;
+  const int cr = cin + 4 == W ? 0 : cin + 4;
+  int row = r0 + orow;                                  // input row of tap di = 0
+  if (row >= H) row -= H;
+  // every window load is issued before any arithmetic: (SV_RPT + KH - 1) rows x 3 requests
+  // in flight per thread
+  float v[SV_RPT + KH - 1][6];
+#pragma unroll
+  for (int rr = 0; rr < SV_RPT + KH - 1; ++rr) {
+    const float* xr = x + (size_t)row * (size_t)W;
+    const float4 q = __ldg(reinterpret_cast<const float4*>(xr + cin));
+    v[rr][0] = __ldg(xr + cl);
+    v[rr][1] = q.x; v[rr][2] = q.y; v[rr][3] = q.z; v[rr][4] = q.w;
+    v[rr][5] = __ldg(xr + cr);
+    if (++row == H) row = 0;
+  }
+  const bool whole = (int64_t)r0 * W + c0 >= first && (int64_t)(r0 + SV_RPT - 1) * W + c0 + 3 <= last &&
+                     r0 + SV_RPT <= rows;
+#pragma unroll
+  for (int i = 0; i < SV_RPT; ++i) {
+    float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
+#pragma unroll
+    for (int di = 0; di < KH; ++di) {
+      const float* vr = v[i + di];
+#pragma unroll
+      for (int dj = 0; dj < 3; ++dj) {
+        const float wt = wr[di * 3 + dj];
+        st_add2(a0, a1, __fmul_rn(wt, vr[dj]), __fmul_rn(wt, vr[dj + 1]));
+        st_add2(a2, a3, __fmul_rn(wt, vr[dj + 2]), __fmul_rn(wt, vr[dj + 3]));
+      }
+    }
+    const int r = r0 + i;
+    float* yr = y + (size_t)r * (size_t)W + c0;
+    if (whole) {
+      *reinterpret_cast<float4*>(yr) = make_float4(a0, a1, a2, a3);
+    } else if (r < rows) {
+      const int64_t lin = (int64_t)r * W + c0;
+      const float a[4] = {a0, a1, a2, a3};
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (lin + j >= first && lin + j <= last) yr[j] = a[j];
+    }
+  }
+}
+
 // Recognise the box-stencil tiler pair; returns false when the generic kernel must run.
 bool stencil_box_applicable(const aol_task& t, int& KH, int& KW) {
   const aol_tiler &tx = t.tilers[0], &ty = t.tilers[1];
@@ -126,6 +200,16 @@ int launch_stencil_box(const aol_task& t, int64_t first, int64_t count, void* co
   const int64_t f2 = first - (int64_t)rlo * W, l2 = last - (int64_t)rlo * W;
   const int Hrows = rhi - rlo + 1;
   // rows are addressed relative to rlo for the output; the input row is (r + rlo + orow) mod H
+  const int cshift = (int)emod((int64_t)ocol + 1, W);
+  if (W % 4 == 0 && cshift % 4 == 0 && !getenv("AOL_STENCIL_BOX")) {
+    dim3 g2((W / 4 + SV_TX - 1) / SV_TX, (Hrows + SV_RPT - 1) / SV_RPT);
+    if (KH == 3)
+      k_stencil_slide<3><<<g2, SV_TX, 0, s>>>(x, w, y, H, W, orow_shift, ocol, Hrows, f2, l2);
+    else
+      k_stencil_slide<5><<<g2, SV_TX, 0, s>>>(x, w, y, H, W, orow_shift, ocol, Hrows, f2, l2);
+    AOL_LAUNCH_CHECK("k_stencil_slide");
+    return AOL_OK;
+  }
   if (KH == 3)
     k_stencil_box<3, 3><<<grid, block, 0, s>>>(x, w, y, H, W, orow_shift, ocol, f2, l2);
   else

@@ -354,8 +354,13 @@ def _plan(op_tilers, dtype="float32"):
 
 @pytest.mark.parametrize("H,W,origin,kh,devices", [
     (256, 512, None, 3, 1), (256, 512, None, 3, 3), (130, 260, (0, 0), 3, 2), (64, 128, (5, 7), 3, 5),
-    (96, 64, None, 5, 4), (33, 44, (32, 43), 3, 1)])
-def test_stencil_box_kernel_vs_oracle(H, W, origin, kh, devices):
+    (96, 64, None, 5, 4), (33, 44, (32, 43), 3, 1), (100, 1024, (99, 3), 3, 7), (17, 4096, None, 5, 2)])
+@pytest.mark.parametrize("form", ["slide", "box"])
+def test_stencil_box_kernel_vs_oracle(H, W, origin, kh, devices, form, monkeypatch):
+    """Sliding-window (default when columns are float4-aligned) and register-box stencil kernels,
+    bit-exact vs the oracle for toroidal origins, 5-row boxes and launch ranges that split rows."""
+    if form == "box":
+        monkeypatch.setenv("AOL_STENCIL_BOX", "1")
     t = orc.stencil_tilers(H, W)
     if origin is not None:
         t["x"] = dict(t["x"], origin=origin)
