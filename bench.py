@@ -565,10 +565,11 @@ class CGWorkload(Workload):
                             "per_unit": "per iteration 2*nnz (spmv) + 3 dots + 3 vector updates (12n)"}
         self.workload = (f"CG (bundled cg.gmodel resized) poisson_2d({k}): n={n}, nnz={self.nnz}, {self.iters} "
                          f"iterations; the whole LoopStep as ONE persistent cooperative kernel interpreting the loop body (Executor setup timed)")
-        self.l2 = "vectors (1 MB) fit in L2: the solve is launch- and host-sync-bound"
+        self.l2 = "working set (~12 MB) fits in L2: L2 flushed (256 MiB write) before every timed step"
         self.ex = None
 
     graphs = True
+    l2_flush = True
 
     def step(self):
         from paper_1105_4424_b200.executor import Executor
@@ -636,7 +637,9 @@ class C1Workload(Workload):
         self.units_per_step = 2.0 * n ** 3 / 1e12
         self.algorithmic = {"flop_per_launch": 2 * n ** 3, "per_unit": "2 FLOP per (m, n, k)"}
         self.workload = f"C1 matmul {n}x{n}x{n} fp32 via execute_schedule (host numpy in/out, TF32 tcgen05)"
-        self.l2 = "small: L2-resident, launch- and API-overhead-bound"
+        self.l2 = "small (768 KB): L2 flushed (256 MiB write) before every timed step; launch- and API-overhead-bound"
+
+    l2_flush = True
 
     def step(self):
         from paper_1105_4424_b200.executor import execute_schedule
@@ -671,7 +674,10 @@ WORKLOADS = {"matmul": MatmulWorkload, "stencil": StencilWorkload, "downscaler":
 
 # ---------------------------------------------------------------- the arms --
 
-def time_steps(torch, fn, steps, warmup, stream, barrier):
+def time_steps(torch, fn, steps, warmup, stream, barrier, flush=None):
+    """K steps bracketed by barrier + synchronize.  With `flush` (workloads whose working set
+    fits in the 126 MB L2) a 256 MiB buffer is written between steps, outside each step's
+    event pair; the step time is then the sum of the per-step event times."""
     for _ in range(warmup):
         fn()
     torch.cuda.synchronize()
@@ -682,14 +688,16 @@ def time_steps(torch, fn, steps, warmup, stream, barrier):
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
     for s, e in ev:
+        if flush is not None:
+            flush()
         s.record(stream)
         fn()
         e.record(stream)
     t1.record(stream)
     torch.cuda.synchronize()
     barrier()
-    total_ms = t0.elapsed_time(t1)
     per = [s.elapsed_time(e) for s, e in ev]
+    total_ms = sum(per) if flush is not None else t0.elapsed_time(t1)
     return total_ms, per
 
 
@@ -725,8 +733,14 @@ def run_gpu(args):
         wl.step()
     torch.cuda.synchronize()
     warm_launches = _capi.launch_counter() - launches0
+    flush = None
+    if getattr(wl, "l2_flush", False):
+        scrub = torch.empty(64 << 20, dtype=torch.float32, device=device)      # 256 MiB > 126 MB L2
+
+        def flush():
+            scrub.fill_(1.0)
     clocks.start()
-    total_ms, per = time_steps(torch, wl.step, args.steps, 0, stream, barrier)
+    total_ms, per = time_steps(torch, wl.step, args.steps, 0, stream, barrier, flush)
     clk = clocks.stop()
     launches = (_capi.launch_counter() - launches0 - warm_launches)
     total_ms = allmax(total_ms)

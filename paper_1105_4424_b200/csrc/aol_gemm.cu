@@ -605,6 +605,22 @@ int launch_gemm_tf32(const aol_task& t, int64_t first, int64_t count, void* cons
   const int64_t m_lo = first / g.N, m_hi = (first + count - 1) / g.N, rows = m_hi - m_lo + 1;
   const int64_t lda3 = (3 * g.K + 3) / 4 * 4, ldb3 = (g.N + 3) / 4 * 4;   // 16-byte TMA pitches
   float *Ap = nullptr, *Bp = nullptr;
+  {
+    // keep freed split buffers in the stream-ordered pool: with the default release
+    // threshold (0) every synchronize returns them to the driver and the next launch pays
+    // to map them again (measured: tens of ms of jitter per call)
+    static std::once_flag once[64];
+    int dev = 0;
+    AOL_CUDA_CHECK(cudaGetDevice(&dev));
+    if (dev >= 0 && dev < 64)
+      std::call_once(once[dev], [dev] {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+          uint64_t keep = UINT64_MAX;
+          cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+      });
+  }
   AOL_CUDA_CHECK(cudaMallocAsync((void**)&Ap, (size_t)rows * lda3 * sizeof(float), stream));
   AOL_CUDA_CHECK(cudaMallocAsync((void**)&Bp, (size_t)3 * g.K * ldb3 * sizeof(float), stream));
   const int64_t sa_m = g.a_kmajor ? g.lda : 1, sa_k = g.a_kmajor ? 1 : g.lda;

@@ -20,9 +20,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "aol_common.cuh"
@@ -63,6 +65,7 @@ struct LProg {
   unsigned* flag;                             // [2][64] last published dot sequence number
   double* result;                             // [2][64] published dot values
   unsigned long long* prof;                   // AOL_LOOP_PROFILE: ns per group, CTA 0's view
+  unsigned backoff_ns;                        // sleep between polls of a dot's flag
   LGroup groups[kLoopMaxGroups];
   LOp ops[kLoopMaxOps];
   void* ports[kLoopMaxPorts];
@@ -265,7 +268,7 @@ __global__ void __launch_bounds__(kLoopThreads, 1) k_loop_persistent(const __gri
           }
         }
       } else if (threadIdx.x == 0) {
-        while (ld_relaxed(P.flag + cell) != seq) __nanosleep(64);
+        while (ld_relaxed(P.flag + cell) != seq) __nanosleep(P.backoff_ns);
         __threadfence();
       }
       __syncthreads();
@@ -473,6 +476,7 @@ using namespace aol;
 extern "C" int aol_loop_persistent(const aol_loop_op* ops, int n_ops, void* const* ports, int n_ports, int dtype,
                                    int index_dtype, int relres_port, double tol, int64_t max_iter, void* stream,
                                    int64_t* iterations, double* final_relres, int* converged) {
+  const auto host_t0 = std::chrono::steady_clock::now();
   if (!ops || !ports || n_ops < 1 || max_iter < 1) return fail(AOL_EINVAL, "aol_loop_persistent: bad arguments");
   if (n_ops > kLoopMaxOps || n_ports > kLoopMaxPorts)
     return fail(AOL_EUNSUPPORTED, "loop body too large for the persistent interpreter");
@@ -529,6 +533,10 @@ extern "C" int aol_loop_persistent(const aol_loop_op* ops, int n_ops, void* cons
   P.n_groups = (int)pl.groups.size();
   for (int p = 0; p < n_ports; ++p) P.ports[p] = ports[p];
   P.scalar_mask = scalar;
+  {
+    const char* b = getenv("AOL_LOOP_BACKOFF_NS");
+    P.backoff_ns = b ? (unsigned)atoi(b) : 64u;
+  }
 
   int dev = 0, coop = 0, per_sm = 0, sms = 0;
   AOL_CUDA_CHECK(cudaGetDevice(&dev));
@@ -538,16 +546,27 @@ extern "C" int aol_loop_persistent(const aol_loop_op* ops, int n_ops, void* cons
   void (*kern)(LProg);
   if (dtype == AOL_F64) kern = index_dtype == AOL_I64 ? k_loop_persistent<double, int64_t> : k_loop_persistent<double, int32_t>;
   else kern = index_dtype == AOL_I64 ? k_loop_persistent<float, int64_t> : k_loop_persistent<float, int32_t>;
-  AOL_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kLoopThreads, 0));
-  if (per_sm < 1) return fail(AOL_EUNSUPPORTED, "persistent loop kernel does not fit on an SM");
+  if (dev < 0 || dev >= 64) return fail(AOL_EUNSUPPORTED, "device index out of range");
+  // per device: occupancy checked once, scratch allocated once (the call is synchronous and
+  // holds the device's lock, so loops on one device never share scratch concurrently)
+  static std::mutex locks[64];
+  static char* scratch_of[64] = {nullptr};
+  static int fits_of[64] = {0};
+  std::lock_guard<std::mutex> lock(locks[dev]);
+  const int kid = (dtype == AOL_F64 ? 2 : 0) + (index_dtype == AOL_I64 ? 1 : 0);
+  if (!((fits_of[dev] >> kid) & 1)) {
+    AOL_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kLoopThreads, 0));
+    if (per_sm < 1) return fail(AOL_EUNSUPPORTED, "persistent loop kernel does not fit on an SM");
+    fits_of[dev] |= 1 << kid;
+  }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const size_t part_bytes = (size_t)2 * 64 * kDotBlocks * sizeof(double);
   const size_t prof_bytes = (kLoopMaxGroups + 2 * 1024) * sizeof(unsigned long long);
   const char* prof_env = getenv("AOL_LOOP_PROFILE");
   const bool profile = prof_env && prof_env[0] == '1';
-  char* scratch = nullptr;
   const size_t sync_bytes = 128 * (4 + 4 + 8);
-  AOL_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&scratch), part_bytes + 64 + sync_bytes + prof_bytes, s));
+  if (!scratch_of[dev]) AOL_CUDA_CHECK(cudaMalloc(&scratch_of[dev], part_bytes + 64 + sync_bytes + prof_bytes));
+  char* scratch = scratch_of[dev];
   P.part = reinterpret_cast<double*>(scratch);
   P.state = reinterpret_cast<int64_t*>(scratch + part_bytes);
   P.ticket = reinterpret_cast<unsigned*>(scratch + part_bytes + 64);
@@ -559,28 +578,33 @@ extern "C" int aol_loop_persistent(const aol_loop_op* ops, int n_ops, void* cons
   if (profile) AOL_CUDA_CHECK(cudaMemsetAsync(P.prof, 0, prof_bytes, s));
   void* args[] = {&P};
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  if (profile) {
+  const char* time_env = getenv("AOL_LOOP_TIME");
+  const bool timed = profile || (time_env && time_env[0] == '1');
+  if (timed) {
     cudaEventCreate(&ev0);
     cudaEventCreate(&ev1);
     cudaEventRecord(ev0, s);
   }
   cudaError_t e = cudaLaunchCooperativeKernel((const void*)kern, dim3(sms), dim3(kLoopThreads), args, 0, s);
-  if (profile) cudaEventRecord(ev1, s);
+  if (timed) cudaEventRecord(ev1, s);
   int64_t h[3] = {0, 0, 0};
   static unsigned long long prof[kLoopMaxGroups + 2 * 1024];
   if (e == cudaSuccess) e = cudaMemcpyAsync(h, P.state, sizeof(h), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess && profile) e = cudaMemcpyAsync(prof, P.prof, prof_bytes, cudaMemcpyDeviceToHost, s);
-  cudaFreeAsync(scratch, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return cuda_fail(e, "aol_loop_persistent");
   count_launch();
-  if (profile) {
+  if (timed) {
     float ms = 0;
     cudaEventElapsedTime(&ms, ev0, ev1);
     cudaEventDestroy(ev0);
     cudaEventDestroy(ev1);
-    fprintf(stderr, "aol_loop_persistent kernel %.3f ms, %lld iterations, %.2f us/iter\n", ms, (long long)h[0],
-            1e3 * ms / (h[0] ? h[0] : 1));
+    const double host_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host_t0).count();
+    fprintf(stderr, "aol_loop_persistent kernel %.3f ms, %lld iterations, %.2f us/iter; whole call %.3f ms\n", ms,
+            (long long)h[0], 1e3 * ms / (h[0] ? h[0] : 1), host_ms);
+  }
+  if (profile) {
     for (int g = 0; g < P.n_groups; ++g) {
       const LGroup& G = P.groups[g];
       if (g == 0) {
