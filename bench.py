@@ -516,6 +516,31 @@ def _poisson_2d(k: int):
     return n, rowptr, c.astype(np.int32), v
 
 
+def _poisson_3d27(k: int = 51, diag: float = 26.0):
+    """27-point 3-D operator on a k^3 grid (diag 26, off-diagonals -1), CSR with sorted rows.
+    k = 51 gives exactly the paper's matrix shape: N = 132,651, NNZ = (3k-2)^3 = 3,442,951
+    (PAPER.md:289).  The paper does not give its values; this one is the standard SPD
+    27-point operator (85 CG iterations to 1e-10 from b = 1, the paper reports 116)."""
+    n = k ** 3
+    idx = np.arange(n, dtype=np.int64).reshape(k, k, k)
+    rows, cols = [], []
+    for dz in (-1, 0, 1):
+        for dy in (-1, 0, 1):
+            for dx in (-1, 0, 1):
+                z0, z1 = max(0, -dz), k - max(0, dz)
+                y0, y1 = max(0, -dy), k - max(0, dy)
+                x0, x1 = max(0, -dx), k - max(0, dx)
+                rows.append(idx[z0:z1, y0:y1, x0:x1].ravel())
+                cols.append(idx[z0 + dz:z1 + dz, y0 + dy:y1 + dy, x0 + dx:x1 + dx].ravel())
+    r, c = np.concatenate(rows), np.concatenate(cols)
+    order = np.lexsort((c, r))
+    r, c = r[order], c[order]
+    v = np.where(r == c, diag, -1.0)
+    rowptr = np.zeros(n + 1, np.int32)
+    np.cumsum(np.bincount(r, minlength=n), out=rowptr[1:])
+    return n, rowptr, c.astype(np.int32), v
+
+
 def _resize_model_dict(d: dict, n_old: int, nnz_old: int, n: int, nnz: int) -> dict:
     """instantiate_for_matrix (refexec.py:552-596) restated on the plain-data model."""
     import copy
@@ -543,13 +568,18 @@ class CGWorkload(Workload):
     unit = "GFLOP/s"
     dtype = "f64"
 
-    def __init__(self, torch, device, rank, world, k=364):
+    matrix = "poisson_2d(364)"
+
+    def _matrix(self):
+        return _poisson_2d(364)
+
+    def __init__(self, torch, device, rank, world):
         from paper_1105_4424_b200.executor import Executor
         from paper_1105_4424_b200.model import model_from_dict
         from paper_1105_4424_b200.partition import build_schedule
         meta = json.loads((ROOT / "tests" / "golden" / "reference_golden.json").read_text())
         base = meta["cg_k20"]["model"]
-        n, rowptr, colidx, vals = _poisson_2d(k)
+        n, rowptr, colidx, vals = self._matrix()
         self.n, self.nnz = n, int(rowptr[-1])
         self.model = model_from_dict(_resize_model_dict(base, 400, 1920, n, self.nnz))
         self.schedule = build_schedule(self.model, 1)
@@ -563,7 +593,7 @@ class CGWorkload(Workload):
         self.units_per_step = self.flop / 1e9
         self.algorithmic = {"flop_per_solve": self.flop, "iterations": self.iters,
                             "per_unit": "per iteration 2*nnz (spmv) + 3 dots + 3 vector updates (12n)"}
-        self.workload = (f"CG (bundled cg.gmodel resized) poisson_2d({k}): n={n}, nnz={self.nnz}, {self.iters} "
+        self.workload = (f"CG (bundled cg.gmodel resized) {self.matrix}: n={n}, nnz={self.nnz}, {self.iters} "
                          f"iterations; the whole LoopStep as ONE persistent cooperative kernel interpreting the loop body (Executor setup timed)")
         self.l2 = "working set (~12 MB) fits in L2: L2 flushed (256 MiB write) before every timed step"
         self.ex = None
@@ -610,6 +640,17 @@ class CGWorkload(Workload):
         dt = (time.perf_counter() - t0) / it
         return {"value": (2 * self.nnz + 12 * n) / dt / 1e9, "unit": "GFLOP/s", "cores": 1, "kind": "port",
                 "sample": f"10 CG iterations with the oracle's level-synchronous spmv (numpy), {dt * 1e3:.1f} ms/iter"}
+
+
+class CG27Workload(CGWorkload):
+    """The paper's CG matrix shape (N = 132,651, NNZ = 3,442,951): a 27-point
+    operator on a 51^3 grid.  Paper, Tesla T10: 116 iterations in 0.659 s, 1.45 GFLOP/s."""
+
+    name = "cg27"
+    matrix = "27-point 3-D operator on 51^3 (the paper's N and NNZ)"
+
+    def _matrix(self):
+        return _poisson_3d27(51)
 
 
 class C1Workload(Workload):
@@ -669,7 +710,7 @@ class C1Workload(Workload):
 
 
 WORKLOADS = {"matmul": MatmulWorkload, "stencil": StencilWorkload, "downscaler": DownscalerWorkload,
-             "sweep": SweepWorkload, "cg": CGWorkload, "c1": C1Workload}
+             "sweep": SweepWorkload, "cg": CGWorkload, "cg27": CG27Workload, "c1": C1Workload}
 
 
 # ---------------------------------------------------------------- the arms --

@@ -821,7 +821,8 @@ def test_scalar_seq_bit_exact_and_errors():
         _capi.launch(_capi.make_task("scalar_seq", "float64"), 0, 1, [p[0]], [_capi.OP["axpy"], 0, 0, 0])
 
 
-@pytest.mark.parametrize("devices,k,max_iter", [(1, 600, 40), (3, 600, 25), (2, 364, 3000)])
+@pytest.mark.parametrize("devices,k,max_iter", [(1, 600, 40), (3, 600, 25), (2, 364, 3000), (1, "p27", 3000),
+                                                (4, "p27", 30)])
 def test_cg_persistent_large_equals_graph_and_eager(devices, k, max_iter, monkeypatch):
     """Persistent LoopStep kernel on the bench's Poisson matrices (n up to 360,000, so virtual
     blocks wrap more than once): x, iterations and relres identical to the CUDA-graph loop
@@ -833,7 +834,7 @@ def test_cg_persistent_large_equals_graph_and_eager(devices, k, max_iter, monkey
     import json
     from pathlib import Path
     meta = json.loads((Path(__file__).parent / "golden" / "reference_golden.json").read_text())
-    n, rowptr, colidx, vals = bench._poisson_2d(k)
+    n, rowptr, colidx, vals = bench._poisson_3d27(51) if k == "p27" else bench._poisson_2d(k)
     model = model_from_dict(bench._resize_model_dict(meta["cg_k20"]["model"], 400, 1920, n, int(rowptr[-1])))
     sched = build_schedule(model, devices)
     bind = {"rowptr": rowptr, "colidx": colidx, "values": vals, "b": np.ones(n)}
