@@ -849,3 +849,26 @@ def test_cg_persistent_large_equals_graph_and_eager(devices, k, max_iter, monkey
     for mode in ("graph", "eager"):
         assert runs[mode][:3] == runs["persistent"][:3], mode
         assert np.array_equal(runs[mode][3], runs["persistent"][3]), mode
+
+
+def test_loop_persistent_abi_errors():
+    """aol_loop_persistent: bodies outside its op set are refused with nothing launched (the
+    executor then falls back to the CUDA-graph loop); malformed programs raise."""
+    from paper_1105_4424_b200 import _capi
+    v = torch.zeros(16, dtype=torch.float64, device="cuda")
+    p = [v[i:i + 1].data_ptr() for i in range(4)]
+    ops = [_capi.loop_op("div", [0, 1, 2])]
+    assert _capi.loop_persistent([_capi.loop_op("tile_copy", [0, 1], 0, 1)] + ops, p, "float64", "int32", 2,
+                                 1e-10, 5) is None
+    assert _capi.loop_persistent(ops, p, "int32", "int32", 2, 1e-10, 5) is None
+    with pytest.raises(_capi.AolError):
+        _capi.loop_persistent([_capi.loop_op("div", [0, 1, 9])], p, "float64", "int32", 2, 1e-10, 5)
+    with pytest.raises(_capi.AolError):
+        _capi.loop_persistent(ops, p, "float64", "int32", 2, 1e-10, 0)
+    # relres must be a scalar written by the body
+    assert _capi.loop_persistent([_capi.loop_op("copy", [0, 1], 0, 1)], p, "float64", "int32", 1, 1e-10, 5) is None
+    # a pure scalar body runs: q = 1 / 1 = 1 > tol every iteration -> stops at max_iter
+    v[0] = 1.0
+    v[1] = 1.0
+    it, rr, conv = _capi.loop_persistent(ops, p, "float64", "int32", 2, 1e-10, 7)
+    assert (it, rr, conv) == (7, 1.0, False)

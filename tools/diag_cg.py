@@ -9,7 +9,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import bench  # noqa: E402
 from paper_1105_4424_b200.executor import Executor  # noqa: E402
 
-w = [c for c in vars(bench).values() if getattr(c, "name", None) == "cg"][0](torch, torch.device("cuda:0"), 0, 1)
+w = bench.WORKLOADS[__import__("os").environ.get("DIAG_WL", "cg")](torch, torch.device("cuda:0"), 0, 1)
 modes = sys.argv[1:] or ["graphs"]
 for mode in modes:
     graphs = mode != "eager"
