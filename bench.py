@@ -192,6 +192,13 @@ class Workload:
     def step(self):
         self.ex.run()
 
+    def output_shard(self):
+        """This rank's output array in HBM (for the N>1 gather measurement), or None."""
+        ex = getattr(self, "ex", None)
+        if ex is None or not self.out_sizes:
+            return None
+        return ex.outputs(on_device=True)[next(iter(self.out_sizes))]
+
     def e2e_setup(self):
         torch = self.torch
         gen = torch.Generator().manual_seed(7)
@@ -748,10 +755,19 @@ def run_gpu(args):
     from paper_1105_4424_b200 import _capi
 
     rank, world, local = dist_env()
+    # AOL_BENCH_BACKEND=gloo: test mode for the multi-rank logic on a 1-GPU box (ranks share
+    # cuda:0; their kernels never wait on each other, only the host barriers do).  Numbers
+    # from this mode are not scaling results.
+    backend = os.environ.get("AOL_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend == "gloo" else local
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:
+            dist.init_process_group(backend)
+    red_dev = device if backend == "nccl" else torch.device("cpu")
 
     def barrier():
         if world > 1:
@@ -760,7 +776,7 @@ def run_gpu(args):
     def allmax(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], device=device, dtype=torch.float64)
+        t = torch.tensor([x], device=red_dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -809,6 +825,31 @@ def run_gpu(args):
                "path": "paper_1105_4424_b200.executor.execute_schedule(pipeline=%d): pinned host bindings and "
                        "out= buffers; chunked H2D / launch / D2H overlap" % getattr(wl, "pipeline", 0)}
 
+    # N > 1: the output shards gathered to rank 0 over NCCL, timed separately from the
+    # concurrent per-rank phase (north_star: "NCCL output gather reported separately")
+    gather = None
+    if world > 1 and not args.no_gather:
+        shard = wl.output_shard()
+        if shard is not None:
+            shard = shard.contiguous()
+            dst = [torch.empty_like(shard) for _ in range(world)] if rank == 0 else None
+            if backend != "nccl":
+                shard_h = shard.cpu()
+                dst = [torch.empty_like(shard_h) for _ in range(world)] if rank == 0 else None
+            reps, times = 3, []
+            for _ in range(reps + 1):
+                barrier()
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                dist.gather(shard if backend == "nccl" else shard_h, dst, dst=0)
+                torch.cuda.synchronize()
+                times.append(time.perf_counter() - t0)
+            g = allmax(min(times[1:]))
+            nbytes = shard.numel() * shard.element_size() * (world - 1)
+            gather = {"ms": g * 1e3, "bytes_to_root": nbytes, "GBps": nbytes / g / 1e9,
+                      "backend": backend, "op": "torch.distributed.gather of each rank's output shard to rank 0"}
+            del dst
+
     peaks = measured_peaks()
     out = None
     if rank == 0:
@@ -848,6 +889,9 @@ def run_gpu(args):
             "config": {"workload": wl.workload, "l2": wl.l2,
                        "parallelism": f"repetition space sharded by contiguous blocks over {world} rank(s)"},
             "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "clocks": clk,
+            **({"gather": gather} if gather else {}),
+            **({"test_mode": "AOL_BENCH_BACKEND=gloo: ranks share one GPU; not a scaling result"}
+               if backend != "nccl" and world > 1 else {}),
             **extra,
         }
         print(json.dumps(out), flush=True)
@@ -907,6 +951,7 @@ def main():
     ap.add_argument("--no-peak", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-points", action="store_true")
+    ap.add_argument("--no-gather", action="store_true", help="N>1: skip the output-gather measurement")
     ap.add_argument("--no-fuse", action="store_true", help="disable task fusion (downscaler H->V as two kernels)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
