@@ -87,6 +87,78 @@ def input_hull(bt: BoundTiler, first: int, count: int) -> tuple[int, int]:
     return (int(lo), int(hi) + 1)
 
 
+def input_ranges(bt: BoundTiler, first: int, count: int) -> list[tuple[int, int]]:
+    """Disjoint [lo, hi) flat-offset ranges covering what repetitions [first, first+count) read.
+
+    Affine (non-wrapping) tilers: the exact bounding range of :func:`input_hull`.
+    Toroidal tilers: the unwrapped coordinate range of the outermost array axis over the
+    repetition box and the full pattern, taken modulo its extent -- one range, or two when
+    it crosses the wrap seam (e.g. a stencil chunk needs its rows plus the last row), with
+    the inner axes whole.  Covers every offset the index function produces (tested).
+    """
+    if count <= 0:
+        return []
+    if bt.affine is not None:
+        return [input_hull(bt, first, count)]
+    import numpy as np
+    r_lo = np.unravel_index(first, bt.rep)
+    r_hi = np.unravel_index(first + count - 1, bt.rep)
+    lo_box, hi_box, differ = [], [], False
+    for j, ext in enumerate(bt.rep):
+        if differ:
+            lo_box.append(0)
+            hi_box.append(ext - 1)
+        else:
+            lo_box.append(int(r_lo[j]))
+            hi_box.append(int(r_hi[j]))
+            differ = differ or r_lo[j] != r_hi[j]
+    tl = bt.tiler
+    mn = mx = int(tl.origin[0])
+    for j in range(len(bt.rep)):
+        p = int(tl.paving[0][j])
+        mn += min(p * lo_box[j], p * hi_box[j])
+        mx += max(p * lo_box[j], p * hi_box[j])
+    for k, ext in enumerate(tl.pattern):
+        f = int(tl.fitting[0][k])
+        mn += min(0, f * (ext - 1))
+        mx += max(0, f * (ext - 1))
+    s0 = int(bt.array[0])
+    stride0 = bt.array_total // s0
+    if mx - mn + 1 >= s0:
+        return [(0, bt.array_total)]
+    a0 = mn % s0
+    b0 = a0 + (mx - mn)
+    ivs = [(a0, b0)] if b0 < s0 else [(0, b0 - s0), (a0, s0 - 1)]
+    return [(a * stride0, (b + 1) * stride0) for a, b in ivs]
+
+
+def missing_ranges(have: list[tuple[int, int]], lo: int, hi: int) -> list[tuple[int, int]]:
+    """Parts of [lo, hi) not covered by the sorted disjoint ranges in `have`."""
+    out, pos = [], lo
+    for a, b in have:
+        if b <= pos or a >= hi:
+            continue
+        if a > pos:
+            out.append((pos, a))
+        pos = max(pos, b)
+        if pos >= hi:
+            break
+    if pos < hi:
+        out.append((pos, hi))
+    return out
+
+
+def add_range(have: list[tuple[int, int]], lo: int, hi: int) -> list[tuple[int, int]]:
+    """Union of sorted disjoint ranges with [lo, hi), merged and sorted."""
+    out = []
+    for a, b in sorted(have + [(lo, hi)]):
+        if out and a <= out[-1][1]:
+            out[-1] = (out[-1][0], max(out[-1][1], b))
+        else:
+            out.append((a, b))
+    return out
+
+
 class Exchange:
     """Variable-size all-gather of packed pattern streams over a torch.distributed group."""
 

@@ -288,13 +288,13 @@ class Executor:
         """Run a one-step schedule chunk by chunk straight from host memory.
 
         Each launch range is split into ``pipeline`` contiguous chunks.  For
-        chunk c: the part of every input's hull (distributed.input_hull) not
+        chunk c: the part of every input's ranges (distributed.input_ranges) not
         yet resident is copied H2D on a copy stream; the chunk launches on the
         compute stream once its inputs landed; its output hull is copied D2H
         on a third stream.  PCIe upload, tensor-core compute and download of
         consecutive chunks overlap.  Returns the root outputs (host).
         """
-        from .distributed import input_hull
+        from .distributed import add_range, input_hull, input_ranges, missing_ranges
         torch = _torch()
         step = self.schedule.steps[0]
         t = self.task(step.task_path)
@@ -313,7 +313,7 @@ class Executor:
                  or t.spec.port_spec(n).scalar]
         in_ports = [n for n in in_ports if n not in whole]
         bound = {n: self._port_bound(t, n) for n in in_ports + out_ports}
-        uploaded = {n: [0, 0] for n in in_ports}
+        uploaded: dict[str, list] = {n: [] for n in in_ports}
         root = self.model.application_components[self.model.application_root]
         root_out = {p.name: st.array(p.name) for p in root.ports if enum_value(p.direction) == "out"}
         hosts = {}
@@ -348,18 +348,11 @@ class Executor:
         for first, count in chunks:
             with torch.cuda.stream(cin):
                 for n in in_ports:
-                    lo, hi = input_hull(bound[n], first, count) if n in bound else (0, arrays[n].numel())
-                    u = uploaded[n]
-                    if u[1] == u[0]:
-                        upload(n, lo, hi)
-                        u[0], u[1] = lo, hi
-                    else:
-                        if lo < u[0]:
-                            upload(n, lo, u[0])
-                            u[0] = lo
-                        if hi > u[1]:
-                            upload(n, u[1], hi)
-                            u[1] = hi
+                    need = input_ranges(bound[n], first, count) if n in bound else [(0, arrays[n].numel())]
+                    for lo, hi in need:
+                        for a, b in missing_ranges(uploaded[n], lo, hi):
+                            upload(n, a, b)
+                            uploaded[n] = add_range(uploaded[n], a, b)
                 ev_in = torch.cuda.Event()
                 ev_in.record(cin)
             comp.wait_event(ev_in)

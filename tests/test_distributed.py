@@ -155,3 +155,42 @@ def test_input_hull_matches_offsets_single_process():
                     assert lo <= offs.min() and hi >= offs.max() + 1
                     if key == "a":   # rows of A: the hull is exact
                         assert lo == offs.min() and hi == offs.max() + 1
+
+
+def test_input_ranges_cover_toroidal_offsets():
+    """Seam-split ranges of wrapping tilers cover every offset the index function produces,
+    and stay small (a stencil chunk needs its rows plus the wrapped halo row only)."""
+    from paper_1105_4424_b200 import Tiler
+    from paper_1105_4424_b200.distributed import add_range, input_ranges, missing_ranges
+    rng = np.random.default_rng(17)
+    H, W = 64, 48
+    t = orc.stencil_tilers(H, W)
+    d = t["x"]
+    bt = Tiler(d["origin"], d["paving"], d["fitting"], d["pattern"]).bind(d["array"], d["rep"])
+    for first, count in ((0, 8 * W), (5 * W + 3, 17 * W), ((H - 4) * W, 4 * W), (0, H * W), (7, 1)):
+        rs = input_ranges(bt, first, count)
+        offs = orc.tiler_offsets(d, first, count)
+        covered = np.zeros(H * W, bool)
+        for lo, hi in rs:
+            covered[lo:hi] = True
+        assert covered[offs].all()
+        if count == 8 * W and first == 0:
+            assert rs == [(0, 9 * W), ((H - 1) * W, H * W)]
+    # random wrapping tilers
+    for _ in range(40):
+        arr = tuple(int(v) for v in rng.integers(3, 20, 2))
+        rep = tuple(int(v) for v in rng.integers(1, 9, 2))
+        d = dict(array=arr, rep=rep, pattern=(int(rng.integers(1, 4)),),
+                 origin=tuple(int(v) for v in rng.integers(-30, 30, 2)),
+                 paving=tuple(tuple(int(v) for v in rng.integers(-3, 4, 2)) for _ in range(2)),
+                 fitting=tuple(tuple(int(v) for v in rng.integers(-2, 3, 1)) for _ in range(2)))
+        bt = Tiler(d["origin"], d["paving"], d["fitting"], d["pattern"]).bind(d["array"], d["rep"])
+        R = int(np.prod(rep))
+        first = int(rng.integers(0, R))
+        count = int(rng.integers(1, R - first + 1))
+        covered = np.zeros(int(np.prod(arr)), bool)
+        for lo, hi in input_ranges(bt, first, count):
+            covered[lo:hi] = True
+        assert covered[orc.tiler_offsets(d, first, count)].all()
+    assert missing_ranges([(0, 4), (10, 12)], 2, 14) == [(4, 10), (12, 14)]
+    assert add_range([(0, 4), (10, 12)], 4, 10) == [(0, 12)]
