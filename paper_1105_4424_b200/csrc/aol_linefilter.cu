@@ -225,7 +225,14 @@ __global__ void __launch_bounds__(256, (REPS <= 2 ? 4 : 3)) k_line_filter_vstrip
 
 static_assert(sizeof(LineGeom) <= 256, "LineGeomBuf in aol_tile.cu must hold a LineGeom");
 
+static bool hline_stream_ok(const LineGeom& g);
+static bool vline_stream_ok(const LineGeom& g);
+static int launch_line_stream(const LineGeom& lg, int64_t first, int64_t count, const float* x, const float* w,
+                              float* y, cudaStream_t s);
+
 const char* line_filter_variant(const LineGeom& g) {
+  if (hline_stream_ok(g)) return "tile_filter.line_13x3_stream";
+  if (vline_stream_ok(g)) return "tile_filter.line_14x4_stream";
   if (g.px == 13 && g.py == 3) return "tile_filter.line_13x3";
   if (g.px == 14 && g.py == 4 && g.inner > 1 && g.sx == 9) return "tile_filter.line_14x4_vstrip";
   if (g.px == 14 && g.py == 4) return "tile_filter.line_14x4";
@@ -237,6 +244,7 @@ int launch_line_filter(const aol_task& t, const LineGeom& g, int64_t first, int6
   const float* x = static_cast<const float*>(ports[0]);
   const float* w = static_cast<const float*>(ports[1]);
   float* y = static_cast<float*>(ports[2]);
+  if (count > 0 && (hline_stream_ok(g) || vline_stream_ok(g))) return launch_line_stream(g, first, count, x, w, y, s);
   const unsigned grid = grid_for(count, 256, 8);
   // 32-bit offsets whenever both arrays fit (every in-range offset < 2^32)
   const bool idx32 = g.outer * g.Sx * g.inner < (1ll << 32) && g.outer * g.Sy * g.inner < (1ll << 32);
@@ -448,13 +456,16 @@ struct StreamGeom {
   int64_t first, last;           // consumer repetition range (rho, inclusive)
 };
 
-template <int PXH, int SXH, int PYH, int PXV, int SXV, int PYV>
+// VONLY: the consumer alone (unfused vertical filter): the ring holds rows of its input
+// (width W = Wm, no halo) and a thread's PYH "producer outputs" are the row's columns
+// PYH*lh .. PYH*lh + PYH-1, read from shared memory instead of computed.
+template <int PXH, int SXH, int PYH, int PXV, int SXV, int PYV, bool VONLY = false>
 __global__ void __launch_bounds__(512, 1) k_fused_stream(const float* __restrict__ x, const float* __restrict__ wh,
                                                           const float* __restrict__ wv, float* __restrict__ y,
                                                           StreamGeom g, int n_consumer_warps) {
   static_assert(PXV > SXV && PXV - SXV <= SXV, "consumer windows overlap by less than one paving step");
   extern __shared__ __align__(128) unsigned char fs_smem[];
-  const int RS = (int)g.W + 8;                                   // floats per stage (row + halo)
+  const int RS = (int)g.W + (VONLY ? 0 : 8);                     // floats per stage (row + halo)
   float* stages = reinterpret_cast<float*>(fs_smem);
   uint64_t* full = reinterpret_cast<uint64_t*>(fs_smem + (size_t)FS_NST * RS * 4);
   uint64_t* empty = full + FS_NST;
@@ -487,10 +498,10 @@ __global__ void __launch_bounds__(512, 1) k_fused_stream(const float* __restrict
           const int64_t row = (ra * SXV + sidx) % g.R;
           const float* src = x + (f * g.R + row) * g.W;
           mbar_wait(empty + stage, phase ^ 1);
-          mbar_expect_tx(full + stage, row_bytes + 32);
+          mbar_expect_tx(full + stage, row_bytes + (VONLY ? 0 : 32));
           float* dst = stages + (size_t)stage * RS;
           bulk_load(dst, src, row_bytes, full + stage);
-          bulk_load(dst + g.W, src, 32, full + stage);          // wrap halo: x[row][0..7]
+          if (!VONLY) bulk_load(dst + g.W, src, 32, full + stage);   // wrap halo: x[row][0..7]
           if (++stage == FS_NST) {
             stage = 0;
             phase ^= 1;
@@ -506,12 +517,17 @@ __global__ void __launch_bounds__(512, 1) k_fused_stream(const float* __restrict
   // window and never store)
   const int lh = threadIdx.x;
   const bool active = lh < g.NLh;
-  const uint32_t win = (uint32_t)(SXH * (active ? lh : 0)) * 4;   // window byte offset in a row
+  // window (fused) / column group (VONLY) byte offset in a row
+  const uint32_t win = (uint32_t)((VONLY ? PYH : SXH) * (active ? lh : 0)) * 4;
+  const int64_t left = g.Wm - (int64_t)PYH * lh;
+  const int ncol = VONLY ? (left < PYH ? (int)(left > 0 ? left : 0) : PYH) : PYH;   // columns this thread stores
   float whr[PYH][PXH];
+  if (!VONLY) {
 #pragma unroll
-  for (int j = 0; j < PYH; ++j)
+    for (int j = 0; j < PYH; ++j)
 #pragma unroll
-    for (int t = 0; t < PXH; ++t) whr[j][t] = wh[j * PXH + t];
+      for (int t = 0; t < PXH; ++t) whr[j][t] = wh[j * PXH + t];
+  }
   const uint32_t stage0 = smem_u32(stages);
   const uint32_t stage_bytes = (uint32_t)RS * 4;
   int stage = 0;
@@ -529,8 +545,12 @@ __global__ void __launch_bounds__(512, 1) k_fused_stream(const float* __restrict
         if (u == nrep && t >= PXV - SXV) break;
         mbar_wait(full + stage, phase);
         float xw[16];
-        {
-          const uint32_t a = stage0 + (uint32_t)stage * stage_bytes + win;
+        const uint32_t a = stage0 + (uint32_t)stage * stage_bytes + win;
+        if (VONLY) {
+#pragma unroll
+          for (int c = 0; c < PYH; ++c)
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xw[c]) : "r"(a + 4 * c));
+        } else {
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             float4 q;
@@ -556,14 +576,19 @@ __global__ void __launch_bounds__(512, 1) k_fused_stream(const float* __restrict
             }
         }
         float hv[PYH];                              // the producer's outputs, unfused order
+        if (VONLY) {
 #pragma unroll
-        for (int c = 0; c < PYH; ++c) hv[c] = 0.0f;
+          for (int c = 0; c < PYH; ++c) hv[c] = xw[c];
+        } else {
 #pragma unroll
-        for (int k = 0; k < PXH; ++k) {
+          for (int c = 0; c < PYH; ++c) hv[c] = 0.0f;
 #pragma unroll
-          for (int c = 0; c + 1 < PYH; c += 2)
-            add2_rn(hv[c], hv[c + 1], __fmul_rn(whr[c][k], xw[k]), __fmul_rn(whr[c + 1][k], xw[k]));
-          if (PYH % 2) hv[PYH - 1] = __fadd_rn(hv[PYH - 1], __fmul_rn(whr[PYH - 1][k], xw[k]));
+          for (int k = 0; k < PXH; ++k) {
+#pragma unroll
+            for (int c = 0; c + 1 < PYH; c += 2)
+              add2_rn(hv[c], hv[c + 1], __fmul_rn(whr[c][k], xw[k]), __fmul_rn(whr[c + 1][k], xw[k]));
+            if (PYH % 2) hv[PYH - 1] = __fadd_rn(hv[PYH - 1], __fmul_rn(whr[PYH - 1][k], xw[k]));
+          }
         }
         static_assert(PYV % 2 == 0, "consumer outputs are accumulated in pairs");
         if (u < nrep) {
@@ -585,7 +610,7 @@ __global__ void __launch_bounds__(512, 1) k_fused_stream(const float* __restrict
           if (t == PXV - SXV - 1 && active) {       // rep u-1 complete: store it
             const int64_t lv = ra + u - 1;
             float* yp = y + (f * g.Sy + lv * PYV) * g.Wm + (int64_t)lh * PYH;
-            if (whole) {
+            if (whole && ncol == PYH) {
 #pragma unroll
               for (int j = 0; j < PYV; ++j)
 #pragma unroll
@@ -596,7 +621,7 @@ __global__ void __launch_bounds__(512, 1) k_fused_stream(const float* __restrict
               for (int j = 0; j < PYV; ++j)
 #pragma unroll
                 for (int c = 0; c < PYH; ++c)
-                  if (rho0 + c >= g.first && rho0 + c <= g.last) yp[(int64_t)j * g.Wm + c] = prev[c][j];
+                  if (c < ncol && rho0 + c >= g.first && rho0 + c <= g.last) yp[(int64_t)j * g.Wm + c] = prev[c][j];
             }
           }
         }
@@ -630,6 +655,151 @@ static int launch_fused_stream(const FusedGeom& fg, int64_t first, int64_t count
   const int grid = (int)(nv < sms ? nv : sms);
   kern<<<grid, (cw + 1) * 32, smem, s>>>(x, wh, wv, y, g, cw);
   AOL_LAUNCH_CHECK("k_fused_stream");
+  return AOL_OK;
+}
+
+// Streaming horizontal line filter (inner == 1, the unfused H task): whole x rows (+ the
+// 32-byte wrap halo) through the same bulk-copy ring; thread lh computes the PY outputs of
+// repetition lh from a 16-float shared-memory window in k_line_filter's tap order.
+template <int PX, int SX, int PY>
+__global__ void __launch_bounds__(512, 1) k_hline_stream(const float* __restrict__ x, const float* __restrict__ w,
+                                                         float* __restrict__ y, StreamGeom g, int n_consumer_warps) {
+  extern __shared__ __align__(128) unsigned char fs_smem[];
+  const int RS = (int)g.W + 8;
+  float* stages = reinterpret_cast<float*>(fs_smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(fs_smem + (size_t)FS_NST * RS * 4);
+  uint64_t* empty = full + FS_NST;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < FS_NST; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, n_consumer_warps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t o_lo = g.first / g.NLh, o_hi = g.last / g.NLh + 1, no = o_hi - o_lo;
+  const int64_t r0 = o_lo + no * blockIdx.x / gridDim.x, r1 = o_lo + no * (blockIdx.x + 1) / gridDim.x;
+  const uint32_t row_bytes = (uint32_t)g.W * 4;
+  if (warp == n_consumer_warps) {                                 // producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t o = r0; o < r1; ++o) {
+        const float* src = x + o * g.W;
+        mbar_wait(empty + stage, phase ^ 1);
+        mbar_expect_tx(full + stage, row_bytes + 32);
+        float* dst = stages + (size_t)stage * RS;
+        bulk_load(dst, src, row_bytes, full + stage);
+        bulk_load(dst + g.W, src, 32, full + stage);
+        if (++stage == FS_NST) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    return;
+  }
+  const int lh = threadIdx.x;
+  const bool active = lh < g.NLh;
+  const uint32_t win = (uint32_t)(SX * (active ? lh : 0)) * 4;
+  float wr[PY][PX];
+#pragma unroll
+  for (int j = 0; j < PY; ++j)
+#pragma unroll
+    for (int t = 0; t < PX; ++t) wr[j][t] = w[j * PX + t];
+  const uint32_t stage0 = smem_u32(stages), stage_bytes = (uint32_t)RS * 4;
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int64_t o = r0; o < r1; ++o) {
+    mbar_wait(full + stage, phase);
+    float xw[16];
+    const uint32_t a = stage0 + (uint32_t)stage * stage_bytes + win;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float4 q;
+      asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(q.x), "=f"(q.y), "=f"(q.z), "=f"(q.w)
+                   : "r"(a + 16 * e));
+      xw[4 * e] = q.x; xw[4 * e + 1] = q.y; xw[4 * e + 2] = q.z; xw[4 * e + 3] = q.w;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + stage);
+    if (++stage == FS_NST) {
+      stage = 0;
+      phase ^= 1;
+    }
+    float hv[PY];
+#pragma unroll
+    for (int c = 0; c < PY; ++c) hv[c] = 0.0f;
+#pragma unroll
+    for (int k = 0; k < PX; ++k) {
+#pragma unroll
+      for (int c = 0; c + 1 < PY; c += 2)
+        add2_rn(hv[c], hv[c + 1], __fmul_rn(wr[c][k], xw[k]), __fmul_rn(wr[c + 1][k], xw[k]));
+      if (PY % 2) hv[PY - 1] = __fadd_rn(hv[PY - 1], __fmul_rn(wr[PY - 1][k], xw[k]));
+    }
+    const int64_t rho = o * g.NLh + lh;
+    if (active && rho >= g.first && rho <= g.last) {
+      float* yp = y + o * g.Wm + (int64_t)lh * PY;
+#pragma unroll
+      for (int c = 0; c < PY; ++c) yp[c] = hv[c];
+    }
+  }
+}
+
+// the unfused streaming forms (H: 13 taps paving 8 -> 3; V: 14 taps paving 9 -> 4)
+static bool hline_stream_ok(const LineGeom& g) {
+  if (getenv("AOL_LINE_CLASSIC")) return false;
+  return g.inner == 1 && g.px == 13 && g.sx == 8 && g.py == 3 && g.sy == 3 && g.ox == 0 && g.oy == 0 &&
+         g.NL * g.sx == g.Sx && g.NL * g.sy == g.Sy && g.Sx % 4 == 0 && g.NL <= 15 * 32 &&
+         (size_t)FS_NST * (g.Sx + 8) * 4 + 256 <= 200 * 1024;
+}
+
+static bool vline_stream_ok(const LineGeom& g) {
+  if (getenv("AOL_LINE_CLASSIC")) return false;
+  return g.inner > 1 && g.px == 14 && g.sx == 9 && g.py == 4 && g.sy == 4 && g.ox == 0 && g.oy == 0 &&
+         g.inner % 4 == 0 && (g.inner + 2) / 3 <= 15 * 32 && (size_t)FS_NST * g.inner * 4 + 256 <= 200 * 1024;
+}
+
+static int launch_line_stream(const LineGeom& lg, int64_t first, int64_t count, const float* x, const float* w,
+                              float* y, cudaStream_t s) {
+  StreamGeom g;
+  g.first = first;
+  g.last = first + count - 1;
+  int dev = 0, sms = 0;
+  AOL_CUDA_CHECK(cudaGetDevice(&dev));
+  AOL_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  if (lg.inner == 1) {
+    g.F = lg.outer;
+    g.R = 1;
+    g.W = lg.Sx;
+    g.NLh = lg.NL;
+    g.NLv = 1;
+    g.Wm = lg.Sy;
+    g.Sy = lg.Sy;
+    const int cw = (int)((lg.NL + 31) / 32);
+    const size_t smem = (size_t)FS_NST * (g.W + 8) * 4 + 2 * FS_NST * sizeof(uint64_t);
+    auto kern = k_hline_stream<13, 8, 3>;
+    AOL_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t rows = g.last / g.NLh - g.first / g.NLh + 1;
+    kern<<<(int)(rows < sms ? rows : sms), (cw + 1) * 32, smem, s>>>(x, w, y, g, cw);
+    AOL_LAUNCH_CHECK("k_hline_stream");
+    return AOL_OK;
+  }
+  g.F = lg.outer;
+  g.R = lg.Sx;
+  g.W = lg.inner;
+  g.NLh = (lg.inner + 2) / 3;
+  g.NLv = lg.NL;
+  g.Wm = lg.inner;
+  g.Sy = lg.Sy;
+  const int cw = (int)((g.NLh + 31) / 32);
+  const size_t smem = (size_t)FS_NST * g.W * 4 + 2 * FS_NST * sizeof(uint64_t);
+  auto kern = k_fused_stream<13, 8, 3, 14, 9, 4, true>;
+  AOL_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t nv = g.last / g.Wm - g.first / g.Wm + 1;
+  kern<<<(int)(nv < sms ? nv : sms), (cw + 1) * 32, smem, s>>>(x, nullptr, w, y, g, cw);
+  AOL_LAUNCH_CHECK("k_vline_stream");
   return AOL_OK;
 }
 

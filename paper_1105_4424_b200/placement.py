@@ -214,6 +214,12 @@ KERNEL_STAGING = {
     "tile_copy.affine": "HBM -> registers -> HBM (4-way unrolled scalars)",
     "tile_copy.generic": "HBM -> registers -> HBM (full index function)",
     "tile_filter.stencil_box": "coefficients: smem broadcast; (4+KH-1) x 6 input window: registers; outputs float4",
+    "tile_filter.line_13x3_stream": "x rows: HBM -> cp.async.bulk -> 8-stage smem ring (mbarriers); 16-float window: "
+                                    "ld.shared.v4 -> registers; outputs HBM",
+    "tile_filter.line_14x4_stream": "input rows: HBM -> cp.async.bulk -> 8-stage smem ring; 3 columns per thread; "
+                                    "2 x 12 consumer accumulators in registers; outputs HBM",
+    "tile_filter.fused_stream": "x rows: HBM -> cp.async.bulk -> 8-stage smem ring; producer outputs in registers "
+                                "folded into 2 x 12 consumer accumulators; intermediate never stored",
     "tile_filter.line_13x3": "coefficients: smem broadcast; 13-tap window: registers (float4 loads); outputs HBM",
     "tile_filter.line_14x4": "coefficients: smem broadcast; 14-tap window: registers (coalesced row taps)",
     "tile_filter.line_14x4_vstrip": "coefficients: smem broadcast; 4 overlapping 14-tap windows (41 rows): registers "

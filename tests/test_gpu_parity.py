@@ -375,17 +375,23 @@ def test_stencil_box_kernel_vs_oracle(H, W, origin, kh, devices, form, monkeypat
     assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
 
 
+@pytest.mark.parametrize("form", ["stream", "classic"])
 @pytest.mark.parametrize("kind,dims,devices", [
     ("h", (2, 5, 384), 1), ("h", (3, 7, 96), 3), ("v", (2, 45, 64), 1), ("v", (3, 27, 40), 4),
-    ("h_shift", (2, 3, 128), 2), ("v_generic", (2, 40, 24), 3)])
-def test_line_filter_kernel_vs_oracle(kind, dims, devices):
+    ("h_shift", (2, 3, 128), 2), ("v_generic", (2, 40, 24), 3), ("h", (2, 9, 3840), 5), ("v", (2, 54, 1440), 3),
+    ("v", (1, 36, 1436), 2)])
+def test_line_filter_kernel_vs_oracle(kind, dims, devices, form, monkeypatch):
+    """Line filters (streaming bulk-copy ring forms and the register forms) bit-exact vs the oracle,
+    for launch ranges that split rows, toroidal windows and column counts not divisible by 3."""
+    if form == "classic":
+        monkeypatch.setenv("AOL_LINE_CLASSIC", "1")
     F, H, W = dims
     if kind.startswith("h"):
         t = orc.hfilter_tilers(F, H, W)
         w = orc.hfilter_weights()
         if kind == "h_shift":
             t["x"] = dict(t["x"], origin=(0, 0, W - 2))       # window starts 2 left: wraps at the row start
-        expect = "tile_filter.line_13x3"
+        expect = "tile_filter.line_13x3" if (form == "classic" or kind == "h_shift") else "tile_filter.line_13x3_stream"
     else:
         if kind == "v_generic":
             t = orc.vfilter_tilers(F, H, W, taps=6, step=4, outs=2)
@@ -394,7 +400,7 @@ def test_line_filter_kernel_vs_oracle(kind, dims, devices):
         else:
             t = orc.vfilter_tilers(F, H, W)
             w = orc.vfilter_weights()
-            expect = "tile_filter.line_14x4_vstrip"
+            expect = "tile_filter.line_14x4_vstrip" if form == "classic" else "tile_filter.line_14x4_stream"
     assert _plan([t["x"], t["y"]]) == expect
     x = np.random.default_rng(F * H * W).random(int(np.prod(t["x"]["array"]))).astype(np.float32)
     got, ref = _filter_case("tile_filter", t, w, x, devices)
