@@ -62,8 +62,7 @@ struct LProg {
   double* part;                               // [2][64][kDotBlocks] partials
   int64_t* state;                             // iterations, relres (bits), converged
   unsigned* ticket;                           // [2][64] arrivals per dot
-  unsigned* flag;                             // [2][64] last published dot sequence number
-  double* result;                             // [2][64] published dot values
+  unsigned long long* result;                 // [2][64] published dot values (kSlotEmpty: not yet)
   unsigned long long* prof;                   // AOL_LOOP_PROFILE: ns per group, CTA 0's view
   unsigned backoff_ns;                        // sleep between polls of a dot's flag
   LGroup groups[kLoopMaxGroups];
@@ -71,13 +70,15 @@ struct LProg {
   void* ports[kLoopMaxPorts];
 };
 
-__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
+constexpr unsigned long long kSlotEmpty = ~0ull;   // sentinel NaN: never an arithmetic result
+
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
 
 __device__ __forceinline__ void sub_sync(int sub) {
@@ -91,7 +92,6 @@ __global__ void __launch_bounds__(kLoopThreads, 1) k_loop_persistent(const __gri
   __shared__ double red[kLoopSub][8];
   __shared__ double gred[32];
   __shared__ int s_last;
-  unsigned seq = 0;                           // dots executed so far (same in every CTA)
   const int sub = threadIdx.x >> 8, t = threadIdx.x & 255, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int slot = blockIdx.x * kLoopSub + sub, nslots = gridDim.x * kLoopSub;
   const bool writer = blockIdx.x == 0 && threadIdx.x == 0;
@@ -240,8 +240,10 @@ __global__ void __launch_bounds__(kLoopThreads, 1) k_loop_persistent(const __gri
         atomicAdd(P.prof + kLoopMaxGroups + 2 * blockIdx.x, t1 - t_grp);
       }
       // Ticket instead of a grid barrier: the last CTA to arrive runs k_dot's final tree
-      // once and publishes the value; the others wait for it and read 8 bytes.
-      ++seq;
+      // once and publishes the value into an 8-byte slot holding a sentinel NaN (all ones:
+      // arithmetic only produces the canonical NaN); the others poll that slot with acquire
+      // loads and get the value in the same load.  The slot of the other parity (read by
+      // everyone one iteration ago, written again one iteration ahead) is re-armed first.
       __syncthreads();
       if (threadIdx.x == 0) {
         __threadfence();
@@ -261,20 +263,24 @@ __global__ void __launch_bounds__(kLoopThreads, 1) k_loop_persistent(const __gri
         if (threadIdx.x < 32) {
           const double w = warp_sum(gred[lane]);
           if (lane == 0) {
-            P.result[cell] = w;
             P.ticket[cell] = 0;
+            P.result[cell ^ 64] = kSlotEmpty;
             __threadfence();
-            st_release(P.flag + cell, seq);
+            st_release_u64(P.result + cell, (unsigned long long)__double_as_longlong(w));
+            gred[0] = w;
           }
         }
       } else if (threadIdx.x == 0) {
-        while (ld_relaxed(P.flag + cell) != seq) __nanosleep(P.backoff_ns);
-        __threadfence();
+        unsigned long long v;
+        uint32_t polls = 0;
+        while ((v = ld_acquire_u64(P.result + cell)) == kSlotEmpty) {
+          if (++polls == (1u << 31)) __trap();                  // a lost publish: fail, never hang
+          __nanosleep(P.backoff_ns);
+        }
+        gred[0] = __longlong_as_double((long long)v);
       }
       __syncthreads();
       if (P.prof && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2));
-      if (threadIdx.x == 0) gred[0] = __ldcg(P.result + cell);
-      __syncthreads();
       if (threadIdx.x < 32) {
         const double w = gred[0];
         if (lane == 0) {
@@ -535,7 +541,7 @@ extern "C" int aol_loop_persistent(const aol_loop_op* ops, int n_ops, void* cons
   P.scalar_mask = scalar;
   {
     const char* b = getenv("AOL_LOOP_BACKOFF_NS");
-    P.backoff_ns = b ? (unsigned)atoi(b) : 64u;
+    P.backoff_ns = b ? (unsigned)atoi(b) : 32u;
   }
 
   int dev = 0, coop = 0, per_sm = 0, sms = 0;
@@ -570,9 +576,9 @@ extern "C" int aol_loop_persistent(const aol_loop_op* ops, int n_ops, void* cons
   P.part = reinterpret_cast<double*>(scratch);
   P.state = reinterpret_cast<int64_t*>(scratch + part_bytes);
   P.ticket = reinterpret_cast<unsigned*>(scratch + part_bytes + 64);
-  P.flag = P.ticket + 128;
-  P.result = reinterpret_cast<double*>(P.flag + 128);
-  AOL_CUDA_CHECK(cudaMemsetAsync(P.ticket, 0, sync_bytes, s));
+  P.result = reinterpret_cast<unsigned long long*>(P.ticket + 256);
+  AOL_CUDA_CHECK(cudaMemsetAsync(P.ticket, 0, 256 * sizeof(unsigned), s));
+  AOL_CUDA_CHECK(cudaMemsetAsync(P.result, 0xff, 128 * sizeof(unsigned long long), s));
   AOL_CUDA_CHECK(cudaMemsetAsync(P.part, 0, part_bytes, s));
   P.prof = profile ? reinterpret_cast<unsigned long long*>(scratch + part_bytes + 64 + sync_bytes) : nullptr;
   if (profile) AOL_CUDA_CHECK(cudaMemsetAsync(P.prof, 0, prof_bytes, s));
