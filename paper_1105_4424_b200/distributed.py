@@ -262,7 +262,6 @@ def _written_ports(task) -> list[str]:
 
 def _port_tiler(ex, task, name: str) -> BoundTiler:
     """Output tiler of a port: the task's tiler for tile ops, the identity tiler for reference ops."""
-    from .model import enum_value
     from .tiler import Tiler
     tl = dict(getattr(task.comp, "tilers", ()) or ())
     tl.update(ex.tilers.get(task.path, {}) or {})
