@@ -8,6 +8,9 @@
 // deterministic warp-shuffle tree (tolerance-pinned like the reference's BLAS
 // dot, tests/test_refexec.py:374-389).
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "aol_common.cuh"
 #include "aol_ident.cuh"
@@ -113,21 +116,23 @@ struct ScalarSeq {
   void* ports[3 * kMaxScalarSeq];
 };
 
-// Per device: kDotBlocks partials followed by the ticket counter (zeroed once, reset by
-// the last block of every dot).
-static double* dot_scratch(int dev) {
-  static double* bufs[64] = {nullptr};
-  if (dev < 0 || dev >= 64) return nullptr;
-  if (!bufs[dev]) {
-    double* p = nullptr;
-    if (cudaMalloc(&p, (kDotBlocks + 1) * sizeof(double)) != cudaSuccess) return nullptr;
-    if (cudaMemset(p, 0, (kDotBlocks + 1) * sizeof(double)) != cudaSuccess) {
-      cudaFree(p);
-      return nullptr;
-    }
-    bufs[dev] = p;
+// kDotBlocks partials followed by the ticket counter, per (device, stream): dots on one
+// stream are ordered, dots on different streams never share partials or tickets.  Zeroed
+// once; the last block of every dot resets the ticket.
+static double* dot_scratch(int dev, cudaStream_t stream) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, double*> bufs;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = bufs.find({dev, stream});
+  if (it != bufs.end()) return it->second;
+  double* p = nullptr;
+  if (cudaMalloc(&p, (kDotBlocks + 1) * sizeof(double)) != cudaSuccess) return nullptr;
+  if (cudaMemset(p, 0, (kDotBlocks + 1) * sizeof(double)) != cudaSuccess) {
+    cudaFree(p);
+    return nullptr;
   }
-  return bufs[dev];
+  bufs[{dev, stream}] = p;
+  return p;
 }
 
 // Host scalar ops of the reference (refexec.py:462-474) as one-thread device kernels, so a
@@ -166,10 +171,10 @@ __global__ void k_scalar_seq(ScalarSeq q) {
   }
 }
 
-double* dot_scratch_for_current_device() {
+double* dot_scratch_for_stream(cudaStream_t stream) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
-  return dot_scratch(dev);
+  return dot_scratch(dev, stream);
 }
 
 template <typename T>
@@ -222,7 +227,7 @@ static int launch_ident_t(const aol_task& t, int64_t first, int64_t count, void*
     case AOL_OP_DOT_PARTIAL: {
       int dev = 0;
       AOL_CUDA_CHECK(cudaGetDevice(&dev));
-      double* part = dot_scratch(dev);
+      double* part = dot_scratch(dev, s);
       if (!part) return fail(AOL_ECUDA, "cannot allocate dot scratch");
       k_dot<T><<<kDotBlocks, 256, 0, s>>>((const T*)ports[0], (const T*)ports[1], first, count, part,
                                           reinterpret_cast<unsigned*>(part + kDotBlocks), (T*)ports[2]);

@@ -11,7 +11,7 @@
 
 namespace aol {
 
-double* dot_scratch_for_current_device();
+double* dot_scratch_for_stream(cudaStream_t stream);
 
 struct LoopState {
   int64_t iterations;
@@ -58,7 +58,8 @@ int aol_loop_begin(void* stream, const void* relres_dev, int relres_dtype, doubl
                    aol_loop** out) {
   if (!stream || !relres_dev || !out || max_iter < 1) return fail(AOL_EINVAL, "aol_loop_begin: bad arguments");
   if (relres_dtype != AOL_F32 && relres_dtype != AOL_F64) return fail(AOL_EINVAL, "relres must be float32/float64");
-  if (!dot_scratch_for_current_device()) return fail(AOL_ECUDA, "cannot allocate dot scratch");
+  // dots captured on this stream use its scratch: allocate it now (no cudaMalloc during capture)
+  if (!dot_scratch_for_stream(static_cast<cudaStream_t>(stream))) return fail(AOL_ECUDA, "cannot allocate dot scratch");
   aol_loop* L = new (std::nothrow) aol_loop();
   if (!L) return fail(AOL_ECUDA, "out of host memory");
   L->stream = static_cast<cudaStream_t>(stream);

@@ -878,3 +878,27 @@ def test_loop_persistent_abi_errors():
     v[1] = 1.0
     it, rr, conv = _capi.loop_persistent(ops, p, "float64", "int32", 2, 1e-10, 7)
     assert (it, rr, conv) == (7, 1.0, False)
+
+
+def test_dots_on_concurrent_streams():
+    """dot_partial launches on different streams at once do not share partials or tickets:
+    every result equals the same dot launched alone."""
+    from paper_1105_4424_b200 import _capi
+    rng = np.random.default_rng(23)
+    n = 3_000_000
+    task = _capi.make_task("dot_partial", "float64")
+    vecs = [(torch.from_numpy(rng.standard_normal(n)).cuda(), torch.from_numpy(rng.standard_normal(n)).cuda())
+            for _ in range(6)]
+    alone = []
+    for a, b in vecs:
+        o = torch.zeros(1, dtype=torch.float64, device="cuda")
+        _capi.launch(task, 0, n, [a.data_ptr(), b.data_ptr(), o.data_ptr()])
+        torch.cuda.synchronize()
+        alone.append(o.item())
+    streams = [torch.cuda.Stream() for _ in vecs]
+    outs = [torch.zeros(1, dtype=torch.float64, device="cuda") for _ in vecs]
+    for _ in range(20):
+        for (a, b), st, o in zip(vecs, streams, outs):
+            _capi.launch(task, 0, n, [a.data_ptr(), b.data_ptr(), o.data_ptr()], (), st.cuda_stream)
+        torch.cuda.synchronize()
+        assert [o.item() for o in outs] == alone
