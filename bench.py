@@ -398,39 +398,52 @@ class SweepWorkload(Workload):
 
     POINTS_M = (1, 2, 4, 8, 16, 32, 64)
 
-    def __init__(self, torch, device, rank, world, max_out_bytes=8 << 30):
+    # per-point HBM footprint cap (input span + output): <= ~150 GB of the 180 GB
+    MAX_FOOTPRINT = 120e9
+    # the step()/e2e point stays resident while the table is measured
+    MAIN_MAX_OUT = 8 << 30
+
+    @staticmethod
+    def _geometry(m, kind, T):
+        """(input span, distinct input elements) of one sweep point."""
+        if kind == "rowstride":
+            return m * T, m * T
+        p = {"dense": m, "overlap": max(1, m // 2), "gaps": 2 * m, "strided": m * 2}[kind]
+        f = 2 if kind == "strided" else 1
+        span = (T - 1) * p + (m - 1) * f + 1
+        return span, (span if kind == "overlap" else T * m)
+
+    def __init__(self, torch, device, rank, world):
         self.torch, self.device = torch, device
-        self.max_out = max_out_bytes
         self.points = []
         for m in self.POINTS_M:
             for kind in ("dense", "overlap", "gaps", "strided", "rowstride"):
                 if kind in ("overlap", "strided", "rowstride") and m == 1:
                     continue
                 for T in (10 ** 3, 10 ** 5, 10 ** 7, 10 ** 8, 10 ** 9):
-                    if T * m * 4 > self.max_out:
+                    if (self._geometry(m, kind, T)[0] + T * m) * 4 > self.MAX_FOOTPRINT:
                         continue
                     self.points.append((m, kind, T))
-        big = [p for p in self.points if p[2] >= 10 ** 7]
+        big = [p for p in self.points if p[2] >= 10 ** 7 and p[2] * p[0] * 4 <= self.MAIN_MAX_OUT]
         self.main = max(big, key=lambda p: p[2] * p[0])
         self.task = self._make(*self.main)
         self.units_per_step = self.task["bytes"] / 1e9
         self.algorithmic = {"bytes_per_launch": self.task["bytes"],
                             "per_unit": "distinct input elements read + output elements written, x 4 B"}
         self.workload = f"tile_copy sweep; step = pattern {self.main[0]} {self.main[1]} T={self.main[2]:.0e}"
-        self.l2 = "sweep points with T*m >= 1e7 exceed the L2"
+        self.l2 = ("step point exceeds the L2; table points below 3x the L2 are timed with a 256 MiB "
+                   "L2 flush before each launch (l2_flushed)")
 
     def _make(self, m, kind, T):
         from paper_1105_4424_b200 import Tiler, _capi
         torch = self.torch
+        span, distinct = self._geometry(m, kind, T)
         if kind == "rowstride":
             # array [m, T] row-major: repetition r walks a row, pattern i walks down a column
-            span, distinct = m * T, m * T
             src = Tiler((0, 0), ((0,), (1,)), ((1,), (0,)), (m,)).bind((m, T), (T,))
         else:
             p = {"dense": m, "overlap": max(1, m // 2), "gaps": 2 * m, "strided": m * 2}[kind]
             f = 2 if kind == "strided" else 1
-            span = (T - 1) * p + (m - 1) * f + 1
-            distinct = span if (kind == "overlap") else T * m
             src = Tiler((0,), ((p,),), ((f,),), (m,)).bind((span,), (T,))
         dst = Tiler((0,), ((m,),), ((1,),), (m,)).bind((T * m,), (T,))
         x = torch.empty(span, device=self.device).uniform_()
@@ -445,26 +458,45 @@ class SweepWorkload(Workload):
         t = self.task
         _capi.launch(t["task"], 0, t["T"], t["ptrs"], (), int(self.torch.cuda.current_stream().cuda_stream))
 
+    L2_BYTES = 126 << 20
+
     def measure_points(self, steps=10, warmup=3):
+        """Per-point table.  Points whose footprint is below 3x the L2 are timed launch by
+        launch with a 256 MiB L2 flush before each launch (outside its event pair); larger
+        points are timed back to back."""
         torch = self.torch
+        from paper_1105_4424_b200 import _capi
         rows = []
+        scrub = torch.empty(64 << 20, dtype=torch.float32, device=self.device)
         for m, kind, T in self.points:
             t = self._make(m, kind, T)
-            from paper_1105_4424_b200 import _capi
             st = int(torch.cuda.current_stream().cuda_stream)
             for _ in range(warmup):
                 _capi.launch(t["task"], 0, T, t["ptrs"], (), st)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            for _ in range(steps):
-                _capi.launch(t["task"], 0, T, t["ptrs"], (), st)
-            e1.record()
-            e1.synchronize()
-            ms = e0.elapsed_time(e1) / steps
+            flush = (t["x"].numel() + t["y"].numel()) * 4 < 3 * self.L2_BYTES
+            if flush:
+                ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                      for _ in range(steps)]
+                for a, b in ev:
+                    scrub.fill_(float(len(rows)))
+                    a.record()
+                    _capi.launch(t["task"], 0, T, t["ptrs"], (), st)
+                    b.record()
+                torch.cuda.synchronize()
+                ms = sum(a.elapsed_time(b) for a, b in ev) / steps
+            else:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(steps):
+                    _capi.launch(t["task"], 0, T, t["ptrs"], (), st)
+                e1.record()
+                e1.synchronize()
+                ms = e0.elapsed_time(e1) / steps
             rows.append({"m": m, "paving": kind, "T": T, "plan": t["plan"], "ms": ms,
-                         "GBps": t["bytes"] / (ms * 1e-3) / 1e9})
+                         "GBps": t["bytes"] / (ms * 1e-3) / 1e9, "l2_flushed": flush})
             del t
             torch.cuda.empty_cache()
+        del scrub
         return rows
 
     def e2e_setup(self):

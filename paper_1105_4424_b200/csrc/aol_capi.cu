@@ -25,7 +25,8 @@ void count_launch(int n) { g_launches += n; }
 // defined in the kernel translation units
 int launch_tiler_offsets(const aol_tiler& t, int64_t first, int64_t count, int64_t* out, cudaStream_t s);
 int launch_tile_copy(const aol_task& t, int64_t first, int64_t count, void* const* ports, cudaStream_t s);
-const char* tile_copy_plan_name(const aol_tiler& ts, const aol_tiler& td, int64_t first, int64_t count);
+const char* tile_copy_plan_name(const aol_tiler& ts, const aol_tiler& td, int64_t first, int64_t count,
+                                size_t esz, void* const* ports);
 int launch_matmul_generic(const aol_task& t, int64_t first, int64_t count, void* const* ports, cudaStream_t s);
 int launch_filter_generic(const aol_task& t, int64_t first, int64_t count, void* const* ports, cudaStream_t s);
 const char* filter_plan_name(const aol_task& t);
@@ -81,7 +82,8 @@ static int64_t task_rep_total(const aol_task* t) {
 
 static const char* plan_name(const aol_task* t, int64_t first, int64_t count, void* const* ports) {
   switch (t->op) {
-    case AOL_OP_TILE_COPY: return tile_copy_plan_name(t->tilers[0], t->tilers[1], first, count);
+    case AOL_OP_TILE_COPY:
+      return tile_copy_plan_name(t->tilers[0], t->tilers[1], first, count, dtype_size(t->dtype), ports);
     case AOL_OP_MATMUL:
       if (ports && gemm_tf32_applicable(*t, ports))
         return t->precision == AOL_PREC_3XTF32 ? "matmul.tcgen05_3xtf32" : "matmul.tcgen05_tf32";

@@ -15,6 +15,9 @@ void set_error(const std::string& msg);
 int fail(int status, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* what);
 void count_launch(int n = 1);
+// cuTensorMapEncodeTiled through the runtime's driver entry point (nullptr if unavailable);
+// cast to PFN_cuTensorMapEncodeTiled_v12000 (cudaTypedefs.h)
+void* tensor_map_encoder();
 
 #define AOL_CUDA_CHECK(expr)                                   \
   do {                                                         \

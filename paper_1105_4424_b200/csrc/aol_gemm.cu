@@ -490,6 +490,12 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+}  // namespace gemm
+
+void* tensor_map_encoder() { return reinterpret_cast<void*>(gemm::encode_fn()); }
+
+namespace gemm {
+
 // 2-D fp32 tensor map: dims {inner, outer}, row pitch in elements, box {bi, bo}, 128B swizzle.
 static int make_map(CUtensorMap* map, const float* base, int64_t inner, int64_t outer, int64_t pitch, int bi,
                     int bo, bool kmajor) {

@@ -8,9 +8,13 @@
 // Arithmetic in the tile intrinsics uses __fmul_rn/__fadd_rn (no FMA contraction)
 // in pattern order, which is the order of the reference's spmv_csr executor
 // (refexec.py:111-121) that pins the oracle — results are bit-exact.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cstring>
 
+#include "aol_async.cuh"
 #include "aol_common.cuh"
 
 namespace aol {
@@ -241,6 +245,50 @@ __global__ void __launch_bounds__(256) k_tile_copy_vec(const T* __restrict__ src
       for (int u = 0; u < V; ++u) dst[doff + u] = v[u];
     }
   }
+}
+
+// TMA box copy: rows of `P` contiguous elements, row pitch As (source) / Ad (destination).
+// Both sides are 2-D tensor maps {P, rows}; a CTA streams boxes of R rows through a
+// STAGES-deep shared-memory ring: TMA load (mbarrier completion) -> TMA store
+// (bulk-group completion).  The copy engine issues only the bytes of each box, the SM
+// issues one instruction per box, and no register ever holds the data.  One elected
+// thread per CTA drives the whole pipeline (2 CTAs per SM for >= 128 B rows).
+template <int STAGES>
+__global__ void __launch_bounds__(32) k_tile_copy_tma(const __grid_constant__ CUtensorMap ms,
+                                                      const __grid_constant__ CUtensorMap md, int64_t ntiles, int R,
+                                                      uint32_t stage_bytes, uint32_t stage_pitch) {
+  extern __shared__ __align__(128) unsigned char ring[];
+  __shared__ __align__(8) uint64_t full[STAGES];
+  if (threadIdx.x != 0) return;
+  for (int st = 0; st < STAGES; ++st) mbar_init(&full[st], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  const int64_t mine = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;   // tiles blockIdx.x + k*gridDim.x
+  auto load = [&](int64_t k) {
+    const int st = (int)(k % STAGES);
+    const int row = (int)((blockIdx.x + k * gridDim.x) * R);
+    mbar_expect_tx(&full[st], stage_bytes);
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(ring + (size_t)st * stage_pitch)),
+        "l"(&ms), "r"(0), "r"(row), "r"(smem_u32(&full[st]))
+        : "memory");
+  };
+  for (int64_t k = 0; k < mine && k < STAGES; ++k) load(k);
+  for (int64_t k = 0; k < mine; ++k) {
+    const int st = (int)(k % STAGES);
+    mbar_wait(&full[st], (uint32_t)((k / STAGES) & 1));
+    const int row = (int)((blockIdx.x + k * gridDim.x) * R);
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(&md), "r"(0),
+                 "r"(row), "r"(smem_u32(ring + (size_t)st * stage_pitch))
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    // refill the stage of box k-1 once its store has finished reading shared memory
+    if (k >= 1 && k - 1 + STAGES < mine) {
+      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      load(k - 1 + STAGES);
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // "Row-stride" gathers: consecutive repetitions are adjacent in the source (As == 1) while
@@ -579,14 +627,28 @@ static bool collapse(const int64_t* coef, const int64_t* dims, int n, int64_t& s
   return true;
 }
 
+// TMA box rows: 16-byte aligned pitches, P*esz a 16-byte multiple of at least 32 bytes
+// (16-byte rows measured slower than register vectors), P <= 256 (box limit),
+// non-overlapping rows.
+static bool tma_rows_ok(int64_t P, int64_t As, int64_t Ad, size_t esz) {
+  const int64_t rb = P * (int64_t)esz;
+  return P <= 256 && rb >= 32 && rb % 16 == 0 && (As * (int64_t)esz) % 16 == 0 && (Ad * (int64_t)esz) % 16 == 0 &&
+         As >= P && Ad >= P;
+}
+
+constexpr int64_t kTmaStreamRow = 256;      // bytes per TMA row when a dense copy is streamed as boxes
+constexpr int64_t kTmaMinBytes = 1 << 20;   // below this the single-pass register copy wins (launch-bound)
+
 struct CopyPlan {
   int kind;  // 0 generic, 1 affine1, 2 stream, 3 vector (V elements / thread), 4 transpose
   int64_t cs, As, Bs, cd, Ad, Bd;
   int V;
   bool src_vec;
+  bool tma;  // kinds 2/3: TMA box ring first (k_tile_copy_tma), the register path if misaligned
 };
 
-static CopyPlan plan_tile_copy(const aol_tiler& ts, const aol_tiler& td, int64_t first, int64_t count) {
+static CopyPlan plan_tile_copy(const aol_tiler& ts, const aol_tiler& td, int64_t first, int64_t count,
+                               size_t esz) {
   CopyPlan p{};
   Affine s = tiler_affine(ts), d = tiler_affine(td);
   if (!s.ok || !d.ok) return p;
@@ -595,7 +657,6 @@ static CopyPlan plan_tile_copy(const aol_tiler& ts, const aol_tiler& td, int64_t
   if (!collapse(s.A, ts.rep, ts.rep_rank, As) || !collapse(d.A, td.rep, td.rep_rank, Ad)) return p;
   if (!collapse(s.B, ts.pattern, ts.pat_rank, Bs) || !collapse(d.B, td.pattern, td.pat_rank, Bd)) return p;
   const int64_t P = tiler_pat_total(ts);
-  if (count * P >= (1ll << 32)) return p;
   p.kind = 1;
   p.cs = s.c0; p.As = As; p.Bs = P > 1 ? Bs : 0;
   p.cd = d.c0; p.Ad = Ad; p.Bd = P > 1 ? Bd : 0;
@@ -603,6 +664,7 @@ static CopyPlan plan_tile_copy(const aol_tiler& ts, const aol_tiler& td, int64_t
   const bool dst_dense = (P == 1 || p.Bd == 1) && p.Ad == P;
   if (src_dense && dst_dense) {
     p.kind = 2;
+    p.tma = count * P * (int64_t)esz >= kTmaMinBytes && (p.cs * (int64_t)esz) % 16 == (p.cd * (int64_t)esz) % 16;
     return p;
   }
   // row-stride gather into a dense stream: transpose through shared memory
@@ -623,48 +685,125 @@ static CopyPlan plan_tile_copy(const aol_tiler& ts, const aol_tiler& td, int64_t
       break;
     }
   }
+  // contiguous pattern rows on both sides at 16-byte pitches: TMA boxes
+  if (p.kind == 3 && P > 1 && p.Bs == 1 && p.Bd == 1 && (p.cs * (int64_t)esz) % 16 == 0 &&
+      (p.cd * (int64_t)esz) % 16 == 0 && tma_rows_ok(P, p.As, p.Ad, esz) && count * P * (int64_t)esz >= kTmaMinBytes)
+    p.tma = true;
   (void)first;
   return p;
 }
 
-const char* tile_copy_plan_name(const aol_tiler& ts, const aol_tiler& td, int64_t first, int64_t count) {
-  const CopyPlan pl = plan_tile_copy(ts, td, first, count);
+const char* tile_copy_plan_name(const aol_tiler& ts, const aol_tiler& td, int64_t first, int64_t count,
+                                size_t esz, void* const* ports) {
+  const CopyPlan pl = plan_tile_copy(ts, td, first, count, esz);
+  const bool aligned = !ports || ((uintptr_t)ports[0] % 16 == 0 && (uintptr_t)ports[1] % 16 == 0);
   switch (pl.kind) {
     case 4: return "tile_copy.transpose";
-    case 3: return pl.src_vec ? "tile_copy.vec" : "tile_copy.vec_store";
-    case 2: return "tile_copy.stream16";
+    case 3:
+      if (pl.tma && aligned) return "tile_copy.tma_box";
+      return pl.src_vec ? "tile_copy.vec" : "tile_copy.vec_store";
+    case 2: return pl.tma ? "tile_copy.tma_stream" : "tile_copy.stream16";
     case 1: return "tile_copy.affine";
     default: return "tile_copy.generic";
   }
+}
+
+// Rows of P contiguous elements at pitches As (src) / Ad (dst) through k_tile_copy_tma.
+// Returns AOL_EUNSUPPORTED (nothing launched) when the alignment is not expressible as
+// TMA boxes (tma_rows_ok + 16-byte aligned bases).
+static int launch_tma_rows(const void* src, void* dst, int64_t rows, int64_t P, int64_t As, int64_t Ad, size_t esz,
+                           cudaStream_t stream) {
+  if (!tma_rows_ok(P, As, Ad, esz) || (uintptr_t)src % 16 || (uintptr_t)dst % 16) return AOL_EUNSUPPORTED;
+  auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(tensor_map_encoder());
+  if (!encode) return AOL_EUNSUPPORTED;
+  const int64_t rb = P * (int64_t)esz;
+  // ring geometry (measured, tools/micro/gapload.cu): ~32 KB in flight per CTA for 32-64 B
+  // rows, 4 x 8 KB stages and 2 CTAs per SM for >= 128 B rows
+  const int R = (int)std::min<int64_t>(256, std::max<int64_t>(1, (rb <= 32 ? 2048 : rb < 128 ? 4096 : 8192) / rb));
+  const int stages = rb <= 32 ? 16 : rb < 128 ? 8 : 4;
+  const int cps = rb < 128 ? 1 : 2;
+  const uint32_t stage_bytes = (uint32_t)(R * rb);
+  const uint32_t stage_pitch = (stage_bytes + 127) & ~127u;   // TMA shared-memory boxes are 128 B aligned
+  const CUtensorMapDataType dt = esz == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32;
+  const int64_t kMaxRows = (int64_t)1 << 30;            // box coordinates are int32
+  for (int64_t r0 = 0; r0 < rows; r0 += kMaxRows) {
+    const int64_t n = std::min<int64_t>(kMaxRows, rows - r0);
+    CUtensorMap ms, md;
+    cuuint64_t dims[2] = {(cuuint64_t)P, (cuuint64_t)n};
+    cuuint64_t ss[1] = {(cuuint64_t)(As * (int64_t)esz)}, ds[1] = {(cuuint64_t)(Ad * (int64_t)esz)};
+    cuuint32_t box[2] = {(cuuint32_t)P, (cuuint32_t)R}, es[2] = {1, 1};
+    const char* s0 = static_cast<const char*>(src) + r0 * As * (int64_t)esz;
+    char* d0 = static_cast<char*>(dst) + r0 * Ad * (int64_t)esz;
+    if (encode(&ms, dt, 2, const_cast<char*>(s0), dims, ss, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+            CUDA_SUCCESS ||
+        encode(&md, dt, 2, d0, dims, ds, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+      if (r0 == 0) return AOL_EUNSUPPORTED;
+      return fail(AOL_ECUDA, "cuTensorMapEncodeTiled failed for a tile_copy chunk");
+    }
+    const int64_t ntiles = (n + R - 1) / R;
+    const int smem = stages * (int)stage_pitch;
+    int sms = kNumSMs, dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)sms * cps);
+    void (*k)(const CUtensorMap, const CUtensorMap, int64_t, int, uint32_t, uint32_t) =
+        stages == 16 ? k_tile_copy_tma<16> : stages == 8 ? k_tile_copy_tma<8> : k_tile_copy_tma<4>;
+    AOL_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    k<<<grid, 32, smem, stream>>>(ms, md, ntiles, R, stage_bytes, stage_pitch);
+    AOL_LAUNCH_CHECK("k_tile_copy_tma");
+  }
+  return AOL_OK;
 }
 
 template <typename T>
 static int launch_tile_copy_t(const aol_tiler& ts, const aol_tiler& td, int64_t first, int64_t count,
                               const void* src, void* dst, cudaStream_t stream) {
   const int64_t P = tiler_pat_total(ts);
-  CopyPlan p = plan_tile_copy(ts, td, first, count);
+  // the register kernels index (rho, iota) pairs with 32-bit divisions: split huge ranges
+  const int64_t max_count = std::max<int64_t>(1, ((int64_t)1 << 31) / std::max<int64_t>(P, 1));
+  if (count > max_count) {
+    for (int64_t c0 = 0; c0 < count; c0 += max_count) {
+      const int rc = launch_tile_copy_t<T>(ts, td, first + c0, std::min(max_count, count - c0), src, dst, stream);
+      if (rc) return rc;
+    }
+    return AOL_OK;
+  }
+  CopyPlan p = plan_tile_copy(ts, td, first, count, sizeof(T));
   const T* s = static_cast<const T*>(src);
   T* d = static_cast<T*>(dst);
+  if (p.kind == 3 && p.tma) {
+    const int rc = launch_tma_rows(s + p.cs + p.As * first, d + p.cd + p.Ad * first, count, P, p.As, p.Ad,
+                                   sizeof(T), stream);
+    if (rc != AOL_EUNSUPPORTED) return rc;
+  }
   if (p.kind == 2) {
     const T* s0 = s + p.cs + first * P;
     T* d0 = d + p.cd + first * P;
     const int64_t n = count * P;
-    const int64_t bytes = n * (int64_t)sizeof(T);
     if (((uintptr_t)s0 % 16) == ((uintptr_t)d0 % 16)) {
-      // peel to 16-byte alignment, stream the body, copy the tail
+      // peel to 16-byte alignment, stream the body (TMA box rows, then 16-byte vectors), copy the tail
       int64_t head = ((16 - ((uintptr_t)s0 % 16)) % 16) / sizeof(T);
       if (head > n) head = n;
       if (head) {
         k_stream_copy_tail<T><<<1, 32, 0, stream>>>(s0, d0, head);
         AOL_LAUNCH_CHECK("k_stream_copy_tail");
       }
-      const int64_t body16 = (bytes - head * (int64_t)sizeof(T)) / 16;
+      int64_t done = head;
+      constexpr int64_t row = kTmaStreamRow / (int64_t)sizeof(T);
+      if (p.tma && (n - done) / row > 0) {
+        const int64_t rows = (n - done) / row;
+        const int rc = launch_tma_rows(s0 + done, d0 + done, rows, row, row, row, sizeof(T), stream);
+        if (rc == AOL_OK) done += rows * row;
+        else if (rc != AOL_EUNSUPPORTED) return rc;
+      }
+      const int64_t body16 = (n - done) * (int64_t)sizeof(T) / 16;
       if (body16) {
         k_stream_copy16<<<grid_for(body16, 1024, 8), 256, 0, stream>>>(
-            reinterpret_cast<const uint4*>(s0 + head), reinterpret_cast<uint4*>(d0 + head), body16);
+            reinterpret_cast<const uint4*>(s0 + done), reinterpret_cast<uint4*>(d0 + done), body16);
         AOL_LAUNCH_CHECK("k_stream_copy16");
       }
-      const int64_t done = head + body16 * 16 / (int64_t)sizeof(T);
+      done += body16 * 16 / (int64_t)sizeof(T);
       if (n - done) {
         k_stream_copy_tail<T><<<1, 256, 0, stream>>>(s0 + done, d0 + done, n - done);
         AOL_LAUNCH_CHECK("k_stream_copy_tail");

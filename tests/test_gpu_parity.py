@@ -171,6 +171,49 @@ def test_tile_copy_plans_vs_oracle(case, devices, dtype):
     assert name.startswith("tile_copy.")
 
 
+@pytest.mark.parametrize("case", [
+    # (dtype, src array, T, m, src paving, dst pitch, expected plan)        TMA box ring plans (>= 1 MB)
+    ("float32", None, 40001, 8, 16, 8, "tile_copy.tma_box"),       # sweep "gaps", 32 B rows, ragged T
+    ("float32", None, 30000, 16, 20, 16, "tile_copy.tma_box"),     # 80 B source pitch
+    ("float32", None, 5000, 64, 128, 64, "tile_copy.tma_box"),     # 256 B rows
+    ("float32", None, 30000, 12, 12, 24, "tile_copy.tma_box"),     # gaps on the destination side
+    ("float64", None, 40000, 4, 8, 4, "tile_copy.tma_box"),        # 32 B fp64 rows
+    ("float32", None, 300001, 4, 4, 4, "tile_copy.tma_stream"),    # dense: 256 B rows + 16 B vectors + tail
+    ("float64", None, 150001, 2, 2, 2, "tile_copy.tma_stream"),
+    ("float32", None, 40000, 8, 4, 8, "tile_copy.vec"),            # overlapping rows: not a TMA box
+])
+@pytest.mark.parametrize("devices", [1, 3])
+def test_tile_copy_tma_plans_vs_oracle(case, devices):
+    from paper_1105_4424_b200 import _capi
+    dtype, _, T, m, p, pd, plan = case
+    span = (T - 1) * p + m
+    ts = dict(array=(span,), rep=(T,), pattern=(m,), origin=(0,), paving=((p,),), fitting=((1,),))
+    n_out = (T - 1) * pd + m
+    td = dict(array=(n_out,), rep=(T,), pattern=(m,), origin=(0,), paving=((pd,),), fitting=((1,),))
+    src = (np.arange(span) % (1 << 22)).astype(dtype) + 1
+    ports = {"src": _spec(ts, "in", dtype), "dst": _spec(td, "out", dtype)}
+    res = _run_tile("tile_copy", {"src": ts, "dst": td}, ports, {"src": src}, devices)
+    ref = orc.run_tile_task("tile_copy", {"src": ts, "dst": td}, {"src": src},
+                            {"dst": (n_out, np.dtype(dtype))}, T, devices)["dst"]
+    assert np.array_equal(res.outputs["p_dst"], ref)
+    bts, btd = _tiler(ts).bind(ts["array"], (T,)), _tiler(td).bind(td["array"], (T,))
+    task = _capi.make_task("tile_copy", dtype, [bts, btd])
+    x = torch.from_numpy(src).cuda()
+    y = torch.zeros(n_out, dtype=x.dtype, device="cuda")
+    assert _capi.plan_name(task, 0, T, [x.data_ptr(), y.data_ptr()]) == plan
+    if plan == "tile_copy.tma_box":
+        # misaligned bases fall back to the register path, same bits
+        xb = torch.zeros(span + 1, dtype=x.dtype, device="cuda")
+        xb[1:] = x
+        yb = torch.zeros(n_out + 1, dtype=x.dtype, device="cuda")
+        ptrs = [xb[1:].data_ptr(), yb[1:].data_ptr()]
+        assert _capi.plan_name(task, 0, T, ptrs) != plan
+        for off, cnt in orc.partition_equally(T, devices):
+            _capi.launch(task, off, cnt, ptrs, (), 0)
+        torch.cuda.synchronize()
+        assert np.array_equal(yb[1:].cpu().numpy(), ref)
+
+
 def _gemm_bound(a64, b64, K):
     return (2.0 ** -9 + K * 2.0 ** -23) * (np.abs(a64) @ np.abs(b64))
 
