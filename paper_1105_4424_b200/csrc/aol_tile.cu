@@ -628,12 +628,14 @@ static bool collapse(const int64_t* coef, const int64_t* dims, int n, int64_t& s
 }
 
 // TMA box rows: 16-byte aligned pitches, P*esz a 16-byte multiple of at least 32 bytes
-// (16-byte rows measured slower than register vectors), P <= 256 (box limit),
-// non-overlapping rows.
+// (16-byte rows measured slower than register vectors), P <= 256 (box limit), destination
+// rows disjoint.  Overlapping source rows (paving < pattern: the overlap re-reads hit L2)
+// only from 128-byte rows, where the box ring measured 6.1 vs 5.5 TB/s; below that the
+// register path wins (tools/micro/gapload.cu, profiles/r1_tma_vs_ldg_gather.json).
 static bool tma_rows_ok(int64_t P, int64_t As, int64_t Ad, size_t esz) {
   const int64_t rb = P * (int64_t)esz;
   return P <= 256 && rb >= 32 && rb % 16 == 0 && (As * (int64_t)esz) % 16 == 0 && (Ad * (int64_t)esz) % 16 == 0 &&
-         As >= P && Ad >= P;
+         As > 0 && (As >= P || rb >= 128) && Ad >= P;
 }
 
 constexpr int64_t kTmaStreamRow = 256;      // bytes per TMA row when a dense copy is streamed as boxes

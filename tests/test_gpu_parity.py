@@ -180,7 +180,8 @@ def test_tile_copy_plans_vs_oracle(case, devices, dtype):
     ("float64", None, 40000, 4, 8, 4, "tile_copy.tma_box"),        # 32 B fp64 rows
     ("float32", None, 300001, 4, 4, 4, "tile_copy.tma_stream"),    # dense: 256 B rows + 16 B vectors + tail
     ("float64", None, 150001, 2, 2, 2, "tile_copy.tma_stream"),
-    ("float32", None, 40000, 8, 4, 8, "tile_copy.vec"),            # overlapping rows: not a TMA box
+    ("float32", None, 40000, 8, 4, 8, "tile_copy.vec"),            # overlapping 32 B rows: register path
+    ("float32", None, 20001, 32, 16, 32, "tile_copy.tma_box"),     # overlapping 128 B rows: TMA box (L2 re-reads)
 ])
 @pytest.mark.parametrize("devices", [1, 3])
 def test_tile_copy_tma_plans_vs_oracle(case, devices):

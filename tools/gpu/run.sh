@@ -1,2 +1,2 @@
-python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
+python -m pytest tests/test_gpu_parity.py -x -q -k "tile_copy" > gpurun_out/pytest_tma.log 2>&1; echo pytest=$?
 python bench.py --workload sweep > gpurun_out/bench_sweep.json 2> gpurun_out/bench_sweep.err; echo sweep=$?

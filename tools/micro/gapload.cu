@@ -87,7 +87,7 @@ __global__ void k_fill(uint32_t* x, int64_t n) {
 __global__ void k_check(const uint32_t* d, int64_t T, int m, int pf, unsigned long long* bad) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < T * m; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / m, k = i - r * m;
-    if (d[i] != (uint32_t)(r * pf * m + k)) atomicAdd(bad, 1ull);
+    if (d[i] != (uint32_t)(r * pf + k)) atomicAdd(bad, 1ull);
   }
 }
 
@@ -98,12 +98,12 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode() {
   return (PFN_cuTensorMapEncodeTiled_v12000)p;
 }
 
-int PF = 2;   // paving = PF * m (1: dense, 2: gaps)
+int PF = 4;   // paving = PF * m / 2 (1: overlap, 2: dense, 4: gaps)
 template <int STAGES>
 float run_tma(const float* src, float* dst, int64_t T, int m, int reps, int R, int ctas_per_sm) {
   CUtensorMap ms, md;
   cuuint64_t dims[2] = {(cuuint64_t)m, (cuuint64_t)T};
-  cuuint64_t ss[1] = {(cuuint64_t)(PF * m * 4)}, ds[1] = {(cuuint64_t)(m * 4)};
+  cuuint64_t ss[1] = {(cuuint64_t)(PF * m / 2 * 4)}, ds[1] = {(cuuint64_t)(m * 4)};
   cuuint32_t box[2] = {(cuuint32_t)m, (cuuint32_t)R}, es[2] = {1, 1};
   auto fn = encode();
   CUresult r1 = fn(&ms, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)src, dims, ss, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -139,9 +139,9 @@ float run(const float* src, float* dst, int64_t T, int m, int reps) {
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  k_gap<MODE><<<grid, 256>>>(src, dst, ng, gpp, PF * m);
+  k_gap<MODE><<<grid, 256>>>(src, dst, ng, gpp, PF * m / 2);
   cudaEventRecord(a);
-  for (int i = 0; i < reps; ++i) k_gap<MODE><<<grid, 256>>>(src, dst, ng, gpp, PF * m);
+  for (int i = 0; i < reps; ++i) k_gap<MODE><<<grid, 256>>>(src, dst, ng, gpp, PF * m / 2);
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   float ms;
@@ -154,11 +154,11 @@ int main(int argc, char** argv) {
   const int only = argc > 2 ? atoi(argv[2]) : -1;
   const int reps = argc > 3 ? atoi(argv[3]) : 10;
   const int only_m = argc > 4 ? atoi(argv[4]) : 0;
-  PF = argc > 5 ? atoi(argv[5]) : 2;
+  PF = argc > 5 ? atoi(argv[5]) : 4;
   for (int m : {4, 8, 16, 32, 64}) {
     if (only_m && m != only_m) continue;
     float *src, *dst;
-    const size_t span = (size_t)T * PF * m;
+    const size_t span = (size_t)T * PF * m / 2 + m;
     if (cudaMalloc(&src, span * 4) != cudaSuccess || cudaMalloc(&dst, (size_t)T * m * 4) != cudaSuccess) {
       printf("alloc failed\n");
       return 1;
@@ -166,7 +166,7 @@ int main(int argc, char** argv) {
     k_fill<<<1184, 256>>>((uint32_t*)src, (int64_t)span);
     unsigned long long* bad;
     cudaMalloc(&bad, 8);
-    const double bytes = 2.0 * T * m * 4;
+    const double bytes = ((PF >= 2 ? (double)T * m : (double)span) + (double)T * m) * 4;
     for (int mode = 0; mode < 6; ++mode) {
       if (only >= 0 && mode != only) continue;
       float ms = 0;
@@ -188,7 +188,7 @@ int main(int argc, char** argv) {
           float ms = st == 4 ? run_tma<4>(src, dst, T, m, reps, R, cps)
                    : st == 8 ? run_tma<8>(src, dst, T, m, reps, R, cps) : run_tma<16>(src, dst, T, m, reps, R, cps);
           cudaMemset(bad, 0, 8);
-          k_check<<<1184, 256>>>((const uint32_t*)dst, T, m, PF, bad);
+          k_check<<<1184, 256>>>((const uint32_t*)dst, T, m, PF * m / 2, bad);
           unsigned long long nb = 0;
           cudaMemcpy(&nb, bad, 8, cudaMemcpyDeviceToHost);
           cudaMemset(dst, 0, (size_t)T * m * 4);
