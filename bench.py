@@ -933,40 +933,113 @@ def run_gpu(args):
     return out
 
 
+def _reference_arm(workload: str):
+    """(setup-free step function, unit, sample text, cores) of the reference's CPU algorithm for one
+    workload: the oracle's C restatement (oracle/aol_oracle.c, OpenMP) or its numpy interpreter
+    (CG), each step a bounded sample of the same workload.  Returns step(i) -> units done."""
+    from oracle import aol_oracle as orc
+    from oracle import c_oracle as co
+    thr = co.threads()
+    rng = np.random.default_rng(0)
+    if workload in ("matmul", "c1"):
+        M = N = K = 8192 if workload == "matmul" else 256
+        A = rng.standard_normal(M * K, dtype=np.float32)
+        B = rng.standard_normal(K * N, dtype=np.float32)
+        Cm = np.zeros(M * N, np.float32)
+        rows = max(thr, 8) if workload == "matmul" else M
+
+        def step(i):
+            lo = (i * rows) % max(1, M - rows)
+            co.gemm_rows(A, B, Cm, N, K, lo, lo + rows)
+            return 2.0 * rows * N * K / 1e12
+        return step, "TFLOP/s", (f"matmul {M}x{N}x{K} fp32, {rows} rows of C per step (oracle/aol_oracle.c, "
+                                 f"k-ascending fp32, OpenMP {thr} threads)"), thr
+    if workload == "stencil":
+        n = 16384
+        x = rng.standard_normal(n * n, dtype=np.float32)
+        y = np.zeros_like(x)
+        w = orc.stencil_weights()
+        rows = 256
+
+        def step(i):
+            lo = (i * rows) % (n - rows)
+            co.stencil_rows(x, w, y, n, n, lo, lo + rows)
+            return 2.0 * rows * n * 4 / 1e9
+        return step, "GB/s", f"toroidal 3x3 stencil {n}x{n} fp32, {rows} rows per step (oracle/aol_oracle.c)", thr
+    if workload == "downscaler":
+        H, W = 2160, 3840
+        th = orc.hfilter_tilers(1, H, W)
+        Wo = th["y"]["array"][2]
+        tv = orc.vfilter_tilers(1, H, Wo)
+        Ho = tv["y"]["array"][1]
+        x = rng.random(H * W, dtype=np.float32)
+        mid = np.zeros(H * Wo, np.float32)
+        y = np.zeros(Ho * Wo, np.float32)
+        rh, rv = int(np.prod(th["x"]["rep"])), int(np.prod(tv["x"]["rep"]))
+        wh, wv = orc.hfilter_weights(), orc.vfilter_weights()
+
+        def step(i):
+            co.tile_filter(x, wh, mid, th["x"], th["y"], 0, rh)
+            co.tile_filter(mid, wv, y, tv["x"], tv["y"], 0, rv)
+            return ((H * W + H * Wo) + (H * Wo + Ho * Wo)) * 4 / 1e9
+        return step, "GB/s", (f"downscaler, one {H}x{W} frame per step through hfilter then vfilter "
+                              f"(two tasks, as the reference schedules them; oracle/aol_oracle.c)"), thr
+    if workload == "sweep":
+        m, Ts = 2, 2_000_000
+        span = Ts * m
+        ts = dict(array=(span,), rep=(Ts,), pattern=(m,), origin=(0,), paving=((m,),), fitting=((1,),))
+        x = rng.random(span, dtype=np.float32)
+        y = np.zeros(Ts * m, np.float32)
+
+        def step(i):
+            co.tile_copy(x, y, ts, ts, 0, Ts)
+            return 2.0 * Ts * m * 4 / 1e9
+        return step, "GB/s", f"tile_copy sweep main point (pattern 2 dense), T={Ts} per step (oracle/aol_oracle.c)", thr
+    if workload in ("cg", "cg27"):
+        n, rp, ci, va = (_poisson_2d(364) if workload == "cg" else _poisson_3d27(51))
+        nnz = int(rp[-1])
+        st = {"x": np.zeros(n), "r": np.ones(n), "p": np.ones(n)}
+        st["rr"] = float(np.dot(st["r"], st["r"]))
+
+        def step(i):
+            ap = np.zeros(n)
+            orc.spmv_rows(rp, ci, va, st["p"], ap, 0, n)
+            alpha = st["rr"] / float(np.dot(st["p"], ap))
+            st["x"] += alpha * st["p"]
+            st["r"] += (-alpha) * ap
+            rrn = float(np.dot(st["r"], st["r"]))
+            st["p"] *= rrn / st["rr"]
+            st["p"] += st["r"]
+            st["rr"] = rrn
+            return (2 * nnz + 12 * n) / 1e9
+        return step, "GFLOP/s", (f"one CG iteration per step (n={n}, nnz={nnz}) with the oracle's "
+                                 f"level-synchronous spmv (refexec.py:111-121 restated, numpy)"), 1
+    raise ValueError(f"no reference arm for workload '{workload}'")
+
+
 def run_reference(args):
     """The reference arm: the reference's CPU algorithm (oracle port) on the host cores, rank 0 only."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     sys.path.insert(0, str(ROOT))
-    from oracle import c_oracle as co
-    M = N = K = 8192
-    rng = np.random.default_rng(0)
-    A = rng.standard_normal(M * K, dtype=np.float32)
-    B = rng.standard_normal(K * N, dtype=np.float32)
-    Cm = np.zeros(M * N, np.float32)
-    thr = co.threads()
-    rows = max(thr, 8)
-    for _ in range(args.warmup):
-        co.gemm_rows(A, B, Cm, N, K, 0, thr)
-    t = []
+    step, unit, sample, cores = _reference_arm(args.workload)
+    for i in range(args.warmup):
+        step(i)
+    t, units = [], 0.0
     for i in range(args.steps):
-        lo = (i * rows) % (M - rows)
         t0 = time.perf_counter()
-        co.gemm_rows(A, B, Cm, N, K, lo, lo + rows)
+        units += step(i)
         t.append(time.perf_counter() - t0)
     el = sum(t)
-    flops = 2.0 * rows * N * K * args.steps
-    value = flops / el / 1e12
-    out = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+    value = units / el
+    out = {"metric": METRIC, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": el * 1e3 / args.steps, "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (numpy default_rng)",
-           "impl": "reference",
-           "config": {"workload": f"matmul {M}x{N}x{K} fp32, bounded sample of {rows} rows of C per step"},
-           "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": thr, "kind": "port",
-                            "sample": f"{rows} rows x {N} cols x {K} k per step (oracle/aol_oracle.c, "
-                                      f"k-ascending fp32, OpenMP {thr} threads)"},
-           "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64" if args.workload.startswith("cg") else "f32",
+           "data": "synthetic (numpy default_rng)", "impl": "reference",
+           "config": {"workload": f"{args.workload}: bounded sample per step: {sample}"},
+           "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "port", "sample": sample},
+           "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
 
