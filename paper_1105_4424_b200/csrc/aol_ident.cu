@@ -53,12 +53,7 @@ __global__ void k_copy(const T* __restrict__ s, T* __restrict__ d, int64_t first
 template <typename T, typename I>
 __global__ void k_spmv(const I* __restrict__ rowptr, const I* __restrict__ colidx, const T* __restrict__ values,
                        const T* __restrict__ x, T* __restrict__ y, int64_t first, int64_t count) {
-  GRID_STRIDE(i, first, count) {
-    T acc = T(0);
-    const int64_t e = rowptr[i + 1];
-    for (int64_t k = rowptr[i]; k < e; ++k) acc = add_rn(acc, mul_rn(values[k], x[colidx[k]]));
-    y[i] = acc;
-  }
+  GRID_STRIDE(i, first, count) y[i] = csr_row(colidx, values, x, (int64_t)rowptr[i], (int64_t)rowptr[i + 1]);
 }
 
 // Deterministic single-pass dot: a fixed grid of kDotBlocks blocks, each reduces a fixed

@@ -43,7 +43,20 @@ constexpr int kLoopThreads = 256 * kLoopSub;
 
 struct LOp {
   int op, n_scalars, part, n_parts, dot;
+  int sell;                                   // spmv: index into LProg::sell, or -1 (CSR rows)
   int port[6];
+};
+
+// An spmv matrix the body never writes, re-laid out once per call as SELL-32: slice s holds
+// rows first+32s .. first+32s+31 of the op's range, entry k of lane l at base[s] + 32k + l.
+// A warp's 32 rows then load their k-th entries as one coalesced access instead of 32 lines
+// 216 B apart (tools/micro/sell.cu: 16.4 -> 7.6 us per 27-point spmv); the row sum still runs
+// k = 0, 1, ... left to right, so results are the CSR rows' bit for bit.
+constexpr int kLoopMaxSell = 4;
+struct LSell {
+  const int64_t* base;
+  const void* colidx;
+  const void* values;
 };
 
 // A group: consecutive vector ops over one launch range that need no barrier between them
@@ -63,8 +76,11 @@ struct LProg {
   int64_t* state;                             // iterations, relres (bits), converged
   unsigned* ticket;                           // [2][64] arrivals per dot
   unsigned long long* result;                 // [2][64] published dot values (kSlotEmpty: not yet)
+  unsigned long long* arrive;                 // [64] monotonic arrivals per dot (dot_mode 1)
+  int dot_mode;                               // 0: last CTA reduces and publishes; 1: every CTA reduces
   unsigned long long* prof;                   // AOL_LOOP_PROFILE: ns per group, CTA 0's view
   unsigned backoff_ns;                        // sleep between polls of a dot's flag
+  LSell sell[kLoopMaxSell];
   LGroup groups[kLoopMaxGroups];
   LOp ops[kLoopMaxOps];
   void* ports[kLoopMaxPorts];
@@ -83,6 +99,81 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
 
 __device__ __forceinline__ void sub_sync(int sub) {
   asm volatile("bar.sync %0, 256;" ::"r"(sub + 1) : "memory");
+}
+
+// one SELL-32 row: entries at b, b+32, b+64, ...; batches of 4 loads in flight, adds in order
+template <typename T, typename I>
+__device__ __forceinline__ T sell_row(const I* sc, const T* sv, const T* x, int64_t b, int len) {
+  T acc = T(0);
+  int k = 0;
+  for (; k + 4 <= len; k += 4) {
+    I c[4];
+    T v[4], xv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      c[u] = sc[b + 32 * (k + u)];
+      v[u] = sv[b + 32 * (k + u)];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) xv[u] = x[c[u]];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc = add_rn(acc, mul_rn(v[u], xv[u]));
+  }
+  for (; k < len; ++k) acc = add_rn(acc, mul_rn(sv[b + 32 * k], x[sc[b + 32 * k]]));
+  return acc;
+}
+
+// SELL build, step 1: 32 x (longest row) entries per slice (one warp per slice)
+template <typename I>
+__global__ void k_sell_width(const I* __restrict__ rowptr, int64_t first, int64_t count, int64_t* __restrict__ width) {
+  const int64_t ns = (count + 31) / 32;
+  const int lane = threadIdx.x & 31;
+  for (int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; s < ns;
+       s += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t r = s * 32 + lane;
+    int64_t len = r < count ? (int64_t)(rowptr[first + r + 1] - rowptr[first + r]) : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) len = max(len, __shfl_xor_sync(0xffffffffu, len, o));
+    if (lane == 0) width[s] = 32 * len;
+  }
+}
+
+// step 2: exclusive scan of the slice widths into base[0..ns] (one CTA, ns small)
+__global__ void __launch_bounds__(1024) k_sell_scan(const int64_t* __restrict__ width, int64_t ns,
+                                                    int64_t* __restrict__ base) {
+  __shared__ int64_t part[1024];
+  const int64_t per = (ns + 1023) / 1024, lo = threadIdx.x * per, hi = min(ns, lo + per);
+  int64_t sum = 0;
+  for (int64_t s = lo; s < hi; ++s) sum += width[s];
+  part[threadIdx.x] = sum;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    const int64_t v = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
+    __syncthreads();
+    part[threadIdx.x] += v;
+    __syncthreads();
+  }
+  int64_t run = threadIdx.x ? part[threadIdx.x - 1] : 0;
+  for (int64_t s = lo; s < hi; ++s) {
+    base[s] = run;
+    run += width[s];
+  }
+  if (threadIdx.x == 1023) base[ns] = part[1023];
+}
+
+// step 3: scatter every row's entries into its slice, in row order
+template <typename T, typename I>
+__global__ void k_sell_fill(const I* __restrict__ rowptr, const I* __restrict__ colidx, const T* __restrict__ values,
+                            int64_t first, int64_t count, const int64_t* __restrict__ base, I* __restrict__ sc,
+                            T* __restrict__ sv) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < count; r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q0 = rowptr[first + r], q1 = rowptr[first + r + 1];
+    const int64_t b = base[r >> 5] + (r & 31);
+    for (int64_t q = q0; q < q1; ++q) {
+      sc[b + 32 * (q - q0)] = colidx[q];
+      sv[b + 32 * (q - q0)] = values[q];
+    }
+  }
 }
 
 template <typename T, typename I>
@@ -198,11 +289,16 @@ __global__ void __launch_bounds__(kLoopThreads, 1) k_loop_persistent(const __gri
             const T* values = (const T*)s_ports[o.port[2]];
             const T* x = (const T*)s_ports[o.port[3]];
             T* y = (T*)s_ports[o.port[4]];
-            LOOP_EW(i) {
-              T acc = T(0);
-              const int64_t e = rowptr[i + 1];
-              for (int64_t q = rowptr[i]; q < e; ++q) acc = add_rn(acc, mul_rn(values[q], x[colidx[q]]));
-              y[i] = acc;
+            if (o.sell >= 0) {
+              const LSell& S = P.sell[o.sell];
+              const I* sc = (const I*)S.colidx;
+              const T* sv = (const T*)S.values;
+              LOOP_EW(i) {
+                const int64_t r = i - G.first;
+                y[i] = sell_row(sc, sv, x, S.base[r >> 5] + (r & 31), (int)(rowptr[i + 1] - rowptr[i]));
+              }
+            } else {
+              LOOP_EW(i) y[i] = csr_row(colidx, values, x, (int64_t)rowptr[i], (int64_t)rowptr[i + 1]);
             }
             break;
           }
@@ -239,6 +335,35 @@ __global__ void __launch_bounds__(kLoopThreads, 1) k_loop_persistent(const __gri
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
         atomicAdd(P.prof + kLoopMaxGroups + 2 * blockIdx.x, t1 - t_grp);
       }
+      if (P.dot_mode == 1) {
+        // Arrival count instead of a grid barrier, and no publish hop: every CTA adds itself
+        // to the dot's monotonic counter (release), waits until all gridDim.x arrivals of
+        // this iteration are in (acquire), then runs k_dot's final tree itself over the 1024
+        // partials.  Same inputs, same order: every CTA gets the same bits.
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          unsigned long long* ctr = P.arrive + o.dot;
+          const unsigned long long target = (unsigned long long)gridDim.x * (unsigned long long)(it + 1);
+          asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(ctr) : "memory");
+          uint32_t polls = 0;
+          while (ld_acquire_u64(ctr) < target) {
+            if (++polls == (1u << 31)) __trap();                // a lost arrival: fail, never hang
+            __nanosleep(P.backoff_ns);
+          }
+        }
+        __syncthreads();
+        {                                             // 32 warps: one 32-partial group each
+          static_assert(kLoopThreads / 32 == kDotBlocks / 32, "one warp per partial group");
+          double w = __ldcg(part + warp * 32 + lane);
+          w = warp_sum(w);
+          if (lane == 0) gred[warp] = w;
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {
+          const double w = warp_sum(gred[lane]);
+          if (lane == 0) gred[0] = w;
+        }
+      } else {
       // Ticket instead of a grid barrier: the last CTA to arrive runs k_dot's final tree
       // once and publishes the value into an 8-byte slot holding a sentinel NaN (all ones:
       // arithmetic only produces the canonical NaN); the others poll that slot with acquire
@@ -278,6 +403,7 @@ __global__ void __launch_bounds__(kLoopThreads, 1) k_loop_persistent(const __gri
           __nanosleep(P.backoff_ns);
         }
         gred[0] = __longlong_as_double((long long)v);
+      }
       }
       __syncthreads();
       if (P.prof && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2));
@@ -473,6 +599,55 @@ Plan plan_groups(const aol_loop_op* ops, int n) {
   return pl;
 }
 
+// SELL-32 copy of one spmv matrix (k_sell_width -> k_sell_scan -> k_sell_fill) into the
+// device's slot buffers; one synchronous read of the total size.
+struct SellBufs {
+  void* meta = nullptr;
+  size_t meta_cap = 0;
+  void* data = nullptr;
+  size_t data_cap = 0;
+};
+
+static int grow(void*& p, size_t& cap, size_t need) {
+  if (need <= cap) return AOL_OK;
+  if (p) AOL_CUDA_CHECK(cudaFree(p));
+  p = nullptr;
+  cap = 0;
+  AOL_CUDA_CHECK(cudaMalloc(&p, need));
+  cap = need;
+  return AOL_OK;
+}
+
+template <typename T, typename I>
+static int build_sell(const aol_loop_op& o, void* const* ports, SellBufs& b, LSell& out, cudaStream_t s) {
+  const I* rowptr = static_cast<const I*>(ports[o.port[0]]);
+  const int64_t ns = (o.count + 31) / 32;
+  int rc = grow(b.meta, b.meta_cap, (size_t)(2 * ns + 1) * sizeof(int64_t));
+  if (rc) return rc;
+  int64_t* width = static_cast<int64_t*>(b.meta);
+  int64_t* base = width + ns;
+  k_sell_width<I><<<(unsigned)std::min<int64_t>((ns + 7) / 8, 4096), 256, 0, s>>>(rowptr, o.first, o.count, width);
+  AOL_LAUNCH_CHECK("k_sell_width");
+  k_sell_scan<<<1, 1024, 0, s>>>(width, ns, base);
+  AOL_LAUNCH_CHECK("k_sell_scan");
+  int64_t total = 0;
+  AOL_CUDA_CHECK(cudaMemcpyAsync(&total, base + ns, sizeof(total), cudaMemcpyDeviceToHost, s));
+  AOL_CUDA_CHECK(cudaStreamSynchronize(s));
+  const size_t sc_bytes = ((size_t)total * sizeof(I) + 255) / 256 * 256;
+  rc = grow(b.data, b.data_cap, sc_bytes + (size_t)total * sizeof(T) + 256);
+  if (rc) return rc;
+  I* sc = static_cast<I*>(b.data);
+  T* sv = reinterpret_cast<T*>(static_cast<char*>(b.data) + sc_bytes);
+  k_sell_fill<T, I><<<(unsigned)std::min<int64_t>((o.count + 255) / 256, 4096), 256, 0, s>>>(
+      rowptr, static_cast<const I*>(ports[o.port[1]]), static_cast<const T*>(ports[o.port[2]]), o.first, o.count,
+      base, sc, sv);
+  AOL_LAUNCH_CHECK("k_sell_fill");
+  out.base = base;
+  out.colidx = sc;
+  out.values = sv;
+  return AOL_OK;
+}
+
 }  // namespace
 
 }  // namespace aol
@@ -531,9 +706,14 @@ extern "C" int aol_loop_persistent(const aol_loop_op* ops, int n_ops, void* cons
   if ( (int)pl.groups.size() > kLoopMaxGroups)
     return fail(AOL_EUNSUPPORTED, "loop body does not fit the persistent interpreter");
   int dot = 0;
+  unsigned written = 0;
+  for (int k = 0; k < n_ops; ++k)
+    for (const Access& a : vector_accesses(ops[k]))
+      if (a.mode == W) written |= 1u << a.port;
   for (int k = 0; k < n_ops; ++k) {
     P.ops[k] = pl.ops[k];
     P.ops[k].dot = ops[k].op == AOL_OP_DOT_PARTIAL ? dot++ : 0;
+    P.ops[k].sell = -1;
   }
   for (size_t g = 0; g < pl.groups.size(); ++g) P.groups[g] = pl.groups[g];
   P.n_groups = (int)pl.groups.size();
@@ -570,7 +750,7 @@ extern "C" int aol_loop_persistent(const aol_loop_op* ops, int n_ops, void* cons
   const size_t prof_bytes = (kLoopMaxGroups + 2 * 1024) * sizeof(unsigned long long);
   const char* prof_env = getenv("AOL_LOOP_PROFILE");
   const bool profile = prof_env && prof_env[0] == '1';
-  const size_t sync_bytes = 128 * (4 + 4 + 8);
+  const size_t sync_bytes = 128 * (4 + 4 + 8) + 64 * 8;
   if (!scratch_of[dev]) AOL_CUDA_CHECK(cudaMalloc(&scratch_of[dev], part_bytes + 64 + sync_bytes + prof_bytes));
   char* scratch = scratch_of[dev];
   P.part = reinterpret_cast<double*>(scratch);
@@ -579,8 +759,34 @@ extern "C" int aol_loop_persistent(const aol_loop_op* ops, int n_ops, void* cons
   P.result = reinterpret_cast<unsigned long long*>(P.ticket + 256);
   AOL_CUDA_CHECK(cudaMemsetAsync(P.ticket, 0, 256 * sizeof(unsigned), s));
   AOL_CUDA_CHECK(cudaMemsetAsync(P.result, 0xff, 128 * sizeof(unsigned long long), s));
+  P.arrive = P.result + 128;
+  AOL_CUDA_CHECK(cudaMemsetAsync(P.arrive, 0, 64 * sizeof(unsigned long long), s));
+  {
+    const char* dm = getenv("AOL_LOOP_DOT");
+    P.dot_mode = (dm && dm[0] == '0') ? 0 : 1;
+  }
   AOL_CUDA_CHECK(cudaMemsetAsync(P.part, 0, part_bytes, s));
   P.prof = profile ? reinterpret_cast<unsigned long long*>(scratch + part_bytes + 64 + sync_bytes) : nullptr;
+  // SELL-32 copies of the spmv matrices the body never writes (AOL_LOOP_SELL=0: CSR rows)
+  {
+    static SellBufs sell_bufs[64][kLoopMaxSell];
+    const char* se = getenv("AOL_LOOP_SELL");
+    int n_sell = 0;
+    for (int k = 0; k < n_ops && !(se && se[0] == '0'); ++k) {
+      const aol_loop_op& o = ops[k];
+      if (o.op != AOL_OP_SPMV_CSR || o.count <= 0 || n_sell >= kLoopMaxSell) continue;
+      if ((written >> o.port[0] & 1u) || (written >> o.port[1] & 1u) || (written >> o.port[2] & 1u)) continue;
+      int rc;
+      if (dtype == AOL_F64)
+        rc = index_dtype == AOL_I64 ? build_sell<double, int64_t>(o, ports, sell_bufs[dev][n_sell], P.sell[n_sell], s)
+                                    : build_sell<double, int32_t>(o, ports, sell_bufs[dev][n_sell], P.sell[n_sell], s);
+      else
+        rc = index_dtype == AOL_I64 ? build_sell<float, int64_t>(o, ports, sell_bufs[dev][n_sell], P.sell[n_sell], s)
+                                    : build_sell<float, int32_t>(o, ports, sell_bufs[dev][n_sell], P.sell[n_sell], s);
+      if (rc) return rc;
+      P.ops[k].sell = n_sell++;
+    }
+  }
   if (profile) AOL_CUDA_CHECK(cudaMemsetAsync(P.prof, 0, prof_bytes, s));
   void* args[] = {&P};
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
