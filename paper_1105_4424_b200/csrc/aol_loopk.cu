@@ -44,6 +44,7 @@ constexpr int kLoopThreads = 256 * kLoopSub;
 struct LOp {
   int op, n_scalars, part, n_parts, dot;
   int sell;                                   // spmv: index into LProg::sell, or -1 (CSR rows)
+  int reuse, reuse_it;                        // dot: take dot `reuse`'s value from iteration reuse_it on
   int port[6];
 };
 
@@ -182,6 +183,7 @@ __global__ void __launch_bounds__(kLoopThreads, 1) k_loop_persistent(const __gri
   __shared__ double sc[kLoopMaxPorts + kLoopMaxParts];
   __shared__ double red[kLoopSub][8];
   __shared__ double gred[32];
+  __shared__ double dval[64];                 // each dot's final-tree value, for reuse
   __shared__ int s_last;
   const int sub = threadIdx.x >> 8, t = threadIdx.x & 255, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int slot = blockIdx.x * kLoopSub + sub, nslots = gridDim.x * kLoopSub;
@@ -303,6 +305,7 @@ __global__ void __launch_bounds__(kLoopThreads, 1) k_loop_persistent(const __gri
             break;
           }
           case AOL_OP_DOT_PARTIAL: {                  // k_dot's per-block partials, exactly
+            if (o.reuse >= 0 && it >= o.reuse_it) break;
             const T* a = (const T*)s_ports[o.port[0]];
             const T* b = (const T*)s_ports[o.port[1]];
             double* part = P.part + ((size_t)parity * 64 + o.dot) * kDotBlocks;
@@ -335,7 +338,10 @@ __global__ void __launch_bounds__(kLoopThreads, 1) k_loop_persistent(const __gri
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
         atomicAdd(P.prof + kLoopMaxGroups + 2 * blockIdx.x, t1 - t_grp);
       }
-      if (P.dot_mode == 1) {
+      const bool reused = o.reuse >= 0 && it >= o.reuse_it;
+      if (reused) {
+        if (threadIdx.x == 0) gred[0] = dval[o.reuse];
+      } else if (P.dot_mode == 1) {
         // Arrival count instead of a grid barrier, and no publish hop: every CTA adds itself
         // to the dot's monotonic counter (release), waits until all gridDim.x arrivals of
         // this iteration are in (acquire), then runs k_dot's final tree itself over the 1024
@@ -406,6 +412,7 @@ __global__ void __launch_bounds__(kLoopThreads, 1) k_loop_persistent(const __gri
       }
       }
       __syncthreads();
+      if (threadIdx.x == 0) dval[o.dot] = gred[0];
       if (P.prof && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2));
       if (threadIdx.x < 32) {
         const double w = gred[0];
@@ -520,7 +527,45 @@ struct Plan {
 
 // Split the body into groups and mark the groups that must start with a grid barrier.
 // Barrier flags are decided over two passes of the body, because the loop wraps.
-Plan plan_groups(const aol_loop_op* ops, int n) {
+// Dot reuse (common-subexpression elimination that keeps the bits): dot j may take the
+// final-tree value of the nearest earlier dot k (cyclically; from iteration 1 on when k
+// comes later in the body) over the same ports and launch range when no op between them
+// writes either vector.  Same inputs in the same fixed order give the same value, so the
+// second reduction, its arrival wait and its final tree are skipped.  CG's dot_rr(r, r)
+// reuses the previous iteration's dot_rrn(r, r) (cg.gmodel).
+struct Reuse {
+  int from = -1, from_it = 0;
+};
+
+static bool writes_port(const aol_loop_op& o, int port) {
+  for (const Access& a : vector_accesses(o))
+    if (a.mode == W && a.port == port) return true;
+  return false;
+}
+
+std::vector<Reuse> plan_dot_reuse(const aol_loop_op* ops, int n) {
+  std::vector<Reuse> r(n);
+  const char* env = getenv("AOL_LOOP_DOT_REUSE");
+  if (env && env[0] == '0') return r;
+  for (int j = 0; j < n; ++j) {
+    const aol_loop_op& oj = ops[j];
+    if (oj.op != AOL_OP_DOT_PARTIAL) continue;
+    for (int step = 1; step < n; ++step) {
+      const int k = (j - step + n) % n;
+      const aol_loop_op& ok = ops[k];
+      if (ok.op == AOL_OP_DOT_PARTIAL && ok.port[0] == oj.port[0] && ok.port[1] == oj.port[1] &&
+          ok.first == oj.first && ok.count == oj.count && ok.part == oj.part && ok.n_parts == oj.n_parts) {
+        r[j].from = k;
+        r[j].from_it = k > j ? 1 : 0;
+        break;
+      }
+      if (writes_port(ok, oj.port[0]) || writes_port(ok, oj.port[1])) break;
+    }
+  }
+  return r;
+}
+
+Plan plan_groups(const aol_loop_op* ops, int n, const std::vector<Reuse>& reuse) {
   Plan pl;
   // 1. grouping (independent of the wrap): a new group at every scalar op, key change,
   //    in-group race, and after every dot
@@ -593,7 +638,8 @@ Plan plan_groups(const aol_loop_op* ops, int n) {
         seen.clear();
       }
       for (const Access& a : acc) seen.push_back({a.port, a.mode, g.first});
-      if (g.dot) seen.clear();                        // the dot's own barrier
+      // the dot's own barrier (a reused dot synchronises nothing)
+      if (g.dot && reuse[g.op0 + g.n_ops - 1].from < 0) seen.clear();
     }
   }
   return pl;
@@ -702,7 +748,8 @@ extern "C" int aol_loop_persistent(const aol_loop_op* ops, int n_ops, void* cons
   if (!((scalar >> relres_port) & 1u)) return fail(AOL_EUNSUPPORTED, "relres is not a scalar of the body");
   for (int p = 0; p < n_ports; ++p)
     if (!ports[p]) return fail(AOL_EINVAL, "null port");
-  Plan pl = plan_groups(ops, n_ops);
+  const std::vector<Reuse> reuse = plan_dot_reuse(ops, n_ops);
+  Plan pl = plan_groups(ops, n_ops, reuse);
   if ( (int)pl.groups.size() > kLoopMaxGroups)
     return fail(AOL_EUNSUPPORTED, "loop body does not fit the persistent interpreter");
   int dot = 0;
@@ -710,10 +757,15 @@ extern "C" int aol_loop_persistent(const aol_loop_op* ops, int n_ops, void* cons
   for (int k = 0; k < n_ops; ++k)
     for (const Access& a : vector_accesses(ops[k]))
       if (a.mode == W) written |= 1u << a.port;
+  std::vector<int> dot_id(n_ops, 0);
   for (int k = 0; k < n_ops; ++k) {
     P.ops[k] = pl.ops[k];
-    P.ops[k].dot = ops[k].op == AOL_OP_DOT_PARTIAL ? dot++ : 0;
+    P.ops[k].dot = dot_id[k] = ops[k].op == AOL_OP_DOT_PARTIAL ? dot++ : 0;
     P.ops[k].sell = -1;
+  }
+  for (int k = 0; k < n_ops; ++k) {
+    P.ops[k].reuse = reuse[k].from >= 0 ? dot_id[reuse[k].from] : -1;
+    P.ops[k].reuse_it = reuse[k].from_it;
   }
   for (size_t g = 0; g < pl.groups.size(); ++g) P.groups[g] = pl.groups[g];
   P.n_groups = (int)pl.groups.size();
