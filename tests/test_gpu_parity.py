@@ -946,3 +946,35 @@ def test_dots_on_concurrent_streams():
             _capi.launch(task, 0, n, [a.data_ptr(), b.data_ptr(), o.data_ptr()], (), st.cuda_stream)
         torch.cuda.synchronize()
         assert [o.item() for o in outs] == alone
+
+
+def test_loop_dot_reuse_keeps_bits_and_respects_writes(monkeypatch):
+    """Dot reuse in the persistent loop: a dot re-reading vectors that no op wrote since an
+    identical dot takes that dot's value (bit-identical to recomputing it); a dot whose
+    vector was written in between is recomputed."""
+    from paper_1105_4424_b200 import _capi
+    n = 5000
+    rng = np.random.default_rng(11)
+    a0 = rng.standard_normal(n)
+
+    def run(reuse):
+        monkeypatch.setenv("AOL_LOOP_DOT_REUSE", reuse)
+        a = torch.from_numpy(a0.copy()).cuda()
+        s = torch.zeros(8, dtype=torch.float64, device="cuda")
+        s[3] = 0.5
+        p = [a.data_ptr()] + [s[i:i + 1].data_ptr() for i in range(1, 8)]
+        ops = [_capi.loop_op("dot_partial", [0, 0, 2], 0, n),     # s1 = a.a   (reuses s2 from iteration 1 on)
+               _capi.loop_op("scale", [0, 3], 0, n, n_scalars=1),  # a *= 0.5
+               _capi.loop_op("dot_partial", [0, 0, 4], 0, n),     # s2 = a.a   (a written: recomputed)
+               _capi.loop_op("div", [4, 2, 5])]                   # q = s2 / s1 = 0.25
+        res = _capi.loop_persistent(ops, p, "float64", "int32", 5, 0.1, 9)
+        torch.cuda.synchronize()
+        return res, a.cpu().numpy(), s.cpu().numpy()
+
+    (it1, q1, c1), a1, s1 = run("1")
+    (it0, q0, c0), a0_, s0 = run("0")
+    assert (it1, c1) == (it0, c0) == (9, False)
+    assert q1 == q0 == 0.25
+    assert np.array_equal(a1.view(np.uint64), a0_.view(np.uint64))
+    assert np.array_equal(s1.view(np.uint64), s0.view(np.uint64))
+    assert s1[4] == s1[2] * 0.25 and s1[2] != s1[4]
