@@ -45,6 +45,7 @@ struct LOp {
   int op, n_scalars, part, n_parts, dot;
   int sell;                                   // spmv: index into LProg::sell, or -1 (CSR rows)
   int reuse, reuse_it;                        // dot: take dot `reuse`'s value from iteration reuse_it on
+  int level;                                  // scalar op: dependency level inside its group
   int port[6];
 };
 
@@ -65,6 +66,7 @@ struct LSell {
 // scalar ops.
 struct LGroup {
   int barrier, op0, n_ops, scalar, dot;
+  int levels;                                 // scalar group: dependency levels (ops of one level run in parallel)
   int64_t first, count;
 };
 
@@ -77,8 +79,9 @@ struct LProg {
   int64_t* state;                             // iterations, relres (bits), converged
   unsigned* ticket;                           // [2][64] arrivals per dot
   unsigned long long* result;                 // [2][64] published dot values (kSlotEmpty: not yet)
-  unsigned long long* arrive;                 // [64] monotonic arrivals per dot (dot_mode 1)
+  unsigned long long* arrive;                 // [64] monotonic arrivals per dot (dot_mode 1), [64] barriers
   int dot_mode;                               // 0: last CTA reduces and publishes; 1: every CTA reduces
+  int barrier_mode;                           // 0: cooperative-groups grid.sync; 1: arrival counter
   unsigned long long* prof;                   // AOL_LOOP_PROFILE: ns per group, CTA 0's view
   unsigned backoff_ns;                        // sleep between polls of a dot's flag
   LSell sell[kLoopMaxSell];
@@ -207,6 +210,7 @@ __global__ void __launch_bounds__(kLoopThreads, 1) k_loop_persistent(const __gri
   __syncthreads();
 
   int64_t it = 0;
+  unsigned long long n_barriers = 0;
   int parity = 0;
   double relres = 0.0;
   int converged = 0;
@@ -223,24 +227,49 @@ __global__ void __launch_bounds__(kLoopThreads, 1) k_loop_persistent(const __gri
       }
       unsigned long long t_grp = 0;
       if (P.prof && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_grp));
-      if (G.barrier) grid.sync();
-      if (G.scalar) {                                   // host scalar ops, redundantly per CTA
-        if (threadIdx.x == 0) for (int k = G.op0; k < G.op0 + G.n_ops; ++k) {
-          const LOp& o = s_ops[k];
-          double z;
-          int out;
-          if (o.op == AOL_OP_SCALAR_NEG) {
-            z = (double)(-(T)sc[o.port[0]]);
-            out = o.port[1];
-          } else if (o.op == AOL_OP_SCALAR_DIV) {
-            z = (double)(T)(sc[o.port[0]] / sc[o.port[1]]);
-            out = o.port[2];
-          } else {
-            z = (double)(T)(sqrt(sc[o.port[0]]) / sqrt(sc[o.port[1]]));
-            out = o.port[2];
+      if (G.barrier) {
+        if (P.barrier_mode == 1) {
+          // the dots' arrival counter as a grid barrier: release-add, acquire-poll the total
+          __syncthreads();
+          ++n_barriers;
+          if (threadIdx.x == 0) {
+            unsigned long long* ctr = P.arrive + 64;
+            const unsigned long long target = (unsigned long long)gridDim.x * n_barriers;
+            asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(ctr) : "memory");
+            uint32_t polls = 0;
+            while (ld_acquire_u64(ctr) < target) {
+              if (++polls == (1u << 31)) __trap();
+              __nanosleep(P.backoff_ns);
+            }
           }
-          sc[out] = z;
-          if (writer) ((T*)s_ports[out])[0] = (T)z;
+          __syncthreads();
+        } else {
+          grid.sync();
+        }
+      }
+      if (G.scalar) {                                   // host scalar ops, redundantly per CTA
+        // lane k of warp 0 runs op op0+k; ops of one dependency level run side by side
+        if (threadIdx.x < G.n_ops) {
+          const LOp& o = s_ops[G.op0 + threadIdx.x];
+          for (int lv = 0; lv < G.levels; ++lv) {
+            if (o.level == lv) {
+              double z;
+              int out;
+              if (o.op == AOL_OP_SCALAR_NEG) {
+                z = (double)(-(T)sc[o.port[0]]);
+                out = o.port[1];
+              } else if (o.op == AOL_OP_SCALAR_DIV) {
+                z = (double)(T)(sc[o.port[0]] / sc[o.port[1]]);
+                out = o.port[2];
+              } else {
+                z = (double)(T)(sqrt(sc[o.port[0]]) / sqrt(sc[o.port[1]]));
+                out = o.port[2];
+              }
+              sc[out] = z;
+              if (blockIdx.x == 0) ((T*)s_ports[out])[0] = (T)z;
+            }
+            __syncwarp(G.n_ops >= 32 ? 0xffffffffu : (1u << G.n_ops) - 1u);
+          }
         }
         __syncthreads();
         continue;
@@ -766,6 +795,33 @@ extern "C" int aol_loop_persistent(const aol_loop_op* ops, int n_ops, void* cons
   for (int k = 0; k < n_ops; ++k) {
     P.ops[k].reuse = reuse[k].from >= 0 ? dot_id[reuse[k].from] : -1;
     P.ops[k].reuse_it = reuse[k].from_it;
+    P.ops[k].level = 0;
+  }
+  // scalar groups: an op's level is 1 + the deepest earlier op of its group it reads from
+  for (size_t g = 0; g < pl.groups.size(); ++g) {
+    LGroup& G = pl.groups[g];
+    G.levels = 1;
+    if (!G.scalar) continue;
+    if (G.n_ops > 32) return fail(AOL_EUNSUPPORTED, "scalar run longer than a warp");
+    for (int k = G.op0; k < G.op0 + G.n_ops; ++k) {
+      const aol_loop_op& o = ops[k];
+      const int n_in = o.op == AOL_OP_SCALAR_NEG ? 1 : 2;
+      int lv = 0;
+      for (int j = G.op0; j < k; ++j) {
+        const aol_loop_op& p = ops[j];
+        const int out = p.op == AOL_OP_SCALAR_NEG ? p.port[1] : p.port[2];
+        for (int q = 0; q < n_in; ++q)
+          if (o.port[q] == out) lv = std::max(lv, P.ops[j].level + 1);
+        // an op overwriting what an earlier op of the group reads or writes goes after it
+        const int my_out = o.op == AOL_OP_SCALAR_NEG ? o.port[1] : o.port[2];
+        const int p_in = p.op == AOL_OP_SCALAR_NEG ? 1 : 2;
+        for (int q = 0; q < p_in; ++q)
+          if (p.port[q] == my_out) lv = std::max(lv, P.ops[j].level + 1);
+        if (out == my_out) lv = std::max(lv, P.ops[j].level + 1);
+      }
+      P.ops[k].level = lv;
+      G.levels = std::max(G.levels, lv + 1);
+    }
   }
   for (size_t g = 0; g < pl.groups.size(); ++g) P.groups[g] = pl.groups[g];
   P.n_groups = (int)pl.groups.size();
@@ -802,7 +858,7 @@ extern "C" int aol_loop_persistent(const aol_loop_op* ops, int n_ops, void* cons
   const size_t prof_bytes = (kLoopMaxGroups + 2 * 1024) * sizeof(unsigned long long);
   const char* prof_env = getenv("AOL_LOOP_PROFILE");
   const bool profile = prof_env && prof_env[0] == '1';
-  const size_t sync_bytes = 128 * (4 + 4 + 8) + 64 * 8;
+  const size_t sync_bytes = 128 * (4 + 4 + 8) + 72 * 8;
   if (!scratch_of[dev]) AOL_CUDA_CHECK(cudaMalloc(&scratch_of[dev], part_bytes + 64 + sync_bytes + prof_bytes));
   char* scratch = scratch_of[dev];
   P.part = reinterpret_cast<double*>(scratch);
@@ -812,10 +868,12 @@ extern "C" int aol_loop_persistent(const aol_loop_op* ops, int n_ops, void* cons
   AOL_CUDA_CHECK(cudaMemsetAsync(P.ticket, 0, 256 * sizeof(unsigned), s));
   AOL_CUDA_CHECK(cudaMemsetAsync(P.result, 0xff, 128 * sizeof(unsigned long long), s));
   P.arrive = P.result + 128;
-  AOL_CUDA_CHECK(cudaMemsetAsync(P.arrive, 0, 64 * sizeof(unsigned long long), s));
+  AOL_CUDA_CHECK(cudaMemsetAsync(P.arrive, 0, 65 * sizeof(unsigned long long), s));
   {
     const char* dm = getenv("AOL_LOOP_DOT");
     P.dot_mode = (dm && dm[0] == '0') ? 0 : 1;
+    const char* bm = getenv("AOL_LOOP_BARRIER");
+    P.barrier_mode = (bm && bm[0] == '0') ? 0 : 1;
   }
   AOL_CUDA_CHECK(cudaMemsetAsync(P.part, 0, part_bytes, s));
   P.prof = profile ? reinterpret_cast<unsigned long long*>(scratch + part_bytes + 64 + sync_bytes) : nullptr;

@@ -1,3 +1,6 @@
-python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
-python bench.py --workload cg > gpurun_out/bench_cg.json 2> gpurun_out/bench_cg.err; echo cg=$?
-python bench.py --workload cg27 > gpurun_out/bench_cg27.json 2> gpurun_out/bench_cg27.err; echo cg27=$?
+python -m pytest tests/test_gpu_parity.py -x -q -k "cg or spmv or identity or dot or loop or scalar" > gpurun_out/pytest_cg.log 2>&1; echo pytest=$?
+for wl in cg cg27; do for r in 0 1 0 1; do
+echo "wl=$wl barrier=$r" >> gpurun_out/ab.log
+AOL_LOOP_BARRIER=$r AOL_LOOP_TIME=1 DIAG_REPS=4 DIAG_WL=$wl python tools/diag_cg.py >> gpurun_out/ab.log 2>&1
+done; done
+AOL_LOOP_PROFILE=1 DIAG_REPS=2 python tools/diag_cg.py > gpurun_out/cgprof.log 2>&1
