@@ -978,3 +978,103 @@ def test_loop_dot_reuse_keeps_bits_and_respects_writes(monkeypatch):
     assert np.array_equal(a1.view(np.uint64), a0_.view(np.uint64))
     assert np.array_equal(s1.view(np.uint64), s0.view(np.uint64))
     assert s1[4] == s1[2] * 0.25 and s1[2] != s1[4]
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_random_tilers_float64_tile_ops_vs_oracle(seed):
+    """The float64 instantiations of every tile intrinsic (copy, filter, sum, generic matmul),
+    random toroidal tilers, bit-exact against the oracle."""
+    rng = np.random.default_rng(2000 + seed)
+    for _ in range(4):
+        tx = _rand_tiler(rng)
+        rep, pat = tx["rep"], tx["pattern"]
+        R, P = int(np.prod(rep)), int(np.prod(pat))
+        x = rng.standard_normal(int(np.prod(tx["array"])))
+        d = int(rng.integers(1, 5))
+        td = _dense_out(rep, pat)
+        got = _run_tile("tile_copy", {"src": tx, "dst": td},
+                        {"src": _spec(tx, "in", "float64"), "dst": _spec(td, "out", "float64")},
+                        {"src": x}, d).outputs["p_dst"]
+        ref = orc.run_tile_task("tile_copy", {"src": tx, "dst": td}, {"src": x}, {"dst": (R * P, np.float64)}, R, d)
+        assert np.array_equal(got.view(np.uint64), ref["dst"].view(np.uint64))
+        py = int(rng.integers(1, 4))
+        ty = _dense_out(rep, (py,))
+        w = rng.standard_normal(py * P)
+        got = _run_tile("tile_filter", {"x": tx, "y": ty},
+                        {"x": _spec(tx, "in", "float64"), "w": f"in float64 [{w.size}]",
+                         "y": _spec(ty, "out", "float64")}, {"x": x, "w": w}, d).outputs["p_y"]
+        ref = orc.run_tile_task("tile_filter", {"x": tx, "y": ty}, {"x": x, "w": w}, {"y": (R * py, np.float64)}, R, d)
+        assert np.array_equal(got.view(np.uint64), ref["y"].view(np.uint64))
+        ts = _dense_out(rep, (1,))
+        got = _run_tile("tile_sum", {"x": tx, "s": ts}, {"x": _spec(tx, "in", "float64"),
+                                                         "s": _spec(ts, "out", "float64")}, {"x": x}, d).outputs["p_s"]
+        ref = orc.run_tile_task("tile_sum", {"x": tx, "s": ts}, {"x": x}, {"s": (R, np.float64)}, R, d)
+        assert np.array_equal(got.view(np.uint64), ref["s"].view(np.uint64))
+        tb = _rand_tiler(rng, rep=rep, pat=pat)
+        b = rng.standard_normal(int(np.prod(tb["array"])))
+        tc = _dense_out(rep, (1,))
+        got = _run_tile("matmul", {"a": tx, "b": tb, "c": tc},
+                        {"a": _spec(tx, "in", "float64"), "b": _spec(tb, "in", "float64"),
+                         "c": _spec(tc, "out", "float64")}, {"a": x, "b": b}, d).outputs["p_c"]
+        ref = orc.run_tile_task("matmul", {"a": tx, "b": tb, "c": tc}, {"a": x, "b": b}, {"c": (R, np.float64)}, R, d)
+        assert np.array_equal(got.view(np.uint64), ref["c"].view(np.uint64))
+
+
+@pytest.mark.parametrize("index_dtype,dtype", [("int64", "float64"), ("int64", "float32"), ("int32", "float32")])
+def test_spmv_index_and_value_dtypes_vs_oracle(index_dtype, dtype):
+    """spmv_csr through the C ABI for every (index, value) dtype pair: left-to-right rows,
+    bit-exact against the oracle's restatement of refexec.py:111-121."""
+    from paper_1105_4424_b200 import _capi
+    rng = np.random.default_rng(5)
+    n = 3000
+    lens = rng.integers(0, 40, n)
+    rowptr = np.concatenate([[0], np.cumsum(lens)]).astype(index_dtype)
+    nnz = int(rowptr[-1])
+    colidx = rng.integers(0, n, nnz).astype(index_dtype)
+    values = rng.standard_normal(nnz).astype(dtype)
+    x = rng.standard_normal(n).astype(dtype)
+    want = np.zeros(n, dtype)
+    orc.spmv_rows(rowptr, colidx, values, x, want, 0, n)
+    t = [torch.from_numpy(a).cuda() for a in (rowptr, colidx, values, x)]
+    y = torch.zeros(n, dtype=t[2].dtype, device="cuda")
+    task = _capi.make_task("spmv_csr", dtype, index_dtype=index_dtype)
+    for off, cnt in orc.partition_equally(n, 3):
+        _capi.launch(task, off, cnt, [a.data_ptr() for a in t] + [y.data_ptr()], (), 0)
+    torch.cuda.synchronize()
+    got = y.cpu().numpy()
+    assert np.array_equal(got.view(f"u{got.itemsize}"), want.view(f"u{want.itemsize}"))
+
+
+@pytest.mark.parametrize("variant", ["int64_index", "float32"])
+def test_cg_dtype_variants_persistent_equals_eager(golden, variant):
+    """The CG model with int64 CSR indices (persistent kernel <double, int64>, SELL copy with
+    64-bit indices) or float32 vectors (<float, int32>): the persistent loop is bit-identical to
+    the eager interpreter; int64 indices change nothing against the int32 model."""
+    import json as _json
+    from paper_1105_4424_b200.executor import Executor
+    from paper_1105_4424_b200.model import model_from_dict
+    from paper_1105_4424_b200.partition import build_schedule
+    data, meta = golden
+    text = _json.dumps(meta["cg_k20"]["model"])
+    bind = {k: data[f"cg_k20/{k}"] for k in ("rowptr", "colidx", "values", "b")}
+    if variant == "int64_index":
+        text = text.replace('"int32"', '"int64"')
+        bind = {k: (v.astype(np.int64) if k in ("rowptr", "colidx") else v) for k, v in bind.items()}
+    else:
+        text = text.replace('"float64"', '"float32"')
+        bind = {k: (v.astype(np.float32) if k in ("values", "b") else v) for k, v in bind.items()}
+    model = model_from_dict(_json.loads(text))
+    sched = build_schedule(model, 1)
+    eager = Executor(model, sched, bind, 1)
+    eager.run()
+    dev = Executor(model, sched, bind, 1, graphs=True)
+    dev.run()
+    assert dev.persistent_loops == 1
+    assert dev.iterations == eager.iterations
+    xe, xd = eager.outputs()["x"], dev.outputs()["x"]
+    assert np.array_equal(xd.view(f"u{xd.itemsize}"), xe.view(f"u{xe.itemsize}"))
+    if variant == "int64_index":
+        base = Executor(model_from_dict(meta["cg_k20"]["model"]), sched,
+                        {k: data[f"cg_k20/{k}"] for k in ("rowptr", "colidx", "values", "b")}, 1, graphs=True)
+        base.run()
+        assert np.array_equal(base.outputs()["x"].view(np.uint64), xd.view(np.uint64))

@@ -1,6 +1,1 @@
-python -m pytest tests/test_gpu_parity.py -x -q -k "cg or spmv or identity or dot or loop or scalar" > gpurun_out/pytest_cg.log 2>&1; echo pytest=$?
-for wl in cg cg27; do for r in 0 1 0 1; do
-echo "wl=$wl barrier=$r" >> gpurun_out/ab.log
-AOL_LOOP_BARRIER=$r AOL_LOOP_TIME=1 DIAG_REPS=4 DIAG_WL=$wl python tools/diag_cg.py >> gpurun_out/ab.log 2>&1
-done; done
-AOL_LOOP_PROFILE=1 DIAG_REPS=2 python tools/diag_cg.py > gpurun_out/cgprof.log 2>&1
+python -m pytest tests/test_gpu_parity.py -x -q -k "float64_tile_ops or index_and_value or dtype_variants or dot_reuse" > gpurun_out/pytest_new.log 2>&1; echo pytest=$?
