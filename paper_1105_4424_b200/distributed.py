@@ -170,14 +170,33 @@ class Exchange:
         self.world = dist.get_world_size(group)
 
     def all_gather_v(self, local, counts: list[int]):
-        """``local`` is this rank's flat stream (counts[rank] elements); returns every rank's stream."""
+        """``local`` is this rank's flat stream (counts[rank] elements); returns every rank's stream.
+
+        One grouped batch of point-to-point sends/receives of the exact stream sizes
+        (``batch_isend_irecv``: ncclGroupStart/End on NCCL), so the unequal shard sizes
+        of partition_equally need no padding."""
         import torch
-        n = max(counts)
-        buf = torch.zeros(n, dtype=local.dtype, device=local.device)
-        buf[:local.numel()] = local
-        out = [torch.empty(n, dtype=local.dtype, device=local.device) for _ in range(self.world)]
-        self.dist.all_gather(out, buf, group=self.group)
-        return [o[:c] for o, c in zip(out, counts)]
+        dist = self.dist
+        out = []
+        ops = []
+        for r in range(self.world):
+            if r == self.rank:
+                out.append(local)
+                continue
+            buf = torch.empty(counts[r], dtype=local.dtype, device=local.device)
+            out.append(buf)
+            if counts[r]:
+                ops.append(dist.P2POp(dist.irecv, buf, self._peer(r), self.group))
+            if counts[self.rank]:
+                ops.append(dist.P2POp(dist.isend, local, self._peer(r), self.group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        return out
+
+    def _peer(self, r: int) -> int:
+        """Global rank of group rank ``r`` (P2P ops address global ranks)."""
+        return r if self.group is None else self.dist.get_global_rank(self.group, r)
 
     def all_gather_scalars(self, value: float) -> list[float]:
         import torch
