@@ -45,6 +45,7 @@ struct Params {
   int m_tiles, n_tiles, k_blocks, num_tiles;
   int c_vec;           // 16-byte stores allowed
   int group_m;         // tile raster: M-tiles per group sharing each B panel
+  int epi_smem;        // pair kernel: stage 32x32 chunks through shared memory for row-contiguous stores
 };
 
 // ------------------------------------------------------------ PTX helpers ----
@@ -276,7 +277,9 @@ constexpr int A_BYTES = HALF_M * BK * 4;           // 16 KB
 constexpr int B_BYTES = HALF_N * BK * 4;           // 16 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;     // 32 KB per CTA
 constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;        // shared::cluster address of the same offset in CTA 0
-constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 1024 + 256;
+constexpr int EPI_PITCH = 33;                     // padded 32x32 staging: conflict-free both ways
+constexpr int EPI_BYTES = 4 * 32 * EPI_PITCH * 4;  // one 32x32 fp32 chunk per epilogue warp
+constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 1024 + 256 + EPI_BYTES;
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -345,6 +348,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* epi = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
@@ -446,6 +450,36 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint32_t v[32];
         tmem_ld32(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + ch * 32, v);
         const int64_t c0 = (int64_t)nt * BN + ch * 32;
+        if (p.epi_smem) {
+          // lane = row in TMEM; transpose the 32x32 chunk through padded shared memory so each
+          // 16-byte store instruction covers 4 rows x 128 contiguous bytes instead of 32 rows x 16 B
+          float* st = epi + ew * 32 * EPI_PITCH;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) st[lane * EPI_PITCH + j] = __uint_as_float(v[j]);
+          __syncwarp();
+          const int64_t row0 = p.m_lo + (int64_t)mt * BM + rank * HALF_M + ew * 32;
+#pragma unroll
+          for (int rr = 0; rr < 32; rr += 4) {
+            const int r = rr + (lane >> 3), cc = 4 * (lane & 7);
+            const int64_t g = row0 + r;
+            const float* sp = st + r * EPI_PITCH + cc;
+            if (g > p.m_hi || g >= p.M) continue;
+            int64_t lo = 0, hi = p.N;
+            if (g == p.m_lo) lo = p.first - p.m_lo * p.N;
+            if (g == p.m_hi) hi = p.last - p.m_hi * p.N + 1;
+            float* dst = p.c + g * p.ldc + c0 + cc;
+            const int64_t col = c0 + cc;
+            if (p.c_vec && col >= lo && col + 4 <= hi) {
+              *reinterpret_cast<float4*>(dst) = make_float4(sp[0], sp[1], sp[2], sp[3]);
+            } else {
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (col + u >= lo && col + u < hi) dst[u] = sp[u];
+            }
+          }
+          __syncwarp();
+          continue;
+        }
         if (!row_ok) continue;
         if (p.c_vec && c0 >= col_lo && c0 + 32 <= col_hi) {
 #pragma unroll
@@ -688,6 +722,8 @@ static int gemm_core(const float* A, const float* B, float* C, const GemmShape& 
     Params pp = p;
     static const int gm_env = getenv("AOL_GEMM_GROUP_M") ? atoi(getenv("AOL_GEMM_GROUP_M")) : 0;
     pp.group_m = gm_env > 0 ? gm_env : 8;
+    static const char* epi_env = getenv("AOL_GEMM_EPI_SMEM");
+    pp.epi_smem = epi_env ? (epi_env[0] != '0') : 1;
     pp.m_tiles = (int)((p.m_hi - p.m_lo + pair::BM) / pair::BM);
     pp.n_tiles = (int)((g.N + pair::BN - 1) / pair::BN);
     pp.num_tiles = pp.m_tiles * pp.n_tiles;
