@@ -751,7 +751,7 @@ static int launch_tma_rows(const void* src, void* dst, int64_t rows, int64_t P, 
     const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)sms * cps);
     void (*k)(const CUtensorMap, const CUtensorMap, int64_t, int, uint32_t, uint32_t) =
         stages == 16 ? k_tile_copy_tma<16> : stages == 8 ? k_tile_copy_tma<8> : k_tile_copy_tma<4>;
-    AOL_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    // every ring above is <= 34 KB: within the default 48 KB dynamic shared memory limit
     k<<<grid, 32, smem, stream>>>(ms, md, ntiles, R, stage_bytes, stage_pitch);
     AOL_LAUNCH_CHECK("k_tile_copy_tma");
   }
