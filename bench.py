@@ -46,6 +46,28 @@ def log(*a):
 
 # ----------------------------------------------------------------- helpers --
 
+def bind_host_to_gpu_numa(torch, device_index: int) -> dict:
+    """Restrict this process to the CPUs of the GPU's NUMA node (sysfs local_cpulist), so the
+    pinned host buffers of the e2e path are first-touched on the node whose PCIe root the
+    GPU hangs off; a remote node adds a socket hop to every DMA.  Returns what was done."""
+    try:
+        pr = torch.cuda.get_device_properties(device_index)
+        bus = f"{pr.pci_domain_id:04x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+        base = Path("/sys/bus/pci/devices") / bus
+        cpus = (base / "local_cpulist").read_text().strip()
+        node = (base / "numa_node").read_text().strip()
+        sel = set()
+        for part in cpus.split(","):
+            lo, _, hi = part.partition("-")
+            sel.update(range(int(lo), int(hi or lo) + 1))
+        sel &= os.sched_getaffinity(0)
+        if sel:
+            os.sched_setaffinity(0, sel)
+        return {"pci": bus, "numa_node": int(node), "cpus": len(sel)}
+    except (OSError, ValueError, AttributeError) as e:
+        return {"unavailable": str(e)[:80]}
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -813,6 +835,8 @@ def run_gpu(args):
         return float(t.item())
 
     _capi.load()
+    all_cpus = os.sched_getaffinity(0)
+    numa = bind_host_to_gpu_numa(torch, local)
     wl = WORKLOADS[args.workload](torch, device, rank, world)
     stream = torch.cuda.current_stream(device)
 
@@ -855,7 +879,9 @@ def run_gpu(args):
                "h2d_bytes_per_step": wl.e2e_bytes[0] * world, "d2h_bytes_per_step": wl.e2e_bytes[1] * world,
                "ms_per_step": el * 1e3 / args.e2e_steps, "steps": args.e2e_steps,
                "path": "paper_1105_4424_b200.executor.execute_schedule(pipeline=%d): pinned host bindings and "
-                       "out= buffers; chunked H2D / launch / D2H overlap" % getattr(wl, "pipeline", 0)}
+                       "out= buffers; chunked H2D / launch / D2H overlap" % getattr(wl, "pipeline", 0),
+               "host_numa": numa}
+    os.sched_setaffinity(0, all_cpus)            # the CPU baseline gets every host core again
 
     # N > 1: the output shards gathered to rank 0 over NCCL, timed separately from the
     # concurrent per-rank phase (north_star: "NCCL output gather reported separately")
@@ -1047,7 +1073,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=400)
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="matmul", choices=sorted(WORKLOADS))
