@@ -210,6 +210,7 @@ KERNEL_STAGING = {
     "matmul.generic_exact": "patterns gathered from HBM to registers; pattern offset tables in smem",
     "tile_copy.stream16": "HBM -> registers (16 B vectors, streaming hints) -> HBM",
     "tile_copy.tma_stream": "HBM -> TMA 256 B-row boxes -> shared-memory ring (4 x 8 KB, 2 CTAs/SM) -> TMA store -> HBM",
+    "tile_copy.tma_transpose": "HBM -> TMA {32 reps, m} boxes (128B swizzle) -> smem transpose -> TMA store -> HBM",
     "tile_copy.tma_box": "HBM -> TMA pattern-row boxes -> shared-memory ring (32-64 KB in flight/SM) -> TMA store -> HBM",
     "tile_copy.vec": "HBM -> registers (V-element vectors) -> HBM",
     "tile_copy.vec_store": "HBM -> registers (strided scalars) -> HBM (V-element vector stores)",

@@ -1078,3 +1078,26 @@ def test_cg_dtype_variants_persistent_equals_eager(golden, variant):
                         {k: data[f"cg_k20/{k}"] for k in ("rowptr", "colidx", "values", "b")}, 1, graphs=True)
         base.run()
         assert np.array_equal(base.outputs()["x"].view(np.uint64), xd.view(np.uint64))
+
+
+@pytest.mark.parametrize("m,T,plan", [(4, 70000, "tile_copy.transpose"), (8, 40000, "tile_copy.tma_transpose"),
+                                      (16, 20004, "tile_copy.tma_transpose"), (8, 40001, "tile_copy.transpose"),
+                                      (32, 9000, "tile_copy.transpose")])
+@pytest.mark.parametrize("devices", [1, 3])
+def test_tile_copy_row_stride_tma_transpose_vs_oracle(m, T, plan, devices):
+    """Row-stride gathers (pattern down a column of an [m, T] array) into the dense stream:
+    the TMA transpose (swizzled {32, m} boxes, smem transpose, TMA store) for m = 8/16 with a
+    16-byte row pitch, the register transpose otherwise; ragged tiles and unaligned shard
+    starts (devices=3) peel through the register path."""
+    from paper_1105_4424_b200 import _capi
+    ts = dict(array=(m, T), rep=(T,), pattern=(m,), origin=(0, 0), paving=((0,), (1,)), fitting=((1,), (0,)))
+    td = dict(array=(T * m,), rep=(T,), pattern=(m,), origin=(0,), paving=((m,),), fitting=((1,),))
+    src = (np.arange(m * T) % (1 << 22)).astype(np.float32) + 1
+    res = _run_tile("tile_copy", {"src": ts, "dst": td},
+                    {"src": _spec(ts, "in", "float32"), "dst": _spec(td, "out", "float32")}, {"src": src}, devices)
+    ref = orc.run_tile_task("tile_copy", {"src": ts, "dst": td}, {"src": src}, {"dst": (T * m, np.float32)}, T, devices)
+    assert np.array_equal(res.outputs["p_dst"], ref["dst"])
+    task = _capi.make_task("tile_copy", "float32", [_tiler(ts).bind((m, T), (T,)), _tiler(td).bind((T * m,), (T,))])
+    x = torch.from_numpy(src).cuda()
+    y = torch.zeros(T * m, device="cuda")
+    assert _capi.plan_name(task, 0, T, [x.data_ptr(), y.data_ptr()]) == plan
