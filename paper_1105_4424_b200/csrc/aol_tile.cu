@@ -291,23 +291,28 @@ __global__ void __launch_bounds__(32) k_tile_copy_tma(const __grid_constant__ CU
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-// Row-stride gather through TMA (fp32, P in {8, 16}; 4 also correct): a tile of 128 repetitions x P pattern
-// elements arrives as four {32 reps, P} boxes with the 128B swizzle (16-byte chunk c of row i
-// lands at chunk c ^ (i & 7), so a warp reading 8 pattern rows hits 32 distinct banks), is
-// transposed by 128 threads into a dense [128][P] staging tile, and leaves as one TMA store
-// box.  Three input tiles in flight, two staging tiles; one thread issues every bulk copy.
+// Row-stride gather through TMA (fp32, P in {8, 16, 32, 64}): a tile of RT repetitions x P
+// pattern elements arrives as RT/32 {32 reps, P} boxes with the 128B swizzle (16-byte chunk c
+// of row i lands at chunk c ^ (i & 7)), is transposed by 128 threads into a staging tile, and
+// leaves through TMA stores.  P <= 16: dense [RT][P] staging, one store box, thread e takes
+// element e (column reads conflict-free for 8 rows).  P >= 32: staging as P/32 swizzled
+// [RT][32] boxes and 4-rep x 8-element warp blocks (reads conflict-free, writes 2-way).
+// Three input tiles in flight, two staging tiles; one thread issues every bulk copy.
 template <int P>
 __global__ void __launch_bounds__(128) k_tile_copy_tma_transpose(const __grid_constant__ CUtensorMap ms,
                                                                  const __grid_constant__ CUtensorMap md,
                                                                  int64_t ntiles) {
-  constexpr int RT = 128, BOX = 32 * P * 4, BOX_STRIDE = (BOX + 1023) & ~1023, IN_BYTES = 4 * BOX_STRIDE;
-  constexpr int OUT_BYTES = RT * P * 4, NIN = 3, NOUT = 2;
+  constexpr int RT = P >= 64 ? 64 : 128, NBR = RT / 32;
+  constexpr int BOX = 32 * P * 4, BOX_STRIDE = (BOX + 1023) & ~1023, IN_BYTES = NBR * BOX_STRIDE;
+  constexpr bool SWO = P >= 32;                            // swizzled [RT][32] output boxes
+  constexpr int NBO = SWO ? P / 32 : 1, OBOX = SWO ? RT * 128 : RT * P * 4;
+  constexpr int OUT_BYTES = NBO * OBOX, NIN = 3, NOUT = 2;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   unsigned char* in = base;
-  float* out = reinterpret_cast<float*>(base + NIN * IN_BYTES);
+  unsigned char* out = base + NIN * IN_BYTES;
   __shared__ __align__(8) uint64_t full[NIN];
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
     for (int i = 0; i < NIN; ++i) mbar_init(&full[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -317,14 +322,18 @@ __global__ void __launch_bounds__(128) k_tile_copy_tma_transpose(const __grid_co
   auto load = [&](int64_t k) {
     const int st = (int)(k % NIN);
     const int r0 = (int)((blockIdx.x + k * gridDim.x) * RT);
-    mbar_expect_tx(&full[st], 4 * BOX);
+    mbar_expect_tx(&full[st], NBR * BOX);
 #pragma unroll
-    for (int b = 0; b < 4; ++b)
+    for (int b = 0; b < NBR; ++b)
       asm volatile(
           "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
               smem_u32(in + st * IN_BYTES + b * BOX_STRIDE)),
           "l"(&ms), "r"(r0 + 32 * b), "r"(0), "r"(smem_u32(&full[st]))
           : "memory");
+  };
+  auto in_off = [](int r, int i) -> uint32_t {            // byte offset of element (rep r, pattern i)
+    const int rl = r & 31;
+    return (uint32_t)((r >> 5) * BOX_STRIDE + i * 128 + ((((rl >> 2) ^ (i & 7)) << 4) | ((rl & 3) << 2)));
   };
   if (tid == 0)
     for (int64_t k = 0; k < mine && k < NIN; ++k) load(k);
@@ -334,20 +343,30 @@ __global__ void __launch_bounds__(128) k_tile_copy_tma_transpose(const __grid_co
     if (tid == 0 && k >= NOUT) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(NOUT - 1) : "memory");
     __syncthreads();
     const unsigned char* src = in + st * IN_BYTES;
-    float* dst = out + ob * (OUT_BYTES / 4);
+    unsigned char* dst = out + ob * OUT_BYTES;
+    if constexpr (!SWO) {
 #pragma unroll
-    for (int e = tid; e < RT * P; e += 128) {
-      const int r = e / P, i = e % P, rl = r & 31;
-      const uint32_t off = (uint32_t)((r >> 5) * BOX_STRIDE + i * 128 + ((((rl >> 2) ^ (i & 7)) << 4) | ((rl & 3) << 2)));
-      dst[e] = *reinterpret_cast<const float*>(src + off);
+      for (int e = tid; e < RT * P; e += 128)
+        reinterpret_cast<float*>(dst)[e] = *reinterpret_cast<const float*>(src + in_off(e / P, e % P));
+    } else {
+      // warp block: 4 reps x 8 pattern elements (lane: rep lane >> 3, element lane & 7)
+#pragma unroll 4
+      for (int blk = warp; blk < (RT / 4) * (P / 8); blk += 4) {
+        const int r = (blk % (RT / 4)) * 4 + (lane >> 3), i = (blk / (RT / 4)) * 8 + (lane & 7);
+        const int il = i & 31;
+        const uint32_t o = (uint32_t)((i >> 5) * OBOX + r * 128 + ((((il >> 2) ^ (r & 7)) << 4) | ((il & 3) << 2)));
+        *reinterpret_cast<float*>(dst + o) = *reinterpret_cast<const float*>(src + in_off(r, i));
+      }
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
     if (tid == 0) {
       const int r0 = (int)((blockIdx.x + k * gridDim.x) * RT);
-      asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(&md), "r"(0),
-                   "r"(r0), "r"(smem_u32(dst))
-                   : "memory");
+#pragma unroll
+      for (int b = 0; b < NBO; ++b)
+        asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(&md),
+                     "r"(32 * b), "r"(r0), "r"(smem_u32(dst + b * OBOX))
+                     : "memory");
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       if (k + NIN < mine) load(k + NIN);
     }
@@ -736,8 +755,8 @@ static CopyPlan plan_tile_copy(const aol_tiler& ts, const aol_tiler& td, int64_t
   // row-stride gather into a dense stream: transpose through shared memory
   if (p.As == 1 && P > 1 && (p.Bs >= 32 || p.Bs <= -32) && p.Ad == P && p.Bd == 1) {
     p.kind = 4;
-    // TMA transpose for 32 / 64-byte pattern columns (m = 4 measured slower than registers: 4.8 vs 5.2 TB/s)
-    p.tma = esz == 4 && (P == 8 || P == 16) && p.Bs > 0 && p.Bs % 4 == 0 && p.cd % 4 == 0 &&
+    // TMA transpose from 32-byte pattern columns up (m = 4 measured slower than registers: 4.8 vs 5.2 TB/s)
+    p.tma = esz == 4 && (P == 8 || P == 16 || P == 32 || P == 64) && p.Bs > 0 && p.Bs % 4 == 0 && p.cd % 4 == 0 &&
             count >= 128 && count * P * (int64_t)esz >= kTmaMinBytes;
     return p;
   }
@@ -829,31 +848,34 @@ static int launch_tma_rows(const void* src, void* dst, int64_t rows, int64_t P, 
 // with k_tile_copy_tma_transpose.  AOL_EUNSUPPORTED (nothing launched) outside its domain.
 static int launch_tma_transpose(const float* src, float* dst, int64_t count, int64_t P, int64_t Bs,
                                 cudaStream_t stream) {
-  if (!(P == 4 || P == 8 || P == 16) || Bs <= 0 || (Bs * 4) % 16 || (uintptr_t)src % 16 || (uintptr_t)dst % 16 ||
-      count < 128 || count >= ((int64_t)1 << 31))
+  if (!(P == 8 || P == 16 || P == 32 || P == 64) || Bs <= 0 || (Bs * 4) % 16 || (uintptr_t)src % 16 ||
+      (uintptr_t)dst % 16 || count < 128 || count >= ((int64_t)1 << 31))
     return AOL_EUNSUPPORTED;
+  const int RT = P >= 64 ? 64 : 128;
+  const bool swo = P >= 32;
   auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(tensor_map_encoder());
   if (!encode) return AOL_EUNSUPPORTED;
   CUtensorMap ms, md;
   cuuint64_t sdims[2] = {(cuuint64_t)count, (cuuint64_t)P}, sstr[1] = {(cuuint64_t)(Bs * 4)};
   cuuint32_t sbox[2] = {32, (cuuint32_t)P}, es[2] = {1, 1};
   cuuint64_t ddims[2] = {(cuuint64_t)P, (cuuint64_t)count}, dstr[1] = {(cuuint64_t)(P * 4)};
-  cuuint32_t dbox[2] = {(cuuint32_t)P, 128};
+  cuuint32_t dbox[2] = {(cuuint32_t)(swo ? 32 : P), (cuuint32_t)RT};
   if (encode(&ms, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<float*>(src), sdims, sstr, sbox, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||
       encode(&md, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, dst, ddims, dstr, dbox, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
-          CUDA_SUCCESS)
+             swo ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return AOL_EUNSUPPORTED;
-  const int64_t ntiles = (count + 127) / 128;
+  const int64_t ntiles = (count + RT - 1) / RT;
   const int box_stride = ((int)(32 * P * 4) + 1023) & ~1023;
-  const int smem = 3 * 4 * box_stride + 2 * 128 * (int)P * 4 + 1024;
+  const int smem = 3 * (RT / 32) * box_stride + 2 * RT * (int)P * 4 + 1024;
   int sms = kNumSMs, dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)sms * 4);
   void (*k)(const CUtensorMap, const CUtensorMap, int64_t) =
-      P == 4 ? k_tile_copy_tma_transpose<4> : P == 8 ? k_tile_copy_tma_transpose<8> : k_tile_copy_tma_transpose<16>;
+      P == 8 ? k_tile_copy_tma_transpose<8> : P == 16 ? k_tile_copy_tma_transpose<16>
+      : P == 32 ? k_tile_copy_tma_transpose<32> : k_tile_copy_tma_transpose<64>;
   if (smem > 48 * 1024) AOL_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   k<<<grid, 128, smem, stream>>>(ms, md, ntiles);
   AOL_LAUNCH_CHECK("k_tile_copy_tma_transpose");

@@ -1082,11 +1082,12 @@ def test_cg_dtype_variants_persistent_equals_eager(golden, variant):
 
 @pytest.mark.parametrize("m,T,plan", [(4, 70000, "tile_copy.transpose"), (8, 40000, "tile_copy.tma_transpose"),
                                       (16, 20004, "tile_copy.tma_transpose"), (8, 40001, "tile_copy.transpose"),
-                                      (32, 9000, "tile_copy.transpose")])
+                                      (32, 9000, "tile_copy.tma_transpose"), (64, 5004, "tile_copy.tma_transpose"),
+                                      (64, 5001, "tile_copy.transpose")])
 @pytest.mark.parametrize("devices", [1, 3])
 def test_tile_copy_row_stride_tma_transpose_vs_oracle(m, T, plan, devices):
     """Row-stride gathers (pattern down a column of an [m, T] array) into the dense stream:
-    the TMA transpose (swizzled {32, m} boxes, smem transpose, TMA store) for m = 8/16 with a
+    the TMA transpose (swizzled {32, m} boxes, smem transpose, TMA store) for m = 8..64 with a
     16-byte row pitch, the register transpose otherwise; ragged tiles and unaligned shard
     starts (devices=3) peel through the register path."""
     from paper_1105_4424_b200 import _capi
