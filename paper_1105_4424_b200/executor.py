@@ -233,7 +233,15 @@ class Executor:
     def task(self, path: str) -> _Task:
         t = self._tasks.get(path)
         if t is None:
-            t = _Task(self.model, self.storage, path, self.tilers.get(path), self.precision)
+            tl = self.tilers.get(path)
+            if tl is None:
+                # a validated task depends only on the (immutable) model, the path and the
+                # precision: validate once per model, not once per execute_schedule call
+                from .model import model_memo
+                t = model_memo(self.model, f"task:{path}:{self.precision}",
+                               lambda m: _Task(m, self.storage, path, None, self.precision))
+            else:
+                t = _Task(self.model, self.storage, path, tl, self.precision)
             self._tasks[path] = t
         return t
 

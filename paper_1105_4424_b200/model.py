@@ -21,6 +21,7 @@ executor with its ``tilers=`` keyword instead.
 from __future__ import annotations
 
 import enum
+import weakref
 from dataclasses import dataclass, field
 from typing import Any, Iterator
 
@@ -239,7 +240,32 @@ def _node(path: str, port: str) -> str:
     return f"{path}.{port}" if path else port
 
 
+_MODEL_MEMO: dict[int, dict] = {}
+
+
+def model_memo(model, key: str, fn):
+    """``fn(model)`` computed once per model object.  Models are treated as immutable once
+    built (the executor never mutates them); an entry is dropped when its model is
+    garbage-collected.  Objects that take no weak reference are not cached."""
+    mid = id(model)
+    slot = _MODEL_MEMO.get(mid)
+    if slot is None:
+        try:
+            weakref.finalize(model, _MODEL_MEMO.pop, mid, None)
+        except TypeError:
+            return fn(model)
+        slot = _MODEL_MEMO[mid] = {}
+    if key not in slot:
+        slot[key] = fn(model)
+    return slot[key]
+
+
 def connected_port_groups(model) -> dict[str, frozenset[str]]:
+    """Cached :func:`port_groups` (read-only result)."""
+    return model_memo(model, "port_groups", port_groups)
+
+
+def port_groups(model) -> dict[str, frozenset[str]]:
     """Port nodes grouped by connector reachability: one group = one storage array.
 
     Restates metamodel.py:315-349 (union-find over connectors of every

@@ -174,8 +174,11 @@ class Placement:
 
 
 def plan_placement(model, maps: list[MemoryMap] | None = None) -> list[Placement]:
-    """Concrete B200 placement of every data allocation; raises CapacityExceeded on B200 limits."""
-    maps = build_memory_maps(model) if maps is None else maps
+    """Concrete B200 placement of every data allocation; raises CapacityExceeded on B200 limits.
+    Computed once per model object when ``maps`` is not given (model_memo)."""
+    if maps is None:
+        from .model import model_memo
+        return model_memo(model, "placement", lambda m: plan_placement(m, build_memory_maps(m)))
     out = []
     for mm in maps:
         role = memory_role_of(model, mm.owner_path)

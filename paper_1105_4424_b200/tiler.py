@@ -68,6 +68,9 @@ class Tiler:
                           tuple(int(d) for d in rep_shape))
 
 
+_INJECTIVE_OK: set = set()
+
+
 @dataclass(frozen=True)
 class BoundTiler:
     tiler: Tiler
@@ -175,7 +178,15 @@ class BoundTiler:
         return (e * st).sum(axis=0)
 
     def check_injective(self) -> None:
-        """Raise TilerError unless every (rho, iota) maps to a distinct element (output tilers)."""
+        """Raise TilerError unless every (rho, iota) maps to a distinct element (output tilers).
+        A tiler that passed once is remembered (bound tilers are immutable values)."""
+        if self in _INJECTIVE_OK:
+            return
+        self._check_injective()
+        if len(_INJECTIVE_OK) < 4096:
+            _INJECTIVE_OK.add(self)
+
+    def _check_injective(self) -> None:
         n = self.rep_total * self.pattern_total
         if n > self.array_total:
             raise TilerError(f"output tiler writes {n} elements into an array of {self.array_total}")
