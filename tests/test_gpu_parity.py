@@ -180,8 +180,12 @@ def test_tile_copy_plans_vs_oracle(case, devices, dtype):
     ("float64", None, 40000, 4, 8, 4, "tile_copy.tma_box"),        # 32 B fp64 rows
     ("float32", None, 300001, 4, 4, 4, "tile_copy.tma_stream"),    # dense: 256 B rows + 16 B vectors + tail
     ("float64", None, 150001, 2, 2, 2, "tile_copy.tma_stream"),
+    ("float32", None, 200001, 2, 1, 2, "tile_copy.window"),        # overlapping 8-16 B rows: one bulk window/tile
+    ("float32", None, 100001, 4, 2, 4, "tile_copy.window"),
+    ("float32", None, 100000, 4, 3, 4, "tile_copy.window"),        # odd source pitch (windows unaligned)
     ("float32", None, 40000, 8, 4, 8, "tile_copy.vec"),            # overlapping 32 B rows: register path
     ("float32", None, 20001, 32, 16, 32, "tile_copy.tma_box"),     # overlapping 128 B rows: TMA box (L2 re-reads)
+    ("float32", None, 20001, 12, 6, 12, "tile_copy.vec"),          # P not a power of two: register path
 ])
 @pytest.mark.parametrize("devices", [1, 3])
 def test_tile_copy_tma_plans_vs_oracle(case, devices):
@@ -202,7 +206,7 @@ def test_tile_copy_tma_plans_vs_oracle(case, devices):
     x = torch.from_numpy(src).cuda()
     y = torch.zeros(n_out, dtype=x.dtype, device="cuda")
     assert _capi.plan_name(task, 0, T, [x.data_ptr(), y.data_ptr()]) == plan
-    if plan == "tile_copy.tma_box":
+    if plan in ("tile_copy.tma_box", "tile_copy.window"):
         # misaligned bases fall back to the register path, same bits
         xb = torch.zeros(span + 1, dtype=x.dtype, device="cuda")
         xb[1:] = x

@@ -1,2 +1,2 @@
-python tools/prof_c1.py > gpurun_out/prof_c1.log 2>&1; echo a=$?
-python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
+python -m pytest tests/test_gpu_parity.py -x -q -k "tile_copy" > gpurun_out/pytest_win.log 2>&1; echo pytest=$?
+python bench.py --workload sweep --no-cpu > gpurun_out/bench_sweep.json 2> gpurun_out/bench_sweep.err; echo sweep=$?
