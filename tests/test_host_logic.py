@@ -70,6 +70,44 @@ def test_validate_and_plan_without_gpu():
         _capi.validate(_capi.make_task("tile_copy", "float32", [_bt(cp), _bt(mism)]))
 
 
+def _copy_plan(src, dst, dtype="float32"):
+    T = src["rep"][0]
+    return _capi.plan_name(_capi.make_task("tile_copy", dtype, [_bt(src), _bt(dst)]), 0, T)
+
+
+def _dense(T, m):
+    return dict(array=(T * m,), rep=(T,), pattern=(m,), origin=(0,), paving=((m,),), fitting=((1,),))
+
+
+def test_tile_copy_plan_dispatch_rules_without_gpu():
+    """Which kernel each tile_copy geometry selects (host-side planning, no device): TMA box
+    rings from 1 MB on, 16-byte pitches and >= 32 B rows; bulk windows for overlapping 8-16 B
+    rows; the TMA transpose for row-stride gathers with 32-256 B pattern columns."""
+    def row1d(T, m, p, f=1):
+        return dict(array=((T - 1) * p + (m - 1) * f + 1,), rep=(T,), pattern=(m,), origin=(0,), paving=((p,),),
+                    fitting=((f,),))
+    big = 1 << 20
+    assert _copy_plan(row1d(big // 8, 2, 2), _dense(big // 8, 2)) == "tile_copy.tma_stream"       # dense, 1 MB
+    assert _copy_plan(row1d(1000, 2, 2), _dense(1000, 2)) == "tile_copy.stream16"                 # dense, small
+    assert _copy_plan(row1d(40000, 8, 16), _dense(40000, 8)) == "tile_copy.tma_box"               # 32 B rows, gaps
+    assert _copy_plan(row1d(40000, 4, 8), _dense(40000, 4)) == "tile_copy.vec"                    # 16 B rows
+    assert _copy_plan(row1d(40000, 8, 18), _dense(40000, 8)) == "tile_copy.vec"                   # 72 B pitch
+    assert _copy_plan(row1d(20000, 32, 16), _dense(20000, 32)) == "tile_copy.tma_box"             # overlap, 128 B
+    assert _copy_plan(row1d(40000, 8, 4), _dense(40000, 8)) == "tile_copy.vec"                    # overlap, 32 B
+    assert _copy_plan(row1d(200000, 2, 1), _dense(200000, 2)) == "tile_copy.window"               # overlap, 8 B
+    assert _copy_plan(row1d(100000, 4, 3), _dense(100000, 4)) == "tile_copy.window"
+    assert _copy_plan(row1d(40000, 8, 16, f=2), _dense(40000, 8)) == "tile_copy.vec_store"        # strided fitting
+    assert _copy_plan(row1d(40000, 4, 8), _dense(40000, 4), "float64") == "tile_copy.tma_box"    # 32 B fp64 rows
+
+    def rowstride(m, T):
+        return dict(array=(m, T), rep=(T,), pattern=(m,), origin=(0, 0), paving=((0,), (1,)), fitting=((1,), (0,)))
+    assert _copy_plan(rowstride(8, 40000), _dense(40000, 8)) == "tile_copy.tma_transpose"
+    assert _copy_plan(rowstride(64, 5004), _dense(5004, 64)) == "tile_copy.tma_transpose"
+    assert _copy_plan(rowstride(8, 40001), _dense(40001, 8)) == "tile_copy.transpose"             # pitch % 16 B
+    assert _copy_plan(rowstride(4, 80000), _dense(80000, 4)) == "tile_copy.transpose"             # 16 B columns
+    assert _copy_plan(rowstride(8, 40000), _dense(40000, 8), "float64") == "tile_copy.transpose"
+
+
 # -- partitioning (partition.py:105-121) ---------------------------------------
 
 def test_partition_paper_scale():
