@@ -198,7 +198,12 @@ class Executor:
         self.precision = precision
         self.stream = stream
         steps = [st for st in schedule.steps]
-        self.pipeline = pipeline if (pipeline > 1 and len(steps) == 1 and hasattr(steps[0], "launches")) else 0
+        from .intrinsics import FILTER_OPS
+        single = len(steps) == 1 and hasattr(steps[0], "launches")
+        # a two-step filter chain the fusion pass runs as one kernel streams like one step
+        pair = (fuse and len(steps) == 2 and all(hasattr(s_, "launches") for s_ in steps)
+                and steps[0].op in FILTER_OPS and steps[1].op in FILTER_OPS)
+        self.pipeline = pipeline if (pipeline > 1 and (single or pair)) else 0
         with torch.cuda.device(self.device):
             self.storage = DeviceStorage(model, bindings, self.device, stream, defer=bool(self.pipeline))
         self._tasks: dict[str, _Task] = {}
@@ -292,6 +297,110 @@ class Executor:
         from .distributed import _port_tiler
         return _port_tiler(self, t, name)
 
+    def _upload_deferred(self) -> None:
+        """Copy every deferred host binding to its device array (streaming fell through)."""
+        st = self.storage
+        for g, h in st.host.items():
+            st.arrays[g].copy_(h, non_blocking=True)
+
+    def _dense_stream_rep(self, bt):
+        """For an output tiler that writes repetition rho's pattern at c0 + P*rho + i (a dense
+        stream in rho order), return (c0, P); else None."""
+        aff = bt.affine
+        if aff is None:
+            return None
+        c0, rc, pc = aff
+        P = bt.pattern_total
+        pat = bt.tiler.pattern
+        want_pc = tuple(int(np.prod(pat[k + 1:])) for k in range(len(pat)))
+        want_rc = tuple(int(np.prod(bt.rep[j + 1:])) * P for j in range(len(bt.rep)))
+        if tuple(int(p) if e > 1 else want_pc[k] for k, (p, e) in enumerate(zip(pc, pat))) != want_pc:
+            return None
+        if tuple(int(r) if e > 1 else want_rc[j] for j, (r, e) in enumerate(zip(rc, bt.rep))) != want_rc:
+            return None
+        return c0, P
+
+    def _run_streamed_pair(self, s1, s2, out: dict | None) -> dict | None:
+        """Stream a fusable producer -> consumer filter chain: consumer chunks in order; each
+        chunk's producer-input ranges (consumer input ranges on the intermediate, mapped to
+        producer repetitions through its dense output stream, then the producer's input
+        ranges) go up on one stream, the fused kernel runs on another, the chunk's output
+        comes down on a third.  Returns None (nothing run) when the pair is not streamable."""
+        from .distributed import add_range, input_hull, input_ranges, missing_ranges
+        torch = _torch()
+        if not self._fusion_candidate(s1, s2) or len(s2.launches) != 1:
+            return None
+        t1, t2 = self.task(s1.task_path), self.task(s2.task_path)
+        bx, bm_out, bm_in, by = (self._port_bound(t1, "x"), self._port_bound(t1, "y"),
+                                 self._port_bound(t2, "x"), self._port_bound(t2, "y"))
+        ds = self._dense_stream_rep(bm_out)
+        if ds is None:
+            return None
+        c0, P1 = ds
+        st = self.storage
+        xg = st.groups[t1.nodes["x"]]
+        if xg not in st.host:
+            return None
+        comp = torch.cuda.current_stream(self.device) if self.stream is None else self.stream
+        cin, cout = torch.cuda.Stream(self.device), torch.cuda.Stream(self.device)
+        # whole-array inputs (filter weights) first
+        with torch.cuda.stream(cin):
+            for t in (t1, t2):
+                g = st.groups[t.nodes["w"]]
+                if g in st.host:
+                    st.arrays[g].copy_(st.host[g], non_blocking=True)
+        comp.wait_stream(cin)
+        xdev, xhost = st.arrays[xg], st.host[xg]
+        a1 = [st.array(t1.nodes[n]).data_ptr() for n in t1.port_order]
+        a2 = [st.array(t2.nodes[n]).data_ptr() for n in t2.port_order]
+        root = self.model.application_components[self.model.application_root]
+        yname = next(p.name for p in root.ports if enum_value(p.direction) == "out")
+        ydev = st.array(yname)
+        if st.groups[t2.nodes["y"]] is not st.groups[yname]:
+            return None
+        if out is not None and yname in out:
+            h = out[yname]
+            yhost = torch.from_numpy(h) if isinstance(h, np.ndarray) else h.view(-1)
+        else:
+            yhost = torch.empty(ydev.numel(), dtype=ydev.dtype, pin_memory=True)
+        l = s2.launches[0]
+        uploaded: list = []
+        covered: list = []
+        for off, cnt in partition_equally_local(l.range.count, self.pipeline):
+            first = l.range.offset + off
+            with torch.cuda.stream(cin):
+                for lo, hi in input_ranges(bm_in, first, cnt):
+                    r_lo = max(0, (lo - c0) // P1)
+                    r_hi = min(bx.rep_total, -(-(hi - c0) // P1))
+                    if r_hi <= r_lo:
+                        continue
+                    for xlo, xhi in input_ranges(bx, r_lo, r_hi - r_lo):
+                        for a, b in missing_ranges(uploaded, xlo, xhi):
+                            xdev[a:b].copy_(xhost[a:b], non_blocking=True)
+                            uploaded = add_range(uploaded, a, b)
+                ev_in = torch.cuda.Event()
+                ev_in.record(cin)
+            comp.wait_event(ev_in)
+            if not _capi.launch_fused2(t1.ctask, t2.ctask, first, cnt, a1, a2, int(comp.cuda_stream)):
+                raise RuntimeError("fused pair became unsupported mid-stream")
+            self.fused_launches += 1
+            ev_done = torch.cuda.Event()
+            ev_done.record(comp)
+            cout.wait_event(ev_done)
+            with torch.cuda.stream(cout):
+                lo, hi = input_hull(by, first, cnt)
+                yhost[lo:hi].copy_(ydev[lo:hi], non_blocking=True)
+                covered.append((lo, hi))
+        with torch.cuda.stream(cout):            # never-written elements keep the zero init
+            pos = 0
+            for lo, hi in sorted(covered) + [(ydev.numel(), ydev.numel())]:
+                if lo > pos:
+                    yhost[pos:lo].copy_(ydev[pos:lo], non_blocking=True)
+                pos = max(pos, hi)
+        cout.synchronize()
+        comp.synchronize()
+        return {yname: (out[yname] if out is not None and yname in out else yhost.numpy())}
+
     def run_streamed(self, out: dict | None = None) -> dict:
         """Run a one-step schedule chunk by chunk straight from host memory.
 
@@ -304,7 +413,15 @@ class Executor:
         """
         from .distributed import add_range, input_hull, input_ranges, missing_ranges
         torch = _torch()
-        step = self.schedule.steps[0]
+        steps = list(self.schedule.steps)
+        if len(steps) == 2:
+            res = self._run_streamed_pair(steps[0], steps[1], out)
+            if res is not None:
+                return res
+            self._upload_deferred()               # not streamable: plain run on the uploaded inputs
+            self.run()
+            return self.outputs(out=out)
+        step = steps[0]
         t = self.task(step.task_path)
         comp = torch.cuda.current_stream(self.device) if self.stream is None else self.stream
         cin = torch.cuda.Stream(self.device)

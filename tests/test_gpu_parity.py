@@ -1106,3 +1106,40 @@ def test_tile_copy_row_stride_tma_transpose_vs_oracle(m, T, plan, devices):
     x = torch.from_numpy(src).cuda()
     y = torch.zeros(T * m, device="cuda")
     assert _capi.plan_name(task, 0, T, [x.data_ptr(), y.data_ptr()]) == plan
+
+
+@pytest.mark.parametrize("chunks", [2, 7])
+@pytest.mark.parametrize("devices", [1, 3])
+def test_streamed_fused_downscaler_equals_plain(chunks, devices):
+    """The downscaler chain streamed from host memory (pipeline=k): consumer chunks, producer
+    input ranges derived through the intermediate's dense stream, one fused launch per chunk
+    (devices=1); a multi-launch schedule falls back to upload-then-run (devices=3).  Both
+    return exactly the plain result."""
+    from paper_1105_4424_b200 import builders
+    from paper_1105_4424_b200.executor import Executor, execute_schedule
+    from paper_1105_4424_b200.partition import build_schedule
+    F, H, W = 3, 54, 128
+    th = orc.hfilter_tilers(F, H, W)
+    Wo = th["y"]["array"][2]
+    tv = orc.vfilter_tilers(F, H, Wo)
+    wh, wv = orc.hfilter_weights(), orc.vfilter_weights()
+    model = builders.chain_model(
+        [("h", "hfilter", {"x": _spec(th["x"], "in", "float32"), "w": f"in float32 [{wh.size}]",
+                           "y": _spec(th["y"], "out", "float32")}, {k: _tiler(v) for k, v in th.items()},
+          th["x"]["rep"]),
+         ("v", "vfilter", {"x": _spec(tv["x"], "in", "float32"), "w": f"in float32 [{wv.size}]",
+                           "y": _spec(tv["y"], "out", "float32")}, {k: _tiler(v) for k, v in tv.items()},
+          tv["x"]["rep"])],
+        {"x": _spec(th["x"], "in", "float32"), "wh": f"in float32 [{wh.size}]", "wv": f"in float32 [{wv.size}]"},
+        {"y": _spec(tv["y"], "out", "float32")},
+        [("x", "h.x"), ("wh", "h.w"), ("h.y", "v.x"), ("wv", "v.w"), ("v.y", "y")])
+    x = np.random.default_rng(chunks).random(F * H * W).astype(np.float32)
+    bind = {"x": x, "wh": wh, "wv": wv}
+    sched = build_schedule(model, devices)
+    plain = execute_schedule(model, sched, bind, devices).outputs["y"]
+    ex = Executor(model, sched, {k: torch.from_numpy(v).pin_memory() for k, v in bind.items()}, devices,
+                  pipeline=chunks)
+    with torch.cuda.device(ex.device):
+        got = ex.run_streamed()["y"]
+    assert np.array_equal(got.view(np.uint32), plain.view(np.uint32))
+    assert ex.fused_launches == (chunks if devices == 1 else devices)
