@@ -198,6 +198,19 @@ __global__ void __launch_bounds__(256) k_tile_copy_affine(const T* __restrict__ 
   }
 }
 
+// Single-element patterns every other element (P == 1, As == 2) into a dense stream, fp32:
+// a thread takes 4 consecutive repetitions, reads the 8-element source span as two 16-byte
+// vectors (even elements kept) and writes one 16-byte vector -- half the load instructions
+// of the scalar gather; the DRAM traffic (whole sectors) is the same.
+__global__ void __launch_bounds__(256) k_gather_stride2(const float* __restrict__ src, float* __restrict__ dst,
+                                                        int64_t ngroups) {
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ngroups; g += (int64_t)gridDim.x * blockDim.x) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(src) + 2 * g);
+    const float4 b = __ldg(reinterpret_cast<const float4*>(src) + 2 * g + 1);
+    reinterpret_cast<float4*>(dst)[g] = make_float4(a.x, a.z, b.x, b.z);
+  }
+}
+
 // Affine copy, V consecutive pattern elements per thread (P % V == 0, destination
 // contiguous within a pattern and V-aligned).  The source is read as one V-vector
 // when the pattern is contiguous (SRC_VEC), else as V strided scalars.
@@ -868,7 +881,7 @@ const char* tile_copy_plan_name(const aol_tiler& ts, const aol_tiler& td, int64_
       if (pl.tma && aligned) return "tile_copy.tma_box";
       return pl.src_vec ? "tile_copy.vec" : "tile_copy.vec_store";
     case 2: return pl.tma ? "tile_copy.tma_stream" : "tile_copy.stream16";
-    case 1: return "tile_copy.affine";
+    case 1: return pl.As == 2 && pl.Ad == 1 && tiler_pat_total(ts) == 1 && esz == 4 ? "tile_copy.stride2" : "tile_copy.affine";
     default: return "tile_copy.generic";
   }
 }
@@ -1103,6 +1116,21 @@ static int launch_tile_copy_t(const aol_tiler& ts, const aol_tiler& td, int64_t 
       return AOL_OK;
     }
     p.kind = 1;
+  }
+  if (p.kind == 1 && sizeof(T) == 4 && P == 1 && p.As == 2 && p.Ad == 1) {
+    // stride-2 gather: whole groups of 4 repetitions from 16-byte aligned source/destination
+    const float* s0 = reinterpret_cast<const float*>(s) + p.cs + 2 * first;
+    float* d0 = reinterpret_cast<float*>(d) + p.cd + first;
+    // every group reads 8 source elements: stay inside the source array
+    const int64_t room = (tiler_arr_total(ts) - (p.cs + 2 * first)) / 8;
+    const int64_t groups = std::min<int64_t>(count / 4, std::max<int64_t>(room, 0));
+    if (groups > 0 && (uintptr_t)s0 % 16 == 0 && (uintptr_t)d0 % 16 == 0) {
+      k_gather_stride2<<<grid_for(groups, 1024, 16), 256, 0, stream>>>(s0, d0, groups);
+      AOL_LAUNCH_CHECK("k_gather_stride2");
+      first += 4 * groups;                              // the < 4 trailing repetitions below
+      count -= 4 * groups;
+      if (count == 0) return AOL_OK;
+    }
   }
   if (p.kind == 1) {
     const int64_t n = count * P;

@@ -186,6 +186,7 @@ def test_tile_copy_plans_vs_oracle(case, devices, dtype):
     ("float32", None, 40000, 8, 4, 8, "tile_copy.vec"),            # overlapping 32 B rows: register path
     ("float32", None, 20001, 32, 16, 32, "tile_copy.tma_box"),     # overlapping 128 B rows: TMA box (L2 re-reads)
     ("float32", None, 20001, 12, 6, 12, "tile_copy.vec"),          # P not a power of two: register path
+    ("float32", None, 300003, 1, 2, 1, "tile_copy.stride2"),       # every other element (m = 1 gaps)
 ])
 @pytest.mark.parametrize("devices", [1, 3])
 def test_tile_copy_tma_plans_vs_oracle(case, devices):

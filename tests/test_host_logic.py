@@ -97,6 +97,8 @@ def test_tile_copy_plan_dispatch_rules_without_gpu():
     assert _copy_plan(row1d(200000, 2, 1), _dense(200000, 2)) == "tile_copy.window"               # overlap, 8 B
     assert _copy_plan(row1d(100000, 4, 3), _dense(100000, 4)) == "tile_copy.window"
     assert _copy_plan(row1d(40000, 8, 16, f=2), _dense(40000, 8)) == "tile_copy.vec_store"        # strided fitting
+    assert _copy_plan(row1d(1000, 1, 2), _dense(1000, 1)) == "tile_copy.stride2"                  # m = 1 gaps
+    assert _copy_plan(row1d(1000, 1, 3), _dense(1000, 1)) == "tile_copy.affine"
     assert _copy_plan(row1d(40000, 4, 8), _dense(40000, 4), "float64") == "tile_copy.tma_box"    # 32 B fp64 rows
 
     def rowstride(m, T):
