@@ -268,3 +268,26 @@ def test_model_json_roundtrip(golden):
     assert model_to_dict(m) == d
     s = build_schedule(m, 4)
     assert len(s.steps) == 4 and hasattr(s.steps[-1], "body") and len(s.steps[-1].body) == 12
+
+
+def test_model_memo_per_object_and_evicted():
+    """Derived per-model structures are computed once per model object and dropped with it."""
+    import gc
+    from paper_1105_4424_b200 import builders
+    from paper_1105_4424_b200.model import _MODEL_MEMO, connected_port_groups, model_memo
+    g = orc.gemm_tilers(8, 8, 4)
+    mk = lambda: builders.tile_task_model(  # noqa: E731
+        "matmul", {"a": "in float32 [8,4]", "b": "in float32 [4,8]", "c": "out float32 [8,8]"},
+        {k: Tiler(v["origin"], v["paving"], v["fitting"], v["pattern"]) for k, v in g.items()}, (8, 8))
+    m1, m2 = mk(), mk()
+    calls = []
+    assert model_memo(m1, "k", lambda m: calls.append(1) or 7) == 7
+    assert model_memo(m1, "k", lambda m: calls.append(1) or 8) == 7
+    assert model_memo(m2, "k", lambda m: calls.append(1) or 9) == 9
+    assert len(calls) == 2
+    assert connected_port_groups(m1) is connected_port_groups(m1)
+    key = id(m1)
+    assert key in _MODEL_MEMO
+    del m1
+    gc.collect()
+    assert key not in _MODEL_MEMO
