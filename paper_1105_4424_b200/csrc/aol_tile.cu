@@ -307,23 +307,23 @@ __global__ void __launch_bounds__(32) k_tile_copy_tma(const __grid_constant__ CU
 // Overlapping source rows (0 < As < P, unit fitting, fp32) into dense destination rows: tile t
 // of R repetitions needs the contiguous source window [cs + As*r0, cs + As*(r0+R-1) + P), read
 // ONCE from DRAM by one bulk copy (the 16-byte aligned part; the <= 3 trailing elements come
-// from global memory) into a 4-deep shared-memory ring; 256 threads expand it into P-element
+// from global memory) into a double-buffered shared-memory ring; 256 threads expand it into P-element
 // rows with coalesced 16-byte stores.  Each input element is read once instead of P/As times
 // through L1/L2 as the register gather does.
-constexpr int kWinStages = 4;
+constexpr int kWinMaxStages = 8;
 template <int LOGP>
 __global__ void __launch_bounds__(256) k_tile_copy_window(const float* __restrict__ src, float* __restrict__ dst,
                                                           int64_t cs, int64_t As, int64_t cd, int64_t first,
-                                                          int64_t count, int R, uint32_t win_pitch) {
+                                                          int64_t count, int R, uint32_t win_pitch, int nst) {
   constexpr int P = 1 << LOGP;
   extern __shared__ __align__(128) unsigned char ring_raw[];
   float* ring = reinterpret_cast<float*>(ring_raw);
-  __shared__ __align__(8) uint64_t full[kWinStages];
+  __shared__ __align__(8) uint64_t full[kWinMaxStages];
   const int tid = threadIdx.x;
   const int64_t ntiles = (count + R - 1) / R;
   const int64_t mine = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
   if (tid == 0) {
-    for (int i = 0; i < kWinStages; ++i) mbar_init(&full[i], 1);
+    for (int i = 0; i < nst; ++i) mbar_init(&full[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -338,18 +338,18 @@ __global__ void __launch_bounds__(256) k_tile_copy_window(const float* __restric
   auto load = [&](int64_t k) {
     int64_t a0, a1, w1, r0, n;
     window(k, a0, a1, w1, r0, n);
-    const int st = (int)(k % kWinStages);
+    const int st = (int)(k % nst);
     const uint32_t bytes = (uint32_t)((a1 - a0) * 4);
     mbar_expect_tx(&full[st], bytes);
     if (bytes) bulk_load(ring + (size_t)st * win_pitch, src + a0, bytes, &full[st]);
   };
   if (tid == 0)
-    for (int64_t k = 0; k < mine && k < kWinStages; ++k) load(k);
+    for (int64_t k = 0; k < mine && k < nst; ++k) load(k);
   for (int64_t k = 0; k < mine; ++k) {
-    const int st = (int)(k % kWinStages);
+    const int st = (int)(k % nst);
     int64_t a0, a1, w1, r0, n;
     window(k, a0, a1, w1, r0, n);
-    mbar_wait(&full[st], (uint32_t)((k / kWinStages) & 1));
+    mbar_wait(&full[st], (uint32_t)((k / nst) & 1));
     const float* win = ring + (size_t)st * win_pitch;
     float* out = dst + cd + r0 * P;                    // dense rows: [n][P]
     const int total = (int)(n * P);
@@ -368,7 +368,7 @@ __global__ void __launch_bounds__(256) k_tile_copy_window(const float* __restric
       for (int e = tid; e < total; e += 256) out[e] = at(e);
     }
     __syncthreads();                                     // stage st consumed by every thread
-    if (tid == 0 && k + kWinStages < mine) load(k + kWinStages);
+    if (tid == 0 && k + nst < mine) load(k + nst);
   }
 }
 
@@ -855,9 +855,9 @@ static CopyPlan plan_tile_copy(const aol_tiler& ts, const aol_tiler& td, int64_t
       break;
     }
   }
-  // overlapping contiguous source rows into dense rows: one bulk window per tile (measured best for
-  // 8-16 B rows: 5.1 -> 5.6-5.9 TB/s; 32-64 B rows tie with registers, >= 128 B rows go to TMA boxes)
-  if (p.kind == 3 && esz == 4 && P > 1 && P <= 4 && (P & (P - 1)) == 0 && p.Bs == 1 && p.Bd == 1 && p.As > 0 &&
+  // overlapping contiguous source rows into dense rows: one bulk window per tile (measured 6.0-6.1
+  // TB/s for 8-64 B rows vs 5.1-5.6 through registers; >= 128 B rows go to TMA boxes, 6.1)
+  if (p.kind == 3 && esz == 4 && P > 1 && P <= 16 && (P & (P - 1)) == 0 && p.Bs == 1 && p.Bd == 1 && p.As > 0 &&
       p.As < P && p.Ad == P && count * P * (int64_t)esz >= kTmaMinBytes) {
     p.window = true;
     return p;
@@ -935,22 +935,25 @@ static int launch_tma_rows(const void* src, void* dst, int64_t rows, int64_t P, 
 }
 
 // Overlapping source rows into dense rows through k_tile_copy_window (fp32, P a power of two
-// up to 64 (the plan uses it for P <= 4), 0 < As < P, Bs == 1, Ad == P).  AOL_EUNSUPPORTED (nothing launched) otherwise.
+// up to 64 (the plan uses it for P <= 16), 0 < As < P, Bs == 1, Ad == P).  AOL_EUNSUPPORTED (nothing launched) otherwise.
 static int launch_window(const float* src, float* dst, int64_t cs, int64_t As, int64_t cd, int64_t first,
                          int64_t count, int64_t P, cudaStream_t stream) {
   int logp = -1;
   for (int l = 0; l <= 6; ++l)
     if ((int64_t)1 << l == P) logp = l;
   if (logp < 0 || As <= 0 || As >= P || (uintptr_t)src % 16) return AOL_EUNSUPPORTED;
-  const int R = (int)std::max<int64_t>(32, std::min<int64_t>(4096, 2048 / As));   // ~8 KB windows
+  // ring geometry (measured, m = 2/4 overlap at T = 1e8/1e9): 32 KB windows, double-buffered,
+  // 8 CTAs per SM in the grid (about 3 resident): 6.0-6.1 TB/s; 8 KB x 4 stages gave 5.4-5.7
+  constexpr int win_kb = 32, nst = 2, cps = 8;
+  const int R = (int)std::max<int64_t>(32, std::min<int64_t>(16384, win_kb * 256 / As));
   const uint32_t win_pitch = (uint32_t)(((As * (R - 1) + P + 8) + 31) & ~int64_t(31));
-  const int smem = kWinStages * (int)win_pitch * 4;
-  if (smem > 48 * 1024) return AOL_EUNSUPPORTED;
+  const int smem = nst * (int)win_pitch * 4;
+  if (smem > 200 * 1024) return AOL_EUNSUPPORTED;
   const int64_t ntiles = (count + R - 1) / R;
   int sms = kNumSMs, dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)sms * 4);
-  void (*k)(const float*, float*, int64_t, int64_t, int64_t, int64_t, int64_t, int, uint32_t);
+  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)sms * cps);
+  void (*k)(const float*, float*, int64_t, int64_t, int64_t, int64_t, int64_t, int, uint32_t, int);
   switch (logp) {
     case 0: k = k_tile_copy_window<0>; break;
     case 1: k = k_tile_copy_window<1>; break;
@@ -960,7 +963,9 @@ static int launch_window(const float* src, float* dst, int64_t cs, int64_t As, i
     case 5: k = k_tile_copy_window<5>; break;
     default: k = k_tile_copy_window<6>; break;
   }
-  k<<<grid, 256, smem, stream>>>(src, dst, cs, As, cd, first, count, R, win_pitch);
+  if (smem > 48 * 1024) AOL_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  // (the attribute call is per launch: launches reach here only for >= 1 MB copies)
+  k<<<grid, 256, smem, stream>>>(src, dst, cs, As, cd, first, count, R, win_pitch, nst);
   AOL_LAUNCH_CHECK("k_tile_copy_window");
   return AOL_OK;
 }
@@ -998,6 +1003,7 @@ static int launch_tma_transpose(const float* src, float* dst, int64_t count, int
       P == 8 ? k_tile_copy_tma_transpose<8> : P == 16 ? k_tile_copy_tma_transpose<16>
       : P == 32 ? k_tile_copy_tma_transpose<32> : k_tile_copy_tma_transpose<64>;
   if (smem > 48 * 1024) AOL_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  // (the attribute call is per launch: launches reach here only for >= 1 MB copies)
   k<<<grid, 128, smem, stream>>>(ms, md, ntiles);
   AOL_LAUNCH_CHECK("k_tile_copy_tma_transpose");
   return AOL_OK;

@@ -180,10 +180,11 @@ def test_tile_copy_plans_vs_oracle(case, devices, dtype):
     ("float64", None, 40000, 4, 8, 4, "tile_copy.tma_box"),        # 32 B fp64 rows
     ("float32", None, 300001, 4, 4, 4, "tile_copy.tma_stream"),    # dense: 256 B rows + 16 B vectors + tail
     ("float64", None, 150001, 2, 2, 2, "tile_copy.tma_stream"),
-    ("float32", None, 200001, 2, 1, 2, "tile_copy.window"),        # overlapping 8-16 B rows: one bulk window/tile
+    ("float32", None, 200001, 2, 1, 2, "tile_copy.window"),        # overlapping 8-64 B rows: one bulk window/tile
     ("float32", None, 100001, 4, 2, 4, "tile_copy.window"),
     ("float32", None, 100000, 4, 3, 4, "tile_copy.window"),        # odd source pitch (windows unaligned)
-    ("float32", None, 40000, 8, 4, 8, "tile_copy.vec"),            # overlapping 32 B rows: register path
+    ("float32", None, 40000, 8, 4, 8, "tile_copy.window"),         # overlapping 32 B rows
+    ("float32", None, 20001, 16, 5, 16, "tile_copy.window"),
     ("float32", None, 20001, 32, 16, 32, "tile_copy.tma_box"),     # overlapping 128 B rows: TMA box (L2 re-reads)
     ("float32", None, 20001, 12, 6, 12, "tile_copy.vec"),          # P not a power of two: register path
     ("float32", None, 300003, 1, 2, 1, "tile_copy.stride2"),       # every other element (m = 1 gaps)

@@ -93,7 +93,7 @@ def test_tile_copy_plan_dispatch_rules_without_gpu():
     assert _copy_plan(row1d(40000, 4, 8), _dense(40000, 4)) == "tile_copy.vec"                    # 16 B rows
     assert _copy_plan(row1d(40000, 8, 18), _dense(40000, 8)) == "tile_copy.vec"                   # 72 B pitch
     assert _copy_plan(row1d(20000, 32, 16), _dense(20000, 32)) == "tile_copy.tma_box"             # overlap, 128 B
-    assert _copy_plan(row1d(40000, 8, 4), _dense(40000, 8)) == "tile_copy.vec"                    # overlap, 32 B
+    assert _copy_plan(row1d(40000, 8, 4), _dense(40000, 8)) == "tile_copy.window"                 # overlap, 32 B
     assert _copy_plan(row1d(200000, 2, 1), _dense(200000, 2)) == "tile_copy.window"               # overlap, 8 B
     assert _copy_plan(row1d(100000, 4, 3), _dense(100000, 4)) == "tile_copy.window"
     assert _copy_plan(row1d(40000, 8, 16, f=2), _dense(40000, 8)) == "tile_copy.vec_store"        # strided fitting
