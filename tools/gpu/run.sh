@@ -1,1 +1,1 @@
-nvcc -gencode arch=compute_100a,code=sm_100a -o /tmp/clus tools/micro/cluster_occupancy.cu && /tmp/clus > gpurun_out/clus.log 2>&1; echo a=$?
+python tools/time_3xtf32.py > gpurun_out/t3x.log 2>&1; echo a=$?
