@@ -307,6 +307,7 @@ def make_distributed_executor(model, schedule, bindings: dict, *, group=None, **
             import torch.distributed as dist
             self.xch = Exchange(group)
             kw.setdefault("fuse", False)     # fused chains skip the intermediate exchange
+            kw.setdefault("graphs", False)   # loop bodies need the per-step exchange and dot combine
             super().__init__(model, schedule, bindings, self.xch.world, **kw)
             self.rank, self.world = self.xch.rank, self.xch.world
 

@@ -183,7 +183,7 @@ class Executor:
 
     def __init__(self, model, schedule, bindings: dict, device_count: int, *, tilers: dict | None = None,
                  precision: str = "default", device=None, stream=None, pipeline: int = 0, fuse: bool = True,
-                 graphs: bool = False):
+                 graphs: bool = True):
         torch = _torch()
         _capi.load()
         if not torch.cuda.is_available():
@@ -803,8 +803,11 @@ class Executor:
 def execute_schedule(model, schedule, bindings: dict, device_count: int, tol: float | None = None,
                      max_iter: int | None = None, *, tilers: dict | None = None, precision: str = "default",
                      device_outputs: bool = False, out: dict | None = None, device=None,
-                     stream=None, pipeline: int = 0, fuse: bool = True, graphs: bool = False) -> ExecutionResult:
-    """Interpret ``schedule`` on the B200 with ``device_count`` launch shards per device step."""
+                     stream=None, pipeline: int = 0, fuse: bool = True, graphs: bool = True) -> ExecutionResult:
+    """Interpret ``schedule`` on the B200 with ``device_count`` launch shards per device step.
+
+    ``graphs`` (default on): a LoopStep runs on the device -- the persistent interpreter, else
+    one CUDA graph with a WHILE node -- bit-identical to host-driven iterations (graphs=False)."""
     ex = Executor(model, schedule, bindings, device_count, tilers=tilers, precision=precision,
                   device=device, stream=stream, pipeline=0 if device_outputs else pipeline, fuse=fuse,
                   graphs=graphs)

@@ -693,7 +693,7 @@ def test_cg_graph_mode_equals_eager(golden, devices, persistent, monkeypatch):
     model = model_from_dict(m["model"])
     bind = {k: data[f"cg_k20/{k}"] for k in ("rowptr", "colidx", "values", "b")}
     sched = build_schedule(model, devices)
-    eager = Executor(model, sched, bind, devices)
+    eager = Executor(model, sched, bind, devices, graphs=False)
     eager.run()
     gr = Executor(model, sched, bind, devices, graphs=True)
     gr.run()
@@ -1071,7 +1071,7 @@ def test_cg_dtype_variants_persistent_equals_eager(golden, variant):
         bind = {k: (v.astype(np.float32) if k in ("values", "b") else v) for k, v in bind.items()}
     model = model_from_dict(_json.loads(text))
     sched = build_schedule(model, 1)
-    eager = Executor(model, sched, bind, 1)
+    eager = Executor(model, sched, bind, 1, graphs=False)
     eager.run()
     dev = Executor(model, sched, bind, 1, graphs=True)
     dev.run()

@@ -1,1 +1,2 @@
-python tools/time_3xtf32.py > gpurun_out/t3x.log 2>&1; echo a=$?
+python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?
