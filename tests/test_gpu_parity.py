@@ -1145,3 +1145,53 @@ def test_streamed_fused_downscaler_equals_plain(chunks, devices):
         got = ex.run_streamed()["y"]
     assert np.array_equal(got.view(np.uint32), plain.view(np.uint32))
     assert ex.fused_launches == (chunks if devices == 1 else devices)
+
+
+def _rand_big_copy(rng):
+    """A random >= 1 MB affine gather that lands on one of the bulk plans (TMA stream / box /
+    transpose, bulk window, stride-2, register paths), with random origins and pitches."""
+    kind = rng.choice(["box", "window", "transpose", "stride2", "dense", "dstgap"])
+    if kind == "transpose":
+        m = int(rng.choice([8, 16, 32, 64]))
+        T = int(rng.integers(1 << 20, 1 << 21) // (4 * m)) * 4 + int(rng.integers(0, 2)) * 4
+        extra = int(rng.integers(0, 3)) * 4
+        return dict(array=(m, T + extra), rep=(T,), pattern=(m,), origin=(0, int(rng.integers(0, extra + 1))),
+                    paving=((0,), (1,)), fitting=((1,), (0,))), T, m
+    if kind == "stride2":
+        T = int(rng.integers(300000, 600000))
+        o = int(rng.integers(0, 9))
+        return dict(array=(2 * T + o + 3,), rep=(T,), pattern=(1,), origin=(o,), paving=((2,),), fitting=((1,),)), T, 1
+    m = int(rng.choice([2, 4, 8, 16, 32, 64]))
+    p = {"box": 2 * m + 4 * int(rng.integers(0, 3)), "window": max(1, m // 2 - int(rng.integers(0, max(1, m // 4)))),
+         "dense": m, "dstgap": m}[kind]
+    T = int(rng.integers((1 << 20) // (4 * m), (1 << 21) // (4 * m)))
+    o = int(rng.integers(0, 64))
+    return dict(array=((T - 1) * p + m + o + int(rng.integers(0, 5)),), rep=(T,), pattern=(m,), origin=(o,),
+                paving=((p,),), fitting=((1,),)), T, m
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_large_copies_on_bulk_plans_vs_oracle(seed):
+    """Randomised >= 1 MB gathers through the bulk-copy plans, shards with arbitrary starts,
+    destinations with and without gaps: bit-exact against the C oracle."""
+    from paper_1105_4424_b200 import _capi
+    from oracle import c_oracle as co
+    rng = np.random.default_rng(7000 + seed)
+    plans = set()
+    for _ in range(5):
+        ts, T, m = _rand_big_copy(rng)
+        gap = int(rng.choice([0, 0, 4]))
+        td = dict(array=(T * (m + gap),), rep=(T,), pattern=(m,), origin=(0,), paving=((m + gap,),), fitting=((1,),))
+        src = (np.arange(int(np.prod(ts["array"]))) % (1 << 22)).astype(np.float32) + 1
+        want = np.zeros(T * (m + gap), np.float32)
+        co.tile_copy(src, want, ts, td, 0, T)
+        x = torch.from_numpy(src).cuda()
+        y = torch.zeros(T * (m + gap), device="cuda")
+        task = _capi.make_task("tile_copy", "float32",
+                               [_tiler(ts).bind(ts["array"], (T,)), _tiler(td).bind(td["array"], (T,))])
+        plans.add(_capi.plan_name(task, 0, T, [x.data_ptr(), y.data_ptr()]))
+        for off, cnt in orc.partition_equally(T, int(rng.choice([1, 2, 3, 5]))):
+            _capi.launch(task, off, cnt, [x.data_ptr(), y.data_ptr()], (), 0)
+        torch.cuda.synchronize()
+        assert np.array_equal(y.cpu().numpy(), want), (ts, gap)
+    assert plans

@@ -1,2 +1,1 @@
-python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?
+python -m pytest tests/test_gpu_parity.py -x -q -k "random_large" > gpurun_out/pytest_rl.log 2>&1; echo pytest=$?
