@@ -160,6 +160,73 @@ __global__ void __launch_bounds__(SV_TX) k_stencil_slide(const float* __restrict
   }
 }
 
+// Wider windows (KW = 5 or 7, any KH in {3, 5, 7}; the window centre column 16-byte aligned):
+// a thread still owns 4 columns, but each input row arrives as three float4s -- the aligned
+// quads left of, at and right of the centre -- of which the KW/2 innermost neighbours on
+// each side are kept.  RPT output rows per thread with every window load issued before any
+// arithmetic; the same tap order (di-major, dj-minor) and rounding as every other form.
+template <int KH, int KW, int RPT>
+__global__ void __launch_bounds__(SV_TX) k_stencil_slide_wide(const float* __restrict__ x,
+                                                              const float* __restrict__ w, float* __restrict__ y,
+                                                              int H, int W, int orow, int ocol, int rows,
+                                                              int64_t first, int64_t last) {
+  constexpr int HW = KW / 2;
+  static_assert(KW % 2 == 1 && HW >= 1 && HW <= 4, "odd window widths 3..9");
+  float wr[KH * KW];
+#pragma unroll
+  for (int k = 0; k < KH * KW; ++k) wr[k] = __ldg(w + k);
+  const int c0 = (blockIdx.x * SV_TX + threadIdx.x) * 4;
+  const int r0 = blockIdx.y * RPT;
+  if (c0 >= W || r0 >= rows) return;
+  const int cin = (int)(((int64_t)c0 + ocol + HW) % W);   // window centre of column c0, aligned
+  const int cl4 = cin >= 4 ? cin - 4 : cin - 4 + W;        // aligned quads either side
+  const int cr4 = cin + 4 >= W ? cin + 4 - W : cin + 4;
+  int row = (int)(((int64_t)r0 + orow) % H);
+  float v[RPT + KH - 1][4 + 2 * HW];
+#pragma unroll
+  for (int rr = 0; rr < RPT + KH - 1; ++rr) {
+    const float* xr = x + (size_t)row * (size_t)W;
+    const float4 l = __ldg(reinterpret_cast<const float4*>(xr + cl4));
+    const float4 c = __ldg(reinterpret_cast<const float4*>(xr + cin));
+    const float4 r = __ldg(reinterpret_cast<const float4*>(xr + cr4));
+    const float lq[4] = {l.x, l.y, l.z, l.w}, rq[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+    for (int k = 0; k < HW; ++k) {
+      v[rr][k] = lq[4 - HW + k];
+      v[rr][HW + 4 + k] = rq[k];
+    }
+    v[rr][HW] = c.x; v[rr][HW + 1] = c.y; v[rr][HW + 2] = c.z; v[rr][HW + 3] = c.w;
+    if (++row == H) row = 0;
+  }
+  const bool whole = (int64_t)r0 * W + c0 >= first && (int64_t)(r0 + RPT - 1) * W + c0 + 3 <= last &&
+                     r0 + RPT <= rows;
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
+#pragma unroll
+    for (int di = 0; di < KH; ++di) {
+      const float* vr = v[i + di];
+#pragma unroll
+      for (int dj = 0; dj < KW; ++dj) {
+        const float wt = wr[di * KW + dj];
+        st_add2(a0, a1, __fmul_rn(wt, vr[dj]), __fmul_rn(wt, vr[dj + 1]));
+        st_add2(a2, a3, __fmul_rn(wt, vr[dj + 2]), __fmul_rn(wt, vr[dj + 3]));
+      }
+    }
+    const int r = r0 + i;
+    float* yr = y + (size_t)r * (size_t)W + c0;
+    if (whole) {
+      *reinterpret_cast<float4*>(yr) = make_float4(a0, a1, a2, a3);
+    } else if (r < rows) {
+      const int64_t lin = (int64_t)r * W + c0;
+      const float a[4] = {a0, a1, a2, a3};
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (lin + j >= first && lin + j <= last) yr[j] = a[j];
+    }
+  }
+}
+
 // Recognise the box-stencil tiler pair; returns false when the generic kernel must run.
 bool stencil_box_applicable(const aol_task& t, int& KH, int& KW) {
   const aol_tiler &tx = t.tilers[0], &ty = t.tilers[1];
@@ -176,8 +243,13 @@ bool stencil_box_applicable(const aol_task& t, int& KH, int& KW) {
   if (ty.origin[0] % ty.array[0] != 0 || ty.origin[1] % ty.array[1] != 0) return false;
   KH = (int)tx.pattern[0];
   KW = (int)tx.pattern[1];
-  if (KW != 3 || !(KH == 3 || KH == 5)) return false;
+  if (!(KH == 3 || KH == 5 || KH == 7) || !(KW == 3 || KW == 5 || KW == 7)) return false;
   if (tx.array[0] >= (1ll << 31) || tx.array[1] >= (1ll << 31)) return false;
+  if (KW != 3) {                     // wide windows: only the aligned quad form exists
+    const int64_t W = tx.array[1];
+    const int64_t oc = ((tx.origin[1] % W) + W) % W;
+    if (W % 4 || (oc + KW / 2) % W % 4 || W < 8) return false;
+  }
   return true;
 }
 
@@ -201,7 +273,20 @@ int launch_stencil_box(const aol_task& t, int64_t first, int64_t count, void* co
   const int Hrows = rhi - rlo + 1;
   // rows are addressed relative to rlo for the output; the input row is (r + rlo + orow) mod H
   const int cshift = (int)emod((int64_t)ocol + 1, W);
-  if (W % 4 == 0 && cshift % 4 == 0 && !getenv("AOL_STENCIL_BOX")) {
+  if (KW != 3) {
+    // (applicability guaranteed W % 4 == 0 and an aligned window centre)
+    constexpr int RPT = 8;                 // measured: 16 rows per thread is slower (registers)
+    dim3 g3((W / 4 + SV_TX - 1) / SV_TX, (Hrows + RPT - 1) / RPT);
+    void (*k)(const float*, const float*, float*, int, int, int, int, int, int64_t, int64_t) =
+        KW == 5 ? (KH == 3 ? k_stencil_slide_wide<3, 5, RPT> : KH == 5 ? k_stencil_slide_wide<5, 5, RPT>
+                                                                        : k_stencil_slide_wide<7, 5, RPT>)
+                : (KH == 3 ? k_stencil_slide_wide<3, 7, RPT> : KH == 5 ? k_stencil_slide_wide<5, 7, RPT>
+                                                                        : k_stencil_slide_wide<7, 7, RPT>);
+    k<<<g3, SV_TX, 0, s>>>(x, w, y, H, W, orow_shift, ocol, Hrows, f2, l2);
+    AOL_LAUNCH_CHECK("k_stencil_slide_wide");
+    return AOL_OK;
+  }
+  if (W % 4 == 0 && cshift % 4 == 0 && !getenv("AOL_STENCIL_BOX") && KH != 7) {
     dim3 g2((W / 4 + SV_TX - 1) / SV_TX, (Hrows + SV_RPT - 1) / SV_RPT);
     if (KH == 3)
       k_stencil_slide<3><<<g2, SV_TX, 0, s>>>(x, w, y, H, W, orow_shift, ocol, Hrows, f2, l2);
@@ -212,8 +297,10 @@ int launch_stencil_box(const aol_task& t, int64_t first, int64_t count, void* co
   }
   if (KH == 3)
     k_stencil_box<3, 3><<<grid, block, 0, s>>>(x, w, y, H, W, orow_shift, ocol, f2, l2);
-  else
+  else if (KH == 5)
     k_stencil_box<5, 3><<<grid, block, 0, s>>>(x, w, y, H, W, orow_shift, ocol, f2, l2);
+  else
+    k_stencil_box<7, 3><<<grid, block, 0, s>>>(x, w, y, H, W, orow_shift, ocol, f2, l2);
   (void)Hrows;
   AOL_LAUNCH_CHECK("k_stencil_box");
   return AOL_OK;

@@ -1195,3 +1195,24 @@ def test_random_large_copies_on_bulk_plans_vs_oracle(seed):
         torch.cuda.synchronize()
         assert np.array_equal(y.cpu().numpy(), want), (ts, gap)
     assert plans
+
+
+@pytest.mark.parametrize("kh,kw", [(3, 5), (5, 5), (7, 5), (3, 7), (5, 7), (7, 7), (7, 3)])
+@pytest.mark.parametrize("H,W,devices", [(64, 256, 1), (37, 512, 3), (100, 1024, 5)])
+def test_stencil_wide_windows_vs_oracle(kh, kw, H, W, devices):
+    """KH x KW toroidal box stencils beyond 3 columns (aligned quad form, k_stencil_slide_wide)
+    and 7-row windows: bit-exact vs the oracle (random weights, origin centring the window)."""
+    t = orc.stencil_tilers(H, W)
+    t["x"] = dict(t["x"], pattern=(kh, kw), origin=(H - kh // 2, W - kw // 2))
+    w = (np.random.default_rng(kh * 10 + kw).standard_normal(kh * kw) / 8).astype(np.float32)
+    assert _plan([t["x"], t["y"]]) == "tile_filter.stencil_box"
+    x = np.random.default_rng(H + W + kw).standard_normal(H * W).astype(np.float32)
+    got, ref = _filter_case("stencil", t, w, x, devices)
+    assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
+    # a misaligned window centre has no wide form: the generic filter takes it, still exact
+    if kw != 3:
+        t2 = dict(t)
+        t2["x"] = dict(t["x"], origin=(H - kh // 2, W - kw // 2 + 1))
+        assert _plan([t2["x"], t2["y"]]) != "tile_filter.stencil_box"
+        got, ref = _filter_case("stencil", t2, w, x, devices)
+        assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
