@@ -1,5 +1,4 @@
-python -m pytest tests/test_gpu_parity.py -x -q -k "cg or loop or dot" > gpurun_out/pytest_cg.log 2>&1; echo pytest=$?
-for wl in cg cg27; do for f in 0 1 0 1; do
-echo "wl=$wl fuse=$f" >> gpurun_out/ab.log
-AOL_LOOP_FUSE_SCALARS=$f AOL_LOOP_TIME=1 DIAG_REPS=4 DIAG_WL=$wl python tools/diag_cg.py >> gpurun_out/ab.log 2>&1
-done; done
+for w in matmul downscaler cg sweep; do
+AOL_BENCH_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port $((29500 + RANDOM % 400)) bench.py --gpus 2 --workload $w --steps 10 --warmup 3 --no-cpu --no-peak --no-points > gpurun_out/n2_$w.json 2> gpurun_out/n2_$w.err
+echo $w=$?
+done
