@@ -25,6 +25,7 @@ void count_launch(int n) { g_launches += n; }
 // defined in the kernel translation units
 int launch_tiler_offsets(const aol_tiler& t, int64_t first, int64_t count, int64_t* out, cudaStream_t s);
 int launch_tile_copy(const aol_task& t, int64_t first, int64_t count, void* const* ports, cudaStream_t s);
+const char* tile_sum_plan_name(const aol_task& t);
 const char* tile_copy_plan_name(const aol_tiler& ts, const aol_tiler& td, int64_t first, int64_t count,
                                 size_t esz, void* const* ports);
 int launch_matmul_generic(const aol_task& t, int64_t first, int64_t count, void* const* ports, cudaStream_t s);
@@ -89,7 +90,7 @@ static const char* plan_name(const aol_task* t, int64_t first, int64_t count, vo
         return t->precision == AOL_PREC_3XTF32 ? "matmul.tcgen05_3xtf32" : "matmul.tcgen05_tf32";
       return "matmul.generic_exact";
     case AOL_OP_TILE_FILTER: return filter_plan_name(*t);
-    case AOL_OP_TILE_SUM: return "tile_sum.generic";
+    case AOL_OP_TILE_SUM: return tile_sum_plan_name(*t);
     default: return "identity";
   }
 }

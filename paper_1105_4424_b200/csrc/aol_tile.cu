@@ -754,6 +754,102 @@ __global__ void k_tile_sum_generic(const T* __restrict__ x, T* __restrict__ s, D
   }
 }
 
+// Pattern reductions over an affine x tiler (x[cs + As*rho + Bs*i], collapsed to one repetition
+// and one pattern stride).  Always i ascending with one rounding per add, like the generic form.
+//
+// Contiguous patterns (Bs == 1, e.g. row sums): a warp owns 32 repetitions and walks their
+// patterns in 32-element chunks.  Lane l copies element i0+l of each of the 32 rows with
+// cp.async (every copy instruction covers one row's 128 contiguous bytes: coalesced) into a
+// padded 32x33 shared tile; TS_DEPTH chunks are in flight while lane j adds row j's values of
+// the oldest chunk in order.  The sum of a row is one dependent chain (i ascending, one
+// rounding per add), so the loads are what has to be hidden.
+constexpr int TS_DEPTH = 4;
+template <typename T> constexpr int ts_warps() { return sizeof(T) == 4 ? 2 : 1; }   // <= 48 KB static smem
+
+template <typename T>
+__device__ __forceinline__ void cp_async_elem(T* dst, const T* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(dst)), "l"(src), "n"(sizeof(T)) : "memory");
+}
+
+template <typename T>
+__global__ void __launch_bounds__(32 * ts_warps<T>()) k_tile_sum_rows(const T* __restrict__ x, T* __restrict__ s,
+                                                                  int64_t cs, int64_t As, int64_t P, DevTiler ts,
+                                                                  int64_t first, int64_t count) {
+  constexpr int WARPS = ts_warps<T>();
+  __shared__ T tile[WARPS][TS_DEPTH][32][33];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * WARPS;
+  const int64_t nchunks = (P + 31) / 32;
+  for (int64_t wb = blockIdx.x * WARPS + warp; wb * 32 < count; wb += nwarps) {
+    const int64_t r0 = first + wb * 32;
+    const int nr = (int)(first + count - r0 < 32 ? first + count - r0 : 32);
+    auto issue = [&](int64_t c) {
+      if (c < nchunks) {
+        const int64_t i0 = c * 32;
+        const int ni = (int)(P - i0 < 32 ? P - i0 : 32);
+        T(*tl)[33] = tile[warp][c % TS_DEPTH];
+        if (lane < ni)
+          for (int j = 0; j < nr; ++j) cp_async_elem(&tl[j][lane], x + cs + As * (r0 + j) + i0 + lane);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");      // (empty groups keep the count)
+    };
+    for (int c = 0; c < TS_DEPTH - 1; ++c) issue(c);
+    T acc = T(0);
+    for (int64_t c = 0; c < nchunks; ++c) {
+      issue(c + TS_DEPTH - 1);
+      asm volatile("cp.async.wait_group %0;" ::"n"(TS_DEPTH - 1) : "memory");
+      __syncwarp();
+      const int ni = (int)(P - c * 32 < 32 ? P - c * 32 : 32);
+      const T(*tl)[33] = tile[warp][c % TS_DEPTH];
+      if (lane < nr) {
+        for (int k = 0; k < ni; ++k) {
+          if constexpr (sizeof(T) == 4) acc = __fadd_rn(acc, tl[lane][k]);
+          else acc = __dadd_rn(acc, tl[lane][k]);
+        }
+      }
+      __syncwarp();                                               // slot c % TS_DEPTH free again
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    if (lane < nr) s[tiler_offset(ts, r0 + lane, 0)] = acc;
+  }
+}
+
+// Any other affine pattern (e.g. column sums, As == 1: consecutive threads read consecutive
+// addresses), and, with `table == false`, wrapping tilers too large for the offset table.
+template <typename T, bool AFFINE>
+__global__ void __launch_bounds__(256) k_tile_sum_direct(const T* __restrict__ x, T* __restrict__ s, int64_t cs,
+                                                         int64_t As, int64_t Bs, DevTiler tx, DevTiler ts,
+                                                         int64_t first, int64_t count, int64_t P) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rho = first + e;
+    T acc = T(0);
+    if (AFFINE) {
+      const T* p = x + cs + As * rho;
+      int64_t i = 0;
+      for (; i + 64 <= P; i += 64) {               // 64 loads in flight, then the 64 adds in order
+        T v[64];
+#pragma unroll
+        for (int u = 0; u < 64; ++u) v[u] = __ldg(p + Bs * (i + u));
+#pragma unroll
+        for (int u = 0; u < 64; ++u) {
+          if constexpr (sizeof(T) == 4) acc = __fadd_rn(acc, v[u]);
+          else acc = __dadd_rn(acc, v[u]);
+        }
+      }
+      for (; i < P; ++i) {
+        if constexpr (sizeof(T) == 4) acc = __fadd_rn(acc, __ldg(p + Bs * i));
+        else acc = __dadd_rn(acc, __ldg(p + Bs * i));
+      }
+    } else {
+      for (int64_t i = 0; i < P; ++i) {
+        if constexpr (sizeof(T) == 4) acc = __fadd_rn(acc, x[tiler_offset(tx, rho, i)]);
+        else acc = __dadd_rn(acc, x[tiler_offset(tx, rho, i)]);
+      }
+    }
+    s[tiler_offset(ts, rho, 0)] = acc;
+  }
+}
+
 // ------------------------------------------------------- launch wrappers ----
 
 int launch_tiler_offsets(const aol_tiler& t, int64_t first, int64_t count, int64_t* out,
@@ -1272,12 +1368,65 @@ int launch_filter_generic(const aol_task& t, int64_t first, int64_t count, void*
              : launch_filter_t<double, 16, false>(t, tx, ty, first, count, (int)px, (int)py, ports, stream);
 }
 
+// tile_sum plan: "rows" (affine, contiguous pattern), "direct" (other affine), "generic"
+// (offset table in shared memory), "generic_direct" (wrapping and too large for the table).
+static int tile_sum_kind(const aol_task& t, int64_t& cs, int64_t& As, int64_t& Bs) {
+  const aol_tiler& tx = t.tilers[0];
+  Affine a = tiler_affine(tx);
+  const int64_t P = tiler_pat_total(tx);
+  if (a.ok && collapse(a.A, tx.rep, tx.rep_rank, As) && collapse(a.B, tx.pattern, tx.pat_rank, Bs)) {
+    cs = a.c0;
+    if (P == 1) Bs = 0;
+    return P >= 32 && Bs == 1 ? 0 : 1;
+  }
+  int64_t dummy = 0;
+  DevTiler d;
+  if (make_dev_tiler(tx, d) == AOL_OK) dummy = P * d.a;
+  return dummy <= kTableMax ? 2 : 3;
+}
+
+const char* tile_sum_plan_name(const aol_task& t) {
+  int64_t cs, As, Bs;
+  switch (tile_sum_kind(t, cs, As, Bs)) {
+    case 0: return "tile_sum.rows";
+    case 1: return "tile_sum.direct";
+    case 2: return "tile_sum.generic";
+    default: return "tile_sum.generic_direct";
+  }
+}
+
 int launch_tile_sum(const aol_task& t, int64_t first, int64_t count, void* const* ports, cudaStream_t stream) {
   DevTiler tx, ts;
   int rc;
   if ((rc = make_dev_tiler(t.tilers[0], tx)) || (rc = make_dev_tiler(t.tilers[1], ts))) return rc;
   const int64_t px = tiler_pat_total(t.tilers[0]);
-  if (px * tx.a > kTableMax) return fail(AOL_EUNSUPPORTED, "tile_sum pattern too large");
+  int64_t cs = 0, As = 0, Bs = 0;
+  const int kind = tile_sum_kind(t, cs, As, Bs);
+  const bool f32 = t.dtype == AOL_F32;
+  if (kind == 0) {
+    const int per = 32 * (f32 ? ts_warps<float>() : ts_warps<double>());
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((count + per - 1) / per, (int64_t)kNumSMs * 32));
+    if (f32)
+      k_tile_sum_rows<float><<<grid, per, 0, stream>>>((const float*)ports[0], (float*)ports[1], cs, As, px, ts,
+                                                       first, count);
+    else
+      k_tile_sum_rows<double><<<grid, per, 0, stream>>>((const double*)ports[0], (double*)ports[1], cs, As, px, ts,
+                                                        first, count);
+    AOL_LAUNCH_CHECK("k_tile_sum_rows");
+    return AOL_OK;
+  }
+  if (kind == 1 || kind == 3) {
+    const unsigned grid = grid_for(count, 256, 16);
+    if (kind == 1) {
+      if (f32) k_tile_sum_direct<float, true><<<grid, 256, 0, stream>>>((const float*)ports[0], (float*)ports[1], cs, As, Bs, tx, ts, first, count, px);
+      else k_tile_sum_direct<double, true><<<grid, 256, 0, stream>>>((const double*)ports[0], (double*)ports[1], cs, As, Bs, tx, ts, first, count, px);
+    } else {
+      if (f32) k_tile_sum_direct<float, false><<<grid, 256, 0, stream>>>((const float*)ports[0], (float*)ports[1], cs, As, Bs, tx, ts, first, count, px);
+      else k_tile_sum_direct<double, false><<<grid, 256, 0, stream>>>((const double*)ports[0], (double*)ports[1], cs, As, Bs, tx, ts, first, count, px);
+    }
+    AOL_LAUNCH_CHECK("k_tile_sum_direct");
+    return AOL_OK;
+  }
   const size_t smem = (size_t)px * tx.a * sizeof(int64_t);
   if (t.dtype == AOL_F32)
     k_tile_sum_generic<float><<<grid_for(count, 256, 16), 256, smem, stream>>>(

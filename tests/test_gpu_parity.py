@@ -1216,3 +1216,36 @@ def test_stencil_wide_windows_vs_oracle(kh, kw, H, W, devices):
         assert _plan([t2["x"], t2["y"]]) != "tile_filter.stencil_box"
         got, ref = _filter_case("stencil", t2, w, x, devices)
         assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
+
+
+@pytest.mark.parametrize("case,plan", [("rows", "tile_sum.rows"), ("rows_ragged", "tile_sum.rows"),
+                                       ("cols", "tile_sum.direct"), ("wrap_small", "tile_sum.generic"),
+                                       ("wrap_big", "tile_sum.generic_direct")])
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+@pytest.mark.parametrize("devices", [1, 3])
+def test_tile_sum_plans_vs_oracle(case, plan, dtype, devices):
+    """Pattern reductions (i ascending, one rounding per add) on every tile_sum plan: coalesced
+    warp-transposed row sums, direct affine sums (column sums), the offset-table generic form
+    and the table-free form for large wrapping patterns -- bit-exact against the oracle."""
+    if case in ("rows", "rows_ragged"):
+        R, P = (300, 1000) if case == "rows" else (77, 45)
+        tx = dict(array=(R, P), rep=(R,), pattern=(P,), origin=(0, 0), paving=((1,), (0,)), fitting=((0,), (1,)))
+    elif case == "cols":
+        R, P = 700, 300
+        tx = dict(array=(P, R), rep=(R,), pattern=(P,), origin=(0, 0), paving=((0,), (1,)), fitting=((1,), (0,)))
+    elif case == "wrap_small":
+        R, P = 500, 9
+        tx = dict(array=(600,), rep=(R,), pattern=(P,), origin=(595,), paving=((1,),), fitting=((1,),))
+    else:
+        R, P = 40, 5000
+        tx = dict(array=(6000,), rep=(R,), pattern=(P,), origin=(5990,), paving=((7,),), fitting=((1,),))
+    ts = dict(array=(R,), rep=(R,), pattern=(1,), origin=(0,), paving=((1,),), fitting=((0,),))
+    x = np.random.default_rng(R + P).standard_normal(int(np.prod(tx["array"]))).astype(dtype)
+    got = _run_tile("tile_sum", {"x": tx, "s": ts}, {"x": _spec(tx, "in", dtype), "s": _spec(ts, "out", dtype)},
+                    {"x": x}, devices).outputs["p_s"]
+    ref = orc.run_tile_task("tile_sum", {"x": tx, "s": ts}, {"x": x}, {"s": (R, np.dtype(dtype))}, R, devices)["s"]
+    u = f"u{np.dtype(dtype).itemsize}"
+    assert np.array_equal(got.view(u), ref.view(u))
+    from paper_1105_4424_b200 import _capi
+    task = _capi.make_task("tile_sum", dtype, [_tiler(tx).bind(tx["array"], (R,)), _tiler(ts).bind(ts["array"], (R,))])
+    assert _capi.plan_name(task, 0, R) == plan
