@@ -1,2 +1,1 @@
-python -m pytest tests/test_gpu_parity.py -x -q -k "tile_sum or golden or random_tilers" > gpurun_out/pytest_ts.log 2>&1; echo pytest=$?
-python tools/time_tile_sum.py > gpurun_out/tsum.log 2>&1; echo a=$?
+timeout 600 python tools/time_filters.py > gpurun_out/filters.log 2>&1; echo a=$?
