@@ -230,12 +230,88 @@ static bool vline_stream_ok(const LineGeom& g);
 static int launch_line_stream(const LineGeom& lg, int64_t first, int64_t count, const float* x, const float* w,
                               float* y, cudaStream_t s);
 
+// Generic horizontal line filter (inner == 1: 1-D FIRs and decimating FIRs with paving <= 4,
+// any px <= 32 / py <= 8): a CTA takes up to 8192 consecutive repetitions of one line, loads
+// their whole input window [ox + sx*l0, ox + sx*(l0+n-1) + px) once with coalesced loads into
+// shared memory (padded one float per 32 so strided window starts hit distinct banks), then
+// each thread forms its repetitions' py outputs from it, taps in pattern order with
+// __fmul_rn / __fadd_rn (bit-exact).  Replaces one thread per repetition re-reading
+// overlapping windows through L1 (1-D FIR, 8 taps, 2^27 elements: 2.18 -> 0.75 ms).  Wider
+// pavings keep the thread-per-repetition kernel, which measured faster there.
+constexpr int LT_THREADS = 256, LT_WIN = 8192;          // window floats per tile (32 KB + padding)
+
+__device__ __forceinline__ int lt_pad(int k) { return k + (k >> 5); }
+
+__global__ void __launch_bounds__(LT_THREADS) k_line_tiled(const float* __restrict__ x, const float* __restrict__ w,
+                                                           float* __restrict__ y, LineGeom g, int TL,
+                                                           int64_t first, int64_t last, int64_t tile0,
+                                                           int64_t ntiles) {
+  __shared__ float win[LT_WIN + LT_WIN / 32 + 1];
+  __shared__ float ws[32 * 8];
+  const int px = g.px, py = g.py;
+  for (int k = threadIdx.x; k < px * py; k += LT_THREADS) ws[k] = w[k];
+  const int64_t tpl = (g.NL + TL - 1) / TL;                 // tiles per line
+  for (int64_t tt = blockIdx.x; tt < ntiles; tt += gridDim.x) {
+    const int64_t tile = tile0 + tt;
+    const int64_t o = tile / tpl, l0 = (tile - o * tpl) * TL;
+    const int n = (int)(g.NL - l0 < TL ? g.NL - l0 : TL);
+    const int64_t rho0 = o * g.NL + l0;
+    // clip to the launch range
+    const int a = (int)(first > rho0 ? first - rho0 : 0);
+    const int b = (int)(last < rho0 + n - 1 ? last - rho0 + 1 : n);
+    __syncthreads();                                        // previous tile's window consumed
+    if (a < b) {
+      const int64_t c0 = (g.ox + g.sx * (l0 + a)) % g.Sx;
+      const int wl = (int)(g.sx * (b - 1 - a) + px);
+      const float* xr = x + o * g.Sx;
+      for (int k = threadIdx.x; k < wl; k += LT_THREADS) {
+        int64_t c = c0 + k;
+        if (c >= g.Sx) c %= g.Sx;
+        win[lt_pad(k)] = __ldg(xr + c);
+      }
+    }
+    __syncthreads();
+    if (a < b) {
+      float* yr = y + o * g.Sy + g.oy;
+      for (int r = a + threadIdx.x; r < b; r += LT_THREADS) {
+        const int base = (int)(g.sx * (r - a));
+        float* yp = yr + (l0 + r) * g.sy;
+        for (int j = 0; j < py; ++j) {
+          float acc = 0.0f;
+          for (int t = 0; t < px; ++t) acc = __fadd_rn(acc, __fmul_rn(ws[j * px + t], win[lt_pad(base + t)]));
+          yp[j] = acc;
+        }
+      }
+    }
+  }
+}
+
+static bool line_tiled_ok(const LineGeom& g) {
+  return g.inner == 1 && g.sx >= 1 && g.sx <= 4 && !(g.px == 13 && g.py == 3) && !(g.px == 14 && g.py == 4);
+}
+
+static int launch_line_tiled(const LineGeom& g, int64_t first, int64_t count, const float* x, const float* w,
+                             float* y, cudaStream_t s) {
+  const int TL = (int)std::min<int64_t>(LT_WIN, (LT_WIN - g.px) / g.sx + 1);
+  const int64_t last = first + count - 1;
+  const int64_t tpl = (g.NL + TL - 1) / TL;
+  const int64_t o_lo = first / g.NL, o_hi = last / g.NL;
+  const int64_t t_lo = o_lo * tpl + (first - o_lo * g.NL) / TL;
+  const int64_t t_hi = o_hi * tpl + (last - o_hi * g.NL) / TL;
+  const int64_t ntiles = t_hi - t_lo + 1;
+  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)kNumSMs * 8);
+  k_line_tiled<<<grid, LT_THREADS, 0, s>>>(x, w, y, g, TL, first, last, t_lo, ntiles);
+  AOL_LAUNCH_CHECK("k_line_tiled");
+  return AOL_OK;
+}
+
 const char* line_filter_variant(const LineGeom& g) {
   if (hline_stream_ok(g)) return "tile_filter.line_13x3_stream";
   if (vline_stream_ok(g)) return "tile_filter.line_14x4_stream";
   if (g.px == 13 && g.py == 3) return "tile_filter.line_13x3";
   if (g.px == 14 && g.py == 4 && g.inner > 1 && g.sx == 9) return "tile_filter.line_14x4_vstrip";
   if (g.px == 14 && g.py == 4) return "tile_filter.line_14x4";
+  if (line_tiled_ok(g)) return "tile_filter.line_tiled";
   return "tile_filter.line";
 }
 
@@ -266,6 +342,7 @@ int launch_line_filter(const aol_task& t, const LineGeom& g, int64_t first, int6
     AOL_LAUNCH_CHECK("k_line_filter_vstrip");
     return AOL_OK;
   }
+  if (line_tiled_ok(g)) return launch_line_tiled(g, first, count, x, w, y, s);
   if (idx32) {
     if (g.px == 13 && g.py == 3)
       k_line_filter<13, 3, uint32_t><<<grid, 256, 0, s>>>(x, w, y, g, first, count);

@@ -1249,3 +1249,28 @@ def test_tile_sum_plans_vs_oracle(case, plan, dtype, devices):
     from paper_1105_4424_b200 import _capi
     task = _capi.make_task("tile_sum", dtype, [_tiler(tx).bind(tx["array"], (R,)), _tiler(ts).bind(ts["array"], (R,))])
     assert _capi.plan_name(task, 0, R) == plan
+
+
+@pytest.mark.parametrize("outer,S,px,sx,py,sy,ox", [
+    (1, 5000, 8, 1, 1, 1, 0), (1, 4096, 16, 1, 1, 1, 4093), (3, 2000, 32, 1, 1, 1, 7), (2, 8192, 16, 4, 1, 1, 0),
+    (4, 3000, 13, 8, 3, 3, 5), (2, 1000, 5, 2, 8, 8, 999), (1, 10000, 7, 3, 2, 2, 1), (2, 6000, 16, 8, 2, 2, 3)])
+@pytest.mark.parametrize("devices", [1, 3, 5])
+def test_line_tiled_filters_vs_oracle(outer, S, px, sx, py, sy, ox, devices):
+    """Generic horizontal line filters (1-D FIRs, decimating FIRs, wrapping windows, up to 8
+    outputs per repetition) through the shared-memory-windowed kernel: bit-exact vs the oracle,
+    shard starts anywhere inside a line."""
+    NL = (S - 1) // sx + 1 if sx > 1 else S
+    NL = min(NL, S // sx) if sx > 1 else NL
+    Sy = NL * sy if sy >= py else NL * py
+    tx = dict(array=(outer, S), rep=(outer, NL), pattern=(px,), origin=(0, ox), paving=((1, 0), (0, sx)),
+              fitting=((0,), (1,)))
+    ty = dict(array=(outer, Sy), rep=(outer, NL), pattern=(py,), origin=(0, 0), paving=((1, 0), (0, sy)),
+              fitting=((0,), (1,)))
+    t = {"x": tx, "y": ty}
+    w = (np.random.default_rng(px * 10 + py).standard_normal(px * py) / px).astype(np.float32)
+    x = np.random.default_rng(S + px).standard_normal(outer * S).astype(np.float32)
+    want = ("tile_filter.line_13x3" if (px, py) == (13, 3) else
+            "tile_filter.line_tiled" if sx <= 4 else "tile_filter.line")
+    assert _plan([tx, ty]) == want
+    got, ref = _filter_case("tile_filter", t, w, x, devices)
+    assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
