@@ -306,4 +306,96 @@ int launch_stencil_box(const aol_task& t, int64_t first, int64_t count, void* co
   return AOL_OK;
 }
 
+// Block pooling / decimating 2-D filters: x tiler = a KH x KW box (fitting I2) paved by its
+// own size (paving diag(KH, KW)), origin 0, over [H, W] with repetition space [H/KH, W/KW];
+// y the identity over [H/KH, W/KW].  Output (r, c) = sum_{di, dj} w[di*KW + dj] *
+// x[r*KH + di][c*KW + dj], taps row-major (bit-exact).  A thread owns 4 consecutive outputs
+// of one row: KH input rows x 4*KW contiguous floats as float4s, one float4 store.
+template <int KH, int KW>
+__global__ void __launch_bounds__(256) k_box_pool(const float* __restrict__ x, const float* __restrict__ w,
+                                                  float* __restrict__ y, int64_t Ho, int64_t Wo, int64_t W,
+                                                  int64_t first, int64_t last) {
+  float wr[KH * KW];
+#pragma unroll
+  for (int k = 0; k < KH * KW; ++k) wr[k] = __ldg(w + k);
+  const int64_t q0 = first / 4, q1 = last / 4;                    // quads of outputs in range
+  const int64_t wq = Wo / 4;                                      // quads per output row (Wo % 4 == 0)
+  for (int64_t q = q0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q <= q1;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = q / wq, c0 = (q - r * wq) * 4;
+    float v[KH][4 * KW];
+#pragma unroll
+    for (int di = 0; di < KH; ++di) {
+      const float4* xr = reinterpret_cast<const float4*>(x + (r * KH + di) * W + c0 * KW);
+#pragma unroll
+      for (int e = 0; e < KW; ++e) {
+        const float4 t4 = __ldg(xr + e);
+        v[di][4 * e] = t4.x; v[di][4 * e + 1] = t4.y; v[di][4 * e + 2] = t4.z; v[di][4 * e + 3] = t4.w;
+      }
+    }
+    float a[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float acc = 0.0f;
+#pragma unroll
+      for (int di = 0; di < KH; ++di)
+#pragma unroll
+        for (int dj = 0; dj < KW; ++dj) acc = __fadd_rn(acc, __fmul_rn(wr[di * KW + dj], v[di][j * KW + dj]));
+      a[j] = acc;
+    }
+    const int64_t lin = r * Wo + c0;
+    float* yp = y + lin;
+    if (lin >= first && lin + 3 <= last) {
+      *reinterpret_cast<float4*>(yp) = make_float4(a[0], a[1], a[2], a[3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (lin + j >= first && lin + j <= last) yp[j] = a[j];
+    }
+  }
+}
+
+bool box_pool_applicable(const aol_task& t, int& KH, int& KW) {
+  const aol_tiler &tx = t.tilers[0], &ty = t.tilers[1];
+  if (t.dtype != AOL_F32) return false;
+  if (tx.arr_rank != 2 || tx.rep_rank != 2 || tx.pat_rank != 2 || ty.arr_rank != 2 || ty.rep_rank != 2) return false;
+  KH = (int)tx.pattern[0];
+  KW = (int)tx.pattern[1];
+  if (KH < 1 || KH > 4 || KW < 1 || KW > 4 || KH * KW < 2) return false;
+  if (tx.paving[0][0] != KH || tx.paving[0][1] != 0 || tx.paving[1][0] != 0 || tx.paving[1][1] != KW) return false;
+  if (tx.fitting[0][0] != 1 || tx.fitting[0][1] != 0 || tx.fitting[1][0] != 0 || tx.fitting[1][1] != 1) return false;
+  if (tx.origin[0] % tx.array[0] != 0 || tx.origin[1] % tx.array[1] != 0) return false;
+  const int64_t Ho = tx.rep[0], Wo = tx.rep[1];
+  if (tx.array[0] != Ho * KH || tx.array[1] != Wo * KW) return false;
+  if (ty.array[0] != Ho || ty.array[1] != Wo || ty.rep[0] != Ho || ty.rep[1] != Wo) return false;
+  if (ty.paving[0][0] != 1 || ty.paving[0][1] != 0 || ty.paving[1][0] != 0 || ty.paving[1][1] != 1) return false;
+  for (int k = 0; k < ty.pat_rank; ++k)
+    if (ty.pattern[k] != 1) return false;
+  if (ty.origin[0] % ty.array[0] != 0 || ty.origin[1] % ty.array[1] != 0) return false;
+  return Wo % 4 == 0;                                    // float4 quads of outputs, 16 B input rows
+}
+
+int launch_box_pool(const aol_task& t, int64_t first, int64_t count, void* const* ports, cudaStream_t s) {
+  int KH, KW;
+  if (!box_pool_applicable(t, KH, KW)) return fail(AOL_EUNSUPPORTED, "not a block pooling filter");
+  const aol_tiler& tx = t.tilers[0];
+  const float* x = static_cast<const float*>(ports[0]);
+  const float* w = static_cast<const float*>(ports[1]);
+  float* y = static_cast<float*>(ports[2]);
+  if ((uintptr_t)x % 16 || (uintptr_t)y % 16) return fail(AOL_EUNSUPPORTED, "unaligned pooling ports");
+  const int64_t Ho = tx.rep[0], Wo = tx.rep[1], W = tx.array[1];
+  const int64_t last = first + count - 1;
+  const int64_t quads = last / 4 - first / 4 + 1;
+  const unsigned grid = (unsigned)std::min<int64_t>((quads + 255) / 256, (int64_t)kNumSMs * 16);
+  void (*k)(const float*, const float*, float*, int64_t, int64_t, int64_t, int64_t, int64_t) = nullptr;
+#define AOL_POOL(a, b) if (KH == a && KW == b) k = k_box_pool<a, b>;
+  AOL_POOL(1, 2) AOL_POOL(1, 3) AOL_POOL(1, 4) AOL_POOL(2, 1) AOL_POOL(2, 2) AOL_POOL(2, 3) AOL_POOL(2, 4)
+  AOL_POOL(3, 1) AOL_POOL(3, 2) AOL_POOL(3, 3) AOL_POOL(3, 4) AOL_POOL(4, 1) AOL_POOL(4, 2) AOL_POOL(4, 3)
+  AOL_POOL(4, 4)
+#undef AOL_POOL
+  k<<<grid, 256, 0, s>>>(x, w, y, Ho, Wo, W, first, last);
+  AOL_LAUNCH_CHECK("k_box_pool");
+  return AOL_OK;
+}
+
 }  // namespace aol

@@ -1325,6 +1325,8 @@ static int launch_filter_t(const aol_task& t, const DevTiler& tx, const DevTiler
 
 bool stencil_box_applicable(const aol_task& t, int& KH, int& KW);
 int launch_stencil_box(const aol_task& t, int64_t first, int64_t count, void* const* ports, cudaStream_t s);
+bool box_pool_applicable(const aol_task& t, int& KH, int& KW);
+int launch_box_pool(const aol_task& t, int64_t first, int64_t count, void* const* ports, cudaStream_t s);
 struct LineGeom;
 bool line_filter_geometry(const aol_task& t, LineGeom& g);
 const char* line_filter_variant(const LineGeom& g);
@@ -1336,6 +1338,7 @@ struct alignas(16) LineGeomBuf { unsigned char b[256]; };
 const char* filter_plan_name(const aol_task& t) {
   int kh, kw;
   if (stencil_box_applicable(t, kh, kw)) return "tile_filter.stencil_box";
+  if (box_pool_applicable(t, kh, kw)) return "tile_filter.box_pool";
   LineGeomBuf gb;
   if (line_filter_geometry(t, *reinterpret_cast<LineGeom*>(&gb)))
     return line_filter_variant(*reinterpret_cast<LineGeom*>(&gb));
@@ -1348,6 +1351,8 @@ int launch_filter_generic(const aol_task& t, int64_t first, int64_t count, void*
                           cudaStream_t stream) {
   int kh, kw;
   if (stencil_box_applicable(t, kh, kw)) return launch_stencil_box(t, first, count, ports, stream);
+  if (box_pool_applicable(t, kh, kw) && (uintptr_t)ports[0] % 16 == 0 && (uintptr_t)ports[2] % 16 == 0)
+    return launch_box_pool(t, first, count, ports, stream);
   LineGeomBuf gb;
   if (line_filter_geometry(t, *reinterpret_cast<LineGeom*>(&gb)))
     return launch_line_filter(t, *reinterpret_cast<LineGeom*>(&gb), first, count, ports, stream);

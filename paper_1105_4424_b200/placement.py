@@ -215,6 +215,7 @@ KERNEL_STAGING = {
     "tile_copy.tma_stream": "HBM -> TMA 256 B-row boxes -> shared-memory ring (4 x 8 KB, 2 CTAs/SM) -> TMA store -> HBM",
     "tile_copy.tma_transpose": "HBM -> TMA {32 reps, m} boxes (128B swizzle) -> smem transpose -> TMA store -> HBM",
     "tile_copy.stride2": "HBM -> registers (two 16 B source vectors per 4 repetitions) -> HBM (16 B stores)",
+    "tile_filter.box_pool": "HBM -> registers (KH rows x 4*KW floats as float4) -> HBM (float4 stores)",
     "tile_filter.line_tiled": "HBM -> coalesced window per tile of <= 8192 repetitions -> padded smem -> registers -> HBM",
     "tile_sum.rows": "HBM -> cp.async 32x32 tiles (coalesced rows) -> smem ring (4 chunks) -> one ordered add chain per lane",
     "tile_sum.direct": "HBM -> registers (64 loads in flight per repetition) -> ordered add chain",

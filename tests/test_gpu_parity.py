@@ -1274,3 +1274,26 @@ def test_line_tiled_filters_vs_oracle(outer, S, px, sx, py, sy, ox, devices):
     assert _plan([tx, ty]) == want
     got, ref = _filter_case("tile_filter", t, w, x, devices)
     assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
+
+
+@pytest.mark.parametrize("kh,kw", [(2, 2), (3, 3), (4, 4), (2, 4), (1, 2), (4, 1), (3, 2)])
+@pytest.mark.parametrize("devices", [1, 3])
+def test_box_pool_filters_vs_oracle(kh, kw, devices):
+    """Block pooling / decimating 2-D filters (a KH x KW box paved by its own size): the
+    float4 quad kernel, bit-exact vs the oracle; an output width not divisible by 4 takes the
+    generic filter, also exact."""
+    for Ho, Wo, plan in ((40, 96, "tile_filter.box_pool"), (17, 30, None)):
+        H, W = Ho * kh, Wo * kw
+        tx = dict(array=(H, W), rep=(Ho, Wo), pattern=(kh, kw), origin=(0, 0), paving=((kh, 0), (0, kw)),
+                  fitting=((1, 0), (0, 1)))
+        ty = dict(array=(Ho, Wo), rep=(Ho, Wo), pattern=(1,), origin=(0, 0), paving=((1, 0), (0, 1)),
+                  fitting=((0,), (0,)))
+        t = {"x": tx, "y": ty}
+        w = (np.random.default_rng(kh * 10 + kw).standard_normal(kh * kw) / (kh * kw)).astype(np.float32)
+        x = np.random.default_rng(H + W).standard_normal(H * W).astype(np.float32)
+        if plan:
+            assert _plan([tx, ty]) == plan
+        else:
+            assert _plan([tx, ty]) != "tile_filter.box_pool"
+        got, ref = _filter_case("tile_filter", t, w, x, devices)
+        assert np.array_equal(got.view(np.uint32), ref.view(np.uint32)), (kh, kw, Ho, Wo)
