@@ -372,6 +372,42 @@ __global__ void __launch_bounds__(256) k_tile_copy_window(const float* __restric
   }
 }
 
+// Affine copies whose repetition space and pattern each need two strides per side (2-D block
+// tilers: an image cut into b x b blocks written as a dense stream, and back).  Element e of the
+// launch is (rho, iota) = (first + e / P, e % P); each side decomposes rho into (r0, r1) with its
+// own repetition strides and iota into (i0, i1) with its own pattern strides.  V consecutive
+// elements stay inside one row i1 of both patterns, so they move as one V-vector when both
+// sides are contiguous there.
+struct Side2 {
+  int64_t c, A0, A1, B0, B1;
+  FastDiv32 nr1, p1;
+};
+
+__device__ __forceinline__ int64_t side2_off(const Side2& sd, uint32_t rho, uint32_t iota) {
+  uint32_t r0, r1, i0, i1;
+  sd.nr1.divmod(rho, r0, r1);
+  sd.p1.divmod(iota, i0, i1);
+  return sd.c + sd.A0 * r0 + sd.A1 * r1 + sd.B0 * i0 + sd.B1 * i1;
+}
+
+template <typename T, int V>
+__global__ void __launch_bounds__(256) k_tile_copy_affine2d(const T* __restrict__ src, T* __restrict__ dst, Side2 ss,
+                                                            Side2 sd, int64_t first, int64_t ngroups, FastDiv32 pdiv) {
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ngroups; g += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t q, iota;
+    pdiv.divmod((uint32_t)(g * V), q, iota);
+    const uint32_t rho = (uint32_t)(first + q);
+    const int64_t so = side2_off(ss, rho, iota), doff = side2_off(sd, rho, iota);
+    if constexpr (V == 4 && sizeof(T) == 4) {
+      *reinterpret_cast<uint4*>(dst + doff) = __ldg(reinterpret_cast<const uint4*>(src + so));
+    } else if constexpr (V == 2 && sizeof(T) == 4) {
+      *reinterpret_cast<uint2*>(dst + doff) = __ldg(reinterpret_cast<const uint2*>(src + so));
+    } else {
+      dst[doff] = __ldg(src + so);
+    }
+  }
+}
+
 // Row-stride gather through TMA (fp32, P in {8, 16, 32, 64}): a tile of RT repetitions x P
 // pattern elements arrives as RT/32 {32 reps, P} boxes with the 128B swizzle (16-byte chunk c
 // of row i lands at chunk c ^ (i & 7)), is transposed by 128 threads into a staging tile, and
@@ -901,6 +937,46 @@ static bool tma_rows_ok(int64_t P, int64_t As, int64_t Ad, size_t esz) {
 constexpr int64_t kTmaStreamRow = 256;      // bytes per TMA row when a dense copy is streamed as boxes
 constexpr int64_t kTmaMinBytes = 1 << 20;   // below this the single-pass register copy wins (launch-bound)
 
+// Merge adjacent row-major dims whose coefficients nest (coef[j] == coef[j+1] * dims[j+1]) and
+// drop extent-1 dims; true with <= 2 dims left: (outer extent, outer coef, inner extent, inner coef).
+static bool squeeze2(const int64_t* coef, const int64_t* dims, int n, int64_t& d0, int64_t& c0, int64_t& d1,
+                     int64_t& c1) {
+  int64_t ed[AOL_MAX_RANK], ec[AOL_MAX_RANK];
+  int m = 0;
+  for (int j = 0; j < n; ++j) {
+    if (dims[j] == 1) continue;
+    if (m > 0 && ec[m - 1] == coef[j] * dims[j]) {
+      ed[m - 1] *= dims[j];
+      ec[m - 1] = coef[j];
+    } else {
+      ed[m] = dims[j];
+      ec[m] = coef[j];
+      ++m;
+    }
+  }
+  if (m > 2) return false;
+  if (m == 0) { d0 = 1; c0 = 0; d1 = 1; c1 = 0; return true; }
+  if (m == 1) { d0 = 1; c0 = 0; d1 = ed[0]; c1 = ec[0]; return true; }
+  d0 = ed[0]; c0 = ec[0]; d1 = ed[1]; c1 = ec[1];
+  return true;
+}
+
+struct Affine2 {
+  int64_t c, A0, A1, nr1, B0, B1, p1;
+};
+
+static bool affine2_of(const aol_tiler& t, Affine2& o) {
+  Affine a = tiler_affine(t);
+  if (!a.ok) return false;
+  int64_t d0, d1, p0;
+  if (!squeeze2(a.A, t.rep, t.rep_rank, d0, o.A0, o.nr1, o.A1)) return false;
+  if (!squeeze2(a.B, t.pattern, t.pat_rank, p0, o.B0, o.p1, o.B1)) return false;
+  (void)d0;
+  (void)p0;
+  o.c = a.c0;
+  return true;
+}
+
 struct CopyPlan {
   int kind;  // 0 generic, 1 affine1, 2 stream, 3 vector (V elements / thread), 4 transpose
   int64_t cs, As, Bs, cd, Ad, Bd;
@@ -917,8 +993,13 @@ static CopyPlan plan_tile_copy(const aol_tiler& ts, const aol_tiler& td, int64_t
   if (!s.ok || !d.ok) return p;
   int64_t As, Ad, Bs, Bd;
   // the shared repetition space must collapse identically on both sides
-  if (!collapse(s.A, ts.rep, ts.rep_rank, As) || !collapse(d.A, td.rep, td.rep_rank, Ad)) return p;
-  if (!collapse(s.B, ts.pattern, ts.pat_rank, Bs) || !collapse(d.B, td.pattern, td.pat_rank, Bd)) return p;
+  if (!collapse(s.A, ts.rep, ts.rep_rank, As) || !collapse(d.A, td.rep, td.rep_rank, Ad) ||
+      !collapse(s.B, ts.pattern, ts.pat_rank, Bs) || !collapse(d.B, td.pattern, td.pat_rank, Bd)) {
+    // two strides per side still affine: block tilers
+    Affine2 a2s, a2d;
+    if (affine2_of(ts, a2s) && affine2_of(td, a2d)) p.kind = 5;
+    return p;
+  }
   const int64_t P = tiler_pat_total(ts);
   p.kind = 1;
   p.cs = s.c0; p.As = As; p.Bs = P > 1 ? Bs : 0;
@@ -977,6 +1058,7 @@ const char* tile_copy_plan_name(const aol_tiler& ts, const aol_tiler& td, int64_
       if (pl.tma && aligned) return "tile_copy.tma_box";
       return pl.src_vec ? "tile_copy.vec" : "tile_copy.vec_store";
     case 2: return pl.tma ? "tile_copy.tma_stream" : "tile_copy.stream16";
+    case 5: return "tile_copy.affine2d";
     case 1: return pl.As == 2 && pl.Ad == 1 && tiler_pat_total(ts) == 1 && esz == 4 ? "tile_copy.stride2" : "tile_copy.affine";
     default: return "tile_copy.generic";
   }
@@ -1218,6 +1300,42 @@ static int launch_tile_copy_t(const aol_tiler& ts, const aol_tiler& td, int64_t 
       return AOL_OK;
     }
     p.kind = 1;
+  }
+  if (p.kind == 5) {
+    Affine2 a, b;
+    affine2_of(ts, a);
+    affine2_of(td, b);
+    const int64_t nr1s = std::max<int64_t>(1, a.nr1), nr1d = std::max<int64_t>(1, b.nr1);
+    const int64_t p1s = std::max<int64_t>(1, a.p1), p1d = std::max<int64_t>(1, b.p1);
+    if (first + count < ((int64_t)1 << 32) && P < ((int64_t)1 << 31)) {
+      Side2 ss{a.c, a.A0, a.A1, a.B0, a.B1, FastDiv32((uint32_t)nr1s), FastDiv32((uint32_t)p1s)};
+      Side2 sd{b.c, b.A0, b.A1, b.B0, b.B1, FastDiv32((uint32_t)nr1d), FastDiv32((uint32_t)p1d)};
+      // widest vector V: V | both inner pattern extents, unit inner strides, every offset V-aligned
+      int V = 1;
+      for (int v = 4; v >= 2 && sizeof(T) == 4; v /= 2) {
+        auto ok = [&](const Affine2& q, int64_t p1) {
+          return p1 % v == 0 && (q.B1 == 1 || p1 == 1) && q.c % v == 0 && q.A0 % v == 0 && q.A1 % v == 0 &&
+                 q.B0 % v == 0;
+        };
+        if (P % v == 0 && ok(a, p1s) && ok(b, p1d) && (uintptr_t)s % (v * sizeof(T)) == 0 &&
+            (uintptr_t)d % (v * sizeof(T)) == 0) {
+          V = v;
+          break;
+        }
+      }
+      const int64_t groups = count * P / V;
+      const unsigned grid = grid_for(groups, 1024, 16);
+      const FastDiv32 pd((uint32_t)P);
+      if (V == 4)
+        k_tile_copy_affine2d<T, 4><<<grid, 256, 0, stream>>>(s, d, ss, sd, first, groups, pd);
+      else if (V == 2)
+        k_tile_copy_affine2d<T, 2><<<grid, 256, 0, stream>>>(s, d, ss, sd, first, groups, pd);
+      else
+        k_tile_copy_affine2d<T, 1><<<grid, 256, 0, stream>>>(s, d, ss, sd, first, groups, pd);
+      AOL_LAUNCH_CHECK("k_tile_copy_affine2d");
+      return AOL_OK;
+    }
+    p.kind = 0;                                          // 32-bit index space exceeded: generic
   }
   if (p.kind == 1 && sizeof(T) == 4 && P == 1 && p.As == 2 && p.Ad == 1) {
     // stride-2 gather: whole groups of 4 repetitions from 16-byte aligned source/destination

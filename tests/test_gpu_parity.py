@@ -1297,3 +1297,32 @@ def test_box_pool_filters_vs_oracle(kh, kw, devices):
             assert _plan([tx, ty]) != "tile_filter.box_pool"
         got, ref = _filter_case("tile_filter", t, w, x, devices)
         assert np.array_equal(got.view(np.uint32), ref.view(np.uint32)), (kh, kw, Ho, Wo)
+
+
+@pytest.mark.parametrize("bh,bw", [(8, 8), (4, 16), (3, 5), (2, 2)])
+@pytest.mark.parametrize("devices", [1, 3])
+def test_tile_copy_block_tilers_vs_oracle(bh, bw, devices):
+    """2-D block tilers (an image cut into bh x bw blocks, each block a pattern) to a dense
+    stream and back, through the two-stride affine kernel (`tile_copy.affine2d`): bit-exact vs
+    the oracle, with an origin offset and shards starting inside block rows."""
+    from paper_1105_4424_b200 import _capi
+    nbh, nbw = 24, 20
+    H, W = nbh * bh + 3, nbw * bw + 4
+    blk = dict(array=(H, W), rep=(nbh, nbw), pattern=(bh, bw), origin=(2, 4), paving=((bh, 0), (0, bw)),
+               fitting=((1, 0), (0, 1)))
+    P = bh * bw
+    dense = dict(array=(nbh * nbw * P,), rep=(nbh, nbw), pattern=(bh, bw), origin=(0,),
+                 paving=((nbw * P, P),), fitting=((bw, 1),))
+    img = (np.arange(H * W) % (1 << 20)).astype(np.float32) + 1
+    R = nbh * nbw
+    for src, dst, n_out, data in ((blk, dense, R * P, img), (dense, blk, H * W, None)):
+        if data is None:
+            data = (np.arange(R * P) % (1 << 20)).astype(np.float32) + 7
+        ports = {"src": _spec(src, "in", "float32"), "dst": _spec(dst, "out", "float32")}
+        res = _run_tile("tile_copy", {"src": src, "dst": dst}, ports, {"src": data}, devices)
+        ref = orc.run_tile_task("tile_copy", {"src": src, "dst": dst}, {"src": data},
+                                {"dst": (n_out, np.dtype("float32"))}, R, devices)["dst"]
+        assert np.array_equal(res.outputs["p_dst"], ref)
+        task = _capi.make_task("tile_copy", "float32", [_tiler(src).bind(src["array"], (nbh, nbw)),
+                                                        _tiler(dst).bind(dst["array"], (nbh, nbw))])
+        assert _capi.plan_name(task, 0, R) == "tile_copy.affine2d"
