@@ -597,6 +597,68 @@ bool gemm_tf32_applicable(const aol_task& t, void* const* ports) {
   return ((uintptr_t)a % 16 == 0) && ((uintptr_t)b % 16 == 0);
 }
 
+int launch_gemm_tf32(const aol_task& t, int64_t first, int64_t count, void* const* ports, cudaStream_t stream);
+
+// Batched MatMul: a repetition space [B..., M, N] whose last two axes form a canonical GEMM for
+// every leading index (e.g. a[b, m, k], b[b, k, n], c[b, m, n]).  Each batch slice is the same
+// task with a 2-D repetition space [M, N] and the origins advanced by the leading paving
+// columns; slices run as ordinary tcgen05 launches over their share of [first, first+count).
+static bool gemm_slice(const aol_task& t, int64_t batch, aol_task& out) {
+  out = t;
+  const int q = t.tilers[0].rep_rank;
+  for (int i = 0; i < 3; ++i) {
+    const aol_tiler& src = t.tilers[i];
+    aol_tiler& dst = out.tilers[i];
+    if (src.rep_rank != q) return false;
+    // unravel the leading repetition index (row-major over the q-2 leading axes)
+    int64_t lead[AOL_MAX_RANK];
+    int64_t rem = batch;
+    for (int j = q - 3; j >= 0; --j) {
+      lead[j] = rem % src.rep[j];
+      rem /= src.rep[j];
+    }
+    dst.rep_rank = 2;
+    dst.rep[0] = src.rep[q - 2];
+    dst.rep[1] = src.rep[q - 1];
+    for (int j = 2; j < AOL_MAX_RANK; ++j) dst.rep[j] = 0;
+    for (int d = 0; d < src.arr_rank; ++d) {
+      int64_t o = src.origin[d];
+      for (int j = 0; j < q - 2; ++j) o += src.paving[d][j] * lead[j];
+      dst.origin[d] = o;
+      dst.paving[d][0] = src.paving[d][q - 2];
+      dst.paving[d][1] = src.paving[d][q - 1];
+      for (int j = 2; j < AOL_MAX_RANK; ++j) dst.paving[d][j] = 0;
+    }
+  }
+  return true;
+}
+
+bool gemm_batched_applicable(const aol_task& t, void* const* ports) {
+  if (t.dtype != AOL_F32 || t.precision == AOL_PREC_EXACT) return false;
+  const int q = t.tilers[0].rep_rank;
+  if (q < 3 || t.tilers[1].rep_rank != q || t.tilers[2].rep_rank != q) return false;
+  int64_t nb = 1;
+  for (int j = 0; j < q - 2; ++j) nb *= t.tilers[0].rep[j];
+  // every slice must be a TMA-compatible GEMM; checking the first and the last suffices for
+  // affine tilers (the origin moves linearly, the strides do not change)
+  aol_task s0, s1;
+  if (!gemm_slice(t, 0, s0) || !gemm_slice(t, nb - 1, s1)) return false;
+  return gemm_tf32_applicable(s0, ports) && gemm_tf32_applicable(s1, ports);
+}
+
+int launch_gemm_batched(const aol_task& t, int64_t first, int64_t count, void* const* ports, cudaStream_t stream) {
+  const int q = t.tilers[0].rep_rank;
+  const int64_t MN = t.tilers[0].rep[q - 2] * t.tilers[0].rep[q - 1];
+  for (int64_t b = first / MN; b * MN < first + count; ++b) {
+    const int64_t lo = std::max<int64_t>(first, b * MN), hi = std::min<int64_t>(first + count, (b + 1) * MN);
+    aol_task sl;
+    if (!gemm_slice(t, b, sl)) return fail(AOL_EINVAL, "batched matmul slice");
+    const int rc = launch_gemm_tf32(sl, lo - b * MN, hi - lo, ports, stream);
+    if (rc) return rc;
+  }
+  return AOL_OK;
+}
+
 // Split x into tf32 hi (low 13 mantissa bits cleared) and lo = x - hi (exact).
 __global__ void __launch_bounds__(256) k_split_a(const float* __restrict__ A, float* __restrict__ Ap, int64_t rows,
                                                  int64_t K, int64_t sm, int64_t sk, int64_t row0, int64_t pitch) {

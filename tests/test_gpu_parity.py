@@ -1326,3 +1326,45 @@ def test_tile_copy_block_tilers_vs_oracle(bh, bw, devices):
         task = _capi.make_task("tile_copy", "float32", [_tiler(src).bind(src["array"], (nbh, nbw)),
                                                         _tiler(dst).bind(dst["array"], (nbh, nbw))])
         assert _capi.plan_name(task, 0, R) == "tile_copy.affine2d"
+
+
+@pytest.mark.parametrize("batch", [(3,), (2, 3)])
+@pytest.mark.parametrize("devices", [1, 4])
+def test_batched_matmul_tf32_within_bound(batch, devices):
+    """MatMul with leading repetition axes (c[b..., m, n] = a[b..., m, :] . b[b..., :, n]): each
+    batch slice runs as a tcgen05 launch over its share of the range; held to the TF32 bound."""
+    from paper_1105_4424_b200 import _capi
+    M, N, K = 200, 264, 96
+    nb = int(np.prod(batch))
+    q = len(batch)
+    eye = lambda i, n: tuple(1 if j == i else 0 for j in range(n))  # noqa: E731
+    rep = batch + (M, N)
+    R = q + 2
+    ta = dict(array=batch + (M, K), rep=rep, pattern=(K,), origin=(0,) * (q + 2),
+              paving=tuple(eye(i, R) if i < q else (eye(q, R) if i == q else (0,) * R) for i in range(q + 2)),
+              fitting=tuple((1,) if i == q + 1 else (0,) for i in range(q + 2)))
+    tb = dict(array=batch + (K, N), rep=rep, pattern=(K,), origin=(0,) * (q + 2),
+              paving=tuple(eye(i, R) if i < q else ((0,) * R if i == q else eye(q + 1, R)) for i in range(q + 2)),
+              fitting=tuple((1,) if i == q else (0,) for i in range(q + 2)))
+    tc = dict(array=batch + (M, N), rep=rep, pattern=(1,), origin=(0,) * (q + 2),
+              paving=tuple(eye(i, R) for i in range(q + 2)), fitting=tuple((0,) for _ in range(q + 2)))
+    rng = np.random.default_rng(nb)
+    a = rng.standard_normal(nb * M * K).astype(np.float32)
+    b = rng.standard_normal(nb * K * N).astype(np.float32)
+    ports = {"a": _spec(ta, "in", "float32"), "b": _spec(tb, "in", "float32"), "c": _spec(tc, "out", "float32")}
+    c = _run_tile("matmul", {"a": ta, "b": tb, "c": tc}, ports, {"a": a, "b": b}, devices).outputs["p_c"]
+    A = a.reshape(nb, M, K).astype(np.float64)
+    B = b.reshape(nb, K, N).astype(np.float64)
+    C = c.reshape(nb, M, N)
+    for i in range(nb):
+        c64 = A[i] @ B[i]
+        assert np.all(np.abs(C[i] - c64) <= _gemm_bound(A[i], B[i], K)), i
+    bt = [_tiler(d).bind(d["array"], rep) for d in (ta, tb, tc)]
+    task = _capi.make_task("matmul", "float32", bt)
+    t0 = torch.zeros(4, device="cuda")
+    assert _capi.plan_name(task, 0, nb * M * N, [t0.data_ptr()] * 3) == "matmul.tcgen05_tf32_batched"
+    # exact mode keeps the bit-exact generic kernel
+    ex = _run_tile("matmul", {"a": ta, "b": tb, "c": tc}, ports, {"a": a, "b": b}, devices, precision="exact")
+    ref = orc.run_tile_task("matmul", {"a": ta, "b": tb, "c": tc}, {"a": a, "b": b},
+                            {"c": (nb * M * N, np.float32)}, nb * M * N, devices)["c"]
+    assert np.array_equal(ex.outputs["p_c"], ref)
