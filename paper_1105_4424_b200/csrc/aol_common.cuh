@@ -65,6 +65,7 @@ struct FastDiv32 {
 // are the unravel divisors (32-bit fast path when every index fits).
 struct DevTiler {
   int a, q, p, small;           // ranks; small = repetition and pattern totals < 2^31
+  int cheap;                    // every raw coordinate lies in [-2 s_d, 3 s_d): mod by compare/subtract
   int64_t s[AOL_MAX_RANK];      // array shape
   int64_t st[AOL_MAX_RANK];     // row-major array strides
   int64_t o[AOL_MAX_RANK];      // origin reduced mod s
@@ -119,7 +120,19 @@ __device__ __forceinline__ int64_t tiler_offset(const DevTiler& t, int64_t rho, 
 #pragma unroll
     for (int k = 0; k < AOL_MAX_RANK; ++k)
       if (k < t.p) e += t.F[d][k] * i[k];
-    off += emod(e, t.s[d]) * t.st[d];
+    if (t.cheap) {                                  // at most two wraps either way
+      const int64_t sd = t.s[d];
+      if (e >= sd) {
+        e -= sd;
+        if (e >= sd) e -= sd;
+      } else if (e < 0) {
+        e += sd;
+        if (e < 0) e += sd;
+      }
+      off += e * t.st[d];
+    } else {
+      off += emod(e, t.s[d]) * t.st[d];
+    }
   }
   return off;
 }

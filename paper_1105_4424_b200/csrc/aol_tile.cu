@@ -51,21 +51,28 @@ int make_dev_tiler(const aol_tiler& in, DevTiler& out) {
     if (in.pattern[k] < 1) return fail(AOL_EINVAL, "tiler pattern dimensions must be >= 1");
   const double lim = 4.0e18;  // keep every raw coordinate inside int64 (< 2^62)
   int64_t acc = 1;
+  out.cheap = 1;
   for (int d = out.a - 1; d >= 0; --d) {
     out.s[d] = in.array[d];
     out.st[d] = acc;
     acc *= in.array[d];
     out.o[d] = emod_h(in.origin[d], in.array[d]);
     double span = (double)in.array[d];
+    double lo = (double)out.o[d], hi = (double)out.o[d];   // raw coordinate range along d
     for (int j = 0; j < out.q; ++j) {
       out.P[d][j] = in.paving[d][j];
-      span += fabs((double)in.paving[d][j]) * (double)(in.rep[j] - 1);
+      const double v = (double)in.paving[d][j] * (double)(in.rep[j] - 1);
+      span += fabs(v);
+      (v < 0 ? lo : hi) += v;
     }
     for (int k = 0; k < out.p; ++k) {
       out.F[d][k] = in.fitting[d][k];
-      span += fabs((double)in.fitting[d][k]) * (double)(in.pattern[k] - 1);
+      const double v = (double)in.fitting[d][k] * (double)(in.pattern[k] - 1);
+      span += fabs(v);
+      (v < 0 ? lo : hi) += v;
     }
     if (span > lim) return fail(AOL_EINVAL, "tiler coordinates overflow int64");
+    if (lo < -2.0 * (double)in.array[d] || hi >= 3.0 * (double)in.array[d]) out.cheap = 0;
   }
   for (int j = 0; j < out.q; ++j) out.rep[j] = in.rep[j];
   for (int k = 0; k < out.p; ++k) out.pat[k] = in.pattern[k];
@@ -156,14 +163,23 @@ __global__ void k_tiler_offsets(DevTiler t, int64_t first, int64_t count, int64_
     out[e] = tiler_offset(t, first + e / npat, e % npat);
 }
 
-// Generic gather -> scatter: one thread per (rho, iota) element.
+// Generic gather -> scatter: one thread per (rho, iota) element (32-bit split when it fits).
 template <typename T>
-__global__ void k_tile_copy_generic(const T* __restrict__ src, T* __restrict__ dst, DevTiler ts,
-                                    DevTiler td, int64_t first, int64_t count, int64_t npat) {
+__global__ void __launch_bounds__(256) k_tile_copy_generic(const T* __restrict__ src, T* __restrict__ dst,
+                                                           DevTiler ts, DevTiler td, int64_t first, int64_t count,
+                                                           int64_t npat, FastDiv32 pdiv, int small) {
   const int64_t n = count * npat;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t rho = first + e / npat, iota = e % npat;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t rho, iota;
+    if (small) {
+      uint32_t q, r;
+      pdiv.divmod((uint32_t)e, q, r);
+      rho = first + q;
+      iota = r;
+    } else {
+      rho = first + e / npat;
+      iota = e % npat;
+    }
     dst[tiler_offset(td, rho, iota)] = src[tiler_offset(ts, rho, iota)];
   }
 }
@@ -1047,6 +1063,8 @@ static CopyPlan plan_tile_copy(const aol_tiler& ts, const aol_tiler& td, int64_t
   return p;
 }
 
+static bool seam_boxes(const aol_tiler& ts, const aol_tiler& td, int64_t cuts[AOL_MAX_RANK][3], int ncut[AOL_MAX_RANK]);
+
 const char* tile_copy_plan_name(const aol_tiler& ts, const aol_tiler& td, int64_t first, int64_t count,
                                 size_t esz, void* const* ports) {
   const CopyPlan pl = plan_tile_copy(ts, td, first, count, esz);
@@ -1060,7 +1078,12 @@ const char* tile_copy_plan_name(const aol_tiler& ts, const aol_tiler& td, int64_
     case 2: return pl.tma ? "tile_copy.tma_stream" : "tile_copy.stream16";
     case 5: return "tile_copy.affine2d";
     case 1: return pl.As == 2 && pl.Ad == 1 && tiler_pat_total(ts) == 1 && esz == 4 ? "tile_copy.stride2" : "tile_copy.affine";
-    default: return "tile_copy.generic";
+    default: {
+      int64_t cuts[AOL_MAX_RANK][3];
+      int ncut[AOL_MAX_RANK];
+      if (first == 0 && count == tiler_rep_total(ts) && seam_boxes(ts, td, cuts, ncut)) return "tile_copy.seam_boxes";
+      return "tile_copy.generic";
+    }
   }
 }
 
@@ -1185,6 +1208,62 @@ static int launch_tma_transpose(const float* src, float* dst, int64_t count, int
   k<<<grid, 128, smem, stream>>>(ms, md, ntiles);
   AOL_LAUNCH_CHECK("k_tile_copy_tma_transpose");
   return AOL_OK;
+}
+
+// Toroidal copies (shifts, rotations): when every array axis of both tilers is driven by exactly
+// one repetition axis with paving 1 and no pattern extent (pattern total 1), the only wraps are
+// at r_j = s_d - o_d.  Splitting every repetition axis at those seams gives <= 2^q boxes over
+// which both tilers are affine; each box is the same task with its repetition extents and the
+// origins advanced to the box corner, and runs on the affine plans.  Whole-range launches only.
+static bool seam_boxes(const aol_tiler& ts, const aol_tiler& td, int64_t cuts[AOL_MAX_RANK][3], int ncut[AOL_MAX_RANK]) {
+  const int q = ts.rep_rank;
+  if (td.rep_rank != q || tiler_pat_total(ts) != 1) return false;
+  for (int j = 0; j < q; ++j) {
+    cuts[j][0] = 0;
+    ncut[j] = 1;
+  }
+  for (const aol_tiler* t : {&ts, &td}) {
+    for (int d = 0; d < t->arr_rank; ++d) {
+      int jd = -1;
+      for (int j = 0; j < q; ++j)
+        if (t->paving[d][j] != 0) {
+          if (jd >= 0 || t->paving[d][j] != 1) return false;
+          jd = j;
+        }
+      for (int k = 0; k < t->pat_rank; ++k)
+        if (t->fitting[d][k] != 0 && t->pattern[k] > 1) return false;
+      const int64_t sd = t->array[d];
+      const int64_t o = ((t->origin[d] % sd) + sd) % sd;
+      if (jd < 0) continue;                                  // constant coordinate: never wraps
+      if (t->rep[jd] > sd) return false;                     // would wrap more than once
+      const int64_t seam = sd - o;
+      if (o > 0 && seam < t->rep[jd]) {
+        bool have = false;
+        for (int c = 0; c < ncut[jd]; ++c) have = have || cuts[jd][c] == seam;
+        if (!have) {
+          if (ncut[jd] >= 3) return false;
+          cuts[jd][ncut[jd]++] = seam;
+        }
+      }
+    }
+  }
+  for (int j = 0; j < q; ++j)                                // sort the (<= 3) cut points
+    for (int a = 1; a < ncut[j]; ++a)
+      for (int b = a; b > 0 && cuts[j][b] < cuts[j][b - 1]; --b) std::swap(cuts[j][b], cuts[j][b - 1]);
+  int boxes = 1;
+  for (int j = 0; j < q; ++j) boxes *= ncut[j];
+  return boxes > 1;
+}
+
+static aol_tiler box_tiler(const aol_tiler& t, const int64_t lo[AOL_MAX_RANK], const int64_t ext[AOL_MAX_RANK]) {
+  aol_tiler b = t;
+  for (int d = 0; d < t.arr_rank; ++d) {
+    int64_t o = t.origin[d];
+    for (int j = 0; j < t.rep_rank; ++j) o += t.paving[d][j] * lo[j];
+    b.origin[d] = o;
+  }
+  for (int j = 0; j < t.rep_rank; ++j) b.rep[j] = ext[j];
+  return b;
 }
 
 template <typename T>
@@ -1359,12 +1438,40 @@ static int launch_tile_copy_t(const aol_tiler& ts, const aol_tiler& td, int64_t 
     AOL_LAUNCH_CHECK("k_tile_copy_affine");
     return AOL_OK;
   }
+  // toroidal shifts over the whole repetition space: affine boxes between the seams
+  int64_t cuts[AOL_MAX_RANK][3];
+  int ncut[AOL_MAX_RANK];
+  if (p.kind == 0 && first == 0 && count == tiler_rep_total(ts) && seam_boxes(ts, td, cuts, ncut)) {
+    const int q = ts.rep_rank;
+    int idx[AOL_MAX_RANK] = {0, 0, 0, 0};
+    for (;;) {
+      int64_t lo[AOL_MAX_RANK] = {0, 0, 0, 0}, ext[AOL_MAX_RANK] = {0, 0, 0, 0};
+      int64_t n = 1;
+      for (int j = 0; j < q; ++j) {
+        lo[j] = cuts[j][idx[j]];
+        const int64_t hi = idx[j] + 1 < ncut[j] ? cuts[j][idx[j] + 1] : ts.rep[j];
+        ext[j] = hi - lo[j];
+        n *= ext[j];
+      }
+      if (n > 0) {
+        const aol_tiler bs = box_tiler(ts, lo, ext), bd = box_tiler(td, lo, ext);
+        const int rc = launch_tile_copy_t<T>(bs, bd, 0, n, src, dst, stream);
+        if (rc) return rc;
+      }
+      int j = q - 1;
+      while (j >= 0 && ++idx[j] == ncut[j]) idx[j--] = 0;
+      if (j < 0) break;
+    }
+    return AOL_OK;
+  }
   DevTiler dts, dtd;
   int rc = make_dev_tiler(ts, dts);
   if (rc) return rc;
   rc = make_dev_tiler(td, dtd);
   if (rc) return rc;
-  k_tile_copy_generic<T><<<grid_for(count * P, 256), 256, 0, stream>>>(s, d, dts, dtd, first, count, P);
+  const bool small = count * P < ((int64_t)1 << 32) && P < ((int64_t)1 << 32);
+  k_tile_copy_generic<T><<<grid_for(count * P, 256), 256, 0, stream>>>(
+      s, d, dts, dtd, first, count, P, FastDiv32(small ? (uint32_t)P : 1u), small ? 1 : 0);
   AOL_LAUNCH_CHECK("k_tile_copy_generic");
   return AOL_OK;
 }
