@@ -599,6 +599,115 @@ bool gemm_tf32_applicable(const aol_task& t, void* const* ports) {
 
 int launch_gemm_tf32(const aol_task& t, int64_t first, int64_t count, void* const* ports, cudaStream_t stream);
 
+// Exact-order MatMul (precision="exact", or dtypes / alignments the tensor-core path does not
+// take) for canonical GEMM tilers with any strides: a 64x64 output tile per 256-thread CTA, 4x4
+// outputs per thread, K staged through shared memory 16 at a time.  Every output accumulates
+// k = 0, 1, ... with the product and the sum rounded separately (__fmul_rn then __fadd_rn, no
+// FMA) -- the reference spmv order the oracle pins -- so results are bit-identical to the
+// one-thread-per-repetition kernel, at CUDA-core throughput instead of a strided K loop.
+struct GemmStrides {
+  int64_t M, N, K, ca, sam, sak, cb, sbk, sbn, cc, scm, scn;
+};
+
+bool recognise_gemm_strides(const aol_task& t, GemmStrides& g) {
+  const aol_tiler &ta = t.tilers[0], &tb = t.tilers[1], &tc = t.tilers[2];
+  if (ta.rep_rank != 2 || tb.rep_rank != 2 || tc.rep_rank != 2) return false;
+  if (tiler_pat_total(ta) != ta.pattern[ta.pat_rank - 1] || tiler_pat_total(tb) != tb.pattern[tb.pat_rank - 1])
+    return false;
+  Affine a = tiler_affine(ta), b = tiler_affine(tb), c = tiler_affine(tc);
+  if (!a.ok || !b.ok || !c.ok) return false;
+  if (a.A[1] != 0 || b.A[0] != 0) return false;          // a depends on m only, b on n only
+  g.M = ta.rep[0]; g.N = ta.rep[1]; g.K = tiler_pat_total(ta);
+  g.ca = a.c0; g.sam = a.A[0]; g.sak = a.B[ta.pat_rank - 1];
+  g.cb = b.c0; g.sbk = b.B[tb.pat_rank - 1]; g.sbn = b.A[1];
+  g.cc = c.c0; g.scm = c.A[0]; g.scn = c.A[1];
+  return g.M < (1ll << 31) && g.N < (1ll << 31);
+}
+
+bool recognise_gemm_strides(const aol_task& t) {
+  GemmStrides g;
+  return recognise_gemm_strides(t, g);
+}
+
+constexpr int EX_T = 64, EX_K = 16;
+
+template <typename T>
+__device__ __forceinline__ T ex_mac(T acc, T a, T b);
+template <> __device__ __forceinline__ float ex_mac(float acc, float a, float b) { return __fadd_rn(acc, __fmul_rn(a, b)); }
+template <> __device__ __forceinline__ double ex_mac(double acc, double a, double b) { return __dadd_rn(acc, __dmul_rn(a, b)); }
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_gemm_exact(const T* __restrict__ A, const T* __restrict__ B, T* __restrict__ C,
+                                                    GemmStrides g, int64_t m_lo, int64_t first, int64_t last,
+                                                    int n_tiles) {
+  __shared__ T As[EX_K][EX_T + 1];
+  __shared__ T Bs[EX_K][EX_T + 1];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int64_t mt = blockIdx.x / n_tiles, nt = blockIdx.x - mt * n_tiles;
+  const int64_t m0 = m_lo + mt * EX_T, n0 = nt * EX_T;
+  T acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = T(0);
+  for (int64_t k0 = 0; k0 < g.K; k0 += EX_K) {
+    // stage a 64 x 16 slab of A and a 16 x 64 slab of B (zero-padded past the edges: the padded
+    // products are never added to a stored output's chain)
+    for (int e = threadIdx.x; e < EX_T * EX_K; e += 256) {
+      const int r = e / EX_K, kk = e % EX_K;
+      const int64_t m = m0 + r, k = k0 + kk;
+      As[kk][r] = (m < g.M && k < g.K) ? A[g.ca + g.sam * m + g.sak * k] : T(0);
+      const int cidx = e % EX_T, kb = e / EX_T;
+      const int64_t n = n0 + cidx, k2 = k0 + kb;
+      Bs[kb][cidx] = (n < g.N && k2 < g.K) ? B[g.cb + g.sbk * k2 + g.sbn * n] : T(0);
+    }
+    __syncthreads();
+    const int kn = (int)(g.K - k0 < EX_K ? g.K - k0 : EX_K);
+    for (int kk = 0; kk < kn; ++kk) {
+      T a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = ex_mac(acc[i][j], a[i], b[j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t m = m0 + ty * 4 + i;
+    if (m >= g.M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t n = n0 + tx * 4 + j;
+      const int64_t lin = m * g.N + n;
+      if (n < g.N && lin >= first && lin <= last) C[g.cc + g.scm * m + g.scn * n] = acc[i][j];
+    }
+  }
+}
+
+int launch_gemm_exact(const aol_task& t, int64_t first, int64_t count, void* const* ports, cudaStream_t stream) {
+  GemmStrides g;
+  if (!recognise_gemm_strides(t, g)) return AOL_EUNSUPPORTED;
+  if (count <= 0) return AOL_OK;
+  const int64_t last = first + count - 1;
+  const int64_t m_lo = first / g.N, m_hi = last / g.N;
+  const int64_t m_tiles = (m_hi - m_lo + EX_T) / EX_T, n_tiles = (g.N + EX_T - 1) / EX_T;
+  if (m_tiles * n_tiles >= (1ll << 31)) return AOL_EUNSUPPORTED;
+  const unsigned grid = (unsigned)(m_tiles * n_tiles);
+  if (t.dtype == AOL_F32)
+    k_gemm_exact<float><<<grid, 256, 0, stream>>>((const float*)ports[0], (const float*)ports[1], (float*)ports[2], g,
+                                                   m_lo, first, last, (int)n_tiles);
+  else
+    k_gemm_exact<double><<<grid, 256, 0, stream>>>((const double*)ports[0], (const double*)ports[1],
+                                                    (double*)ports[2], g, m_lo, first, last, (int)n_tiles);
+  AOL_LAUNCH_CHECK("k_gemm_exact");
+  return AOL_OK;
+}
+
 // Batched MatMul: a repetition space [B..., M, N] whose last two axes form a canonical GEMM for
 // every leading index (e.g. a[b, m, k], b[b, k, n], c[b, m, n]).  Each batch slice is the same
 // task with a 2-D repetition space [M, N] and the origins advanced by the leading paving

@@ -211,6 +211,7 @@ KERNEL_STAGING = {
                            "ring; accumulators: TMEM 2 x (128 lanes x 256 cols fp32); C: TMEM -> registers -> "
                            "st.global.v4",
     "matmul.generic_exact": "patterns gathered from HBM to registers; pattern offset tables in smem",
+    "matmul.exact_tiled": "64x16 A and 16x64 B slabs in smem; 4x4 outputs per thread in registers (k-ascending, no FMA)",
     "tile_copy.stream16": "HBM -> registers (16 B vectors, streaming hints) -> HBM",
     "tile_copy.tma_stream": "HBM -> TMA 256 B-row boxes -> shared-memory ring (4 x 8 KB, 2 CTAs/SM) -> TMA store -> HBM",
     "tile_copy.tma_transpose": "HBM -> TMA {32 reps, m} boxes (128B swizzle) -> smem transpose -> TMA store -> HBM",

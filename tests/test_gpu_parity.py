@@ -244,7 +244,7 @@ def test_matmul_tf32_within_stated_bound(M, N, K, devices):
     assert np.linalg.norm(c - c64) / np.linalg.norm(c64) < 2e-3
     bt = [_tiler(g[k]).bind(g[k]["array"], (M, N)) for k in "abc"]
     task = _capi.make_task("matmul", "float32", bt)
-    expect = "matmul.tcgen05_tf32" if (K % 4 == 0 and N % 4 == 0) else "matmul.generic_exact"
+    expect = "matmul.tcgen05_tf32" if (K % 4 == 0 and N % 4 == 0) else "matmul.exact_tiled"
     ta = torch.zeros(4, device="cuda")
     assert _capi.plan_name(task, 0, M * N, [ta.data_ptr()] * 3) == expect
 

@@ -47,7 +47,7 @@ def test_validate_and_plan_without_gpu():
     g = orc.gemm_tilers(64, 64, 32)
     task = _capi.make_task("matmul", "float32", [_bt(g[k]) for k in "abc"])
     _capi.validate(task)
-    assert _capi.plan_name(task, 0, 64 * 64) == "matmul.generic_exact"      # no ports -> no TMA check
+    assert _capi.plan_name(task, 0, 64 * 64) == "matmul.exact_tiled"        # no ports -> no TMA check
     bad = _capi.make_task("matmul", "float32", [_bt(g[k]) for k in "ab"])
     with pytest.raises(_capi.AolError, match="tilers"):
         _capi.validate(bad)
