@@ -1,2 +1,3 @@
-python -m pytest tests/test_gpu_parity.py -x -q -k "matmul or golden or random_tilers" > gpurun_out/pytest_ex.log 2>&1; echo pytest=$?
-timeout 600 python tools/time_exact.py > gpurun_out/exact.log 2>&1; echo a=$?
+python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?
+python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; echo bench=$?
