@@ -66,6 +66,7 @@ struct FastDiv32 {
 struct DevTiler {
   int a, q, p, small;           // ranks; small = repetition and pattern totals < 2^31
   int cheap;                    // every raw coordinate lies in [-2 s_d, 3 s_d): mod by compare/subtract
+  int fits32;                   // small && cheap && every raw coordinate and offset fits in int32
   int64_t s[AOL_MAX_RANK];      // array shape
   int64_t st[AOL_MAX_RANK];     // row-major array strides
   int64_t o[AOL_MAX_RANK];      // origin reduced mod s
@@ -133,6 +134,48 @@ __device__ __forceinline__ int64_t tiler_offset(const DevTiler& t, int64_t rho, 
     } else {
       off += emod(e, t.s[d]) * t.st[d];
     }
+  }
+  return off;
+}
+
+// 32-bit form of tiler_offset (DevTiler::fits32): the same Appendix-A arithmetic in int32 --
+// one IMAD per term instead of a 64-bit multiply sequence; the generic kernels are integer-bound.
+template <int A, int Q, int P>
+__device__ __forceinline__ int32_t tiler_offset32(const DevTiler& t, uint32_t rho, uint32_t iota) {
+  int32_t r[Q > 0 ? Q : 1], i[P > 0 ? P : 1];
+#pragma unroll
+  for (int j = Q - 1; j >= 1; --j) {
+    uint32_t qv, rv;
+    t.rep_div[j].divmod(rho, qv, rv);
+    r[j] = (int32_t)rv;
+    rho = qv;
+  }
+  r[0] = (int32_t)rho;
+#pragma unroll
+  for (int k = P - 1; k >= 1; --k) {
+    uint32_t qv, rv;
+    t.pat_div[k].divmod(iota, qv, rv);
+    i[k] = (int32_t)rv;
+    iota = qv;
+  }
+  i[0] = (int32_t)iota;
+  int32_t off = 0;
+#pragma unroll
+  for (int d = 0; d < A; ++d) {
+    int32_t e = (int32_t)t.o[d];
+#pragma unroll
+    for (int j = 0; j < Q; ++j) e += (int32_t)t.P[d][j] * r[j];
+#pragma unroll
+    for (int k = 0; k < P; ++k) e += (int32_t)t.F[d][k] * i[k];
+    const int32_t sd = (int32_t)t.s[d];
+    if (e >= sd) {
+      e -= sd;
+      if (e >= sd) e -= sd;
+    } else if (e < 0) {
+      e += sd;
+      if (e < 0) e += sd;
+    }
+    off += e * (int32_t)t.st[d];
   }
   return off;
 }

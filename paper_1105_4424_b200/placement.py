@@ -215,6 +215,7 @@ KERNEL_STAGING = {
     "tile_copy.stream16": "HBM -> registers (16 B vectors, streaming hints) -> HBM",
     "tile_copy.tma_stream": "HBM -> TMA 256 B-row boxes -> shared-memory ring (4 x 8 KB, 2 CTAs/SM) -> TMA store -> HBM",
     "tile_copy.tma_transpose": "HBM -> TMA {32 reps, m} boxes (128B swizzle) -> smem transpose -> TMA store -> HBM",
+    "tile_copy.generic": "32-bit compile-time-rank index arithmetic when it fits; registers (4 elements in flight)",
     "tile_copy.seam_boxes": "split at the wrap seams into affine boxes, each on the affine / affine2d register paths",
     "tile_copy.affine2d": "HBM -> registers (V-element vectors along the inner pattern row) -> HBM",
     "tile_copy.stride2": "HBM -> registers (two 16 B source vectors per 4 repetitions) -> HBM (16 B stores)",
