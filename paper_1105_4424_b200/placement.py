@@ -215,7 +215,6 @@ KERNEL_STAGING = {
     "tile_copy.stream16": "HBM -> registers (16 B vectors, streaming hints) -> HBM",
     "tile_copy.tma_stream": "HBM -> TMA 256 B-row boxes -> shared-memory ring (4 x 8 KB, 2 CTAs/SM) -> TMA store -> HBM",
     "tile_copy.tma_transpose": "HBM -> TMA {32 reps, m} boxes (128B swizzle) -> smem transpose -> TMA store -> HBM",
-    "tile_copy.generic": "32-bit compile-time-rank index arithmetic when it fits; registers (4 elements in flight)",
     "tile_copy.seam_boxes": "split at the wrap seams into affine boxes, each on the affine / affine2d register paths",
     "tile_copy.affine2d": "HBM -> registers (V-element vectors along the inner pattern row) -> HBM",
     "tile_copy.stride2": "HBM -> registers (two 16 B source vectors per 4 repetitions) -> HBM (16 B stores)",
@@ -228,7 +227,7 @@ KERNEL_STAGING = {
     "tile_copy.vec": "HBM -> registers (V-element vectors) -> HBM",
     "tile_copy.vec_store": "HBM -> registers (strided scalars) -> HBM (V-element vector stores)",
     "tile_copy.affine": "HBM -> registers -> HBM (4-way unrolled scalars)",
-    "tile_copy.generic": "HBM -> registers -> HBM (full index function)",
+    "tile_copy.generic": "HBM -> registers -> HBM (full index function; 32-bit compile-time-rank form, 4 in flight, when it fits)",
     "tile_filter.stencil_box": "coefficients: smem broadcast; (4+KH-1) x 6 input window: registers; outputs float4",
     "tile_filter.line_13x3_stream": "x rows: HBM -> cp.async.bulk -> 8-stage smem ring (mbarriers); 16-float window: "
                                     "ld.shared.v4 -> registers; outputs HBM",
