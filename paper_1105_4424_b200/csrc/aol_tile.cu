@@ -761,14 +761,14 @@ __global__ void __launch_bounds__(256) k_filter_generic(const T* __restrict__ x,
     int64_t bx[AOL_MAX_RANK], by[AOL_MAX_RANK];
     tiler_base_raw(tx, rho, bx);
     tiler_base_raw(ty, rho, by);
+#pragma unroll
+    for (int d = 0; d < AOL_MAX_RANK; ++d) {   // a window one period away is still whole
+      if (d < tx.a) bx[d] = emod(bx[d], tx.s[d]);
+      if (d < ty.a) by[d] = emod(by[d], ty.s[d]);
+    }
     int64_t xoff, yoff;
     const bool xfree = wrap_free(tx, sx, bx, xoff);
     const bool yfree = wrap_free(ty, sy, by, yoff);
-    if (!xfree) {
-#pragma unroll
-      for (int d = 0; d < AOL_MAX_RANK; ++d)
-        if (d < tx.a) bx[d] = emod(bx[d], tx.s[d]);
-    }
     T acc[MAXO];
 #pragma unroll
     for (int j = 0; j < MAXO; ++j) acc[j] = T(0);
@@ -805,11 +805,205 @@ __global__ void __launch_bounds__(256) k_filter_generic(const T* __restrict__ x,
         if (j < py) y[yoff + oy[j]] = acc[j];
     } else {
 #pragma unroll
-      for (int d = 0; d < AOL_MAX_RANK; ++d)
-        if (d < ty.a) by[d] = emod(by[d], ty.s[d]);
-#pragma unroll
       for (int j = 0; j < MAXO; ++j)
         if (j < py) y[table_offset(ty, by, fy, j)] = acc[j];
+    }
+  }
+}
+
+// ---- 32-bit batched form (both tilers fits32, one shared repetition space, indices < 2^31) ----
+// A warp covers 32*R consecutive repetitions; lane l takes rho0 + l + 32k (k < R), so each load
+// instruction of the warp walks one run of the array while the R repetitions of a lane share one
+// unravel, one window check and every weight read.  Same pattern order and rounding as
+// k_filter_generic: y_pat[j] = sum_i w[j, i] * x_pat[i], i ascending, mul then add.
+__device__ __forceinline__ int32_t wrap2(int32_t e, int32_t s) {   // raw coordinate in [-2s, 3s)
+  if (e >= s) {
+    e -= s;
+    if (e >= s) e -= s;
+  } else if (e < 0) {
+    e += s;
+    if (e < 0) e += s;
+  }
+  return e;
+}
+
+template <int Q>
+__device__ __forceinline__ void base32(const DevTiler& t, const int32_t r[Q], int32_t b[AOL_MAX_RANK]) {
+#pragma unroll
+  for (int d = 0; d < AOL_MAX_RANK; ++d) {
+    int32_t e = 0;
+    if (d < t.a) {
+      e = (int32_t)t.o[d];
+#pragma unroll
+      for (int j = 0; j < Q; ++j) e += (int32_t)t.P[d][j] * r[j];
+    }
+    b[d] = e;
+  }
+}
+
+// base reduced into [0, s_d) (raw bases lie in [-2s, 3s)): the window test and flat offsets use it
+__device__ __forceinline__ void reduce32(const DevTiler& t, const int32_t b[AOL_MAX_RANK], int32_t c[AOL_MAX_RANK]) {
+#pragma unroll
+  for (int d = 0; d < AOL_MAX_RANK; ++d) c[d] = d < t.a ? wrap2(b[d], (int32_t)t.s[d]) : 0;
+}
+
+// window of the repetition whose base is b + k*step (k in [0, kmax]) stays inside the array:
+// linear in k, so the two ends decide
+__device__ __forceinline__ bool window_free32(const DevTiler& t, const PatSpan& sp, const int32_t b[AOL_MAX_RANK],
+                                              const int32_t step[AOL_MAX_RANK], int kmax) {
+  bool ok = true;
+#pragma unroll
+  for (int d = 0; d < AOL_MAX_RANK; ++d) {
+    if (d >= t.a) break;
+    const int32_t e = b[d] + kmax * step[d];
+    const int32_t lo = min(b[d], e), hi = max(b[d], e);
+    ok = ok && lo + (int32_t)sp.lo[d] >= 0 && hi + (int32_t)sp.hi[d] < (int32_t)t.s[d];
+  }
+  return ok;
+}
+
+__device__ __forceinline__ int32_t flat32(const DevTiler& t, const int32_t b[AOL_MAX_RANK]) {
+  int32_t o = 0;
+#pragma unroll
+  for (int d = 0; d < AOL_MAX_RANK; ++d)
+    if (d < t.a) o += b[d] * (int32_t)t.st[d];
+  return o;
+}
+
+// element i of a (possibly wrapping) window: raw base + raw pattern coordinate, reduced per dim
+__device__ __forceinline__ int32_t wrapped32(const DevTiler& t, const int32_t b[AOL_MAX_RANK], const int32_t* rc,
+                                             int i) {
+  int32_t o = 0;
+#pragma unroll
+  for (int d = 0; d < AOL_MAX_RANK; ++d)
+    if (d < t.a) o += wrap2(b[d] + rc[i * t.a + d], (int32_t)t.s[d]) * (int32_t)t.st[d];
+  return o;
+}
+
+template <typename T>
+__device__ __forceinline__ T mul_add_rn(T acc, T w, T x) {
+  if constexpr (sizeof(T) == 4) return __fadd_rn(acc, __fmul_rn(w, x));
+  else return __dadd_rn(acc, __dmul_rn(w, x));
+}
+
+template <typename T, int MAXO, int R, int Q>
+__global__ void __launch_bounds__(256) k_filter_batched32(const T* __restrict__ x, const T* __restrict__ w,
+                                                          T* __restrict__ y, DevTiler tx, DevTiler ty, PatSpan sx,
+                                                          PatSpan sy, int32_t first, int32_t count, int px,
+                                                          int py) {
+  extern __shared__ __align__(16) unsigned char fsm[];
+  T* ws = reinterpret_cast<T*>(fsm);
+  int32_t* ox = reinterpret_cast<int32_t*>(ws + px * py);   // raw flat pattern offsets
+  int32_t* oy = ox + px;
+  int32_t* rx = oy + py;                                     // raw per-dim pattern coordinates
+  int32_t* ry = rx + px * tx.a;
+  for (int k = threadIdx.x; k < px * py; k += blockDim.x) ws[k] = w[k];
+  for (int k = threadIdx.x; k < px + py; k += blockDim.x) {
+    const bool isx = k < px;
+    const DevTiler& t = isx ? tx : ty;
+    const int kk = isx ? k : k - px;
+    int64_t i[AOL_MAX_RANK];
+    unravel(t, false, kk, i);
+    int32_t o = 0;
+    for (int d = 0; d < t.a; ++d) {
+      int32_t e = 0;
+      for (int m = 0; m < t.p; ++m) e += (int32_t)t.F[d][m] * (int32_t)i[m];
+      (isx ? rx : ry)[kk * t.a + d] = e;
+      o += e * (int32_t)t.st[d];
+    }
+    (isx ? ox : oy)[kk] = o;
+  }
+  __syncthreads();
+  int32_t stx[AOL_MAX_RANK], sty[AOL_MAX_RANK];   // base step between a lane's repetitions
+#pragma unroll
+  for (int d = 0; d < AOL_MAX_RANK; ++d) {
+    stx[d] = d < tx.a ? 32 * (int32_t)tx.P[d][Q - 1] : 0;
+    sty[d] = d < ty.a ? 32 * (int32_t)ty.P[d][Q - 1] : 0;
+  }
+  const int32_t nl = (int32_t)tx.rep[Q - 1];
+  const int lane = threadIdx.x & 31;
+  const int32_t stride = gridDim.x * 256 * R;
+  for (int32_t c = blockIdx.x * 256 * R + (threadIdx.x >> 5) * 32 * R + lane; c < count; c += stride) {
+    int32_t r[Q];
+    {
+      uint32_t v = (uint32_t)(first + c);
+#pragma unroll
+      for (int j = Q - 1; j >= 1; --j) {
+        uint32_t qv, rv;
+        tx.rep_div[j].divmod(v, qv, rv);
+        r[j] = (int32_t)rv;
+        v = qv;
+      }
+      r[0] = (int32_t)v;
+    }
+    int32_t bx[AOL_MAX_RANK], by[AOL_MAX_RANK], cx[AOL_MAX_RANK], cy[AOL_MAX_RANK];
+    base32<Q>(tx, r, bx);
+    base32<Q>(ty, r, by);
+    reduce32(tx, bx, cx);
+    reduce32(ty, by, cy);
+    const bool run = r[Q - 1] + 32 * (R - 1) < nl && c + 32 * (R - 1) < count;
+    if (run && window_free32(tx, sx, cx, stx, R - 1) && window_free32(ty, sy, cy, sty, R - 1)) {
+      const int32_t xo = flat32(tx, cx), yo = flat32(ty, cy);
+      const int32_t dx = flat32(tx, stx), dy = flat32(ty, sty);
+      T acc[R][MAXO];
+#pragma unroll
+      for (int k = 0; k < R; ++k)
+#pragma unroll
+        for (int j = 0; j < MAXO; ++j) acc[k][j] = T(0);
+#pragma unroll 4
+      for (int i = 0; i < px; ++i) {
+        T xv[R];
+        const int32_t oi = xo + ox[i];
+#pragma unroll
+        for (int k = 0; k < R; ++k) xv[k] = __ldg(x + oi + k * dx);
+#pragma unroll
+        for (int j = 0; j < MAXO; ++j)
+          if (j < py) {
+            const T wv = ws[j * px + i];
+#pragma unroll
+            for (int k = 0; k < R; ++k) acc[k][j] = mul_add_rn(acc[k][j], wv, xv[k]);
+          }
+      }
+#pragma unroll
+      for (int k = 0; k < R; ++k)
+#pragma unroll
+        for (int j = 0; j < MAXO; ++j)
+          if (j < py) y[yo + k * dy + oy[j]] = acc[k][j];
+      continue;
+    }
+    // one repetition at a time (window wraps, or the lane's run leaves the repetition row)
+    for (int k = 0; k < R; ++k) {
+      const int32_t e = c + 32 * k;
+      if (e >= count) break;
+      if (k > 0) {
+        uint32_t v = (uint32_t)(first + e);
+#pragma unroll
+        for (int j = Q - 1; j >= 1; --j) {
+          uint32_t qv, rv;
+          tx.rep_div[j].divmod(v, qv, rv);
+          r[j] = (int32_t)rv;
+          v = qv;
+        }
+        r[0] = (int32_t)v;
+        base32<Q>(tx, r, bx);
+        base32<Q>(ty, r, by);
+        reduce32(tx, bx, cx);
+        reduce32(ty, by, cy);
+      }
+      const bool xf = window_free32(tx, sx, cx, stx, 0), yf = window_free32(ty, sy, cy, sty, 0);
+      const int32_t xo = flat32(tx, cx), yo = flat32(ty, cy);
+      T acc[MAXO];
+#pragma unroll
+      for (int j = 0; j < MAXO; ++j) acc[j] = T(0);
+      for (int i = 0; i < px; ++i) {
+        const T xv = __ldg(x + (xf ? xo + ox[i] : wrapped32(tx, bx, rx, i)));
+#pragma unroll
+        for (int j = 0; j < MAXO; ++j)
+          if (j < py) acc[j] = mul_add_rn(acc[j], ws[j * px + i], xv);
+      }
+#pragma unroll
+      for (int j = 0; j < MAXO; ++j)
+        if (j < py) y[yf ? yo + oy[j] : wrapped32(ty, by, ry, j)] = acc[j];
     }
   }
 }
@@ -1600,6 +1794,45 @@ static int launch_filter_t(const aol_task& t, const DevTiler& tx, const DevTiler
   return AOL_OK;
 }
 
+// both tilers 32-bit safe over one repetition space, range inside int32
+static bool filter_batched_ok(const DevTiler& tx, const DevTiler& ty, int64_t first, int64_t count) {
+  static const bool off = getenv("AOL_FILTER_WIDE") != nullptr;   // diagnostic: the int64 kernel
+  if (off || !tx.fits32 || !ty.fits32 || tx.q != ty.q || first + count >= ((int64_t)1 << 31)) return false;
+  for (int j = 0; j < tx.q; ++j)
+    if (tx.rep[j] != ty.rep[j]) return false;
+  return true;
+}
+
+template <typename T, int MAXO, int R, int Q>
+static int launch_filter_b32(const aol_task& t, const DevTiler& tx, const DevTiler& ty, int64_t first,
+                              int64_t count, int px, int py, void* const* ports, cudaStream_t stream) {
+  const size_t smem = (size_t)px * py * sizeof(T) + ((size_t)px + py + (size_t)px * tx.a + (size_t)py * ty.a) * 4;
+  auto kern = k_filter_batched32<T, MAXO, R, Q>;
+  if (smem > 48 * 1024)
+    AOL_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t per = 256 * R;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((count + per - 1) / per, (int64_t)kNumSMs * 8));
+  kern<<<grid, 256, smem, stream>>>((const T*)ports[0], (const T*)ports[1], (T*)ports[2], tx, ty,
+                                    pattern_span(t.tilers[0]), pattern_span(t.tilers[1]), (int32_t)first,
+                                    (int32_t)count, px, py);
+  return AOL_OK;
+}
+
+template <typename T, int MAXO, int R>
+static int launch_filter_b32_q(const aol_task& t, const DevTiler& tx, const DevTiler& ty, int64_t first,
+                               int64_t count, int px, int py, void* const* ports, cudaStream_t stream) {
+  int rc;
+  switch (tx.q) {
+    case 1: rc = launch_filter_b32<T, MAXO, R, 1>(t, tx, ty, first, count, px, py, ports, stream); break;
+    case 2: rc = launch_filter_b32<T, MAXO, R, 2>(t, tx, ty, first, count, px, py, ports, stream); break;
+    case 3: rc = launch_filter_b32<T, MAXO, R, 3>(t, tx, ty, first, count, px, py, ports, stream); break;
+    default: rc = launch_filter_b32<T, MAXO, R, 4>(t, tx, ty, first, count, px, py, ports, stream); break;
+  }
+  if (rc) return rc;
+  AOL_LAUNCH_CHECK("k_filter_batched32");
+  return AOL_OK;
+}
+
 bool stencil_box_applicable(const aol_task& t, int& KH, int& KW);
 int launch_stencil_box(const aol_task& t, int64_t first, int64_t count, void* const* ports, cudaStream_t s);
 bool box_pool_applicable(const aol_task& t, int& KH, int& KW);
@@ -1643,6 +1876,13 @@ int launch_filter_generic(const aol_task& t, int64_t first, int64_t count, void*
   const bool f32 = t.dtype == AOL_F32;
   if (f32 && px <= 16 && py <= 4 && contiguous_pattern(t.tilers[0]))
     return launch_filter_t<float, 4, true>(t, tx, ty, first, count, (int)px, (int)py, ports, stream);
+  if (filter_batched_ok(tx, ty, first, count)) {
+    if (py <= 4)
+      return f32 ? launch_filter_b32_q<float, 4, 4>(t, tx, ty, first, count, (int)px, (int)py, ports, stream)
+                 : launch_filter_b32_q<double, 4, 4>(t, tx, ty, first, count, (int)px, (int)py, ports, stream);
+    return f32 ? launch_filter_b32_q<float, 16, 2>(t, tx, ty, first, count, (int)px, (int)py, ports, stream)
+               : launch_filter_b32_q<double, 16, 2>(t, tx, ty, first, count, (int)px, (int)py, ports, stream);
+  }
   if (py <= 4)
     return f32 ? launch_filter_t<float, 4, false>(t, tx, ty, first, count, (int)px, (int)py, ports, stream)
                : launch_filter_t<double, 4, false>(t, tx, ty, first, count, (int)px, (int)py, ports, stream);

@@ -1391,3 +1391,56 @@ def test_tile_copy_toroidal_shift_vs_oracle(shape, origin, devices):
     assert np.array_equal(res.outputs["p_dst"], ref)
     task = _capi.make_task("tile_copy", "float32", [_tiler(src).bind(shape, shape), _tiler(dst).bind(shape, shape)])
     assert _capi.plan_name(task, 0, n) == ("tile_copy.seam_boxes" if a > 1 else "tile_copy.generic")
+
+
+def _generic_filter_cases():
+    H, W = 70, 300
+    return [
+        # 3x3 stride-2 window on a torus (origin -1, -1): wrapping rows/columns at both edges
+        ("s2_torus", dict(array=(H, W), rep=(H // 2, W // 2), pattern=(3, 3), origin=(H - 1, W - 1),
+                          paving=((2, 0), (0, 2)), fitting=((1, 0), (0, 1))),
+         dict(array=(H // 2, W // 2), rep=(H // 2, W // 2), pattern=(1,), origin=(0, 0),
+              paving=((1, 0), (0, 1)), fitting=((0,), (0,)))),
+        # 4x4 window -> 2x2 outputs (16 taps, 4 outputs per repetition)
+        ("win4_out2", dict(array=(H - 2, W), rep=((H - 2) // 4, W // 4), pattern=(4, 4), origin=(0, 0),
+                           paving=((4, 0), (0, 4)), fitting=((1, 0), (0, 1))),
+         dict(array=((H - 2) // 2, W // 2), rep=((H - 2) // 4, W // 4), pattern=(2, 2), origin=(0, 0),
+              paving=((2, 0), (0, 2)), fitting=((1, 0), (0, 1)))),
+        # 3-D repetition space, column (strided) pattern, 6 outputs written along a wrapping row
+        ("rank3_cols", dict(array=(4, 40, 50), rep=(4, 10, 50), pattern=(5,), origin=(0, 1, 0),
+                            paving=((1, 0, 0), (0, 4, 0), (0, 0, 1)), fitting=((0,), (1,), (0,))),
+         dict(array=(4, 10, 300), rep=(4, 10, 50), pattern=(6,), origin=(0, 0, 7),
+              paving=((1, 0, 0), (0, 1, 0), (0, 0, 6)), fitting=((0,), (0,), (1,)))),
+        # diagonal (non-separable) 2-D pattern fitting, negative paving along columns
+        ("diag_neg", dict(array=(64, 96), rep=(60, 90), pattern=(3, 2), origin=(2, 5),
+                          paving=((1, 0), (0, -1)), fitting=((1, 1), (1, -1))),
+         dict(array=(60, 90), rep=(60, 90), pattern=(1,), origin=(0, 0),
+              paving=((1, 0), (0, 1)), fitting=((0,), (0,)))),
+    ]
+
+
+@pytest.mark.parametrize("case", [c[0] for c in _generic_filter_cases()])
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+@pytest.mark.parametrize("devices", [1, 3])
+@pytest.mark.parametrize("wide", [False, True])
+def test_generic_filter_batched32_vs_oracle(case, dtype, devices, wide, monkeypatch):
+    """Filters no specialised kernel covers (strided windows on a torus, several outputs per
+    repetition, rank-3 repetition spaces, diagonal fittings, negative pavings): the 32-bit batched
+    kernel (default) and the int64 kernel (AOL_FILTER_WIDE) bit-exact vs the oracle."""
+    if wide:
+        monkeypatch.setenv("AOL_FILTER_WIDE", "1")
+    _, tx, ty = next(c for c in _generic_filter_cases() if c[0] == case)
+    assert _plan([tx, ty], dtype) == "tile_filter.generic"
+    np_dt = np.dtype(dtype)
+    px = int(np.prod(tx["pattern"]))
+    py = int(np.prod(ty["pattern"]))
+    nx, ny = int(np.prod(tx["array"])), int(np.prod(ty["array"]))
+    w = (np.random.default_rng(px + py).standard_normal(px * py) / px).astype(np_dt)
+    x = np.random.default_rng(nx).standard_normal(nx).astype(np_dt)
+    t = {"x": tx, "y": ty}
+    R = int(np.prod(tx["rep"]))
+    ports = {"x": _spec(tx, "in", dtype), "w": f"in {dtype} [{w.size}]", "y": _spec(ty, "out", dtype)}
+    res = _run_tile("tile_filter", t, ports, {"x": x, "w": w}, devices)
+    ref = orc.run_tile_task("tile_filter", t, {"x": x, "w": w}, {"y": (ny, np_dt)}, R, devices)["y"]
+    got = res.outputs["p_y"]
+    assert got.dtype == np_dt and np.array_equal(got.view(np.uint8), ref.view(np.uint8)), (case, dtype)

@@ -46,3 +46,7 @@ run("2-D 2x2 downsample", (H, W), Tiler((0, 0), ((2, 0), (0, 2)), ((1, 0), (0, 1
     Tiler((0, 0), ((1, 0), (0, 1)), ((0,), (0,)), (1,)), (H // 2, W // 2), 4, 1)
 run("line 16 taps along rows /8", (64, 2048, 2048), Tiler((0, 0, 0), ((1, 0, 0), (0, 1, 0), (0, 0, 8)), ((0,), (0,), (1,)), (16,)),
     (64, 2048, 256 * 2), Tiler((0, 0, 0), ((1, 0, 0), (0, 1, 0), (0, 0, 2)), ((0,), (0,), (1,)), (2,)), (64, 2048, 256), 16, 2)
+run("2-D 3x3 stride 2 (torus)", (H, W), Tiler((H - 1, W - 1), ((2, 0), (0, 2)), ((1, 0), (0, 1)), (3, 3)),
+    (H // 2, W // 2), Tiler((0, 0), ((1, 0), (0, 1)), ((0,), (0,)), (1,)), (H // 2, W // 2), 9, 1)
+run("2-D 2x2 outputs per 4x4 window", (H, W), Tiler((0, 0), ((4, 0), (0, 4)), ((1, 0), (0, 1)), (4, 4)),
+    (H // 2, W // 2), Tiler((0, 0), ((2, 0), (0, 2)), ((1, 0), (0, 1)), (2, 2)), (H // 4, W // 4), 16, 4)
