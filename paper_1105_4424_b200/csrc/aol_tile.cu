@@ -1796,7 +1796,7 @@ static int launch_filter_t(const aol_task& t, const DevTiler& tx, const DevTiler
 
 // both tilers 32-bit safe over one repetition space, range inside int32
 static bool filter_batched_ok(const DevTiler& tx, const DevTiler& ty, int64_t first, int64_t count) {
-  static const bool off = getenv("AOL_FILTER_WIDE") != nullptr;   // diagnostic: the int64 kernel
+  const bool off = getenv("AOL_FILTER_WIDE") != nullptr;   // diagnostic: the int64 / line_tiled kernels
   if (off || !tx.fits32 || !ty.fits32 || tx.q != ty.q || first + count >= ((int64_t)1 << 31)) return false;
   for (int j = 0; j < tx.q; ++j)
     if (tx.rep[j] != ty.rep[j]) return false;
@@ -1845,13 +1845,29 @@ int launch_line_filter(const aol_task& t, const LineGeom& g, int64_t first, int6
 // opaque storage for a LineGeom (defined in aol_linefilter.cu)
 struct alignas(16) LineGeomBuf { unsigned char b[256]; };
 
+// Routing: the config-shaped kernels (stencil boxes, block pooling, the 13->3 / 14->4 line forms and
+// strided line filters) first; then the 32-bit batched kernel, which beats the shared-memory line
+// window (`line_tiled`, 2-4x on 1-D FIRs and decimators, tools/time_filters.py) and every
+// thread-per-repetition form; the int64 kernels last.
+static bool filter_batched_route(const aol_task& t, int64_t first, int64_t count, DevTiler& tx, DevTiler& ty) {
+  if (make_dev_tiler(t.tilers[0], tx) || make_dev_tiler(t.tilers[1], ty)) return false;
+  const int64_t px = tiler_pat_total(t.tilers[0]), py = tiler_pat_total(t.tilers[1]);
+  const int64_t esz = t.dtype == AOL_F32 ? 4 : 8;
+  const int64_t smem = px * py * esz + (px + py + px * tx.a + py * ty.a) * 4;
+  return py <= 16 && smem <= 200 * 1024 && filter_batched_ok(tx, ty, first, count);
+}
+
 const char* filter_plan_name(const aol_task& t) {
   int kh, kw;
   if (stencil_box_applicable(t, kh, kw)) return "tile_filter.stencil_box";
   if (box_pool_applicable(t, kh, kw)) return "tile_filter.box_pool";
   LineGeomBuf gb;
-  if (line_filter_geometry(t, *reinterpret_cast<LineGeom*>(&gb)))
-    return line_filter_variant(*reinterpret_cast<LineGeom*>(&gb));
+  const bool line = line_filter_geometry(t, *reinterpret_cast<LineGeom*>(&gb));
+  const char* variant = line ? line_filter_variant(*reinterpret_cast<LineGeom*>(&gb)) : nullptr;
+  if (line && strcmp(variant, "tile_filter.line_tiled") != 0) return variant;
+  DevTiler tx, ty;
+  if (filter_batched_route(t, 0, tiler_rep_total(t.tilers[0]), tx, ty)) return "tile_filter.batched";
+  if (line) return variant;
   const int64_t px = tiler_pat_total(t.tilers[0]), py = tiler_pat_total(t.tilers[1]);
   if (t.dtype == AOL_F32 && px <= 16 && py <= 4 && contiguous_pattern(t.tilers[0])) return "tile_filter.window_vec";
   return "tile_filter.generic";
@@ -1864,25 +1880,37 @@ int launch_filter_generic(const aol_task& t, int64_t first, int64_t count, void*
   if (box_pool_applicable(t, kh, kw) && (uintptr_t)ports[0] % 16 == 0 && (uintptr_t)ports[2] % 16 == 0)
     return launch_box_pool(t, first, count, ports, stream);
   LineGeomBuf gb;
-  if (line_filter_geometry(t, *reinterpret_cast<LineGeom*>(&gb)))
+  const bool line = line_filter_geometry(t, *reinterpret_cast<LineGeom*>(&gb));
+  if (line && strcmp(line_filter_variant(*reinterpret_cast<LineGeom*>(&gb)), "tile_filter.line_tiled") != 0)
     return launch_line_filter(t, *reinterpret_cast<LineGeom*>(&gb), first, count, ports, stream);
   DevTiler tx, ty;
+  const bool batched = filter_batched_route(t, first, count, tx, ty);
+  if (!batched && line) return launch_line_filter(t, *reinterpret_cast<LineGeom*>(&gb), first, count, ports, stream);
   int rc;
   if ((rc = make_dev_tiler(t.tilers[0], tx)) || (rc = make_dev_tiler(t.tilers[1], ty))) return rc;
   const int64_t px = tiler_pat_total(t.tilers[0]), py = tiler_pat_total(t.tilers[1]);
-  if (px * tx.a + py * ty.a + px + py > kTableMax * 4 || px * py > 16384)
-    return fail(AOL_EUNSUPPORTED, "tile_filter pattern too large (px*py <= 16384)");
-  if (py > 16) return fail(AOL_EUNSUPPORTED, "tile_filter supports at most 16 outputs per pattern");
   const bool f32 = t.dtype == AOL_F32;
-  if (f32 && px <= 16 && py <= 4 && contiguous_pattern(t.tilers[0]))
-    return launch_filter_t<float, 4, true>(t, tx, ty, first, count, (int)px, (int)py, ports, stream);
-  if (filter_batched_ok(tx, ty, first, count)) {
+  if (batched) {
+    // R = 16 when a lane's repetitions are one element apart (dense 1-D runs), else 8 (measured)
+    int32_t lane_step = 0;
+    for (int d = 0; d < tx.a; ++d) lane_step += (int32_t)tx.P[d][tx.q - 1] * (int32_t)tx.st[d];
+    if (py == 1 && lane_step == 1)
+      return f32 ? launch_filter_b32_q<float, 1, 16>(t, tx, ty, first, count, (int)px, (int)py, ports, stream)
+                 : launch_filter_b32_q<double, 1, 16>(t, tx, ty, first, count, (int)px, (int)py, ports, stream);
+    if (py == 1)
+      return f32 ? launch_filter_b32_q<float, 1, 8>(t, tx, ty, first, count, (int)px, (int)py, ports, stream)
+                 : launch_filter_b32_q<double, 1, 8>(t, tx, ty, first, count, (int)px, (int)py, ports, stream);
     if (py <= 4)
-      return f32 ? launch_filter_b32_q<float, 4, 4>(t, tx, ty, first, count, (int)px, (int)py, ports, stream)
+      return f32 ? launch_filter_b32_q<float, 4, 8>(t, tx, ty, first, count, (int)px, (int)py, ports, stream)
                  : launch_filter_b32_q<double, 4, 4>(t, tx, ty, first, count, (int)px, (int)py, ports, stream);
     return f32 ? launch_filter_b32_q<float, 16, 2>(t, tx, ty, first, count, (int)px, (int)py, ports, stream)
                : launch_filter_b32_q<double, 16, 2>(t, tx, ty, first, count, (int)px, (int)py, ports, stream);
   }
+  if (px * tx.a + py * ty.a + px + py > kTableMax * 4 || px * py > 16384)
+    return fail(AOL_EUNSUPPORTED, "tile_filter pattern too large (px*py <= 16384)");
+  if (py > 16) return fail(AOL_EUNSUPPORTED, "tile_filter supports at most 16 outputs per pattern");
+  if (f32 && px <= 16 && py <= 4 && contiguous_pattern(t.tilers[0]))
+    return launch_filter_t<float, 4, true>(t, tx, ty, first, count, (int)px, (int)py, ports, stream);
   if (py <= 4)
     return f32 ? launch_filter_t<float, 4, false>(t, tx, ty, first, count, (int)px, (int)py, ports, stream)
                : launch_filter_t<double, 4, false>(t, tx, ty, first, count, (int)px, (int)py, ports, stream);

@@ -240,6 +240,7 @@ KERNEL_STAGING = {
     "tile_filter.line_14x4_vstrip": "coefficients: smem broadcast; 4 overlapping 14-tap windows (41 rows): registers "
                                     "(coalesced row taps)",
     "tile_filter.line": "coefficients: smem broadcast; window: registers",
+    "tile_filter.batched": "coefficients + int32 pattern tables: smem; 8-16 repetitions per lane, window: registers",
     "tile_filter.window_vec": "coefficients + pattern tables: smem; window: registers",
     "tile_filter.generic": "coefficients + pattern tables: smem; window: registers",
     "tile_sum.generic": "pattern table: smem; accumulation: registers",

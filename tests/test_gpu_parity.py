@@ -1255,10 +1255,13 @@ def test_tile_sum_plans_vs_oracle(case, plan, dtype, devices):
     (1, 5000, 8, 1, 1, 1, 0), (1, 4096, 16, 1, 1, 1, 4093), (3, 2000, 32, 1, 1, 1, 7), (2, 8192, 16, 4, 1, 1, 0),
     (4, 3000, 13, 8, 3, 3, 5), (2, 1000, 5, 2, 8, 8, 999), (1, 10000, 7, 3, 2, 2, 1), (2, 6000, 16, 8, 2, 2, 3)])
 @pytest.mark.parametrize("devices", [1, 3, 5])
-def test_line_tiled_filters_vs_oracle(outer, S, px, sx, py, sy, ox, devices):
+@pytest.mark.parametrize("wide", [False, True])
+def test_line_tiled_filters_vs_oracle(outer, S, px, sx, py, sy, ox, devices, wide, monkeypatch):
     """Generic horizontal line filters (1-D FIRs, decimating FIRs, wrapping windows, up to 8
-    outputs per repetition) through the shared-memory-windowed kernel: bit-exact vs the oracle,
-    shard starts anywhere inside a line."""
+    outputs per repetition) through the 32-bit batched kernel (default) and the shared-memory
+    window kernel (`AOL_FILTER_WIDE`): bit-exact vs the oracle, shard starts anywhere inside a line."""
+    if wide:
+        monkeypatch.setenv("AOL_FILTER_WIDE", "1")
     NL = (S - 1) // sx + 1 if sx > 1 else S
     NL = min(NL, S // sx) if sx > 1 else NL
     Sy = NL * sy if sy >= py else NL * py
@@ -1270,7 +1273,7 @@ def test_line_tiled_filters_vs_oracle(outer, S, px, sx, py, sy, ox, devices):
     w = (np.random.default_rng(px * 10 + py).standard_normal(px * py) / px).astype(np.float32)
     x = np.random.default_rng(S + px).standard_normal(outer * S).astype(np.float32)
     want = ("tile_filter.line_13x3" if (px, py) == (13, 3) else
-            "tile_filter.line_tiled" if sx <= 4 else "tile_filter.line")
+            "tile_filter.line" if sx > 4 else "tile_filter.line_tiled" if wide else "tile_filter.batched")
     assert _plan([tx, ty]) == want
     got, ref = _filter_case("tile_filter", t, w, x, devices)
     assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
@@ -1430,7 +1433,7 @@ def test_generic_filter_batched32_vs_oracle(case, dtype, devices, wide, monkeypa
     if wide:
         monkeypatch.setenv("AOL_FILTER_WIDE", "1")
     _, tx, ty = next(c for c in _generic_filter_cases() if c[0] == case)
-    assert _plan([tx, ty], dtype) == "tile_filter.generic"
+    assert _plan([tx, ty], dtype) == ("tile_filter.generic" if wide else "tile_filter.batched")
     np_dt = np.dtype(dtype)
     px = int(np.prod(tx["pattern"]))
     py = int(np.prod(ty["pattern"]))

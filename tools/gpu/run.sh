@@ -1,3 +1,2 @@
 timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "filter or stencil or box_pool" > gpurun_out/t.log 2>&1; echo t=$?
 timeout 300 python tools/time_filters.py > gpurun_out/filters.log 2>&1; echo a=$?
-AOL_FILTER_WIDE=1 timeout 300 python tools/time_filters.py > gpurun_out/filters_wide.log 2>&1; echo b=$?

@@ -50,3 +50,10 @@ run("2-D 3x3 stride 2 (torus)", (H, W), Tiler((H - 1, W - 1), ((2, 0), (0, 2)), 
     (H // 2, W // 2), Tiler((0, 0), ((1, 0), (0, 1)), ((0,), (0,)), (1,)), (H // 2, W // 2), 9, 1)
 run("2-D 2x2 outputs per 4x4 window", (H, W), Tiler((0, 0), ((4, 0), (0, 4)), ((1, 0), (0, 1)), (4, 4)),
     (H // 2, W // 2), Tiler((0, 0), ((2, 0), (0, 2)), ((1, 0), (0, 1)), (2, 2)), (H // 4, W // 4), 16, 4)
+run("1-D 8 taps /2, 2 outputs", (N,), Tiler((0,), ((2,),), ((1,),), (8,)), (N,), Tiler((0,), ((2,),), ((1,),), (2,)), (N // 2,), 8, 2)
+run("1-D 13 taps /8, 3 outputs", (N,), Tiler((0,), ((8,),), ((1,),), (13,)), (N // 8 * 3,),
+    Tiler((0,), ((3,),), ((1,),), (3,)), (N // 8,), 13, 3)
+run("1-D 7 taps /3 (wrap)", (3 * (N // 3),), Tiler((5,), ((3,),), ((1,),), (7,)), (N // 3,),
+    Tiler((0,), ((1,),), ((0,),), (1,)), (N // 3,), 7, 1)
+run("rows 16 taps /8, 1 output", (64, 2048, 2048), Tiler((0, 0, 0), ((1, 0, 0), (0, 1, 0), (0, 0, 8)), ((0,), (0,), (1,)), (16,)),
+    (64, 2048, 256), Tiler((0, 0, 0), ((1, 0, 0), (0, 1, 0), (0, 0, 1)), ((0,), (0,), (0,)), (1,)), (64, 2048, 256), 16, 1)
