@@ -886,11 +886,13 @@ __device__ __forceinline__ T mul_add_rn(T acc, T w, T x) {
   else return __dadd_rn(acc, __dmul_rn(w, x));
 }
 
-template <typename T, int MAXO, int R, int Q>
+// XV: the x pattern is one contiguous run of <= 16 floats and a lane's repetitions are 16 B apart:
+// each window comes in as four float4 loads with the weights held in registers.
+template <typename T, int MAXO, int R, int Q, bool XV>
 __global__ void __launch_bounds__(256) k_filter_batched32(const T* __restrict__ x, const T* __restrict__ w,
                                                           T* __restrict__ y, DevTiler tx, DevTiler ty, PatSpan sx,
                                                           PatSpan sy, int32_t first, int32_t count, int px,
-                                                          int py) {
+                                                          int py, int32_t nx) {
   extern __shared__ __align__(16) unsigned char fsm[];
   T* ws = reinterpret_cast<T*>(fsm);
   int32_t* ox = reinterpret_cast<int32_t*>(ws + px * py);   // raw flat pattern offsets
@@ -950,8 +952,36 @@ __global__ void __launch_bounds__(256) k_filter_batched32(const T* __restrict__ 
       for (int k = 0; k < R; ++k)
 #pragma unroll
         for (int j = 0; j < MAXO; ++j) acc[k][j] = T(0);
+      bool vec = false;
+      if constexpr (XV) {
+        if ((xo & 3) == 0 && xo + (R - 1) * dx + 16 <= nx) {
+          vec = true;
+          float wr[MAXO][16];
+#pragma unroll
+          for (int j = 0; j < MAXO; ++j)
+#pragma unroll
+            for (int i = 0; i < 16; ++i) wr[j][i] = (j < py && i < px) ? ws[j * px + i] : 0.f;
+#pragma unroll
+          for (int k = 0; k < R; ++k) {
+            float xv[16];
+            const float4* xp = reinterpret_cast<const float4*>(x + xo + k * dx);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float4 v = __ldg(xp + q);
+              xv[4 * q] = v.x; xv[4 * q + 1] = v.y; xv[4 * q + 2] = v.z; xv[4 * q + 3] = v.w;
+            }
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (i < px) {
+#pragma unroll
+                for (int j = 0; j < MAXO; ++j)
+                  if (j < py) acc[k][j] = mul_add_rn(acc[k][j], wr[j][i], xv[i]);
+              }
+          }
+        }
+      }
 #pragma unroll 4
-      for (int i = 0; i < px; ++i) {
+      for (int i = 0; i < (vec ? 0 : px); ++i) {
         T xv[R];
         const int32_t oi = xo + ox[i];
 #pragma unroll
@@ -1803,30 +1833,30 @@ static bool filter_batched_ok(const DevTiler& tx, const DevTiler& ty, int64_t fi
   return true;
 }
 
-template <typename T, int MAXO, int R, int Q>
+template <typename T, int MAXO, int R, int Q, bool XV>
 static int launch_filter_b32(const aol_task& t, const DevTiler& tx, const DevTiler& ty, int64_t first,
                               int64_t count, int px, int py, void* const* ports, cudaStream_t stream) {
   const size_t smem = (size_t)px * py * sizeof(T) + ((size_t)px + py + (size_t)px * tx.a + (size_t)py * ty.a) * 4;
-  auto kern = k_filter_batched32<T, MAXO, R, Q>;
+  auto kern = k_filter_batched32<T, MAXO, R, Q, XV>;
   if (smem > 48 * 1024)
     AOL_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t per = 256 * R;
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((count + per - 1) / per, (int64_t)kNumSMs * 8));
   kern<<<grid, 256, smem, stream>>>((const T*)ports[0], (const T*)ports[1], (T*)ports[2], tx, ty,
                                     pattern_span(t.tilers[0]), pattern_span(t.tilers[1]), (int32_t)first,
-                                    (int32_t)count, px, py);
+                                    (int32_t)count, px, py, (int32_t)tiler_arr_total(t.tilers[0]));
   return AOL_OK;
 }
 
-template <typename T, int MAXO, int R>
+template <typename T, int MAXO, int R, bool XV = false>
 static int launch_filter_b32_q(const aol_task& t, const DevTiler& tx, const DevTiler& ty, int64_t first,
                                int64_t count, int px, int py, void* const* ports, cudaStream_t stream) {
   int rc;
   switch (tx.q) {
-    case 1: rc = launch_filter_b32<T, MAXO, R, 1>(t, tx, ty, first, count, px, py, ports, stream); break;
-    case 2: rc = launch_filter_b32<T, MAXO, R, 2>(t, tx, ty, first, count, px, py, ports, stream); break;
-    case 3: rc = launch_filter_b32<T, MAXO, R, 3>(t, tx, ty, first, count, px, py, ports, stream); break;
-    default: rc = launch_filter_b32<T, MAXO, R, 4>(t, tx, ty, first, count, px, py, ports, stream); break;
+    case 1: rc = launch_filter_b32<T, MAXO, R, 1, XV>(t, tx, ty, first, count, px, py, ports, stream); break;
+    case 2: rc = launch_filter_b32<T, MAXO, R, 2, XV>(t, tx, ty, first, count, px, py, ports, stream); break;
+    case 3: rc = launch_filter_b32<T, MAXO, R, 3, XV>(t, tx, ty, first, count, px, py, ports, stream); break;
+    default: rc = launch_filter_b32<T, MAXO, R, 4, XV>(t, tx, ty, first, count, px, py, ports, stream); break;
   }
   if (rc) return rc;
   AOL_LAUNCH_CHECK("k_filter_batched32");
@@ -1849,6 +1879,10 @@ struct alignas(16) LineGeomBuf { unsigned char b[256]; };
 // strided line filters) first; then the 32-bit batched kernel, which beats the shared-memory line
 // window (`line_tiled`, 2-4x on 1-D FIRs and decimators, tools/time_filters.py) and every
 // thread-per-repetition form; the int64 kernels last.
+// line-filter variants the batched kernel replaces when it applies (`tile_filter.line`, paving > 4,
+// stays: 0.82 vs 1.02 ms on 64x2048x2048 rows /8, tools/time_filters.py)
+static bool line_yields(const char* variant) { return strcmp(variant, "tile_filter.line_tiled") == 0; }
+
 static bool filter_batched_route(const aol_task& t, int64_t first, int64_t count, DevTiler& tx, DevTiler& ty) {
   if (make_dev_tiler(t.tilers[0], tx) || make_dev_tiler(t.tilers[1], ty)) return false;
   const int64_t px = tiler_pat_total(t.tilers[0]), py = tiler_pat_total(t.tilers[1]);
@@ -1864,7 +1898,7 @@ const char* filter_plan_name(const aol_task& t) {
   LineGeomBuf gb;
   const bool line = line_filter_geometry(t, *reinterpret_cast<LineGeom*>(&gb));
   const char* variant = line ? line_filter_variant(*reinterpret_cast<LineGeom*>(&gb)) : nullptr;
-  if (line && strcmp(variant, "tile_filter.line_tiled") != 0) return variant;
+  if (line && !line_yields(variant)) return variant;
   DevTiler tx, ty;
   if (filter_batched_route(t, 0, tiler_rep_total(t.tilers[0]), tx, ty)) return "tile_filter.batched";
   if (line) return variant;
@@ -1881,7 +1915,7 @@ int launch_filter_generic(const aol_task& t, int64_t first, int64_t count, void*
     return launch_box_pool(t, first, count, ports, stream);
   LineGeomBuf gb;
   const bool line = line_filter_geometry(t, *reinterpret_cast<LineGeom*>(&gb));
-  if (line && strcmp(line_filter_variant(*reinterpret_cast<LineGeom*>(&gb)), "tile_filter.line_tiled") != 0)
+  if (line && !line_yields(line_filter_variant(*reinterpret_cast<LineGeom*>(&gb))))
     return launch_line_filter(t, *reinterpret_cast<LineGeom*>(&gb), first, count, ports, stream);
   DevTiler tx, ty;
   const bool batched = filter_batched_route(t, first, count, tx, ty);
@@ -1894,6 +1928,9 @@ int launch_filter_generic(const aol_task& t, int64_t first, int64_t count, void*
     // R = 16 when a lane's repetitions are one element apart (dense 1-D runs), else 8 (measured)
     int32_t lane_step = 0;
     for (int d = 0; d < tx.a; ++d) lane_step += (int32_t)tx.P[d][tx.q - 1] * (int32_t)tx.st[d];
+    if (f32 && py <= 2 && px <= 16 && lane_step % 4 == 0 && contiguous_pattern(t.tilers[0]))
+      return py == 1 ? launch_filter_b32_q<float, 1, 8, true>(t, tx, ty, first, count, (int)px, (int)py, ports, stream)
+                     : launch_filter_b32_q<float, 2, 8, true>(t, tx, ty, first, count, (int)px, (int)py, ports, stream);
     if (py == 1 && lane_step == 1)
       return f32 ? launch_filter_b32_q<float, 1, 16>(t, tx, ty, first, count, (int)px, (int)py, ports, stream)
                  : launch_filter_b32_q<double, 1, 16>(t, tx, ty, first, count, (int)px, (int)py, ports, stream);

@@ -1253,7 +1253,8 @@ def test_tile_sum_plans_vs_oracle(case, plan, dtype, devices):
 
 @pytest.mark.parametrize("outer,S,px,sx,py,sy,ox", [
     (1, 5000, 8, 1, 1, 1, 0), (1, 4096, 16, 1, 1, 1, 4093), (3, 2000, 32, 1, 1, 1, 7), (2, 8192, 16, 4, 1, 1, 0),
-    (4, 3000, 13, 8, 3, 3, 5), (2, 1000, 5, 2, 8, 8, 999), (1, 10000, 7, 3, 2, 2, 1), (2, 6000, 16, 8, 2, 2, 3)])
+    (4, 3000, 13, 8, 3, 3, 5), (2, 1000, 5, 2, 8, 8, 999), (1, 10000, 7, 3, 2, 2, 1), (2, 6000, 16, 8, 2, 2, 3),
+    (2, 4096, 12, 4, 2, 2, 0), (1, 4100, 9, 4, 1, 1, 8), (3, 2048, 16, 4, 1, 1, 4090)])
 @pytest.mark.parametrize("devices", [1, 3, 5])
 @pytest.mark.parametrize("wide", [False, True])
 def test_line_tiled_filters_vs_oracle(outer, S, px, sx, py, sy, ox, devices, wide, monkeypatch):
