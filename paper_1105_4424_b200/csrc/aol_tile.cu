@@ -1155,6 +1155,140 @@ __global__ void __launch_bounds__(256) k_tile_sum_direct(const T* __restrict__ x
   }
 }
 
+// Column sums (affine tile_sum with As == 1: consecutive repetitions are consecutive columns, the
+// pattern walks rows of pitch Bs).  A CTA owns 32 columns; one elected producer thread streams
+// {32 columns x RB rows} TMA boxes (8 KB) through a 4-deep shared-memory ring, and the consumer
+// warp's lane j adds column j's rows in order (i ascending, one rounding per add, like
+// k_tile_sum_direct).  The thread-per-column kernel has only count/32 warps to keep loads in
+// flight; here every SM holds ~100 KB of boxes in flight while the add chains run from smem.
+constexpr int kColStages = 4;
+template <typename T>
+__global__ void __launch_bounds__(64) k_tile_sum_cols(const __grid_constant__ CUtensorMap mx, T* __restrict__ s,
+                                                      DevTiler ts, int64_t first, int rem, int64_t count,
+                                                      int64_t P) {
+  constexpr int RB = 8192 / (32 * (int)sizeof(T));   // rows per box
+  extern __shared__ __align__(128) unsigned char cring[];
+  __shared__ __align__(8) uint64_t full[kColStages], empty[kColStages];
+  const T* ring = reinterpret_cast<const T*>(cring);
+  const int64_t nbox = (P + RB - 1) / RB;
+  const int c0 = blockIdx.x * 32;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kColStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 32) {                           // producer
+    for (int64_t k = 0; k < nbox; ++k) {
+      const int st = (int)(k % kColStages);
+      if (k >= kColStages) mbar_wait(&empty[st], (uint32_t)((k / kColStages - 1) & 1));
+      mbar_expect_tx(&full[st], 8192);
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+              smem_u32(cring + st * 8192)),
+          "l"(&mx), "r"(c0), "r"((int)(k * RB)), "r"(smem_u32(&full[st]))
+          : "memory");
+    }
+    return;
+  }
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  T acc = T(0);
+  for (int64_t k = 0; k < nbox; ++k) {
+    const int st = (int)(k % kColStages);
+    mbar_wait(&full[st], (uint32_t)((k / kColStages) & 1));
+    const T* b = ring + st * (8192 / sizeof(T)) + lane;
+    const int64_t rows = P - k * RB;
+    if (rows >= RB) {
+#pragma unroll 16
+      for (int r = 0; r < RB; ++r) {
+        if constexpr (sizeof(T) == 4) acc = __fadd_rn(acc, b[r * 32]);
+        else acc = __dadd_rn(acc, b[r * 32]);
+      }
+    } else {
+      for (int r = 0; r < (int)rows; ++r) {
+        if constexpr (sizeof(T) == 4) acc = __fadd_rn(acc, b[r * 32]);
+        else acc = __dadd_rn(acc, b[r * 32]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+  const int c = c0 + lane;
+  if (c >= rem && c < rem + count) s[tiler_offset(ts, first - rem + c, 0)] = acc;
+}
+
+// Row sums over non-overlapping rows (tile_sum.rows with a 16 B row pitch >= P): a CTA owns 32
+// repetitions (rows); the producer streams {128 B of each row x 32 rows} TMA boxes with the 128B
+// swizzle (16 B chunk c of row r lands at c ^ (r & 7)) through an 8-deep ring, so lane j's 16 B
+// reads of row j are conflict-free per quarter warp; lane j adds its row's elements in order.
+constexpr int kRowStages = 8;
+template <typename T>
+__global__ void __launch_bounds__(64) k_tile_sum_rows_tma(const __grid_constant__ CUtensorMap mx, T* __restrict__ s,
+                                                          DevTiler ts, int64_t first, int64_t count, int64_t P) {
+  constexpr int E = 128 / (int)sizeof(T);            // elements per row per box
+  constexpr int EC = 16 / (int)sizeof(T);            // elements per 16 B chunk
+  extern __shared__ __align__(1024) unsigned char rring_raw[];
+  unsigned char* rring = reinterpret_cast<unsigned char*>(((uintptr_t)rring_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t full[kRowStages], empty[kRowStages];
+  const int64_t nbox = (P + E - 1) / E;
+  const int r0 = blockIdx.x * 32;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kRowStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 32) {
+    for (int64_t k = 0; k < nbox; ++k) {
+      const int st = (int)(k % kRowStages);
+      if (k >= kRowStages) mbar_wait(&empty[st], (uint32_t)((k / kRowStages - 1) & 1));
+      mbar_expect_tx(&full[st], 4096);
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+              smem_u32(rring + st * 4096)),
+          "l"(&mx), "r"((int)(k * E)), "r"(r0), "r"(smem_u32(&full[st]))
+          : "memory");
+    }
+    return;
+  }
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  T acc = T(0);
+  for (int64_t k = 0; k < nbox; ++k) {
+    const int st = (int)(k % kRowStages);
+    mbar_wait(&full[st], (uint32_t)((k / kRowStages) & 1));
+    const unsigned char* row = rring + st * 4096 + lane * 128;
+    const int64_t left = P - k * E;
+    if (left >= E) {
+      T v[E];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const uint4 q = *reinterpret_cast<const uint4*>(row + ((c ^ (lane & 7)) << 4));
+        memcpy(&v[c * EC], &q, 16);
+      }
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        if constexpr (sizeof(T) == 4) acc = __fadd_rn(acc, v[e]);
+        else acc = __dadd_rn(acc, v[e]);
+      }
+    } else {
+      for (int e = 0; e < (int)left; ++e) {
+        const T v = *reinterpret_cast<const T*>(row + (((e / EC) ^ (lane & 7)) << 4) + (e % EC) * sizeof(T));
+        if constexpr (sizeof(T) == 4) acc = __fadd_rn(acc, v);
+        else acc = __dadd_rn(acc, v);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+  if (r0 + lane < count) s[tiler_offset(ts, first + r0 + lane, 0)] = acc;
+}
+
 // ------------------------------------------------------- launch wrappers ----
 
 int launch_tiler_offsets(const aol_tiler& t, int64_t first, int64_t count, int64_t* out,
@@ -1955,6 +2089,12 @@ int launch_filter_generic(const aol_task& t, int64_t first, int64_t count, void*
              : launch_filter_t<double, 16, false>(t, tx, ty, first, count, (int)px, (int)py, ports, stream);
 }
 
+// tile_sum.columns: As == 1, 16 B row pitch, enough columns and rows to stream (else direct)
+static bool tile_sum_cols_ok(int64_t As, int64_t Bs, int64_t P, int64_t count, int64_t esz) {
+  return As == 1 && (Bs * esz) % 16 == 0 && Bs >= count && P >= 128 && count >= 256 &&
+         count < ((int64_t)1 << 31) && P < ((int64_t)1 << 31);
+}
+
 // tile_sum plan: "rows" (affine, contiguous pattern), "direct" (other affine), "generic"
 // (offset table in shared memory), "generic_direct" (wrapping and too large for the table).
 static int tile_sum_kind(const aol_task& t, int64_t& cs, int64_t& As, int64_t& Bs) {
@@ -1976,10 +2116,60 @@ const char* tile_sum_plan_name(const aol_task& t) {
   int64_t cs, As, Bs;
   switch (tile_sum_kind(t, cs, As, Bs)) {
     case 0: return "tile_sum.rows";
-    case 1: return "tile_sum.direct";
+    case 1:
+      return tile_sum_cols_ok(As, Bs, tiler_pat_total(t.tilers[0]), tiler_rep_total(t.tilers[0]),
+                              t.dtype == AOL_F32 ? 4 : 8) ? "tile_sum.columns" : "tile_sum.direct";
     case 2: return "tile_sum.generic";
     default: return "tile_sum.generic_direct";
   }
+}
+
+// 1 = this range needs the cp.async rows kernel (overlapping rows or misaligned start)
+template <typename T>
+static int launch_tile_sum_rows_tma(const T* x, T* sp, const DevTiler& ts, int64_t cs, int64_t As, int64_t P,
+                                    int64_t first, int64_t count, cudaStream_t stream) {
+  const T* base = x + cs + As * first;
+  if (As < P || (As * (int64_t)sizeof(T)) % 16 || (uintptr_t)base % 16 || P < 256 || count < 256 ||
+      count >= ((int64_t)1 << 31) || P >= ((int64_t)1 << 31) || getenv("AOL_TILE_SUM_CPASYNC"))
+    return 1;
+  auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(tensor_map_encoder());
+  if (!encode) return 1;
+  CUtensorMap mx;
+  cuuint64_t dims[2] = {(cuuint64_t)P, (cuuint64_t)count}, str[1] = {(cuuint64_t)(As * sizeof(T))};
+  cuuint32_t box[2] = {(cuuint32_t)(128 / sizeof(T)), 32}, es[2] = {1, 1};
+  if (encode(&mx, sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+             const_cast<T*>(base), dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return 1;
+  const int smem = kRowStages * 4096 + 1024;
+  const unsigned grid = (unsigned)((count + 31) / 32);
+  k_tile_sum_rows_tma<T><<<grid, 64, smem, stream>>>(mx, sp, ts, first, count, P);
+  AOL_LAUNCH_CHECK("k_tile_sum_rows_tma");
+  return AOL_OK;
+}
+
+template <typename T>
+static int launch_tile_sum_cols(const T* x, T* sp, const DevTiler& ts, int64_t cs, int64_t Bs, int64_t P,
+                                int64_t first, int64_t count, cudaStream_t stream) {
+  const T* base = x + cs + first;
+  const int rem = (int)(((uintptr_t)base % 16) / sizeof(T));
+  if (count + rem > Bs || (uintptr_t)base % sizeof(T)) return 1;   // the tensor's rows must not overlap
+  base -= rem;
+  auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(tensor_map_encoder());
+  if (!encode) return fail(AOL_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  CUtensorMap mx;
+  constexpr int RB = 8192 / (32 * (int)sizeof(T));
+  cuuint64_t dims[2] = {(cuuint64_t)(count + rem), (cuuint64_t)P}, str[1] = {(cuuint64_t)(Bs * sizeof(T))};
+  cuuint32_t box[2] = {32, (cuuint32_t)RB}, es[2] = {1, 1};
+  if (encode(&mx, sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+             const_cast<T*>(base), dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return fail(AOL_ECUDA, "tile_sum.columns: tensor map encode failed");
+  const int smem = kColStages * 8192;
+  const unsigned grid = (unsigned)((count + rem + 31) / 32);
+  k_tile_sum_cols<T><<<grid, 64, smem, stream>>>(mx, sp, ts, first, rem, count, P);
+  AOL_LAUNCH_CHECK("k_tile_sum_cols");
+  return AOL_OK;
 }
 
 int launch_tile_sum(const aol_task& t, int64_t first, int64_t count, void* const* ports, cudaStream_t stream) {
@@ -1991,6 +2181,11 @@ int launch_tile_sum(const aol_task& t, int64_t first, int64_t count, void* const
   const int kind = tile_sum_kind(t, cs, As, Bs);
   const bool f32 = t.dtype == AOL_F32;
   if (kind == 0) {
+    rc = f32 ? launch_tile_sum_rows_tma<float>((const float*)ports[0], (float*)ports[1], ts, cs, As, px, first, count,
+                                               stream)
+             : launch_tile_sum_rows_tma<double>((const double*)ports[0], (double*)ports[1], ts, cs, As, px, first,
+                                                count, stream);
+    if (rc <= 0) return rc;
     const int per = 32 * (f32 ? ts_warps<float>() : ts_warps<double>());
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((count + per - 1) / per, (int64_t)kNumSMs * 32));
     if (f32)
@@ -2001,6 +2196,13 @@ int launch_tile_sum(const aol_task& t, int64_t first, int64_t count, void* const
                                                         first, count);
     AOL_LAUNCH_CHECK("k_tile_sum_rows");
     return AOL_OK;
+  }
+  if (kind == 1 && tile_sum_cols_ok(As, Bs, px, count, f32 ? 4 : 8)) {
+    // returns 1 when this range's alignment needs the direct form
+    rc = f32 ? launch_tile_sum_cols<float>((const float*)ports[0], (float*)ports[1], ts, cs, Bs, px, first, count, stream)
+             : launch_tile_sum_cols<double>((const double*)ports[0], (double*)ports[1], ts, cs, Bs, px, first, count,
+                                            stream);
+    if (rc <= 0) return rc;
   }
   if (kind == 1 || kind == 3) {
     const unsigned grid = grid_for(count, 256, 16);

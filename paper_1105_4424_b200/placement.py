@@ -221,6 +221,7 @@ KERNEL_STAGING = {
     "tile_filter.box_pool": "HBM -> registers (KH rows x 4*KW floats as float4) -> HBM (float4 stores)",
     "tile_filter.line_tiled": "HBM -> coalesced window per tile of <= 8192 repetitions -> padded smem -> registers -> HBM",
     "tile_sum.rows": "HBM -> cp.async 32x32 tiles (coalesced rows) -> smem ring (4 chunks) -> one ordered add chain per lane",
+    "tile_sum.columns": "HBM -> TMA {32 columns x 8 KB} boxes -> 4-stage smem ring -> one ordered add chain per lane",
     "tile_sum.direct": "HBM -> registers (64 loads in flight per repetition) -> ordered add chain",
     "tile_copy.window": "HBM -> one bulk copy per tile of the overlapping source window -> smem ring -> registers (16 B stores) -> HBM",
     "tile_copy.tma_box": "HBM -> TMA pattern-row boxes -> shared-memory ring (32-64 KB in flight/SM) -> TMA store -> HBM",

@@ -1219,20 +1219,31 @@ def test_stencil_wide_windows_vs_oracle(kh, kw, H, W, devices):
 
 
 @pytest.mark.parametrize("case,plan", [("rows", "tile_sum.rows"), ("rows_ragged", "tile_sum.rows"),
-                                       ("cols", "tile_sum.direct"), ("wrap_small", "tile_sum.generic"),
+                                       ("rows_pitch", "tile_sum.rows"),
+                                       ("cols", "tile_sum.columns"), ("cols_small", "tile_sum.direct"),
+                                       ("cols_pitch", "tile_sum.columns"), ("wrap_small", "tile_sum.generic"),
                                        ("wrap_big", "tile_sum.generic_direct")])
 @pytest.mark.parametrize("dtype", ["float32", "float64"])
 @pytest.mark.parametrize("devices", [1, 3])
 def test_tile_sum_plans_vs_oracle(case, plan, dtype, devices):
     """Pattern reductions (i ascending, one rounding per add) on every tile_sum plan: coalesced
-    warp-transposed row sums, direct affine sums (column sums), the offset-table generic form
+    warp-transposed and TMA-swizzled row sums, TMA-streamed column sums (shard starts off 16 B), direct affine
+    sums, the offset-table generic form
     and the table-free form for large wrapping patterns -- bit-exact against the oracle."""
     if case in ("rows", "rows_ragged"):
         R, P = (300, 1000) if case == "rows" else (77, 45)
         tx = dict(array=(R, P), rep=(R,), pattern=(P,), origin=(0, 0), paving=((1,), (0,)), fitting=((0,), (1,)))
-    elif case == "cols":
-        R, P = 700, 300
+    elif case == "rows_pitch":
+        # 777 of every 780 elements (TMA row boxes, partial last box), 1000 rows
+        R, P = 1000, 777
+        tx = dict(array=(R, 780), rep=(R,), pattern=(P,), origin=(0, 2), paving=((1,), (0,)), fitting=((0,), (1,)))
+    elif case in ("cols", "cols_small"):
+        R, P = (700, 300) if case == "cols" else (100, 300)
         tx = dict(array=(P, R), rep=(R,), pattern=(P,), origin=(0, 0), paving=((0,), (1,)), fitting=((1,), (0,)))
+    elif case == "cols_pitch":
+        # columns 5..1004 of a 2-D array with a wider row pitch, 1000 rows (partial last box)
+        R, P = 1000, 1000
+        tx = dict(array=(P, 1024), rep=(R,), pattern=(P,), origin=(0, 5), paving=((0,), (1,)), fitting=((1,), (0,)))
     elif case == "wrap_small":
         R, P = 500, 9
         tx = dict(array=(600,), rep=(R,), pattern=(P,), origin=(595,), paving=((1,),), fitting=((1,),))
