@@ -226,6 +226,7 @@ __global__ void __launch_bounds__(256, (REPS <= 2 ? 4 : 3)) k_line_filter_vstrip
 static_assert(sizeof(LineGeom) <= 256, "LineGeomBuf in aol_tile.cu must hold a LineGeom");
 
 static bool hline_stream_ok(const LineGeom& g);
+static bool hline_stream_any_ok(const LineGeom& g);
 static bool vline_stream_ok(const LineGeom& g);
 static int launch_line_stream(const LineGeom& lg, int64_t first, int64_t count, const float* x, const float* w,
                               float* y, cudaStream_t s);
@@ -307,6 +308,7 @@ static int launch_line_tiled(const LineGeom& g, int64_t first, int64_t count, co
 
 const char* line_filter_variant(const LineGeom& g) {
   if (hline_stream_ok(g)) return "tile_filter.line_13x3_stream";
+  if (hline_stream_any_ok(g)) return "tile_filter.line_stream";
   if (vline_stream_ok(g)) return "tile_filter.line_14x4_stream";
   if (g.px == 13 && g.py == 3) return "tile_filter.line_13x3";
   if (g.px == 14 && g.py == 4 && g.inner > 1 && g.sx == 9) return "tile_filter.line_14x4_vstrip";
@@ -320,7 +322,8 @@ int launch_line_filter(const aol_task& t, const LineGeom& g, int64_t first, int6
   const float* x = static_cast<const float*>(ports[0]);
   const float* w = static_cast<const float*>(ports[1]);
   float* y = static_cast<float*>(ports[2]);
-  if (count > 0 && (hline_stream_ok(g) || vline_stream_ok(g))) return launch_line_stream(g, first, count, x, w, y, s);
+  if (count > 0 && (hline_stream_ok(g) || hline_stream_any_ok(g) || vline_stream_ok(g)))
+    return launch_line_stream(g, first, count, x, w, y, s);
   const unsigned grid = grid_for(count, 256, 8);
   // 32-bit offsets whenever both arrays fit (every in-range offset < 2^32)
   const bool idx32 = g.outer * g.Sx * g.inner < (1ll << 32) && g.outer * g.Sy * g.inner < (1ll << 32);
@@ -738,9 +741,15 @@ static int launch_fused_stream(const FusedGeom& fg, int64_t first, int64_t count
 // Streaming horizontal line filter (inner == 1, the unfused H task): whole x rows (+ the
 // 32-byte wrap halo) through the same bulk-copy ring; thread lh computes the PY outputs of
 // repetition lh from a 16-float shared-memory window in k_line_filter's tap order.
+// PX == 0 / SX == 0: taps (<= 16) and paving (a multiple of 4, >= 8) given at run time
+// (`tile_filter.line_stream`: strided 1-D line filters other than the config's 13 -> 3).
 template <int PX, int SX, int PY>
 __global__ void __launch_bounds__(512, 1) k_hline_stream(const float* __restrict__ x, const float* __restrict__ w,
-                                                         float* __restrict__ y, StreamGeom g, int n_consumer_warps) {
+                                                         float* __restrict__ y, StreamGeom g, int n_consumer_warps,
+                                                         int px_rt, int sx_rt) {
+  constexpr int PXM = PX > 0 ? PX : 16;
+  const int px = PX > 0 ? PX : px_rt;
+  const int sx = SX > 0 ? SX : sx_rt;
   extern __shared__ __align__(128) unsigned char fs_smem[];
   const int RS = (int)g.W + 8;
   float* stages = reinterpret_cast<float*>(fs_smem);
@@ -779,12 +788,12 @@ __global__ void __launch_bounds__(512, 1) k_hline_stream(const float* __restrict
   }
   const int lh = threadIdx.x;
   const bool active = lh < g.NLh;
-  const uint32_t win = (uint32_t)(SX * (active ? lh : 0)) * 4;
-  float wr[PY][PX];
+  const uint32_t win = (uint32_t)(sx * (active ? lh : 0)) * 4;
+  float wr[PY][PXM];
 #pragma unroll
   for (int j = 0; j < PY; ++j)
 #pragma unroll
-    for (int t = 0; t < PX; ++t) wr[j][t] = w[j * PX + t];
+    for (int t = 0; t < PXM; ++t) wr[j][t] = t < px ? w[j * px + t] : 0.0f;
   const uint32_t stage0 = smem_u32(stages), stage_bytes = (uint32_t)RS * 4;
   int stage = 0;
   uint32_t phase = 0;
@@ -809,7 +818,8 @@ __global__ void __launch_bounds__(512, 1) k_hline_stream(const float* __restrict
 #pragma unroll
     for (int c = 0; c < PY; ++c) hv[c] = 0.0f;
 #pragma unroll
-    for (int k = 0; k < PX; ++k) {
+    for (int k = 0; k < PXM; ++k) {
+      if (PX == 0 && k >= px) break;
 #pragma unroll
       for (int c = 0; c + 1 < PY; c += 2)
         add2_rn(hv[c], hv[c + 1], __fmul_rn(wr[c][k], xw[k]), __fmul_rn(wr[c + 1][k], xw[k]));
@@ -830,6 +840,15 @@ static bool hline_stream_ok(const LineGeom& g) {
   return g.inner == 1 && g.px == 13 && g.sx == 8 && g.py == 3 && g.sy == 3 && g.ox == 0 && g.oy == 0 &&
          g.NL * g.sx == g.Sx && g.NL * g.sy == g.Sy && g.Sx % 4 == 0 && g.NL <= 15 * 32 &&
          (size_t)FS_NST * (g.Sx + 8) * 4 + 256 <= 200 * 1024;
+}
+
+// other strided 1-D line filters through the same ring: 16 B-aligned windows of <= 16 taps whose
+// overhang past the row end fits the 8-float wrap halo
+static bool hline_stream_any_ok(const LineGeom& g) {
+  if (getenv("AOL_LINE_CLASSIC") || hline_stream_ok(g)) return false;
+  return g.inner == 1 && g.sx % 4 == 0 && g.sx >= 8 && g.px <= 16 && g.px <= g.sx + 8 && g.py >= 1 && g.py <= 4 &&
+         g.sy == g.py && g.ox == 0 && g.oy == 0 && g.NL * g.sx == g.Sx && g.NL * g.sy == g.Sy && g.Sx % 4 == 0 &&
+         g.NL <= 15 * 32 && (size_t)FS_NST * (g.Sx + 8) * 4 + 256 <= 200 * 1024;
 }
 
 static bool vline_stream_ok(const LineGeom& g) {
@@ -856,10 +875,12 @@ static int launch_line_stream(const LineGeom& lg, int64_t first, int64_t count, 
     g.Sy = lg.Sy;
     const int cw = (int)((lg.NL + 31) / 32);
     const size_t smem = (size_t)FS_NST * (g.W + 8) * 4 + 2 * FS_NST * sizeof(uint64_t);
-    auto kern = k_hline_stream<13, 8, 3>;
+    auto kern = hline_stream_ok(lg) ? k_hline_stream<13, 8, 3>
+                : lg.py == 1 ? k_hline_stream<0, 0, 1> : lg.py == 2 ? k_hline_stream<0, 0, 2>
+                : lg.py == 3 ? k_hline_stream<0, 0, 3> : k_hline_stream<0, 0, 4>;
     AOL_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t rows = g.last / g.NLh - g.first / g.NLh + 1;
-    kern<<<(int)(rows < sms ? rows : sms), (cw + 1) * 32, smem, s>>>(x, w, y, g, cw);
+    kern<<<(int)(rows < sms ? rows : sms), (cw + 1) * 32, smem, s>>>(x, w, y, g, cw, lg.px, (int)lg.sx);
     AOL_LAUNCH_CHECK("k_hline_stream");
     return AOL_OK;
   }

@@ -219,6 +219,7 @@ KERNEL_STAGING = {
     "tile_copy.affine2d": "HBM -> registers (V-element vectors along the inner pattern row) -> HBM",
     "tile_copy.stride2": "HBM -> registers (two 16 B source vectors per 4 repetitions) -> HBM (16 B stores)",
     "tile_filter.box_pool": "HBM -> registers (KH rows x 4*KW floats as float4) -> HBM (float4 stores)",
+    "tile_filter.line_stream": "HBM -> cp.async.bulk whole rows (+32 B wrap halo) -> 8-stage smem ring -> 16-float window per repetition -> registers -> HBM",
     "tile_filter.line_tiled": "HBM -> coalesced window per tile of <= 8192 repetitions -> padded smem -> registers -> HBM",
     "tile_sum.rows": "HBM -> cp.async 32x32 tiles (coalesced rows) -> smem ring (4 chunks) -> one ordered add chain per lane",
     "tile_sum.columns": "HBM -> TMA {32 columns x 8 KB} boxes -> 4-stage smem ring -> one ordered add chain per lane",

@@ -1265,13 +1265,15 @@ def test_tile_sum_plans_vs_oracle(case, plan, dtype, devices):
 @pytest.mark.parametrize("outer,S,px,sx,py,sy,ox", [
     (1, 5000, 8, 1, 1, 1, 0), (1, 4096, 16, 1, 1, 1, 4093), (3, 2000, 32, 1, 1, 1, 7), (2, 8192, 16, 4, 1, 1, 0),
     (4, 3000, 13, 8, 3, 3, 5), (2, 1000, 5, 2, 8, 8, 999), (1, 10000, 7, 3, 2, 2, 1), (2, 6000, 16, 8, 2, 2, 3),
-    (2, 4096, 12, 4, 2, 2, 0), (1, 4100, 9, 4, 1, 1, 8), (3, 2048, 16, 4, 1, 1, 4090)])
+    (2, 4096, 12, 4, 2, 2, 0), (1, 4100, 9, 4, 1, 1, 8), (3, 2048, 16, 4, 1, 1, 4090),
+    (2, 2048, 16, 8, 2, 2, 0), (3, 1600, 12, 16, 1, 1, 0), (1, 3072, 16, 12, 4, 4, 0), (2, 2048, 9, 8, 3, 3, 0)])
 @pytest.mark.parametrize("devices", [1, 3, 5])
 @pytest.mark.parametrize("wide", [False, True])
 def test_line_tiled_filters_vs_oracle(outer, S, px, sx, py, sy, ox, devices, wide, monkeypatch):
     """Generic horizontal line filters (1-D FIRs, decimating FIRs, wrapping windows, up to 8
-    outputs per repetition) through the 32-bit batched kernel (default) and the shared-memory
-    window kernel (`AOL_FILTER_WIDE`): bit-exact vs the oracle, shard starts anywhere inside a line."""
+    outputs per repetition) through the 32-bit batched kernel (default), the shared-memory
+    window kernel (`AOL_FILTER_WIDE`) and the row-streaming ring for strided windows
+    (`line_stream`): bit-exact vs the oracle, shard starts anywhere inside a line."""
     if wide:
         monkeypatch.setenv("AOL_FILTER_WIDE", "1")
     NL = (S - 1) // sx + 1 if sx > 1 else S
@@ -1284,7 +1286,9 @@ def test_line_tiled_filters_vs_oracle(outer, S, px, sx, py, sy, ox, devices, wid
     t = {"x": tx, "y": ty}
     w = (np.random.default_rng(px * 10 + py).standard_normal(px * py) / px).astype(np.float32)
     x = np.random.default_rng(S + px).standard_normal(outer * S).astype(np.float32)
-    want = ("tile_filter.line_13x3" if (px, py) == (13, 3) else
+    stream = (ox == 0 and sx % 4 == 0 and sx >= 8 and px <= min(16, sx + 8) and py <= 4 and sy == py
+              and NL * sx == S and (px, py) != (13, 3))
+    want = ("tile_filter.line_13x3" if (px, py) == (13, 3) else "tile_filter.line_stream" if stream else
             "tile_filter.line" if sx > 4 else "tile_filter.line_tiled" if wide else "tile_filter.batched")
     assert _plan([tx, ty]) == want
     got, ref = _filter_case("tile_filter", t, w, x, devices)
