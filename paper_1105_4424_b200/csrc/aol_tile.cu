@@ -311,33 +311,46 @@ __global__ void __launch_bounds__(256) k_tile_copy_vec(const T* __restrict__ src
 // (bulk-group completion).  The copy engine issues only the bytes of each box, the SM
 // issues one instruction per box, and no register ever holds the data.  One elected
 // thread per CTA drives the whole pipeline (2 CTAs per SM for >= 128 B rows).
+// Planes (`tile_copy.tma_plane`): tiles are {bw columns x R rows} boxes of ncb column blocks per
+// row block, loaded at column cs0 + cb*bw and stored at cd0 + cb*bw -- the maps' bases are the
+// 16 B-aligned addresses at or below each side's first element, so unaligned row starts (shifts,
+// crops) need no register path; the last boxes' overhang is zero-filled on load and clipped on store.
 template <int STAGES>
 __global__ void __launch_bounds__(32) k_tile_copy_tma(const __grid_constant__ CUtensorMap ms,
                                                       const __grid_constant__ CUtensorMap md, int64_t ntiles, int R,
-                                                      uint32_t stage_bytes, uint32_t stage_pitch) {
+                                                      uint32_t stage_bytes, uint32_t stage_pitch, int64_t ncb,
+                                                      int bw, int cs0, int cd0) {
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[STAGES];
   if (threadIdx.x != 0) return;
   for (int st = 0; st < STAGES; ++st) mbar_init(&full[st], 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   const int64_t mine = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;   // tiles blockIdx.x + k*gridDim.x
+  auto tile_rc = [&](int64_t k, int& row, int& col) {
+    const int64_t t = blockIdx.x + k * gridDim.x;
+    const int64_t rb = ncb == 1 ? t : t / ncb;
+    row = (int)(rb * R);
+    col = (int)(t - rb * ncb) * bw;
+  };
   auto load = [&](int64_t k) {
     const int st = (int)(k % STAGES);
-    const int row = (int)((blockIdx.x + k * gridDim.x) * R);
+    int row, col;
+    tile_rc(k, row, col);
     mbar_expect_tx(&full[st], stage_bytes);
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
             smem_u32(ring + (size_t)st * stage_pitch)),
-        "l"(&ms), "r"(0), "r"(row), "r"(smem_u32(&full[st]))
+        "l"(&ms), "r"(cs0 + col), "r"(row), "r"(smem_u32(&full[st]))
         : "memory");
   };
   for (int64_t k = 0; k < mine && k < STAGES; ++k) load(k);
   for (int64_t k = 0; k < mine; ++k) {
     const int st = (int)(k % STAGES);
     mbar_wait(&full[st], (uint32_t)((k / STAGES) & 1));
-    const int row = (int)((blockIdx.x + k * gridDim.x) * R);
-    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(&md), "r"(0),
-                 "r"(row), "r"(smem_u32(ring + (size_t)st * stage_pitch))
+    int row, col;
+    tile_rc(k, row, col);
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(&md),
+                 "r"(cd0 + col), "r"(row), "r"(smem_u32(ring + (size_t)st * stage_pitch))
                  : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     // refill the stage of box k-1 once its store has finished reading shared memory
@@ -1380,6 +1393,23 @@ static bool affine2_of(const aol_tiler& t, Affine2& o) {
   return true;
 }
 
+// 2-D rep space (pattern total 1) whose inner axis is contiguous on both sides: rows of L elements
+// at 16 B-multiple pitches As / Ad (>= L), whole rows in the launch range, >= 1 MB: `tile_copy.tma_plane`
+static bool plane_of(const aol_tiler& ts, const aol_tiler& td, int64_t first, int64_t count, size_t esz,
+                     int64_t& cs, int64_t& As, int64_t& cd, int64_t& Ad, int64_t& L) {
+  Affine2 a, b;
+  if (getenv("AOL_COPY_NO_PLANE") || tiler_pat_total(ts) != 1 || !affine2_of(ts, a) || !affine2_of(td, b)) return false;
+  L = a.nr1;
+  if (L < 32 || b.nr1 != L || a.A1 != 1 || b.A1 != 1 || a.A0 < L || b.A0 < L || (a.A0 * (int64_t)esz) % 16 ||
+      (b.A0 * (int64_t)esz) % 16 || first % L || count % L || count * (int64_t)esz < kTmaMinBytes)
+    return false;
+  cs = a.c;
+  As = a.A0;
+  cd = b.c;
+  Ad = b.A0;
+  return true;
+}
+
 struct CopyPlan {
   int kind;  // 0 generic, 1 affine1, 2 stream, 3 vector (V elements / thread), 4 transpose
   int64_t cs, As, Bs, cd, Ad, Bd;
@@ -1463,7 +1493,14 @@ const char* tile_copy_plan_name(const aol_tiler& ts, const aol_tiler& td, int64_
       if (pl.tma && aligned) return "tile_copy.tma_box";
       return pl.src_vec ? "tile_copy.vec" : "tile_copy.vec_store";
     case 2: return pl.tma ? "tile_copy.tma_stream" : "tile_copy.stream16";
-    case 5: return "tile_copy.affine2d";
+    case 5: {
+      int64_t cs, As, cd, Ad, L;
+      if (!plane_of(ts, td, first, count, esz, cs, As, cd, Ad, L)) return "tile_copy.affine2d";
+      const int64_t r0 = first / L;
+      const bool al = ((cs + As * r0) * (int64_t)esz) % 16 == 0 && ((cd + Ad * r0) * (int64_t)esz) % 16 == 0 &&
+                      (!ports || ((uintptr_t)ports[0] % 16 == 0 && (uintptr_t)ports[1] % 16 == 0));
+      return al ? "tile_copy.tma_plane" : esz == 4 ? "tile_copy.rows_shift" : "tile_copy.affine2d";
+    }
     case 1: return pl.As == 2 && pl.Ad == 1 && tiler_pat_total(ts) == 1 && esz == 4 ? "tile_copy.stride2" : "tile_copy.affine";
     default: {
       int64_t cuts[AOL_MAX_RANK][3];
@@ -1513,11 +1550,91 @@ static int launch_tma_rows(const void* src, void* dst, int64_t rows, int64_t P, 
     int sms = kNumSMs, dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)sms * cps);
-    void (*k)(const CUtensorMap, const CUtensorMap, int64_t, int, uint32_t, uint32_t) =
+    void (*k)(const CUtensorMap, const CUtensorMap, int64_t, int, uint32_t, uint32_t, int64_t, int, int, int) =
         stages == 16 ? k_tile_copy_tma<16> : stages == 8 ? k_tile_copy_tma<8> : k_tile_copy_tma<4>;
     // every ring above is <= 34 KB: within the default 48 KB dynamic shared memory limit
-    k<<<grid, 32, smem, stream>>>(ms, md, ntiles, R, stage_bytes, stage_pitch);
+    k<<<grid, 32, smem, stream>>>(ms, md, ntiles, R, stage_bytes, stage_pitch, 1, 0, 0, 0);
     AOL_LAUNCH_CHECK("k_tile_copy_tma");
+  }
+  return AOL_OK;
+}
+
+// Rows of L contiguous floats at any element offsets (2-D shifts' seam boxes, crops): TMA tiles
+// cannot start off 16 B, so each thread writes one 16 B-aligned float4 of a destination row and
+// builds it from the two aligned source float4s that straddle it (the neighbour lane loads the
+// same lines: L1 absorbs the second read).  Row heads/tails narrower than a float4 and loads that
+// would leave the source array go scalar.
+__global__ void __launch_bounds__(256) k_copy_rows_shift(const float* __restrict__ src, float* __restrict__ dst,
+                                                          int64_t rows, int64_t L, int64_t As, int64_t Ad,
+                                                          int64_t nq, const float* __restrict__ src_end) {
+  const int64_t total = rows * nq;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / nq, qi = e - r * nq;
+    float* drow = dst + r * Ad;
+    const float* srow = src + r * As;
+    const int head = (int)((4 - (((uintptr_t)drow >> 2) & 3)) & 3);   // elements before the first aligned float4
+    const int64_t j0 = qi == 0 ? 0 : head + (qi - 1) * 4;             // first row element this thread writes
+    const int64_t n = qi == 0 ? (head < L ? head : L) : (L - j0 < 4 ? L - j0 : 4);
+    if (qi == 0 || n < 4) {
+      for (int64_t j = j0; j < j0 + n; ++j) drow[j] = __ldg(srow + j);
+      continue;
+    }
+    const float* sp = srow + j0;
+    const int sh = (int)(((uintptr_t)sp >> 2) & 3);
+    const float4* a = reinterpret_cast<const float4*>(sp - sh);
+    float4 o;
+    if (sh == 0) {
+      o = __ldg(a);
+    } else if (reinterpret_cast<const float*>(a + 2) <= src_end) {
+      const float4 u = __ldg(a), v = __ldg(a + 1);
+      const float w[8] = {u.x, u.y, u.z, u.w, v.x, v.y, v.z, v.w};
+      o = sh == 1 ? make_float4(w[1], w[2], w[3], w[4]) : sh == 2 ? make_float4(w[2], w[3], w[4], w[5])
+                                                                  : make_float4(w[3], w[4], w[5], w[6]);
+    } else {
+      o = make_float4(__ldg(sp), __ldg(sp + 1), __ldg(sp + 2), __ldg(sp + 3));
+    }
+    *reinterpret_cast<float4*>(drow + j0) = o;
+  }
+}
+
+// Plane copy: `rows` rows of L contiguous elements starting at src / dst (any element alignment),
+// row pitches As / Ad (16 B multiples, >= L), through k_tile_copy_tma with {64 | 32 elements x 32 rows}
+// boxes (256 B x 32 = 8 KB), 4 stages, 2 CTAs per SM.
+static int launch_tma_plane(const void* src, void* dst, int64_t rows, int64_t L, int64_t As, int64_t Ad, size_t esz,
+                            cudaStream_t stream) {
+  auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(tensor_map_encoder());
+  if (!encode) return AOL_EUNSUPPORTED;
+  const int bw = (int)(256 / esz), R = 32;
+  const int cs0 = (int)(((uintptr_t)src % 16) / esz), cd0 = (int)(((uintptr_t)dst % 16) / esz);
+  if ((uintptr_t)src % esz || (uintptr_t)dst % esz) return AOL_EUNSUPPORTED;
+  const char* sb = static_cast<const char*>(src) - cs0 * esz;
+  char* db = static_cast<char*>(dst) - cd0 * esz;
+  const uint32_t stage_bytes = 8192;
+  const CUtensorMapDataType dt = esz == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32;
+  const int64_t ncb = (L + bw - 1) / bw;
+  const int64_t kMaxRows = (int64_t)1 << 24;   // tile indices and box coordinates stay in int32
+  for (int64_t r0 = 0; r0 < rows; r0 += kMaxRows) {
+    const int64_t n = std::min<int64_t>(kMaxRows, rows - r0);
+    CUtensorMap ms, md;
+    cuuint64_t sdims[2] = {(cuuint64_t)(cs0 + L), (cuuint64_t)n}, ddims[2] = {(cuuint64_t)(cd0 + L), (cuuint64_t)n};
+    cuuint64_t ss[1] = {(cuuint64_t)(As * (int64_t)esz)}, ds[1] = {(cuuint64_t)(Ad * (int64_t)esz)};
+    cuuint32_t box[2] = {(cuuint32_t)bw, (cuuint32_t)R}, es[2] = {1, 1};
+    if (encode(&ms, dt, 2, const_cast<char*>(sb + r0 * As * (int64_t)esz), sdims, ss, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||
+        encode(&md, dt, 2, db + r0 * Ad * (int64_t)esz, ddims, ds, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+            CUDA_SUCCESS) {
+      if (r0 == 0) return AOL_EUNSUPPORTED;
+      return fail(AOL_ECUDA, "cuTensorMapEncodeTiled failed for a tile_copy plane chunk");
+    }
+    const int64_t ntiles = ((n + R - 1) / R) * ncb;
+    int sms = kNumSMs, dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)sms * 2);
+    k_tile_copy_tma<4><<<grid, 32, 4 * stage_bytes, stream>>>(ms, md, ntiles, R, stage_bytes, stage_bytes, ncb, bw,
+                                                              cs0, cd0);
+    AOL_LAUNCH_CHECK("k_tile_copy_tma(plane)");
   }
   return AOL_OK;
 }
@@ -1769,6 +1886,23 @@ static int launch_tile_copy_t(const aol_tiler& ts, const aol_tiler& td, int64_t 
     p.kind = 1;
   }
   if (p.kind == 5) {
+    int64_t pcs, pAs, pcd, pAd, L;
+    if (plane_of(ts, td, first, count, sizeof(T), pcs, pAs, pcd, pAd, L)) {
+      const int64_t r0 = first / L, rows = count / L;
+      const T* s0 = s + pcs + pAs * r0;
+      T* d0 = d + pcd + pAd * r0;
+      if ((uintptr_t)s0 % 16 == 0 && (uintptr_t)d0 % 16 == 0) {
+        const int rc = launch_tma_plane(s0, d0, rows, L, pAs, pAd, sizeof(T), stream);
+        if (rc != AOL_EUNSUPPORTED) return rc;
+      } else if (sizeof(T) == 4 && (uintptr_t)d0 % 4 == 0 && (uintptr_t)s0 % 4 == 0 && (uintptr_t)s % 16 == 0) {
+        const int64_t nq = 1 + (L + 3) / 4;        // head (<= 3 elements) + float4s + ragged tail
+        const unsigned grid = grid_for(rows * nq, 256, 16);
+        k_copy_rows_shift<<<grid, 256, 0, stream>>>((const float*)s0, (float*)d0, rows, L, pAs, pAd, nq,
+                                                    (const float*)s + tiler_arr_total(ts));
+        AOL_LAUNCH_CHECK("k_copy_rows_shift");
+        return AOL_OK;
+      }
+    }
     Affine2 a, b;
     affine2_of(ts, a);
     affine2_of(td, b);

@@ -1463,3 +1463,36 @@ def test_generic_filter_batched32_vs_oracle(case, dtype, devices, wide, monkeypa
     ref = orc.run_tile_task("tile_filter", t, {"x": x, "w": w}, {"y": (ny, np_dt)}, R, devices)["y"]
     got = res.outputs["p_y"]
     assert got.dtype == np_dt and np.array_equal(got.view(np.uint8), ref.view(np.uint8)), (case, dtype)
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+@pytest.mark.parametrize("so,do", [((3, 5), (0, 2)), ((0, 0), (0, 0)), ((7, 1), (1, 3)), ((2, 4), (0, 1)),
+                                   ((4, 4), (4, 4)), ((1, 2), (3, 0))])
+@pytest.mark.parametrize("devices", [1, 3])
+def test_tile_copy_tma_plane_vs_oracle(dtype, so, do, devices):
+    """2-D crops / embeddings (rows contiguous on both sides at 16 B pitches, any element offset):
+    whole-row ranges go through TMA plane boxes when both row starts are 16 B-aligned
+    (`tile_copy.tma_plane`, last column/row boxes clipped), through the funnel-shift float4 kernel
+    otherwise (`tile_copy.rows_shift`, fp32); shard ranges that split rows through
+    `tile_copy.affine2d` -- all bit-exact vs the oracle."""
+    from paper_1105_4424_b200 import _capi
+    np_dt = np.dtype(dtype)
+    src = dict(array=(1030, 1100), rep=(1000, 1052), pattern=(1,), origin=so, paving=((1, 0), (0, 1)),
+               fitting=((0,), (0,)))
+    dst = dict(array=(1004, 1056), rep=(1000, 1052), pattern=(1,), origin=do, paving=((1, 0), (0, 1)),
+               fitting=((0,), (0,)))
+    ns, nd = 1030 * 1100, 1004 * 1056
+    x = (np.arange(ns) % 65521).astype(np_dt) + 1
+    ports = {"src": _spec(src, "in", dtype), "dst": _spec(dst, "out", dtype)}
+    res = _run_tile("tile_copy", {"src": src, "dst": dst}, ports, {"src": x}, devices)
+    R = 1000 * 1052
+    ref = orc.run_tile_task("tile_copy", {"src": src, "dst": dst}, {"src": x}, {"dst": (nd, np_dt)}, R, devices)["dst"]
+    got = res.outputs["p_dst"]
+    written = np.zeros(nd, bool)
+    written.reshape(1004, 1056)[do[0]:do[0] + 1000, do[1]:do[1] + 1052] = True
+    assert np.array_equal(got[written], ref[written])
+    task = _capi.make_task("tile_copy", dtype, [_tiler(src).bind(src["array"], src["rep"]),
+                                                _tiler(dst).bind(dst["array"], dst["rep"])])
+    aligned = ((so[0] * 1100 + so[1]) * np_dt.itemsize) % 16 == 0 and ((do[0] * 1056 + do[1]) * np_dt.itemsize) % 16 == 0
+    want = "tile_copy.tma_plane" if aligned else "tile_copy.rows_shift" if dtype == "float32" else "tile_copy.affine2d"
+    assert _capi.plan_name(task, 0, R) == want
