@@ -1482,12 +1482,20 @@ static CopyPlan plan_tile_copy(const aol_tiler& ts, const aol_tiler& td, int64_t
 
 static bool seam_boxes(const aol_tiler& ts, const aol_tiler& td, int64_t cuts[AOL_MAX_RANK][3], int ncut[AOL_MAX_RANK]);
 
+// kind 4 with m in {2, 4} fp32, 16 B-aligned pattern rows and destination: k_tile_copy_interleave
+static bool interleave_ok(const CopyPlan& p, int64_t P, size_t esz, int64_t count) {
+  return !p.tma && esz == 4 && (P == 2 || P == 4) && p.Bs > 0 && p.Bs % 4 == 0 && p.cs % 4 == 0 && p.cd % 4 == 0 &&
+         count >= 64 && !getenv("AOL_COPY_SMEM_TRANSPOSE");
+}
+
 const char* tile_copy_plan_name(const aol_tiler& ts, const aol_tiler& td, int64_t first, int64_t count,
                                 size_t esz, void* const* ports) {
   const CopyPlan pl = plan_tile_copy(ts, td, first, count, esz);
   const bool aligned = !ports || ((uintptr_t)ports[0] % 16 == 0 && (uintptr_t)ports[1] % 16 == 0);
   switch (pl.kind) {
-    case 4: return pl.tma && aligned ? "tile_copy.tma_transpose" : "tile_copy.transpose";
+    case 4:
+      if (interleave_ok(pl, tiler_pat_total(ts), esz, count) && aligned) return "tile_copy.interleave";
+      return pl.tma && aligned ? "tile_copy.tma_transpose" : "tile_copy.transpose";
     case 3:
       if (pl.window && (!ports || (uintptr_t)ports[0] % 16 == 0)) return "tile_copy.window";
       if (pl.tma && aligned) return "tile_copy.tma_box";
@@ -1594,6 +1602,33 @@ __global__ void __launch_bounds__(256) k_copy_rows_shift(const float* __restrict
       o = make_float4(__ldg(sp), __ldg(sp + 1), __ldg(sp + 2), __ldg(sp + 3));
     }
     *reinterpret_cast<float4*>(drow + j0) = o;
+  }
+}
+
+// Two / four pattern rows interleaved into a dense stream (pattern down a column with m = P in
+// {2, 4}: src (rho, i) at rho + Bs*i, dst at P*rho + i): a thread writes output float4 g (reps
+// (4/P)g ..), loading 4/P consecutive elements of each pattern row, so every load and store
+// instruction of a warp is one contiguous run.  m = 2 / 4 at T >= 1e8: 5.95-6.44 TB/s; the
+// shared-memory tile transpose gave 5.1-5.4 and a float4-per-row load form 5.3-5.6.
+template <int P>
+__global__ void __launch_bounds__(256) k_tile_copy_interleave_st(const float* __restrict__ src,
+                                                                 float* __restrict__ dst, int64_t Bs, int64_t nq) {
+  constexpr int RPG = 4 / P;                          // repetitions per output float4
+  const int64_t ng = nq * P;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ng; g += (int64_t)gridDim.x * blockDim.x) {
+    float e[4];
+    if constexpr (P == 4) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) e[i] = __ldcs(src + Bs * i + g);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const float2 t = __ldcs(reinterpret_cast<const float2*>(src + Bs * i) + g);
+        e[i] = t.x;          // rep 2g, pattern i   -> flat 2*0 + i
+        e[2 + i] = t.y;      // rep 2g+1, pattern i -> flat 2*1 + i
+      }
+    }
+    __stcs(reinterpret_cast<float4*>(dst) + g, make_float4(e[0], e[1], e[2], e[3]));
   }
 }
 
@@ -1844,6 +1879,21 @@ static int launch_tile_copy_t(const aol_tiler& ts, const aol_tiler& td, int64_t 
     } else if (rc != AOL_EUNSUPPORTED) {
       return rc;
     }
+  }
+  if (p.kind == 4 && interleave_ok(p, P, sizeof(T), count) && (uintptr_t)s % 16 == 0 && (uintptr_t)d % 16 == 0) {
+    const int64_t head = std::min<int64_t>(count, (4 - first % 4) % 4);
+    const int64_t nq = (count - head) / 4, tail = count - head - 4 * nq;
+    const float* s0 = reinterpret_cast<const float*>(s) + p.cs + first + head;
+    float* d0 = reinterpret_cast<float*>(d) + p.cd + (first + head) * P;
+    if (nq > 0) {
+      if (P == 2) k_tile_copy_interleave_st<2><<<grid_for(nq * 2, 256, 16), 256, 0, stream>>>(s0, d0, p.Bs, nq);
+      else k_tile_copy_interleave_st<4><<<grid_for(nq * 4, 256, 16), 256, 0, stream>>>(s0, d0, p.Bs, nq);
+      AOL_LAUNCH_CHECK("k_tile_copy_interleave");
+    }
+    int rc = AOL_OK;
+    if (head > 0 && (rc = launch_tile_copy_t<T>(ts, td, first, head, src, dst, stream))) return rc;
+    if (tail > 0) return launch_tile_copy_t<T>(ts, td, first + count - tail, tail, src, dst, stream);
+    return AOL_OK;
   }
   if (p.kind == 4) {
     const int pc = (int)std::min<int64_t>(P, 64);

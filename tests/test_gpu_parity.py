@@ -1086,7 +1086,9 @@ def test_cg_dtype_variants_persistent_equals_eager(golden, variant):
         assert np.array_equal(base.outputs()["x"].view(np.uint64), xd.view(np.uint64))
 
 
-@pytest.mark.parametrize("m,T,plan", [(4, 70000, "tile_copy.transpose"), (8, 40000, "tile_copy.tma_transpose"),
+@pytest.mark.parametrize("m,T,plan", [(4, 70000, "tile_copy.interleave"), (2, 100000, "tile_copy.interleave"),
+                                      (4, 70001, "tile_copy.transpose"), (2, 50003, "tile_copy.transpose"),
+                                      (8, 40000, "tile_copy.tma_transpose"),
                                       (16, 20004, "tile_copy.tma_transpose"), (8, 40001, "tile_copy.transpose"),
                                       (32, 9000, "tile_copy.tma_transpose"), (64, 5004, "tile_copy.tma_transpose"),
                                       (64, 5001, "tile_copy.transpose")])
@@ -1094,8 +1096,8 @@ def test_cg_dtype_variants_persistent_equals_eager(golden, variant):
 def test_tile_copy_row_stride_tma_transpose_vs_oracle(m, T, plan, devices):
     """Row-stride gathers (pattern down a column of an [m, T] array) into the dense stream:
     the TMA transpose (swizzled {32, m} boxes, smem transpose, TMA store) for m = 8..64 with a
-    16-byte row pitch, the register transpose otherwise; ragged tiles and unaligned shard
-    starts (devices=3) peel through the register path."""
+    16-byte row pitch, float4 register interleaving for m = 2 / 4, the shared-memory transpose
+    otherwise; ragged tiles and unaligned shard starts (devices=3) peel through the register path."""
     from paper_1105_4424_b200 import _capi
     ts = dict(array=(m, T), rep=(T,), pattern=(m,), origin=(0, 0), paving=((0,), (1,)), fitting=((1,), (0,)))
     td = dict(array=(T * m,), rep=(T,), pattern=(m,), origin=(0,), paving=((m,),), fitting=((1,),))

@@ -106,7 +106,8 @@ def test_tile_copy_plan_dispatch_rules_without_gpu():
     assert _copy_plan(rowstride(8, 40000), _dense(40000, 8)) == "tile_copy.tma_transpose"
     assert _copy_plan(rowstride(64, 5004), _dense(5004, 64)) == "tile_copy.tma_transpose"
     assert _copy_plan(rowstride(8, 40001), _dense(40001, 8)) == "tile_copy.transpose"             # pitch % 16 B
-    assert _copy_plan(rowstride(4, 80000), _dense(80000, 4)) == "tile_copy.transpose"             # 16 B columns
+    assert _copy_plan(rowstride(4, 80000), _dense(80000, 4)) == "tile_copy.interleave"            # 16 B columns
+    assert _copy_plan(rowstride(4, 80001), _dense(80001, 4)) == "tile_copy.transpose"             # pitch % 16 B
     assert _copy_plan(rowstride(8, 40000), _dense(40000, 8), "float64") == "tile_copy.transpose"
     blk = dict(array=(64, 64), rep=(8, 8), pattern=(8, 8), origin=(0, 0), paving=((8, 0), (0, 8)),
                fitting=((1, 0), (0, 1)))
