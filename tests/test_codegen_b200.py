@@ -1,4 +1,5 @@
-"""Row f4: generated B200 host programs (C++ over the C ABI) — compile here, run on the B200."""
+"""Row f4: generated B200 programs -- host C++ over the C ABI, and standalone CUDA text (kernels
+generated from the model) -- compile here, run on the B200."""
 
 import json
 import subprocess
@@ -83,6 +84,55 @@ def test_generated_programs_match_the_drop_in(golden, tmp_path):
         r = subprocess.run([str(exe), str(work)], capture_output=True, text=True, timeout=120)
         assert r.returncode == 0, r.stderr
         ref = execute_schedule(model, sched, bind, len(sched.device_steps()[0].launches))
+        for p in root.ports:
+            if enum_value(p.direction) == "out":
+                got = np.fromfile(work / f"{p.name}.out.bin", dtype=enum_value(p.data_type))
+                assert np.array_equal(got, ref.outputs[p.name]), (name, p.name)
+        if name == "cg":
+            assert f"iterations={ref.iterations} " in r.stdout
+
+
+def _nvcc(src: str, out: Path, link: bool) -> Path:
+    cu = out.with_suffix(".cu")
+    cu.write_text(src)
+    cmd = ["nvcc", "-std=c++17", "-O2", "-gencode", "arch=compute_100a,code=sm_100a", str(cu), "-o", str(out)]
+    r = subprocess.run(cmd if link else cmd[:-2] + ["-c", "-o", str(out)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    assert "warning" not in r.stderr, r.stderr
+    return out
+
+
+def test_generated_cuda_programs_compile(golden, tmp_path):
+    """backend="cuda": the kernels are CUDA text generated from the model (the analog of the
+    reference's OpenCL templates); the programs cross-compile for sm_100a without warnings."""
+    from paper_1105_4424_b200.codegen_b200 import generate_host_cpp, generate_kernels_cu
+    for name, model, sched, _ in _cases(golden):
+        src = generate_host_cpp(model, sched, backend="cuda")
+        assert "aol_launch" not in src and "__global__ void k_" in src
+        assert generate_kernels_cu(model, sched) in src
+        _nvcc(src, tmp_path / f"{name}.o", link=False)
+
+
+@pytest.mark.gpu
+def test_generated_cuda_programs_match_the_drop_in(golden, tmp_path):
+    """The generated CUDA programs are bit-identical to execute_schedule: CG (same iteration count,
+    the same deterministic dot tree), the exact-order matmul (precision="exact") and the stencil."""
+    from paper_1105_4424_b200.codegen_b200 import generate_host_cpp
+    from paper_1105_4424_b200.executor import execute_schedule
+    from paper_1105_4424_b200.model import enum_value
+    for name, model, sched, bind in _cases(golden):
+        exe = _nvcc(generate_host_cpp(model, sched, backend="cuda"), tmp_path / name, link=True)
+        work = tmp_path / f"{name}_io"
+        work.mkdir()
+        root = model.application_components[model.application_root]
+        for p in root.ports:
+            if enum_value(p.direction) in ("in", "inout"):
+                np.ascontiguousarray(np.asarray(bind[p.name]).astype(enum_value(p.data_type))).tofile(
+                    work / f"{p.name}.bin")
+        r = subprocess.run([str(exe), str(work)], capture_output=True, text=True, timeout=120)
+        assert r.returncode == 0, r.stderr
+        kw = {"precision": "exact"} if name == "matmul" else {}
+        ref = execute_schedule(model, sched, bind, len(sched.device_steps()[0].launches), **kw)
         for p in root.ports:
             if enum_value(p.direction) == "out":
                 got = np.fromfile(work / f"{p.name}.out.bin", dtype=enum_value(p.data_type))
