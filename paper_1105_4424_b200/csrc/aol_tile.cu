@@ -1574,34 +1574,36 @@ static int launch_tma_rows(const void* src, void* dst, int64_t rows, int64_t P, 
 // would leave the source array go scalar.
 __global__ void __launch_bounds__(256) k_copy_rows_shift(const float* __restrict__ src, float* __restrict__ dst,
                                                           int64_t rows, int64_t L, int64_t As, int64_t Ad,
-                                                          int64_t nq, const float* __restrict__ src_end) {
-  const int64_t total = rows * nq;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = e / nq, qi = e - r * nq;
+                                                          int64_t vblocks, const float* __restrict__ src_end) {
+  // block b -> (row, 256-float4 chunk): thread q writes the row's aligned float4 q; the thread one
+  // past the last float4 writes the scalar head and tail
+  for (int64_t b = blockIdx.x; b < rows * vblocks; b += gridDim.x) {
+    const int64_t r = b / vblocks;
+    const int64_t q = (b - r * vblocks) * 256 + threadIdx.x;
     float* drow = dst + r * Ad;
     const float* srow = src + r * As;
-    const int head = (int)((4 - (((uintptr_t)drow >> 2) & 3)) & 3);   // elements before the first aligned float4
-    const int64_t j0 = qi == 0 ? 0 : head + (qi - 1) * 4;             // first row element this thread writes
-    const int64_t n = qi == 0 ? (head < L ? head : L) : (L - j0 < 4 ? L - j0 : 4);
-    if (qi == 0 || n < 4) {
-      for (int64_t j = j0; j < j0 + n; ++j) drow[j] = __ldg(srow + j);
-      continue;
+    const int64_t head = (int64_t)((4 - (((uintptr_t)drow >> 2) & 3)) & 3) < L ? (int64_t)((4 - (((uintptr_t)drow >> 2) & 3)) & 3) : L;
+    const int64_t nvec = (L - head) >> 2;
+    if (q < nvec) {
+      const int64_t j0 = head + 4 * q;
+      const float* sp = srow + j0;
+      const int sh = (int)(((uintptr_t)sp >> 2) & 3);
+      const float4* a = reinterpret_cast<const float4*>(sp - sh);
+      float4 o;
+      if (sh == 0) {
+        o = __ldg(a);
+      } else if (reinterpret_cast<const float*>(a + 2) <= src_end) {
+        const float4 u = __ldg(a), v = __ldg(a + 1);
+        o = sh == 1 ? make_float4(u.y, u.z, u.w, v.x) : sh == 2 ? make_float4(u.z, u.w, v.x, v.y)
+                                                                : make_float4(u.w, v.x, v.y, v.z);
+      } else {
+        o = make_float4(__ldg(sp), __ldg(sp + 1), __ldg(sp + 2), __ldg(sp + 3));
+      }
+      *reinterpret_cast<float4*>(drow + j0) = o;
+    } else if (q == nvec) {
+      for (int64_t j = 0; j < head; ++j) drow[j] = __ldg(srow + j);
+      for (int64_t j = head + 4 * nvec; j < L; ++j) drow[j] = __ldg(srow + j);
     }
-    const float* sp = srow + j0;
-    const int sh = (int)(((uintptr_t)sp >> 2) & 3);
-    const float4* a = reinterpret_cast<const float4*>(sp - sh);
-    float4 o;
-    if (sh == 0) {
-      o = __ldg(a);
-    } else if (reinterpret_cast<const float*>(a + 2) <= src_end) {
-      const float4 u = __ldg(a), v = __ldg(a + 1);
-      const float w[8] = {u.x, u.y, u.z, u.w, v.x, v.y, v.z, v.w};
-      o = sh == 1 ? make_float4(w[1], w[2], w[3], w[4]) : sh == 2 ? make_float4(w[2], w[3], w[4], w[5])
-                                                                  : make_float4(w[3], w[4], w[5], w[6]);
-    } else {
-      o = make_float4(__ldg(sp), __ldg(sp + 1), __ldg(sp + 2), __ldg(sp + 3));
-    }
-    *reinterpret_cast<float4*>(drow + j0) = o;
   }
 }
 
@@ -1945,9 +1947,9 @@ static int launch_tile_copy_t(const aol_tiler& ts, const aol_tiler& td, int64_t 
         const int rc = launch_tma_plane(s0, d0, rows, L, pAs, pAd, sizeof(T), stream);
         if (rc != AOL_EUNSUPPORTED) return rc;
       } else if (sizeof(T) == 4 && (uintptr_t)d0 % 4 == 0 && (uintptr_t)s0 % 4 == 0 && (uintptr_t)s % 16 == 0) {
-        const int64_t nq = 1 + (L + 3) / 4;        // head (<= 3 elements) + float4s + ragged tail
-        const unsigned grid = grid_for(rows * nq, 256, 16);
-        k_copy_rows_shift<<<grid, 256, 0, stream>>>((const float*)s0, (float*)d0, rows, L, pAs, pAd, nq,
+        const int64_t vblocks = (L / 4 + 1 + 255) / 256;   // float4s + the head/tail thread, per row
+        const unsigned grid = (unsigned)std::min<int64_t>(rows * vblocks, (int64_t)kNumSMs * 64);
+        k_copy_rows_shift<<<grid, 256, 0, stream>>>((const float*)s0, (float*)d0, rows, L, pAs, pAd, vblocks,
                                                     (const float*)s + tiler_arr_total(ts));
         AOL_LAUNCH_CHECK("k_copy_rows_shift");
         return AOL_OK;
