@@ -1411,7 +1411,7 @@ def test_tile_copy_toroidal_shift_vs_oracle(shape, origin, devices):
                             n, devices)["dst"]
     assert np.array_equal(res.outputs["p_dst"], ref)
     task = _capi.make_task("tile_copy", "float32", [_tiler(src).bind(shape, shape), _tiler(dst).bind(shape, shape)])
-    assert _capi.plan_name(task, 0, n) == ("tile_copy.seam_boxes" if a > 1 else "tile_copy.generic")
+    assert _capi.plan_name(task, 0, n) == "tile_copy.seam_boxes"
 
 
 def _generic_filter_cases():
