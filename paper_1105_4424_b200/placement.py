@@ -215,7 +215,7 @@ KERNEL_STAGING = {
     "tile_copy.stream16": "HBM -> registers (16 B vectors, streaming hints) -> HBM",
     "tile_copy.tma_stream": "HBM -> TMA 256 B-row boxes -> shared-memory ring (4 x 8 KB, 2 CTAs/SM) -> TMA store -> HBM",
     "tile_copy.tma_transpose": "HBM -> TMA {32 reps, m} boxes (128B swizzle) -> smem transpose -> TMA store -> HBM",
-    "tile_copy.seam_boxes": "split at the wrap seams into affine boxes, each on the affine / affine2d register paths",
+    "tile_copy.seam_boxes": "split at the wrap seams into affine boxes, each on its own plan (rows_shift / tma_plane / stream / affine2d)",
     "tile_copy.interleave": "HBM -> one float4 per pattern row (m = 2 / 4) -> register transpose -> m float4 stores -> HBM",
     "tile_copy.tma_plane": "HBM -> TMA {256 B x 32 rows} boxes -> 4-stage smem ring -> TMA store -> HBM",
     "tile_copy.rows_shift": "HBM -> two aligned float4 loads (L1) -> funnel shift in registers -> aligned float4 store -> HBM",
