@@ -1498,3 +1498,36 @@ def test_tile_copy_tma_plane_vs_oracle(dtype, so, do, devices):
     aligned = ((so[0] * 1100 + so[1]) * np_dt.itemsize) % 16 == 0 and ((do[0] * 1056 + do[1]) * np_dt.itemsize) % 16 == 0
     want = "tile_copy.tma_plane" if aligned else "tile_copy.rows_shift" if dtype == "float32" else "tile_copy.affine2d"
     assert _capi.plan_name(task, 0, R) == want
+
+
+@pytest.mark.parametrize("seed", range(8))
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+def test_random_long_rows_batched_filters_vs_oracle(seed, dtype):
+    """Random filter tilers whose last repetition axis is long (200-700), so the 32-bit batched
+    kernel's lane runs (32 x R repetitions of one row) and its wrapping / row-leaving fallbacks
+    all occur: negative pavings and fittings, toroidal origins, 1-4 outputs written through a
+    shifted (wrapping) dense output tiler, several shard counts -- bit-exact vs the oracle."""
+    rng = np.random.default_rng(5000 + seed)
+    np_dt = np.dtype(dtype)
+    for _ in range(3):
+        q = int(rng.integers(1, 3))
+        rep = tuple(int(x) for x in rng.integers(2, 5, q - 1)) + (int(rng.integers(200, 700)),)
+        p = int(rng.integers(1, 3))
+        pat = tuple(int(x) for x in rng.integers(1, 5, p))
+        a = int(rng.integers(1, 3))
+        arr = tuple(int(x) for x in rng.integers(50, 900, a))
+        tx = dict(array=arr, rep=rep, pattern=pat, origin=tuple(int(x) for x in rng.integers(-900, 900, a)),
+                  paving=tuple(tuple(int(x) for x in rng.integers(-4, 5, q)) for _ in range(a)),
+                  fitting=tuple(tuple(int(x) for x in rng.integers(-3, 4, p)) for _ in range(a)))
+        R, P = int(np.prod(rep)), int(np.prod(pat))
+        py = int(rng.integers(1, 5))
+        ty = _dense_out(rep, (py,))
+        ty = dict(ty, origin=(int(rng.integers(0, R * py)),))
+        nx = int(np.prod(arr))
+        x = rng.standard_normal(nx).astype(np_dt)
+        w = rng.standard_normal(py * P).astype(np_dt)
+        d = int(rng.integers(1, 4))
+        ports = {"x": _spec(tx, "in", dtype), "w": f"in {dtype} [{w.size}]", "y": _spec(ty, "out", dtype)}
+        got = _run_tile("tile_filter", {"x": tx, "y": ty}, ports, {"x": x, "w": w}, d).outputs["p_y"]
+        ref = orc.run_tile_task("tile_filter", {"x": tx, "y": ty}, {"x": x, "w": w}, {"y": (R * py, np_dt)}, R, d)
+        assert np.array_equal(got.view(np.uint8), ref["y"].view(np.uint8)), (tx, ty)
