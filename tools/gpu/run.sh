@@ -1,1 +1,5 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "random_long_rows or random_tilers" > gpurun_out/t.log 2>&1; echo t=$?
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo s=$?
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/t.log 2>&1; echo t=$?
+timeout 900 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; echo b=$?
+timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo r=$?
+for w in stencil downscaler cg cg27 c1; do timeout 900 python bench.py --workload $w > gpurun_out/bench_$w.json 2> gpurun_out/bench_$w.err; echo $w=$?; done
