@@ -1,5 +1,1 @@
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo s=$?
-timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/t.log 2>&1; echo t=$?
-timeout 900 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; echo b=$?
-timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo r=$?
-for w in stencil downscaler cg cg27 c1; do timeout 900 python bench.py --workload $w > gpurun_out/bench_$w.json 2> gpurun_out/bench_$w.err; echo $w=$?; done
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_copy_rows_shift -c 1 -o gpurun_out/rows_shift python tools/gpu/crop_probe.py > gpurun_out/ncu_rs.log 2>&1; echo a=$?
