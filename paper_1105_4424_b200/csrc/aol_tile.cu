@@ -912,7 +912,7 @@ __global__ void __launch_bounds__(256) k_filter_batched32(const T* __restrict__ 
   int32_t* oy = ox + px;
   int32_t* rx = oy + py;                                     // raw per-dim pattern coordinates
   int32_t* ry = rx + px * tx.a;
-  for (int k = threadIdx.x; k < px * py; k += blockDim.x) ws[k] = w[k];
+  for (int k = threadIdx.x; k < px * py; k += blockDim.x) ws[k] = w ? w[k] : T(1);   // no w: tile_sum (1*x == x)
   for (int k = threadIdx.x; k < px + py; k += blockDim.x) {
     const bool isx = k < px;
     const DevTiler& t = isx ? tx : ty;
@@ -2322,15 +2322,25 @@ static int tile_sum_kind(const aol_task& t, int64_t& cs, int64_t& As, int64_t& B
   return dummy <= kTableMax ? 2 : 3;
 }
 
+// Wrapping patterns and strided non-column patterns: tile_sum is the one-output filter with unit
+// weights (1*x == x bit for bit, so the sums are the same), so the 32-bit batched filter kernel
+// serves it (`tile_sum.batched`).
+static bool tile_sum_batched_ok(const aol_task& t, int64_t first, int64_t count, int64_t As) {
+  DevTiler a, b;
+  (void)As;
+  return count >= 1024 && filter_batched_route(t, first, count, a, b);
+}
+
 const char* tile_sum_plan_name(const aol_task& t) {
   int64_t cs, As, Bs;
   switch (tile_sum_kind(t, cs, As, Bs)) {
     case 0: return "tile_sum.rows";
     case 1:
-      return tile_sum_cols_ok(As, Bs, tiler_pat_total(t.tilers[0]), tiler_rep_total(t.tilers[0]),
-                              t.dtype == AOL_F32 ? 4 : 8) ? "tile_sum.columns" : "tile_sum.direct";
-    case 2: return "tile_sum.generic";
-    default: return "tile_sum.generic_direct";
+      if (tile_sum_cols_ok(As, Bs, tiler_pat_total(t.tilers[0]), tiler_rep_total(t.tilers[0]), t.dtype == AOL_F32 ? 4 : 8))
+        return "tile_sum.columns";
+      return As != 1 && tile_sum_batched_ok(t, 0, tiler_rep_total(t.tilers[0]), As) ? "tile_sum.batched" : "tile_sum.direct";
+    case 2: return tile_sum_batched_ok(t, 0, tiler_rep_total(t.tilers[0]), As) ? "tile_sum.batched" : "tile_sum.generic";
+    default: return tile_sum_batched_ok(t, 0, tiler_rep_total(t.tilers[0]), As) ? "tile_sum.batched" : "tile_sum.generic_direct";
   }
 }
 
@@ -2413,6 +2423,13 @@ int launch_tile_sum(const aol_task& t, int64_t first, int64_t count, void* const
              : launch_tile_sum_cols<double>((const double*)ports[0], (double*)ports[1], ts, cs, Bs, px, first, count,
                                             stream);
     if (rc <= 0) return rc;
+  }
+  if ((kind >= 2 || (kind == 1 && As != 1)) && tile_sum_batched_ok(t, first, count, As)) {
+    DevTiler bx, by;
+    filter_batched_route(t, first, count, bx, by);
+    void* fp[3] = {ports[0], nullptr, ports[1]};
+    return f32 ? launch_filter_b32_q<float, 1, 8>(t, bx, by, first, count, (int)px, 1, fp, stream)
+               : launch_filter_b32_q<double, 1, 8>(t, bx, by, first, count, (int)px, 1, fp, stream);
   }
   if (kind == 1 || kind == 3) {
     const unsigned grid = grid_for(count, 256, 16);

@@ -225,6 +225,7 @@ KERNEL_STAGING = {
     "tile_filter.line_stream": "HBM -> cp.async.bulk whole rows (+32 B wrap halo) -> 8-stage smem ring -> 16-float window per repetition -> registers -> HBM",
     "tile_filter.line_tiled": "HBM -> coalesced window per tile of <= 8192 repetitions -> padded smem -> registers -> HBM",
     "tile_sum.rows": "HBM -> cp.async 32x32 tiles (coalesced rows) -> smem ring (4 chunks) -> one ordered add chain per lane",
+    "tile_sum.batched": "the batched filter kernel with unit weights: int32 pattern tables in smem, 8 repetitions per lane, window in registers",
     "tile_sum.columns": "HBM -> TMA {32 columns x 8 KB} boxes -> 4-stage smem ring -> one ordered add chain per lane",
     "tile_sum.direct": "HBM -> registers (64 loads in flight per repetition) -> ordered add chain",
     "tile_copy.window": "HBM -> one bulk copy per tile of the overlapping source window -> smem ring -> registers (16 B stores) -> HBM",

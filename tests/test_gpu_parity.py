@@ -1224,13 +1224,14 @@ def test_stencil_wide_windows_vs_oracle(kh, kw, H, W, devices):
                                        ("rows_pitch", "tile_sum.rows"),
                                        ("cols", "tile_sum.columns"), ("cols_small", "tile_sum.direct"),
                                        ("cols_pitch", "tile_sum.columns"), ("wrap_small", "tile_sum.generic"),
+                                       ("wrap_long", "tile_sum.batched"), ("strided", "tile_sum.batched"),
                                        ("wrap_big", "tile_sum.generic_direct")])
 @pytest.mark.parametrize("dtype", ["float32", "float64"])
 @pytest.mark.parametrize("devices", [1, 3])
 def test_tile_sum_plans_vs_oracle(case, plan, dtype, devices):
     """Pattern reductions (i ascending, one rounding per add) on every tile_sum plan: coalesced
     warp-transposed and TMA-swizzled row sums, TMA-streamed column sums (shard starts off 16 B), direct affine
-    sums, the offset-table generic form
+    sums, the batched unit-weight filter kernel (wrapping or strided patterns), the offset-table generic form
     and the table-free form for large wrapping patterns -- bit-exact against the oracle."""
     if case in ("rows", "rows_ragged"):
         R, P = (300, 1000) if case == "rows" else (77, 45)
@@ -1246,6 +1247,12 @@ def test_tile_sum_plans_vs_oracle(case, plan, dtype, devices):
         # columns 5..1004 of a 2-D array with a wider row pitch, 1000 rows (partial last box)
         R, P = 1000, 1000
         tx = dict(array=(P, 1024), rep=(R,), pattern=(P,), origin=(0, 5), paving=((0,), (1,)), fitting=((1,), (0,)))
+    elif case == "wrap_long":
+        R, P = 4000, 9
+        tx = dict(array=(5000,), rep=(R,), pattern=(P,), origin=(4995,), paving=((1,),), fitting=((1,),))
+    elif case == "strided":
+        R, P = 3000, 7
+        tx = dict(array=(30000,), rep=(R,), pattern=(P,), origin=(11,), paving=((3,),), fitting=((2,),))
     elif case == "wrap_small":
         R, P = 500, 9
         tx = dict(array=(600,), rep=(R,), pattern=(P,), origin=(595,), paving=((1,),), fitting=((1,),))
