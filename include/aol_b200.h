@@ -140,6 +140,12 @@ int aol_tiler_offsets(const aol_tiler* tiler, int64_t first, int64_t count,
 /* Number of kernels this library has launched in this process (evidence counter). */
 int64_t aol_launch_counter(void);
 
+/* Free the library's cached device scratch: the per-(device, stream) dot_partial partials
+ * (bounded LRU cache of 64 entries) and the persistent loop's per-device block.  Waits for
+ * each owning device to go idle first; scratch pinned by a live aol_loop graph is kept.
+ * The next launch that needs scratch allocates it again.  No reference counterpart. */
+int aol_release_scratch(void);
+
 /* Task fusion: run `consumer` over its repetitions [first, first+count) computing
  * the part of `producer`'s output it reads on the fly, in shared memory, instead of
  * reading a materialised intermediate array (bit-identical results; the

@@ -28,7 +28,7 @@ PRECISION = {"default": 0, "tf32": 1, "3xtf32": 2, "exact": 3}
 
 EXPORTS = ("aol_abi_version", "aol_last_error", "aol_device_count", "aol_validate", "aol_launch",
            "aol_plan_name", "aol_tiler_offsets", "aol_launch_counter", "aol_launch_fused2", "aol_loop_begin",
-           "aol_loop_end", "aol_loop_run", "aol_loop_destroy", "aol_loop_persistent")
+           "aol_loop_end", "aol_loop_run", "aol_loop_destroy", "aol_loop_persistent", "aol_release_scratch")
 
 
 class NativeLibraryError(RuntimeError):
@@ -230,6 +230,11 @@ def loop_run(handle: int, stream: int) -> tuple[int, float, bool]:
 def loop_destroy(handle: int) -> None:
     if handle:
         load().aol_loop_destroy(C.c_void_p(handle))
+
+
+def release_scratch() -> None:
+    """Free the library's cached dot / loop scratch (aol_release_scratch)."""
+    check(load().aol_release_scratch())
 
 
 def launch_counter() -> int:

@@ -42,6 +42,8 @@ int launch_gemm_batched(const aol_task& t, int64_t first, int64_t count, void* c
 int launch_fused_line_filters(const aol_task& th, const aol_task& tv, int64_t first, int64_t count,
                               void* const* ph, void* const* pv, cudaStream_t s);
 int launch_gemm_tf32(const aol_task& t, int64_t first, int64_t count, void* const* ports, cudaStream_t s);
+int release_dot_scratch();
+int release_loop_scratch();
 
 static int tilers_needed(int op) {
   switch (op) {
@@ -168,6 +170,12 @@ int aol_tiler_offsets(const aol_tiler* tiler, int64_t first, int64_t count, int6
 }
 
 int64_t aol_launch_counter(void) { return g_launches.load(); }
+
+int aol_release_scratch(void) {
+  release_dot_scratch();
+  release_loop_scratch();
+  return AOL_OK;
+}
 
 int aol_launch_fused2(const aol_task* producer, const aol_task* consumer, int64_t first, int64_t count,
                       void* const* producer_ports, void* const* consumer_ports, void* stream) {

@@ -113,21 +113,73 @@ struct ScalarSeq {
 
 // kDotBlocks partials followed by the ticket counter, per (device, stream): dots on one
 // stream are ordered, dots on different streams never share partials or tickets.  Zeroed
-// once; the last block of every dot resets the ticket.
-static double* dot_scratch(int dev, cudaStream_t stream) {
-  static std::mutex mu;
-  static std::map<std::pair<int, cudaStream_t>, double*> bufs;
-  std::lock_guard<std::mutex> lock(mu);
-  auto it = bufs.find({dev, stream});
-  if (it != bufs.end()) return it->second;
+// once; the last block of every dot resets the ticket.  The cache is bounded: past
+// kMaxDotScratch entries the least recently used unpinned one is freed (after its device
+// is idle), and aol_release_scratch() frees every unpinned entry.  Captured device loops
+// pin the scratch of their stream (the graph holds its address) until aol_loop_destroy.
+struct DotScratch {
+  double* p = nullptr;
+  int pins = 0;
+  uint64_t used = 0;
+};
+constexpr size_t kMaxDotScratch = 64;
+static std::mutex g_scratch_mu;
+static std::map<std::pair<int, cudaStream_t>, DotScratch> g_scratch;
+static uint64_t g_scratch_tick = 0;
+
+static double* dot_scratch(int dev, cudaStream_t stream, int pin_delta = 0) {
+  std::lock_guard<std::mutex> lock(g_scratch_mu);
+  auto it = g_scratch.find({dev, stream});
+  if (it != g_scratch.end()) {
+    it->second.used = ++g_scratch_tick;
+    it->second.pins += pin_delta;
+    return it->second.p;
+  }
+  if (pin_delta < 0) return nullptr;
+  if (g_scratch.size() >= kMaxDotScratch) {
+    auto victim = g_scratch.end();
+    for (auto v = g_scratch.begin(); v != g_scratch.end(); ++v)
+      if (v->second.pins == 0 && (victim == g_scratch.end() || v->second.used < victim->second.used)) victim = v;
+    if (victim != g_scratch.end()) {
+      int cur = 0;
+      cudaGetDevice(&cur);
+      cudaSetDevice(victim->first.first);
+      cudaDeviceSynchronize();               // no kernel still reads the victim's partials
+      cudaFree(victim->second.p);
+      cudaSetDevice(cur);
+      g_scratch.erase(victim);
+    }
+  }
   double* p = nullptr;
   if (cudaMalloc(&p, (kDotBlocks + 1) * sizeof(double)) != cudaSuccess) return nullptr;
   if (cudaMemset(p, 0, (kDotBlocks + 1) * sizeof(double)) != cudaSuccess) {
     cudaFree(p);
     return nullptr;
   }
-  bufs[{dev, stream}] = p;
+  DotScratch e;
+  e.p = p;
+  e.pins = pin_delta;
+  e.used = ++g_scratch_tick;
+  g_scratch[{dev, stream}] = e;
   return p;
+}
+
+int release_dot_scratch() {
+  std::lock_guard<std::mutex> lock(g_scratch_mu);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (auto it = g_scratch.begin(); it != g_scratch.end();) {
+    if (it->second.pins > 0) {
+      ++it;
+      continue;
+    }
+    cudaSetDevice(it->first.first);
+    cudaDeviceSynchronize();
+    cudaFree(it->second.p);
+    it = g_scratch.erase(it);
+  }
+  cudaSetDevice(cur);
+  return (int)g_scratch.size();
 }
 
 // Host scalar ops of the reference (refexec.py:462-474) as one-thread device kernels, so a
@@ -166,10 +218,10 @@ __global__ void k_scalar_seq(ScalarSeq q) {
   }
 }
 
-double* dot_scratch_for_stream(cudaStream_t stream) {
+double* dot_scratch_for_stream(cudaStream_t stream, int pin_delta) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
-  return dot_scratch(dev, stream);
+  return dot_scratch(dev, stream, pin_delta);
 }
 
 template <typename T>

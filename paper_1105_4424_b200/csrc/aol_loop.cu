@@ -11,7 +11,7 @@
 
 namespace aol {
 
-double* dot_scratch_for_stream(cudaStream_t stream);
+double* dot_scratch_for_stream(cudaStream_t stream, int pin_delta);
 
 struct LoopState {
   int64_t iterations;
@@ -48,6 +48,7 @@ struct aol_loop {
   double tol = 0;
   int64_t max_iter = 0;
   aol::LoopState* state = nullptr;
+  int device = 0;
 };
 
 using namespace aol;
@@ -58,11 +59,13 @@ int aol_loop_begin(void* stream, const void* relres_dev, int relres_dtype, doubl
                    aol_loop** out) {
   if (!stream || !relres_dev || !out || max_iter < 1) return fail(AOL_EINVAL, "aol_loop_begin: bad arguments");
   if (relres_dtype != AOL_F32 && relres_dtype != AOL_F64) return fail(AOL_EINVAL, "relres must be float32/float64");
-  // dots captured on this stream use its scratch: allocate it now (no cudaMalloc during capture)
-  if (!dot_scratch_for_stream(static_cast<cudaStream_t>(stream))) return fail(AOL_ECUDA, "cannot allocate dot scratch");
+  // dots captured on this stream use its scratch: allocate it now (no cudaMalloc during
+  // capture) and pin it for the graph's lifetime (aol_loop_destroy unpins)
+  if (!dot_scratch_for_stream(static_cast<cudaStream_t>(stream), 1)) return fail(AOL_ECUDA, "cannot allocate dot scratch");
   aol_loop* L = new (std::nothrow) aol_loop();
   if (!L) return fail(AOL_ECUDA, "out of host memory");
   L->stream = static_cast<cudaStream_t>(stream);
+  cudaGetDevice(&L->device);
   L->relres = relres_dev;
   L->relres_dtype = relres_dtype;
   L->tol = tol;
@@ -84,6 +87,7 @@ int aol_loop_begin(void* stream, const void* relres_dev, int relres_dtype, doubl
   if (e != cudaSuccess) {
     if (L->graph) cudaGraphDestroy(L->graph);
     if (L->state) cudaFree(L->state);
+    dot_scratch_for_stream(L->stream, -1);
     delete L;
     return cuda_fail(e, "aol_loop_begin");
   }
@@ -127,6 +131,11 @@ int aol_loop_destroy(aol_loop* L) {
   if (L->exec) cudaGraphExecDestroy(L->exec);
   if (L->graph) cudaGraphDestroy(L->graph);
   if (L->state) cudaFree(L->state);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (L->device != cur) cudaSetDevice(L->device);
+  dot_scratch_for_stream(L->stream, -1);
+  if (L->device != cur) cudaSetDevice(cur);
   delete L;
   return AOL_OK;
 }

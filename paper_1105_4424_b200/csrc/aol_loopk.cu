@@ -729,6 +729,28 @@ static int build_sell(const aol_loop_op& o, void* const* ports, SellBufs& b, LSe
 
 using namespace aol;
 
+namespace aol {
+// persistent-loop scratch, one block per device, allocated on first use (see below)
+static std::mutex g_loop_locks[64];
+static char* g_loop_scratch[64] = {nullptr};
+static int g_loop_fits[64] = {0};
+
+int release_loop_scratch() {
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (int d = 0; d < 64; ++d) {
+    std::lock_guard<std::mutex> lock(g_loop_locks[d]);
+    if (!g_loop_scratch[d]) continue;
+    cudaSetDevice(d);
+    cudaDeviceSynchronize();
+    cudaFree(g_loop_scratch[d]);
+    g_loop_scratch[d] = nullptr;
+  }
+  cudaSetDevice(cur);
+  return 0;
+}
+}  // namespace aol
+
 extern "C" int aol_loop_persistent(const aol_loop_op* ops, int n_ops, void* const* ports, int n_ports, int dtype,
                                    int index_dtype, int relres_port, double tol, int64_t max_iter, void* stream,
                                    int64_t* iterations, double* final_relres, int* converged) {
@@ -843,10 +865,9 @@ extern "C" int aol_loop_persistent(const aol_loop_op* ops, int n_ops, void* cons
   if (dev < 0 || dev >= 64) return fail(AOL_EUNSUPPORTED, "device index out of range");
   // per device: occupancy checked once, scratch allocated once (the call is synchronous and
   // holds the device's lock, so loops on one device never share scratch concurrently)
-  static std::mutex locks[64];
-  static char* scratch_of[64] = {nullptr};
-  static int fits_of[64] = {0};
-  std::lock_guard<std::mutex> lock(locks[dev]);
+  std::lock_guard<std::mutex> lock(g_loop_locks[dev]);
+  char** scratch_of = g_loop_scratch;
+  int* fits_of = g_loop_fits;
   const int kid = (dtype == AOL_F64 ? 2 : 0) + (index_dtype == AOL_I64 ? 1 : 0);
   if (!((fits_of[dev] >> kid) & 1)) {
     AOL_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kLoopThreads, 0));

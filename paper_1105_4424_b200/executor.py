@@ -181,6 +181,8 @@ class _Task:
 class Executor:
     """Prepared schedule: storage resident in HBM, tasks validated, ready to run repeatedly."""
 
+    _STREAMABLE_REF_OPS = ("copy", "sub", "scale", "axpy")
+
     def __init__(self, model, schedule, bindings: dict, device_count: int, *, tilers: dict | None = None,
                  precision: str = "default", device=None, stream=None, pipeline: int = 0, fuse: bool = True,
                  graphs: bool = True):
@@ -199,12 +201,16 @@ class Executor:
         self.stream = stream
         steps = [st for st in schedule.steps]
         from .intrinsics import FILTER_OPS
-        single = len(steps) == 1 and hasattr(steps[0], "launches")
+        # streaming splits launch ranges into chunks: only ops whose chunks are independent
+        # repetitions qualify (tile ops, identity elementwise ops); spmv_csr gathers whole
+        # index/value arrays and dot_partial sums one partial per launch, so they run plainly
+        single = (len(steps) == 1 and hasattr(steps[0], "launches") and steps[0].op in INTRINSICS
+                  and (INTRINSICS[steps[0].op].tile or steps[0].op in self._STREAMABLE_REF_OPS))
         # a two-step filter chain the fusion pass runs as one kernel streams like one step
         pair = (fuse and len(steps) == 2 and all(hasattr(s_, "launches") for s_ in steps)
                 and steps[0].op in FILTER_OPS and steps[1].op in FILTER_OPS)
         self.pipeline = pipeline if (pipeline > 1 and (single or pair)) else 0
-        with torch.cuda.device(self.device):
+        with torch.cuda.device(self.device), self._on_stream():
             self.storage = DeviceStorage(model, bindings, self.device, stream, defer=bool(self.pipeline))
         self._tasks: dict[str, _Task] = {}
         self.fuse = fuse
@@ -222,6 +228,13 @@ class Executor:
         self.iterations = 0
         self.final_relres = None
         self.converged = True
+
+    def _on_stream(self):
+        """Make the caller's ``stream`` torch's current stream, so uploads, zero-fills, scalar
+        reads, kernels and downloads are all ordered on it (no cross-stream races)."""
+        import contextlib
+        torch = _torch()
+        return torch.cuda.stream(self.stream) if self.stream is not None else contextlib.nullcontext()
 
     def placement_report(self) -> str:
         """Placement of every data allocation plus the staging each device task's kernel uses."""
@@ -341,6 +354,12 @@ class Executor:
         xg = st.groups[t1.nodes["x"]]
         if xg not in st.host:
             return None
+        a1 = [st.array(t1.nodes[n]).data_ptr() for n in t1.port_order]
+        a2 = [st.array(t2.nodes[n]).data_ptr() for n in t2.port_order]
+        # an empty launch is the library's fusability query: nothing runs, EUNSUPPORTED -> False
+        if not _capi.launch_fused2(t1.ctask, t2.ctask, 0, 0, a1, a2, self._stream_handle()):
+            self._fusable[(s1.task_path, s2.task_path)] = False
+            return None
         comp = torch.cuda.current_stream(self.device) if self.stream is None else self.stream
         cin, cout = torch.cuda.Stream(self.device), torch.cuda.Stream(self.device)
         # whole-array inputs (filter weights) first
@@ -351,8 +370,6 @@ class Executor:
                     st.arrays[g].copy_(st.host[g], non_blocking=True)
         comp.wait_stream(cin)
         xdev, xhost = st.arrays[xg], st.host[xg]
-        a1 = [st.array(t1.nodes[n]).data_ptr() for n in t1.port_order]
-        a2 = [st.array(t2.nodes[n]).data_ptr() for n in t2.port_order]
         root = self.model.application_components[self.model.application_root]
         yname = next(p.name for p in root.ports if enum_value(p.direction) == "out")
         ydev = st.array(yname)
@@ -767,7 +784,7 @@ class Executor:
 
     def run(self, tol=None, max_iter=None) -> None:
         torch = _torch()
-        with torch.cuda.device(self.device):
+        with torch.cuda.device(self.device), self._on_stream():
             self.run_steps(self.schedule.steps, tol, max_iter)
 
     def outputs(self, on_device: bool = False, out: dict | None = None) -> dict:
@@ -776,6 +793,11 @@ class Executor:
         ``out`` maps port name -> caller-owned host buffer (numpy array or
         pinned torch tensor) that receives the result instead of a fresh array.
         """
+        torch = _torch()
+        with torch.cuda.device(self.device), self._on_stream():
+            return self._outputs(on_device, out)
+
+    def _outputs(self, on_device: bool, out: dict | None) -> dict:
         torch = _torch()
         root = self.model.application_components[self.model.application_root]
         res = {}
@@ -813,7 +835,7 @@ def execute_schedule(model, schedule, bindings: dict, device_count: int, tol: fl
                   graphs=graphs)
     if ex.pipeline:
         torch = _torch()
-        with torch.cuda.device(ex.device):
+        with torch.cuda.device(ex.device), ex._on_stream():
             outs = ex.run_streamed(out)
     else:
         ex.run(tol, max_iter)

@@ -1,0 +1,154 @@
+"""Round-2 GPU checks: streamed-path gating, fused-pair fallback, caller streams.
+
+Each case runs through ``execute_schedule`` (refexec.py:427) on the B200 and is
+compared with the plain (unstreamed) run and with the CPU oracle.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import aol_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+
+
+def _tiler(d):
+    from paper_1105_4424_b200 import Tiler
+    return Tiler(d["origin"], d["paving"], d["fitting"], d["pattern"])
+
+
+def _spmv_model(n, nnz, dt="float64"):
+    from paper_1105_4424_b200 import builders
+    return builders.single_task_model(
+        "spmv_csr",
+        [f"rowptr in int32 [{n + 1}]", f"colidx in int32 [{nnz}]", f"values in {dt} [{nnz}]",
+         f"x in {dt} [{n}]", f"y out {dt} [{n}]"],
+        [f"rp in int32 [{n + 1}]", f"ci in int32 [{nnz}]", f"va in {dt} [{nnz}]",
+         f"vx in {dt} [{n}]", f"o out {dt} [{n}]"],
+        ["rp -> t.rowptr", "ci -> t.colidx", "va -> t.values", "vx -> t.x", "t.y -> o"],
+        ["allocate data rp onto dev.gmem", "allocate data ci onto dev.gmem", "allocate data va onto dev.gmem",
+         "allocate data vx onto dev.gmem", "allocate data t.y onto dev.gmem", "allocate task t onto dev.cu"], n)
+
+
+def _random_csr(rng, n, per_row=7):
+    cols = [np.sort(rng.choice(n, size=int(rng.integers(0, per_row + 1)), replace=False)) for _ in range(n)]
+    rowptr = np.zeros(n + 1, np.int32)
+    rowptr[1:] = np.cumsum([c.size for c in cols])
+    colidx = np.concatenate(cols).astype(np.int32)
+    return rowptr, colidx, rng.standard_normal(colidx.size)
+
+
+@pytest.mark.parametrize("chunks", [2, 7])
+@pytest.mark.parametrize("devices", [1, 3])
+def test_streamed_spmv_equals_plain_and_oracle(chunks, devices):
+    """pipeline>1 on a spmv_csr schedule: rowptr/colidx/values are gathered whole, so the
+    executor must not stream it chunk-wise -- results equal the plain run."""
+    from paper_1105_4424_b200.executor import execute_schedule
+    from paper_1105_4424_b200.partition import build_schedule
+    rng = np.random.default_rng(11)
+    n = 1500
+    rp, ci, va = _random_csr(rng, n)
+    x = rng.standard_normal(n)
+    model = _spmv_model(n, ci.size)
+    sched = build_schedule(model, devices)
+    bind = {"rp": rp, "ci": ci, "va": va, "vx": x}
+    plain = execute_schedule(model, sched, bind, devices).outputs["o"]
+    streamed = execute_schedule(model, sched, bind, devices, pipeline=chunks).outputs["o"]
+    ref = np.zeros(n)
+    orc.spmv_rows(rp, ci, va, x, ref, 0, n)
+    assert np.array_equal(plain, ref)
+    assert np.array_equal(streamed, ref)
+
+
+@pytest.mark.parametrize("chunks", [2, 5])
+@pytest.mark.parametrize("devices", [1, 4])
+def test_streamed_dot_equals_plain(chunks, devices):
+    """pipeline>1 on dot_partial: one partial per launch summed in device order, not the last chunk's."""
+    from paper_1105_4424_b200 import builders
+    from paper_1105_4424_b200.executor import execute_schedule
+    from paper_1105_4424_b200.partition import build_schedule
+    n = 10007
+    model = builders.single_task_model(
+        "dot_partial", [f"a in float64 [{n}]", f"b in float64 [{n}]", "s out float64 [1]"],
+        [f"i1 in float64 [{n}]", f"i2 in float64 [{n}]", "o out float64 [1]"],
+        ["i1 -> t.a", "i2 -> t.b", "t.s -> o"],
+        ["allocate data i1 onto dev.gmem", "allocate data i2 onto dev.gmem", "allocate data t.s onto host.ram",
+         "allocate task t onto dev.cu"], n)
+    rng = np.random.default_rng(3)
+    a, b = rng.standard_normal(n), rng.standard_normal(n)
+    sched = build_schedule(model, devices)
+    plain = execute_schedule(model, sched, {"i1": a, "i2": b}, devices).outputs["o"]
+    streamed = execute_schedule(model, sched, {"i1": a, "i2": b}, devices, pipeline=chunks).outputs["o"]
+    assert np.array_equal(plain, streamed)
+    assert abs(float(plain[0]) - float(a @ b)) <= 1e-12 * max(1.0, abs(float(a @ b)))
+
+
+@pytest.mark.parametrize("chunks", [2, 6])
+def test_streamed_unfusable_filter_pair_falls_back(chunks):
+    """Two chained 1-D FIRs (not the 13x3 -> 14x4 geometry the fused kernel exists for) with
+    pipeline>1: the streamed pair path must fall back to unfused launches."""
+    from paper_1105_4424_b200 import builders
+    from paper_1105_4424_b200.executor import execute_schedule
+    from paper_1105_4424_b200.partition import build_schedule
+    n = 4096
+    taps1, taps2 = 5, 3
+    t1 = {"x": dict(array=(n,), rep=(n,), pattern=(taps1,), origin=(0,), paving=((1,),), fitting=((1,),)),
+          "y": dict(array=(n,), rep=(n,), pattern=(1,), origin=(0,), paving=((1,),), fitting=((0,),))}
+    t2 = {"x": dict(array=(n,), rep=(n,), pattern=(taps2,), origin=(n - 1,), paving=((1,),), fitting=((1,),)),
+          "y": dict(array=(n,), rep=(n,), pattern=(1,), origin=(0,), paving=((1,),), fitting=((0,),))}
+    w1 = np.array([1, 2, 4, 2, 1], np.float32) / 8
+    w2 = np.array([1, 2, 1], np.float32) / 4
+    model = builders.chain_model(
+        [("f", "tile_filter", {"x": f"in float32 [{n}]", "w": "in float32 [5]", "y": f"out float32 [{n}]"},
+          {k: _tiler(v) for k, v in t1.items()}, (n,)),
+         ("g", "tile_filter", {"x": f"in float32 [{n}]", "w": "in float32 [3]", "y": f"out float32 [{n}]"},
+          {k: _tiler(v) for k, v in t2.items()}, (n,))],
+        {"x": f"in float32 [{n}]", "w1": "in float32 [5]", "w2": "in float32 [3]"}, {"y": f"out float32 [{n}]"},
+        [("x", "f.x"), ("w1", "f.w"), ("f.y", "g.x"), ("w2", "g.w"), ("g.y", "y")])
+    x = np.random.default_rng(5).random(n).astype(np.float32)
+    sched = build_schedule(model, 2)
+    bind = {"x": x, "w1": w1, "w2": w2}
+    plain = execute_schedule(model, sched, bind, 2).outputs["y"]
+    streamed = execute_schedule(model, sched, bind, 2, pipeline=chunks).outputs["y"]
+    mid = np.zeros(n, np.float32)
+    orc.tile_filter(x, w1, mid, t1["x"], t1["y"], 0, n)
+    ref = np.zeros(n, np.float32)
+    orc.tile_filter(mid, w2, ref, t2["x"], t2["y"], 0, n)
+    assert np.array_equal(plain, ref)
+    assert np.array_equal(streamed, ref)
+
+
+def test_caller_stream_orders_uploads_kernels_and_downloads():
+    """stream= kwarg: storage uploads, kernels and the output copy all run on the caller's
+    stream.  A busy default stream must not be raced."""
+    from paper_1105_4424_b200 import builders
+    from paper_1105_4424_b200.executor import execute_schedule
+    from paper_1105_4424_b200.partition import build_schedule
+    M, N, K = 512, 384, 256
+    g = orc.gemm_tilers(M, N, K)
+    model = builders.tile_task_model(
+        "matmul", {"a": f"in float32 [{M},{K}]", "b": f"in float32 [{K},{N}]", "c": f"out float32 [{M},{N}]"},
+        {k: _tiler(v) for k, v in g.items()}, (M, N))
+    rng = np.random.default_rng(8)
+    a = torch.from_numpy(rng.standard_normal(M * K).astype(np.float32)).pin_memory()
+    b = torch.from_numpy(rng.standard_normal(K * N).astype(np.float32)).pin_memory()
+    s = torch.cuda.Stream()
+    ref = execute_schedule(model, build_schedule(model, 2), {"p_a": a, "p_b": b}, 2,
+                           precision="exact").outputs["p_c"]
+    for _ in range(3):
+        busy = torch.empty(1 << 26, device="cuda")
+        busy.normal_()                                   # keep the default stream occupied
+        res = execute_schedule(model, build_schedule(model, 2), {"p_a": a, "p_b": b}, 2, precision="exact",
+                               stream=s).outputs["p_c"]
+        assert np.array_equal(res, ref)
+        dev = execute_schedule(model, build_schedule(model, 2), {"p_a": a.cuda(), "p_b": b.cuda()}, 2,
+                               precision="exact", stream=s, device_outputs=True).outputs["p_c"]
+        s.synchronize()
+        assert np.array_equal(dev.cpu().numpy(), ref)
