@@ -273,14 +273,31 @@ def cuda_unpack(array, bt: BoundTiler, first: int, count: int, stream) -> None:
                  int(torch.cuda.current_stream(array.device).cuda_stream))
 
 
-# -- distributed drop-in ----------------------------------------------------------
+# -- sharded execution: launch d on rank d mod world, exchange only what crosses shards ----
+
+def rank_of(device_index: int, world: int) -> int:
+    """Rank that runs launch ``device_index`` of a step (launch d -> rank d mod world)."""
+    return device_index % world
+
+
+def _walk(steps):
+    for st in steps:
+        if hasattr(st, "body"):
+            yield from _walk(st.body)
+        else:
+            yield st
+
 
 def _written_ports(task) -> list[str]:
     return [ps.name for ps in task.spec.ports if ps.direction in ("out", "inout") and task.comp.port(ps.name)]
 
 
+def _read_ports(task) -> list[str]:
+    return [ps.name for ps in task.spec.ports if ps.direction in ("in", "inout") and task.comp.port(ps.name)]
+
+
 def _port_tiler(ex, task, name: str) -> BoundTiler:
-    """Output tiler of a port: the task's tiler for tile ops, the identity tiler for reference ops."""
+    """Tiler of a port: the task's tiler for tile ops, the identity tiler for reference ops."""
     from .tiler import Tiler
     tl = dict(getattr(task.comp, "tilers", ()) or ())
     tl.update(ex.tilers.get(task.path, {}) or {})
@@ -298,48 +315,555 @@ def _port_tiler(ex, task, name: str) -> BoundTiler:
     return Tiler((0,), ((0,),), ((0,),), (1,)).bind((n,), (T,))
 
 
-def make_distributed_executor(model, schedule, bindings: dict, *, group=None, **kw):
-    """Executor for rank ``dist.get_rank(group)`` of a schedule built with device_count == world size."""
-    from .executor import Executor, _capi
+def dense_stream(bt: BoundTiler) -> tuple[int, int] | None:
+    """(c0, P) when repetition rho's pattern lands at [c0 + P*rho, c0 + P*rho + P) -- the
+    tiler writes a dense stream in rho order, so a launch range writes one flat range --
+    else None."""
+    import numpy as np
+    aff = bt.affine
+    if aff is None:
+        return None
+    c0, rc, pc = aff
+    P = bt.pattern_total
+    pat = bt.tiler.pattern
+    want_pc = tuple(int(np.prod(pat[k + 1:])) for k in range(len(pat)))
+    want_rc = tuple(int(np.prod(bt.rep[j + 1:])) * P for j in range(len(bt.rep)))
+    if tuple(int(p) if e > 1 else want_pc[k] for k, (p, e) in enumerate(zip(pc, pat))) != want_pc:
+        return None
+    if tuple(int(r) if e > 1 else want_rc[j] for j, (r, e) in enumerate(zip(rc, bt.rep))) != want_rc:
+        return None
+    return int(c0), P
 
-    class DistributedExecutor(Executor):
-        def __init__(self):
-            import torch.distributed as dist
-            self.xch = Exchange(group)
-            kw.setdefault("fuse", False)     # fused chains skip the intermediate exchange
-            kw.setdefault("graphs", False)   # loop bodies need the per-step exchange and dot combine
-            super().__init__(model, schedule, bindings, self.xch.world, **kw)
-            self.rank, self.world = self.xch.rank, self.xch.world
 
-        def run_device(self, step) -> None:
-            import torch
-            t = self.task(step.task_path)
-            if len(step.launches) > self.world:
-                raise ValueError(f"step '{step.task_path}' has {len(step.launches)} launches for "
-                                 f"{self.world} ranks: build the schedule with device_count == world size")
-            s = self._stream_handle()
-            arrays = {name: self.storage.array(node) for name, node in t.nodes.items()}
-            mine = [l for l in step.launches if l.device_index == self.rank]
-            if step.op == "dot_partial":
-                part = 0.0
-                if mine:
-                    buf = torch.zeros(1, dtype=arrays["a"].dtype, device=self.device)
-                    l = mine[0]
-                    _capi.launch(t.ctask, l.range.offset, l.range.count,
-                                 [arrays["a"].data_ptr(), arrays["b"].data_ptr(), buf.data_ptr()], (), s)
-                    part = float(buf.double().item())
-                arrays["s"][0] = combine_partials(self.xch, part)
-                return
-            scalars = [float(arrays[n][0].item()) for n in t.scalar_ports]
-            ptrs = [arrays[name].data_ptr() for name in t.port_order]
-            for l in mine:
-                _capi.launch(t.ctask, l.range.offset, l.range.count, ptrs, scalars, s)
-            total = sum(l.range.count for l in step.launches)
-            sh = Shard(self.rank, self.world, tuple(l.range for l in step.launches))
-            for name in _written_ports(t):
-                bt = _port_tiler(self, t, name)
-                if bt.rep_total != total:
+def read_ranges(ex, task, name: str, first: int, count: int) -> list[tuple[int, int]]:
+    """Flat ranges of port ``name`` that launch [first, first+count) of ``task`` reads.
+
+    Tiled ports: :func:`input_ranges`.  spmv_csr (refexec.py:111-121): rowptr rows
+    [first, first+count], x / colidx / values gathered anywhere (whole).  Filter weights,
+    scalars: whole.  Identity ports of the reference ops: the launch range itself."""
+    spec = task.spec
+    n = task.comp.port(name).shape.total
+    ps = spec.port_spec(name)
+    if spec.tile:
+        return input_ranges(_port_tiler(ex, task, name), first, count) if ps.tiled else [(0, n)]
+    if spec.name == "spmv_csr":
+        return [(first, min(n, first + count + 1))] if name == "rowptr" else [(0, n)]
+    if ps.scalar:
+        return [(0, n)]
+    return input_ranges(_port_tiler(ex, task, name), first, count)
+
+
+def _set_owner(lst: list, lo: int, hi: int, owner) -> list:
+    """Sorted disjoint (lo, hi, owner) intervals with [lo, hi) re-assigned to ``owner``
+    (owner None removes it)."""
+    out = []
+    for a, b, o in lst:
+        if b <= lo or a >= hi:
+            out.append((a, b, o))
+            continue
+        if a < lo:
+            out.append((a, lo, o))
+        if b > hi:
+            out.append((hi, b, o))
+    if owner is not None and hi > lo:
+        out.append((lo, hi, owner))
+    return sorted(out)
+
+
+class PlanHost:
+    """What a :class:`ShardPlan` reads from an executor -- the model's port groups, validated
+    tasks, the schedule and per-task tilers -- without any device storage (host-side use
+    and CPU tests)."""
+
+    def __init__(self, model, schedule, tilers: dict | None = None, precision: str = "default"):
+        import types
+        from .model import connected_port_groups
+        self.model, self.schedule, self.tilers, self.precision = model, schedule, tilers or {}, precision
+        self.storage = types.SimpleNamespace(groups=connected_port_groups(model))
+        self._tasks: dict = {}
+
+    def task(self, path: str):
+        from .executor import _Task
+        t = self._tasks.get(path)
+        if t is None:
+            t = self._tasks[path] = _Task(self.model, self.storage, path, self.tilers.get(path), self.precision)
+        return t
+
+
+def _continuations(steps) -> dict:
+    """id(step) -> the execution sequences that can follow it (loops flattened).
+
+    A top-level step continues with the rest of the schedule.  A step at position k of a
+    LoopStep body continues either with body[k+1:] and whatever follows the loop (the loop
+    exits), or with body[k+1:] + body[:k+1] (one more iteration up to and including itself,
+    refexec.py:525-541).  Nested loops are walked the same way, innermost first."""
+    conts: dict = {}
+
+    def flat(seq):
+        return list(_walk(seq))
+
+    def visit(seq, after: list, looping: bool):
+        for k, st in enumerate(seq):
+            rest = flat(seq[k + 1:])
+            outs = [rest + a for a in after]
+            if looping:
+                outs.append(rest + flat(seq[:k + 1]))
+            if hasattr(st, "body"):
+                visit(st.body, outs if outs else [[]], True)
+            else:
+                conts[id(st)] = outs
+    visit(list(steps), [[]], False)
+    return conts
+
+
+class ShardPlan:
+    """Static exchange plan of a schedule whose launch d runs on rank d mod ``world``.
+
+    For every device step and written port: if the output tiler writes a dense stream,
+    each launch writes one flat range, and exactly the part of it that another rank reads
+    before that part is overwritten again by its own writer travels to that rank -- a list
+    of (writer, reader, lo, hi) ranges.  Readers are found along every execution path that
+    can follow the step (:func:`_continuations`; loop bodies wrap), stopping at the first
+    later step that rewrites the same ranges on the same ranks (CG's ``scale_p`` is followed
+    by ``axpy_p`` on the same shards, so only ``axpy_p``'s p travels to the spmv).
+    Non-dense output tilers fall back to the packed-pattern all-gather (``None``).  Host
+    scalar ops read on every rank; dot_partial results are combined by the partial
+    reduction, not exchanged.  Nothing is exchanged for the caller's outputs until
+    :meth:`ShardedExecutor.outputs` gathers them to the root (NCCL only
+    where an output crosses shards)."""
+
+    def __init__(self, ex, world: int):
+        self.world = world
+        st = ex.storage
+        self.groups = st.groups
+        reads: dict = {}        # id(step) -> {group: [ranges per rank]}
+        writes: dict = {}       # id(step) -> {group: (dense, [(w, lo, hi)])}
+        steps = list(_walk(ex.schedule.steps))
+        for step in steps:
+            t = ex.task(step.task_path)
+            rd: dict = {}
+
+            def add(g, r, lo, hi):
+                if hi > lo:
+                    lst = rd.setdefault(g, [[] for _ in range(world)])
+                    lst[r] = add_range(lst[r], lo, hi)
+            if not hasattr(step, "launches"):
+                for n in _read_ports(t):
+                    for r in range(world):
+                        add(st.groups[t.nodes[n]], r, 0, t.comp.port(n).shape.total)
+                reads[id(step)] = rd
+                continue
+            for l in step.launches:
+                r = rank_of(l.device_index, world)
+                for n in _read_ports(t):
+                    for lo, hi in read_ranges(ex, t, n, l.range.offset, l.range.count):
+                        add(st.groups[t.nodes[n]], r, lo, hi)
+            reads[id(step)] = rd
+            wr: dict = {}
+            if step.op != "dot_partial":
+                for name in _written_ports(t):
+                    bt = _port_tiler(ex, t, name)
+                    ds = dense_stream(bt)
+                    ranges = []
+                    if ds is not None:
+                        c0, P = ds
+                        for l in step.launches:
+                            lo, hi = c0 + P * l.range.offset, c0 + P * (l.range.offset + l.range.count)
+                            if hi > lo:
+                                ranges.append((rank_of(l.device_index, world), lo, hi))
+                    wr[st.groups[t.nodes[name]]] = (name, ds is not None, ranges)
+            writes[id(step)] = wr
+        conts = _continuations(ex.schedule.steps)
+
+        def kills(later: dict, g, ranges) -> bool:
+            """The later step rewrites every range of this write on the same rank."""
+            if g not in later or not later[g][1]:
+                return False
+            cover = later[g][2]
+            return all(any(w2 == w and lo2 <= lo and hi2 >= hi for w2, lo2, hi2 in cover) for w, lo, hi in ranges)
+
+        # task path -> [(port, group, dense transfers | None, [(writer, lo, hi)])]
+        self.writes: dict[str, list] = {}
+        self.need: dict = {}
+        for step in steps:
+            if not hasattr(step, "launches") or step.op == "dot_partial":
+                continue
+            entries = []
+            for g, (name, dense, ranges) in writes[id(step)].items():
+                if not dense:
+                    entries.append((name, g, None, []))
                     continue
-                gather_output(arrays[name], bt, sh, self.xch, cuda_pack, cuda_unpack)
+                need = [[] for _ in range(world)]
+                for seq in conts[id(step)]:
+                    for nxt in seq:
+                        rd = reads[id(nxt)].get(g)
+                        if rd:
+                            for r in range(world):
+                                for a, b in rd[r]:
+                                    need[r] = add_range(need[r], a, b)
+                        if kills(writes.get(id(nxt), {}), g, ranges):
+                            break
+                self.need[(step.task_path, g)] = need
+                tr = []
+                for w, lo, hi in ranges:
+                    for r in range(world):
+                        if r == w:
+                            continue
+                        for a, b in need[r]:
+                            if min(hi, b) > max(lo, a):
+                                tr.append((w, r, max(lo, a), min(hi, b)))
+                entries.append((name, g, tr, ranges))
+            self.writes[step.task_path] = entries
+
+    @classmethod
+    def for_model(cls, model, schedule, world: int, tilers: dict | None = None) -> "ShardPlan":
+        return cls(PlanHost(model, schedule, tilers), world)
+
+    def exchanged_bytes(self, task_path: str, esize: dict) -> int:
+        """Bytes the dense transfers of one step move (for tests / reports)."""
+        tot = 0
+        for name, g, tr, _ in self.writes.get(task_path, []):
+            if tr:
+                tot += sum(hi - lo for _, _, lo, hi in tr) * esize.get(g, 4)
+        return tot
+
+
+class Replica:
+    """One rank's storage in this process: the rank, its CUDA device, its port arrays."""
+
+    def __init__(self, rank: int, device, storage):
+        self.rank, self.device, self.storage = rank, device, storage
+        self.pbuf = {}
+
+
+class DistTransport:
+    """Exchange over a torch.distributed group: NCCL over NVLink on GPUs (device buffers
+    straight into the NCCL send/recv), or host-staged over gloo (CPU ranks, or several
+    ranks sharing one GPU in tests).  One grouped batch of exact-size point-to-point
+    transfers per exchange (ncclGroupStart/End); every rank derives the same transfer
+    list from the same plan, so the k-th send w->r matches the k-th receive on r."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.staged = dist.get_backend(group) != "nccl"
+        self.bytes_moved = 0
+
+    def _peer(self, r: int) -> int:
+        return r if self.group is None else self.dist.get_global_rank(self.group, r)
+
+    def move(self, replicas: dict, g, transfers: list) -> None:
+        dist = self.dist
+        me = self.rank
+        rep = replicas[me]
+        arr = rep.storage.arrays[g]
+        ops, back = [], []
+        for w, r, lo, hi in transfers:
+            if w == me:
+                buf = arr[lo:hi].cpu() if self.staged else arr[lo:hi]
+                ops.append(dist.P2POp(dist.isend, buf, self._peer(r), self.group))
+                self.bytes_moved += (hi - lo) * arr.element_size()
+            elif r == me:
+                if self.staged:
+                    import torch
+                    buf = torch.empty(hi - lo, dtype=arr.dtype)
+                    back.append((buf, lo, hi))
+                else:
+                    buf = arr[lo:hi]
+                ops.append(dist.P2POp(dist.irecv, buf, self._peer(w), self.group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        for buf, lo, hi in back:
+            arr[lo:hi].copy_(buf)
+
+    def reduce_partials(self, replicas: dict, key) -> None:
+        """Every rank's dot partials (zeros in the slots it does not own) summed slot-wise:
+        x + 0 is exact, so each slot ends up holding its launch's partial bit for bit."""
+        buf = replicas[self.rank].pbuf[key]
+        if self.staged:
+            h = buf.cpu()
+            self.dist.all_reduce(h, group=self.group)
+            buf.copy_(h)
+        else:
+            self.dist.all_reduce(buf, group=self.group)
+
+    def all_gather_v(self, replicas: dict, local, counts: list[int]):
+        import torch
+        if self.staged:
+            ex = Exchange(self.group)
+            streams = ex.all_gather_v(local.cpu(), counts)
+            dev = replicas[self.rank].device
+            return [s_.to(dev) if isinstance(s_, torch.Tensor) else s_ for s_ in streams]
+        return Exchange(self.group).all_gather_v(local, counts)
+
+    def barrier(self):
+        self.dist.barrier(group=self.group)
+
+
+class LocalTransport:
+    """Exchange between replicas in one process (``execute_schedule(device_count=D)`` with
+    several visible GPUs): peer copies, which travel over NVLink between devices.  Two
+    replicas may share a device (used by tests on one GPU); the copies are then local."""
+
+    def __init__(self, world: int):
+        self.world = world
+        self.bytes_moved = 0
+
+    def move(self, replicas: dict, g, transfers: list) -> None:
+        import torch
+        for w, r, lo, hi in transfers:
+            src = replicas[w].storage.arrays[g]
+            dst = replicas[r].storage.arrays[g]
+            with torch.cuda.device(replicas[r].device):
+                dst[lo:hi].copy_(src[lo:hi], non_blocking=True)
+            self.bytes_moved += (hi - lo) * src.element_size()
+
+    def reduce_partials(self, replicas: dict, key) -> None:
+        import torch
+        bufs = {r: rep.pbuf[key] for r, rep in replicas.items()}
+        n = next(iter(bufs.values())).numel()
+        for k in range(n):
+            w = k % self.world
+            for r, b in bufs.items():
+                if r != w:
+                    with torch.cuda.device(replicas[r].device):
+                        b[k:k + 1].copy_(bufs[w][k:k + 1], non_blocking=True)
+
+    def all_gather_v(self, replicas: dict, local, counts):
+        raise NotImplementedError
+
+    def barrier(self):
+        pass
+
+
+class ShardedExecutor:
+    """Mixin over :class:`executor.Executor`: launch d of every device step runs on rank
+    d mod world; only what a later step of another rank reads is exchanged (ShardPlan);
+    dot partials are reduced on the device and combined in ascending launch order by the
+    partials_sum kernel (refexec.py:478-487) -- no host round trip per dot; host scalar ops
+    run as device scalar kernels on every rank, so a CG iteration syncs the host once, for
+    the loop test (refexec.py:525-541).  Outputs are gathered to the root (rank 0)."""
+
+    def _init_sharded(self, transport, replicas: list, world: int):
+        self.transport = transport
+        self.world = world
+        self.replicas = {rep.rank: rep for rep in replicas}
+        self.root = 0
+        self.plan = ShardPlan(self, world)
+        self.stale: dict = {}          # group -> [(lo, hi, owner)] ranges the root holds stale
+        self.exchanged_bytes = 0
+
+    # -- per-replica context -------------------------------------------------------
+    def _enter(self, rep):
+        self.storage, self.device = rep.storage, rep.device
+
+    def _each(self):
+        import torch
+        home = (self.storage, self.device)
+        try:
+            for r in sorted(self.replicas):
+                rep = self.replicas[r]
+                self._enter(rep)
+                with torch.cuda.device(rep.device):
+                    yield rep
+        finally:
+            self.storage, self.device = home
+
+    def _mine(self, step, rank):
+        return [l for l in step.launches if rank_of(l.device_index, self.world) == rank]
+
+    # -- steps ---------------------------------------------------------------------
+    def run_host(self, step) -> None:
+        t = self.task(step.task_path)
+        dt = enum_value_dtype(t)
+        for rep in self._each():
+            self._scalar_seq([step], dt, self._stream_handle())
+
+    def run_device(self, step) -> None:
+        from . import _capi
+        t = self.task(step.task_path)
+        if step.op == "dot_partial":
+            self._dot(step, t)
+            return
+        ctask, names = self._dev_task(step)
+        for rep in self._each():
+            mine = self._mine(step, rep.rank)
+            if not mine:
+                continue
+            ptrs = [rep.storage.array(t.nodes[n]).data_ptr() for n in names]
+            s = self._stream_handle()
+            for l in mine:
+                _capi.launch(ctask, l.range.offset, l.range.count, ptrs, (), s)
+        self._after_write(step, t)
+
+    def _dot(self, step, t) -> None:
+        import torch
+        from . import _capi
+        from .executor import torch_dtype
+        n = len(step.launches)
+        key = (t.dtype, n)
+        red = _capi.make_task("partials_sum", t.dtype)
+        for rep in self._each():
+            buf = rep.pbuf.get(key)
+            if buf is None:
+                buf = rep.pbuf[key] = torch.zeros(n, dtype=torch_dtype(t.dtype), device=rep.device)
+            else:
+                buf.zero_()
+            a, b = rep.storage.array(t.nodes["a"]), rep.storage.array(t.nodes["b"])
+            s = self._stream_handle()
+            for l in self._mine(step, rep.rank):
+                _capi.launch(t.ctask, l.range.offset, l.range.count,
+                             [a.data_ptr(), b.data_ptr(), buf.data_ptr() + l.device_index * buf.element_size()],
+                             (), s)
+        self.transport.reduce_partials(self.replicas, key)
+        for rep in self._each():
+            _capi.launch(red, 0, n, [rep.pbuf[key].data_ptr(), rep.storage.array(t.nodes["s"]).data_ptr()], (),
+                         self._stream_handle())
+
+    def _after_write(self, step, t) -> None:
+        for name, g, tr, wr in self.plan.writes.get(step.task_path, []):
+            if tr is None:
+                self._pack_exchange(step, t, name)
+                continue
+            if tr:
+                self.transport.move(self.replicas, g, tr)
+                esz = next(iter(self.replicas.values())).storage.arrays[g].element_size()
+                self.exchanged_bytes += sum(hi - lo for _, _, lo, hi in tr) * esz
+            lst = self.stale.get(g, [])
+            for w, lo, hi in wr:
+                lst = _set_owner(lst, lo, hi, None if w == self.root else w)
+            for w, r, lo, hi in tr:
+                if r == self.root:
+                    lst = _set_owner(lst, lo, hi, None)
+            self.stale[g] = lst
+
+    def _pack_exchange(self, step, t, name) -> None:
+        """Non-dense output tiler: every rank packs its launches' patterns (rho order) through
+        the output tiler, the packed streams are all-gathered, and each rank scatters the
+        others' streams back through the same tiler."""
+        import torch
+        bt = _port_tiler(self, t, name)
+        P = bt.pattern_total
+        by_rank = {r: self._mine(step, r) for r in range(self.world)}
+        counts = [sum(l.range.count for l in by_rank[r]) * P for r in range(self.world)]
+        if isinstance(self.transport, LocalTransport):
+            for rep in self._each():
+                src = rep.storage.array(t.nodes[name])
+                for w in range(self.world):
+                    if w == rep.rank or not by_rank[w]:
+                        continue
+                    other = self.replicas[w].storage.array(t.nodes[name])
+                    for l in by_rank[w]:
+                        with torch.cuda.device(self.replicas[w].device):
+                            packed = cuda_pack(other, bt, l.range.offset, l.range.count)
+                        cuda_unpack(src, bt, l.range.offset, l.range.count, packed.to(rep.device))
+            return
+        rep = self.replicas[self.transport.rank]
+        arr = rep.storage.array(t.nodes[name])
+        with torch.cuda.device(rep.device):
+            parts = [cuda_pack(arr, bt, l.range.offset, l.range.count) for l in by_rank[rep.rank]]
+            local = torch.cat(parts) if parts else torch.zeros(0, dtype=arr.dtype, device=rep.device)
+            streams = self.transport.all_gather_v(self.replicas, local, counts)
+            for r in range(self.world):
+                if r == rep.rank:
+                    continue
+                pos = 0
+                for l in by_rank[r]:
+                    k = l.range.count * P
+                    cuda_unpack(arr, bt, l.range.offset, l.range.count, streams[r][pos:pos + k])
+                    pos += k
+
+    def _run_fused(self, s1, s2) -> bool:
+        from . import _capi
+        t1, t2 = self.task(s1.task_path), self.task(s2.task_path)
+        first = True
+        for rep in self._each():
+            a1 = [rep.storage.array(t1.nodes[n]).data_ptr() for n in t1.port_order]
+            a2 = [rep.storage.array(t2.nodes[n]).data_ptr() for n in t2.port_order]
+            s = self._stream_handle()
+            if first and not _capi.launch_fused2(t1.ctask, t2.ctask, 0, 0, a1, a2, s):
+                self._fusable[(s1.task_path, s2.task_path)] = False
+                return False
+            first = False
+            for l in self._mine(s2, rep.rank):
+                if not _capi.launch_fused2(t1.ctask, t2.ctask, l.range.offset, l.range.count, a1, a2, s):
+                    raise RuntimeError("fusion became unsupported mid-step")
+                self.fused_launches += 1
+        self._after_write(s2, t2)
+        return True
+
+    # -- results -------------------------------------------------------------------
+    def gather_to_root(self) -> int:
+        """Move every range of a root output the root holds stale to the root; returns bytes."""
+        root = self.model.application_components[self.model.application_root]
+        moved = 0
+        for port in root.ports:
+            if getattr(port.direction, "value", port.direction) != "out":
+                continue
+            g = self.storage.groups[port.name]
+            tr = [(o, self.root, lo, hi) for lo, hi, o in self.stale.get(g, [])]
+            if tr:
+                self.transport.move(self.replicas, g, tr)
+                moved += sum(hi - lo for _, _, lo, hi in tr) * self.replicas[next(iter(self.replicas))] \
+                    .storage.arrays[g].element_size()
+            self.stale[g] = []
+        return moved
+
+    def outputs(self, on_device: bool = False, out: dict | None = None) -> dict:
+        self.gather_to_root()
+        if self.root in self.replicas:
+            self._enter(self.replicas[self.root])
+        from .executor import Executor
+        return Executor.outputs(self, on_device=on_device, out=out)
+
+
+def enum_value_dtype(task) -> str:
+    from .model import enum_value
+    return enum_value(task.comp.ports[0].data_type)
+
+
+def make_sharded_executor(model, schedule, bindings: dict, device_count: int, devices: list, **kw):
+    """In-process sharding over ``devices`` (one replica per entry; launch d on replica
+    d mod len(devices)).  The replicas hold full copies of the inputs; outputs gather to
+    replica 0."""
+    import torch
+    from .executor import DeviceStorage, Executor
+
+    if kw.get("stream") is not None and len({str(torch.device(d)) for d in devices}) > 1:
+        raise ValueError("stream= names one device's stream; it cannot drive replicas on several devices")
+
+    class LocalShardedExecutor(ShardedExecutor, Executor):
+        def __init__(self):
+            kw["graphs"] = False             # loop bodies need the per-step exchange
+            kw["pipeline"] = 0
+            Executor.__init__(self, model, schedule, bindings, device_count, device=devices[0], **kw)
+            reps = [Replica(0, self.device, self.storage)]
+            for r, dev in enumerate(devices[1:], start=1):
+                d = torch.device(dev)
+                with torch.cuda.device(d):
+                    reps.append(Replica(r, d, DeviceStorage(model, bindings, d)))
+            self._init_sharded(LocalTransport(len(devices)), reps, len(devices))
+
+    return LocalShardedExecutor()
+
+
+def make_distributed_executor(model, schedule, bindings: dict, *, group=None, **kw):
+    """Executor for rank ``dist.get_rank(group)`` of a schedule whose launches are spread over
+    the group's ranks (launch d on rank d mod world; build the schedule with device_count ==
+    world size for one launch per rank, as the reference's D simulated devices)."""
+    from .executor import Executor
+
+    class DistributedExecutor(ShardedExecutor, Executor):
+        def __init__(self):
+            tr = DistTransport(group)
+            kw["graphs"] = False             # loop bodies need the per-step exchange
+            kw["pipeline"] = 0
+            D = max((len(st.launches) for st in schedule.device_steps()), default=1)
+            Executor.__init__(self, model, schedule, bindings, D, **kw)
+            self.rank = tr.rank
+            self._init_sharded(tr, [Replica(tr.rank, self.device, self.storage)], tr.world)
 
     return DistributedExecutor()

@@ -317,21 +317,8 @@ class Executor:
             st.arrays[g].copy_(h, non_blocking=True)
 
     def _dense_stream_rep(self, bt):
-        """For an output tiler that writes repetition rho's pattern at c0 + P*rho + i (a dense
-        stream in rho order), return (c0, P); else None."""
-        aff = bt.affine
-        if aff is None:
-            return None
-        c0, rc, pc = aff
-        P = bt.pattern_total
-        pat = bt.tiler.pattern
-        want_pc = tuple(int(np.prod(pat[k + 1:])) for k in range(len(pat)))
-        want_rc = tuple(int(np.prod(bt.rep[j + 1:])) * P for j in range(len(bt.rep)))
-        if tuple(int(p) if e > 1 else want_pc[k] for k, (p, e) in enumerate(zip(pc, pat))) != want_pc:
-            return None
-        if tuple(int(r) if e > 1 else want_rc[j] for j, (r, e) in enumerate(zip(rc, bt.rep))) != want_rc:
-            return None
-        return c0, P
+        from .distributed import dense_stream
+        return dense_stream(bt)
 
     def _run_streamed_pair(self, s1, s2, out: dict | None) -> dict | None:
         """Stream a fusable producer -> consumer filter chain: consumer chunks in order; each
@@ -822,14 +809,41 @@ class Executor:
         return res
 
 
+def _default_devices(device_count: int, device, pipeline: int):
+    """Launch d of a step goes to cuda:(d mod P) when P > 1 GPUs are visible (P = min(D, visible));
+    None keeps every launch on one device (one GPU, an explicit ``device``, the streamed path,
+    or AOL_MULTI_DEVICE=0)."""
+    if device is not None or device_count < 2 or pipeline > 1 or os.environ.get("AOL_MULTI_DEVICE", "1") == "0":
+        return None
+    torch = _torch()
+    n = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    if n < 2:
+        return None
+    return [torch.device("cuda", i) for i in range(min(device_count, n))]
+
+
 def execute_schedule(model, schedule, bindings: dict, device_count: int, tol: float | None = None,
                      max_iter: int | None = None, *, tilers: dict | None = None, precision: str = "default",
                      device_outputs: bool = False, out: dict | None = None, device=None,
-                     stream=None, pipeline: int = 0, fuse: bool = True, graphs: bool = True) -> ExecutionResult:
+                     stream=None, pipeline: int = 0, fuse: bool = True, graphs: bool = True,
+                     devices: list | None = None) -> ExecutionResult:
     """Interpret ``schedule`` on the B200 with ``device_count`` launch shards per device step.
 
     ``graphs`` (default on): a LoopStep runs on the device -- the persistent interpreter, else
-    one CUDA graph with a WHILE node -- bit-identical to host-driven iterations (graphs=False)."""
+    one CUDA graph with a WHILE node -- bit-identical to host-driven iterations (graphs=False).
+    ``devices``: run launch d on ``devices[d mod len(devices)]`` (one replica of the storage per
+    entry; only what crosses shards is exchanged, outputs gather to ``devices[0]``).  By default
+    the D launches spread over min(D, visible GPUs) devices."""
+    if devices is None:
+        devices = _default_devices(device_count, device, pipeline)
+    if devices is not None and len(devices) > 1:
+        from .distributed import make_sharded_executor
+        ex = make_sharded_executor(model, schedule, bindings, device_count, list(devices), tilers=tilers,
+                                   precision=precision, stream=stream, fuse=fuse)
+        ex.run(tol, max_iter)
+        outs = ex.outputs(on_device=device_outputs, out=out)
+        return ExecutionResult(outputs=outs, iterations=ex.iterations, final_relres=ex.final_relres,
+                               converged=ex.converged)
     ex = Executor(model, schedule, bindings, device_count, tilers=tilers, precision=precision,
                   device=device, stream=stream, pipeline=0 if device_outputs else pipeline, fuse=fuse,
                   graphs=graphs)

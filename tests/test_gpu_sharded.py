@@ -1,0 +1,177 @@
+"""Sharded execution on the B200: launch d of every step on rank d mod world, only what
+crosses shards exchanged, outputs gathered to the root -- checked against the CPU oracle.
+
+Two forms are exercised on one GPU:
+  * replicas in one process (``execute_schedule(devices=[...])``, LocalTransport): two or
+    three full storage replicas on cuda:0, exchanged by device copies;
+  * two torch.distributed ranks (``make_distributed_executor``) sharing cuda:0 over gloo
+    with host-staged transfers (DistTransport).  The ranks' kernels never wait on each
+    other -- only the host-side gloo exchange does -- so this is a logic test of the
+    multi-rank executor, not a stand-in for NVLink timing.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from _sharded_cases import CASES
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+
+
+def _run_local(case, D, replicas, **kw):
+    from paper_1105_4424_b200.executor import execute_schedule
+    from paper_1105_4424_b200.partition import build_schedule
+    model, bind, out, ref = CASES[case]()
+    res = execute_schedule(model, build_schedule(model, D), bind, D, devices=["cuda:0"] * replicas, **kw)
+    return res, out, ref
+
+
+@pytest.mark.parametrize("case", sorted(CASES))
+@pytest.mark.parametrize("D,replicas", [(2, 2), (3, 2), (5, 3), (4, 4)])
+def test_local_replicas_vs_oracle(case, D, replicas):
+    kw = {"precision": "exact"} if case == "matmul" else {}
+    res, out, ref = _run_local(case, D, replicas, **kw)
+    got = res.outputs[out]
+    if ref.dtype == np.float64:
+        assert np.array_equal(got, ref), case
+    else:
+        assert np.array_equal(got.view(np.uint32), ref.view(np.uint32)), case
+
+
+def test_local_plan_exchanges_only_what_crosses_shards():
+    """Elementwise chain: zero exchanged bytes during the run, one gather of the output.
+    Stencil chain: only the halo rows of the intermediate travel."""
+    from paper_1105_4424_b200.distributed import make_sharded_executor
+    from paper_1105_4424_b200.partition import build_schedule
+    model, bind, out, ref = CASES["elementwise"]()
+    ex = make_sharded_executor(model, build_schedule(model, 2), bind, 2, ["cuda:0", "cuda:0"])
+    ex.run()
+    assert ex.exchanged_bytes == 0
+    moved = ex.gather_to_root()
+    n = ref.size
+    assert moved == (n - (n + 1) // 2) * 8                # rank 1's half of the output, once
+    assert np.array_equal(ex.outputs()[out], ref)
+    model, bind, out, ref = CASES["stencil_chain"](H=48, W=80)
+    ex = make_sharded_executor(model, build_schedule(model, 2), bind, 2, ["cuda:0", "cuda:0"])
+    ex.run()
+    # each rank needs one row above and one below its 24 rows (wrap included): 2 rows each way
+    assert ex.exchanged_bytes == 4 * 80 * 4
+    assert np.array_equal(ex.outputs()[out].view(np.uint32), ref.view(np.uint32))
+
+
+@pytest.mark.parametrize("fuse", [True, False])
+def test_local_fused_downscaler_vs_oracle(fuse):
+    res, out, ref = _run_local("downscaler", 3, 2, fuse=fuse)
+    assert np.array_equal(res.outputs[out].view(np.uint32), ref.view(np.uint32))
+
+
+@pytest.mark.parametrize("D,replicas", [(2, 2), (4, 2), (4, 3)])
+def test_local_cg_bitwise_equals_single_device(golden, D, replicas):
+    """The paper's CG through replicas: dot partials reduced on the device and combined in
+    launch order, host scalar ops as device kernels on every replica -- same iterations and
+    the same bits as the single-device drop-in at the same D (itself within 1e-10 of the
+    reference executor, tests/test_gpu_parity.py)."""
+    from paper_1105_4424_b200.executor import execute_schedule
+    from paper_1105_4424_b200.model import model_from_dict
+    from paper_1105_4424_b200.partition import build_schedule
+    data, meta = golden
+    m = meta["cg_k20"]
+    model = model_from_dict(m["model"])
+    bind = {k: data[f"cg_k20/{k}"] for k in ("rowptr", "colidx", "values", "b")}
+    one = execute_schedule(model, build_schedule(model, D), bind, D, graphs=False)
+    rep = execute_schedule(model, build_schedule(model, D), bind, D, devices=["cuda:0"] * replicas)
+    assert rep.iterations == one.iterations and rep.converged
+    assert np.array_equal(rep.outputs["x"], one.outputs["x"])
+    if str(D) in m["runs"]:
+        assert rep.iterations == m["runs"][str(D)]["iterations"]
+
+
+# -- two ranks over torch.distributed --------------------------------------------------
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _dist_worker(rank, world, port, q, cases, golden_dir):
+    import torch as th
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    th.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import json
+        from paper_1105_4424_b200.distributed import make_distributed_executor
+        from paper_1105_4424_b200.model import model_from_dict
+        from paper_1105_4424_b200.partition import build_schedule
+        results = {}
+        for case in cases:
+            if case == "cg":
+                data = np.load(os.path.join(golden_dir, "reference_golden.npz"))
+                meta = json.load(open(os.path.join(golden_dir, "reference_golden.json")))
+                model = model_from_dict(meta["cg_k20"]["model"])
+                bind = {k: data[f"cg_k20/{k}"] for k in ("rowptr", "colidx", "values", "b")}
+                out, ref = "x", None
+            else:
+                model, bind, out, ref = CASES[case]()
+            kw = {"precision": "exact"} if case == "matmul" else {}
+            ex = make_distributed_executor(model, build_schedule(model, world), bind, **kw)
+            ex.run()
+            got = ex.outputs()[out]
+            results[case] = (got, ex.iterations, ex.exchanged_bytes, ref)
+        q.put((rank, {k: (v[0] if rank == 0 else None, v[1], v[2], v[3] if rank == 0 else None)
+                      for k, v in results.items()}))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_ranks_gloo_on_one_gpu_vs_oracle(golden):
+    import torch.multiprocessing as mp
+    from pathlib import Path
+    cases = ["matmul", "stencil_chain", "downscaler", "transpose_chain", "elementwise", "cg"]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    gdir = str(Path(__file__).resolve().parent / "golden")
+    procs = [ctx.Process(target=_dist_worker, args=(r, 2, port, q, cases, gdir)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = {}
+    for _ in procs:
+        rank, res = q.get(timeout=600)
+        out[rank] = res
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    r0 = out[0]
+    for case in cases:
+        got, iters, xbytes, ref = r0[case]
+        assert out[1][case][1] == iters            # both ranks ran the same number of iterations
+        if case == "cg":
+            data, meta = golden
+            assert iters == meta["cg_k20"]["runs"]["2"]["iterations"]
+            from paper_1105_4424_b200.executor import execute_schedule
+            from paper_1105_4424_b200.model import model_from_dict
+            from paper_1105_4424_b200.partition import build_schedule
+            model = model_from_dict(meta["cg_k20"]["model"])
+            bind = {k: data[f"cg_k20/{k}"] for k in ("rowptr", "colidx", "values", "b")}
+            one = execute_schedule(model, build_schedule(model, 2), bind, 2, graphs=False)
+            assert np.array_equal(got, one.outputs["x"])
+            continue
+        if ref.dtype == np.float64:
+            assert np.array_equal(got, ref), case
+        else:
+            assert np.array_equal(got.view(np.uint32), ref.view(np.uint32)), case
+    assert r0["elementwise"][2] == 0
