@@ -2,22 +2,24 @@
 
 Default workload (BASELINE.json configs[1]): the MatMul repetitive task
 8192x8192x8192 fp32 (TF32 tensor cores) — repetition space [M, N] with the
-canonical GEMM tilers, sharded over ranks by contiguous blocks of the
-linearised repetition space (partition.py:105-121).  Weak scaling: every
-rank owns 8192 rows of C (its shard of an [8192*N, 8192] repetition space),
-its A row block and all of B — no data-path collective.
+canonical GEMM tilers.  At N ranks the SAME repetition space is sharded by
+contiguous blocks (partition.py:105-121): launch d of the schedule built with
+device_count = N runs on rank d through the drop-in's distributed executor
+(strong scaling; 1024 rows of C per rank at N = 8), with no data-path
+collective; the output gather to rank 0 is timed separately.
 
   value : TFLOP/s of the whole job with inputs resident in HBM (device-timed,
           CUDA events on the launching stream, max over ranks)
   e2e   : the same metric through the public API ``execute_schedule`` with
           pinned host bindings: H2D of A and B, the launch, D2H of C, every step
+          (plus ``e2e_numpy``: numpy in, numpy out, exactly the reference call)
   roofline : the GEMM kernel's achieved TFLOP/s vs the measured TF32 peak
-  cpu_baseline : the oracle's C restatement (oracle/aol_oracle.c) on the host
-          cores, on a bounded sample of rows of the same workload
+  cpu_baseline : numpy.matmul fp32 (OpenBLAS sgemm, every host core) on the
+          same A and B, with its accuracy next to ours
 
-``--impl reference`` times the reference's CPU algorithm (the oracle port)
-on the same workload and prints the reference arm's line.
-``--workload stencil|downscaler|sweep`` runs the tiler-bound configs.
+``--impl reference`` times the reference's CPU path for the workload on the host
+cores and prints the reference arm's line.
+``--workload stencil|downscaler|sweep|cg|cg27|c1`` runs the other configs.
 """
 
 from __future__ import annotations
@@ -196,30 +198,47 @@ def _spec(d, direction):
 
 
 class Workload:
-    """One repetitive-task schedule prepared in HBM; step() = one pass over one batch."""
+    """One repetitive-task schedule prepared in HBM; step() = one pass over one batch.
+
+    ``scaling = "strong"``: the configured problem is the whole job at every N; at N > 1 the
+    schedule is built with device_count = N and rank r runs launch r through the drop-in's
+    distributed executor (make_distributed_executor).  ``"weak"``: every rank runs its own
+    copy of the problem."""
 
     name = "?"
     unit = "GB/s"
     bound = "hbm"
+    scaling = "strong"
 
     fuse = True
 
-    def _prepare(self, torch, device, model, schedule, dev_bindings: dict, host_specs: dict, outputs: dict):
+    def _prepare(self, torch, device, model, dev_bindings: dict, host_specs: dict, outputs: dict,
+                 rank: int = 0, world: int = 1):
         from paper_1105_4424_b200.executor import Executor
+        from paper_1105_4424_b200.partition import build_schedule
         self.torch, self.device = torch, device
-        self.model, self.schedule = model, schedule
-        self.ex = Executor(model, schedule, dev_bindings, 1, fuse=Workload.fuse)
+        self.model, self.rank, self.world = model, rank, world
+        if world > 1 and self.scaling == "strong":
+            from paper_1105_4424_b200.distributed import make_distributed_executor
+            self.schedule = build_schedule(model, world)
+            self.ex = make_distributed_executor(model, self.schedule, dev_bindings, fuse=Workload.fuse)
+            steps = self.schedule.device_steps()
+            mine = sum(l.range.count for st in steps for l in st.launches if l.device_index == rank)
+            self.rank_fraction = mine / max(1, sum(st.total_work for st in steps))
+        else:
+            self.schedule = build_schedule(model, 1)
+            self.ex = Executor(model, self.schedule, dev_bindings, 1, fuse=Workload.fuse)
+            self.rank_fraction = 1.0
         self.host_specs, self.out_sizes = host_specs, outputs
 
     def step(self):
         self.ex.run()
 
-    def output_shard(self):
-        """This rank's output array in HBM (for the N>1 gather measurement), or None."""
-        ex = getattr(self, "ex", None)
-        if ex is None or not self.out_sizes:
-            return None
-        return ex.outputs(on_device=True)[next(iter(self.out_sizes))]
+    def gather(self):
+        """N > 1: move every output range the root does not hold to rank 0 (the distributed
+        executor's gather, NCCL send/recv of exact ranges); returns bytes moved to the root."""
+        gt = getattr(self.ex, "gather_to_root", None)
+        return gt() if gt is not None else None
 
     def e2e_setup(self):
         torch = self.torch
@@ -234,11 +253,60 @@ class Workload:
 
     def e2e_step(self):
         from paper_1105_4424_b200.executor import execute_schedule
-        return execute_schedule(self.model, self.schedule, self.hin, 1, out=self.hout,
+        if self.world > 1 and self.scaling == "strong":
+            # every rank uploads its input hull from the pinned host arrays, runs its launch,
+            # the output ranges gather to rank 0, rank 0 copies the whole result down
+            from paper_1105_4424_b200.distributed import make_distributed_executor
+            ex = make_distributed_executor(self.model, self.schedule, self.hin, fuse=Workload.fuse)
+            ex.run()
+            self.e2e_h2d = ex.h2d_bytes
+            return ex.outputs(out=self.hout if self.rank == 0 else None)
+        return execute_schedule(self.model, build_schedule_1(self.model), self.hin, 1, out=self.hout,
+                                pipeline=self.pipeline).outputs
+
+    def e2e_numpy_setup(self):
+        """The reference-call form: pageable numpy arrays in, fresh numpy arrays out."""
+        self.nin = {k: t.numpy().copy() for k, t in self.hin.items()}
+
+    def e2e_numpy_step(self):
+        from paper_1105_4424_b200.executor import execute_schedule
+        return execute_schedule(self.model, build_schedule_1(self.model), self.nin, 1,
                                 pipeline=self.pipeline).outputs
 
     def e2e_free(self):
         del self.hin, self.hout
+        self.__dict__.pop("nin", None)
+
+
+_SCHED_CACHE: dict = {}
+
+
+def build_schedule_1(model):
+    from paper_1105_4424_b200.partition import build_schedule
+    s = _SCHED_CACHE.get(id(model))
+    if s is None:
+        s = _SCHED_CACHE[id(model)] = build_schedule(model, 1)
+    return s
+
+
+def openblas_info() -> dict:
+    """numpy / BLAS threading facts for the CPU baseline line."""
+    info = {"cpu_count": os.cpu_count(), "numpy": np.__version__}
+    try:
+        from threadpoolctl import threadpool_info
+        blas = [d for d in threadpool_info() if d.get("user_api") == "blas"]
+        if blas:
+            info.update(blas=blas[0].get("internal_api"), blas_version=blas[0].get("version"),
+                        blas_threads=blas[0].get("num_threads"))
+    except Exception as e:  # noqa: BLE001 - informational only
+        info["blas"] = f"unknown ({type(e).__name__})"
+    return info
+
+
+def normwise(c, ref) -> float:
+    """||C - C_ref||_F / ||C_ref||_F over the sampled rows."""
+    c, ref = np.asarray(c, np.float64), np.asarray(ref, np.float64)
+    return float(np.linalg.norm(c - ref) / np.linalg.norm(ref))
 
 
 class MatmulWorkload(Workload):
@@ -247,27 +315,21 @@ class MatmulWorkload(Workload):
     bound = "tensor"
 
     def __init__(self, torch, device, rank, world, M=8192, N=8192, K=8192):
-        from oracle import aol_oracle as orc
         from paper_1105_4424_b200 import builders
-        from paper_1105_4424_b200.partition import build_schedule, partition_equally
         self.M, self.N, self.K = M, N, K
-        # weak scaling: the job's repetition space is [M*world, N]; this rank's contiguous
-        # shard is M whole rows, executed as a local task over its input hull.
-        shard = partition_equally(M * world * N, world)[rank]
-        assert shard.count == M * N and shard.offset == rank * M * N
-        g = orc.gemm_tilers(M, N, K)
-        model = builders.tile_task_model(
-            "matmul", {"a": f"in float32 [{M},{K}]", "b": f"in float32 [{K},{N}]", "c": f"out float32 [{M},{N}]"},
-            {k: _tiler(v) for k, v in g.items()}, (M, N))
-        gen = torch.Generator(device=device).manual_seed(2 + rank)
-        a = torch.randn(M * K, device=device, generator=gen)
+        model = builders.matmul_model(M, N, K)
+        # every rank holds the same A and B (seeded); at N > 1 rank r runs launch r of the
+        # schedule built with device_count = N: rows [r*M/N, (r+1)*M/N) of C
+        a = torch.randn(M * K, device=device, generator=torch.Generator(device=device).manual_seed(2))
         b = torch.randn(K * N, device=device, generator=torch.Generator(device=device).manual_seed(3))
-        self._prepare(torch, device, model, build_schedule(model, 1), {"p_a": a, "p_b": b}, {}, {"p_c": M * N})
+        self._prepare(torch, device, model, {"p_a": a, "p_b": b}, {}, {"p_c": M * N}, rank, world)
         del a, b
-        self.units_per_step = 2.0 * M * N * K / 1e12          # TFLOP
-        self.algorithmic = {"flop_per_launch": 2 * M * N * K, "per_unit": "2 FLOP per (m, n, k)"}
-        self.workload = f"matmul {M}x{N}x{K} fp32 (TF32 tcgen05), rep space [{M}x{world},{N}] sharded by rows"
-        self.l2 = "inputs (768 MiB/rank) exceed the 126 MB L2"
+        self.units_per_step = 2.0 * M * N * K / 1e12          # TFLOP of the whole job
+        self.algorithmic = {"flop_per_launch": int(2 * M * N * K * self.rank_fraction),
+                            "per_unit": "2 FLOP per (m, n, k)"}
+        self.workload = (f"matmul {M}x{N}x{K} fp32 (TF32 tcgen05), rep space [{M},{N}] sharded by contiguous "
+                         f"row blocks over {world} rank(s)")
+        self.l2 = "inputs (768 MiB) exceed the 126 MB L2"
 
     def e2e_setup(self):
         torch = self.torch
@@ -277,55 +339,67 @@ class MatmulWorkload(Workload):
         self.hout = {"p_c": torch.empty(self.M * self.N).pin_memory()}
         self.e2e_bytes = ((self.M * self.K + self.K * self.N) * 4, self.M * self.N * 4)
 
-    # CPU oracle on a bounded sample of rows
     def cpu_sample(self, seconds: float = 8.0):
+        """SURVEY.md §8(d) C2 baseline: numpy.matmul fp32 (OpenBLAS sgemm on every host core) on
+        the same A and B the GPU multiplied, the whole 8192^3 product, best of 2; plus the
+        normwise error of both results against an fp64 product on 64 sampled rows, and the
+        oracle's k-ascending C port (the reference's order) on a few rows as a secondary."""
         from oracle import c_oracle as co
         M, N, K = self.M, self.N, self.K
-        rng = np.random.default_rng(0)
-        A = rng.standard_normal(M * K, dtype=np.float32)
-        B = rng.standard_normal(K * N, dtype=np.float32)
-        Cm = np.zeros(M * N, np.float32)
+        st = self.ex.storage
+        A = st.array("p_a").cpu().numpy().reshape(M, K)
+        B = st.array("p_b").cpu().numpy().reshape(K, N)
+        ours = self.ex.outputs(on_device=True)["p_c"].view(M, N)
+        best = None
+        for _ in range(2):
+            t0 = time.perf_counter()
+            C = np.matmul(A, B)
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+            if best * 2 > seconds * 2:
+                break
+        rows = np.random.default_rng(1).choice(M, 64, replace=False)
+        ref64 = A[rows].astype(np.float64) @ B.astype(np.float64)
+        err_blas = normwise(C[rows], ref64)
+        err_ours = normwise(ours[rows].cpu().numpy(), ref64)
+        del C
+        # secondary: the oracle's order-pinned C port on a bounded block of rows
         thr = co.threads()
-        rows = max(1, thr)
+        Cm = np.zeros(M * N, np.float32)
+        r2 = max(thr, 8)
         t0 = time.perf_counter()
-        co.gemm_rows(A, B, Cm, N, K, 0, rows)
-        dt = time.perf_counter() - t0
-        target = int(rows * seconds / max(dt, 1e-3))
-        rows2 = max(rows, min(M, (target // thr) * thr))
-        t0 = time.perf_counter()
-        co.gemm_rows(A, B, Cm, N, K, 0, rows2)
-        dt = time.perf_counter() - t0
-        flops = 2.0 * rows2 * N * K
-        return {"value": flops / dt / 1e12, "unit": self.unit, "cores": thr, "kind": "port",
-                "sample": f"{rows2} of {M} rows of C ({flops / 1e9:.1f} GFLOP), oracle/aol_oracle.c "
-                          f"k-ascending fp32, OpenMP {thr} threads, {dt:.2f} s"}
+        co.gemm_rows(A.ravel(), B.ravel(), Cm, N, K, 0, r2)
+        dt2 = time.perf_counter() - t0
+        flops = 2.0 * M * N * K
+        return {"value": flops / best / 1e12, "unit": self.unit, "cores": os.cpu_count(), "kind": "port",
+                "impl": "numpy.matmul fp32 (OpenBLAS sgemm)",
+                "sample": f"the whole {M}x{N}x{K} product on the GPU's A and B, best of 2: {best:.2f} s",
+                "blas": openblas_info(),
+                "accuracy": {"normwise_vs_fp64_64_rows": {"openblas_fp32": err_blas, "ours": err_ours}},
+                "secondary": {"value": 2.0 * r2 * N * K / dt2 / 1e12, "unit": self.unit, "cores": thr,
+                              "kind": "port", "sample": f"{r2} rows of C with oracle/aol_oracle.c "
+                                                        f"(k-ascending fp32, the reference's order), {dt2:.2f} s"}}
 
 
 class StencilWorkload(Workload):
-    """Config C4: 3x3 toroidal stencil on a 16384^2 fp32 torus per rank (N independent tori)."""
+    """Config C4: 3x3 toroidal stencil on a 16384^2 fp32 torus (at N ranks: 16384/N rows each)."""
 
     name = "stencil"
 
     def __init__(self, torch, device, rank, world, n=16384):
-        from oracle import aol_oracle as orc
         from paper_1105_4424_b200 import builders
-        from paper_1105_4424_b200.partition import build_schedule
         self.n = n
-        t = orc.stencil_tilers(n, n)
-        w = orc.stencil_weights()
-        model = builders.tile_task_model(
-            "stencil", {"x": _spec(t["x"], "in"), "w": "in float32 [9]", "y": _spec(t["y"], "out")},
-            {k: _tiler(v) for k, v in t.items()}, (n, n))
-        gen = torch.Generator(device=device).manual_seed(5 + rank)
-        x = torch.randn(n * n, device=device, generator=gen)
-        self._prepare(torch, device, model, build_schedule(model, 1),
-                      {"p_x": x, "p_w": torch.from_numpy(w).to(device)},
-                      {"p_x": (n * n, "rand"), "p_w": (9, w)}, {"p_y": n * n})
+        w = builders.stencil_weights()
+        x = torch.randn(n * n, device=device, generator=torch.Generator(device=device).manual_seed(5))
+        self._prepare(torch, device, builders.stencil_model(n, n), {"p_x": x, "p_w": torch.from_numpy(w).to(device)},
+                      {"p_x": (n * n, "rand"), "p_w": (9, w)}, {"p_y": n * n}, rank, world)
         del x
         self.units_per_step = 2.0 * n * n * 4 / 1e9            # GB (read x once, write y once)
-        self.algorithmic = {"bytes_per_launch": 2 * n * n * 4, "per_unit": "4 B read + 4 B written per element"}
-        self.workload = f"toroidal 3x3 stencil {n}x{n} fp32, origin (-1,-1), weights [1,2,1]^T[1,2,1]/16"
-        self.l2 = "inputs (1 GiB/rank) exceed the 126 MB L2"
+        self.algorithmic = {"bytes_per_launch": int(2 * n * n * 4 * self.rank_fraction),
+                            "per_unit": "4 B read + 4 B written per element"}
+        self.workload = (f"toroidal 3x3 stencil {n}x{n} fp32, origin (-1,-1), weights [1,2,1]^T[1,2,1]/16, "
+                         f"rows sharded over {world} rank(s)")
+        self.l2 = "inputs (1 GiB) exceed the 126 MB L2"
 
     def cpu_sample(self, seconds: float = 8.0):
         from oracle import c_oracle as co
@@ -350,30 +424,17 @@ class DownscalerWorkload(Workload):
     name = "downscaler"
 
     def __init__(self, torch, device, rank, world, frames=256, H=2160, W=3840):
-        from oracle import aol_oracle as orc
         from paper_1105_4424_b200 import builders
-        from paper_1105_4424_b200.partition import build_schedule
-        th = orc.hfilter_tilers(frames, H, W)
-        Wo = th["y"]["array"][2]
-        tv = orc.vfilter_tilers(frames, H, Wo)
-        Ho = tv["y"]["array"][1]
-        wh, wv = orc.hfilter_weights(), orc.vfilter_weights()
-        model = builders.chain_model(
-            [("h", "hfilter", {"x": _spec(th["x"], "in"), "w": f"in float32 [{wh.size}]",
-                               "y": _spec(th["y"], "out")}, {k: _tiler(v) for k, v in th.items()},
-              th["x"]["rep"]),
-             ("v", "vfilter", {"x": _spec(tv["x"], "in"), "w": f"in float32 [{wv.size}]",
-                               "y": _spec(tv["y"], "out")}, {k: _tiler(v) for k, v in tv.items()},
-              tv["x"]["rep"])],
-            {"x": _spec(th["x"], "in"), "wh": f"in float32 [{wh.size}]", "wv": f"in float32 [{wv.size}]"},
-            {"y": _spec(tv["y"], "out")},
-            [("x", "h.x"), ("wh", "h.w"), ("h.y", "v.x"), ("wv", "v.w"), ("v.y", "y")])
+        model = builders.downscaler_model(frames, H, W)
+        Wo = W // 8 * 3
+        Ho = H // 9 * 4
+        wh, wv = builders.downscaler_weights(13, 3), builders.downscaler_weights(14, 4)
         nx = frames * H * W
-        gen = torch.Generator(device=device).manual_seed(4 + rank)
-        x = torch.rand(nx, device=device, generator=gen)
-        self._prepare(torch, device, model, build_schedule(model, 1),
+        x = torch.rand(nx, device=device, generator=torch.Generator(device=device).manual_seed(4))
+        self._prepare(torch, device, model,
                       {"x": x, "wh": torch.from_numpy(wh).to(device), "wv": torch.from_numpy(wv).to(device)},
-                      {"x": (nx, "rand"), "wh": (wh.size, wh), "wv": (wv.size, wv)}, {"y": frames * Ho * Wo})
+                      {"x": (nx, "rand"), "wh": (wh.size, wh), "wv": (wv.size, wv)}, {"y": frames * Ho * Wo},
+                      rank, world)
         del x
         hbytes = (nx + frames * H * Wo) * 4
         vbytes = (frames * H * Wo + frames * Ho * Wo) * 4
@@ -384,13 +445,14 @@ class DownscalerWorkload(Workload):
         fused = self.ex.fused_launches > 0
         step_bytes = (nx + frames * Ho * Wo) * 4 if fused else hbytes + vbytes
         self.units_per_step = step_bytes / 1e9
-        self.algorithmic = {"bytes_per_step": step_bytes, "fused": fused, "unfused_h_bytes": hbytes,
-                            "unfused_v_bytes": vbytes,
+        self.algorithmic = {"bytes_per_step": int(step_bytes * self.rank_fraction), "fused": fused,
+                            "unfused_h_bytes": hbytes, "unfused_v_bytes": vbytes,
                             "per_unit": "each array element read once / written once "
                                         + ("(fused: x and y only)" if fused else "per filter")}
         self.workload = (f"downscaler {frames}x{H}x{W} fp32: hfilter 13->3 paving 8 -> vfilter 14->4 paving 9, "
-                         + ("fused into one streaming kernel (intermediate never leaves registers)" if fused else "two tasks"))
-        self.l2 = "inputs (8.5 GB/rank) exceed the 126 MB L2"
+                         + ("fused into one streaming kernel (intermediate never leaves registers)" if fused
+                            else "two tasks") + f", frames sharded over {world} rank(s)")
+        self.l2 = "inputs (8.5 GB) exceed the 126 MB L2"
         self.dims = (frames, H, W, Wo, Ho)
 
     def cpu_sample(self, seconds: float = 8.0):
@@ -417,6 +479,7 @@ class SweepWorkload(Workload):
     step() runs the largest point; the per-point table is measured separately (measure_points)."""
 
     name = "sweep"
+    scaling = "weak"
 
     POINTS_M = (1, 2, 4, 8, 16, 32, 64)
 
@@ -437,6 +500,7 @@ class SweepWorkload(Workload):
 
     def __init__(self, torch, device, rank, world):
         self.torch, self.device = torch, device
+        self.rank, self.world, self.rank_fraction = rank, world, 1.0
         self.points = []
         for m in self.POINTS_M:
             for kind in ("dense", "overlap", "gaps", "strided", "rowstride"):
@@ -659,13 +723,17 @@ class CGWorkload(Workload):
         n, rowptr, colidx, vals = self._matrix()
         self.n, self.nnz = n, int(rowptr[-1])
         self.model = model_from_dict(_resize_model_dict(base, 400, 1920, n, self.nnz))
-        self.schedule = build_schedule(self.model, 1)
+        self.rank, self.world = rank, world
+        # at N ranks: D = N launches per step, launch r on rank r (the distributed executor:
+        # p all-gathered after each update, dot partials reduced on the device)
+        self.schedule = build_schedule(self.model, world)
+        self.rank_fraction = 1.0 / world
         self.bind = {"rowptr": rowptr, "colidx": colidx, "values": vals, "b": np.ones(n)}
         # `value` is measured with the inputs already resident in HBM (the executor's storage is
         # filled by device-to-device copies); e2e_step binds the host arrays instead
         self.dbind = {k: torch.from_numpy(np.ascontiguousarray(v)).to(device) for k, v in self.bind.items()}
         self.torch, self.device = torch, device
-        ex = Executor(self.model, self.schedule, self.bind, 1)
+        ex = self._executor(self.bind)
         ex.run()
         torch.cuda.synchronize()
         self.iters = ex.iterations
@@ -673,25 +741,45 @@ class CGWorkload(Workload):
         self.units_per_step = self.flop / 1e9
         self.algorithmic = {"flop_per_solve": self.flop, "iterations": self.iters,
                             "per_unit": "per iteration 2*nnz (spmv) + 3 dots + 3 vector updates (12n)"}
+        how = ("the whole LoopStep as ONE persistent cooperative kernel interpreting the loop body" if world == 1
+               else f"rows sharded over {world} ranks, p exchanged after each update, dots reduced on the device")
         self.workload = (f"CG (bundled cg.gmodel resized) {self.matrix}: n={n}, nnz={self.nnz}, {self.iters} "
-                         f"iterations; the whole LoopStep as ONE persistent cooperative kernel interpreting the loop body (Executor setup timed, inputs resident in HBM)")
+                         f"iterations; {how} (Executor setup timed, inputs resident in HBM)")
         self.l2 = "working set (~12 MB) fits in L2: L2 flushed (256 MiB write) before every timed step"
         self.ex = None
 
     graphs = True
     l2_flush = True
 
-    def step(self):
+    def _executor(self, bind):
+        if self.world > 1:
+            from paper_1105_4424_b200.distributed import make_distributed_executor
+            return make_distributed_executor(self.model, self.schedule, bind)
         from paper_1105_4424_b200.executor import Executor
-        ex = Executor(self.model, self.schedule, self.dbind, 1, graphs=self.graphs)
-        ex.run()
+        return Executor(self.model, self.schedule, bind, 1, graphs=self.graphs)
+
+    def step(self):
+        self._executor(self.dbind).run()
+
+    def gather(self):
+        return None
 
     def e2e_setup(self):
         self.e2e_bytes = (sum(v.nbytes for v in self.bind.values()), self.n * 8)
 
     def e2e_step(self):
         from paper_1105_4424_b200.executor import execute_schedule
+        if self.world > 1:
+            ex = self._executor(self.bind)
+            ex.run()
+            return ex.outputs()
         return execute_schedule(self.model, self.schedule, self.bind, 1, graphs=self.graphs).outputs
+
+    def e2e_numpy_setup(self):
+        pass
+
+    def e2e_numpy_step(self):
+        return self.e2e_step()
 
     def e2e_free(self):
         pass
@@ -742,15 +830,14 @@ class C1Workload(Workload):
     unit = "TFLOP/s"
     bound = "tensor"
 
+    scaling = "weak"
+
     def __init__(self, torch, device, rank, world, n=256):
-        from oracle import aol_oracle as orc
         from paper_1105_4424_b200 import builders
         from paper_1105_4424_b200.partition import build_schedule
         self.torch, self.device, self.n = torch, device, n
-        g = orc.gemm_tilers(n, n, n)
-        self.model = builders.tile_task_model(
-            "matmul", {"a": f"in float32 [{n},{n}]", "b": f"in float32 [{n},{n}]", "c": f"out float32 [{n},{n}]"},
-            {k: _tiler(v) for k, v in g.items()}, (n, n))
+        self.rank, self.world, self.rank_fraction = rank, world, 1.0
+        self.model = builders.matmul_model(n, n, n)
         self.schedule = build_schedule(self.model, 1)
         rng = np.random.default_rng(0)
         self.bind = {"p_a": rng.standard_normal(n * n, dtype=np.float32),
@@ -776,6 +863,12 @@ class C1Workload(Workload):
         # host numpy in, host numpy out, exactly like the reference executor is called
         from paper_1105_4424_b200.executor import execute_schedule
         execute_schedule(self.model, self.schedule, self.bind, 1)
+
+    def e2e_numpy_setup(self):
+        pass
+
+    def e2e_numpy_step(self):
+        self.e2e_step()
 
     def e2e_free(self):
         pass
@@ -858,6 +951,13 @@ def run_gpu(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    def allsum(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=red_dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
     _capi.load()
     all_cpus = os.sched_getaffinity(0)
     numa = bind_host_to_gpu_numa(torch, local)
@@ -882,60 +982,77 @@ def run_gpu(args):
     launches = (_capi.launch_counter() - launches0 - warm_launches)
     total_ms = allmax(total_ms)
     ms_per_step = total_ms / args.steps
-    value = wl.units_per_step * world * args.steps / (total_ms * 1e-3)
+    # whole-job units per step: the configured problem (strong) or one copy per rank (weak)
+    job_units = wl.units_per_step * (world if wl.scaling == "weak" else 1)
+    value = job_units * args.steps / (total_ms * 1e-3)
     kernel_ms = allmax(statistics.mean(per))
 
-    # end to end through the public API (H2D + launch + D2H every step)
-    e2e = None
-    if not args.no_e2e:
-        wl.e2e_setup()
-        for _ in range(3):
-            wl.e2e_step()
+    def timed_e2e(step_fn, setup_fn, steps):
+        setup_fn()
+        for _ in range(2):
+            step_fn()
         torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()
-        for _ in range(args.e2e_steps):
-            wl.e2e_step()
+        for _ in range(steps):
+            step_fn()
         torch.cuda.synchronize()
-        el = allmax(time.perf_counter() - t0)
-        wl.e2e_free()
-        e2e = {"value": wl.units_per_step * world * args.e2e_steps / el, "unit": wl.unit,
-               "h2d_bytes_per_step": wl.e2e_bytes[0] * world, "d2h_bytes_per_step": wl.e2e_bytes[1] * world,
+        return allmax(time.perf_counter() - t0)
+
+    # end to end through the public API (H2D + launch + D2H every step)
+    e2e = None
+    e2e_np = None
+    if not args.no_e2e:
+        el = timed_e2e(wl.e2e_step, wl.e2e_setup, args.e2e_steps)
+        h2d = wl.e2e_bytes[0] * (world if wl.scaling == "weak" else 1)
+        if world > 1 and wl.scaling == "strong" and hasattr(wl, "e2e_h2d"):
+            h2d = int(allsum(float(wl.e2e_h2d)))
+        e2e = {"value": job_units * args.e2e_steps / el, "unit": wl.unit,
+               "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": wl.e2e_bytes[1] * (world if wl.scaling == "weak" else 1),
                "ms_per_step": el * 1e3 / args.e2e_steps, "steps": args.e2e_steps,
-               "path": "paper_1105_4424_b200.executor.execute_schedule(pipeline=%d): pinned host bindings and "
-                       "out= buffers; chunked H2D / launch / D2H overlap" % getattr(wl, "pipeline", 0),
+               "path": ("paper_1105_4424_b200.executor.execute_schedule(pipeline=%d): pinned host bindings and "
+                        "out= buffers; chunked H2D / launch / D2H overlap" % getattr(wl, "pipeline", 0))
+               if world == 1 or wl.scaling == "weak" else
+               ("make_distributed_executor on pinned host bindings: each rank uploads its input hull, runs "
+                "its launch; output ranges gather to rank 0 (NCCL send/recv), rank 0 copies the result down"),
                "host_numa": numa}
+        if not args.no_e2e_numpy and hasattr(wl, "e2e_numpy_setup") and wl.name not in ("downscaler", "sweep") \
+                and (world == 1 or wl.scaling == "weak"):
+            el = timed_e2e(wl.e2e_numpy_step, wl.e2e_numpy_setup, max(3, args.e2e_steps // 2))
+            n = max(3, args.e2e_steps // 2)
+            e2e_np = {"value": job_units * n / el, "unit": wl.unit, "ms_per_step": el * 1e3 / n, "steps": n,
+                      "h2d_bytes_per_step": e2e["h2d_bytes_per_step"], "d2h_bytes_per_step": e2e["d2h_bytes_per_step"],
+                      "path": "execute_schedule(model, schedule, {port: numpy array}, D) -> numpy outputs: the "
+                              "reference's call (refexec.py:427), pageable host memory both ways"}
+        wl.e2e_free()
     os.sched_setaffinity(0, all_cpus)            # the CPU baseline gets every host core again
 
-    # N > 1: the output shards gathered to rank 0 over NCCL, timed separately from the
-    # concurrent per-rank phase (north_star: "NCCL output gather reported separately")
+    # N > 1: the output ranges gathered to rank 0, timed separately from the concurrent
+    # per-rank phase (north_star: "NCCL output gather reported separately")
     gather = None
     if world > 1 and not args.no_gather:
-        shard = wl.output_shard()
-        if shard is not None:
-            shard = shard.contiguous()
-            dst = [torch.empty_like(shard) for _ in range(world)] if rank == 0 else None
-            if backend != "nccl":
-                shard_h = shard.cpu()
-                dst = [torch.empty_like(shard_h) for _ in range(world)] if rank == 0 else None
-            reps, times = 3, []
-            for _ in range(reps + 1):
-                barrier()
-                torch.cuda.synchronize()
-                t0 = time.perf_counter()
-                dist.gather(shard if backend == "nccl" else shard_h, dst, dst=0)
-                torch.cuda.synchronize()
-                times.append(time.perf_counter() - t0)
-            g = allmax(min(times[1:]))
-            nbytes = shard.numel() * shard.element_size() * (world - 1)
-            gather = {"ms": g * 1e3, "bytes_to_root": nbytes, "GBps": nbytes / g / 1e9,
-                      "backend": backend, "op": "torch.distributed.gather of each rank's output shard to rank 0"}
-            del dst
+        times, nbytes = [], 0
+        for _ in range(3):
+            wl.step()
+            torch.cuda.synchronize()
+            barrier()
+            t0 = time.perf_counter()
+            moved = wl.gather()
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t0)
+            nbytes = moved or 0
+        if nbytes:
+            g = allmax(min(times))
+            nb = int(allsum(float(nbytes)))
+            gather = {"ms": g * 1e3, "bytes_to_root": nb, "GBps": nb / g / 1e9, "backend": backend,
+                      "op": "ShardedExecutor.gather_to_root: each rank's written output ranges to rank 0 "
+                            "(batched send/recv of exact ranges)"}
 
     peaks = measured_peaks()
     out = None
     if rank == 0:
-        achieved = wl.units_per_step / (kernel_ms * 1e-3)
+        achieved = wl.units_per_step * wl.rank_fraction / (kernel_ms * 1e-3)
         if wl.bound == "tensor":
             burst, sustained = (None, None) if args.no_peak else tf32_peak(torch, device)
             long_region = total_ms > 250.0
@@ -959,18 +1076,19 @@ def run_gpu(args):
                     "traffic": profile_traffic(wl.name),
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650",
                     "kernel_ms": kernel_ms, "algorithmic": wl.algorithmic}
-        cpu = None if args.no_cpu else wl.cpu_sample(args.cpu_seconds)
+        cpu = None if (args.no_cpu or world > 1) else wl.cpu_sample(args.cpu_seconds)
         extra = {}
         if wl.name == "sweep" and not args.no_points:
             extra["sweep_points"] = wl.measure_points()
         out = {
             "metric": METRIC, "value": value, "unit": wl.unit, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": wl.scaling,
             "vs_baseline": None, "dtype": getattr(wl, "dtype", "f32" if wl.bound == "hbm" else "tf32 (fp32 in/out)"),
             "data": "synthetic (torch.randn, seeded)",
             "config": {"workload": wl.workload, "l2": wl.l2,
                        "parallelism": f"repetition space sharded by contiguous blocks over {world} rank(s)"},
-            "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "clocks": clk,
+            "e2e": e2e, **({"e2e_numpy": e2e_np} if e2e_np else {}),
+            "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "clocks": clk,
             **({"gather": gather} if gather else {}),
             **({"test_mode": "AOL_BENCH_BACKEND=gloo: ranks share one GPU; not a scaling result"}
                if backend != "nccl" and world > 1 else {}),
@@ -991,19 +1109,39 @@ def _reference_arm(workload: str):
     from oracle import c_oracle as co
     thr = co.threads()
     rng = np.random.default_rng(0)
-    if workload in ("matmul", "c1"):
-        M = N = K = 8192 if workload == "matmul" else 256
-        A = rng.standard_normal(M * K, dtype=np.float32)
-        B = rng.standard_normal(K * N, dtype=np.float32)
-        Cm = np.zeros(M * N, np.float32)
-        rows = max(thr, 8) if workload == "matmul" else M
+    if workload == "matmul":
+        # the C2 CPU baseline is numpy.matmul fp32 (OpenBLAS sgemm, every
+        # host core) -- the whole 8192^3 product every step, same config as the GPU arm
+        M = N = K = 8192
+        A = rng.standard_normal((M, K), dtype=np.float32)
+        B = rng.standard_normal((K, N), dtype=np.float32)
 
         def step(i):
-            lo = (i * rows) % max(1, M - rows)
-            co.gemm_rows(A, B, Cm, N, K, lo, lo + rows)
-            return 2.0 * rows * N * K / 1e12
-        return step, "TFLOP/s", (f"matmul {M}x{N}x{K} fp32, {rows} rows of C per step (oracle/aol_oracle.c, "
-                                 f"k-ascending fp32, OpenMP {thr} threads)"), thr
+            np.matmul(A, B)
+            return 2.0 * M * N * K / 1e12
+        info = openblas_info()
+        return step, "TFLOP/s", (f"matmul {M}x{N}x{K} fp32, the whole product per step: numpy.matmul "
+                                 f"(OpenBLAS sgemm, {info.get('blas_threads')} threads)"), os.cpu_count()
+    if workload == "c1":
+        # the reference executor's route for the paper's MatMul: ONE spmv_csr
+        # repetitive task over the Kronecker matrix I (x) A, rows left to right with product and
+        # sum rounded separately -- refexec.py:111-121 restated by the oracle (numpy, 1 core)
+        n = 256
+        A = rng.standard_normal((n, n), dtype=np.float32)
+        B = rng.standard_normal(n * n, dtype=np.float32)
+        rows = np.repeat(np.arange(n * n), n)
+        i, j = rows // n, rows % n          # output (i, j) of C = A B as row i*n+j of kron(A, I) . vec(B)
+        k = np.tile(np.arange(n), n * n)
+        colidx = (k * n + j).astype(np.int32)
+        values = A[i, k].astype(np.float32)
+        rowptr = (np.arange(n * n + 1) * n).astype(np.int32)
+
+        def step(i_):
+            y = np.zeros(n * n, np.float32)
+            orc.spmv_rows(rowptr, colidx, values, B, y, 0, n * n)
+            return 2.0 * n ** 3 / 1e12
+        return step, "TFLOP/s", ("matmul 256^3 fp32 as the reference executes it: one spmv_csr over the "
+                                 "Kronecker CSR (16.8 M nnz), refexec.py:111-121 restated (oracle, numpy)"), 1
     if workload == "stencil":
         n = 16384
         x = rng.standard_normal(n * n, dtype=np.float32)
@@ -1085,10 +1223,12 @@ def run_reference(args):
     value = units / el
     out = {"metric": METRIC, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": el * 1e3 / args.steps, "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f64" if args.workload.startswith("cg") else "f32",
+           "scaling": WORKLOADS[args.workload].scaling, "vs_baseline": None,
+           "dtype": "f64" if args.workload.startswith("cg") else "f32",
            "data": "synthetic (numpy default_rng)", "impl": "reference",
-           "config": {"workload": f"{args.workload}: bounded sample per step: {sample}"},
-           "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "port", "sample": sample},
+           "config": {"workload": f"{args.workload}: {sample}"},
+           "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "port", "sample": sample,
+                            **({"blas": openblas_info()} if args.workload == "matmul" else {})},
            "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
@@ -1107,6 +1247,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-points", action="store_true")
     ap.add_argument("--no-gather", action="store_true", help="N>1: skip the output-gather measurement")
+    ap.add_argument("--no-e2e-numpy", action="store_true", help="skip the numpy-in / numpy-out e2e form")
     ap.add_argument("--no-fuse", action="store_true", help="disable task fusion (downscaler H->V as two kernels)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":

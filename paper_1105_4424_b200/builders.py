@@ -161,3 +161,92 @@ def b200_platform(n_sm: int = 148, lanes: int = 128, smem_bytes: int = 227 * 102
                                             PartInstance("cmem", "Cmem"))),
         "p": Component("p", P, parts=(PartInstance("host", "Host"), PartInstance("gpu", "B200"))),
     }
+
+
+# -- the BASELINE.json configs as models (SURVEY.md §8(d), Appendix A canonical tilers) -----
+
+def _bound(origin, paving, fitting, pattern, array, rep) -> tuple[Tiler, tuple, tuple]:
+    return Tiler(origin, paving, fitting, pattern), tuple(array), tuple(rep)
+
+
+def gemm_tilers(M: int, N: int, K: int) -> dict[str, Tiler]:
+    """C[i, j] = sum_k A[i, k] B[k, j] as a repetitive task over rep [M, N] (Appendix A):
+    A row i (pattern [K] along axis 1), B column j (pattern [K] along axis 0), C element."""
+    return {"a": Tiler((0, 0), ((1, 0), (0, 0)), ((0,), (1,)), (K,)),
+            "b": Tiler((0, 0), ((0, 0), (0, 1)), ((1,), (0,)), (K,)),
+            "c": Tiler((0, 0), ((1, 0), (0, 1)), ((0,), (0,)), (1,))}
+
+
+def matmul_model(M: int, N: int, K: int) -> Model:
+    """Configs C1/C2: the paper's MatMul repetitive task, fp32 in / fp32 out."""
+    return tile_task_model("matmul", {"a": f"in float32 [{M},{K}]", "b": f"in float32 [{K},{N}]",
+                                      "c": f"out float32 [{M},{N}]"}, gemm_tilers(M, N, K), (M, N))
+
+
+def stencil_tilers(H: int, W: int) -> dict[str, Tiler]:
+    """3x3 window centred on each point of an H x W torus: origin (-1, -1) written mod the
+    shape as (H-1, W-1) (DSL numbers are unsigned), identity paving and fitting."""
+    return {"x": Tiler((H - 1, W - 1), ((1, 0), (0, 1)), ((1, 0), (0, 1)), (3, 3)),
+            "y": Tiler((0, 0), ((1, 0), (0, 1)), ((0,), (0,)), (1,))}
+
+
+def stencil_weights():
+    """[1,2,1]^T [1,2,1] / 16: powers of two, so products are exact."""
+    import numpy as np
+    v = np.array([1.0, 2.0, 1.0])
+    return (np.outer(v, v) / 16.0).astype(np.float32).ravel()
+
+
+def stencil_model(H: int, W: int) -> Model:
+    """Config C4: toroidal 3x3 stencil on an H x W fp32 array."""
+    return tile_task_model("stencil", {"x": f"in float32 [{H},{W}]", "w": "in float32 [9]",
+                                       "y": f"out float32 [{H},{W}]"}, stencil_tilers(H, W), (H, W))
+
+
+def line_filter_tilers(F: int, H: int, W: int, axis: int, taps: int, step: int, outs: int):
+    """1-D window of `taps` along `axis` (1 = rows / vertical, 2 = columns / horizontal) paved by
+    `step`, `outs` outputs per repetition paved by `outs`: the Array-OL downscaler stage."""
+    rep = [F, H, W]
+    rep[axis] //= step
+    arr_out = [F, H, W]
+    arr_out[axis] = rep[axis] * outs
+    pav_x = [[1, 0, 0], [0, 1, 0], [0, 0, 1]]
+    pav_y = [[1, 0, 0], [0, 1, 0], [0, 0, 1]]
+    pav_x[axis][axis] = step
+    pav_y[axis][axis] = outs
+    fit = tuple((1,) if d == axis else (0,) for d in range(3))
+    x = Tiler((0, 0, 0), tuple(map(tuple, pav_x)), fit, (taps,))
+    y = Tiler((0, 0, 0), tuple(map(tuple, pav_y)), fit, (outs,))
+    return {"x": x, "y": y}, tuple(rep), tuple(arr_out)
+
+
+def downscaler_weights(taps: int, outs: int):
+    """Frozen downscaler weights: output j is a normalised triangle of half-width 3 centred at
+    (taps-1)(j+1/2)/outs (the spec decision the oracle also freezes)."""
+    import numpy as np
+    w = np.zeros((outs, taps))
+    for j in range(outs):
+        c = (taps - 1) * (j + 0.5) / outs
+        for i in range(taps):
+            w[j, i] = max(0.0, 3.0 - abs(i - c))
+        w[j] /= w[j].sum()
+    return w.astype(np.float32).ravel()
+
+
+def downscaler_model(F: int, H: int, W: int) -> Model:
+    """Config C3: hfilter (13 taps, paving 8 -> 3 outputs) then vfilter (14 taps, paving 9 ->
+    4 outputs) on F frames of H x W, chained through an intermediate array."""
+    th, rep_h, arr_h = line_filter_tilers(F, H, W, 2, 13, 8, 3)
+    Wo = arr_h[2]
+    tv, rep_v, arr_v = line_filter_tilers(F, H, Wo, 1, 14, 9, 4)
+
+    def dims(a):
+        return ",".join(str(d) for d in a)
+    return chain_model(
+        [("h", "hfilter", {"x": f"in float32 [{F},{H},{W}]", "w": "in float32 [39]",
+                           "y": f"out float32 [{dims(arr_h)}]"}, th, rep_h),
+         ("v", "vfilter", {"x": f"in float32 [{dims(arr_h)}]", "w": "in float32 [56]",
+                           "y": f"out float32 [{dims(arr_v)}]"}, tv, rep_v)],
+        {"x": f"in float32 [{F},{H},{W}]", "wh": "in float32 [39]", "wv": "in float32 [56]"},
+        {"y": f"out float32 [{dims(arr_v)}]"},
+        [("x", "h.x"), ("wh", "h.w"), ("h.y", "v.x"), ("wv", "v.w"), ("v.y", "y")])

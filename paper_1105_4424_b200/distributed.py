@@ -473,6 +473,14 @@ class ShardPlan:
                                 ranges.append((rank_of(l.device_index, world), lo, hi))
                     wr[st.groups[t.nodes[name]]] = (name, ds is not None, ranges)
             writes[id(step)] = wr
+        # every range of every group each rank reads at some point (the input hulls)
+        self.reads_by_rank: dict = {}
+        for rd in reads.values():
+            for g, per in rd.items():
+                acc = self.reads_by_rank.setdefault(g, [[] for _ in range(world)])
+                for r in range(world):
+                    for a, b in per[r]:
+                        acc[r] = add_range(acc[r], a, b)
         conts = _continuations(ex.schedule.steps)
 
         def kills(later: dict, g, ranges) -> bool:
@@ -655,6 +663,32 @@ class ShardedExecutor:
         self.plan = ShardPlan(self, world)
         self.stale: dict = {}          # group -> [(lo, hi, owner)] ranges the root holds stale
         self.exchanged_bytes = 0
+        self._upload_hulls()
+
+    def _upload_hulls(self) -> None:
+        """Deferred host bindings: each rank uploads only the ranges it ever reads (its input
+        hull); the root also uploads every root-output group whole, so
+        elements no launch writes keep their bound (or zero) value there."""
+        import torch
+        root_groups = set()
+        root = self.model.application_components[self.model.application_root]
+        for port in root.ports:
+            if getattr(port.direction, "value", port.direction) == "out":
+                root_groups.add(self.storage.groups[port.name])
+        self.h2d_bytes = 0
+        for rep in self._each():
+            st = rep.storage
+            for g, h in list(st.host.items()):
+                dev = st.arrays[g]
+                if rep.rank == self.root and g in root_groups:
+                    ranges = [(0, dev.numel())]
+                else:
+                    ranges = self.plan.reads_by_rank.get(g, [[]] * self.world)[rep.rank]
+                for lo, hi in ranges:
+                    dev[lo:hi].copy_(h[lo:hi], non_blocking=True)
+                    self.h2d_bytes += (hi - lo) * dev.element_size()
+                st.host.clear()
+            torch.cuda.current_stream(rep.device).synchronize()
 
     # -- per-replica context -------------------------------------------------------
     def _enter(self, rep):
@@ -813,9 +847,12 @@ class ShardedExecutor:
         return moved
 
     def outputs(self, on_device: bool = False, out: dict | None = None) -> dict:
+        """Root outputs, flat row-major (refexec.py:545-547), after gathering the stale ranges to
+        the root; other ranks take part in the gather and return {} (the root holds results)."""
         self.gather_to_root()
-        if self.root in self.replicas:
-            self._enter(self.replicas[self.root])
+        if self.root not in self.replicas:
+            return {}
+        self._enter(self.replicas[self.root])
         from .executor import Executor
         return Executor.outputs(self, on_device=on_device, out=out)
 
@@ -862,6 +899,7 @@ def make_distributed_executor(model, schedule, bindings: dict, *, group=None, **
             kw["graphs"] = False             # loop bodies need the per-step exchange
             kw["pipeline"] = 0
             D = max((len(st.launches) for st in schedule.device_steps()), default=1)
+            kw.setdefault("defer", True)      # host bindings: upload only this rank's input hull
             Executor.__init__(self, model, schedule, bindings, D, **kw)
             self.rank = tr.rank
             self._init_sharded(tr, [Replica(tr.rank, self.device, self.storage)], tr.world)

@@ -185,7 +185,7 @@ class Executor:
 
     def __init__(self, model, schedule, bindings: dict, device_count: int, *, tilers: dict | None = None,
                  precision: str = "default", device=None, stream=None, pipeline: int = 0, fuse: bool = True,
-                 graphs: bool = True):
+                 graphs: bool = True, defer: bool = False):
         torch = _torch()
         _capi.load()
         if not torch.cuda.is_available():
@@ -211,7 +211,7 @@ class Executor:
                 and steps[0].op in FILTER_OPS and steps[1].op in FILTER_OPS)
         self.pipeline = pipeline if (pipeline > 1 and (single or pair)) else 0
         with torch.cuda.device(self.device), self._on_stream():
-            self.storage = DeviceStorage(model, bindings, self.device, stream, defer=bool(self.pipeline))
+            self.storage = DeviceStorage(model, bindings, self.device, stream, defer=defer or bool(self.pipeline))
         self._tasks: dict[str, _Task] = {}
         self.fuse = fuse
         self.graphs = graphs

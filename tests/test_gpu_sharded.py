@@ -129,7 +129,9 @@ def _dist_worker(rank, world, port, q, cases, golden_dir):
             kw = {"precision": "exact"} if case == "matmul" else {}
             ex = make_distributed_executor(model, build_schedule(model, world), bind, **kw)
             ex.run()
-            got = ex.outputs()[out]
+            res = ex.outputs()
+            got = res[out] if rank == 0 else None
+            assert (rank == 0) == bool(res)
             results[case] = (got, ex.iterations, ex.exchanged_bytes, ref)
         q.put((rank, {k: (v[0] if rank == 0 else None, v[1], v[2], v[3] if rank == 0 else None)
                       for k, v in results.items()}))

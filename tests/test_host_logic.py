@@ -297,3 +297,32 @@ def test_model_memo_per_object_and_evicted():
     del m1
     gc.collect()
     assert key not in _MODEL_MEMO
+
+
+def test_config_builders_equal_the_oracle_tilers():
+    """The package's config models (used by bench.py) carry the same tilers and weights as
+    the oracle's independent restatement of SURVEY.md Appendix A."""
+    import numpy as np
+    from oracle import aol_oracle as orc
+    from paper_1105_4424_b200 import builders
+
+    def same(t, d):
+        return (tuple(t.origin) == tuple(d["origin"]) and tuple(map(tuple, t.paving)) == tuple(map(tuple, d["paving"]))
+                and tuple(map(tuple, t.fitting)) == tuple(map(tuple, d["fitting"]))
+                and tuple(t.pattern) == tuple(d["pattern"]))
+    for M, N, K in ((256, 256, 256), (13, 7, 5)):
+        o = orc.gemm_tilers(M, N, K)
+        assert all(same(builders.gemm_tilers(M, N, K)[k], o[k]) for k in "abc")
+    o = orc.stencil_tilers(33, 45)
+    assert all(same(builders.stencil_tilers(33, 45)[k], o[k]) for k in "xy")
+    assert np.array_equal(builders.stencil_weights(), orc.stencil_weights())
+    oh = orc.hfilter_tilers(2, 18, 64)
+    th, rep, arr = builders.line_filter_tilers(2, 18, 64, 2, 13, 8, 3)
+    assert all(same(th[k], oh[k]) for k in "xy") and rep == tuple(oh["x"]["rep"]) and arr == tuple(oh["y"]["array"])
+    ov = orc.vfilter_tilers(2, 18, 24)
+    tv, rep, arr = builders.line_filter_tilers(2, 18, 24, 1, 14, 9, 4)
+    assert all(same(tv[k], ov[k]) for k in "xy") and rep == tuple(ov["x"]["rep"]) and arr == tuple(ov["y"]["array"])
+    assert np.array_equal(builders.downscaler_weights(13, 3), orc.hfilter_weights())
+    assert np.array_equal(builders.downscaler_weights(14, 4), orc.vfilter_weights())
+    m = builders.downscaler_model(2, 18, 64)
+    assert set(m.application_components) >= {"HT", "VT", "m"}
