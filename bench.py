@@ -339,6 +339,54 @@ class MatmulWorkload(Workload):
         self.hout = {"p_c": torch.empty(self.M * self.N).pin_memory()}
         self.e2e_bytes = ((self.M * self.K + self.K * self.N) * 4, self.M * self.N * 4)
 
+    def fp32_faithful(self, reps: int = 10) -> dict:
+        """Secondary line: the same task in precision='3xtf32' (the fused tcgen05 hi/lo kernel
+        with K-chunked accumulation), device-timed like `value`, and its normwise error on 64
+        sampled rows against an fp64 product, next to the TF32 default and cuBLAS SIMT fp32
+        (torch.matmul, allow_tf32=False) on the same A and B."""
+        from paper_1105_4424_b200.executor import Executor
+        torch, M, N, K = self.torch, self.M, self.N, self.K
+        st = self.ex.storage
+        a, b = st.array("p_a"), st.array("p_b")
+        rows = torch.randperm(M, generator=torch.Generator().manual_seed(1))[:64].to(self.device)
+        A, B = a.view(M, K), b.view(K, N)
+        ref = A[rows].double() @ B.double()
+
+        def err(c):
+            return float(torch.linalg.norm(c.view(M, N)[rows].double() - ref) / torch.linalg.norm(ref))
+
+        def timed(fn):
+            for _ in range(3):
+                fn()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            for _ in range(reps):
+                fn()
+            e1.record()
+            e1.synchronize()
+            return e0.elapsed_time(e1) / reps
+        ex3 = Executor(self.model, self.schedule, {"p_a": a, "p_b": b}, 1, precision="3xtf32")
+        ms3 = timed(ex3.run)
+        err3 = err(ex3.outputs(on_device=True)["p_c"])
+        del ex3
+        err_tf32 = err(self.ex.outputs(on_device=True)["p_c"])
+        prev = torch.backends.cuda.matmul.allow_tf32
+        torch.backends.cuda.matmul.allow_tf32 = False
+        try:
+            ms_simt = timed(lambda: A @ B)
+            err_simt = err(A @ B)
+        finally:
+            torch.backends.cuda.matmul.allow_tf32 = prev
+        torch.cuda.empty_cache()
+        flop = 2.0 * M * N * K
+        return {"precision": "3xtf32", "value": flop / (ms3 * 1e-3) / 1e12, "unit": "TFLOP/s", "ms": ms3,
+                "normwise_vs_fp64": err3, "normwise_tf32_default": err_tf32,
+                "kernel": "k_gemm_3xtf32_pair (hi/lo split in shared memory, 3 tcgen05 products per k-slice, "
+                          "64-deep TMEM chunks summed with round-to-nearest adds)",
+                "cublas_fp32_simt": {"value": flop / (ms_simt * 1e-3) / 1e12, "ms": ms_simt,
+                                     "normwise_vs_fp64": err_simt}}
+
     def cpu_sample(self, seconds: float = 8.0):
         """SURVEY.md §8(d) C2 baseline: numpy.matmul fp32 (OpenBLAS sgemm on every host core) on
         the same A and B the GPU multiplied, the whole 8192^3 product, best of 2; plus the
@@ -1078,6 +1126,8 @@ def run_gpu(args):
                     "kernel_ms": kernel_ms, "algorithmic": wl.algorithmic}
         cpu = None if (args.no_cpu or world > 1) else wl.cpu_sample(args.cpu_seconds)
         extra = {}
+        if hasattr(wl, "fp32_faithful") and world == 1 and not args.no_peak:
+            extra["fp32_faithful"] = wl.fp32_faithful()
         if wl.name == "sweep" and not args.no_points:
             extra["sweep_points"] = wl.measure_points()
         out = {

@@ -46,6 +46,8 @@ struct Params {
   int c_vec;           // 16-byte stores allowed
   int group_m;         // tile raster: M-tiles per group sharing each B panel
   int epi_smem;        // pair kernel: stage 32x32 chunks through shared memory for row-contiguous stores
+  int chunk_kb;        // 3xtf32: k-blocks accumulated in TMEM between round-to-nearest adds
+  int hi_round;        // 3xtf32: 1 = hi rounded to tf32 (rna) and written back; 0 = hi = tensor-core truncation
 };
 
 // ------------------------------------------------------------ PTX helpers ----
@@ -509,6 +511,295 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
 }  // namespace pair
 
+// =============================================================================
+// fp32-faithful MatMul (precision="3xtf32"), fused: C = Alo.B + A.Blo + A.B with
+// A = Ahi + Alo, B = Bhi + Blo (hi = x truncated to tf32, lo = x - hi exactly), all three
+// products on the tensor cores from ONE fp32 TMA load of each operand tile.
+//   warp 0      TMA producer (each CTA): fp32 A 128x32 and B 64x32 k-blocks -> its own
+//               smem ring, completion on its own full barrier
+//   warps 8-11  converters (each CTA): write lo = x - hi next to the landed tile, where hi is
+//               x with its 13 low mantissa bits dropped -- exactly what kind::tf32 reads
+//               from an fp32 container (measured: TF32-level error otherwise), so the tile
+//               itself is the hi operand; fence.proxy.async, arrive on the leader's conv
+//               barrier.  (AOL_3XTF32_HI=1: hi rounded to nearest and written back instead.)
+//   warp 1      MMA issuer (leader CTA): per k-slice tcgen05.mma cta_group::2 kind::tf32
+//               M=256 N=128 for lo.hi, hi.lo then hi.hi
+//   warps 4-7   epilogue (each CTA): the tensor core's fp32 accumulation rounds toward
+//               zero, so its error grows linearly with K (3xtf32 through one accumulator:
+//               1.9e-5 normwise at K = 8192); here TMEM accumulates K-chunks of 64 only
+//               (two accumulators, alternating) and the epilogue adds each chunk into a
+//               running sum R in TMEM with round-to-nearest fp32 adds (tcgen05.ld/st),
+//               storing R after the last chunk.
+// TMEM: acc0 cols 0-127, acc1 cols 128-255, R cols 256-383.
+// =============================================================================
+namespace x3 {
+
+constexpr int BM = 256, BN = 128, HALF_M = 128, HALF_N = 64, STAGES = 4, CHUNK_KB = 2;
+constexpr int NUM_THREADS = 384;
+constexpr int A_BYTES = HALF_M * BK * 4;              // 16 KB fp32 (rewritten as hi)
+constexpr int B_BYTES = HALF_N * BK * 4;              // 8 KB
+constexpr int LO_OFF = A_BYTES + B_BYTES;             // lo copies follow, same layout
+constexpr int STAGE_BYTES = 2 * LO_OFF;               // 48 KB per CTA
+constexpr int R_COL = 256;
+constexpr int EPI_PITCH = 33;
+constexpr int EPI_BYTES = 4 * 32 * EPI_PITCH * 4;
+constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 1024 + 256 + EPI_BYTES;
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]),
+      "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]),
+      "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+template <bool KMAJOR, int R>
+__device__ __forceinline__ void load_operand_local(const CUtensorMap* map, uint64_t* bar, uint8_t* dst, int kcoord,
+                                                   int rcoord) {
+  if (KMAJOR) {
+    tma_load_2d(map, bar, dst, kcoord, rcoord);
+  } else {
+#pragma unroll
+    for (int c = 0; c < R / 32; ++c) tma_load_2d(map, bar, dst + c * (BK * 128), rcoord + 32 * c, kcoord);
+  }
+}
+
+template <bool A_KMAJOR, bool B_KMAJOR>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    k_gemm_3xtf32_pair(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                       Params p) {
+  using pair::arrive_leader;
+  using pair::cluster_rank;
+  using pair::cluster_sync;
+  using pair::commit_pair_multicast;
+  using pair::mma_tf32_pair;
+  using pair::PEER_MASK;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* conv = empty + STAGES;
+  uint64_t* tfull = conv + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* epi = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int pair_id = blockIdx.x >> 1, num_pairs = gridDim.x >> 1;
+  const int chunk_kb = p.chunk_kb;
+  const int n_chunks = (p.k_blocks + chunk_kb - 1) / chunk_kb;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&map_a);
+    prefetch_tmap(&map_b);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+      mbar_init(&conv[s], 2 * 128);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 2 * 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------- TMA producer (both CTAs) ----
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = pair_id; tile < p.num_tiles; tile += num_pairs) {
+        int mt, nt;
+        pair::tile_coords_pair(p, tile, mt, nt);
+        const int row0 = (int)(p.m_lo + (int64_t)mt * BM) + (int)rank * HALF_M;
+        const int col0 = nt * BN + (int)rank * HALF_N;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * STAGE_BYTES;
+          mbar_expect_tx(&full[stage], A_BYTES + B_BYTES);
+          load_operand_local<A_KMAJOR, HALF_M>(&map_a, &full[stage], sa, kb * BK, row0);
+          load_operand_local<B_KMAJOR, HALF_N>(&map_b, &full[stage], sa + A_BYTES, kb * BK, col0);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp >= 8) {
+    // ------------------------------------------------------ converters (both CTAs) ----
+    const int t = threadIdx.x - 256;
+    const uint32_t cbar0 = smem_u32(&conv[0]) & PEER_MASK;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tile = pair_id; tile < p.num_tiles; tile += num_pairs) {
+      for (int kb = 0; kb < p.k_blocks; ++kb) {
+        mbar_wait(&full[stage], phase);
+        float4* x = reinterpret_cast<float4*>(smem + stage * STAGE_BYTES);
+        float4* lo = reinterpret_cast<float4*>(smem + stage * STAGE_BYTES + LO_OFF);
+        if (p.hi_round) {
+#pragma unroll
+          for (int i = t; i < LO_OFF / 16; i += 128) {
+            const float4 v = x[i];
+            float4 h, l;
+            h.x = tf32_rna(v.x); l.x = __fsub_rn(v.x, h.x);
+            h.y = tf32_rna(v.y); l.y = __fsub_rn(v.y, h.y);
+            h.z = tf32_rna(v.z); l.z = __fsub_rn(v.z, h.z);
+            h.w = tf32_rna(v.w); l.w = __fsub_rn(v.w, h.w);
+            x[i] = h;
+            lo[i] = l;
+          }
+        } else {
+          // hi = x with the 13 low mantissa bits dropped, which is what the tensor core
+          // reads from an fp32 container; only lo is written
+#pragma unroll
+          for (int i = t; i < LO_OFF / 16; i += 128) {
+            const float4 v = x[i];
+            float4 l;
+            l.x = __fsub_rn(v.x, __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u));
+            l.y = __fsub_rn(v.y, __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u));
+            l.z = __fsub_rn(v.z, __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u));
+            l.w = __fsub_rn(v.w, __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u));
+            lo[i] = l;
+          }
+        }
+        fence_proxy_async_smem();            // generic-proxy writes -> visible to the tensor core
+        asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cbar0 + stage * 8) : "memory");
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // ---------------------------------------------------- MMA issuer (leader) ----
+      constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((A_KMAJOR ? 0u : 1u) << 15) |
+                                 ((B_KMAJOR ? 0u : 1u) << 16) | ((uint32_t)(BN >> 3) << 17) |
+                                 ((uint32_t)(BM >> 4) << 24);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = pair_id; tile < p.num_tiles; tile += num_pairs) {
+        for (int c = 0; c < n_chunks; ++c) {
+          mbar_wait(&tempty[acc], acc_phase ^ 1);
+          tc_fence_after();
+          const uint32_t d_tmem = tmem_base + acc * BN;
+          const int kb_end = min(p.k_blocks, (c + 1) * chunk_kb);
+          for (int kb = c * chunk_kb; kb < kb_end; ++kb) {
+            mbar_wait(&conv[stage], phase);
+            tc_fence_after();
+            const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+            const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+            for (int k = 0; k < BK / UMMA_K; ++k) {
+              const uint64_t ah = operand_desc<A_KMAJOR>(sa, k), al = operand_desc<A_KMAJOR>(sa + LO_OFF, k);
+              const uint64_t bh = operand_desc<B_KMAJOR>(sb, k), bl = operand_desc<B_KMAJOR>(sb + LO_OFF, k);
+              mma_tf32_pair(d_tmem, al, bh, idesc, (kb != c * chunk_kb) || (k != 0));
+              mma_tf32_pair(d_tmem, ah, bl, idesc, 1u);
+              mma_tf32_pair(d_tmem, ah, bh, idesc, 1u);
+            }
+            commit_pair_multicast(&empty[stage]);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          }
+          commit_pair_multicast(&tfull[acc]);
+          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // -------------------------------------------------------- epilogue (both CTAs) ----
+    const int ew = warp - 4;
+    const uint32_t lane_base = (uint32_t)(ew * 32) << 16;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = pair_id; tile < p.num_tiles; tile += num_pairs) {
+      int mt, nt;
+      pair::tile_coords_pair(p, tile, mt, nt);
+      for (int c = 0; c < n_chunks; ++c) {
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        const bool last = (c == n_chunks - 1);
+#pragma unroll 1
+        for (int ch = 0; ch < BN / 32; ++ch) {
+          uint32_t v[32];
+          tmem_ld32(tmem_base + lane_base + acc * BN + ch * 32, v);
+          if (c > 0) {
+            uint32_t r[32];
+            tmem_ld32(tmem_base + lane_base + R_COL + ch * 32, r);
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              v[j] = __float_as_uint(__fadd_rn(__uint_as_float(r[j]), __uint_as_float(v[j])));
+          }
+          if (!last) {
+            tmem_st32(tmem_base + lane_base + R_COL + ch * 32, v);
+            continue;
+          }
+          // final chunk: transpose the 32x32 block through padded smem, row-contiguous stores
+          const int64_t c0 = (int64_t)nt * BN + ch * 32;
+          float* st = epi + ew * 32 * EPI_PITCH;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) st[lane * EPI_PITCH + j] = __uint_as_float(v[j]);
+          __syncwarp();
+          const int64_t row0 = p.m_lo + (int64_t)mt * BM + rank * HALF_M + ew * 32;
+#pragma unroll
+          for (int rr = 0; rr < 32; rr += 4) {
+            const int r = rr + (lane >> 3), cc = 4 * (lane & 7);
+            const int64_t g = row0 + r;
+            const float* sp = st + r * EPI_PITCH + cc;
+            if (g > p.m_hi || g >= p.M) continue;
+            int64_t lo = 0, hi = p.N;
+            if (g == p.m_lo) lo = p.first - p.m_lo * p.N;
+            if (g == p.m_hi) hi = p.last - p.m_hi * p.N + 1;
+            float* dst = p.c + g * p.ldc + c0 + cc;
+            const int64_t col = c0 + cc;
+            if (p.c_vec && col >= lo && col + 4 <= hi) {
+              *reinterpret_cast<float4*>(dst) = make_float4(sp[0], sp[1], sp[2], sp[3]);
+            } else {
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (col + u >= lo && col + u < hi) dst[u] = sp[u];
+            }
+          }
+          __syncwarp();
+        }
+        if (!last) tmem_wait_st();
+        tc_fence_before();
+        arrive_leader(&tempty[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+  }
+}
+
+}  // namespace x3
+
 // ------------------------------------------------------------ host side ----
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -802,6 +1093,8 @@ __global__ void __launch_bounds__(256) k_split_b(const float* __restrict__ B, fl
 
 static int gemm_core(const float* A, const float* B, float* C, const GemmShape& g, int64_t first, int64_t count,
                      cudaStream_t stream);
+static int gemm_core_3x(const float* A, const float* B, float* C, const GemmShape& g, int64_t first, int64_t count,
+                        cudaStream_t stream);
 
 int launch_gemm_tf32(const aol_task& t, int64_t first, int64_t count, void* const* ports, cudaStream_t stream) {
   GemmShape g = recognise_gemm(t);
@@ -811,27 +1104,15 @@ int launch_gemm_tf32(const aol_task& t, int64_t first, int64_t count, void* cons
   const float* B = static_cast<const float*>(ports[1]) + g.cb;
   float* C = static_cast<float*>(ports[2]) + g.cc;
   if (t.precision != AOL_PREC_3XTF32) return gemm_core(A, B, C, g, first, count, stream);
-  // 3xTF32: C = Alo.Bhi + Ahi.Blo + Ahi.Bhi as ONE tensor-core GEMM over K' = 3K of the
-  // K-concatenated operands [Alo|Ahi|Ahi] . [Bhi;Blo;Bhi] (fp32 accumulation in TMEM).
+  const char* split_env = getenv("AOL_3XTF32_SPLIT");
+  const bool split = split_env != nullptr && split_env[0] == '1';
+  if (!split) return gemm_core_3x(A, B, C, g, first, count, stream);
+  // diagnostic form (AOL_3XTF32_SPLIT=1): C = Alo.Bhi + Ahi.Blo + Ahi.Bhi as ONE tensor-core
+  // GEMM over K' = 3K of K-concatenated operands [Alo|Ahi|Ahi] . [Bhi;Blo;Bhi] materialised in
+  // HBM (one fp32 accumulation in TMEM over all of K')
   const int64_t m_lo = first / g.N, m_hi = (first + count - 1) / g.N, rows = m_hi - m_lo + 1;
   const int64_t lda3 = (3 * g.K + 3) / 4 * 4, ldb3 = (g.N + 3) / 4 * 4;   // 16-byte TMA pitches
   float *Ap = nullptr, *Bp = nullptr;
-  {
-    // keep freed split buffers in the stream-ordered pool: with the default release
-    // threshold (0) every synchronize returns them to the driver and the next launch pays
-    // to map them again (measured: tens of ms of jitter per call)
-    static std::once_flag once[64];
-    int dev = 0;
-    AOL_CUDA_CHECK(cudaGetDevice(&dev));
-    if (dev >= 0 && dev < 64)
-      std::call_once(once[dev], [dev] {
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-          uint64_t keep = UINT64_MAX;
-          cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-        }
-      });
-  }
   AOL_CUDA_CHECK(cudaMallocAsync((void**)&Ap, (size_t)rows * lda3 * sizeof(float), stream));
   AOL_CUDA_CHECK(cudaMallocAsync((void**)&Bp, (size_t)3 * g.K * ldb3 * sizeof(float), stream));
   const int64_t sa_m = g.a_kmajor ? g.lda : 1, sa_k = g.a_kmajor ? 1 : g.lda;
@@ -932,6 +1213,60 @@ static int gemm_core(const float* A, const float* B, float* C, const GemmShape& 
   const int grid = p.num_tiles < sms ? p.num_tiles : sms;
   kern<<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(ma, mb, p);
   AOL_LAUNCH_CHECK("k_gemm_tf32");
+  return AOL_OK;
+}
+
+static int gemm_core_3x(const float* A, const float* B, float* C, const GemmShape& g, int64_t first, int64_t count,
+                        cudaStream_t stream) {
+  using namespace gemm;
+  CUtensorMap ma, mb;
+  int rc;
+  if (g.a_kmajor) rc = make_map(&ma, A, g.K, g.M, g.lda, BK, x3::HALF_M, true);
+  else rc = make_map(&ma, A, g.M, g.K, g.lda, 32, BK, false);
+  if (rc) return rc;
+  if (g.b_kmajor) rc = make_map(&mb, B, g.K, g.N, g.ldb, BK, x3::HALF_N, true);
+  else rc = make_map(&mb, B, g.N, g.K, g.ldb, 32, BK, false);
+  if (rc) return rc;
+  Params p{};
+  p.c = C;
+  p.ldc = g.ldc;
+  p.M = g.M; p.N = g.N; p.K = g.K;
+  p.first = first;
+  p.last = first + count - 1;
+  p.m_lo = first / g.N;
+  p.m_hi = p.last / g.N;
+  p.m_tiles = (int)((p.m_hi - p.m_lo + x3::BM) / x3::BM);
+  p.n_tiles = (int)((g.N + x3::BN - 1) / x3::BN);
+  p.k_blocks = (int)((g.K + BK - 1) / BK);
+  p.num_tiles = p.m_tiles * p.n_tiles;
+  p.c_vec = ((uintptr_t)C % 16 == 0) && (g.ldc % 4 == 0);
+  p.group_m = 8;
+  const char* ck = getenv("AOL_3XTF32_CHUNK");          // K elements per TMEM chunk (multiple of 32)
+  p.chunk_kb = ck ? (atoi(ck) / BK > 0 ? atoi(ck) / BK : 1) : x3::CHUNK_KB;
+  const char* hr = getenv("AOL_3XTF32_HI");
+  p.hi_round = hr ? (hr[0] != '0') : 0;
+  void (*k)(const CUtensorMap, const CUtensorMap, Params);
+  if (g.a_kmajor) k = g.b_kmajor ? x3::k_gemm_3xtf32_pair<true, true> : x3::k_gemm_3xtf32_pair<true, false>;
+  else k = g.b_kmajor ? x3::k_gemm_3xtf32_pair<false, true> : x3::k_gemm_3xtf32_pair<false, false>;
+  AOL_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)x3::SMEM_BYTES));
+  int sms = kNumSMs;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int pairs = p.num_tiles < sms / 2 ? p.num_tiles : sms / 2;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(x3::NUM_THREADS);
+  cfg.dynamicSmemBytes = x3::SMEM_BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  AOL_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k, ma, mb, p));
+  AOL_LAUNCH_CHECK("k_gemm_3xtf32_pair");
   return AOL_OK;
 }
 

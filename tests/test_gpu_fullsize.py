@@ -193,3 +193,29 @@ def test_zero_count_launch_is_a_noop():
     assert _capi.launch_counter() == before
     with pytest.raises(Exception):
         _capi.launch(task, 31, 2, [x.data_ptr(), y.data_ptr()], (), 0)   # past the repetition space
+
+
+def test_c2_matmul_8192_3xtf32_fp32_faithful():
+    """C2 in precision='3xtf32' at full size: normwise error on sampled rows <= 1e-6 and below
+    cuBLAS SIMT fp32 (allow_tf32=False) on the same rows."""
+    from paper_1105_4424_b200 import builders
+    M = N = K = 8192
+    model = builders.matmul_model(M, N, K)
+    a = torch.randn(M * K, device="cuda", generator=torch.Generator(device="cuda").manual_seed(2))
+    b = torch.randn(K * N, device="cuda", generator=torch.Generator(device="cuda").manual_seed(3))
+    from paper_1105_4424_b200.executor import Executor
+    from paper_1105_4424_b200.partition import build_schedule
+    ex = Executor(model, build_schedule(model, 3), {"p_a": a, "p_b": b}, 3, precision="3xtf32")
+    ex.run()
+    c = ex.outputs(on_device=True)["p_c"].view(M, N)
+    A, B = a.view(M, K), b.view(K, N)
+    rows = torch.tensor([0, 1, 255, 256, 2730, 2731, 5461, 5462, 8191], device="cuda")
+    c64 = A[rows].double() @ B.double()
+    ours = float(torch.linalg.norm(c[rows].double() - c64) / torch.linalg.norm(c64))
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        simt = float(torch.linalg.norm((A[rows] @ B).double() - c64) / torch.linalg.norm(c64))
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    assert ours <= 1e-6 and ours <= simt, (ours, simt)

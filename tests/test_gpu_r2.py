@@ -152,3 +152,68 @@ def test_caller_stream_orders_uploads_kernels_and_downloads():
                                precision="exact", stream=s, device_outputs=True).outputs["p_c"]
         s.synchronize()
         assert np.array_equal(dev.cpu().numpy(), ref)
+
+
+# -- fp32-faithful matmul (precision="3xtf32", the fused tcgen05 kernel) --------------------
+
+def _gemm_case(M, N, K, a_mn, b_k, seed):
+    """(tilers, ports, bindings, A, B) with A stored [M,K] or transposed [K,M], B [K,N] or [N,K]."""
+    rng = np.random.default_rng(seed)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    B = rng.standard_normal((K, N)).astype(np.float32)
+    if a_mn:
+        ta = dict(array=(K, M), rep=(M, N), pattern=(K,), origin=(0, 0), paving=((0, 0), (1, 0)),
+                  fitting=((1,), (0,)))
+        a_bind, a_arr = A.T.copy().ravel(), (K, M)
+    else:
+        ta = dict(array=(M, K), rep=(M, N), pattern=(K,), origin=(0, 0), paving=((1, 0), (0, 0)),
+                  fitting=((0,), (1,)))
+        a_bind, a_arr = A.ravel(), (M, K)
+    if b_k:
+        tb = dict(array=(N, K), rep=(M, N), pattern=(K,), origin=(0, 0), paving=((0, 1), (0, 0)),
+                  fitting=((0,), (1,)))
+        b_bind, b_arr = B.T.copy().ravel(), (N, K)
+    else:
+        tb = dict(array=(K, N), rep=(M, N), pattern=(K,), origin=(0, 0), paving=((0, 0), (0, 1)),
+                  fitting=((1,), (0,)))
+        b_bind, b_arr = B.ravel(), (K, N)
+    tc = dict(array=(M, N), rep=(M, N), pattern=(1,), origin=(0, 0), paving=((1, 0), (0, 1)),
+              fitting=((0,), (0,)))
+    ports = {"a": f"in float32 [{a_arr[0]},{a_arr[1]}]", "b": f"in float32 [{b_arr[0]},{b_arr[1]}]",
+             "c": f"out float32 [{M},{N}]"}
+    return {"a": ta, "b": tb, "c": tc}, ports, {"p_a": a_bind, "p_b": b_bind}, A, B
+
+
+@pytest.mark.parametrize("M,N,K,devices", [(256, 128, 64, 1), (300, 520, 200, 3), (1024, 768, 2048, 2),
+                                           (129, 132, 96, 5), (777, 1000, 1500, 7)])
+@pytest.mark.parametrize("a_mn,b_k", [(False, False), (False, True), (True, False), (True, True)])
+def test_matmul_3xtf32_fused_accuracy(M, N, K, devices, a_mn, b_k):
+    """Stated tolerance of precision='3xtf32' (fused kernel, K-chunked accumulation):
+    element-wise |C - C64| <= (2^-20 + 2^-21 * sqrt(K)) * (|A||B|) and normwise <= 1e-6
+    (cuBLAS SIMT fp32 measures 1.6e-6 normwise at 8192^3; TF32 alone ~8e-4)."""
+    from paper_1105_4424_b200 import builders
+    from paper_1105_4424_b200.executor import execute_schedule
+    from paper_1105_4424_b200.partition import build_schedule
+    t, ports, bind, A, B = _gemm_case(M, N, K, a_mn, b_k, M + K)
+    model = builders.tile_task_model("matmul", ports, {k: _tiler(v) for k, v in t.items()}, (M, N))
+    c = execute_schedule(model, build_schedule(model, devices), bind, devices,
+                         precision="3xtf32").outputs["p_c"].reshape(M, N)
+    a64, b64 = A.astype(np.float64), B.astype(np.float64)
+    c64 = a64 @ b64
+    bound = (2.0 ** -20 + 2.0 ** -21 * np.sqrt(K)) * (np.abs(a64) @ np.abs(b64))
+    assert np.all(np.abs(c - c64) <= bound), float(np.max(np.abs(c - c64) / bound))
+    assert np.linalg.norm(c - c64) / np.linalg.norm(c64) <= 1e-6
+
+
+def test_matmul_3xtf32_split_form_still_matches(monkeypatch):
+    """AOL_3XTF32_SPLIT=1 keeps the round-1 form (hi/lo copies in HBM, one accumulation)."""
+    from paper_1105_4424_b200 import builders
+    from paper_1105_4424_b200.executor import execute_schedule
+    from paper_1105_4424_b200.partition import build_schedule
+    monkeypatch.setenv("AOL_3XTF32_SPLIT", "1")
+    M, N, K = 320, 256, 512
+    t, ports, bind, A, B = _gemm_case(M, N, K, False, False, 9)
+    model = builders.tile_task_model("matmul", ports, {k: _tiler(v) for k, v in t.items()}, (M, N))
+    c = execute_schedule(model, build_schedule(model, 2), bind, 2, precision="3xtf32").outputs["p_c"]
+    c64 = A.astype(np.float64) @ B.astype(np.float64)
+    assert np.linalg.norm(c.reshape(M, N) - c64) / np.linalg.norm(c64) <= 4e-9 * K + 1e-6
