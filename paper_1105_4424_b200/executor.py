@@ -73,6 +73,57 @@ def torch_dtype(name: str):
     return _TORCH_DTYPES[name]
 
 
+class HostStager:
+    """Pinned staging ring for uploads from pageable host memory (numpy bindings).
+
+    A DMA from pageable memory is staged by the driver synchronously, piece by piece, so
+    it neither overlaps the host nor runs at PCIe speed.  Here piece k of a copy is
+    memcpy'd on the host into pinned slot k mod R (torch's multi-threaded CPU copy) while
+    the DMAs of the previous pieces run asynchronously on the copy stream; a slot is reused
+    only after its DMA's event completed.  Pinned sources bypass the ring."""
+
+    def __init__(self, slot_bytes: int = 16 << 20, slots: int = 4):
+        torch = _torch()
+        self.slot_bytes = slot_bytes
+        self.bufs = [torch.empty(slot_bytes, dtype=torch.uint8, pin_memory=True) for _ in range(slots)]
+        self.events = [None] * slots
+        self.k = 0
+
+    def copy(self, dst, src, stream) -> None:
+        """dst[:] = src (1-D, same dtype): dst on the device, src in host memory."""
+        torch = _torch()
+        if src.is_pinned():
+            with torch.cuda.stream(stream):
+                dst.copy_(src, non_blocking=True)
+            return
+        sb, db = src.view(torch.uint8), dst.view(torch.uint8)
+        n = sb.numel()
+        for off in range(0, n, self.slot_bytes):
+            m = min(self.slot_bytes, n - off)
+            i = self.k % len(self.bufs)
+            self.k += 1
+            if self.events[i] is not None:
+                self.events[i].synchronize()
+            buf = self.bufs[i][:m]
+            buf.copy_(sb[off:off + m])
+            with torch.cuda.stream(stream):
+                db[off:off + m].copy_(buf, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(stream)
+            self.events[i] = ev
+
+
+_STAGERS: dict = {}
+
+
+def host_stager() -> HostStager:
+    """One staging ring per process (64 MiB pinned, from torch's caching host allocator)."""
+    st = _STAGERS.get("default")
+    if st is None:
+        st = _STAGERS["default"] = HostStager()
+    return st
+
+
 class DeviceStorage:
     """Arrays per connected-port group, resident on one CUDA device (refexec.py:375-412)."""
 
@@ -357,6 +408,7 @@ class Executor:
                     st.arrays[g].copy_(st.host[g], non_blocking=True)
         comp.wait_stream(cin)
         xdev, xhost = st.arrays[xg], st.host[xg]
+        stager = host_stager()
         root = self.model.application_components[self.model.application_root]
         yname = next(p.name for p in root.ports if enum_value(p.direction) == "out")
         ydev = st.array(yname)
@@ -380,7 +432,7 @@ class Executor:
                         continue
                     for xlo, xhi in input_ranges(bx, r_lo, r_hi - r_lo):
                         for a, b in missing_ranges(uploaded, xlo, xhi):
-                            xdev[a:b].copy_(xhost[a:b], non_blocking=True)
+                            stager.copy(xdev[a:b], xhost[a:b], cin)
                             uploaded = add_range(uploaded, a, b)
                 ev_in = torch.cuda.Event()
                 ev_in.record(cin)
@@ -469,10 +521,12 @@ class Executor:
             for r in partition_equally_local(l.range.count, self.pipeline):
                 chunks.append((l.range.offset + r[0], r[1]))
 
+        stager = host_stager()
+
         def upload(name, lo, hi):
             g = st.groups[t.nodes[name]]
             if hi > lo:
-                arrays[name][lo:hi].copy_(st.host[g][lo:hi], non_blocking=True)
+                stager.copy(arrays[name][lo:hi], st.host[g][lo:hi], cin)
 
         for first, count in chunks:
             with torch.cuda.stream(cin):

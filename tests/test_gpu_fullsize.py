@@ -215,7 +215,7 @@ def test_c2_matmul_8192_3xtf32_fp32_faithful():
     prev = torch.backends.cuda.matmul.allow_tf32
     torch.backends.cuda.matmul.allow_tf32 = False
     try:
-        simt = float(torch.linalg.norm((A[rows] @ B).double() - c64) / torch.linalg.norm(c64))
+        simt = float(torch.linalg.norm((A @ B)[rows].double() - c64) / torch.linalg.norm(c64))
     finally:
         torch.backends.cuda.matmul.allow_tf32 = prev
     assert ours <= 1e-6 and ours <= simt, (ours, simt)
