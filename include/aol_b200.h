@@ -72,6 +72,11 @@ typedef enum aol_op {
  * the vector ports instead of `scalars` — lets a whole loop body run without host
  * round trips (CUDA-graph capture of LoopStep bodies). */
 #define AOL_FLAG_DEVICE_SCALARS 1
+/* flags: the task's tiled input is placed in deviceLocal memory by the MARTE allocation
+ * (memmap.py:65-133 -> placement.py): kernels with a shared-memory-staged form take it
+ * (tile_filter: the per-tile smem window `line_tiled` instead of the register-window
+ * batched kernel).  Results are identical; only the staging changes. */
+#define AOL_FLAG_STAGE_SMEM 2
 
 typedef enum aol_precision {
   AOL_PREC_DEFAULT = 0,   /* matmul: TF32 tensor cores; everything else: exact order */

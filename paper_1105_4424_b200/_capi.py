@@ -16,6 +16,7 @@ from .tiler import MAX_RANK, BoundTiler
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libaolb200.so"
 ABI_VERSION = 2
 FLAG_DEVICE_SCALARS = 1
+FLAG_STAGE_SMEM = 2
 MAX_TILERS = 4
 
 AOL_OK, AOL_EINVAL, AOL_ECUDA, AOL_EUNSUPPORTED, AOL_ENODEV = 0, -1, -2, -3, -4

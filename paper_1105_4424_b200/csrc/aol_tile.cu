@@ -2225,7 +2225,11 @@ struct alignas(16) LineGeomBuf { unsigned char b[256]; };
 // thread-per-repetition form; the int64 kernels last.
 // line-filter variants the batched kernel replaces when it applies (`tile_filter.line`, paving > 4,
 // stays: 0.82 vs 1.02 ms on 64x2048x2048 rows /8, tools/time_filters.py)
-static bool line_yields(const char* variant) { return strcmp(variant, "tile_filter.line_tiled") == 0; }
+// A task whose input the MARTE placement puts in deviceLocal memory (AOL_FLAG_STAGE_SMEM) keeps the
+// shared-memory-staged window: the placement decides the staging, not the routing heuristic.
+static bool line_yields(const aol_task& t, const char* variant) {
+  return strcmp(variant, "tile_filter.line_tiled") == 0 && !(t.flags & AOL_FLAG_STAGE_SMEM);
+}
 
 static bool filter_batched_route(const aol_task& t, int64_t first, int64_t count, DevTiler& tx, DevTiler& ty) {
   if (make_dev_tiler(t.tilers[0], tx) || make_dev_tiler(t.tilers[1], ty)) return false;
@@ -2242,7 +2246,7 @@ const char* filter_plan_name(const aol_task& t) {
   LineGeomBuf gb;
   const bool line = line_filter_geometry(t, *reinterpret_cast<LineGeom*>(&gb));
   const char* variant = line ? line_filter_variant(*reinterpret_cast<LineGeom*>(&gb)) : nullptr;
-  if (line && !line_yields(variant)) return variant;
+  if (line && !line_yields(t, variant)) return variant;
   DevTiler tx, ty;
   if (filter_batched_route(t, 0, tiler_rep_total(t.tilers[0]), tx, ty)) return "tile_filter.batched";
   if (line) return variant;
@@ -2259,7 +2263,7 @@ int launch_filter_generic(const aol_task& t, int64_t first, int64_t count, void*
     return launch_box_pool(t, first, count, ports, stream);
   LineGeomBuf gb;
   const bool line = line_filter_geometry(t, *reinterpret_cast<LineGeom*>(&gb));
-  if (line && !line_yields(line_filter_variant(*reinterpret_cast<LineGeom*>(&gb))))
+  if (line && !line_yields(t, line_filter_variant(*reinterpret_cast<LineGeom*>(&gb))))
     return launch_line_filter(t, *reinterpret_cast<LineGeom*>(&gb), first, count, ports, stream);
   DevTiler tx, ty;
   const bool batched = filter_batched_route(t, first, count, tx, ty);

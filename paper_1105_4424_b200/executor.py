@@ -139,6 +139,21 @@ class DeviceStorage:
                 self.ports[f"{path}.{port.name}" if path else port.name] = port
         self.arrays: dict = {}
         self.h2d_bytes = 0
+        # MARTE placement drives allocation: every deviceGlobal memory is ONE HBM arena and each
+        # of its port groups lives at the plan's 256 B-aligned offset (placement.plan_placement);
+        # groups without a data allocation, or placed on another tier, get their own buffers
+        from .placement import hbm_arenas, placement_of_groups
+        self.placement = placement_of_groups(model)
+        self.arenas = {mem: torch.zeros(nbytes, dtype=torch.uint8, device=device)
+                       for mem, nbytes in hbm_arenas(model).items()}
+        for node, port in self.ports.items():
+            g = self.groups[node]
+            if g in self.arrays:
+                continue
+            pl = self.placement.get(g)
+            tdt = torch_dtype(enum_value(port.data_type))
+            if pl is not None and pl.tier == "hbm" and pl.memory in self.arenas:
+                self.arrays[g] = self.arenas[pl.memory][pl.b200_offset:pl.b200_offset + pl.size_bytes].view(tdt)
         root = model.application_components[model.application_root]
         for port in root.ports:
             if enum_value(port.direction) not in ("in", "inout"):
@@ -154,9 +169,15 @@ class DeviceStorage:
                                          f"port expects {port.shape.total}")
                 if flat.device.type != "cuda":
                     self.h2d_bytes += flat.numel() * flat.element_size()
+                g = self.groups[port.name]
                 if defer and flat.device.type != "cuda" and flat.dtype == torch_dtype(dt):
-                    self.host[self.groups[port.name]] = flat
-                    t = torch.empty(flat.numel(), dtype=flat.dtype, device=device)
+                    self.host[g] = flat
+                    t = self.arrays.get(g)
+                    if t is None:
+                        t = torch.empty(flat.numel(), dtype=flat.dtype, device=device)
+                elif g in self.arrays:
+                    t = self.arrays[g]
+                    t.copy_(flat, non_blocking=True)
                 else:
                     t = flat.to(device=device, dtype=torch_dtype(dt), copy=True, non_blocking=True)
             else:
@@ -166,9 +187,15 @@ class DeviceStorage:
                                          f"port expects {port.shape.total}")
                 arr = np.ascontiguousarray(arr.astype(dt, copy=False))
                 self.h2d_bytes += arr.nbytes
+                g = self.groups[port.name]
                 if defer:
-                    self.host[self.groups[port.name]] = torch.from_numpy(arr)
-                    t = torch.empty(arr.size, dtype=torch_dtype(dt), device=device)
+                    self.host[g] = torch.from_numpy(arr)
+                    t = self.arrays.get(g)
+                    if t is None:
+                        t = torch.empty(arr.size, dtype=torch_dtype(dt), device=device)
+                elif g in self.arrays:
+                    t = self.arrays[g]
+                    t.copy_(torch.from_numpy(arr))
                 else:
                     t = torch.from_numpy(arr).to(device=device, copy=True)
             self.arrays[self.groups[port.name]] = t
@@ -180,6 +207,20 @@ class DeviceStorage:
 
     def array(self, node: str):
         return self.arrays[self.groups[node]]
+
+
+def _task_placement_flags(model, groups: dict, path: str, spec) -> int:
+    """Kernel-staging flags the MARTE placement implies for a tile task: a tiled input placed
+    in deviceLocal memory (tier "smem") asks for the shared-memory-staged kernel form."""
+    from .placement import placement_of_groups
+    pg = placement_of_groups(model)
+    flags = 0
+    for ps in spec.ports:
+        if ps.tiled and enum_value(ps.direction) in ("in", "inout"):
+            pl = pg.get(groups.get(f"{path}.{ps.name}"))
+            if pl is not None and pl.tier == "smem":
+                flags |= _capi.FLAG_STAGE_SMEM
+    return flags
 
 
 class _Task:
@@ -204,15 +245,17 @@ class _Task:
                         f"task '{task_path}': output port '{port.name}' aliases input port '{other.name}'")
         self.comp, self.spec, self.path = comp, spec, task_path
         self.nodes = {p.name: f"{task_path}.{p.name}" for p in comp.ports}
+        self.flags = 0
         self.dtype = None
         self.ctask = None
         if spec.kind != "device":
             return
         if spec.tile:
             self.dtype = enum_value(comp.port(spec.ports[0].name).data_type)
+            self.flags = _task_placement_flags(model, storage.groups, task_path, spec)
             self.ctask = _capi.make_task(spec.name, self.dtype,
                                          [bound[ps.name] for ps in spec.ports if ps.tiled],
-                                         precision=precision)
+                                         precision=precision, flags=self.flags)
             self.port_order = [ps.name for ps in spec.ports]
             self.scalar_ports = []
         else:
@@ -244,8 +287,9 @@ class Executor:
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self.model, self.schedule = model, schedule
         # MARTE memory allocation -> B200 placement; CapacityExceeded before anything is launched
-        from .placement import plan_placement
+        from .placement import check_private_and_tmem, plan_placement
         self.placement = plan_placement(model)
+        check_private_and_tmem(model, self.placement)
         self.device_count = device_count
         self.tilers = tilers or {}
         self.precision = precision

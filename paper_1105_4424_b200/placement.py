@@ -206,6 +206,53 @@ def plan_placement(model, maps: list[MemoryMap] | None = None) -> list[Placement
     return out
 
 
+# B200 register file per thread: 255 x 32-bit registers (ptxas' limit); a devicePrivate
+# (work-item private) allocation has to fit there next to the kernel's own state
+B200_PRIVATE_BYTES_PER_THREAD = 255 * 4
+# TMEM per SM (512 columns x 128 lanes x 4 B); the tcgen05 matmul allocates all 512 columns
+TMEM_COLS_PER_SM = 512
+
+
+def check_private_and_tmem(model, plan: list[Placement]) -> None:
+    """Capacity checks of the on-chip tiers the reference's memmap cannot see:
+    devicePrivate data must fit a thread's register file; every matmul task's accumulators
+    (2 x 256 fp32 TMEM columns for the TF32 kernel, 3 x 128 for the fp32-faithful one)
+    must fit the SM's 512 TMEM columns (raises CapacityExceeded)."""
+    for p in plan:
+        if p.tier == "registers" and p.size_bytes > B200_PRIVATE_BYTES_PER_THREAD:
+            raise CapacityExceeded(p.memory, p.size_bytes, B200_PRIVATE_BYTES_PER_THREAD)
+    from .model import iter_app_instances
+    for _, comp in iter_app_instances(model):
+        if comp.elementary_op == "matmul":
+            need = max(2 * 256, 3 * 128)
+            if need > TMEM_COLS_PER_SM:
+                raise CapacityExceeded("tmem", need * 128 * 4, TMEM_COLS_PER_SM * 128 * 4)
+
+
+def placement_of_groups(model, plan: list[Placement] | None = None) -> dict:
+    """Connected-port group -> its Placement (groups without a data allocation are absent)."""
+    plan = plan_placement(model) if plan is None else plan
+    groups = connected_port_groups(model)
+    out = {}
+    for p in plan:
+        for node in p.ports:
+            g = groups.get(node)
+            if g is not None:
+                out[g] = p
+    return out
+
+
+def hbm_arenas(model, plan: list[Placement] | None = None) -> dict:
+    """deviceGlobal memory path -> arena bytes: the span of its placements at their 256 B offsets."""
+    plan = plan_placement(model) if plan is None else plan
+    out: dict = {}
+    for p in plan:
+        if p.tier in ("hbm",):
+            end = p.b200_offset + p.size_bytes
+            out[p.memory] = max(out.get(p.memory, 0), (end + HBM_ALIGN - 1) // HBM_ALIGN * HBM_ALIGN)
+    return out
+
+
 KERNEL_STAGING = {
     "matmul.tcgen05_tf32": "A,B k-blocks: HBM -> TMA (128B swizzle; MN-major tf32: 128B/32B-atom) -> 4 x 48 KB smem "
                            "ring; accumulators: TMEM 2 x (128 lanes x 256 cols fp32); C: TMEM -> registers -> "

@@ -133,3 +133,28 @@ def elementwise_chain_case(n=9001, seed=4):
 
 CASES = {"matmul": matmul_case, "stencil_chain": stencil_chain_case, "downscaler": downscaler_case,
          "transpose_chain": transpose_chain_case, "elementwise": elementwise_chain_case}
+
+
+def fir_model(n=16384, taps=7, memory="dev.gmem"):
+    """1-D FIR (tile_filter, rep [n], pattern [taps], torus origin) whose input array is allocated
+    onto ``memory``: "dev.gmem" (deviceGlobal) or "dev.cu.lmem" (deviceLocal, 227 KB capacity)."""
+    import dataclasses
+    from paper_1105_4424_b200 import Tiler, builders
+    tx = Tiler((n - taps // 2,), ((1,),), ((1,),), (taps,))
+    ty = Tiler((0,), ((1,),), ((0,),), (1,))
+    model = builders.single_task_model(
+        "tile_filter", [f"x in float32 [{n}]", f"w in float32 [{taps}]", f"y out float32 [{n}]"],
+        [f"p_x in float32 [{n}]", f"p_w in float32 [{taps}]", f"p_y out float32 [{n}]"],
+        ["p_x -> t.x", "p_w -> t.w", "t.y -> p_y"],
+        [f"allocate data p_x onto {memory}", "allocate data p_w onto dev.gmem",
+         "allocate data t.y onto dev.gmem", "allocate task t onto dev.cu"],
+        repeat=(n,), tilers={"x": tx, "y": ty})
+    model = dataclasses.replace(model, platform_components=builders.platform(local_capacity=227 * 1024))
+    rng = np.random.default_rng(taps)
+    x = rng.random(n).astype(np.float32)
+    w = (rng.integers(1, 8, taps) / 8).astype(np.float32)
+    d = lambda t, arr: dict(array=arr, rep=(n,), pattern=tuple(t.pattern), origin=tuple(t.origin),  # noqa: E731
+                            paving=tuple(map(tuple, t.paving)), fitting=tuple(map(tuple, t.fitting)))
+    ref = np.zeros(n, np.float32)
+    orc.tile_filter(x, w, ref, d(tx, (n,)), d(ty, (n,)), 0, n)
+    return model, {"p_x": x, "p_w": w}, "p_y", ref

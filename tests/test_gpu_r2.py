@@ -217,3 +217,36 @@ def test_matmul_3xtf32_split_form_still_matches(monkeypatch):
     c = execute_schedule(model, build_schedule(model, 2), bind, 2, precision="3xtf32").outputs["p_c"]
     c64 = A.astype(np.float64) @ B.astype(np.float64)
     assert np.linalg.norm(c.reshape(M, N) - c64) / np.linalg.norm(c64) <= 4e-9 * K + 1e-6
+
+
+# -- placement drives execution (rows a9 / f3) ---------------------------------------------
+
+def test_memory_role_selects_the_kernel_staging():
+    """Two FIR models that differ only in where the input is allocated: deviceGlobal runs the
+    register-window batched kernel, deviceLocal the shared-memory-staged line window; both
+    equal the oracle bit for bit, and the deviceGlobal groups live in one arena at the
+    placement's offsets."""
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    from _sharded_cases import fir_model
+    from paper_1105_4424_b200 import _capi
+    from paper_1105_4424_b200.executor import Executor
+    from paper_1105_4424_b200.partition import build_schedule
+    plans = {}
+    for mem in ("dev.gmem", "dev.cu.lmem"):
+        model, bind, out, ref = fir_model(memory=mem)
+        for D in (1, 3):
+            ex = Executor(model, build_schedule(model, D), bind, D)
+            ex.run()
+            got = ex.outputs()[out]
+            assert np.array_equal(got.view(np.uint32), ref.view(np.uint32)), (mem, D)
+        t = ex.task("t")
+        ptrs = [ex.storage.array(t.nodes[n]).data_ptr() for n in t.port_order]
+        plans[mem] = _capi.plan_name(t.ctask, 0, 16384, ptrs)
+        arena = ex.storage.arenas["dev.gmem"]
+        for g, pl in ex.storage.placement.items():
+            if pl.tier == "hbm":
+                assert ex.storage.arrays[g].data_ptr() == arena.data_ptr() + pl.b200_offset
+        assert "line_tiled" in ex.placement_report() or mem == "dev.gmem"
+    assert plans == {"dev.gmem": "tile_filter.batched", "dev.cu.lmem": "tile_filter.line_tiled"}

@@ -79,3 +79,44 @@ def test_constant_and_host_tiers():
     tiers = {p.name: p.tier for p in plan_placement(m)}
     assert tiers["i"] == "hbm_readonly"                      # 128 KB > 64 KB broadcast limit
     assert kernel_staging("matmul.tcgen05_tf32").startswith("A,B k-blocks")
+
+
+def test_placement_drives_arena_offsets_and_staging_flags():
+    """Row a9/f3: the plan decides where groups live (one HBM arena per deviceGlobal memory at
+    256 B offsets) and which staging a kernel uses (deviceLocal input -> AOL_FLAG_STAGE_SMEM)."""
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    from _sharded_cases import fir_model
+    from paper_1105_4424_b200 import _capi
+    from paper_1105_4424_b200.executor import _task_placement_flags
+    from paper_1105_4424_b200.intrinsics import INTRINSICS
+    from paper_1105_4424_b200.model import connected_port_groups
+    from paper_1105_4424_b200.placement import hbm_arenas, placement_of_groups
+    flags = {}
+    for mem in ("dev.gmem", "dev.cu.lmem"):
+        model, _, _, _ = fir_model(memory=mem)
+        groups = connected_port_groups(model)
+        flags[mem] = _task_placement_flags(model, groups, "t", INTRINSICS["tile_filter"])
+        pg = placement_of_groups(model)
+        arenas = hbm_arenas(model)
+        assert list(arenas) == ["dev.gmem"]
+        offs = sorted(p.b200_offset for p in pg.values() if p.tier == "hbm")
+        assert all(o % 256 == 0 for o in offs) and len(set(offs)) == len(offs)
+        assert arenas["dev.gmem"] >= max(p.b200_offset + p.size_bytes for p in pg.values() if p.tier == "hbm")
+    assert flags == {"dev.gmem": 0, "dev.cu.lmem": _capi.FLAG_STAGE_SMEM}
+
+
+def test_private_register_budget_enforced():
+    from paper_1105_4424_b200.placement import B200_PRIVATE_BYTES_PER_THREAD, check_private_and_tmem
+    plat = builders.b200_platform()
+    n = B200_PRIVATE_BYTES_PER_THREAD // 4 + 1
+    m = _model_on(plat, [f"src in float32 [{n}]", f"dst out float32 [{n}]"],
+                  ["allocate data i onto gpu.sm.rf", "allocate data t.dst onto gpu.hbm",
+                   "allocate task t onto gpu.sm"], n=n)
+    with pytest.raises(CapacityExceeded):
+        check_private_and_tmem(m, plan_placement(m))
+    m_ok = _model_on(plat, [f"src in float32 [{n - 1}]", f"dst out float32 [{n - 1}]"],
+                     ["allocate data i onto gpu.sm.rf", "allocate data t.dst onto gpu.hbm",
+                      "allocate task t onto gpu.sm"], n=n - 1)
+    check_private_and_tmem(m_ok, plan_placement(m_ok))
