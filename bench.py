@@ -78,18 +78,71 @@ def dist_env():
 
 
 class Clocks:
-    """nvidia-smi sampler running during the timed region."""
+    """SM clock / throttle-reason sampler running during the timed region: an NVML thread at a
+    2 ms period (so a 30 ms region still gets ~15 samples), nvidia-smi -lms 100 as a fallback."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event reason bits (nvml.h: nvmlClocksEventReason*)
+    BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+            "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80}
+    PERIOD_S = 0.002
 
-    def __init__(self, gpu_index: int):
+    def __init__(self, gpu_index: int, pci_bus_id: str | None = None):
         self.gpu = gpu_index
+        self.pci = pci_bus_id
         self.proc = None
         self.path = None
+        self.thread = None
+        self.rows = []
+        self.nvml = None
+        self.handle = None
+
+    def _nvml_handle(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = None
+            if self.pci:
+                try:
+                    h = pynvml.nvmlDeviceGetHandleByPciBusId(self.pci.encode() if isinstance(self.pci, str)
+                                                             else self.pci)
+                except Exception:
+                    h = None
+            if h is None:
+                h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.nvml = pynvml
+            return h
+        except Exception:
+            return None
+
+    def _sample_loop(self):
+        nv, h = self.nvml, self.handle
+        try:
+            reasons_fn = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        except AttributeError:
+            reasons_fn = None
+        while not self.stop_flag.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+                rs = reasons_fn(h) if reasons_fn else 0
+                self.rows.append((float(sm), pw, int(rs)))
+            except Exception:
+                pass
+            self.stop_flag.wait(self.PERIOD_S)
 
     def start(self):
+        import threading
+        self.handle = self._nvml_handle()
+        if self.handle is not None:
+            self.rows = []
+            self.stop_flag = threading.Event()
+            self.thread = threading.Thread(target=self._sample_loop, daemon=True)
+            self.thread.start()
+            return
         fd, self.path = tempfile.mkstemp(suffix=".csv")
         os.close(fd)
         try:
@@ -104,6 +157,23 @@ class Clocks:
             time.sleep(0.05)
 
     def stop(self) -> dict:
+        if self.thread is not None:
+            self.stop_flag.set()
+            self.thread.join(timeout=2)
+            rows, nv = self.rows, self.nvml
+            try:
+                mx = float(nv.nvmlDeviceGetMaxClockInfo(self.handle, nv.NVML_CLOCK_SM))
+            except Exception:
+                mx = None
+            if not rows:
+                return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": ["no samples"], "source": "nvml"}
+            sm = [r[0] for r in rows]
+            reasons = sorted({n for r in rows for n, b in self.BITS.items() if r[2] & b})
+            counts = {n: sum(1 for r in rows if r[2] & b) for n, b in self.BITS.items() if any(r[2] & b for r in rows)}
+            return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "sm_mhz_min": min(sm),
+                    "sm_mhz_max": max(sm), "reasons": reasons, "reason_samples": counts,
+                    "samples": len(rows), "period_ms": self.PERIOD_S * 1e3, "source": "nvml",
+                    "power_w_max": max(r[1] for r in rows), "power_w_median": statistics.median(r[1] for r in rows)}
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -124,7 +194,7 @@ class Clocks:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows),
+                "reasons": reasons, "samples": len(rows), "source": "nvidia-smi",
                 "power_w_max": max((float(r[3]) for r in rows if r[3].replace(".", "").isdigit()), default=None)}
 
 
@@ -1012,7 +1082,8 @@ def run_gpu(args):
     wl = WORKLOADS[args.workload](torch, device, rank, world)
     stream = torch.cuda.current_stream(device)
 
-    clocks = Clocks(local)
+    _pp = torch.cuda.get_device_properties(device)
+    clocks = Clocks(local, f"{_pp.pci_domain_id:08X}:{_pp.pci_bus_id:02X}:{_pp.pci_device_id:02X}.0")
     launches0 = _capi.launch_counter()
     for _ in range(args.warmup):
         wl.step()

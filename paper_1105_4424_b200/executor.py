@@ -33,12 +33,13 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _capi
+from ._refcompat import ref_bases
 from .intrinsics import (INTRINSICS, IntrinsicShapeMismatch, _ports_match_spec, check_task_signature,
                          check_tile_signature)
 from .model import connected_port_groups, enum_value, iter_app_instances, task_component
 
 
-class MissingBinding(KeyError):
+class MissingBinding(*ref_bases("refexec", "MissingBinding", KeyError)):
     pass
 
 

@@ -27,18 +27,19 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+from ._refcompat import ref_bases
 from .model import enum_value
 from .tiler import BoundTiler, Tiler, TilerError
 
 
-class UnknownIntrinsic(ValueError):
+class UnknownIntrinsic(*ref_bases("intrinsics", "UnknownIntrinsic", ValueError)):
     def __init__(self, task_path: str, op_name: str):
-        super().__init__(f"task '{task_path}' deploys unknown intrinsic '{op_name}'")
+        ValueError.__init__(self, f"task '{task_path}' deploys unknown intrinsic '{op_name}'")
         self.task_path = task_path
         self.op_name = op_name
 
 
-class IntrinsicShapeMismatch(ValueError):
+class IntrinsicShapeMismatch(*ref_bases("intrinsics", "IntrinsicShapeMismatch", ValueError)):
     pass
 
 

@@ -56,6 +56,35 @@ def _cases(golden):
     return out
 
 
+def _check_vs_oracle(golden, name, sched, bind, outputs, stdout, exact):
+    """Pin a generated program's outputs to the oracle / the reference golden, not only the drop-in:
+    CG -> the reference executor's iteration count and x within 1e-10 (tests/test_refexec.py:237-247);
+    stencil -> bit-exact oracle; matmul -> bit-exact oracle for the exact order, else the TF32 bound."""
+    data, meta = golden
+    D = len(sched.device_steps()[0].launches)
+    if name == "cg":
+        ref = meta["cg_k20"]["runs"][str(D)]
+        assert f"iterations={ref['iterations']} " in stdout, stdout
+        x_ref = data[f"cg_k20/x_d{D}"]
+        assert np.max(np.abs(outputs["x"] - x_ref)) / np.max(np.abs(x_ref)) <= 1e-10
+    elif name == "stencil":
+        t = orc.stencil_tilers(64, 96)
+        want = orc.run_tile_task("stencil", t, {"x": bind["p_x"], "w": bind["p_w"]},
+                                 {"y": (64 * 96, np.float32)}, 64 * 96, D)["y"]
+        assert np.array_equal(outputs["p_y"], want)
+    elif name == "matmul":
+        M, N, K = 300, 264, 96
+        if exact:
+            want = orc.run_tile_task("matmul", orc.gemm_tilers(M, N, K), {"a": bind["p_a"], "b": bind["p_b"]},
+                                     {"c": (M * N, np.float32)}, M * N, D)["c"]
+            assert np.array_equal(outputs["p_c"], want)
+        else:
+            a64 = bind["p_a"].reshape(M, K).astype(np.float64)
+            b64 = bind["p_b"].reshape(K, N).astype(np.float64)
+            bound = (2.0 ** -9 + K * 2.0 ** -23) * (np.abs(a64) @ np.abs(b64))
+            assert np.all(np.abs(outputs["p_c"].reshape(M, N) - a64 @ b64) <= bound)
+
+
 def test_generated_programs_compile(golden):
     from paper_1105_4424_b200.codegen_b200 import generate_host_cpp
     import tempfile
@@ -68,7 +97,8 @@ def test_generated_programs_compile(golden):
 
 @pytest.mark.gpu
 def test_generated_programs_match_the_drop_in(golden, tmp_path):
-    """The compiled host programs produce bit-identical outputs to execute_schedule on the same inputs."""
+    """The compiled host programs produce bit-identical outputs to execute_schedule on the same inputs,
+    and those outputs match the oracle / the reference golden (_check_vs_oracle)."""
     from paper_1105_4424_b200.codegen_b200 import generate_host_cpp
     from paper_1105_4424_b200.executor import execute_schedule
     from paper_1105_4424_b200.model import enum_value
@@ -84,12 +114,15 @@ def test_generated_programs_match_the_drop_in(golden, tmp_path):
         r = subprocess.run([str(exe), str(work)], capture_output=True, text=True, timeout=120)
         assert r.returncode == 0, r.stderr
         ref = execute_schedule(model, sched, bind, len(sched.device_steps()[0].launches))
+        got_all = {}
         for p in root.ports:
             if enum_value(p.direction) == "out":
                 got = np.fromfile(work / f"{p.name}.out.bin", dtype=enum_value(p.data_type))
                 assert np.array_equal(got, ref.outputs[p.name]), (name, p.name)
+                got_all[p.name] = got
         if name == "cg":
             assert f"iterations={ref.iterations} " in r.stdout
+        _check_vs_oracle(golden, name, sched, bind, got_all, r.stdout, exact=False)
 
 
 def _nvcc(src: str, out: Path, link: bool) -> Path:
@@ -133,9 +166,12 @@ def test_generated_cuda_programs_match_the_drop_in(golden, tmp_path):
         assert r.returncode == 0, r.stderr
         kw = {"precision": "exact"} if name == "matmul" else {}
         ref = execute_schedule(model, sched, bind, len(sched.device_steps()[0].launches), **kw)
+        got_all = {}
         for p in root.ports:
             if enum_value(p.direction) == "out":
                 got = np.fromfile(work / f"{p.name}.out.bin", dtype=enum_value(p.data_type))
                 assert np.array_equal(got, ref.outputs[p.name]), (name, p.name)
+                got_all[p.name] = got
         if name == "cg":
             assert f"iterations={ref.iterations} " in r.stdout
+        _check_vs_oracle(golden, name, sched, bind, got_all, r.stdout, exact=(name == "matmul"))
