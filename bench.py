@@ -664,43 +664,101 @@ class SweepWorkload(Workload):
 
     L2_BYTES = 126 << 20
 
+    LINE = 128          # HBM fetch unit measured for these streams (profiles/r2_sweep_dram.json)
+
+    def line_floor_bytes(self, m, kind, T):
+        """DRAM-level floor of one point: distinct 128 B lines of the source touched + the output.
+
+        ncu shows whole 128 B lines fetched for 32/64 B runs (m = 8/16 gaps read the full span,
+        cudaLimitMaxL2FetchGranularity 32/64 changes nothing: profiles/r2_sweep_dram.json), so
+        this -- not the 32 B sector count -- is what the kernel must move."""
+        if kind == "rowstride":
+            return 2 * m * T * 4
+        p = {"dense": m, "overlap": max(1, m // 2), "gaps": 2 * m, "strided": m * 2}[kind]
+        f = 2 if kind == "strided" else 1
+        Ts = int(min(T, 1 << 15))
+        Ts -= Ts % max(1, self.LINE // 4)
+        Ts = max(Ts, min(T, 1))
+        offs = (np.arange(Ts, dtype=np.int64)[:, None] * p + np.arange(m, dtype=np.int64)[None, :] * f) * 4
+        lines = np.unique(offs // self.LINE).size * (T / Ts)
+        span_lines = -(-(self._geometry(m, kind, T)[0] * 4) // self.LINE)
+        return int(min(lines, span_lines) * self.LINE) + T * m * 4
+
+    def _flush(self, i):
+        # write a buffer larger than L2, then READ another one: the L2 is left holding clean
+        # lines, so the timed launch pays neither for its inputs being cached nor for the
+        # flush's own dirty write-backs (tools/sweep_probe.py: the write-only flush added
+        # 4-8 us of write-back to 15-30 us launches)
+        self.scrub.fill_(float(i))
+        self.acc.copy_(self.rd.sum())
+
+    def _time(self, fn, flush, steps, warmup):
+        torch = self.torch
+        for _ in range(warmup):
+            fn()
+        if flush:
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+            for i, (a, b) in enumerate(ev):
+                self._flush(i)
+                a.record()
+                fn()
+                b.record()
+            torch.cuda.synchronize()
+            return statistics.median(a.elapsed_time(b) for a, b in ev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            fn()
+        e1.record()
+        e1.synchronize()
+        return e0.elapsed_time(e1) / steps
+
     def measure_points(self, steps=10, warmup=3):
         """Per-point table.  Points whose footprint is below 3x the L2 are timed launch by
-        launch with a 256 MiB L2 flush before each launch (outside its event pair); larger
-        points are timed back to back."""
+        launch with an L2 flush before each launch (outside its event pair, median of the
+        launches); larger points are timed back to back.  Each row carries its DRAM line floor
+        (floor_frac = floor bytes / time / peak), a device-to-device copy of the same floor
+        bytes timed the same way (the achievable rate at that size: frac_of_copy), and the ncu
+        DRAM bytes of the same point from profiles/r2_sweep_dram.json when it was captured."""
         torch = self.torch
         from paper_1105_4424_b200 import _capi
         rows = []
-        scrub = torch.empty(64 << 20, dtype=torch.float32, device=self.device)
+        self.scrub = torch.empty(64 << 20, dtype=torch.float32, device=self.device)
+        self.rd = torch.ones(64 << 20, dtype=torch.float32, device=self.device)
+        self.acc = torch.zeros(1, device=self.device)
+        peak = measured_peaks().get("hbm_gbs", 6650.0)
+        ncu = {}
+        pf = ROOT / "profiles" / "r2_sweep_dram.json"
+        if pf.exists():
+            try:
+                ncu = {(r["m"], r["paving"], r["T"]): r for r in json.loads(pf.read_text())["points"]}
+            except (ValueError, KeyError):
+                ncu = {}
         for m, kind, T in self.points:
             t = self._make(m, kind, T)
             st = int(torch.cuda.current_stream().cuda_stream)
-            for _ in range(warmup):
-                _capi.launch(t["task"], 0, T, t["ptrs"], (), st)
             flush = (t["x"].numel() + t["y"].numel()) * 4 < 3 * self.L2_BYTES
-            if flush:
-                ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                      for _ in range(steps)]
-                for a, b in ev:
-                    scrub.fill_(float(len(rows)))
-                    a.record()
-                    _capi.launch(t["task"], 0, T, t["ptrs"], (), st)
-                    b.record()
-                torch.cuda.synchronize()
-                ms = sum(a.elapsed_time(b) for a, b in ev) / steps
-            else:
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record()
-                for _ in range(steps):
-                    _capi.launch(t["task"], 0, T, t["ptrs"], (), st)
-                e1.record()
-                e1.synchronize()
-                ms = e0.elapsed_time(e1) / steps
-            rows.append({"m": m, "paving": kind, "T": T, "plan": t["plan"], "ms": ms,
-                         "GBps": t["bytes"] / (ms * 1e-3) / 1e9, "l2_flushed": flush})
+            ms = self._time(lambda: _capi.launch(t["task"], 0, T, t["ptrs"], (), st), flush, steps, warmup)
+            floor = self.line_floor_bytes(m, kind, T)
+            row = {"m": m, "paving": kind, "T": T, "plan": t["plan"], "ms": ms,
+                   "GBps": t["bytes"] / (ms * 1e-3) / 1e9, "frac": t["bytes"] / (ms * 1e-3) / 1e9 / peak,
+                   "floor_bytes": floor, "floor_frac": floor / (ms * 1e-3) / 1e9 / peak, "l2_flushed": flush}
+            if T <= 10 ** 8 and floor // 8 >= 1:
+                n = floor // 8                                   # copy_ of n floats moves 8n bytes
+                ca = torch.empty(n, device=self.device)
+                cb = torch.empty_like(ca)
+                cms = self._time(lambda: cb.copy_(ca), flush, steps, warmup)
+                row["copy_ms"] = cms
+                row["frac_of_copy"] = cms / ms
+                del ca, cb
+            k = ncu.get((m, kind, T))
+            if k:
+                row["ncu_dram_bytes"] = k["dram_bytes"]
+                row["ncu_dram_over_floor"] = k["dram_bytes"] / floor
+            rows.append(row)
             del t
             torch.cuda.empty_cache()
-        del scrub
+        del self.scrub, self.rd
         return rows
 
     def e2e_setup(self):
@@ -857,8 +915,16 @@ class CGWorkload(Workload):
         self.iters = ex.iterations
         self.flop = self.iters * (2 * self.nnz + 12 * n) + 2 * n
         self.units_per_step = self.flop / 1e9
+        # roofline bytes: per iteration the loop body's distinct HBM-level traffic -- spmv values
+        # (8 B) + colidx (4 B) per nnz, rowptr 4 B and x read / y written 8 B each per row, then
+        # dot(p,Ap) 16n, axpy x 24n, axpy r 24n, dot(r,r) 16n, scale p 16n, axpy p 24n
+        self.roof_bytes = self.iters * (12 * self.nnz + 4 * (n + 1) + 16 * n + 120 * n)
         self.algorithmic = {"flop_per_solve": self.flop, "iterations": self.iters,
-                            "per_unit": "per iteration 2*nnz (spmv) + 3 dots + 3 vector updates (12n)"}
+                            "per_unit": "per iteration 2*nnz (spmv) + 3 dots + 3 vector updates (12n)",
+                            "roof_bytes_per_solve": self.roof_bytes,
+                            "roof_bytes_per_unit": "per iteration 12*nnz + 4*(n+1) + 136*n (spmv + dots + updates)",
+                            "note": "the ~12 MB working set stays in L2 across iterations; the solve is bound by "
+                                    "the per-phase grid barriers (latency), so the HBM fraction is a floor"}
         how = ("the whole LoopStep as ONE persistent cooperative kernel interpreting the loop body" if world == 1
                else f"rows sharded over {world} ranks, p exchanged after each update, dots reduced on the device")
         self.workload = (f"CG (bundled cg.gmodel resized) {self.matrix}: n={n}, nnz={self.nnz}, {self.iters} "
@@ -1191,6 +1257,8 @@ def run_gpu(args):
                     "kernel_ms": kernel_ms, "algorithmic": wl.algorithmic}
         else:
             peak = peaks.get("hbm_gbs", 6650.0)
+            if getattr(wl, "roof_bytes", None):        # metric is not bytes (CG: GFLOP/s): roofline on bytes
+                achieved = wl.roof_bytes * wl.rank_fraction / (kernel_ms * 1e-3) / 1e9
             roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                     "traffic": profile_traffic(wl.name),
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650",

@@ -247,13 +247,34 @@ __global__ void __launch_bounds__(256) k_tile_copy_affine(const T* __restrict__ 
 // a thread takes 4 consecutive repetitions, reads the 8-element source span as two 16-byte
 // vectors (even elements kept) and writes one 16-byte vector -- half the load instructions
 // of the scalar gather; the DRAM traffic (whole sectors) is the same.
+// U groups per thread per pass (all loads issued before the stores) keep 32*U bytes per thread
+// in flight.
+template <int U>
 __global__ void __launch_bounds__(256) k_gather_stride2(const float* __restrict__ src, float* __restrict__ dst,
                                                         int64_t ngroups) {
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ngroups; g += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (; g + (U - 1) * stride < ngroups; g += U * stride) {
+    float4 a[U], b[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      a[u] = __ldg(reinterpret_cast<const float4*>(src) + 2 * (g + u * stride));
+      b[u] = __ldg(reinterpret_cast<const float4*>(src) + 2 * (g + u * stride) + 1);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      reinterpret_cast<float4*>(dst)[g + u * stride] = make_float4(a[u].x, a[u].z, b[u].x, b[u].z);
+  }
+  for (; g < ngroups; g += stride) {
     const float4 a = __ldg(reinterpret_cast<const float4*>(src) + 2 * g);
     const float4 b = __ldg(reinterpret_cast<const float4*>(src) + 2 * g + 1);
     reinterpret_cast<float4*>(dst)[g] = make_float4(a.x, a.z, b.x, b.z);
   }
+}
+
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
 }
 
 // Affine copy, V consecutive pattern elements per thread (P % V == 0, destination
@@ -1705,7 +1726,8 @@ static int launch_window(const float* src, float* dst, int64_t cs, int64_t As, i
   if (logp < 0 || As <= 0 || As >= P || (uintptr_t)src % 16) return AOL_EUNSUPPORTED;
   // ring geometry (measured, m = 2/4 overlap at T = 1e8/1e9): 32 KB windows, double-buffered,
   // 8 CTAs per SM in the grid (about 3 resident): 6.0-6.1 TB/s; 8 KB x 4 stages gave 5.4-5.7
-  constexpr int win_kb = 32, nst = 2, cps = 8;
+  static const int win_kb = env_int("AOL_WIN_KB", 32), nst = env_int("AOL_WIN_NST", 2),
+                   cps = env_int("AOL_WIN_CPS", 8);
   const int R = (int)std::max<int64_t>(32, std::min<int64_t>(16384, win_kb * 256 / As));
   const uint32_t win_pitch = (uint32_t)(((As * (R - 1) + P + 8) + 31) & ~int64_t(31));
   const int smem = nst * (int)win_pitch * 4;
@@ -2022,7 +2044,11 @@ static int launch_tile_copy_t(const aol_tiler& ts, const aol_tiler& td, int64_t 
     const int64_t room = (tiler_arr_total(ts) - (p.cs + 2 * first)) / 8;
     const int64_t groups = std::min<int64_t>(count / 4, std::max<int64_t>(room, 0));
     if (groups > 0 && (uintptr_t)s0 % 16 == 0 && (uintptr_t)d0 % 16 == 0) {
-      k_gather_stride2<<<grid_for(groups, 1024, 16), 256, 0, stream>>>(s0, d0, groups);
+      static const int s2u = env_int("AOL_S2_U", 1), s2w = env_int("AOL_S2_WAVES", 16);
+      const unsigned g2 = grid_for(groups, 256 * s2u, s2w);
+      if (s2u >= 4) k_gather_stride2<4><<<g2, 256, 0, stream>>>(s0, d0, groups);
+      else if (s2u == 2) k_gather_stride2<2><<<g2, 256, 0, stream>>>(s0, d0, groups);
+      else k_gather_stride2<1><<<grid_for(groups, 1024, s2w), 256, 0, stream>>>(s0, d0, groups);
       AOL_LAUNCH_CHECK("k_gather_stride2");
       first += 4 * groups;                              // the < 4 trailing repetitions below
       count -= 4 * groups;

@@ -50,7 +50,7 @@ def timed(fn, mode, reps=20):
     for i, (a, b) in enumerate(ev):
         scrub.fill_(float(i))
         if mode == "write+read":
-            torch.sum(rd, out=acc)
+            acc.copy_(rd.sum())
         a.record()
         fn()
         b.record()
@@ -67,8 +67,7 @@ for spec in args:
     def run():
         _capi.launch(t["task"], 0, T, t["ptrs"], (), st)
     res = {mode: timed(run, mode) for mode in ("none", "write", "write+read")}
-    nb = t["bytes"] // 8
-    a = torch.empty(nb // 4, device="cuda")
+    a = torch.empty(t["bytes"] // 8, device="cuda")        # copy_ of n floats moves 8n bytes
     b = torch.empty_like(a)
     ref = timed(lambda: b.copy_(a), "write+read")
     line = " ".join(f"{k}={v * 1e3:7.1f}us/{t['bytes'] / v / 1e6:6.0f}GB/s" for k, v in res.items())
