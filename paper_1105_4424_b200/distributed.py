@@ -3,23 +3,24 @@
 The reference simulates D devices in one process: launch d covers
 ``partition_equally(T, D)[d]`` (partition.py:105-121, refexec.py:488) and
 devices share nothing except host-ordered dot reductions (refexec.py:5-7,
-:478-487).  Here device d *is* rank d of a ``torch.distributed`` group:
+:478-487).  Here launch d runs on rank d mod world (``ShardedExecutor``):
 
-  * rank r executes only the KernelLaunch whose ``device_index == r``;
-  * an output array that a later step (or the caller) needs whole is made
-    whole by exchanging each rank's **packed output-pattern stream**: the
-    rank gathers its own patterns in rho order through the output tiler
-    (a ``tile_copy`` into a dense [count, P] buffer), the streams are
-    all-gathered (NCCL over NVLink on GPUs, gloo on CPU), and every rank
-    scatters the other ranks' streams back through the same tiler.  No
-    indices travel, and unequal shard sizes (differing by one repetition)
-    need no padding in the payload;
-  * dot_partial partials are all-gathered and summed in ascending device
-    order, exactly the reference's combine.
+  * ``ShardPlan`` lists, for every written port, exactly the ranges another
+    rank reads before they are rewritten (writer, reader, lo, hi); only those
+    travel, as one grouped batch of exact-size point-to-point transfers
+    (NCCL over NVLink on GPUs, gloo host-staged on CPU);
+  * output tilers that do not write a dense stream fall back to packed
+    output-pattern streams: each rank gathers its patterns in rho order
+    through the output tiler (a ``tile_copy`` into a dense [count, P]
+    buffer), the streams are all-gathered and scattered back through the
+    same tiler -- no indices travel, unequal shards need no padding;
+  * dot_partial partials are reduced on the device and summed in ascending
+    launch order by the partials_sum kernel, exactly the reference's combine;
+  * the caller's outputs are gathered to the root only when asked for.
 
-The pack / unpack / launch primitives are injected, so the same exchange
-logic is exercised on CPU (gloo, world size 2, with the oracle as the
-launcher) in tests/test_distributed.py and on B200 with libaolb200.so.
+The exchange primitives (``gather_output``, ``combine_partials``) take injected
+pack / unpack / launch callables, so the same logic runs on CPU (gloo, world
+size 2, the oracle as the launcher) in tests/test_distributed.py.
 """
 
 from __future__ import annotations
