@@ -1230,7 +1230,7 @@ def run_gpu(args):
     # N > 1: the output ranges gathered to rank 0, timed separately from the concurrent
     # per-rank phase (north_star: "NCCL output gather reported separately")
     gather = None
-    if world > 1 and not args.no_gather:
+    if world > 1 and not args.no_gather and wl.scaling == "strong" and getattr(wl, "ex", None) is not None:
         times, nbytes = [], 0
         for _ in range(3):
             wl.step()

@@ -417,6 +417,9 @@ def _continuations(steps) -> dict:
     return conts
 
 
+ROOT_GATHER = "root-gather"      # ShardPlan marker: a non-dense write no later step reads
+
+
 class ShardPlan:
     """Static exchange plan of a schedule whose launch d runs on rank d mod ``world``.
 
@@ -427,7 +430,9 @@ class ShardPlan:
     can follow the step (:func:`_continuations`; loop bodies wrap), stopping at the first
     later step that rewrites the same ranges on the same ranks (CG's ``scale_p`` is followed
     by ``axpy_p`` on the same shards, so only ``axpy_p``'s p travels to the spmv).
-    Non-dense output tilers fall back to the packed-pattern all-gather (``None``).  Host
+    Non-dense output tilers fall back to the packed-pattern all-gather (``None``) when a later
+    step reads the group, and to a packed gather to the root at output time (``ROOT_GATHER``)
+    when none does.  Host
     scalar ops read on every rank; dot_partial results are combined by the partial
     reduction, not exchanged.  Nothing is exchanged for the caller's outputs until
     :meth:`ShardedExecutor.outputs` gathers them to the root (NCCL only
@@ -500,7 +505,10 @@ class ShardPlan:
             entries = []
             for g, (name, dense, ranges) in writes[id(step)].items():
                 if not dense:
-                    entries.append((name, g, None, []))
+                    # packed-pattern exchange only if some later step reads the group at all;
+                    # otherwise (a root output) the patterns go to the root when it gathers
+                    read_later = any(reads[id(nxt)].get(g) for seq in conts[id(step)] for nxt in seq)
+                    entries.append((name, g, None if read_later else ROOT_GATHER, []))
                     continue
                 need = [[] for _ in range(world)]
                 for seq in conts[id(step)]:
@@ -532,7 +540,7 @@ class ShardPlan:
         """Bytes the dense transfers of one step move (for tests / reports)."""
         tot = 0
         for name, g, tr, _ in self.writes.get(task_path, []):
-            if tr:
+            if tr and tr != ROOT_GATHER:
                 tot += sum(hi - lo for _, _, lo, hi in tr) * esize.get(g, 4)
         return tot
 
@@ -608,6 +616,28 @@ class DistTransport:
             return [s_.to(dev) if isinstance(s_, torch.Tensor) else s_ for s_ in streams]
         return Exchange(self.group).all_gather_v(local, counts)
 
+    def gather_v(self, replicas: dict, local, counts: list[int], root: int) -> dict:
+        """Variable-size streams to ``root`` only (one grouped batch of send/recv): the root
+        gets {rank: stream} for every other rank with a non-empty stream, the others {}."""
+        import torch
+        dist, me = self.dist, self.rank
+        ops, out = [], {}
+        if me == root:
+            for r in range(self.world):
+                if r == root or counts[r] == 0:
+                    continue
+                buf = torch.empty(counts[r], dtype=local.dtype, device="cpu" if self.staged else local.device)
+                out[r] = buf
+                ops.append(dist.P2POp(dist.irecv, buf, self._peer(r), self.group))
+        elif counts[me]:
+            ops.append(dist.P2POp(dist.isend, local.cpu() if self.staged else local, self._peer(root), self.group))
+            self.bytes_moved += local.numel() * local.element_size()
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        dev = replicas[me].device
+        return {r: b.to(dev) for r, b in out.items()}
+
     def barrier(self):
         self.dist.barrier(group=self.group)
 
@@ -663,6 +693,7 @@ class ShardedExecutor:
         self.root = 0
         self.plan = ShardPlan(self, world)
         self.stale: dict = {}          # group -> [(lo, hi, owner)] ranges the root holds stale
+        self.pending_pack: dict = {}   # group -> (step, task, port): non-dense write the root lacks
         self.exchanged_bytes = 0
         self._upload_hulls()
 
@@ -760,8 +791,15 @@ class ShardedExecutor:
 
     def _after_write(self, step, t) -> None:
         for name, g, tr, wr in self.plan.writes.get(step.task_path, []):
+            if g in self.pending_pack:
+                # an older packed write of this group must reach the root before this one
+                # lands, so the root sees the writes in program order
+                self._pack_to_root(*self.pending_pack.pop(g))
             if tr is None:
                 self._pack_exchange(step, t, name)
+                continue
+            if tr == ROOT_GATHER:
+                self.pending_pack[g] = (step, t, name)
                 continue
             if tr:
                 self.transport.move(self.replicas, g, tr)
@@ -811,6 +849,47 @@ class ShardedExecutor:
                     cuda_unpack(arr, bt, l.range.offset, l.range.count, streams[r][pos:pos + k])
                     pos += k
 
+    def _pack_to_root(self, step, t, name) -> int:
+        """Non-dense output written by the ranks' launches: each rank other than the root packs
+        its patterns in rho order through the output tiler, the streams travel to the root only,
+        and the root scatters them back through the same tiler.  Returns bytes moved."""
+        import torch
+        bt = _port_tiler(self, t, name)
+        P = bt.pattern_total
+        by_rank = {r: self._mine(step, r) for r in range(self.world)}
+        moved = 0
+        if isinstance(self.transport, LocalTransport):
+            root = self.replicas[self.root]
+            dst = root.storage.array(t.nodes[name])
+            for w in range(self.world):
+                if w == self.root or not by_rank[w]:
+                    continue
+                src = self.replicas[w].storage.array(t.nodes[name])
+                for l in by_rank[w]:
+                    with torch.cuda.device(self.replicas[w].device):
+                        packed = cuda_pack(src, bt, l.range.offset, l.range.count)
+                    with torch.cuda.device(root.device):
+                        cuda_unpack(dst, bt, l.range.offset, l.range.count, packed.to(root.device))
+                    moved += packed.numel() * packed.element_size()
+            return moved
+        counts = [sum(l.range.count for l in by_rank[r]) * P for r in range(self.world)]
+        rep = self.replicas[self.transport.rank]
+        arr = rep.storage.array(t.nodes[name])
+        with torch.cuda.device(rep.device):
+            if rep.rank != self.root and by_rank[rep.rank]:
+                local = torch.cat([cuda_pack(arr, bt, l.range.offset, l.range.count) for l in by_rank[rep.rank]])
+            else:
+                local = torch.zeros(0, dtype=arr.dtype, device=rep.device)
+            streams = self.transport.gather_v(self.replicas, local, counts, self.root)
+            for r, stream in streams.items():
+                pos = 0
+                for l in by_rank[r]:
+                    k = l.range.count * P
+                    cuda_unpack(arr, bt, l.range.offset, l.range.count, stream[pos:pos + k])
+                    pos += k
+                moved += stream.numel() * stream.element_size()
+        return moved
+
     def _run_fused(self, s1, s2) -> bool:
         from . import _capi
         t1, t2 = self.task(s1.task_path), self.task(s2.task_path)
@@ -845,6 +924,12 @@ class ShardedExecutor:
                 moved += sum(hi - lo for _, _, lo, hi in tr) * self.replicas[next(iter(self.replicas))] \
                     .storage.arrays[g].element_size()
             self.stale[g] = []
+        outs = {self.storage.groups[p.name] for p in root.ports
+                if getattr(p.direction, "value", p.direction) == "out"}
+        for g in list(self.pending_pack):
+            pend = self.pending_pack.pop(g)
+            if g in outs:                   # groups nobody reads and the caller never sees stay put
+                moved += self._pack_to_root(*pend)
         return moved
 
     def outputs(self, on_device: bool = False, out: dict | None = None) -> dict:

@@ -138,3 +138,28 @@ def test_dist_transport_world2_gloo():
         assert p.exitcode == 0
     assert res[0][0] and res[1][0]
     assert res[0][1] == 20 * 4 and res[1][1] == 15 * 4      # each rank counts the bytes it sent
+
+
+@pytest.mark.parametrize("D", [2, 3])
+def test_downscaler_root_output_is_gathered_not_exchanged(D):
+    """The V filter writes 4 rows per repetition (not a dense stream) and nothing reads it
+    after: it is packed to the root at output time only (ROOT_GATHER), never all-gathered.
+    At D=2 the H and V shards cover the same frames, so the intermediate does not travel; at
+    D=3 the V shards straddle H shards and only the rows they read cross."""
+    from paper_1105_4424_b200.distributed import ROOT_GATHER
+    plan, sched = _plan("downscaler", D)
+    (h,) = plan.writes["h"]
+    (v,) = plan.writes["v"]
+    if D == 2:
+        assert h[2] == []
+    else:
+        assert h[2] and all(w != r for w, r, _, _ in h[2])
+    assert v[2] == ROOT_GATHER
+    assert plan.exchanged_bytes("v", {}) == 0
+
+
+def test_transpose_chain_pack_is_kept_when_read_later():
+    """A non-dense write that a later step reads still takes the packed all-gather."""
+    from paper_1105_4424_b200.distributed import ROOT_GATHER
+    plan, _ = _plan("transpose_chain", 3)
+    assert plan.writes["t"][0][2] is None and plan.writes["t"][0][2] != ROOT_GATHER
