@@ -1159,7 +1159,12 @@ def run_gpu(args):
     _capi.load()
     all_cpus = os.sched_getaffinity(0)
     numa = bind_host_to_gpu_numa(torch, local)
+    t_start = time.perf_counter()
+
+    def phase(name):
+        log(f"[bench rank {rank}/{world}] {name} at {time.perf_counter() - t_start:.1f} s")
     wl = WORKLOADS[args.workload](torch, device, rank, world)
+    phase("workload prepared")
     stream = torch.cuda.current_stream(device)
 
     _pp = torch.cuda.get_device_properties(device)
@@ -1175,6 +1180,7 @@ def run_gpu(args):
 
         def flush():
             scrub.fill_(1.0)
+    phase("warm")
     clocks.start()
     total_ms, per = time_steps(torch, wl.step, args.steps, 0, stream, barrier, flush)
     clk = clocks.stop()
@@ -1201,6 +1207,7 @@ def run_gpu(args):
     # end to end through the public API (H2D + launch + D2H every step)
     e2e = None
     e2e_np = None
+    phase("timed region done")
     if not args.no_e2e:
         el = timed_e2e(wl.e2e_step, wl.e2e_setup, args.e2e_steps)
         h2d = wl.e2e_bytes[0] * (world if wl.scaling == "weak" else 1)
@@ -1225,6 +1232,7 @@ def run_gpu(args):
                       "path": "execute_schedule(model, schedule, {port: numpy array}, D) -> numpy outputs: the "
                               "reference's call (refexec.py:427), pageable host memory both ways"}
         wl.e2e_free()
+        phase("e2e done")
     os.sched_setaffinity(0, all_cpus)            # the CPU baseline gets every host core again
 
     # N > 1: the output ranges gathered to rank 0, timed separately from the concurrent
@@ -1241,9 +1249,10 @@ def run_gpu(args):
             torch.cuda.synchronize()
             times.append(time.perf_counter() - t0)
             nbytes = moved or 0
-        if nbytes:
-            g = allmax(min(times))
-            nb = int(allsum(float(nbytes)))
+        # collectives on every rank (a rank that moved nothing still takes part)
+        g = allmax(min(times))
+        nb = int(allmax(float(nbytes)))
+        if nb:
             gather = {"ms": g * 1e3, "bytes_to_root": nb, "GBps": nb / g / 1e9, "backend": backend,
                       "op": "ShardedExecutor.gather_to_root: each rank's written output ranges to rank 0 "
                             "(batched send/recv of exact ranges)"}
@@ -1277,6 +1286,7 @@ def run_gpu(args):
                     "traffic": profile_traffic(wl.name),
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650",
                     "kernel_ms": kernel_ms, "algorithmic": wl.algorithmic}
+        phase("gather done")
         cpu = None if (args.no_cpu or world > 1) else wl.cpu_sample(args.cpu_seconds)
         extra = {}
         if hasattr(wl, "fp32_faithful") and world == 1 and not args.no_peak:

@@ -792,9 +792,12 @@ class ShardedExecutor:
     def _after_write(self, step, t) -> None:
         for name, g, tr, wr in self.plan.writes.get(step.task_path, []):
             if g in self.pending_pack:
-                # an older packed write of this group must reach the root before this one
-                # lands, so the root sees the writes in program order
-                self._pack_to_root(*self.pending_pack.pop(g))
+                # an older packed write of this group by ANOTHER step must reach the root before
+                # this one lands (program order); the same step again (the next run(), a loop
+                # iteration) rewrites exactly the same elements, so its older pack is dropped
+                old = self.pending_pack.pop(g)
+                if old[0] is not step:
+                    self._pack_to_root(*old)
             if tr is None:
                 self._pack_exchange(step, t, name)
                 continue
@@ -887,8 +890,8 @@ class ShardedExecutor:
                     k = l.range.count * P
                     cuda_unpack(arr, bt, l.range.offset, l.range.count, stream[pos:pos + k])
                     pos += k
-                moved += stream.numel() * stream.element_size()
-        return moved
+        # every rank reports the same total (like move()), so callers may reduce over it
+        return sum(c for r, c in enumerate(counts) if r != self.root) * arr.element_size()
 
     def _run_fused(self, s1, s2) -> bool:
         from . import _capi
