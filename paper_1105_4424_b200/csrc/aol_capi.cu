@@ -44,6 +44,7 @@ int launch_fused_line_filters(const aol_task& th, const aol_task& tv, int64_t fi
 int launch_gemm_tf32(const aol_task& t, int64_t first, int64_t count, void* const* ports, cudaStream_t s);
 int release_dot_scratch();
 int release_loop_scratch();
+int release_gemm_scratch();
 
 static int tilers_needed(int op) {
   switch (op) {
@@ -174,6 +175,7 @@ int64_t aol_launch_counter(void) { return g_launches.load(); }
 int aol_release_scratch(void) {
   release_dot_scratch();
   release_loop_scratch();
+  release_gemm_scratch();
   return AOL_OK;
 }
 

@@ -18,6 +18,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
+#include <map>
 #include <mutex>
 
 #include "aol_async.cuh"
@@ -48,6 +49,14 @@ struct Params {
   int epi_smem;        // pair kernel: stage 32x32 chunks through shared memory for row-contiguous stores
   int chunk_kb;        // 3xtf32: k-blocks accumulated in TMEM between round-to-nearest adds
   int hi_round;        // 3xtf32: 1 = hi rounded to tf32 (rna) and written back; 0 = hi = tensor-core truncation
+  // pair kernel, split-K tail: tiles [0, dp_tiles) run whole, one per pair per wave; each of the
+  // sk_tiles tail tiles is cut into sk_split k-ranges, and the pieces (k-range major, so the
+  // pieces running together read the same k-slices) are dealt to the pairs like tiles.  A
+  // tile's partial accumulators are summed in k order by whichever piece arrives last.
+  int dp_tiles;
+  int sk_tiles, sk_split;
+  float* sk_ws;        // [piece][2 CTAs][4 warps][8 chunks][8 col quads][32 lanes][4] fp32 partials
+  unsigned* sk_cnt;    // [sk tiles][2 CTAs][4 warps] arrival counters (reset by the last arriver)
 };
 
 // ------------------------------------------------------------ PTX helpers ----
@@ -340,6 +349,93 @@ __device__ __forceinline__ void tile_coords_pair(const Params& p, int tile, int&
   nt = in / gm;
 }
 
+// One unit of a pair's work: k-blocks [kb0, kb1) of output tile `tile`; `piece` >= 0 for a
+// split-K piece of a tail tile (its partial accumulator goes through sk_ws).
+struct Unit {
+  int tile, kb0, kb1, piece;
+};
+
+// Pair `pid` of `np`: whole tiles pid, pid + np, ... below dp_tiles, then tail pieces
+// pid, pid + np, ... below sk_tiles * sk_split; piece j is k-range j / sk_tiles of tail tile
+// j % sk_tiles.  Every role of the pair (producer, MMA issuer, epilogue) walks the same sequence.
+struct UnitIter {
+  const Params& p;
+  int np, next_tile, next_piece;
+  __device__ UnitIter(const Params& p_, int pid, int np_) : p(p_), np(np_), next_tile(pid), next_piece(pid) {}
+  __device__ bool next(Unit& u) {
+    if (next_tile < p.dp_tiles) {
+      u.tile = next_tile;
+      u.kb0 = 0;
+      u.kb1 = p.k_blocks;
+      u.piece = -1;
+      next_tile += np;
+      return true;
+    }
+    if (next_piece >= p.sk_tiles * p.sk_split) return false;
+    const int kq = next_piece / p.sk_tiles;
+    u.tile = p.dp_tiles + (next_piece - kq * p.sk_tiles);
+    u.kb0 = (int)((int64_t)p.k_blocks * kq / p.sk_split);
+    u.kb1 = (int)((int64_t)p.k_blocks * (kq + 1) / p.sk_split);
+    u.piece = next_piece;
+    next_piece += np;
+    return true;
+  }
+};
+
+__device__ __forceinline__ float* sk_slot(const Params& p, int piece, uint32_t rank, int ew) {
+  return p.sk_ws + (((int64_t)piece * 2 + rank) * 4 + ew) * (int64_t)(8 * 32 * 32);
+}
+
+// Masked store of one 32x32 fp32 chunk (rows = the warp's 32 TMEM lanes, columns c0..c0+31)
+// into C, staged through padded shared memory so each 16-byte store covers 4 rows x 128 B.
+__device__ __forceinline__ void store_chunk(const Params& p, float* epi, int ew, int lane, int mt, int nt,
+                                            uint32_t rank, int ch, const float (&v)[32]) {
+  const int64_t c0 = (int64_t)nt * BN + ch * 32;
+  if (p.epi_smem) {
+    float* st = epi + ew * 32 * EPI_PITCH;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) st[lane * EPI_PITCH + j] = v[j];
+    __syncwarp();
+    const int64_t row0 = p.m_lo + (int64_t)mt * BM + rank * HALF_M + ew * 32;
+#pragma unroll
+    for (int rr = 0; rr < 32; rr += 4) {
+      const int r = rr + (lane >> 3), cc = 4 * (lane & 7);
+      const int64_t g = row0 + r;
+      const float* sp = st + r * EPI_PITCH + cc;
+      if (g > p.m_hi || g >= p.M) continue;
+      int64_t lo = 0, hi = p.N;
+      if (g == p.m_lo) lo = p.first - p.m_lo * p.N;
+      if (g == p.m_hi) hi = p.last - p.m_hi * p.N + 1;
+      float* dst = p.c + g * p.ldc + c0 + cc;
+      const int64_t col = c0 + cc;
+      if (p.c_vec && col >= lo && col + 4 <= hi) {
+        *reinterpret_cast<float4*>(dst) = make_float4(sp[0], sp[1], sp[2], sp[3]);
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (col + u >= lo && col + u < hi) dst[u] = sp[u];
+      }
+    }
+    __syncwarp();
+    return;
+  }
+  const int64_t gm = p.m_lo + (int64_t)mt * BM + rank * HALF_M + ew * 32 + lane;
+  if (!(gm <= p.m_hi && gm < p.M)) return;
+  int64_t col_lo = 0, col_hi = p.N;
+  if (gm == p.m_lo) col_lo = p.first - p.m_lo * p.N;
+  if (gm == p.m_hi) col_hi = p.last - p.m_hi * p.N + 1;
+  float* crow = p.c + gm * p.ldc;
+  if (p.c_vec && c0 >= col_lo && c0 + 32 <= col_hi) {
+#pragma unroll
+    for (int j = 0; j < 32; j += 4)
+      *reinterpret_cast<float4*>(crow + c0 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (c0 + j >= col_lo && c0 + j < col_hi) crow[c0 + j] = v[j];
+  }
+}
+
 template <bool A_KMAJOR, bool B_KMAJOR>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_gemm_tf32_pair(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, Params p) {
@@ -384,12 +480,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // ------------------------------------------------- TMA producer (both CTAs) ----
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = pair_id; tile < p.num_tiles; tile += num_pairs) {
+      UnitIter units(p, pair_id, num_pairs);
+      Unit u;
+      while (units.next(u)) {
         int mt, nt;
-        tile_coords_pair(p, tile, mt, nt);
+        tile_coords_pair(p, u.tile, mt, nt);
         const int row0 = (int)(p.m_lo + (int64_t)mt * BM) + (int)rank * HALF_M;
         const int col0 = nt * BN + (int)rank * HALF_N;
-        for (int kb = 0; kb < p.k_blocks; ++kb) {
+        for (int kb = u.kb0; kb < u.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
           uint8_t* sb = sa + A_BYTES;
@@ -411,11 +509,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = pair_id; tile < p.num_tiles; tile += num_pairs) {
+      UnitIter units(p, pair_id, num_pairs);
+      Unit u;
+      while (units.next(u)) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < p.k_blocks; ++kb) {
+        for (int kb = u.kb0; kb < u.kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
@@ -423,7 +523,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int k = 0; k < BK / UMMA_K; ++k)
             mma_tf32_pair(d_tmem, operand_desc<A_KMAJOR>(sa, k), operand_desc<B_KMAJOR>(sb, k), idesc,
-                          (kb | k) != 0);
+                          (kb != u.kb0 || k != 0) ? 1u : 0u);
           commit_pair_multicast(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -436,67 +536,96 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int ew = warp - 4;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = pair_id; tile < p.num_tiles; tile += num_pairs) {
+    UnitIter units(p, pair_id, num_pairs);
+    Unit u;
+    while (units.next(u)) {
       int mt, nt;
-      tile_coords_pair(p, tile, mt, nt);
+      tile_coords_pair(p, u.tile, mt, nt);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int64_t gm = p.m_lo + (int64_t)mt * BM + rank * HALF_M + ew * 32 + lane;
-      const bool row_ok = gm <= p.m_hi && gm < p.M;
-      int64_t col_lo = 0, col_hi = p.N;
-      if (gm == p.m_lo) col_lo = p.first - p.m_lo * p.N;
-      if (gm == p.m_hi) col_hi = p.last - p.m_hi * p.N + 1;
-      float* crow = p.c + gm * p.ldc;
+      const uint32_t tbase = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
+      if (u.piece < 0) {
 #pragma unroll 1
-      for (int ch = 0; ch < BN / 32; ++ch) {
-        uint32_t v[32];
-        tmem_ld32(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + ch * 32, v);
-        const int64_t c0 = (int64_t)nt * BN + ch * 32;
-        if (p.epi_smem) {
-          // lane = row in TMEM; transpose the 32x32 chunk through padded shared memory so each
-          // 16-byte store instruction covers 4 rows x 128 contiguous bytes instead of 32 rows x 16 B
-          float* st = epi + ew * 32 * EPI_PITCH;
+        for (int ch = 0; ch < BN / 32; ++ch) {
+          uint32_t r[32];
+          tmem_ld32(tbase + ch * 32, r);
+          float v[32];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) st[lane * EPI_PITCH + j] = __uint_as_float(v[j]);
-          __syncwarp();
-          const int64_t row0 = p.m_lo + (int64_t)mt * BM + rank * HALF_M + ew * 32;
-#pragma unroll
-          for (int rr = 0; rr < 32; rr += 4) {
-            const int r = rr + (lane >> 3), cc = 4 * (lane & 7);
-            const int64_t g = row0 + r;
-            const float* sp = st + r * EPI_PITCH + cc;
-            if (g > p.m_hi || g >= p.M) continue;
-            int64_t lo = 0, hi = p.N;
-            if (g == p.m_lo) lo = p.first - p.m_lo * p.N;
-            if (g == p.m_hi) hi = p.last - p.m_hi * p.N + 1;
-            float* dst = p.c + g * p.ldc + c0 + cc;
-            const int64_t col = c0 + cc;
-            if (p.c_vec && col >= lo && col + 4 <= hi) {
-              *reinterpret_cast<float4*>(dst) = make_float4(sp[0], sp[1], sp[2], sp[3]);
-            } else {
-#pragma unroll
-              for (int u = 0; u < 4; ++u)
-                if (col + u >= lo && col + u < hi) dst[u] = sp[u];
-            }
-          }
-          __syncwarp();
-          continue;
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+          store_chunk(p, epi, ew, lane, mt, nt, rank, ch, v);
         }
-        if (!row_ok) continue;
-        if (p.c_vec && c0 >= col_lo && c0 + 32 <= col_hi) {
+        tc_fence_before();
+        arrive_leader(&tempty[acc]);
+      } else {
+        // split-K piece: park the partial accumulator (coalesced [chunk][col][lane]), free the
+        // TMEM buffer, then count arrivals; the last piece sums all of them in k order
+        float* mine = sk_slot(p, u.piece, rank, ew);
+#pragma unroll 1
+        for (int ch = 0; ch < BN / 32; ++ch) {
+          uint32_t r[32];
+          tmem_ld32(tbase + ch * 32, r);
+          float4* dst = reinterpret_cast<float4*>(mine) + ch * 8 * 32 + lane;
 #pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            *reinterpret_cast<float4*>(crow + c0 + j) =
-                make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]),
-                            __uint_as_float(v[j + 3]));
-        } else {
+          for (int j4 = 0; j4 < 8; ++j4)
+            __stcg(dst + j4 * 32, make_float4(__uint_as_float(r[4 * j4]), __uint_as_float(r[4 * j4 + 1]),
+                                              __uint_as_float(r[4 * j4 + 2]), __uint_as_float(r[4 * j4 + 3])));
+        }
+        tc_fence_before();
+        arrive_leader(&tempty[acc]);
+        const int t_sk = u.tile - p.dp_tiles;
+        unsigned* cnt = p.sk_cnt + ((int64_t)t_sk * 2 + rank) * 4 + ew;
+        __threadfence();
+        __syncwarp();
+        unsigned prev = 0;
+        if (lane == 0) prev = atomicAdd(cnt, 1u);
+        prev = __shfl_sync(0xffffffffu, prev, 0);
+        if (prev == (unsigned)(p.sk_split - 1)) {
+          __threadfence();
+#pragma unroll 1
+          for (int ch = 0; ch < BN / 32; ++ch) {
+            // partials in k order; two pieces' loads in flight per round (16 x 16 B per lane)
+            float v[32];
+            const float4* s0 = reinterpret_cast<const float4*>(sk_slot(p, t_sk, rank, ew)) + ch * 8 * 32 + lane;
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (c0 + j >= col_lo && c0 + j < col_hi) crow[c0 + j] = __uint_as_float(v[j]);
+            for (int j4 = 0; j4 < 8; ++j4) {
+              const float4 a = __ldcg(s0 + j4 * 32);
+              v[4 * j4] = a.x; v[4 * j4 + 1] = a.y; v[4 * j4 + 2] = a.z; v[4 * j4 + 3] = a.w;
+            }
+            int kq = 1;
+            for (; kq + 1 < p.sk_split; kq += 2) {
+              const float4* s1 = reinterpret_cast<const float4*>(sk_slot(p, kq * p.sk_tiles + t_sk, rank, ew)) +
+                                 ch * 8 * 32 + lane;
+              const float4* s2 = reinterpret_cast<const float4*>(
+                                     sk_slot(p, (kq + 1) * p.sk_tiles + t_sk, rank, ew)) + ch * 8 * 32 + lane;
+              float4 b1[8], b2[8];
+#pragma unroll
+              for (int j4 = 0; j4 < 8; ++j4) {
+                b1[j4] = __ldcg(s1 + j4 * 32);
+                b2[j4] = __ldcg(s2 + j4 * 32);
+              }
+#pragma unroll
+              for (int j4 = 0; j4 < 8; ++j4) {
+                v[4 * j4] += b1[j4].x; v[4 * j4 + 1] += b1[j4].y; v[4 * j4 + 2] += b1[j4].z; v[4 * j4 + 3] += b1[j4].w;
+              }
+#pragma unroll
+              for (int j4 = 0; j4 < 8; ++j4) {
+                v[4 * j4] += b2[j4].x; v[4 * j4 + 1] += b2[j4].y; v[4 * j4 + 2] += b2[j4].z; v[4 * j4 + 3] += b2[j4].w;
+              }
+            }
+            if (kq < p.sk_split) {
+              const float4* s1 = reinterpret_cast<const float4*>(sk_slot(p, kq * p.sk_tiles + t_sk, rank, ew)) +
+                                 ch * 8 * 32 + lane;
+#pragma unroll
+              for (int j4 = 0; j4 < 8; ++j4) {
+                const float4 b = __ldcg(s1 + j4 * 32);
+                v[4 * j4] += b.x; v[4 * j4 + 1] += b.y; v[4 * j4 + 2] += b.z; v[4 * j4 + 3] += b.w;
+              }
+            }
+            store_chunk(p, epi, ew, lane, mt, nt, rank, ch, v);
+          }
+          if (lane == 0) *cnt = 0u;             // ready for the next launch on this scratch
         }
       }
-      tc_fence_before();
-      arrive_leader(&tempty[acc]);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   }
@@ -1096,6 +1225,105 @@ static int gemm_core(const float* A, const float* B, float* C, const GemmShape& 
 static int gemm_core_3x(const float* A, const float* B, float* C, const GemmShape& g, int64_t first, int64_t count,
                         cudaStream_t stream);
 
+// Split-K tail scratch per (device, stream): the partial accumulators of the tail pieces and
+// the arrival counters of the tail tiles.  Launches on one stream are ordered, launches on
+// different streams never share it.  The counters are zeroed once and reset by each tail
+// tile's last piece; the partial buffer grows to the largest tail seen.  Bounded like the dot
+// scratch; aol_release_scratch() frees it.
+struct GemmScratch {
+  float* ws = nullptr;
+  size_t ws_bytes = 0;
+  unsigned* cnt = nullptr;
+  uint64_t used = 0;
+};
+constexpr size_t kMaxGemmScratch = 16;
+constexpr int kSkMaxTiles = 1024;
+constexpr size_t kSkPieceBytes = (size_t)2 * 4 * 8 * 32 * 32 * sizeof(float);   // 256 KB per piece
+static std::mutex g_gemm_mu;
+static std::map<std::pair<int, cudaStream_t>, GemmScratch> g_gemm_scratch;
+static uint64_t g_gemm_tick = 0;
+
+static void free_gemm_entry(int dev, GemmScratch& e) {
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(dev);
+  cudaDeviceSynchronize();                        // no kernel still uses it
+  cudaFree(e.ws);
+  cudaFree(e.cnt);
+  cudaSetDevice(cur);
+}
+
+static bool gemm_scratch(int dev, cudaStream_t stream, int pieces, float** ws, unsigned** cnt) {
+  std::lock_guard<std::mutex> lock(g_gemm_mu);
+  auto it = g_gemm_scratch.find({dev, stream});
+  if (it == g_gemm_scratch.end()) {
+    if (g_gemm_scratch.size() >= kMaxGemmScratch) {
+      auto victim = g_gemm_scratch.begin();
+      for (auto v = g_gemm_scratch.begin(); v != g_gemm_scratch.end(); ++v)
+        if (v->second.used < victim->second.used) victim = v;
+      free_gemm_entry(victim->first.first, victim->second);
+      g_gemm_scratch.erase(victim);
+    }
+    GemmScratch e;
+    const size_t cnt_bytes = (size_t)kSkMaxTiles * 2 * 4 * sizeof(unsigned);
+    if (cudaMalloc(&e.cnt, cnt_bytes) != cudaSuccess) return false;
+    if (cudaMemset(e.cnt, 0, cnt_bytes) != cudaSuccess) {
+      cudaFree(e.cnt);
+      return false;
+    }
+    it = g_gemm_scratch.emplace(std::make_pair(dev, stream), e).first;
+  }
+  GemmScratch& e = it->second;
+  const size_t need = (size_t)pieces * kSkPieceBytes;
+  if (e.ws_bytes < need) {
+    if (e.ws) {
+      cudaStreamSynchronize(stream);              // the previous launch on this stream is done with it
+      cudaFree(e.ws);
+      e.ws = nullptr;
+      e.ws_bytes = 0;
+    }
+    if (cudaMalloc(&e.ws, need) != cudaSuccess) return false;
+    e.ws_bytes = need;
+  }
+  e.used = ++g_gemm_tick;
+  *ws = e.ws;
+  *cnt = e.cnt;
+  return true;
+}
+
+int release_gemm_scratch() {
+  std::lock_guard<std::mutex> lock(g_gemm_mu);
+  for (auto& kv : g_gemm_scratch) free_gemm_entry(kv.first.first, kv.second);
+  g_gemm_scratch.clear();
+  return 0;
+}
+
+// Split-K tail of the pair kernel.  Whole waves of tiles run data-parallel.  A last partial
+// wave of R = tiles % pairs tiles that would leave pairs idle is cut into s k-ranges (pieces
+// of >= 32 k-blocks) when that shortens it: ceil(R s / pairs) / s waves instead of 1, by at
+// least 10% of a wave (R = 34 of 74, the 4-rank C2 shard: s = 2, 0.5 waves).  Returns s
+// (1 = no split).
+static int split_k_tail(int num_tiles, int k_blocks, int pairs) {
+  const char* env = getenv("AOL_GEMM_STREAMK");       // read per launch (A/B probes toggle it)
+  if (env && env[0] == '0') return 1;
+  const int rem = num_tiles % pairs;
+  if (rem == 0 || rem > kSkMaxTiles) return 1;
+  int best = 1;
+  double best_t = 1.0;
+  // s <= 3: with 4+ pieces per tile the pieces' epilogues (partial stores, the k-ordered sum)
+  // outweigh the shorter tail (measured, tools/time_streamk.py: 0.999x at the 8-rank shard with
+  // s = 4, 0.92x at 8192 rows with s = 8; s = 2 at the 4-rank shard: 1.135x)
+  for (int sp : {2, 3}) {
+    if (k_blocks / sp < 32) break;
+    const double t = (double)((rem * sp + pairs - 1) / pairs) / sp;
+    if (t < best_t - 1e-9) {
+      best_t = t;
+      best = sp;
+    }
+  }
+  return best_t <= 0.9 ? best : 1;
+}
+
 int launch_gemm_tf32(const aol_task& t, int64_t first, int64_t count, void* const* ports, cudaStream_t stream) {
   GemmShape g = recognise_gemm(t);
   if (!g.ok) return fail(AOL_EUNSUPPORTED, "matmul tilers are not a TMA-compatible GEMM");
@@ -1186,7 +1414,25 @@ static int gemm_core(const float* A, const float* B, float* C, const GemmShape& 
     int sms2 = kNumSMs;
     int dev2 = 0;
     if (cudaGetDevice(&dev2) == cudaSuccess) cudaDeviceGetAttribute(&sms2, cudaDevAttrMultiProcessorCount, dev2);
-    const int pairs = pp.num_tiles < sms2 / 2 ? pp.num_tiles : sms2 / 2;
+    int pairs = pp.num_tiles < sms2 / 2 ? pp.num_tiles : sms2 / 2;
+    pp.dp_tiles = pp.num_tiles;
+    pp.sk_tiles = 0;
+    pp.sk_split = 1;
+    {
+      const int all = sms2 / 2;
+      const int sp = split_k_tail(pp.num_tiles, pp.k_blocks, all);
+      const int rem = pp.num_tiles % all;
+      float* ws = nullptr;
+      unsigned* cnt = nullptr;
+      if (sp > 1 && gemm_scratch(dev2, stream, rem * sp, &ws, &cnt)) {
+        pp.dp_tiles = pp.num_tiles - rem;
+        pp.sk_tiles = rem;
+        pp.sk_split = sp;
+        pp.sk_ws = ws;
+        pp.sk_cnt = cnt;
+        pairs = all;                                   // the pieces spread over every pair
+      }
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * pairs);
     cfg.blockDim = dim3(NUM_THREADS);

@@ -250,3 +250,35 @@ def test_memory_role_selects_the_kernel_staging():
                 assert ex.storage.arrays[g].data_ptr() == arena.data_ptr() + pl.b200_offset
         assert "line_tiled" in ex.placement_report() or mem == "dev.gmem"
     assert plans == {"dev.gmem": "tile_filter.batched", "dev.cu.lmem": "tile_filter.line_tiled"}
+
+
+# -- stream-K tail of the TF32 pair kernel -----------------------------------------------------
+
+@pytest.mark.parametrize("M,N,K,devices,a_mn,b_k", [
+    (1024, 8192, 8192, 1, False, False),   # C2's 8-rank shard: 128 tiles = 1 wave + 54 (no split)
+    (2048, 8192, 8192, 1, False, False),   # C2's 4-rank shard: 256 tiles = 3 waves + 34 tail tiles, s = 2
+    (2048, 8192, 2048, 1, False, True),    # the same tail, 64 k-blocks: pieces of 32
+    (768, 10496, 3072, 1, True, False),    # 123 tiles = 1 wave + 49 tail tiles, s = 3
+    (256, 256, 4096, 1, True, False),      # one tile (s = 2: two pieces of 64 k-blocks)
+    (300, 520, 200, 3, False, False),      # ragged shards, few k-blocks
+    (777, 1000, 1500, 7, True, True),
+    (2304, 2560, 768, 2, False, False)])   # 2 shards of 1152 rows: 50 tiles each
+def test_matmul_stream_k_tail(M, N, K, devices, a_mn, b_k):
+    """Tiles of the last partial wave are cut into s k-ranges dealt to every pair and summed in
+    k order by the last piece to arrive: inside the stated TF32 bound, and bit-identical from
+    run to run (fixed summation order, counters reset by the last arriver)."""
+    from paper_1105_4424_b200 import builders
+    from paper_1105_4424_b200.executor import execute_schedule
+    from paper_1105_4424_b200.partition import build_schedule
+    t, ports, bind, A, B = _gemm_case(M, N, K, a_mn, b_k, M + N + K)
+    model = builders.tile_task_model("matmul", ports, {k: _tiler(v) for k, v in t.items()}, (M, N))
+    sched = build_schedule(model, devices)
+    c1 = execute_schedule(model, sched, bind, devices).outputs["p_c"].reshape(M, N)
+    c2 = execute_schedule(model, sched, bind, devices).outputs["p_c"].reshape(M, N)
+    assert np.array_equal(c1.view(np.uint32), c2.view(np.uint32))
+    a64, b64 = A.astype(np.float64), B.astype(np.float64)
+    if M * N * K > 2 ** 34:                  # check 64 sampled rows of the big case
+        rows = np.random.default_rng(1).choice(M, 64, replace=False)
+        a64, c1 = a64[rows], c1[rows]
+    bound = (2.0 ** -9 + K * 2.0 ** -23) * (np.abs(a64) @ np.abs(b64))
+    assert np.all(np.abs(c1 - a64 @ b64) <= bound)
