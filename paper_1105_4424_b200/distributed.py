@@ -348,7 +348,10 @@ def read_ranges(ex, task, name: str, first: int, count: int) -> list[tuple[int, 
     if spec.tile:
         return input_ranges(_port_tiler(ex, task, name), first, count) if ps.tiled else [(0, n)]
     if spec.name == "spmv_csr":
-        return [(first, min(n, first + count + 1))] if name == "rowptr" else [(0, n)]
+        if name == "rowptr":
+            return [(first, min(n, first + count + 1))]
+        known = (getattr(ex, "gather_hulls", None) or {}).get((task.path, name, first, count))
+        return known if known is not None else [(0, n)]
     if ps.scalar:
         return [(0, n)]
     return input_ranges(_port_tiler(ex, task, name), first, count)
@@ -371,17 +374,75 @@ def _set_owner(lst: list, lo: int, hi: int, owner) -> list:
     return sorted(out)
 
 
+def _bound_host_array(host, bindings: dict, node: str):
+    """The caller's binding of the port group holding ``node`` as a flat numpy array, or None."""
+    import numpy as np
+    if not bindings:
+        return None
+    g = host.storage.groups.get(node)
+    for name in sorted(g or ()):
+        if name in bindings:
+            v = bindings[name]
+            if hasattr(v, "detach"):
+                v = v.detach().cpu().numpy()
+            return np.asarray(v).ravel()
+    return None
+
+
+def compute_gather_hulls(host, bindings: dict | None) -> dict:
+    """Data-aware read ranges of spmv_csr launches (refexec.py:111-121): rows [first,
+    first+count) read entries rowptr[first] .. rowptr[first+count] of colidx / values and
+    the x elements colidx names there -- for a banded matrix a halo around the launch's own
+    rows instead of all of x.  Only for matrices the caller bound and no step rewrites (the
+    reference caches its spmv plans on the same immutability, refexec.py:404-409).
+    Returns {(task path, port, first, count): [(lo, hi)]}."""
+    hulls: dict = {}
+    if not bindings:
+        return hulls
+    written = set()
+    steps = list(_walk(host.schedule.steps))
+    for step in steps:
+        t = host.task(step.task_path)
+        for name in _written_ports(t):
+            written.add(host.storage.groups[t.nodes[name]])
+    for step in steps:
+        if getattr(step, "op", None) != "spmv_csr":
+            continue
+        t = host.task(step.task_path)
+        if any(host.storage.groups[t.nodes[n]] in written for n in ("rowptr", "colidx")):
+            continue
+        rp = _bound_host_array(host, bindings, t.nodes["rowptr"])
+        ci = _bound_host_array(host, bindings, t.nodes["colidx"])
+        if rp is None or ci is None:
+            continue
+        for l in step.launches:
+            first, count = l.range.offset, l.range.count
+            if count <= 0:
+                continue
+            lo_e, hi_e = int(rp[first]), int(rp[first + count])
+            hulls[(t.path, "colidx", first, count)] = [(lo_e, hi_e)] if hi_e > lo_e else []
+            hulls[(t.path, "values", first, count)] = [(lo_e, hi_e)] if hi_e > lo_e else []
+            if hi_e > lo_e:
+                cols = ci[lo_e:hi_e]
+                hulls[(t.path, "x", first, count)] = [(int(cols.min()), int(cols.max()) + 1)]
+            else:
+                hulls[(t.path, "x", first, count)] = []
+    return hulls
+
+
 class PlanHost:
     """What a :class:`ShardPlan` reads from an executor -- the model's port groups, validated
     tasks, the schedule and per-task tilers -- without any device storage (host-side use
     and CPU tests)."""
 
-    def __init__(self, model, schedule, tilers: dict | None = None, precision: str = "default"):
+    def __init__(self, model, schedule, tilers: dict | None = None, precision: str = "default",
+                 bindings: dict | None = None):
         import types
         from .model import connected_port_groups
         self.model, self.schedule, self.tilers, self.precision = model, schedule, tilers or {}, precision
         self.storage = types.SimpleNamespace(groups=connected_port_groups(model))
         self._tasks: dict = {}
+        self.gather_hulls = compute_gather_hulls(self, bindings)
 
     def task(self, path: str):
         from .executor import _Task
@@ -533,8 +594,9 @@ class ShardPlan:
             self.writes[step.task_path] = entries
 
     @classmethod
-    def for_model(cls, model, schedule, world: int, tilers: dict | None = None) -> "ShardPlan":
-        return cls(PlanHost(model, schedule, tilers), world)
+    def for_model(cls, model, schedule, world: int, tilers: dict | None = None,
+                  bindings: dict | None = None) -> "ShardPlan":
+        return cls(PlanHost(model, schedule, tilers, bindings=bindings), world)
 
     def exchanged_bytes(self, task_path: str, esize: dict) -> int:
         """Bytes the dense transfers of one step move (for tests / reports)."""
@@ -686,10 +748,11 @@ class ShardedExecutor:
     run as device scalar kernels on every rank, so a CG iteration syncs the host once, for
     the loop test (refexec.py:525-541).  Outputs are gathered to the root (rank 0)."""
 
-    def _init_sharded(self, transport, replicas: list, world: int):
+    def _init_sharded(self, transport, replicas: list, world: int, bindings: dict | None = None):
         self.transport = transport
         self.world = world
         self.replicas = {rep.rank: rep for rep in replicas}
+        self.gather_hulls = compute_gather_hulls(self, bindings)
         self.root = 0
         self.plan = ShardPlan(self, world)
         self.stale: dict = {}          # group -> [(lo, hi, owner)] ranges the root holds stale
@@ -971,7 +1034,7 @@ def make_sharded_executor(model, schedule, bindings: dict, device_count: int, de
                 d = torch.device(dev)
                 with torch.cuda.device(d):
                     reps.append(Replica(r, d, DeviceStorage(model, bindings, d)))
-            self._init_sharded(LocalTransport(len(devices)), reps, len(devices))
+            self._init_sharded(LocalTransport(len(devices)), reps, len(devices), bindings)
 
     return LocalShardedExecutor()
 
@@ -991,6 +1054,6 @@ def make_distributed_executor(model, schedule, bindings: dict, *, group=None, **
             kw.setdefault("defer", True)      # host bindings: upload only this rank's input hull
             Executor.__init__(self, model, schedule, bindings, D, **kw)
             self.rank = tr.rank
-            self._init_sharded(tr, [Replica(tr.rank, self.device, self.storage)], tr.world)
+            self._init_sharded(tr, [Replica(tr.rank, self.device, self.storage)], tr.world, bindings)
 
     return DistributedExecutor()

@@ -163,3 +163,29 @@ def test_transpose_chain_pack_is_kept_when_read_later():
     from paper_1105_4424_b200.distributed import ROOT_GATHER
     plan, _ = _plan("transpose_chain", 3)
     assert plan.writes["t"][0][2] is None and plan.writes["t"][0][2] != ROOT_GATHER
+
+
+def test_cg_plan_with_bound_matrix_exchanges_halos_only(golden):
+    """With the matrix bound (and never rewritten), spmv's x reads are the columns its rows
+    name (refexec.py:111-121): on the 20x20 Poisson grid a launch of whole grid rows reads
+    one grid row (20 elements) beyond each end, so p moves 20 elements each way across each
+    shard boundary instead of being all-gathered."""
+    from paper_1105_4424_b200.distributed import ShardPlan
+    from paper_1105_4424_b200.model import model_from_dict
+    from paper_1105_4424_b200.partition import build_schedule
+    data, meta = golden
+    model = model_from_dict(meta["cg_k20"]["model"])
+    bind = {k: data[f"cg_k20/{k}"] for k in ("rowptr", "colidx", "values", "b")}
+    for D in (2, 4):
+        plan = ShardPlan.for_model(model, build_schedule(model, D), D, bindings=bind)
+        moved = {path: sum(hi - lo for name, g, tr, wr in entries for _, _, lo, hi in (tr or []))
+                 for path, entries in plan.writes.items()}
+        halo = 2 * 20 * (D - 1)
+        assert moved == {"init_r": 0, "init_p": halo, "loop.spmv": 0, "loop.axpy_x": 0, "loop.axpy_r": 0,
+                         "loop.scale_p": 0, "loop.axpy_p": halo}, moved
+        # each rank's input hull of the matrix is its own rows' entries only
+        g = plan.groups["colidx"]
+        rp = bind["rowptr"]
+        for r, rng in enumerate(plan.reads_by_rank[g]):
+            lo, hi = 100 * 4 // D * r, 100 * 4 // D * (r + 1)
+            assert rng == [(int(rp[lo]), int(rp[hi]))], (D, r, rng)
