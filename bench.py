@@ -1252,10 +1252,16 @@ def run_gpu(args):
         # collectives on every rank (a rank that moved nothing still takes part)
         g = allmax(min(times))
         nb = int(allmax(float(nbytes)))
+        fused = int(allsum(float(getattr(wl.ex, "fused_bytes", 0) or 0)))
         if nb:
             gather = {"ms": g * 1e3, "bytes_to_root": nb, "GBps": nb / g / 1e9, "backend": backend,
                       "op": "ShardedExecutor.gather_to_root: each rank's written output ranges to rank 0 "
                             "(batched send/recv of exact ranges)"}
+        if fused:
+            gather = {**(gather or {}), "fused_bytes_to_root_per_step": fused, "completion_ms": g * 1e3,
+                      "fused": ("the producing kernels store their output ranges straight into rank 0's array "
+                                "through CUDA IPC peer mappings (NVLink), inside the timed step; "
+                                "gather_to_root only waits for them (completion_ms)")}
 
     peaks = measured_peaks()
     out = None

@@ -151,6 +151,21 @@ int64_t aol_launch_counter(void);
  * The next launch that needs scratch allocates it again.  No reference counterpart. */
 int aol_release_scratch(void);
 
+/* Fused output gather over peer memory (the output array that crosses
+ * shards is assembled at the root by the producing kernels themselves).  The root exports
+ * its output buffer; every other rank maps it and passes the mapped pointer as the output
+ * port of its launches, so the kernels' stores travel over NVLink into the root's array.
+ * Replaces the reference's host-side gather of per-device results (refexec.py:545-547);
+ * no OpenCL counterpart.
+ *   aol_ipc_export: 64-byte CUDA IPC handle of the allocation holding dev_ptr, and dev_ptr's
+ *                   byte offset in that allocation
+ *   aol_ipc_import: map a handle exported by another process (peer access enabled lazily);
+ *                   *dev_ptr = mapped base + offset
+ *   aol_ipc_close:  unmap (by the pointer aol_ipc_import returned) */
+int aol_ipc_export(const void* dev_ptr, void* handle64, int64_t* offset);
+int aol_ipc_import(const void* handle64, int64_t offset, void** dev_ptr);
+int aol_ipc_close(void* dev_ptr);
+
 /* Task fusion: run `consumer` over its repetitions [first, first+count) computing
  * the part of `producer`'s output it reads on the fly, in shared memory, instead of
  * reading a materialised intermediate array (bit-identical results; the

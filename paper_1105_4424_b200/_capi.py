@@ -29,7 +29,8 @@ PRECISION = {"default": 0, "tf32": 1, "3xtf32": 2, "exact": 3}
 
 EXPORTS = ("aol_abi_version", "aol_last_error", "aol_device_count", "aol_validate", "aol_launch",
            "aol_plan_name", "aol_tiler_offsets", "aol_launch_counter", "aol_launch_fused2", "aol_loop_begin",
-           "aol_loop_end", "aol_loop_run", "aol_loop_destroy", "aol_loop_persistent", "aol_release_scratch")
+           "aol_loop_end", "aol_loop_run", "aol_loop_destroy", "aol_loop_persistent", "aol_release_scratch",
+           "aol_ipc_export", "aol_ipc_import", "aol_ipc_close")
 
 
 class NativeLibraryError(RuntimeError):
@@ -124,6 +125,9 @@ def load(path: Path | str | None = None) -> C.CDLL:
     lib.aol_loop_run.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_double),
                                  C.POINTER(C.c_int)]
     lib.aol_loop_destroy.argtypes = [C.c_void_p]
+    lib.aol_ipc_export.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)]
+    lib.aol_ipc_import.argtypes = [C.c_void_p, C.c_int64, C.POINTER(C.c_void_p)]
+    lib.aol_ipc_close.argtypes = [C.c_void_p]
     lib.aol_loop_persistent.argtypes = [C.POINTER(AolLoopOp), C.c_int, C.POINTER(C.c_void_p), C.c_int, C.c_int,
                                         C.c_int, C.c_int, C.c_double, C.c_int64, C.c_void_p,
                                         C.POINTER(C.c_int64), C.POINTER(C.c_double), C.POINTER(C.c_int)]
@@ -231,6 +235,26 @@ def loop_run(handle: int, stream: int) -> tuple[int, float, bool]:
 def loop_destroy(handle: int) -> None:
     if handle:
         load().aol_loop_destroy(C.c_void_p(handle))
+
+
+def ipc_export(ptr: int) -> bytes:
+    """72-byte token (64-byte CUDA IPC handle + int64 offset) for the device buffer at ``ptr``."""
+    h = (C.c_char * 64)()
+    off = C.c_int64(0)
+    check(load().aol_ipc_export(C.c_void_p(ptr), h, C.byref(off)))
+    return bytes(h) + int(off.value).to_bytes(8, "little", signed=True)
+
+
+def ipc_import(token: bytes) -> int:
+    """Map a buffer another process exported with :func:`ipc_export`; returns the device pointer."""
+    h = (C.c_char * 64).from_buffer_copy(token[:64])
+    out = C.c_void_p(0)
+    check(load().aol_ipc_import(h, int.from_bytes(token[64:72], "little", signed=True), C.byref(out)))
+    return int(out.value)
+
+
+def ipc_close(ptr: int) -> None:
+    check(load().aol_ipc_close(C.c_void_p(ptr)))
 
 
 def release_scratch() -> None:

@@ -10,7 +10,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 OUT = PKG / "_lib" / "libaolb200.so"
-SOURCES = ["aol_capi.cu", "aol_tile.cu", "aol_ident.cu", "aol_gemm.cu", "aol_stencil.cu", "aol_linefilter.cu", "aol_loop.cu", "aol_loopk.cu"]
+SOURCES = ["aol_capi.cu", "aol_tile.cu", "aol_ident.cu", "aol_gemm.cu", "aol_stencil.cu", "aol_linefilter.cu", "aol_loop.cu", "aol_loopk.cu", "aol_ipc.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

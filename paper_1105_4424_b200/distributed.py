@@ -759,6 +759,74 @@ class ShardedExecutor:
         self.pending_pack: dict = {}   # group -> (step, task, port): non-dense write the root lacks
         self.exchanged_bytes = 0
         self._upload_hulls()
+        self._setup_fused_gather()
+
+    def _setup_fused_gather(self) -> None:
+        """Fused output gather: a root output that no step reads is written
+        by every rank's kernels straight into the ROOT's array through a CUDA IPC peer mapping
+        (NVLink between GPUs), so nothing is gathered afterwards.  Only over a
+        torch.distributed transport (one process per GPU); AOL_FUSED_GATHER=0 turns it off."""
+        import os
+        self.fused_out: dict = {}          # group -> this rank's output pointer (None on the root)
+        self.fused_bytes = 0               # bytes this rank's launches store into the root per run()
+        self._ipc_ptrs: list = []
+        if not isinstance(self.transport, DistTransport) or os.environ.get("AOL_FUSED_GATHER", "1") == "0":
+            return
+        from . import _capi
+        root = self.model.application_components[self.model.application_root]
+        outs = {self.storage.groups[p.name] for p in root.ports
+                if getattr(p.direction, "value", p.direction) == "out"}
+        device_written, host_written = set(), set()
+        for step in _walk(self.schedule.steps):
+            t = self.task(step.task_path)
+            dst = device_written if hasattr(step, "launches") else host_written
+            for name in _written_ports(t):
+                dst.add(self.storage.groups[t.nodes[name]])
+        cand = sorted((g for g in outs if g in device_written and g not in host_written
+                       and g not in self.plan.reads_by_rank), key=lambda g: sorted(g))
+        if not cand:
+            return
+        tr = self.transport
+        me = tr.rank
+        tokens = [_capi.ipc_export(self.replicas[me].storage.arrays[g].data_ptr()) for g in cand] \
+            if me == self.root else None
+        box = [tokens]
+        tr.dist.broadcast_object_list(box, src=tr._peer(self.root), group=tr.group)
+        for g, tok in zip(cand, box[0]):
+            if me == self.root:
+                self.fused_out[g] = None
+                continue
+            ptr = _capi.ipc_import(tok)
+            self._ipc_ptrs.append(ptr)
+            self.fused_out[g] = ptr
+        for step in self.schedule.device_steps():
+            t = self.task(step.task_path)
+            for name in _written_ports(t):
+                g = self.storage.groups[t.nodes[name]]
+                if g in self.fused_out and me != self.root:
+                    P = _port_tiler(self, t, name).pattern_total
+                    esz = self.replicas[me].storage.arrays[g].element_size()
+                    self.fused_bytes += sum(l.range.count for l in self._mine(step, me)) * P * esz
+
+    def _port_ptr(self, rep, t, name: str) -> int:
+        """Device pointer a launch of this rank uses for port ``name``: the root's mapped
+        array for a fused output, else the rank's own array."""
+        g = rep.storage.groups[t.nodes[name]]
+        p = self.fused_out.get(g) if self.fused_out else None
+        return p if p is not None else rep.storage.array(t.nodes[name]).data_ptr()
+
+    def close(self) -> None:
+        """Unmap the root's arrays (fused gather)."""
+        from . import _capi
+        ptrs, self._ipc_ptrs = getattr(self, "_ipc_ptrs", []), []
+        for p in ptrs:
+            try:
+                _capi.ipc_close(p)
+            except Exception:  # noqa: BLE001 - teardown must not raise
+                pass
+
+    def __del__(self):
+        self.close()
 
     def _upload_hulls(self) -> None:
         """Deferred host bindings: each rank uploads only the ranges it ever reads (its input
@@ -822,7 +890,7 @@ class ShardedExecutor:
             mine = self._mine(step, rep.rank)
             if not mine:
                 continue
-            ptrs = [rep.storage.array(t.nodes[n]).data_ptr() for n in names]
+            ptrs = [self._port_ptr(rep, t, n) for n in names]
             s = self._stream_handle()
             for l in mine:
                 _capi.launch(ctask, l.range.offset, l.range.count, ptrs, (), s)
@@ -854,6 +922,8 @@ class ShardedExecutor:
 
     def _after_write(self, step, t) -> None:
         for name, g, tr, wr in self.plan.writes.get(step.task_path, []):
+            if g in self.fused_out:
+                continue                    # already stored into the root's array by the kernels
             if g in self.pending_pack:
                 # an older packed write of this group by ANOTHER step must reach the root before
                 # this one lands (program order); the same step again (the next run(), a loop
@@ -961,8 +1031,8 @@ class ShardedExecutor:
         t1, t2 = self.task(s1.task_path), self.task(s2.task_path)
         first = True
         for rep in self._each():
-            a1 = [rep.storage.array(t1.nodes[n]).data_ptr() for n in t1.port_order]
-            a2 = [rep.storage.array(t2.nodes[n]).data_ptr() for n in t2.port_order]
+            a1 = [self._port_ptr(rep, t1, n) for n in t1.port_order]
+            a2 = [self._port_ptr(rep, t2, n) for n in t2.port_order]
             s = self._stream_handle()
             if first and not _capi.launch_fused2(t1.ctask, t2.ctask, 0, 0, a1, a2, s):
                 self._fusable[(s1.task_path, s2.task_path)] = False
@@ -977,9 +1047,16 @@ class ShardedExecutor:
 
     # -- results -------------------------------------------------------------------
     def gather_to_root(self) -> int:
-        """Move every range of a root output the root holds stale to the root; returns bytes."""
+        """Move every range of a root output the root holds stale to the root; returns bytes.
+        Fused outputs need no move: every rank waits for its own kernels' remote stores, then
+        all ranks meet at a barrier, after which the root's arrays are complete."""
+        import torch
         root = self.model.application_components[self.model.application_root]
         moved = 0
+        if self.fused_out:
+            for rep in self._each():
+                torch.cuda.current_stream(rep.device).synchronize()
+            self.transport.barrier()
         for port in root.ports:
             if getattr(port.direction, "value", port.direction) != "out":
                 continue
@@ -1003,10 +1080,19 @@ class ShardedExecutor:
         the root; other ranks take part in the gather and return {} (the root holds results)."""
         self.gather_to_root()
         if self.root not in self.replicas:
-            return {}
-        self._enter(self.replicas[self.root])
-        from .executor import Executor
-        return Executor.outputs(self, on_device=on_device, out=out)
+            res = {}
+        else:
+            self._enter(self.replicas[self.root])
+            from .executor import Executor
+            res = Executor.outputs(self, on_device=on_device, out=out)
+        if self.fused_out:
+            # the root has copied the fused arrays before any rank's next run() may store
+            # into them again
+            if not on_device:
+                import torch
+                torch.cuda.current_stream(self.device).synchronize()
+            self.transport.barrier()
+        return res
 
 
 def enum_value_dtype(task) -> str:

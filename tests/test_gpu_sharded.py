@@ -132,8 +132,9 @@ def _dist_worker(rank, world, port, q, cases, golden_dir):
             res = ex.outputs()
             got = res[out] if rank == 0 else None
             assert (rank == 0) == bool(res)
-            results[case] = (got, ex.iterations, ex.exchanged_bytes, ref)
-        q.put((rank, {k: (v[0] if rank == 0 else None, v[1], v[2], v[3] if rank == 0 else None)
+            results[case] = (got, ex.iterations, ex.exchanged_bytes, ref, ex.fused_bytes, len(ex.fused_out))
+            ex.close()
+        q.put((rank, {k: (v[0] if rank == 0 else None, v[1], v[2], v[3] if rank == 0 else None, v[4], v[5])
                       for k, v in results.items()}))
     finally:
         dist.destroy_process_group()
@@ -158,8 +159,13 @@ def test_two_ranks_gloo_on_one_gpu_vs_oracle(golden):
         p.join(timeout=120)
         assert p.exitcode == 0
     r0 = out[0]
+    # fused gather: rank 1's kernels stored their output ranges straight into rank 0's arrays
+    # (CUDA IPC mapping; NVLink on a multi-GPU box) for every root output no step reads
+    for case in ("matmul", "stencil_chain", "downscaler", "transpose_chain"):
+        assert out[1][case][5] >= 1 and out[1][case][4] > 0, case
+    assert out[1]["cg"][5] == 0                   # x is read by the loop body: gathered, not fused
     for case in cases:
-        got, iters, xbytes, ref = r0[case]
+        got, iters, xbytes, ref = r0[case][:4]
         assert out[1][case][1] == iters            # both ranks ran the same number of iterations
         if case == "cg":
             data, meta = golden
