@@ -792,13 +792,23 @@ class ShardedExecutor:
             if me == self.root else None
         box = [tokens]
         tr.dist.broadcast_object_list(box, src=tr._peer(self.root), group=tr.group)
-        for g, tok in zip(cand, box[0]):
-            if me == self.root:
-                self.fused_out[g] = None
-                continue
-            ptr = _capi.ipc_import(tok)
-            self._ipc_ptrs.append(ptr)
-            self.fused_out[g] = ptr
+        ok = True
+        try:
+            for g, tok in zip(cand, box[0]):
+                if me == self.root:
+                    self.fused_out[g] = None
+                    continue
+                ptr = _capi.ipc_import(tok)
+                self._ipc_ptrs.append(ptr)
+                self.fused_out[g] = ptr
+        except _capi.AolError:
+            ok = False          # e.g. the root's GPU is not visible to this process
+        flags = [None] * tr.world
+        tr.dist.all_gather_object(flags, ok, group=tr.group)
+        if not all(flags):      # every rank must take the same path, or the exchanges diverge
+            self.close()
+            self.fused_out = {}
+            return
         for step in self.schedule.device_steps():
             t = self.task(step.task_path)
             for name in _written_ports(t):
