@@ -124,14 +124,17 @@ class Clocks:
                 nv.nvmlDeviceGetCurrentClocksThrottleReasons
         except AttributeError:
             reasons_fn = None
+        k, pw = 0, None
         while not self.stop_flag.is_set():
             try:
                 sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-                pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
                 rs = reasons_fn(h) if reasons_fn else 0
+                if k % 16 == 0:                     # the power query is slow; the clock is the point
+                    pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
                 self.rows.append((float(sm), pw, int(rs)))
             except Exception:
                 pass
+            k += 1
             self.stop_flag.wait(self.PERIOD_S)
 
     def start(self):
@@ -173,7 +176,8 @@ class Clocks:
             return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "sm_mhz_min": min(sm),
                     "sm_mhz_max": max(sm), "reasons": reasons, "reason_samples": counts,
                     "samples": len(rows), "period_ms": self.PERIOD_S * 1e3, "source": "nvml",
-                    "power_w_max": max(r[1] for r in rows), "power_w_median": statistics.median(r[1] for r in rows)}
+                    "power_w_max": max((r[1] for r in rows if r[1] is not None), default=None),
+                    "power_w_median": statistics.median([r[1] for r in rows if r[1] is not None] or [0.0])}
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
