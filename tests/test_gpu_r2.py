@@ -282,3 +282,46 @@ def test_matmul_stream_k_tail(M, N, K, devices, a_mn, b_k):
         a64, c1 = a64[rows], c1[rows]
     bound = (2.0 ** -9 + K * 2.0 ** -23) * (np.abs(a64) @ np.abs(b64))
     assert np.all(np.abs(c1 - a64 @ b64) <= bound)
+
+
+# -- more simulated devices than repetitions (partition.py:105-121: only T ranges) -------------
+
+@pytest.mark.parametrize("D", [5, 8, 13])
+def test_more_devices_than_repetitions_vs_oracle(D):
+    """partition_equally(T, D) with D > T yields T one-repetition launches (refexec.py:488);
+    tile_copy, the stencil and the TF32 matmul then run T tiny launches and still match the
+    oracle (matmul: the TF32 bound), on one device and sharded over local replicas."""
+    from paper_1105_4424_b200 import builders
+    from paper_1105_4424_b200.executor import execute_schedule
+    from paper_1105_4424_b200.partition import build_schedule
+    rng = np.random.default_rng(D)
+    # tile_copy: 3 repetitions of a 4-element reversed pattern
+    ts = dict(array=(12,), rep=(3,), pattern=(4,), origin=(3,), paving=((4,),), fitting=((-1,),))
+    td = dict(array=(12,), rep=(3,), pattern=(4,), origin=(0,), paving=((4,),), fitting=((1,),))
+    m = builders.tile_task_model("tile_copy", {"src": "in float32 [12]", "dst": "out float32 [12]"},
+                                 {"src": _tiler(ts), "dst": _tiler(td)}, (3,))
+    x = (np.arange(12) + 1).astype(np.float32)
+    want = orc.run_tile_task("tile_copy", {"src": ts, "dst": td}, {"src": x}, {"dst": (12, np.float32)}, 3, D)["dst"]
+    sched = build_schedule(m, D)
+    assert len(sched.device_steps()[0].launches) == 3
+    for devices in (None, [0, 0]):
+        got = execute_schedule(m, sched, {"p_src": x}, D, devices=devices).outputs["p_dst"]
+        assert np.array_equal(got, want)
+    # 2x2 toroidal stencil: 4 repetitions
+    t = orc.stencil_tilers(2, 2)
+    m = builders.tile_task_model("stencil", {"x": "in float32 [2,2]", "w": "in float32 [9]", "y": "out float32 [2,2]"},
+                                 {k: _tiler(v) for k, v in t.items()}, (2, 2))
+    xs = rng.random(4).astype(np.float32)
+    want = orc.run_tile_task("stencil", t, {"x": xs, "w": orc.stencil_weights()}, {"y": (4, np.float32)}, 4, D)["y"]
+    got = execute_schedule(m, build_schedule(m, D), {"p_x": xs, "p_w": orc.stencil_weights()}, D).outputs["p_y"]
+    assert np.array_equal(got, want)
+    # 1x2 matmul with K = 96: 2 repetitions
+    M, N, K = 1, 2, 96
+    g = orc.gemm_tilers(M, N, K)
+    m = builders.tile_task_model("matmul", {"a": f"in float32 [{M},{K}]", "b": f"in float32 [{K},{N}]",
+                                            "c": f"out float32 [{M},{N}]"}, {k: _tiler(v) for k, v in g.items()}, (M, N))
+    a = rng.standard_normal(M * K).astype(np.float32)
+    b = rng.standard_normal(K * N).astype(np.float32)
+    c = execute_schedule(m, build_schedule(m, D), {"p_a": a, "p_b": b}, D).outputs["p_c"].reshape(M, N)
+    a64, b64 = a.reshape(M, K).astype(np.float64), b.reshape(K, N).astype(np.float64)
+    assert np.all(np.abs(c - a64 @ b64) <= (2.0 ** -9 + K * 2.0 ** -23) * (np.abs(a64) @ np.abs(b64)))
