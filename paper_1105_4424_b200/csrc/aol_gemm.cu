@@ -1299,21 +1299,24 @@ int release_gemm_scratch() {
 }
 
 // Split-K tail of the pair kernel.  Whole waves of tiles run data-parallel.  A last partial
-// wave of R = tiles % pairs tiles that would leave pairs idle is cut into s k-ranges (pieces
-// of >= 32 k-blocks) when that shortens it: ceil(R s / pairs) / s waves instead of 1, by at
-// least 10% of a wave (R = 34 of 74, the 4-rank C2 shard: s = 2, 0.5 waves).  Returns s
-// (1 = no split).
+// wave of R = tiles % pairs tiles that would leave pairs idle is cut into s = 2 k-ranges
+// (pieces of >= 32 k-blocks) when that shortens it: ceil(2R / pairs) / 2 waves instead of 1
+// (R <= pairs / 2; R = 34 of 74, the 4-rank C2 shard: 0.5 waves).  AOL_GEMM_SPLIT=s forces
+// s (diagnostics, tests).  Returns s (1 = no split).
 static int split_k_tail(int num_tiles, int k_blocks, int pairs) {
   const char* env = getenv("AOL_GEMM_STREAMK");       // read per launch (A/B probes toggle it)
   if (env && env[0] == '0') return 1;
   const int rem = num_tiles % pairs;
   if (rem == 0 || rem > kSkMaxTiles) return 1;
+  const char* force = getenv("AOL_GEMM_SPLIT");           // diagnostic: force s (2..8)
+  if (force && atoi(force) >= 2 && k_blocks / atoi(force) >= 4) return atoi(force);
   int best = 1;
   double best_t = 1.0;
-  // s <= 3: with 4+ pieces per tile the pieces' epilogues (partial stores, the k-ordered sum)
-  // outweigh the shorter tail (measured, tools/time_streamk.py: 0.999x at the 8-rank shard with
-  // s = 4, 0.92x at 8192 rows with s = 8; s = 2 at the 4-rank shard: 1.135x)
-  for (int sp : {2, 3}) {
+  // s = 2 only: at more pieces per tile the pieces' epilogues (partial stores, the k-ordered
+  // sum) outweigh the shorter tail (tools/time_streamk.py, forced s: 8-rank shard s = 2/3/4/8
+  // 0.95/0.93/0.96/0.88x, 4-rank shard s = 3/4/8 0.91/1.03/1.01x; s = 2 at the 4-rank shard
+  // 1.09-1.135x)
+  for (int sp : {2}) {
     if (k_blocks / sp < 32) break;
     const double t = (double)((rem * sp + pairs - 1) / pairs) / sp;
     if (t < best_t - 1e-9) {

@@ -258,18 +258,23 @@ def test_memory_role_selects_the_kernel_staging():
     (1024, 8192, 8192, 1, False, False),   # C2's 8-rank shard: 128 tiles = 1 wave + 54 (no split)
     (2048, 8192, 8192, 1, False, False),   # C2's 4-rank shard: 256 tiles = 3 waves + 34 tail tiles, s = 2
     (2048, 8192, 2048, 1, False, True),    # the same tail, 64 k-blocks: pieces of 32
-    (768, 10496, 3072, 1, True, False),    # 123 tiles = 1 wave + 49 tail tiles, s = 3
+    (768, 10496, 3072, 1, True, False),    # 123 tiles = 1 wave + 49 tail tiles (s = 3 forced below)
     (256, 256, 4096, 1, True, False),      # one tile (s = 2: two pieces of 64 k-blocks)
     (300, 520, 200, 3, False, False),      # ragged shards, few k-blocks
     (777, 1000, 1500, 7, True, True),
     (2304, 2560, 768, 2, False, False)])   # 2 shards of 1152 rows: 50 tiles each
-def test_matmul_stream_k_tail(M, N, K, devices, a_mn, b_k):
+@pytest.mark.parametrize("force", [None, "3", "4", "8"])
+def test_matmul_stream_k_tail(M, N, K, devices, a_mn, b_k, force, monkeypatch):
     """Tiles of the last partial wave are cut into s k-ranges dealt to every pair and summed in
     k order by the last piece to arrive: inside the stated TF32 bound, and bit-identical from
     run to run (fixed summation order, counters reset by the last arriver)."""
     from paper_1105_4424_b200 import builders
     from paper_1105_4424_b200.executor import execute_schedule
     from paper_1105_4424_b200.partition import build_schedule
+    if force is not None:
+        if M * N * K > 2 ** 34:
+            pytest.skip("forced splits are checked on the smaller shapes")
+        monkeypatch.setenv("AOL_GEMM_SPLIT", force)      # read per launch
     t, ports, bind, A, B = _gemm_case(M, N, K, a_mn, b_k, M + N + K)
     model = builders.tile_task_model("matmul", ports, {k: _tiler(v) for k, v in t.items()}, (M, N))
     sched = build_schedule(model, devices)

@@ -36,4 +36,4 @@ for name, fn in (("numpy", lambda: execute_schedule(model, sched, bind, 1)),
         fn()
     torch.cuda.synchronize()
     pr.disable()
-    pstats.Stats(pr).sort_stats("cumulative").print_stats(35)
+    pstats.Stats(pr).sort_stats("tottime").print_stats(30)
