@@ -125,6 +125,38 @@ def host_stager() -> HostStager:
     return st
 
 
+class StorageLayout:
+    """What DeviceStorage derives from the model alone, computed once per model object
+    (model_memo): port nodes, connected groups, the B200 placement of each group, the HBM
+    arenas and each placed group's slice of its arena, and the size / dtype of every group."""
+
+    def __init__(self, model):
+        from .placement import hbm_arenas, placement_of_groups
+        self.groups = connected_port_groups(model)
+        self.ports = {}
+        for path, comp in iter_app_instances(model):
+            for port in comp.ports:
+                self.ports[f"{path}.{port.name}" if path else port.name] = port
+        self.placement = placement_of_groups(model)
+        self.arenas = hbm_arenas(model)
+        self.arena_views: dict = {}      # group -> (memory, lo, hi, torch dtype)
+        self.zero_groups: dict = {}      # group -> (elements, torch dtype), first port seen wins
+        for node, port in self.ports.items():
+            g = self.groups[node]
+            if g in self.zero_groups:
+                continue
+            tdt = torch_dtype(enum_value(port.data_type))
+            self.zero_groups[g] = (port.shape.total, tdt)
+            pl = self.placement.get(g)
+            if pl is not None and pl.tier == "hbm" and pl.memory in self.arenas:
+                self.arena_views[g] = (pl.memory, pl.b200_offset, pl.b200_offset + pl.size_bytes, tdt)
+
+
+def storage_layout(model) -> StorageLayout:
+    from .model import model_memo
+    return model_memo(model, "storage_layout", StorageLayout)
+
+
 class DeviceStorage:
     """Arrays per connected-port group, resident on one CUDA device (refexec.py:375-412)."""
 
@@ -132,29 +164,20 @@ class DeviceStorage:
         """``defer``: allocate device arrays for host bindings but do not copy them; the
         streamed path uploads each chunk's input hull itself (``self.host`` keeps the sources)."""
         torch = _torch()
+        lay = storage_layout(model)
         self.host: dict = {}
-        self.groups = connected_port_groups(model)
-        self.ports = {}
-        for path, comp in iter_app_instances(model):
-            for port in comp.ports:
-                self.ports[f"{path}.{port.name}" if path else port.name] = port
+        self.groups = lay.groups
+        self.ports = lay.ports
         self.arrays: dict = {}
         self.h2d_bytes = 0
         # MARTE placement drives allocation: every deviceGlobal memory is ONE HBM arena and each
         # of its port groups lives at the plan's 256 B-aligned offset (placement.plan_placement);
         # groups without a data allocation, or placed on another tier, get their own buffers
-        from .placement import hbm_arenas, placement_of_groups
-        self.placement = placement_of_groups(model)
+        self.placement = lay.placement
         self.arenas = {mem: torch.zeros(nbytes, dtype=torch.uint8, device=device)
-                       for mem, nbytes in hbm_arenas(model).items()}
-        for node, port in self.ports.items():
-            g = self.groups[node]
-            if g in self.arrays:
-                continue
-            pl = self.placement.get(g)
-            tdt = torch_dtype(enum_value(port.data_type))
-            if pl is not None and pl.tier == "hbm" and pl.memory in self.arenas:
-                self.arrays[g] = self.arenas[pl.memory][pl.b200_offset:pl.b200_offset + pl.size_bytes].view(tdt)
+                       for mem, nbytes in lay.arenas.items()}
+        for g, (mem, lo, hi, tdt) in lay.arena_views.items():
+            self.arrays[g] = self.arenas[mem][lo:hi].view(tdt)
         root = model.application_components[model.application_root]
         for port in root.ports:
             if enum_value(port.direction) not in ("in", "inout"):
@@ -200,11 +223,9 @@ class DeviceStorage:
                 else:
                     t = torch.from_numpy(arr).to(device=device, copy=True)
             self.arrays[self.groups[port.name]] = t
-        for node, port in self.ports.items():
-            g = self.groups[node]
+        for g, (n, tdt) in lay.zero_groups.items():
             if g not in self.arrays:
-                self.arrays[g] = torch.zeros(port.shape.total, dtype=torch_dtype(enum_value(port.data_type)),
-                                             device=device)
+                self.arrays[g] = torch.zeros(n, dtype=tdt, device=device)
 
     def array(self, node: str):
         return self.arrays[self.groups[node]]
@@ -213,8 +234,7 @@ class DeviceStorage:
 def _task_placement_flags(model, groups: dict, path: str, spec) -> int:
     """Kernel-staging flags the MARTE placement implies for a tile task: a tiled input placed
     in deviceLocal memory (tier "smem") asks for the shared-memory-staged kernel form."""
-    from .placement import placement_of_groups
-    pg = placement_of_groups(model)
+    pg = storage_layout(model).placement
     flags = 0
     for ps in spec.ports:
         if ps.tiled and enum_value(ps.direction) in ("in", "inout"):
@@ -288,9 +308,10 @@ class Executor:
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self.model, self.schedule = model, schedule
         # MARTE memory allocation -> B200 placement; CapacityExceeded before anything is launched
+        from .model import model_memo
         from .placement import check_private_and_tmem, plan_placement
         self.placement = plan_placement(model)
-        check_private_and_tmem(model, self.placement)
+        model_memo(model, "private_tmem_checked", lambda m: check_private_and_tmem(m, self.placement) or True)
         self.device_count = device_count
         self.tilers = tilers or {}
         self.precision = precision
@@ -306,7 +327,7 @@ class Executor:
         pair = (fuse and len(steps) == 2 and all(hasattr(s_, "launches") for s_ in steps)
                 and steps[0].op in FILTER_OPS and steps[1].op in FILTER_OPS)
         self.pipeline = pipeline if (pipeline > 1 and (single or pair)) else 0
-        with torch.cuda.device(self.device), self._on_stream():
+        with self._device_ctx():
             self.storage = DeviceStorage(model, bindings, self.device, stream, defer=defer or bool(self.pipeline))
         self._tasks: dict[str, _Task] = {}
         self.fuse = fuse
@@ -324,6 +345,18 @@ class Executor:
         self.iterations = 0
         self.final_relres = None
         self.converged = True
+
+    def _device_ctx(self):
+        """``self.device`` current and the caller's stream current; no context switch at all when
+        both already hold (the common single-GPU call: saves the per-call context overhead)."""
+        import contextlib
+        torch = _torch()
+        if self.stream is None and torch.cuda.current_device() == self.device.index:
+            return contextlib.nullcontext()
+        stack = contextlib.ExitStack()
+        stack.enter_context(torch.cuda.device(self.device))
+        stack.enter_context(self._on_stream())
+        return stack
 
     def _on_stream(self):
         """Make the caller's ``stream`` torch's current stream, so uploads, zero-fills, scalar
@@ -870,7 +903,7 @@ class Executor:
 
     def run(self, tol=None, max_iter=None) -> None:
         torch = _torch()
-        with torch.cuda.device(self.device), self._on_stream():
+        with self._device_ctx():
             self.run_steps(self.schedule.steps, tol, max_iter)
 
     def outputs(self, on_device: bool = False, out: dict | None = None) -> dict:
@@ -880,7 +913,7 @@ class Executor:
         pinned torch tensor) that receives the result instead of a fresh array.
         """
         torch = _torch()
-        with torch.cuda.device(self.device), self._on_stream():
+        with self._device_ctx():
             return self._outputs(on_device, out)
 
     def _outputs(self, on_device: bool, out: dict | None) -> dict:
