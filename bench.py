@@ -295,7 +295,11 @@ class Workload:
         if world > 1 and self.scaling == "strong":
             from paper_1105_4424_b200.distributed import make_distributed_executor
             self.schedule = build_schedule(model, world)
-            self.ex = make_distributed_executor(model, self.schedule, dev_bindings, fuse=Workload.fuse)
+            # the timed phase keeps outputs sharded (scaling is measured on the
+            # concurrent per-rank phase); the fused gather is timed separately (run_gpu)
+            self.ex = make_distributed_executor(model, self.schedule, dev_bindings, fuse=Workload.fuse,
+                                                fused_gather=False)
+            self.dev_bindings = dev_bindings
             steps = self.schedule.device_steps()
             mine = sum(l.range.count for st in steps for l in st.launches if l.device_index == rank)
             self.rank_fraction = mine / max(1, sum(st.total_work for st in steps))
@@ -307,6 +311,25 @@ class Workload:
 
     def step(self):
         self.ex.run()
+
+    def fused_step(self, time_steps, stream, barrier, steps: int):
+        """N > 1, strong scaling: time ``steps`` steps of an executor whose root outputs are
+        stored into rank 0's array by the producing kernels (fused gather), each step closed by
+        gather_to_root's wait; returns (bytes this rank stores into the root per step, ms)."""
+        if self.world < 2 or self.scaling != "strong" or not hasattr(self, "dev_bindings"):
+            return None
+        from paper_1105_4424_b200.distributed import make_distributed_executor
+        ex = make_distributed_executor(self.model, self.schedule, self.dev_bindings, fuse=Workload.fuse,
+                                       fused_gather=True)
+
+        def step():
+            ex.run()
+            ex.gather_to_root()
+        total_ms, _ = time_steps(self.torch, step, steps, 3, stream, barrier)
+        fb = ex.fused_bytes
+        ex.close()
+        del ex
+        return fb, total_ms / steps
 
     def gather(self):
         """N > 1: move every output range the root does not hold to rank 0 (the distributed
@@ -1256,16 +1279,24 @@ def run_gpu(args):
         # collectives on every rank (a rank that moved nothing still takes part)
         g = allmax(min(times))
         nb = int(allmax(float(nbytes)))
-        fused = int(allsum(float(getattr(wl.ex, "fused_bytes", 0) or 0)))
         if nb:
             gather = {"ms": g * 1e3, "bytes_to_root": nb, "GBps": nb / g / 1e9, "backend": backend,
-                      "op": "ShardedExecutor.gather_to_root: each rank's written output ranges to rank 0 "
-                            "(batched send/recv of exact ranges)"}
-        if fused:
-            gather = {**(gather or {}), "fused_bytes_to_root_per_step": fused, "completion_ms": g * 1e3,
-                      "fused": ("the producing kernels store their output ranges straight into rank 0's array "
-                                "through CUDA IPC peer mappings (NVLink), inside the timed step; "
-                                "gather_to_root only waits for them (completion_ms)")}
+                      "op": "ShardedExecutor.gather_to_root after the timed phase: each rank's written output "
+                            "ranges to rank 0 (batched send/recv of exact ranges)"}
+        # the same step with the fused output gather: the producing kernels store their output
+        # ranges straight into rank 0's array (CUDA IPC peer mappings, NVLink), so a step ends
+        # with the whole result at the root
+        fstep = getattr(wl, "fused_step", None)
+        if fstep is not None:
+            fb, fms = fstep(time_steps, stream, barrier, min(args.steps, 20))
+            fms = allmax(fms)
+            fb = int(allsum(float(fb)))
+            if fb:
+                gather = {**(gather or {}), "fused": {
+                    "step_ms": fms, "value": job_units / (fms * 1e-3), "unit": wl.unit,
+                    "bytes_to_root_per_step": fb,
+                    "op": "every rank's kernels store their output ranges into rank 0's array through CUDA IPC "
+                          "peer mappings (NVLink); the step ends when all ranks' stores are done (barrier)"}}
 
     peaks = measured_peaks()
     out = None

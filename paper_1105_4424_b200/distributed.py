@@ -748,7 +748,8 @@ class ShardedExecutor:
     run as device scalar kernels on every rank, so a CG iteration syncs the host once, for
     the loop test (refexec.py:525-541).  Outputs are gathered to the root (rank 0)."""
 
-    def _init_sharded(self, transport, replicas: list, world: int, bindings: dict | None = None):
+    def _init_sharded(self, transport, replicas: list, world: int, bindings: dict | None = None,
+                      fused_gather: bool | None = None):
         self.transport = transport
         self.world = world
         self.replicas = {rep.rank: rep for rep in replicas}
@@ -759,18 +760,21 @@ class ShardedExecutor:
         self.pending_pack: dict = {}   # group -> (step, task, port): non-dense write the root lacks
         self.exchanged_bytes = 0
         self._upload_hulls()
-        self._setup_fused_gather()
+        self._setup_fused_gather(fused_gather)
 
-    def _setup_fused_gather(self) -> None:
+    def _setup_fused_gather(self, enabled: bool | None = None) -> None:
         """Fused output gather: a root output that no step reads is written
         by every rank's kernels straight into the ROOT's array through a CUDA IPC peer mapping
         (NVLink between GPUs), so nothing is gathered afterwards.  Only over a
-        torch.distributed transport (one process per GPU); AOL_FUSED_GATHER=0 turns it off."""
+        torch.distributed transport (one process per GPU); ``fused_gather=False`` (or
+        AOL_FUSED_GATHER=0) keeps outputs sharded until gather_to_root."""
         import os
         self.fused_out: dict = {}          # group -> this rank's output pointer (None on the root)
         self.fused_bytes = 0               # bytes this rank's launches store into the root per run()
         self._ipc_ptrs: list = []
-        if not isinstance(self.transport, DistTransport) or os.environ.get("AOL_FUSED_GATHER", "1") == "0":
+        if enabled is None:
+            enabled = os.environ.get("AOL_FUSED_GATHER", "1") != "0"
+        if not isinstance(self.transport, DistTransport) or not enabled:
             return
         from . import _capi
         root = self.model.application_components[self.model.application_root]
@@ -1135,10 +1139,13 @@ def make_sharded_executor(model, schedule, bindings: dict, device_count: int, de
     return LocalShardedExecutor()
 
 
-def make_distributed_executor(model, schedule, bindings: dict, *, group=None, **kw):
+def make_distributed_executor(model, schedule, bindings: dict, *, group=None, fused_gather: bool | None = None,
+                              **kw):
     """Executor for rank ``dist.get_rank(group)`` of a schedule whose launches are spread over
     the group's ranks (launch d on rank d mod world; build the schedule with device_count ==
-    world size for one launch per rank, as the reference's D simulated devices)."""
+    world size for one launch per rank, as the reference's D simulated devices).
+    ``fused_gather``: root outputs no step reads are stored into the root's array by the
+    producing kernels (default: on unless AOL_FUSED_GATHER=0)."""
     from .executor import Executor
 
     class DistributedExecutor(ShardedExecutor, Executor):
@@ -1150,6 +1157,6 @@ def make_distributed_executor(model, schedule, bindings: dict, *, group=None, **
             kw.setdefault("defer", True)      # host bindings: upload only this rank's input hull
             Executor.__init__(self, model, schedule, bindings, D, **kw)
             self.rank = tr.rank
-            self._init_sharded(tr, [Replica(tr.rank, self.device, self.storage)], tr.world, bindings)
+            self._init_sharded(tr, [Replica(tr.rank, self.device, self.storage)], tr.world, bindings, fused_gather)
 
     return DistributedExecutor()
