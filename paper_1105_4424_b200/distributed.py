@@ -792,10 +792,16 @@ class ShardedExecutor:
             return
         tr = self.transport
         me = tr.rank
-        tokens = [_capi.ipc_export(self.replicas[me].storage.arrays[g].data_ptr()) for g in cand] \
-            if me == self.root else None
+        tokens = None
+        if me == self.root:
+            try:
+                tokens = [_capi.ipc_export(self.replicas[me].storage.arrays[g].data_ptr()) for g in cand]
+            except _capi.AolError:
+                tokens = None           # not exportable (e.g. expandable segments): nobody fuses
         box = [tokens]
         tr.dist.broadcast_object_list(box, src=tr._peer(self.root), group=tr.group)
+        if box[0] is None:
+            return
         ok = True
         try:
             for g, tok in zip(cand, box[0]):

@@ -84,7 +84,9 @@ class HostStager:
     only after its DMA's event completed.  Pinned sources bypass the ring."""
 
     def __init__(self, slot_bytes: int = 16 << 20, slots: int = 4):
+        import threading
         torch = _torch()
+        self.lock = threading.Lock()        # one ring per process: callers on several threads take turns
         self.slot_bytes = slot_bytes
         self.bufs = [torch.empty(slot_bytes, dtype=torch.uint8, pin_memory=True) for _ in range(slots)]
         self.events = [None] * slots
@@ -97,6 +99,11 @@ class HostStager:
             with torch.cuda.stream(stream):
                 dst.copy_(src, non_blocking=True)
             return
+        with self.lock:
+            self._copy_staged(dst, src, stream)
+
+    def _copy_staged(self, dst, src, stream) -> None:
+        torch = _torch()
         sb, db = src.view(torch.uint8), dst.view(torch.uint8)
         n = sb.numel()
         for off in range(0, n, self.slot_bytes):
