@@ -17,6 +17,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -57,6 +58,11 @@ struct Params {
   int sk_tiles, sk_split;
   float* sk_ws;        // [piece][2 CTAs][4 warps][8 chunks][8 col quads][32 lanes][4] fp32 partials
   unsigned* sk_cnt;    // [sk tiles][2 CTAs][4 warps] arrival counters (reset by the last arriver)
+  // pair kernel, mixed-width column tiles (w_narrow > 0): each row of m-tiles is cut into
+  // n_wide 256-column tiles then n_narrow w_narrow-column tiles, wide tiles dealt first, so
+  // every pair gets about the same number of columns (C2's 8-rank shard: 17 x 256 + 20 x 192
+  // per row -> 448 columns per pair instead of 2 x 256)
+  int n_wide, n_narrow, w_narrow;
 };
 
 // ------------------------------------------------------------ PTX helpers ----
@@ -349,6 +355,43 @@ __device__ __forceinline__ void tile_coords_pair(const Params& p, int tile, int&
   nt = in / gm;
 }
 
+// Output tile `tile` of the pair kernel: its m-tile, first column and width (256, or
+// w_narrow for the narrow tiles of a mixed-width plan).
+__device__ __forceinline__ void tile_geom(const Params& p, int tile, int& mt, int& col0, int& width) {
+  if (p.w_narrow == 0) {
+    int nt;
+    tile_coords_pair(p, tile, mt, nt);
+    col0 = nt * BN;
+    width = BN;
+    return;
+  }
+  const int wide = p.m_tiles * p.n_wide;
+  if (tile < wide) {
+    mt = tile % p.m_tiles;
+    col0 = (tile / p.m_tiles) * BN;
+    width = BN;
+  } else {
+    const int u = tile - wide;
+    mt = u % p.m_tiles;
+    col0 = p.n_wide * BN + (u / p.m_tiles) * p.w_narrow;
+    width = p.w_narrow;
+  }
+}
+
+// B operand of one CTA for a tile `width` columns wide (this CTA's half: width / 2 columns
+// from rcoord).  MN-major: (width / 2) / 32 boxes of 32 columns; K-major: one box of the
+// map's HALF_N rows (rows past the half are loaded and not used).  Returns the bytes issued.
+template <bool KMAJOR>
+__device__ __forceinline__ uint32_t load_b_pair(const CUtensorMap* map, uint32_t leader_bar, uint8_t* dst, int kcoord,
+                                                int rcoord, int half) {
+  if (KMAJOR) {
+    tma_load_2d_pair(map, leader_bar, dst, kcoord, rcoord);
+    return (uint32_t)B_BYTES;
+  }
+  for (int c = 0; c < half / 32; ++c) tma_load_2d_pair(map, leader_bar, dst + c * (BK * 128), rcoord + 32 * c, kcoord);
+  return (uint32_t)(half / 32) * (BK * 128);
+}
+
 // One unit of a pair's work: k-blocks [kb0, kb1) of output tile `tile`; `piece` >= 0 for a
 // split-K piece of a tail tile (its partial accumulator goes through sk_ws).
 struct Unit {
@@ -388,9 +431,9 @@ __device__ __forceinline__ float* sk_slot(const Params& p, int piece, uint32_t r
 
 // Masked store of one 32x32 fp32 chunk (rows = the warp's 32 TMEM lanes, columns c0..c0+31)
 // into C, staged through padded shared memory so each 16-byte store covers 4 rows x 128 B.
-__device__ __forceinline__ void store_chunk(const Params& p, float* epi, int ew, int lane, int mt, int nt,
+__device__ __forceinline__ void store_chunk(const Params& p, float* epi, int ew, int lane, int mt, int tcol0,
                                             uint32_t rank, int ch, const float (&v)[32]) {
-  const int64_t c0 = (int64_t)nt * BN + ch * 32;
+  const int64_t c0 = (int64_t)tcol0 + ch * 32;
   if (p.epi_smem) {
     float* st = epi + ew * 32 * EPI_PITCH;
 #pragma unroll
@@ -483,18 +526,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       UnitIter units(p, pair_id, num_pairs);
       Unit u;
       while (units.next(u)) {
-        int mt, nt;
-        tile_coords_pair(p, u.tile, mt, nt);
+        int mt, tcol0, width;
+        tile_geom(p, u.tile, mt, tcol0, width);
+        const int half = width >> 1;
         const int row0 = (int)(p.m_lo + (int64_t)mt * BM) + (int)rank * HALF_M;
-        const int col0 = nt * BN + (int)rank * HALF_N;
+        const int col0 = tcol0 + (int)rank * half;
+        const uint32_t b_bytes = B_KMAJOR ? (uint32_t)B_BYTES : (uint32_t)(half / 32) * (BK * 128);
         for (int kb = u.kb0; kb < u.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
           uint8_t* sb = sa + A_BYTES;
           const uint32_t lbar = smem_u32(&full[stage]) & PEER_MASK;
-          if (rank == 0) mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);
+          if (rank == 0) mbar_expect_tx(&full[stage], 2 * ((uint32_t)A_BYTES + b_bytes));
           load_operand_pair<A_KMAJOR, HALF_M>(&map_a, lbar, sa, kb * BK, row0);
-          load_operand_pair<B_KMAJOR, HALF_N>(&map_b, lbar, sb, kb * BK, col0);
+          load_b_pair<B_KMAJOR>(&map_b, lbar, sb, kb * BK, col0, half);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -502,9 +547,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
       // ---------------------------------------------------- MMA issuer (leader) ----
-      constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((A_KMAJOR ? 0u : 1u) << 15) |
-                                 ((B_KMAJOR ? 0u : 1u) << 16) | ((uint32_t)(BN >> 3) << 17) |
-                                 ((uint32_t)(BM >> 4) << 24);
+      constexpr uint32_t idesc0 = (1u << 4) | (2u << 7) | (2u << 10) | ((A_KMAJOR ? 0u : 1u) << 15) |
+                                  ((B_KMAJOR ? 0u : 1u) << 16) | ((uint32_t)(BM >> 4) << 24);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -512,6 +556,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       UnitIter units(p, pair_id, num_pairs);
       Unit u;
       while (units.next(u)) {
+        int mt, tcol0, width;
+        tile_geom(p, u.tile, mt, tcol0, width);
+        const uint32_t idesc = idesc0 | ((uint32_t)(width >> 3) << 17);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -539,20 +586,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     UnitIter units(p, pair_id, num_pairs);
     Unit u;
     while (units.next(u)) {
-      int mt, nt;
-      tile_coords_pair(p, u.tile, mt, nt);
+      int mt, tcol0, width;
+      tile_geom(p, u.tile, mt, tcol0, width);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
       if (u.piece < 0) {
 #pragma unroll 1
-        for (int ch = 0; ch < BN / 32; ++ch) {
+        for (int ch = 0; ch < width / 32; ++ch) {
           uint32_t r[32];
           tmem_ld32(tbase + ch * 32, r);
           float v[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-          store_chunk(p, epi, ew, lane, mt, nt, rank, ch, v);
+          store_chunk(p, epi, ew, lane, mt, tcol0, rank, ch, v);
         }
         tc_fence_before();
         arrive_leader(&tempty[acc]);
@@ -621,7 +668,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 v[4 * j4] += b.x; v[4 * j4 + 1] += b.y; v[4 * j4 + 2] += b.z; v[4 * j4 + 3] += b.w;
               }
             }
-            store_chunk(p, epi, ew, lane, mt, nt, rank, ch, v);
+            store_chunk(p, epi, ew, lane, mt, tcol0, rank, ch, v);
           }
           if (lane == 0) *cnt = 0u;             // ready for the next launch on this scratch
         }
@@ -1327,6 +1374,56 @@ static int split_k_tail(int num_tiles, int k_blocks, int pairs) {
   return best_t <= 0.9 ? best : 1;
 }
 
+// Mixed-width column tiles for the pair kernel: when whole 256-column tiles leave the last
+// wave partly idle, cut each row of m-tiles into n_wide 256-column tiles then n_narrow tiles
+// of w_narrow (192 or 128) columns, with the wide tiles dealt first (tile t to pair t mod
+// pairs), if that shortens the busiest pair by >= 4%.  A narrow tile still loads the whole A
+// block per k-step, so it costs more than its share of columns: measured at 8192^3 with every
+// tile w wide (tools/gpu/r2_ncol.sh, AOL_GEMM_NARROW_ALL): 192 -> 0.83x, 128 -> 0.64x,
+// 64 -> 0.39x the 256-wide throughput per column, i.e. a 192 / 128 tile takes 0.90 / 0.78 of a
+// 256 tile's time.  C2's 8-rank shard (4 rows, 74 pairs): 17 x 256 + 20 x 192 per row, busiest
+// pair 1.90 instead of 2 tile times (measured 1.02x); tiny products (one 256 x 256 tile) run
+// as two 128-column tiles on two pairs.  Returns false (keep whole tiles) otherwise.
+static bool narrow_plan(int m_tiles, int64_t N, int pairs, int& n_wide, int& n_narrow, int& w_narrow) {
+  const char* env = getenv("AOL_GEMM_NARROW");            // read per launch (A/B probes)
+  if (env && env[0] == '0') return false;
+  const char* fw = getenv("AOL_GEMM_NARROW_ALL");         // diagnostic: every tile w columns wide
+  if (fw && (atoi(fw) == 64 || atoi(fw) == 128 || atoi(fw) == 192)) {
+    n_wide = 0;
+    w_narrow = atoi(fw);
+    n_narrow = (int)((N + w_narrow - 1) / w_narrow);
+    return true;
+  }
+  const int64_t n_full = (N + 255) / 256;
+  const int64_t tiles0 = (int64_t)m_tiles * n_full;
+  const double base = (double)((tiles0 + pairs - 1) / pairs);  // busiest pair, in 256-tile times
+  double best = base;
+  bool found = false;
+  for (int wn : {192, 128}) {
+    const double cost = wn == 192 ? 0.90 : 0.78;           // time of one narrow tile / a 256 tile
+    for (int64_t nw = 0; nw * 256 <= N; ++nw) {
+      const int64_t nn = (N - nw * 256 + wn - 1) / wn;
+      const int64_t wide = (int64_t)m_tiles * nw, total = wide + (int64_t)m_tiles * nn;
+      if (total > (int64_t)1 << 30) continue;
+      // pair q owns tiles q, q + pairs, ...: ceil((wide - q) / pairs) wide ones, the rest narrow
+      double worst = 0.0;
+      for (int q = 0; q < pairs && q < total; ++q) {
+        const int64_t mine = (total - q + pairs - 1) / pairs;
+        const int64_t w = wide > q ? (wide - q + pairs - 1) / pairs : 0;
+        worst = std::max(worst, (double)w + (double)(mine - w) * cost);
+      }
+      if (worst <= base * 0.96 && worst < best - 1e-9) {
+        best = worst;
+        n_wide = (int)nw;
+        n_narrow = (int)nn;
+        w_narrow = wn;
+        found = true;
+      }
+    }
+  }
+  return found;
+}
+
 int launch_gemm_tf32(const aol_task& t, int64_t first, int64_t count, void* const* ports, cudaStream_t stream) {
   GemmShape g = recognise_gemm(t);
   if (!g.ok) return fail(AOL_EUNSUPPORTED, "matmul tilers are not a TMA-compatible GEMM");
@@ -1434,6 +1531,10 @@ static int gemm_core(const float* A, const float* B, float* C, const GemmShape& 
         pp.sk_ws = ws;
         pp.sk_cnt = cnt;
         pairs = all;                                   // the pieces spread over every pair
+      } else if (narrow_plan(pp.m_tiles, g.N, all, pp.n_wide, pp.n_narrow, pp.w_narrow)) {
+        pp.num_tiles = pp.m_tiles * (pp.n_wide + pp.n_narrow);
+        pp.dp_tiles = pp.num_tiles;
+        pairs = std::min(all, pp.num_tiles);
       }
     }
     cudaLaunchConfig_t cfg = {};

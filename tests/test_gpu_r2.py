@@ -330,3 +330,30 @@ def test_more_devices_than_repetitions_vs_oracle(D):
     c = execute_schedule(m, build_schedule(m, D), {"p_a": a, "p_b": b}, D).outputs["p_c"].reshape(M, N)
     a64, b64 = a.reshape(M, K).astype(np.float64), b.reshape(K, N).astype(np.float64)
     assert np.all(np.abs(c - a64 @ b64) <= (2.0 ** -9 + K * 2.0 ** -23) * (np.abs(a64) @ np.abs(b64)))
+
+
+# -- mixed-width column tiles of the TF32 pair kernel -------------------------------------------
+
+@pytest.mark.parametrize("M,N,K,devices,a_mn,b_k", [
+    (1024, 8192, 2048, 1, False, False),   # the 8-rank C2 shard shape: 17 x 256 + 20 x 192 per row
+    (1024, 8192, 1024, 1, False, True),    # the same with K-major B (full 128-row boxes, 96 used)
+    (1024, 8000, 512, 1, True, False),     # ragged N: the last narrow tile runs past N (masked)
+    (300, 520, 200, 3, False, False),      # ragged shards: 128-column tiles
+    (256, 256, 4096, 1, False, True),      # one tile -> two 128-column tiles
+    (2304, 2560, 768, 2, True, True)])     # 192-column tiles only
+@pytest.mark.parametrize("narrow", ["1", "0"])
+def test_matmul_mixed_width_tiles(M, N, K, devices, a_mn, b_k, narrow, monkeypatch):
+    """Whole 256-column tiles that would leave the last wave partly idle are replaced by
+    256- and 192/128-column tiles (tcgen05 N from the instruction descriptor at run time):
+    inside the TF32 bound, and the result does not depend on the tiling beyond the bound."""
+    from paper_1105_4424_b200 import builders
+    from paper_1105_4424_b200.executor import execute_schedule
+    from paper_1105_4424_b200.partition import build_schedule
+    monkeypatch.setenv("AOL_GEMM_NARROW", narrow)          # read per launch
+    monkeypatch.setenv("AOL_GEMM_STREAMK", "0")            # the split-K tail would take precedence
+    t, ports, bind, A, B = _gemm_case(M, N, K, a_mn, b_k, M * 7 + N + K)
+    model = builders.tile_task_model("matmul", ports, {k: _tiler(v) for k, v in t.items()}, (M, N))
+    c = execute_schedule(model, build_schedule(model, devices), bind, devices).outputs["p_c"].reshape(M, N)
+    a64, b64 = A.astype(np.float64), B.astype(np.float64)
+    bound = (2.0 ** -9 + K * 2.0 ** -23) * (np.abs(a64) @ np.abs(b64))
+    assert np.all(np.abs(c - a64 @ b64) <= bound)
