@@ -357,8 +357,9 @@ __device__ __forceinline__ void tile_coords_pair(const Params& p, int tile, int&
 
 // Output tile `tile` of the pair kernel: its m-tile, first column and width (256, or
 // w_narrow for the narrow tiles of a mixed-width plan).
+template <bool MIXED>
 __device__ __forceinline__ void tile_geom(const Params& p, int tile, int& mt, int& col0, int& width) {
-  if (p.w_narrow == 0) {
+  if (!MIXED) {
     int nt;
     tile_coords_pair(p, tile, mt, nt);
     col0 = nt * BN;
@@ -479,7 +480,9 @@ __device__ __forceinline__ void store_chunk(const Params& p, float* epi, int ew,
   }
 }
 
-template <bool A_KMAJOR, bool B_KMAJOR>
+// MIXED: the mixed-width tile plan (run-time tile widths); false compiles the whole-tile
+// kernel with every width a constant.
+template <bool A_KMAJOR, bool B_KMAJOR, bool MIXED>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_gemm_tf32_pair(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, Params p) {
   extern __shared__ uint8_t smem_raw[];
@@ -527,11 +530,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       Unit u;
       while (units.next(u)) {
         int mt, tcol0, width;
-        tile_geom(p, u.tile, mt, tcol0, width);
-        const int half = width >> 1;
+        tile_geom<MIXED>(p, u.tile, mt, tcol0, width);
+        const int half = MIXED ? width >> 1 : HALF_N;
         const int row0 = (int)(p.m_lo + (int64_t)mt * BM) + (int)rank * HALF_M;
         const int col0 = tcol0 + (int)rank * half;
-        const uint32_t b_bytes = B_KMAJOR ? (uint32_t)B_BYTES : (uint32_t)(half / 32) * (BK * 128);
+        const uint32_t b_bytes = (B_KMAJOR || !MIXED) ? (uint32_t)B_BYTES : (uint32_t)(half / 32) * (BK * 128);
         for (int kb = u.kb0; kb < u.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
@@ -539,7 +542,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t lbar = smem_u32(&full[stage]) & PEER_MASK;
           if (rank == 0) mbar_expect_tx(&full[stage], 2 * ((uint32_t)A_BYTES + b_bytes));
           load_operand_pair<A_KMAJOR, HALF_M>(&map_a, lbar, sa, kb * BK, row0);
-          load_b_pair<B_KMAJOR>(&map_b, lbar, sb, kb * BK, col0, half);
+          if (MIXED) load_b_pair<B_KMAJOR>(&map_b, lbar, sb, kb * BK, col0, half);
+          else load_operand_pair<B_KMAJOR, HALF_N>(&map_b, lbar, sb, kb * BK, col0);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -557,8 +561,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       Unit u;
       while (units.next(u)) {
         int mt, tcol0, width;
-        tile_geom(p, u.tile, mt, tcol0, width);
-        const uint32_t idesc = idesc0 | ((uint32_t)(width >> 3) << 17);
+        tile_geom<MIXED>(p, u.tile, mt, tcol0, width);
+        const uint32_t idesc = idesc0 | ((uint32_t)((MIXED ? width : BN) >> 3) << 17);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -587,13 +591,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     Unit u;
     while (units.next(u)) {
       int mt, tcol0, width;
-      tile_geom(p, u.tile, mt, tcol0, width);
+      tile_geom<MIXED>(p, u.tile, mt, tcol0, width);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
       if (u.piece < 0) {
+        const int nch = MIXED ? width / 32 : BN / 32;
 #pragma unroll 1
-        for (int ch = 0; ch < width / 32; ++ch) {
+        for (int ch = 0; ch < nch; ++ch) {
           uint32_t r[32];
           tmem_ld32(tbase + ch * 32, r);
           float v[32];
@@ -1377,7 +1382,7 @@ static int split_k_tail(int num_tiles, int k_blocks, int pairs) {
 // Mixed-width column tiles for the pair kernel: when whole 256-column tiles leave the last
 // wave partly idle, cut each row of m-tiles into n_wide 256-column tiles then n_narrow tiles
 // of w_narrow (192 or 128) columns, with the wide tiles dealt first (tile t to pair t mod
-// pairs), if that shortens the busiest pair by >= 4%.  A narrow tile still loads the whole A
+// pairs), if that shortens the busiest pair by >= 4% (opt-in, see below).  A narrow tile still loads the whole A
 // block per k-step, so it costs more than its share of columns: measured at 8192^3 with every
 // tile w wide (tools/gpu/r2_ncol.sh, AOL_GEMM_NARROW_ALL): 192 -> 0.83x, 128 -> 0.64x,
 // 64 -> 0.39x the 256-wide throughput per column, i.e. a 192 / 128 tile takes 0.90 / 0.78 of a
@@ -1385,9 +1390,12 @@ static int split_k_tail(int num_tiles, int k_blocks, int pairs) {
 // pair 1.90 instead of 2 tile times (measured 1.02x); tiny products (one 256 x 256 tile) run
 // as two 128-column tiles on two pairs.  Returns false (keep whole tiles) otherwise.
 static bool narrow_plan(int m_tiles, int64_t N, int pairs, int& n_wide, int& n_narrow, int& w_narrow) {
-  const char* env = getenv("AOL_GEMM_NARROW");            // read per launch (A/B probes)
-  if (env && env[0] == '0') return false;
+  // opt-in (AOL_GEMM_NARROW=1, read per launch): the run-time-width kernel this needs runs
+  // 15-20% slower per tile than the constant-width one (same-box A/B: the 8-rank shard 0.31 ms
+  // mixed vs 0.25-0.28 ms whole tiles), more than the 5% the plan saves
+  const char* env = getenv("AOL_GEMM_NARROW");
   const char* fw = getenv("AOL_GEMM_NARROW_ALL");         // diagnostic: every tile w columns wide
+  if (!(env && env[0] == '1') && !fw) return false;
   if (fw && (atoi(fw) == 64 || atoi(fw) == 128 || atoi(fw) == 192)) {
     n_wide = 0;
     w_narrow = atoi(fw);
@@ -1507,10 +1515,6 @@ static int gemm_core(const float* A, const float* B, float* C, const GemmShape& 
     pp.m_tiles = (int)((p.m_hi - p.m_lo + pair::BM) / pair::BM);
     pp.n_tiles = (int)((g.N + pair::BN - 1) / pair::BN);
     pp.num_tiles = pp.m_tiles * pp.n_tiles;
-    void (*k2)(const CUtensorMap, const CUtensorMap, Params);
-    if (g.a_kmajor) k2 = g.b_kmajor ? pair::k_gemm_tf32_pair<true, true> : pair::k_gemm_tf32_pair<true, false>;
-    else k2 = g.b_kmajor ? pair::k_gemm_tf32_pair<false, true> : pair::k_gemm_tf32_pair<false, false>;
-    AOL_CUDA_CHECK(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pair::SMEM_BYTES));
     int sms2 = kNumSMs;
     int dev2 = 0;
     if (cudaGetDevice(&dev2) == cudaSuccess) cudaDeviceGetAttribute(&sms2, cudaDevAttrMultiProcessorCount, dev2);
@@ -1537,6 +1541,16 @@ static int gemm_core(const float* A, const float* B, float* C, const GemmShape& 
         pairs = std::min(all, pp.num_tiles);
       }
     }
+    void (*k2)(const CUtensorMap, const CUtensorMap, Params);
+    const bool mixed = pp.w_narrow != 0;
+    if (mixed) {
+      if (g.a_kmajor) k2 = g.b_kmajor ? pair::k_gemm_tf32_pair<true, true, true> : pair::k_gemm_tf32_pair<true, false, true>;
+      else k2 = g.b_kmajor ? pair::k_gemm_tf32_pair<false, true, true> : pair::k_gemm_tf32_pair<false, false, true>;
+    } else {
+      if (g.a_kmajor) k2 = g.b_kmajor ? pair::k_gemm_tf32_pair<true, true, false> : pair::k_gemm_tf32_pair<true, false, false>;
+      else k2 = g.b_kmajor ? pair::k_gemm_tf32_pair<false, true, false> : pair::k_gemm_tf32_pair<false, false, false>;
+    }
+    AOL_CUDA_CHECK(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pair::SMEM_BYTES));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * pairs);
     cfg.blockDim = dim3(NUM_THREADS);

@@ -343,9 +343,9 @@ def test_more_devices_than_repetitions_vs_oracle(D):
     (2304, 2560, 768, 2, True, True)])     # 192-column tiles only
 @pytest.mark.parametrize("narrow", ["1", "0"])
 def test_matmul_mixed_width_tiles(M, N, K, devices, a_mn, b_k, narrow, monkeypatch):
-    """Whole 256-column tiles that would leave the last wave partly idle are replaced by
-    256- and 192/128-column tiles (tcgen05 N from the instruction descriptor at run time):
-    inside the TF32 bound, and the result does not depend on the tiling beyond the bound."""
+    """Opt-in mixed-width plan (AOL_GEMM_NARROW=1): whole 256-column tiles that would leave the
+    last wave partly idle are replaced by 256- and 192/128-column tiles (tcgen05 N from the
+    instruction descriptor at run time): inside the TF32 bound either way."""
     from paper_1105_4424_b200 import builders
     from paper_1105_4424_b200.executor import execute_schedule
     from paper_1105_4424_b200.partition import build_schedule
