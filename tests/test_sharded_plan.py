@@ -116,7 +116,15 @@ def _worker(rank, world, port, q):
         rep.pbuf["k"] = buf
         tr.reduce_partials({rank: rep}, "k")
         ok &= buf.tolist()[:3] == [-0.1, -0.2, -0.30000000000000004] and buf[4].item() == -0.5
-        q.put((rank, ok, tr.bytes_moved))
+        sent = tr.bytes_moved
+        # variable-size streams to the root only (the packed gather of a non-dense output)
+        local = torch.arange(3 + 4 * rank, dtype=torch.float32) + 100 * rank
+        got = tr.gather_v({rank: rep}, local, [3, 7], 0)
+        if rank == 0:
+            ok &= set(got) == {1} and torch.equal(got[1], torch.arange(7, dtype=torch.float32) + 100)
+        else:
+            ok &= got == {}
+        q.put((rank, ok, sent))
     finally:
         dist.destroy_process_group()
 
