@@ -740,6 +740,22 @@ class LocalTransport:
         pass
 
 
+def fused_gather_candidates(host, plan: "ShardPlan") -> list:
+    """Root output groups that only device steps write and no step reads (any rank): their
+    producing kernels may store straight into the root's array (fused gather).  Sorted, so
+    every rank derives the same list."""
+    root = host.model.application_components[host.model.application_root]
+    outs = {host.storage.groups[p.name] for p in root.ports if getattr(p.direction, "value", p.direction) == "out"}
+    device_written, host_written = set(), set()
+    for step in _walk(host.schedule.steps):
+        t = host.task(step.task_path)
+        dst = device_written if hasattr(step, "launches") else host_written
+        for name in _written_ports(t):
+            dst.add(host.storage.groups[t.nodes[name]])
+    return sorted((g for g in outs if g in device_written and g not in host_written and g not in plan.reads_by_rank),
+                  key=lambda g: sorted(g))
+
+
 class ShardedExecutor:
     """Mixin over :class:`executor.Executor`: launch d of every device step runs on rank
     d mod world; only what a later step of another rank reads is exchanged (ShardPlan);
@@ -777,17 +793,7 @@ class ShardedExecutor:
         if not isinstance(self.transport, DistTransport) or not enabled:
             return
         from . import _capi
-        root = self.model.application_components[self.model.application_root]
-        outs = {self.storage.groups[p.name] for p in root.ports
-                if getattr(p.direction, "value", p.direction) == "out"}
-        device_written, host_written = set(), set()
-        for step in _walk(self.schedule.steps):
-            t = self.task(step.task_path)
-            dst = device_written if hasattr(step, "launches") else host_written
-            for name in _written_ports(t):
-                dst.add(self.storage.groups[t.nodes[name]])
-        cand = sorted((g for g in outs if g in device_written and g not in host_written
-                       and g not in self.plan.reads_by_rank), key=lambda g: sorted(g))
+        cand = fused_gather_candidates(self, self.plan)
         if not cand:
             return
         tr = self.transport

@@ -197,3 +197,21 @@ def test_cg_plan_with_bound_matrix_exchanges_halos_only(golden):
         for r, rng in enumerate(plan.reads_by_rank[g]):
             lo, hi = 100 * 4 // D * r, 100 * 4 // D * (r + 1)
             assert rng == [(int(rp[lo]), int(rp[hi]))], (D, r, rng)
+
+
+def test_fused_gather_candidates(golden):
+    """Root outputs that only device steps write and no step reads are stored into the root's
+    array by their producers (fused gather): matmul's C, the stencil chain's and downscaler's
+    final outputs; not CG's x, which the loop body reads and updates."""
+    from paper_1105_4424_b200.distributed import PlanHost, ShardPlan, fused_gather_candidates
+    from paper_1105_4424_b200.model import model_from_dict
+    from paper_1105_4424_b200.partition import build_schedule
+    for case, port in (("matmul", "p_c"), ("stencil_chain", "y"), ("downscaler", "y"), ("transpose_chain", "y")):
+        model, bind, out, ref = CASES[case]()
+        host = PlanHost(model, build_schedule(model, 2))
+        plan = ShardPlan(host, 2)
+        assert fused_gather_candidates(host, plan) == [host.storage.groups[out]], case
+    data, meta = golden
+    model = model_from_dict(meta["cg_k20"]["model"])
+    host = PlanHost(model, build_schedule(model, 2))
+    assert fused_gather_candidates(host, ShardPlan(host, 2)) == []
