@@ -128,7 +128,9 @@ def host_stager() -> HostStager:
     """One staging ring per process (64 MiB pinned, from torch's caching host allocator)."""
     st = _STAGERS.get("default")
     if st is None:
-        st = _STAGERS["default"] = HostStager()
+        mb = int(os.environ.get("AOL_STAGE_SLOT_MB", "16"))
+        n = int(os.environ.get("AOL_STAGE_SLOTS", "4"))
+        st = _STAGERS["default"] = HostStager(slot_bytes=max(1, mb) << 20, slots=max(2, n))
     return st
 
 
