@@ -956,7 +956,7 @@ class CGWorkload(Workload):
                else f"rows sharded over {world} ranks, p exchanged after each update, dots reduced on the device")
         self.workload = (f"CG (bundled cg.gmodel resized) {self.matrix}: n={n}, nnz={self.nnz}, {self.iters} "
                          f"iterations; {how} (Executor setup timed, inputs resident in HBM)")
-        self.l2 = "working set (~12 MB) fits in L2: L2 flushed (256 MiB write) before every timed step"
+        self.l2 = "working set (~12 MB) fits in L2: L2 flushed (256 MiB write + 256 MiB read) before every timed step"
         self.ex = None
 
     graphs = True
@@ -1058,7 +1058,8 @@ class C1Workload(Workload):
         self.algorithmic = {"flop_per_launch": 2 * n ** 3, "per_unit": "2 FLOP per (m, n, k)"}
         self.workload = (f"C1 matmul {n}x{n}x{n} fp32 via execute_schedule (TF32 tcgen05): value with HBM-resident "
                          f"bindings and device outputs, e2e with host numpy in/out")
-        self.l2 = "small (768 KB): L2 flushed (256 MiB write) before every timed step; launch- and API-overhead-bound"
+        self.l2 = ("small (768 KB): L2 flushed (256 MiB write + 256 MiB read) before every timed step; launch- and "
+                   "API-overhead-bound")
 
     l2_flush = True
 
@@ -1204,9 +1205,17 @@ def run_gpu(args):
     flush = None
     if getattr(wl, "l2_flush", False):
         scrub = torch.empty(64 << 20, dtype=torch.float32, device=device)      # 256 MiB > 126 MB L2
+        rd = torch.ones(64 << 20, dtype=torch.float32, device=device)
+        acc = torch.zeros(1, device=device)
 
         def flush():
+            # write 256 MiB, then read another 256 MiB: the L2 is left holding clean lines, so the
+            # timed step neither finds its inputs cached nor pays for the flush's write-backs.
+            # Synchronised: the step's start event then fires when the step itself is enqueued,
+            # so host-bound steps (C1) are not hidden behind the flush's GPU time
             scrub.fill_(1.0)
+            acc.copy_(rd.sum())
+            torch.cuda.synchronize()
     phase("warm")
     clocks.start()
     total_ms, per = time_steps(torch, wl.step, args.steps, 0, stream, barrier, flush)
