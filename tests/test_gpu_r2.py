@@ -357,3 +357,18 @@ def test_matmul_mixed_width_tiles(M, N, K, devices, a_mn, b_k, narrow, monkeypat
     a64, b64 = A.astype(np.float64), B.astype(np.float64)
     bound = (2.0 ** -9 + K * 2.0 ** -23) * (np.abs(a64) @ np.abs(b64))
     assert np.all(np.abs(c - a64 @ b64) <= bound)
+
+
+def test_ipc_abi_errors():
+    """aol_ipc_*: exporting a device pointer gives a 72-byte token (handle + offset inside the
+    allocation); closing a pointer that was never imported, or exporting host memory, fails
+    with an error status instead of crashing."""
+    from paper_1105_4424_b200 import _capi
+    t = torch.zeros(1 << 20, device="cuda")
+    tok = _capi.ipc_export(t.data_ptr() + 4096)
+    assert len(tok) == 72 and int.from_bytes(tok[64:], "little") >= 4096
+    with pytest.raises(_capi.AolError):
+        _capi.ipc_close(t.data_ptr())
+    host = np.zeros(16, np.float32)
+    with pytest.raises(_capi.AolError):
+        _capi.ipc_export(host.ctypes.data)
