@@ -183,10 +183,14 @@ class DeviceStorage:
         # of its port groups lives at the plan's 256 B-aligned offset (placement.plan_placement);
         # groups without a data allocation, or placed on another tier, get their own buffers
         self.placement = lay.placement
-        self.arenas = {mem: torch.zeros(nbytes, dtype=torch.uint8, device=device)
+        # uninitialised arena: bound inputs are overwritten by their upload, and every other
+        # placed group is zero-filled below (refexec.py:399-403) -- zeroing the inputs too would
+        # cost a memset of them and race with uploads issued on another stream
+        self.arenas = {mem: torch.empty(nbytes, dtype=torch.uint8, device=device)
                        for mem, nbytes in lay.arenas.items()}
         for g, (mem, lo, hi, tdt) in lay.arena_views.items():
             self.arrays[g] = self.arenas[mem][lo:hi].view(tdt)
+        bound: set = set()
         root = model.application_components[model.application_root]
         for port in root.ports:
             if enum_value(port.direction) not in ("in", "inout"):
@@ -232,6 +236,10 @@ class DeviceStorage:
                 else:
                     t = torch.from_numpy(arr).to(device=device, copy=True)
             self.arrays[self.groups[port.name]] = t
+            bound.add(self.groups[port.name])
+        for g in lay.arena_views:
+            if g not in bound:
+                self.arrays[g].zero_()
         for g, (n, tdt) in lay.zero_groups.items():
             if g not in self.arrays:
                 self.arrays[g] = torch.zeros(n, dtype=tdt, device=device)
@@ -487,6 +495,7 @@ class Executor:
             return None
         comp = torch.cuda.current_stream(self.device) if self.stream is None else self.stream
         cin, cout = torch.cuda.Stream(self.device), torch.cuda.Stream(self.device)
+        cin.wait_stream(comp)            # uploads land after the storage's zero-fills
         # whole-array inputs (filter weights) first
         with torch.cuda.stream(cin):
             for t in (t1, t2):
@@ -569,6 +578,7 @@ class Executor:
         comp = torch.cuda.current_stream(self.device) if self.stream is None else self.stream
         cin = torch.cuda.Stream(self.device)
         cout = torch.cuda.Stream(self.device)
+        cin.wait_stream(comp)            # uploads land after the storage's zero-fills
         st = self.storage
         arrays = {name: st.array(node) for name, node in t.nodes.items()}
         in_ports = [ps.name for ps in t.spec.ports if enum_value(ps.direction) in ("in", "inout")
