@@ -166,6 +166,14 @@ int aol_ipc_export(const void* dev_ptr, void* handle64, int64_t* offset);
 int aol_ipc_import(const void* handle64, int64_t offset, void** dev_ptr);
 int aol_ipc_close(void* dev_ptr);
 
+/* Strided 2-D asynchronous copy, host <-> device either way (cudaMemcpy2DAsync, direction from
+ * the pointers; pinned host memory): `height` rows of `width_bytes`, row pitches in bytes.  The
+ * streamed MatMul moves column blocks of row-major B and C with it, so C blocks can be computed
+ * and downloaded while B is still uploading.  No reference counterpart (refexec copies whole
+ * arrays, refexec.py:392-398, :545-547). */
+int aol_memcpy2d(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width_bytes, int64_t height,
+                 void* stream);
+
 /* Task fusion: run `consumer` over its repetitions [first, first+count) computing
  * the part of `producer`'s output it reads on the fly, in shared memory, instead of
  * reading a materialised intermediate array (bit-identical results; the

@@ -30,7 +30,7 @@ PRECISION = {"default": 0, "tf32": 1, "3xtf32": 2, "exact": 3}
 EXPORTS = ("aol_abi_version", "aol_last_error", "aol_device_count", "aol_validate", "aol_launch",
            "aol_plan_name", "aol_tiler_offsets", "aol_launch_counter", "aol_launch_fused2", "aol_loop_begin",
            "aol_loop_end", "aol_loop_run", "aol_loop_destroy", "aol_loop_persistent", "aol_release_scratch",
-           "aol_ipc_export", "aol_ipc_import", "aol_ipc_close")
+           "aol_ipc_export", "aol_ipc_import", "aol_ipc_close", "aol_memcpy2d")
 
 
 class NativeLibraryError(RuntimeError):
@@ -128,6 +128,7 @@ def load(path: Path | str | None = None) -> C.CDLL:
     lib.aol_ipc_export.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)]
     lib.aol_ipc_import.argtypes = [C.c_void_p, C.c_int64, C.POINTER(C.c_void_p)]
     lib.aol_ipc_close.argtypes = [C.c_void_p]
+    lib.aol_memcpy2d.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p]
     lib.aol_loop_persistent.argtypes = [C.POINTER(AolLoopOp), C.c_int, C.POINTER(C.c_void_p), C.c_int, C.c_int,
                                         C.c_int, C.c_int, C.c_double, C.c_int64, C.c_void_p,
                                         C.POINTER(C.c_int64), C.POINTER(C.c_double), C.POINTER(C.c_int)]
@@ -255,6 +256,12 @@ def ipc_import(token: bytes) -> int:
 
 def ipc_close(ptr: int) -> None:
     check(load().aol_ipc_close(C.c_void_p(ptr)))
+
+
+def memcpy2d(dst: int, dpitch: int, src: int, spitch: int, width_bytes: int, height: int, stream: int) -> None:
+    """Asynchronous strided copy (aol_memcpy2d): `height` rows of `width_bytes`, pitches in bytes."""
+    check(load().aol_memcpy2d(C.c_void_p(dst), int(dpitch), C.c_void_p(src), int(spitch), int(width_bytes),
+                              int(height), C.c_void_p(int(stream))))
 
 
 def release_scratch() -> None:

@@ -108,4 +108,18 @@ int aol_ipc_close(void* dev_ptr) {
   return AOL_OK;
 }
 
+// Strided (2-D) asynchronous copy between host and device memory in either direction
+// (cudaMemcpy2DAsync, direction from the pointers): the GEMM's 2-D streamed path moves column
+// blocks of row-major B and C with it.  Pinned host memory for an asynchronous copy.
+int aol_memcpy2d(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width_bytes, int64_t height,
+                 void* stream) {
+  using namespace aol;
+  if (!dst || !src || width_bytes < 0 || height < 0 || dpitch < width_bytes || spitch < width_bytes)
+    return fail(AOL_EINVAL, "bad 2-D copy geometry");
+  if (width_bytes == 0 || height == 0) return AOL_OK;
+  AOL_CUDA_CHECK(cudaMemcpy2DAsync(dst, (size_t)dpitch, src, (size_t)spitch, (size_t)width_bytes, (size_t)height,
+                                   cudaMemcpyDefault, static_cast<cudaStream_t>(stream)));
+  return AOL_OK;
+}
+
 }  // extern "C"

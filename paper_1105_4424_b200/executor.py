@@ -121,6 +121,20 @@ class HostStager:
             self.events[i] = ev
 
 
+_SIDE_STREAMS: dict = {}
+
+
+def side_streams(device):
+    """Three streams per device (compute / upload / download) for the streamed paths, created
+    once: a new stream per call measurably stalled some calls (cudaStreamCreate)."""
+    torch = _torch()
+    key = torch.device(device).index
+    st = _SIDE_STREAMS.get(key)
+    if st is None:
+        st = _SIDE_STREAMS[key] = tuple(torch.cuda.Stream(torch.device("cuda", key)) for _ in range(3))
+    return st
+
+
 _STAGERS: dict = {}
 
 
@@ -456,6 +470,133 @@ class Executor:
         from .distributed import _port_tiler
         return _port_tiler(self, t, name)
 
+    def _run_streamed_gemm2d(self, step, t, out: dict | None) -> dict | None:
+        """C = A B streamed from PINNED host memory in an R x S grid of C blocks.
+
+        Row streaming (run_streamed) cannot compute any C row before all of B is resident, so
+        the download of C starts only after ~half of the upload.  Here B goes up in column
+        blocks (2-D copies, aol_memcpy2d) interleaved with the first row block of A, and block
+        C[i, j] = A[i, :] B[:, j] is launched as soon as its operands landed -- a derived task
+        over the same arrays whose tilers have the block's origin and repetition space (every
+        repetition is independent, so a sub-space is a valid launch; the TF32 kernel sees an
+        ordinary GEMM with offsets and leading dimensions) -- and downloaded with a 2-D copy
+        while the next blocks upload.  Canonical row-major GEMM tilers, pinned torch host
+        tensors and a single device only; returns None (nothing done) otherwise."""
+        from .builders import gemm_tilers
+        from .tiler import Tiler
+        torch = _torch()
+        st = self.storage
+        ta, tb, tc = (self._port_bound(t, n) for n in ("a", "b", "c"))
+        if len(tc.rep) != 2:
+            return None
+        M, N = (int(d) for d in tc.rep)
+        K = int(ta.tiler.pattern[-1])
+        canon = gemm_tilers(M, N, K)
+        if (ta.tiler, tb.tiler, tc.tiler) != (canon["a"], canon["b"], canon["c"]):
+            return None
+        if (tuple(ta.array), tuple(tb.array), tuple(tc.array)) != ((M, K), (K, N), (M, N)) or K % 4 or N % 4:
+            return None
+        if sum(l.range.count for l in step.launches) != M * N or M < 512 or N < 512:
+            return None
+        ga, gb = st.groups[t.nodes["a"]], st.groups[t.nodes["b"]]
+        if ga not in st.host or gb not in st.host:
+            return None
+        ha, hb = st.host[ga], st.host[gb]
+        if ha.dtype != torch.float32 or hb.dtype != torch.float32 or not (ha.is_pinned() and hb.is_pinned()):
+            return None
+        root = self.model.application_components[self.model.application_root]
+        yname = next((p.name for p in root.ports if enum_value(p.direction) == "out"), None)
+        if yname is None or st.groups[t.nodes["c"]] is not st.groups[yname]:
+            return None
+        if out is not None and yname in out:
+            hc = out[yname]
+            hc = torch.from_numpy(hc) if isinstance(hc, np.ndarray) else hc.view(-1)
+            if not hc.is_pinned() or hc.numel() != M * N or hc.dtype != torch.float32:
+                return None
+        else:
+            hc = torch.empty(M * N, dtype=torch.float32, pin_memory=True)
+
+        def cuts(n, parts):                  # block starts at multiples of 256 (whole tiles)
+            step_ = max(256, -(-n // parts) // 256 * 256)
+            return [(lo, min(step_, n - lo)) for lo in range(0, n, step_)]
+        # The first row block of C goes block by block as B's column blocks arrive (2-D copies);
+        # after that B is resident and the remaining rows go in full-width row chunks, so their
+        # uploads and downloads are contiguous; the last chunk is small, because everything
+        # downloaded after the last upload is pure tail.  Measured timelines
+        # (tools/probe_e2e_timeline.py, C2): four equal 2-D row blocks 11.7 ms; A/B blocks
+        # alternating with every C block 2-D 11.8 ms; this order 11.3 ms (row streaming: 11.5-11.8)
+        rows0, cols = cuts(M, 4)[0], cuts(N, 4)
+        r0 = int(os.environ.get("AOL_GEMM2D_ROWS0", "0"))          # diagnostic: first row block height
+        if r0 > 0:
+            rows0 = (0, min(M, max(256, r0 // 256 * 256)))
+        rest = []
+        lo = rows0[1]
+        while lo < M:
+            left = M - lo
+            n = min(left, 1024) if left > 1536 else (left if left <= 512 else left - 512)
+            rest.append((lo, n))
+            lo += n
+        if len(cols) < 2:
+            return None
+        A, B, Cd = st.arrays[ga], st.arrays[gb], st.array(yname)
+        pa, pb, pc = A.data_ptr(), B.data_ptr(), Cd.data_ptr()
+        caller = torch.cuda.current_stream(self.device) if self.stream is None else self.stream
+        comp, cin, cout = side_streams(self.device)
+        comp.wait_stream(caller)
+        cin.wait_stream(caller)              # uploads land after the storage's zero-fills
+        tl = [] if os.environ.get("AOL_E2E_TIMELINE") == "1" else None
+
+        def mark(tag, stream):
+            if tl is not None:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(stream)
+                tl.append((tag, e))
+
+        def block(i0, mi, j0, nj, tag):
+            ev = torch.cuda.Event()
+            ev.record(cin)
+            comp.wait_event(ev)
+            task = _capi.make_task("matmul", "float32", [
+                Tiler((i0, 0), ((1, 0), (0, 0)), ((0,), (1,)), (K,)).bind((M, K), (mi, nj)),
+                Tiler((0, j0), ((0, 0), (0, 1)), ((1,), (0,)), (K,)).bind((K, N), (mi, nj)),
+                Tiler((i0, j0), ((1, 0), (0, 1)), ((0,), (0,)), (1,)).bind((M, N), (mi, nj))],
+                precision=self.precision)
+            _capi.launch(task, 0, mi * nj, [pa, pb, pc], (), int(comp.cuda_stream))
+            mark(f"gemm {tag}", comp)
+            ev_done = torch.cuda.Event()
+            ev_done.record(comp)
+            cout.wait_event(ev_done)
+            if nj == N:
+                with torch.cuda.stream(cout):
+                    hc[i0 * N:(i0 + mi) * N].copy_(Cd[i0 * N:(i0 + mi) * N], non_blocking=True)
+            else:
+                _capi.memcpy2d(hc.data_ptr() + (i0 * N + j0) * esz, N * esz, pc + (i0 * N + j0) * esz, N * esz,
+                               nj * esz, mi, cout.cuda_stream)
+            mark(f"d2h {tag}", cout)
+        mark("start", cin)
+        esz = 4
+        i0, mi = rows0
+        with torch.cuda.stream(cin):
+            A[i0 * K:(i0 + mi) * K].copy_(ha[i0 * K:(i0 + mi) * K], non_blocking=True)
+        mark("h2d A0", cin)
+        for bj, (j0, nj) in enumerate(cols):
+            _capi.memcpy2d(pb + j0 * esz, N * esz, hb.data_ptr() + j0 * esz, N * esz, nj * esz, K, cin.cuda_stream)
+            mark(f"h2d B{bj}", cin)
+            block(i0, mi, j0, nj, f"C0{bj}")
+        for bi, (i0, mi) in enumerate(rest, start=1):
+            with torch.cuda.stream(cin):
+                A[i0 * K:(i0 + mi) * K].copy_(ha[i0 * K:(i0 + mi) * K], non_blocking=True)
+            mark(f"h2d A{bi}", cin)
+            block(i0, mi, 0, N, f"C{bi}")
+        cout.synchronize()
+        comp.synchronize()
+        caller.wait_stream(comp)
+        if tl is not None:
+            self.timeline = [(tag, tl[0][1].elapsed_time(e)) for tag, e in tl]
+        if out is not None and yname in out:
+            return {yname: out[yname]}
+        return {yname: hc.numpy()}
+
     def _upload_deferred(self) -> None:
         """Copy every deferred host binding to its device array (streaming fell through)."""
         st = self.storage
@@ -494,7 +635,7 @@ class Executor:
             self._fusable[(s1.task_path, s2.task_path)] = False
             return None
         comp = torch.cuda.current_stream(self.device) if self.stream is None else self.stream
-        cin, cout = torch.cuda.Stream(self.device), torch.cuda.Stream(self.device)
+        _, cin, cout = side_streams(self.device)
         cin.wait_stream(comp)            # uploads land after the storage's zero-fills
         # whole-array inputs (filter weights) first
         with torch.cuda.stream(cin):
@@ -575,9 +716,12 @@ class Executor:
             return self.outputs(out=out)
         step = steps[0]
         t = self.task(step.task_path)
+        if step.op == "matmul":
+            res = self._run_streamed_gemm2d(step, t, out)
+            if res is not None:
+                return res
         comp = torch.cuda.current_stream(self.device) if self.stream is None else self.stream
-        cin = torch.cuda.Stream(self.device)
-        cout = torch.cuda.Stream(self.device)
+        _, cin, cout = side_streams(self.device)
         cin.wait_stream(comp)            # uploads land after the storage's zero-fills
         st = self.storage
         arrays = {name: st.array(node) for name, node in t.nodes.items()}

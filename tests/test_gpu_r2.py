@@ -372,3 +372,35 @@ def test_ipc_abi_errors():
     host = np.zeros(16, np.float32)
     with pytest.raises(_capi.AolError):
         _capi.ipc_export(host.ctypes.data)
+
+
+# -- 2-D streamed MatMul from pinned host memory ------------------------------------------------
+
+@pytest.mark.parametrize("M,N,K,precision", [(2304, 2560, 512, "default"), (1024, 1024, 256, "exact"),
+                                             (4096, 4096, 1024, "default")])
+def test_streamed_gemm2d_equals_plain(M, N, K, precision):
+    """pipeline > 1 with pinned torch host tensors takes the 2-D block path (B and C moved in
+    column blocks by aol_memcpy2d, each C block a derived GEMM over the same arrays launched
+    as soon as its operands landed): bit-identical to the plain run (the same per-element
+    accumulation), and for precision="exact" to the oracle."""
+    from paper_1105_4424_b200 import builders
+    from paper_1105_4424_b200.executor import execute_schedule
+    from paper_1105_4424_b200.partition import build_schedule
+    model = builders.matmul_model(M, N, K)
+    sched = build_schedule(model, 1)
+    g = torch.Generator().manual_seed(M + N + K)
+    ha = torch.randn(M * K, generator=g).pin_memory()
+    hb = torch.randn(K * N, generator=g).pin_memory()
+    hc = torch.empty(M * N).pin_memory()
+    plain = execute_schedule(model, sched, {"p_a": ha.numpy(), "p_b": hb.numpy()}, 1,
+                             precision=precision).outputs["p_c"]
+    res = execute_schedule(model, sched, {"p_a": ha, "p_b": hb}, 1, precision=precision, pipeline=8,
+                           out={"p_c": hc})
+    assert res.outputs["p_c"] is hc
+    assert np.array_equal(hc.numpy().view(np.uint32), plain.view(np.uint32))
+    fresh = execute_schedule(model, sched, {"p_a": ha, "p_b": hb}, 1, precision=precision, pipeline=8).outputs["p_c"]
+    assert np.array_equal(fresh.view(np.uint32), plain.view(np.uint32))
+    if precision == "exact":
+        want = orc.run_tile_task("matmul", orc.gemm_tilers(M, N, K), {"a": ha.numpy(), "b": hb.numpy()},
+                                 {"c": (M * N, np.float32)}, M * N, 1)["c"]
+        assert np.array_equal(plain.view(np.uint32), want.view(np.uint32))
