@@ -38,6 +38,8 @@ bool gemm_tf32_applicable(const aol_task& t, void* const* ports);
 bool gemm_batched_applicable(const aol_task& t, void* const* ports);
 bool recognise_gemm_strides(const aol_task& t);
 int launch_gemm_exact(const aol_task& t, int64_t first, int64_t count, void* const* ports, cudaStream_t s);
+int launch_gemm_exact_batched(const aol_task& t, int64_t first, int64_t count, void* const* ports, cudaStream_t s);
+bool gemm_exact_batched_applicable(const aol_task& t);
 int launch_gemm_batched(const aol_task& t, int64_t first, int64_t count, void* const* ports, cudaStream_t s);
 int launch_fused_line_filters(const aol_task& th, const aol_task& tv, int64_t first, int64_t count,
                               void* const* ph, void* const* pv, cudaStream_t s);
@@ -97,7 +99,8 @@ static const char* plan_name(const aol_task* t, int64_t first, int64_t count, vo
         return t->precision == AOL_PREC_3XTF32 ? "matmul.tcgen05_3xtf32" : "matmul.tcgen05_tf32";
       if (ports && gemm_batched_applicable(*t, ports))
         return t->precision == AOL_PREC_3XTF32 ? "matmul.tcgen05_3xtf32_batched" : "matmul.tcgen05_tf32_batched";
-      return recognise_gemm_strides(*t) ? "matmul.exact_tiled" : "matmul.generic_exact";
+      if (recognise_gemm_strides(*t)) return "matmul.exact_tiled";
+      return gemm_exact_batched_applicable(*t) ? "matmul.exact_tiled_batched" : "matmul.generic_exact";
     case AOL_OP_TILE_FILTER: return filter_plan_name(*t);
     case AOL_OP_TILE_SUM: return tile_sum_plan_name(*t);
     default: return "identity";
@@ -149,6 +152,8 @@ int aol_launch(const aol_task* t, int64_t first, int64_t count, void* const* por
       {
         const int rc = launch_gemm_exact(*t, first, count, ports, s);   // canonical GEMM, exact order
         if (rc != AOL_EUNSUPPORTED) return rc;
+        const int rb = launch_gemm_exact_batched(*t, first, count, ports, s);
+        if (rb != AOL_EUNSUPPORTED) return rb;
       }
       return launch_matmul_generic(*t, first, count, ports, s);
     case AOL_OP_TILE_FILTER: return launch_filter_generic(*t, first, count, ports, s);

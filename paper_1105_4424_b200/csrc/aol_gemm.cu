@@ -1240,6 +1240,43 @@ int launch_gemm_batched(const aol_task& t, int64_t first, int64_t count, void* c
   return AOL_OK;
 }
 
+// Batched exact-order MatMul (precision="exact", repetition space [B..., M, N]): every slice
+// through the tiled exact kernel, bit-identical to the one-thread-per-repetition kernel (both
+// accumulate k = 0, 1, ... with the product and the sum rounded separately).  Returns
+// AOL_EUNSUPPORTED (nothing launched) when a slice is not a canonical GEMM.
+int launch_gemm_exact_batched(const aol_task& t, int64_t first, int64_t count, void* const* ports,
+                              cudaStream_t stream) {
+  const int q = t.tilers[0].rep_rank;
+  if (q < 3 || t.tilers[1].rep_rank != q || t.tilers[2].rep_rank != q) return AOL_EUNSUPPORTED;
+  int64_t nb = 1;
+  for (int j = 0; j < q - 2; ++j) nb *= t.tilers[0].rep[j];
+  aol_task s0, s1;
+  GemmStrides g0, g1;
+  if (!gemm_slice(t, 0, s0) || !gemm_slice(t, nb - 1, s1) || !recognise_gemm_strides(s0, g0) ||
+      !recognise_gemm_strides(s1, g1))
+    return AOL_EUNSUPPORTED;
+  const int64_t MN = t.tilers[0].rep[q - 2] * t.tilers[0].rep[q - 1];
+  for (int64_t b = first / MN; b * MN < first + count; ++b) {
+    const int64_t lo = std::max<int64_t>(first, b * MN), hi = std::min<int64_t>(first + count, (b + 1) * MN);
+    aol_task sl;
+    if (!gemm_slice(t, b, sl)) return fail(AOL_EINVAL, "batched matmul slice");
+    const int rc = launch_gemm_exact(sl, lo - b * MN, hi - lo, ports, stream);
+    if (rc) return rc;
+  }
+  return AOL_OK;
+}
+
+bool gemm_exact_batched_applicable(const aol_task& t) {
+  const int q = t.tilers[0].rep_rank;
+  if (q < 3 || t.tilers[1].rep_rank != q || t.tilers[2].rep_rank != q) return false;
+  int64_t nb = 1;
+  for (int j = 0; j < q - 2; ++j) nb *= t.tilers[0].rep[j];
+  aol_task s0, s1;
+  GemmStrides g0, g1;
+  return gemm_slice(t, 0, s0) && gemm_slice(t, nb - 1, s1) && recognise_gemm_strides(s0, g0) &&
+         recognise_gemm_strides(s1, g1);
+}
+
 // Split x into tf32 hi (low 13 mantissa bits cleared) and lo = x - hi (exact).
 __global__ void __launch_bounds__(256) k_split_a(const float* __restrict__ A, float* __restrict__ Ap, int64_t rows,
                                                  int64_t K, int64_t sm, int64_t sk, int64_t row0, int64_t pitch) {

@@ -1391,11 +1391,13 @@ def test_batched_matmul_tf32_within_bound(batch, devices):
     task = _capi.make_task("matmul", "float32", bt)
     t0 = torch.zeros(4, device="cuda")
     assert _capi.plan_name(task, 0, nb * M * N, [t0.data_ptr()] * 3) == "matmul.tcgen05_tf32_batched"
-    # exact mode keeps the bit-exact generic kernel
+    # exact mode: every slice through the tiled exact kernel, bit-exact against the oracle
     ex = _run_tile("matmul", {"a": ta, "b": tb, "c": tc}, ports, {"a": a, "b": b}, devices, precision="exact")
     ref = orc.run_tile_task("matmul", {"a": ta, "b": tb, "c": tc}, {"a": a, "b": b},
                             {"c": (nb * M * N, np.float32)}, nb * M * N, devices)["c"]
     assert np.array_equal(ex.outputs["p_c"], ref)
+    task_x = _capi.make_task("matmul", "float32", bt, precision="exact")
+    assert _capi.plan_name(task_x, 0, nb * M * N, [t0.data_ptr()] * 3) == "matmul.exact_tiled_batched"
 
 
 @pytest.mark.parametrize("shape,origin", [((100000,), (12345,)), ((300, 257), (299, 5)), ((40, 36, 52), (3, 35, 51)),
