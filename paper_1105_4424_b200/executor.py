@@ -102,6 +102,30 @@ class HostStager:
         with self.lock:
             self._copy_staged(dst, src, stream)
 
+    def copy2d(self, dst_ptr: int, dpitch: int, src, stream) -> None:
+        """Device rows dst_ptr + r * dpitch (bytes) <- host 2-D view src [rows, width] (any
+        strides; pageable or pinned): through the ring piece by piece (a piece = as many rows
+        as fit a slot, gathered contiguous on the host), each piece one aol_memcpy2d."""
+        torch = _torch()
+        rows, width = src.shape
+        wb = width * src.element_size()
+        if rows == 0 or wb == 0:
+            return
+        per = max(1, self.slot_bytes // wb)
+        with self.lock:
+            for r0 in range(0, rows, per):
+                m = min(per, rows - r0)
+                i = self.k % len(self.bufs)
+                self.k += 1
+                if self.events[i] is not None:
+                    self.events[i].synchronize()
+                buf = self.bufs[i][:m * wb].view(src.dtype).view(m, width)
+                buf.copy_(src[r0:r0 + m])
+                _capi.memcpy2d(dst_ptr + r0 * dpitch, dpitch, buf.data_ptr(), wb, wb, m, stream.cuda_stream)
+                ev = torch.cuda.Event()
+                ev.record(stream)
+                self.events[i] = ev
+
     def _copy_staged(self, dst, src, stream) -> None:
         torch = _torch()
         sb, db = src.view(torch.uint8), dst.view(torch.uint8)
@@ -481,7 +505,8 @@ class Executor:
         repetition is independent, so a sub-space is a valid launch; the TF32 kernel sees an
         ordinary GEMM with offsets and leading dimensions) -- and downloaded with a 2-D copy
         while the next blocks upload.  Canonical row-major GEMM tilers, pinned torch host
-        tensors and a single device only; returns None (nothing done) otherwise."""
+        (or pageable, through the staging ring) host tensors on a single device only; returns
+        None (nothing done) otherwise."""
         from .builders import gemm_tilers
         from .tiler import Tiler
         torch = _torch()
@@ -502,8 +527,11 @@ class Executor:
         if ga not in st.host or gb not in st.host:
             return None
         ha, hb = st.host[ga], st.host[gb]
-        if ha.dtype != torch.float32 or hb.dtype != torch.float32 or not (ha.is_pinned() and hb.is_pinned()):
+        if ha.dtype != torch.float32 or hb.dtype != torch.float32:
             return None
+        # pageable sources (numpy bindings, the reference's call) go through the pinned staging
+        # ring: A rows as contiguous pieces, B column blocks gathered piece by piece
+        stager = None if (ha.is_pinned() and hb.is_pinned()) else host_stager()
         root = self.model.application_components[self.model.application_root]
         yname = next((p.name for p in root.ports if enum_value(p.direction) == "out"), None)
         if yname is None or st.groups[t.nodes["c"]] is not st.groups[yname]:
@@ -515,6 +543,19 @@ class Executor:
                 return None
         else:
             hc = torch.empty(M * N, dtype=torch.float32, pin_memory=True)
+
+        def up_rows(i0, mi):
+            if stager is None:
+                with torch.cuda.stream(cin):
+                    A[i0 * K:(i0 + mi) * K].copy_(ha[i0 * K:(i0 + mi) * K], non_blocking=True)
+            else:
+                stager.copy(A[i0 * K:(i0 + mi) * K], ha[i0 * K:(i0 + mi) * K], cin)
+
+        def up_cols(j0, nj):
+            if stager is None:
+                _capi.memcpy2d(pb + j0 * esz, N * esz, hb.data_ptr() + j0 * esz, N * esz, nj * esz, K, cin.cuda_stream)
+            else:
+                stager.copy2d(pb + j0 * esz, N * esz, hb.view(K, N)[:, j0:j0 + nj], cin)
 
         def cuts(n, parts):                  # block starts at multiples of 256 (whole tiles)
             step_ = max(256, -(-n // parts) // 256 * 256)
@@ -576,16 +617,14 @@ class Executor:
         mark("start", cin)
         esz = 4
         i0, mi = rows0
-        with torch.cuda.stream(cin):
-            A[i0 * K:(i0 + mi) * K].copy_(ha[i0 * K:(i0 + mi) * K], non_blocking=True)
+        up_rows(i0, mi)
         mark("h2d A0", cin)
         for bj, (j0, nj) in enumerate(cols):
-            _capi.memcpy2d(pb + j0 * esz, N * esz, hb.data_ptr() + j0 * esz, N * esz, nj * esz, K, cin.cuda_stream)
+            up_cols(j0, nj)
             mark(f"h2d B{bj}", cin)
             block(i0, mi, j0, nj, f"C0{bj}")
         for bi, (i0, mi) in enumerate(rest, start=1):
-            with torch.cuda.stream(cin):
-                A[i0 * K:(i0 + mi) * K].copy_(ha[i0 * K:(i0 + mi) * K], non_blocking=True)
+            up_rows(i0, mi)
             mark(f"h2d A{bi}", cin)
             block(i0, mi, 0, N, f"C{bi}")
         cout.synchronize()

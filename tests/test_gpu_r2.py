@@ -400,6 +400,10 @@ def test_streamed_gemm2d_equals_plain(M, N, K, precision):
     assert np.array_equal(hc.numpy().view(np.uint32), plain.view(np.uint32))
     fresh = execute_schedule(model, sched, {"p_a": ha, "p_b": hb}, 1, precision=precision, pipeline=8).outputs["p_c"]
     assert np.array_equal(fresh.view(np.uint32), plain.view(np.uint32))
+    # pageable numpy sources (the reference's call) take the same path through the staging ring
+    na, nb = ha.numpy().copy(), hb.numpy().copy()
+    paged = execute_schedule(model, sched, {"p_a": na, "p_b": nb}, 1, precision=precision, pipeline=8).outputs["p_c"]
+    assert np.array_equal(paged.view(np.uint32), plain.view(np.uint32))
     if precision == "exact":
         want = orc.run_tile_task("matmul", orc.gemm_tilers(M, N, K), {"a": ha.numpy(), "b": hb.numpy()},
                                  {"c": (M * N, np.float32)}, M * N, 1)["c"]

@@ -21,9 +21,17 @@ hb = torch.randn(K * N, generator=g).pin_memory()
 hc = torch.empty(M * N).pin_memory()
 
 
+NUMPY = os.environ.get("PROBE_NUMPY") == "1"
+na, nb = ha.numpy().copy(), hb.numpy().copy()
+
+
 def call():
-    ex = Executor(model, sched, {"p_a": ha, "p_b": hb}, 1, pipeline=8)
-    ex.run_streamed({"p_c": hc})
+    if NUMPY:                                       # the reference's call: pageable in, fresh out
+        ex = Executor(model, sched, {"p_a": na, "p_b": nb}, 1, pipeline=8)
+        ex.run_streamed(None)
+    else:
+        ex = Executor(model, sched, {"p_a": ha, "p_b": hb}, 1, pipeline=8)
+        ex.run_streamed({"p_c": hc})
     return ex
 
 
