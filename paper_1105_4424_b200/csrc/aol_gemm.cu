@@ -43,6 +43,8 @@ struct Params {
   int64_t ldc;
   int64_t M, N, K;
   int64_t m_lo, m_hi;  // inclusive row range of this launch
+  int64_t row_base;    // first row of the tile grid: m_lo, aligned down to 32 rows when A is MN-major
+                       // (a TMA box starting off a 128 B swizzle atom faults: illegal instruction)
   int64_t first, last; // inclusive linear repetition range
   int m_tiles, n_tiles, k_blocks, num_tiles;
   int c_vec;           // 16-byte stores allowed
@@ -189,7 +191,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
         int mt, nt;
         tile_coords(p, tile, mt, nt);
-        const int row0 = (int)(p.m_lo + (int64_t)mt * BM), col0 = nt * BN;
+        const int row0 = (int)(p.row_base + (int64_t)mt * BM), col0 = nt * BN;
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
@@ -241,8 +243,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tile_coords(p, tile, mt, nt);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int64_t gm = p.m_lo + (int64_t)mt * BM + ew * 32 + lane;
-      const bool row_ok = gm <= p.m_hi && gm < p.M;
+      const int64_t gm = p.row_base + (int64_t)mt * BM + ew * 32 + lane;
+      const bool row_ok = gm >= p.m_lo && gm <= p.m_hi && gm < p.M;
       int64_t col_lo = 0, col_hi = p.N;
       if (gm == p.m_lo) col_lo = p.first - p.m_lo * p.N;
       if (gm == p.m_hi) col_hi = p.last - p.m_hi * p.N + 1;
@@ -440,13 +442,13 @@ __device__ __forceinline__ void store_chunk(const Params& p, float* epi, int ew,
 #pragma unroll
     for (int j = 0; j < 32; ++j) st[lane * EPI_PITCH + j] = v[j];
     __syncwarp();
-    const int64_t row0 = p.m_lo + (int64_t)mt * BM + rank * HALF_M + ew * 32;
+    const int64_t row0 = p.row_base + (int64_t)mt * BM + rank * HALF_M + ew * 32;
 #pragma unroll
     for (int rr = 0; rr < 32; rr += 4) {
       const int r = rr + (lane >> 3), cc = 4 * (lane & 7);
       const int64_t g = row0 + r;
       const float* sp = st + r * EPI_PITCH + cc;
-      if (g > p.m_hi || g >= p.M) continue;
+      if (g < p.m_lo || g > p.m_hi || g >= p.M) continue;
       int64_t lo = 0, hi = p.N;
       if (g == p.m_lo) lo = p.first - p.m_lo * p.N;
       if (g == p.m_hi) hi = p.last - p.m_hi * p.N + 1;
@@ -463,8 +465,8 @@ __device__ __forceinline__ void store_chunk(const Params& p, float* epi, int ew,
     __syncwarp();
     return;
   }
-  const int64_t gm = p.m_lo + (int64_t)mt * BM + rank * HALF_M + ew * 32 + lane;
-  if (!(gm <= p.m_hi && gm < p.M)) return;
+  const int64_t gm = p.row_base + (int64_t)mt * BM + rank * HALF_M + ew * 32 + lane;
+  if (!(gm >= p.m_lo && gm <= p.m_hi && gm < p.M)) return;
   int64_t col_lo = 0, col_hi = p.N;
   if (gm == p.m_lo) col_lo = p.first - p.m_lo * p.N;
   if (gm == p.m_hi) col_hi = p.last - p.m_hi * p.N + 1;
@@ -532,7 +534,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         int mt, tcol0, width;
         tile_geom<MIXED>(p, u.tile, mt, tcol0, width);
         const int half = MIXED ? width >> 1 : HALF_N;
-        const int row0 = (int)(p.m_lo + (int64_t)mt * BM) + (int)rank * HALF_M;
+        const int row0 = (int)(p.row_base + (int64_t)mt * BM) + (int)rank * HALF_M;
         const int col0 = tcol0 + (int)rank * half;
         const uint32_t b_bytes = (B_KMAJOR || !MIXED) ? (uint32_t)B_BYTES : (uint32_t)(half / 32) * (BK * 128);
         for (int kb = u.kb0; kb < u.kb1; ++kb) {
@@ -816,7 +818,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int tile = pair_id; tile < p.num_tiles; tile += num_pairs) {
         int mt, nt;
         pair::tile_coords_pair(p, tile, mt, nt);
-        const int row0 = (int)(p.m_lo + (int64_t)mt * BM) + (int)rank * HALF_M;
+        const int row0 = (int)(p.row_base + (int64_t)mt * BM) + (int)rank * HALF_M;
         const int col0 = nt * BN + (int)rank * HALF_N;
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
@@ -941,13 +943,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) st[lane * EPI_PITCH + j] = __uint_as_float(v[j]);
           __syncwarp();
-          const int64_t row0 = p.m_lo + (int64_t)mt * BM + rank * HALF_M + ew * 32;
+          const int64_t row0 = p.row_base + (int64_t)mt * BM + rank * HALF_M + ew * 32;
 #pragma unroll
           for (int rr = 0; rr < 32; rr += 4) {
             const int r = rr + (lane >> 3), cc = 4 * (lane & 7);
             const int64_t g = row0 + r;
             const float* sp = st + r * EPI_PITCH + cc;
-            if (g > p.m_hi || g >= p.M) continue;
+            if (g < p.m_lo || g > p.m_hi || g >= p.M) continue;
             int64_t lo = 0, hi = p.N;
             if (g == p.m_lo) lo = p.first - p.m_lo * p.N;
             if (g == p.m_hi) hi = p.last - p.m_hi * p.N + 1;
@@ -1527,7 +1529,8 @@ static int gemm_core(const float* A, const float* B, float* C, const GemmShape& 
   p.last = first + count - 1;
   p.m_lo = first / g.N;
   p.m_hi = p.last / g.N;
-  p.m_tiles = (int)((p.m_hi - p.m_lo + BM) / BM);
+  p.row_base = g.a_kmajor ? p.m_lo : (p.m_lo & ~int64_t(31));
+  p.m_tiles = (int)((p.m_hi - p.row_base + BM) / BM);
   p.n_tiles = (int)((g.N + BN - 1) / BN);
   p.k_blocks = (int)((g.K + BK - 1) / BK);
   p.num_tiles = p.m_tiles * p.n_tiles;
@@ -1549,7 +1552,7 @@ static int gemm_core(const float* A, const float* B, float* C, const GemmShape& 
     pp.group_m = gm_env > 0 ? gm_env : 8;
     static const char* epi_env = getenv("AOL_GEMM_EPI_SMEM");
     pp.epi_smem = epi_env ? (epi_env[0] != '0') : 1;
-    pp.m_tiles = (int)((p.m_hi - p.m_lo + pair::BM) / pair::BM);
+    pp.m_tiles = (int)((p.m_hi - p.row_base + pair::BM) / pair::BM);
     pp.n_tiles = (int)((g.N + pair::BN - 1) / pair::BN);
     pp.num_tiles = pp.m_tiles * pp.n_tiles;
     int sms2 = kNumSMs;
@@ -1636,7 +1639,8 @@ static int gemm_core_3x(const float* A, const float* B, float* C, const GemmShap
   p.last = first + count - 1;
   p.m_lo = first / g.N;
   p.m_hi = p.last / g.N;
-  p.m_tiles = (int)((p.m_hi - p.m_lo + x3::BM) / x3::BM);
+  p.row_base = g.a_kmajor ? p.m_lo : (p.m_lo & ~int64_t(31));
+  p.m_tiles = (int)((p.m_hi - p.row_base + x3::BM) / x3::BM);
   p.n_tiles = (int)((g.N + x3::BN - 1) / x3::BN);
   p.k_blocks = (int)((g.K + BK - 1) / BK);
   p.num_tiles = p.m_tiles * p.n_tiles;

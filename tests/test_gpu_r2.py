@@ -408,3 +408,22 @@ def test_streamed_gemm2d_equals_plain(M, N, K, precision):
         want = orc.run_tile_task("matmul", orc.gemm_tilers(M, N, K), {"a": ha.numpy(), "b": hb.numpy()},
                                  {"c": (M * N, np.float32)}, M * N, 1)["c"]
         assert np.array_equal(plain.view(np.uint32), want.view(np.uint32))
+
+
+@pytest.mark.parametrize("M,N,K,devices", [(2048, 264, 2048, 3), (2048, 1000, 512, 7), (1024, 520, 256, 5)])
+def test_matmul_mn_major_a_unaligned_shards(M, N, K, devices):
+    """MN-major A with shards that start mid-matrix (m_lo not a multiple of 32): the TF32 kernel
+    tiles from m_lo aligned down to a 128 B swizzle atom and masks the rows before m_lo
+    (a TMA box starting off the atom raised an illegal-instruction fault)."""
+    from paper_1105_4424_b200 import _capi, builders
+    from paper_1105_4424_b200.executor import execute_schedule
+    from paper_1105_4424_b200.partition import build_schedule
+    t, ports, bind, A, B = _gemm_case(M, N, K, True, False, M + N + K + devices)
+    model = builders.tile_task_model("matmul", ports, {k: _tiler(v) for k, v in t.items()}, (M, N))
+    sched = build_schedule(model, devices)
+    assert any((l.range.offset // N) % 32 for l in sched.device_steps()[0].launches)   # really unaligned
+    c = execute_schedule(model, sched, bind, devices).outputs["p_c"].reshape(M, N)
+    a64, b64 = A.astype(np.float64), B.astype(np.float64)
+    assert np.all(np.abs(c - a64 @ b64) <= (2.0 ** -9 + K * 2.0 ** -23) * (np.abs(a64) @ np.abs(b64)))
+    c3 = execute_schedule(model, sched, bind, devices, precision="3xtf32").outputs["p_c"].reshape(M, N)
+    assert np.linalg.norm(c3 - a64 @ b64) / np.linalg.norm(a64 @ b64) <= 1e-6
