@@ -41,13 +41,28 @@ for case in range(n_cases):
     if os.environ.get("STRESS_VERBOSE"):
         print(f"case {case}: M={M} N={N} K={K} D={D} a_mn={a_mn} b_k={b_k} split={os.environ.get('AOL_GEMM_SPLIT')} "
               f"narrow={os.environ['AOL_GEMM_NARROW']}", flush=True)
-    c1 = execute_schedule(model, sched, {"p_a": a_bind, "p_b": b_bind}, D).outputs["p_c"].reshape(M, N)
-    c2 = execute_schedule(model, sched, {"p_a": a_bind, "p_b": b_bind}, D).outputs["p_c"].reshape(M, N)
+    prec = str(rng.choice(["default", "default", "3xtf32", "exact"]))
+    if prec == "exact" and M * N * K > 2 ** 27:
+        prec = "default"
+    c1 = execute_schedule(model, sched, {"p_a": a_bind, "p_b": b_bind}, D, precision=prec).outputs["p_c"].reshape(M, N)
+    c2 = execute_schedule(model, sched, {"p_a": a_bind, "p_b": b_bind}, D, precision=prec).outputs["p_c"].reshape(M, N)
     a64, b64 = A.astype(np.float64), B.astype(np.float64)
-    bound = (2.0 ** -9 + K * 2.0 ** -23) * (np.abs(a64) @ np.abs(b64))
-    ok = np.all(np.abs(c1 - a64 @ b64) <= bound) and np.array_equal(c1.view(np.uint32), c2.view(np.uint32))
+    c64 = a64 @ b64
+    same = np.array_equal(c1.view(np.uint32), c2.view(np.uint32))
+    if prec == "default":
+        bound = (2.0 ** -9 + K * 2.0 ** -23) * (np.abs(a64) @ np.abs(b64))
+        ok = same and np.all(np.abs(c1 - c64) <= bound)
+    elif prec == "3xtf32":
+        ok = same and np.linalg.norm(c1 - c64) / np.linalg.norm(c64) <= 1e-6
+    else:                                   # the reference's k-ascending order, bit for bit
+        from oracle import aol_oracle as orc
+        tl = {"a": dict(array=a_arr, rep=(M, N), pattern=(K,), origin=ta.origin, paving=ta.paving, fitting=ta.fitting),
+              "b": dict(array=b_arr, rep=(M, N), pattern=(K,), origin=tb.origin, paving=tb.paving, fitting=tb.fitting),
+              "c": dict(array=(M, N), rep=(M, N), pattern=(1,), origin=tc.origin, paving=tc.paving, fitting=tc.fitting)}
+        ref = orc.run_tile_task("matmul", tl, {"a": a_bind, "b": b_bind}, {"c": (M * N, np.float32)}, M * N, D)["c"]
+        ok = same and np.array_equal(c1.ravel().view(np.uint32), ref.view(np.uint32))
     if not ok:
-        print(f"FAIL case {case}: M={M} N={N} K={K} D={D} a_mn={a_mn} b_k={b_k} "
+        print(f"FAIL case {case}: M={M} N={N} K={K} D={D} a_mn={a_mn} b_k={b_k} prec={prec} "
               f"split={os.environ.get('AOL_GEMM_SPLIT')} narrow={os.environ['AOL_GEMM_NARROW']}", flush=True)
         sys.exit(1)
     if case % 20 == 19:
