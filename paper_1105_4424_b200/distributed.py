@@ -843,8 +843,10 @@ class ShardedExecutor:
 
     def close(self) -> None:
         """Unmap the root's arrays (fused gather)."""
-        from . import _capi
         ptrs, self._ipc_ptrs = getattr(self, "_ipc_ptrs", []), []
+        if not ptrs:
+            return
+        from . import _capi
         for p in ptrs:
             try:
                 _capi.ipc_close(p)
@@ -852,7 +854,10 @@ class ShardedExecutor:
                 pass
 
     def __del__(self):
-        self.close()
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 - interpreter shutdown: nothing left to unmap into
+            pass
 
     def _upload_hulls(self) -> None:
         """Deferred host bindings: each rank uploads only the ranges it ever reads (its input
