@@ -377,7 +377,7 @@ def test_ipc_abi_errors():
 # -- 2-D streamed MatMul from pinned host memory ------------------------------------------------
 
 @pytest.mark.parametrize("M,N,K,precision", [(2304, 2560, 512, "default"), (1024, 1024, 256, "exact"),
-                                             (4096, 4096, 1024, "default")])
+                                             (4096, 4096, 1024, "default"), (1536, 2048, 512, "3xtf32")])
 def test_streamed_gemm2d_equals_plain(M, N, K, precision):
     """pipeline > 1 with pinned torch host tensors takes the 2-D block path (B and C moved in
     column blocks by aol_memcpy2d, each C block a derived GEMM over the same arrays launched
