@@ -81,7 +81,9 @@ typedef enum aol_op {
 typedef enum aol_precision {
   AOL_PREC_DEFAULT = 0,   /* matmul: TF32 tensor cores; everything else: exact order */
   AOL_PREC_TF32 = 1,      /* matmul on tcgen05 kind::tf32 (tolerance stated in DESIGN.md) */
-  AOL_PREC_3XTF32 = 2,    /* matmul on tcgen05 with hi/lo split, ~fp32 accuracy */
+  AOL_PREC_3XTF32 = 2,    /* matmul on tcgen05, hi/lo split, 3 products, K-chunked accumulation with
+                             round-to-nearest adds: 8.1e-7 normwise vs fp64 at 8192^3 (cuBLAS SIMT fp32:
+                             1.6e-6); stated bound (2^-20 + 2^-21 sqrt(K)) |A||B| per element */
   AOL_PREC_EXACT = 3      /* CUDA cores, pattern order, no FMA: bit-exact vs the oracle */
 } aol_precision;
 
