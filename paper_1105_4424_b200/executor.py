@@ -831,16 +831,22 @@ class Executor:
                     lo, hi = input_hull(bound[n], first, count)
                     hosts[rn][lo:hi].copy_(root_out[rn][lo:hi], non_blocking=True)
                     covered[n].append((lo, hi))
-        # elements no chunk wrote keep the zero initialisation (refexec.py:399-403)
+        # elements no chunk wrote keep the zero initialisation (refexec.py:399-403) -- or, for an
+        # inout group the caller bound, its bound values, which were uploaded only where a chunk
+        # read them: take those from the host source
         with torch.cuda.stream(cout):
             for n in out_ports:
                 rn = root_of.get(out_group[n])
                 if rn is None:
                     continue
+                bound_src = st.host.get(out_group[n])
                 pos = 0
                 for lo, hi in sorted(covered[n]) + [(root_out[rn].numel(), root_out[rn].numel())]:
                     if lo > pos:
-                        hosts[rn][pos:lo].copy_(root_out[rn][pos:lo], non_blocking=True)
+                        if bound_src is not None:
+                            hosts[rn][pos:lo].copy_(bound_src[pos:lo])
+                        else:
+                            hosts[rn][pos:lo].copy_(root_out[rn][pos:lo], non_blocking=True)
                     pos = max(pos, hi)
         cout.synchronize()
         comp.synchronize()

@@ -427,3 +427,28 @@ def test_matmul_mn_major_a_unaligned_shards(M, N, K, devices):
     assert np.all(np.abs(c - a64 @ b64) <= (2.0 ** -9 + K * 2.0 ** -23) * (np.abs(a64) @ np.abs(b64)))
     c3 = execute_schedule(model, sched, bind, devices, precision="3xtf32").outputs["p_c"].reshape(M, N)
     assert np.linalg.norm(c3 - a64 @ b64) / np.linalg.norm(a64 @ b64) <= 1e-6
+
+
+@pytest.mark.parametrize("chunks", [2, 5])
+def test_streamed_inout_keeps_bound_values_outside_the_repetitions(chunks):
+    """axpy with no `repeat` (repetition space 1: only element 0 is touched) on
+    999-element vectors: the streamed path uploads y only where a chunk reads it, so every other
+    element must come back as the caller's bound value, exactly as the plain run returns it."""
+    from paper_1105_4424_b200 import builders
+    from paper_1105_4424_b200.executor import execute_schedule
+    from paper_1105_4424_b200.partition import build_schedule
+    model = builders.single_task_model(
+        "axpy", ["y inout float64 [999]", "x in float64 [999]", "a in float64 [1]"],
+        ["i in float64 [999]", "v in float64 [999]", "s in float64 [1]", "o out float64 [999]"],
+        ["i -> t.y", "v -> t.x", "s -> t.a", "t.y -> o"],
+        ["allocate data i onto dev.gmem", "allocate data v onto dev.gmem", "allocate data s onto host.ram",
+         "allocate task t onto dev.cu"], None)
+    rng = np.random.default_rng(chunks)
+    bind = {"i": rng.standard_normal(999), "v": rng.standard_normal(999), "s": np.array([0.75])}
+    sched = build_schedule(model, 3)
+    plain = execute_schedule(model, sched, bind, 3).outputs["o"]
+    streamed = execute_schedule(model, sched, bind, 3, pipeline=chunks).outputs["o"]
+    want = bind["i"].copy()
+    want[0] += 0.75 * bind["v"][0]
+    assert np.array_equal(plain, want)
+    assert np.array_equal(streamed, want)
