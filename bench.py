@@ -732,18 +732,20 @@ class SweepWorkload(Workload):
                 b.record()
             torch.cuda.synchronize()
             return statistics.median(a.elapsed_time(b) for a, b in ev)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(steps):
+        # back to back, one event pair per launch (>= 0.1 ms launches: the pairs cost nothing),
+        # median -- a transient power-cap dip in one launch does not move the row
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+        ev[0].record()
+        for i in range(steps):
             fn()
-        e1.record()
-        e1.synchronize()
-        return e0.elapsed_time(e1) / steps
+            ev[i + 1].record()
+        ev[-1].synchronize()
+        return statistics.median(ev[i].elapsed_time(ev[i + 1]) for i in range(steps))
 
     def measure_points(self, steps=10, warmup=3):
         """Per-point table.  Points whose footprint is below 3x the L2 are timed launch by
         launch with an L2 flush before each launch (outside its event pair, median of the
-        launches); larger points are timed back to back.  Each row carries its DRAM line floor
+        launches); larger points are timed back to back (median of per-launch event pairs).  Each row carries its DRAM line floor
         (floor_frac = floor bytes / time / peak), a device-to-device copy of the same floor
         bytes timed the same way (the achievable rate at that size: frac_of_copy), and the ncu
         DRAM bytes of the same point from profiles/r2_sweep_dram.json when it was captured."""
