@@ -126,6 +126,35 @@ class HostStager:
                 ev.record(stream)
                 self.events[i] = ev
 
+    def download(self, dst, src, stream) -> None:
+        """dst[:] = src (1-D, same dtype): src on the device, dst in pageable host memory.
+        Piece k is DMA'd into slot k mod R on ``stream`` (after everything already queued
+        there) while the host copies piece k-1 out of its slot; returns when dst is complete."""
+        torch = _torch()
+        sb, db = src.view(torch.uint8), dst.view(torch.uint8)
+        n = sb.numel()
+        with self.lock:
+            prev = None
+            for off in range(0, n, self.slot_bytes):
+                m = min(self.slot_bytes, n - off)
+                i = self.k % len(self.bufs)
+                self.k += 1
+                if self.events[i] is not None:
+                    self.events[i].synchronize()
+                buf = self.bufs[i][:m]
+                with torch.cuda.stream(stream):
+                    buf.copy_(sb[off:off + m], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(stream)
+                self.events[i] = ev
+                if prev is not None:
+                    prev[0].synchronize()
+                    db[prev[2]:prev[2] + prev[1].numel()].copy_(prev[1])
+                prev = (ev, buf, off)
+            if prev is not None:
+                prev[0].synchronize()
+                db[prev[2]:prev[2] + prev[1].numel()].copy_(prev[1])
+
     def _copy_staged(self, dst, src, stream) -> None:
         torch = _torch()
         sb, db = src.view(torch.uint8), dst.view(torch.uint8)
@@ -1114,6 +1143,8 @@ class Executor:
         with self._device_ctx():
             self.run_steps(self.schedule.steps, tol, max_iter)
 
+    PINNED_OUTPUT_BYTES = 64 << 20
+
     def outputs(self, on_device: bool = False, out: dict | None = None) -> dict:
         """Root out-port arrays, flat row-major (refexec.py:545-547).
 
@@ -1142,8 +1173,21 @@ class Executor:
                 host.view(-1).copy_(t, non_blocking=True)
                 pending = True
                 res[port.name] = dst
+            elif on_device:
+                res[port.name] = t.clone()
+            elif t.numel() * t.element_size() <= self.PINNED_OUTPUT_BYTES:
+                # a DMA from the device into pageable memory is staged by the driver piece by
+                # piece (~2x slower than into pinned memory at 0.25-4 MB,
+                # tools/probe_small_copies.py); small outputs land in a block of torch's
+                # caching pinned allocator, handed to the caller as the numpy array's base
+                host = torch.empty(t.numel(), dtype=t.dtype, pin_memory=True)
+                host.copy_(t, non_blocking=True)
+                pending = True
+                res[port.name] = host.numpy()
             else:
-                res[port.name] = t.clone() if on_device else t.cpu().numpy()
+                host = torch.empty(t.numel(), dtype=t.dtype)
+                host_stager().download(host, t.reshape(-1), torch.cuda.current_stream(self.device))
+                res[port.name] = host.numpy()
         if pending:
             torch.cuda.current_stream(self.device).synchronize()
         return res

@@ -452,3 +452,35 @@ def test_streamed_inout_keeps_bound_values_outside_the_repetitions(chunks):
     want[0] += 0.75 * bind["v"][0]
     assert np.array_equal(plain, want)
     assert np.array_equal(streamed, want)
+
+
+@pytest.mark.parametrize("n", [1, 1000, 4096, 100_003])
+def test_host_stager_download_pieces(n):
+    """HostStager.download through a 4 KiB x 2-slot ring: pieces alternate slots, the host copy
+    of piece k overlaps the DMA of piece k+1, the result equals the device data bit for bit."""
+    import torch
+    from paper_1105_4424_b200.executor import HostStager
+    st = HostStager(slot_bytes=4096, slots=2)
+    src = torch.randn(n, device="cuda", dtype=torch.float32)
+    dst = torch.empty(n, dtype=torch.float32)
+    st.download(dst, src, torch.cuda.current_stream())
+    assert torch.equal(dst, src.cpu())
+
+
+def test_numpy_outputs_pinned_and_staged_forms(monkeypatch):
+    """Numpy outputs come back through a pinned block (small) or the staging ring (large):
+    both forms equal the device-resident result."""
+    from paper_1105_4424_b200 import builders
+    from paper_1105_4424_b200.executor import Executor, execute_schedule
+    from paper_1105_4424_b200.partition import build_schedule
+    n = 192
+    model = builders.matmul_model(n, n, n)
+    sched = build_schedule(model, 2)
+    rng = np.random.default_rng(0)
+    bind = {"p_a": rng.standard_normal(n * n, dtype=np.float32), "p_b": rng.standard_normal(n * n, dtype=np.float32)}
+    dev = execute_schedule(model, sched, bind, 2, device_outputs=True).outputs["p_c"].cpu().numpy()
+    pinned = execute_schedule(model, sched, bind, 2).outputs["p_c"]
+    assert isinstance(pinned, np.ndarray) and np.array_equal(pinned, dev)
+    monkeypatch.setattr(Executor, "PINNED_OUTPUT_BYTES", 0)
+    staged = execute_schedule(model, sched, bind, 2).outputs["p_c"]
+    assert isinstance(staged, np.ndarray) and np.array_equal(staged, dev)
