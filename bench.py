@@ -466,6 +466,13 @@ class MatmulWorkload(Workload):
         ex3 = Executor(self.model, self.schedule, {"p_a": a, "p_b": b}, 1, precision="3xtf32")
         ms3 = timed(ex3.run)
         err3 = err(ex3.outputs(on_device=True)["p_c"])
+        # the same kernel with 128-deep K chunks (half the accumulator hand-offs, wider error)
+        os.environ["AOL_3XTF32_CHUNK"] = "128"
+        try:
+            ms3_128 = timed(ex3.run)
+            err3_128 = err(ex3.outputs(on_device=True)["p_c"])
+        finally:
+            os.environ.pop("AOL_3XTF32_CHUNK", None)
         del ex3
         err_tf32 = err(self.ex.outputs(on_device=True)["p_c"])
         prev = torch.backends.cuda.matmul.allow_tf32
@@ -479,8 +486,12 @@ class MatmulWorkload(Workload):
         flop = 2.0 * M * N * K
         return {"precision": "3xtf32", "value": flop / (ms3 * 1e-3) / 1e12, "unit": "TFLOP/s", "ms": ms3,
                 "normwise_vs_fp64": err3, "normwise_tf32_default": err_tf32,
-                "kernel": "k_gemm_3xtf32_pair (hi/lo split in shared memory, 3 tcgen05 products per k-slice, "
-                          "64-deep TMEM chunks summed with round-to-nearest adds)",
+                "kernel": ("k_gemm_3xtf32_pair (256x128 pair tiles" if os.environ.get("AOL_3XTF32_WIDE") == "0"
+                           else "k_gemm_3xtf32_wide (256x256 pair tiles") +
+                          ": hi/lo split in shared memory, 3 tcgen05 products per k-slice, 64-deep TMEM chunks "
+                          "summed with round-to-nearest adds)",
+                "chunk128": {"value": flop / (ms3_128 * 1e-3) / 1e12, "ms": ms3_128, "normwise_vs_fp64": err3_128,
+                             "switch": "AOL_3XTF32_CHUNK=128"},
                 "cublas_fp32_simt": {"value": flop / (ms_simt * 1e-3) / 1e12, "ms": ms_simt,
                                      "normwise_vs_fp64": err_simt}}
 

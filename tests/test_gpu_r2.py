@@ -484,3 +484,35 @@ def test_numpy_outputs_pinned_and_staged_forms(monkeypatch):
     monkeypatch.setattr(Executor, "PINNED_OUTPUT_BYTES", 0)
     staged = execute_schedule(model, sched, bind, 2).outputs["p_c"]
     assert isinstance(staged, np.ndarray) and np.array_equal(staged, dev)
+
+
+_X3_FORM_SCRIPT = """
+import sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_1105_4424_b200 import builders
+from paper_1105_4424_b200.executor import execute_schedule
+from paper_1105_4424_b200.partition import build_schedule
+M, N, K, D = 300, 520, 1000, 3
+rng = np.random.default_rng(5)
+bind = {"p_a": rng.standard_normal(M * K, dtype=np.float32), "p_b": rng.standard_normal(K * N, dtype=np.float32)}
+model = builders.matmul_model(M, N, K)
+np.save(sys.argv[2], execute_schedule(model, build_schedule(model, D), bind, D, precision="3xtf32").outputs["p_c"])
+"""
+
+
+def test_matmul_3xtf32_wide_equals_narrow_form(tmp_path):
+    """The 256x256-tile 3xTF32 kernel (default) and the 256x128 form (AOL_3XTF32_WIDE=0, read once
+    per process) use the same 64-deep chunks and add order: bit-identical C on unaligned shards."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = str(Path(__file__).resolve().parent.parent)
+    outs = {}
+    for form, env in (("wide", {}), ("narrow", {"AOL_3XTF32_WIDE": "0"})):
+        out = tmp_path / f"{form}.npy"
+        subprocess.run([sys.executable, "-c", _X3_FORM_SCRIPT, root, str(out)],
+                       env={**os.environ, **env}, check=True, timeout=300)
+        outs[form] = np.load(out)
+    assert np.array_equal(outs["wide"], outs["narrow"])
