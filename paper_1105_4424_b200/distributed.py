@@ -764,6 +764,8 @@ class ShardedExecutor:
     run as device scalar kernels on every rank, so a CG iteration syncs the host once, for
     the loop test (refexec.py:525-541).  Outputs are gathered to the root (rank 0)."""
 
+    _SKIP_COVERED_ZERO = False          # each replica writes only its launches' slice
+
     def _init_sharded(self, transport, replicas: list, world: int, bindings: dict | None = None,
                       fused_gather: bool | None = None):
         self.transport = transport

@@ -233,12 +233,55 @@ def storage_layout(model) -> StorageLayout:
     return model_memo(model, "storage_layout", StorageLayout)
 
 
+def _covered_outputs(model) -> frozenset:
+    """Port groups that no task reads and exactly one tile task writes, through an output tiler
+    that is injective (checked at validation) with repetition x pattern == array elements: a
+    bijection, so the schedule's launches (which cover the whole repetition space) write every
+    element and the reference's zero-fill of the group (refexec.py:399-403) is dead work."""
+    lay = storage_layout(model)
+    writers: dict = {}
+    readers: set = set()
+    for path, comp in iter_app_instances(model):
+        if not path or comp.elementary_op is None:
+            continue
+        for port in comp.ports:
+            g = lay.groups.get(f"{path}.{port.name}")
+            d = enum_value(port.direction)
+            if d in ("in", "inout"):
+                readers.add(g)
+            if d in ("out", "inout"):
+                writers.setdefault(g, []).append((path, comp, port))
+    covered = set()
+    for g, ws in writers.items():
+        if g in readers or len(ws) != 1:
+            continue
+        path, comp, port = ws[0]
+        spec = INTRINSICS.get(comp.elementary_op)
+        if spec is None or not spec.tile:
+            continue
+        try:
+            bound = check_tile_signature(path, comp, spec, None)
+        except Exception:                      # invalid task: the run reports it, zero-fill stays
+            continue
+        b = bound.get(port.name)
+        if b is not None and b.rep_total * b.pattern_total == b.array_total == port.shape.total:
+            covered.add(g)
+    return frozenset(covered)
+
+
+def covered_outputs(model) -> frozenset:
+    from .model import model_memo
+    return model_memo(model, "covered_outputs", _covered_outputs)
+
+
 class DeviceStorage:
     """Arrays per connected-port group, resident on one CUDA device (refexec.py:375-412)."""
 
-    def __init__(self, model, bindings: dict, device, stream=None, defer: bool = False):
+    def __init__(self, model, bindings: dict, device, stream=None, defer: bool = False,
+                 skip_zero: frozenset = frozenset()):
         """``defer``: allocate device arrays for host bindings but do not copy them; the
-        streamed path uploads each chunk's input hull itself (``self.host`` keeps the sources)."""
+        streamed path uploads each chunk's input hull itself (``self.host`` keeps the sources).
+        ``skip_zero``: placed groups the run writes completely (covered_outputs), not zero-filled."""
         torch = _torch()
         lay = storage_layout(model)
         self.host: dict = {}
@@ -305,7 +348,7 @@ class DeviceStorage:
             self.arrays[self.groups[port.name]] = t
             bound.add(self.groups[port.name])
         for g in lay.arena_views:
-            if g not in bound:
+            if g not in bound and g not in skip_zero:
                 self.arrays[g].zero_()
         for g, (n, tdt) in lay.zero_groups.items():
             if g not in self.arrays:
@@ -381,6 +424,8 @@ class Executor:
     """Prepared schedule: storage resident in HBM, tasks validated, ready to run repeatedly."""
 
     _STREAMABLE_REF_OPS = ("copy", "sub", "scale", "axpy")
+    # single-device runs write a covered output whole; sharded replicas each write a slice
+    _SKIP_COVERED_ZERO = True
 
     def __init__(self, model, schedule, bindings: dict, device_count: int, *, tilers: dict | None = None,
                  precision: str = "default", device=None, stream=None, pipeline: int = 0, fuse: bool = True,
@@ -412,7 +457,9 @@ class Executor:
                 and steps[0].op in FILTER_OPS and steps[1].op in FILTER_OPS)
         self.pipeline = pipeline if (pipeline > 1 and (single or pair)) else 0
         with self._device_ctx():
-            self.storage = DeviceStorage(model, bindings, self.device, stream, defer=defer or bool(self.pipeline))
+            skip = covered_outputs(model) if (self._SKIP_COVERED_ZERO and not self.tilers) else frozenset()
+            self.storage = DeviceStorage(model, bindings, self.device, stream, defer=defer or bool(self.pipeline),
+                                         skip_zero=skip)
         self._tasks: dict[str, _Task] = {}
         self.fuse = fuse
         self.graphs = graphs
