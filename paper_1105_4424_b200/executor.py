@@ -300,6 +300,20 @@ class DeviceStorage:
                        for mem, nbytes in lay.arenas.items()}
         for g, (mem, lo, hi, tdt) in lay.arena_views.items():
             self.arrays[g] = self.arenas[mem][lo:hi].view(tdt)
+        self.device = device
+        self._standalone_zero: set = set()
+        self._fill(model, bindings, device, defer, skip_zero)
+
+    def rebind(self, model, bindings: dict, skip_zero: frozenset = frozenset()) -> None:
+        """Refill the same arrays for a new call (the prepared-executor cache): bound inputs are
+        copied in, every other group is zeroed again exactly as a fresh storage would be."""
+        self.host = {}
+        self.h2d_bytes = 0
+        self._fill(model, bindings, self.device, False, skip_zero)
+
+    def _fill(self, model, bindings: dict, device, defer: bool, skip_zero: frozenset) -> None:
+        torch = _torch()
+        lay = storage_layout(model)
         bound: set = set()
         root = model.application_components[model.application_root]
         for port in root.ports:
@@ -353,6 +367,9 @@ class DeviceStorage:
         for g, (n, tdt) in lay.zero_groups.items():
             if g not in self.arrays:
                 self.arrays[g] = torch.zeros(n, dtype=tdt, device=device)
+                self._standalone_zero.add(g)
+            elif g in self._standalone_zero and g not in bound:
+                self.arrays[g].zero_()
 
     def array(self, node: str):
         return self.arrays[self.groups[node]]
@@ -473,6 +490,16 @@ class Executor:
         self._fusable: dict[tuple, bool] = {}
         self.fused_launches = 0
         self._dot_buf = None
+        self.iterations = 0
+        self.final_relres = None
+        self.converged = True
+
+    def rebind(self, bindings: dict) -> None:
+        """Prepare this executor for another call on new bindings (execute_schedule's prepared
+        executor cache): same storage, inputs copied in, everything else reset as when fresh."""
+        skip = covered_outputs(self.model) if (self._SKIP_COVERED_ZERO and not self.tilers) else frozenset()
+        with self._device_ctx():
+            self.storage.rebind(self.model, bindings, skip)
         self.iterations = 0
         self.final_relres = None
         self.converged = True
@@ -1240,6 +1267,62 @@ class Executor:
         return res
 
 
+# Prepared-executor cache: repeated small calls on the same (model, schedule) -- the C1 regime,
+# where building the storage and validating tasks costs more than the kernels -- reuse one
+# Executor: its HBM arena is refilled (inputs copied, other groups zeroed as when fresh) and the
+# outputs are always copied out (clone / host copy), so no call sees another's data.  Only
+# schedules of device steps, arenas up to AOL_PREPARED_ARENA_MB (default 64), at most
+# AOL_PREPARED_MAX entries (default 8, 0 disables); a busy entry (another thread) is bypassed.
+_PREPARED: dict = {}
+_PREPARED_MAX = int(os.environ.get("AOL_PREPARED_MAX", "8"))
+_PREPARED_ARENA = int(os.environ.get("AOL_PREPARED_ARENA_MB", "64")) << 20
+
+
+def _prepared_executor(model, schedule, bindings, device_count, precision, device, fuse, graphs):
+    """(executor rebound to ``bindings``, its held lock), or None (not cacheable / busy)."""
+    import threading
+    import weakref
+    torch = _torch()
+    if not torch.cuda.is_available():
+        return None
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    if sum(storage_layout(model).arenas.values()) > _PREPARED_ARENA:
+        return None
+    key = (id(model), id(schedule), device_count, precision, str(dev), fuse, graphs)
+    ent = _PREPARED.get(key)
+    if ent is not None and (ent[0]() is not model or ent[1]() is not schedule):
+        _PREPARED.pop(key, None)                 # ids reused by new objects
+        ent = None
+    if ent is None:
+        try:
+            mref, sref = weakref.ref(model), weakref.ref(schedule)
+        except TypeError:
+            return None
+        ex = Executor(model, schedule, bindings, device_count, precision=precision, device=dev, fuse=fuse,
+                      graphs=graphs)
+        lock = threading.Lock()
+        lock.acquire()
+        if len(_PREPARED) >= _PREPARED_MAX:
+            _PREPARED.pop(next(iter(_PREPARED)))
+        _PREPARED[key] = (mref, sref, ex, lock)
+        return ex, lock
+    _, _, ex, lock = ent
+    if not lock.acquire(blocking=False):
+        return None
+    try:
+        ex.rebind(bindings)
+    except BaseException:
+        lock.release()
+        raise
+    _PREPARED[key] = _PREPARED.pop(key)          # most recently used last
+    return ex, lock
+
+
+def clear_prepared() -> None:
+    """Drop every cached prepared executor (frees their HBM arenas)."""
+    _PREPARED.clear()
+
+
 def _default_devices(device_count: int, device, pipeline: int):
     """Launch d of a step goes to cuda:(d mod P) when P > 1 GPUs are visible (P = min(D, visible));
     None keeps every launch on one device (one GPU, an explicit ``device``, the streamed path,
@@ -1273,6 +1356,19 @@ def execute_schedule(model, schedule, bindings: dict, device_count: int, tol: fl
                                    precision=precision, stream=stream, fuse=fuse)
         ex.run(tol, max_iter)
         outs = ex.outputs(on_device=device_outputs, out=out)
+        return ExecutionResult(outputs=outs, iterations=ex.iterations, final_relres=ex.final_relres,
+                               converged=ex.converged)
+    prepared = None
+    if (stream is None and tilers is None and not pipeline and _PREPARED_MAX > 0
+            and all(hasattr(st, "launches") for st in schedule.steps)):
+        prepared = _prepared_executor(model, schedule, bindings, device_count, precision, device, fuse, graphs)
+    if prepared is not None:
+        ex, lock = prepared
+        try:
+            ex.run(tol, max_iter)
+            outs = ex.outputs(on_device=device_outputs, out=out)
+        finally:
+            lock.release()
         return ExecutionResult(outputs=outs, iterations=ex.iterations, final_relres=ex.final_relres,
                                converged=ex.converged)
     ex = Executor(model, schedule, bindings, device_count, tilers=tilers, precision=precision,
