@@ -516,3 +516,66 @@ def test_matmul_3xtf32_wide_equals_narrow_form(tmp_path):
                        env={**os.environ, **env}, check=True, timeout=300)
         outs[form] = np.load(out)
     assert np.array_equal(outs["wide"], outs["narrow"])
+
+
+def test_prepared_executor_reuse_is_isolated():
+    """Repeated calls on one (model, schedule) reuse a prepared executor: results follow each
+    call's bindings, device outputs from an earlier call are not overwritten by a later one,
+    and a partially written output (gaps) keeps zeros outside the written elements."""
+    import torch
+    from paper_1105_4424_b200 import Tiler, builders
+    from paper_1105_4424_b200 import executor as exm
+    from paper_1105_4424_b200.partition import build_schedule
+    n = 96
+    model = builders.matmul_model(n, n, n)
+    sched = build_schedule(model, 2)
+    rng = np.random.default_rng(1)
+    exm.clear_prepared()
+    results, devs = [], []
+    for i in range(4):
+        a = rng.standard_normal(n * n, dtype=np.float32)
+        b = rng.standard_normal(n * n, dtype=np.float32)
+        want = exm.execute_schedule(model, sched, {"p_a": a, "p_b": b}, 2, precision="exact").outputs["p_c"]
+        dev = exm.execute_schedule(model, sched, {"p_a": torch.from_numpy(a).cuda(), "p_b": torch.from_numpy(b).cuda()},
+                                   2, precision="exact", device_outputs=True).outputs["p_c"]
+        results.append(want)
+        devs.append(dev)
+    assert any(k[0] == id(model) for k in exm._PREPARED)
+    for want, dev in zip(results, devs):
+        assert np.array_equal(dev.cpu().numpy(), want)
+    assert not np.array_equal(results[0], results[1])
+    # gaps: dst written at every other element, the rest must read back zero on every call
+    T = 1000
+    src = Tiler((0,), ((1,),), ((1,),), (1,))
+    dst = Tiler((0,), ((2,),), ((1,),), (1,))
+    gm = builders.tile_task_model("tile_copy", {"src": f"in float32 [{T}]", "dst": f"out float32 [{2 * T}]"},
+                                  {"src": src, "dst": dst}, (T,))
+    gs = build_schedule(gm, 3)
+    for i in range(3):
+        x = rng.standard_normal(T).astype(np.float32) + 10.0
+        y = exm.execute_schedule(gm, gs, {"p_src": x}, 3).outputs["p_dst"]
+        assert np.array_equal(y[0::2], x) and not y[1::2].any()
+    exm.clear_prepared()
+
+
+def test_prepared_executor_busy_entry_is_bypassed():
+    """A call that finds the cached executor in use (another thread) builds its own."""
+    from paper_1105_4424_b200 import builders
+    from paper_1105_4424_b200 import executor as exm
+    from paper_1105_4424_b200.partition import build_schedule
+    n = 64
+    model = builders.matmul_model(n, n, n)
+    sched = build_schedule(model, 1)
+    rng = np.random.default_rng(2)
+    a = rng.standard_normal(n * n, dtype=np.float32)
+    b = rng.standard_normal(n * n, dtype=np.float32)
+    exm.clear_prepared()
+    first = exm.execute_schedule(model, sched, {"p_a": a, "p_b": b}, 1, precision="exact").outputs["p_c"]
+    (_, _, _, lock), = exm._PREPARED.values()
+    assert lock.acquire(blocking=False)                  # simulate a concurrent user
+    try:
+        again = exm.execute_schedule(model, sched, {"p_a": a, "p_b": b}, 1, precision="exact").outputs["p_c"]
+    finally:
+        lock.release()
+    assert np.array_equal(first, again)
+    exm.clear_prepared()
