@@ -1486,6 +1486,15 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
+    # every host thread this process may use: torchrun exports OMP_NUM_THREADS=1 to each rank,
+    # which would leave numpy's OpenBLAS and the OpenMP C port on one core at N > 1
+    n_cpu = len(os.sched_getaffinity(0))
+    os.environ["OMP_NUM_THREADS"] = str(n_cpu)          # read when the C port's OpenMP starts
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(limits=n_cpu)                  # BLAS / OpenMP pools already loaded
+    except Exception:                                    # noqa: BLE001 -- env var still applies
+        pass
     sys.path.insert(0, str(ROOT))
     step, unit, sample, cores = _reference_arm(args.workload)
     for i in range(args.warmup):
