@@ -1200,6 +1200,11 @@ def run_gpu(args):
     _capi.load()
     all_cpus = os.sched_getaffinity(0)
     numa = bind_host_to_gpu_numa(torch, local)
+    if world > 1:
+        # torchrun exports OMP_NUM_THREADS=1; give each rank its share of the host cores for the
+        # host-side copies of the e2e forms (pinned staging of numpy inputs)
+        lws = max(1, int(os.environ.get("LOCAL_WORLD_SIZE", world)))
+        torch.set_num_threads(max(1, min(len(os.sched_getaffinity(0)), len(all_cpus) // lws)))
     t_start = time.perf_counter()
 
     def phase(name):
