@@ -1217,7 +1217,9 @@ class Executor:
         with self._device_ctx():
             self.run_steps(self.schedule.steps, tol, max_iter)
 
-    PINNED_OUTPUT_BYTES = 64 << 20
+    # numpy outputs up to this size come back in pinned blocks (the caller keeps them: a cap on
+    # how much page-locked memory results can pin); larger ones go through the staging ring
+    PINNED_OUTPUT_BYTES = 8 << 20
 
     def outputs(self, on_device: bool = False, out: dict | None = None) -> dict:
         """Root out-port arrays, flat row-major (refexec.py:545-547).
