@@ -271,6 +271,14 @@ def _spec(d, direction):
     return f"{direction} float32 [{','.join(str(x) for x in d['array'])}]"
 
 
+def _x3_form() -> str:
+    """The 3xTF32 kernel form the library picks (aol_gemm.cu gemm_core_3x)."""
+    f = os.environ.get("AOL_3XTF32_FORM")
+    if f in ("narrow", "wide", "regs"):
+        return f
+    return "narrow" if os.environ.get("AOL_3XTF32_WIDE") == "0" else "regs"
+
+
 class Workload:
     """One repetitive-task schedule prepared in HBM; step() = one pass over one batch.
 
@@ -466,11 +474,11 @@ class MatmulWorkload(Workload):
         ex3 = Executor(self.model, self.schedule, {"p_a": a, "p_b": b}, 1, precision="3xtf32")
         ms3 = timed(ex3.run)
         err3 = err(ex3.outputs(on_device=True)["p_c"])
-        # the same kernel with 128-deep K chunks (half the accumulator hand-offs, wider error)
-        os.environ["AOL_3XTF32_CHUNK"] = "128"
+        # the same kernel with 32-deep K chunks (a fold every k-block: tighter error, slower)
+        os.environ["AOL_3XTF32_CHUNK"] = "32"
         try:
-            ms3_128 = timed(ex3.run)
-            err3_128 = err(ex3.outputs(on_device=True)["p_c"])
+            ms3_32 = timed(ex3.run)
+            err3_32 = err(ex3.outputs(on_device=True)["p_c"])
         finally:
             os.environ.pop("AOL_3XTF32_CHUNK", None)
         del ex3
@@ -486,12 +494,14 @@ class MatmulWorkload(Workload):
         flop = 2.0 * M * N * K
         return {"precision": "3xtf32", "value": flop / (ms3 * 1e-3) / 1e12, "unit": "TFLOP/s", "ms": ms3,
                 "normwise_vs_fp64": err3, "normwise_tf32_default": err_tf32,
-                "kernel": ("k_gemm_3xtf32_pair (256x128 pair tiles" if os.environ.get("AOL_3XTF32_WIDE") == "0"
-                           else "k_gemm_3xtf32_wide (256x256 pair tiles") +
-                          ": hi/lo split in shared memory, 3 tcgen05 products per k-slice, 64-deep TMEM chunks "
+                "kernel": {"narrow": "k_gemm_3xtf32_pair (256x128 pair tiles, running sum in TMEM",
+                           "wide": "k_gemm_3xtf32_wide (256x256 pair tiles, one accumulator, running sum in TMEM",
+                           "regs": "k_gemm_3xtf32_regs (256x256 pair tiles, two TMEM accumulators, running sum in "
+                                   "registers"}[_x3_form()] +
+                          "; hi/lo split in shared memory, 3 tcgen05 products per k-slice, 64-deep K chunks "
                           "summed with round-to-nearest adds)",
-                "chunk128": {"value": flop / (ms3_128 * 1e-3) / 1e12, "ms": ms3_128, "normwise_vs_fp64": err3_128,
-                             "switch": "AOL_3XTF32_CHUNK=128"},
+                "chunk32": {"value": flop / (ms3_32 * 1e-3) / 1e12, "ms": ms3_32, "normwise_vs_fp64": err3_32,
+                            "switch": "AOL_3XTF32_CHUNK=32"},
                 "cublas_fp32_simt": {"value": flop / (ms_simt * 1e-3) / 1e12, "ms": ms_simt,
                                      "normwise_vs_fp64": err_simt}}
 

@@ -1216,6 +1216,239 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
 }  // namespace x3w
 
+// =============================================================================
+// 3xTF32, register form: the wide kernel's 256x256 pair tiles and shared-memory operands, but
+// the running sum R lives in registers, so TMEM holds TWO 256-column chunk accumulators
+// (cols 0-255, 256-511) and the MMAs never wait for a fold.  Ten warps (320 threads, so a
+// thread may hold 204 registers): warp 0 TMA producer + TMEM allocator, warp 1 MMA issuer,
+// warps 2-9 both convert (lo = x - hi next to each landed tile) and fold: warp w owns TMEM
+// lane quarter w % 4 and columns ((w - 2) / 4) * 128 .. +127, i.e. 128 fp32 of R per thread.
+// They walk the chunks of their tiles in order: convert chunk j's k-blocks, then fold chunk
+// j - 1 (its accumulator is full by then: the MMAs of chunk j still have work converted), so
+// the fold overlaps the tensor cores.  Same chunks and add order as x3 / x3w: same bits.
+// =============================================================================
+namespace x3r {
+
+constexpr int BM = 256, BN = 256, HALF_M = 128, HALF_N = 128, STAGES = 3, CHUNK_KB = 2;
+constexpr int NUM_THREADS = 320, WORK_THREADS = 256;
+constexpr int A_BYTES = HALF_M * BK * 4;              // 16 KB
+constexpr int B_BYTES = HALF_N * BK * 4;              // 16 KB
+constexpr int LO_OFF = A_BYTES + B_BYTES;
+constexpr int STAGE_BYTES = 2 * LO_OFF;               // 64 KB per CTA
+constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 1024 + 256;
+
+template <bool A_KMAJOR, bool B_KMAJOR>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    k_gemm_3xtf32_regs(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                       Params p) {
+  using pair::arrive_leader;
+  using pair::cluster_rank;
+  using pair::cluster_sync;
+  using pair::commit_pair_multicast;
+  using pair::mma_tf32_pair;
+  using pair::PEER_MASK;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* conv = empty + STAGES;
+  uint64_t* tfull = conv + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int pair_id = blockIdx.x >> 1, num_pairs = gridDim.x >> 1;
+  const int chunk_kb = p.chunk_kb;
+  const int n_chunks = (p.k_blocks + chunk_kb - 1) / chunk_kb;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&map_a);
+    prefetch_tmap(&map_b);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+      mbar_init(&conv[s], 2 * WORK_THREADS);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 2 * WORK_THREADS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------- TMA producer (both CTAs) ----
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = pair_id; tile < p.num_tiles; tile += num_pairs) {
+        int mt, nt;
+        pair::tile_coords_pair(p, tile, mt, nt);
+        const int row0 = (int)(p.row_base + (int64_t)mt * BM) + (int)rank * HALF_M;
+        const int col0 = nt * BN + (int)rank * HALF_N;
+        for (int kb = 0; kb < p.k_blocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * STAGE_BYTES;
+          mbar_expect_tx(&full[stage], A_BYTES + B_BYTES);
+          x3::load_operand_local<A_KMAJOR, HALF_M>(&map_a, &full[stage], sa, kb * BK, row0);
+          x3::load_operand_local<B_KMAJOR, HALF_N>(&map_b, &full[stage], sa + A_BYTES, kb * BK, col0);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // ---------------------------------------------------- MMA issuer (leader) ----
+      constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((A_KMAJOR ? 0u : 1u) << 15) |
+                                 ((B_KMAJOR ? 0u : 1u) << 16) | ((uint32_t)(BN >> 3) << 17) |
+                                 ((uint32_t)(BM >> 4) << 24);
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, acc_phase = 0;
+      for (int tile = pair_id; tile < p.num_tiles; tile += num_pairs) {
+        for (int c = 0; c < n_chunks; ++c) {
+          mbar_wait(&tempty[acc], acc_phase ^ 1);      // this accumulator's previous chunk was read
+          tc_fence_after();
+          const uint32_t d_tmem = tmem_base + acc * BN;
+          const int kb_end = min(p.k_blocks, (c + 1) * chunk_kb);
+          for (int kb = c * chunk_kb; kb < kb_end; ++kb) {
+            mbar_wait(&conv[stage], phase);
+            tc_fence_after();
+            const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+            const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+            for (int k = 0; k < BK / UMMA_K; ++k) {
+              const uint64_t ah = operand_desc<A_KMAJOR>(sa, k), al = operand_desc<A_KMAJOR>(sa + LO_OFF, k);
+              const uint64_t bh = operand_desc<B_KMAJOR>(sb, k), bl = operand_desc<B_KMAJOR>(sb + LO_OFF, k);
+              mma_tf32_pair(d_tmem, al, bh, idesc, (kb != c * chunk_kb) || (k != 0));
+              mma_tf32_pair(d_tmem, ah, bl, idesc, 1u);
+              mma_tf32_pair(d_tmem, ah, bh, idesc, 1u);
+            }
+            commit_pair_multicast(&empty[stage]);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          }
+          commit_pair_multicast(&tfull[acc]);
+          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+      }
+    }
+  } else {
+    // ------------------------------ converters + folds (both CTAs, warps 2-9) ----
+    const int t = threadIdx.x - 64;
+    const int q = warp & 3;                              // TMEM lane quarter
+    const int half = (warp - 2) >> 2;                    // columns half*128 .. +127
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    const uint32_t cbar0 = smem_u32(&conv[0]) & PEER_MASK;
+    int stage = 0, acc = 0;
+    uint32_t phase = 0, acc_phase = 0;
+    float R[4][32];
+    // fold chunk `c` of tile (fmt, fnt) from accumulator `acc` into R; store R after its last chunk
+    auto fold = [&](int c, int fmt, int fnt) {
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) {
+        uint32_t v[32];
+        tmem_ld32(tmem_base + lane_base + acc * BN + half * 128 + ch * 32, v);
+        if (c == 0) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) R[ch][j] = __uint_as_float(v[j]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) R[ch][j] = __fadd_rn(R[ch][j], __uint_as_float(v[j]));
+        }
+      }
+      tc_fence_before();
+      arrive_leader(&tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (c != n_chunks - 1) return;
+      const int64_t g = p.row_base + (int64_t)fmt * BM + rank * HALF_M + q * 32 + lane;
+      if (g < p.m_lo || g > p.m_hi || g >= p.M) return;
+      int64_t lo_col = 0, hi_col = p.N;
+      if (g == p.m_lo) lo_col = p.first - p.m_lo * p.N;
+      if (g == p.m_hi) hi_col = p.last - p.m_hi * p.N + 1;
+      const int64_t c0 = (int64_t)fnt * BN + half * 128;
+      float* dst = p.c + g * p.ldc + c0;
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          const int64_t cc = c0 + ch * 32 + j;
+          if (p.c_vec && cc >= lo_col && cc + 4 <= hi_col) {
+            *reinterpret_cast<float4*>(dst + ch * 32 + j) =
+                make_float4(R[ch][j], R[ch][j + 1], R[ch][j + 2], R[ch][j + 3]);
+          } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (cc + u >= lo_col && cc + u < hi_col) dst[ch * 32 + j + u] = R[ch][j + u];
+          }
+        }
+      }
+    };
+    int pc = -1, pmt = 0, pnt = 0;                       // the chunk waiting to be folded
+    for (int tile = pair_id; tile < p.num_tiles; tile += num_pairs) {
+      int mt, nt;
+      pair::tile_coords_pair(p, tile, mt, nt);
+      for (int c = 0; c < n_chunks; ++c) {
+        const int kb_end = min(p.k_blocks, (c + 1) * chunk_kb);
+        for (int kb = c * chunk_kb; kb < kb_end; ++kb) {
+          mbar_wait(&full[stage], phase);
+          float4* x = reinterpret_cast<float4*>(smem + stage * STAGE_BYTES);
+          float4* lo = reinterpret_cast<float4*>(smem + stage * STAGE_BYTES + LO_OFF);
+          if (p.hi_round) {
+#pragma unroll 2
+            for (int i = t; i < LO_OFF / 16; i += WORK_THREADS) {
+              const float4 v = x[i];
+              float4 h, l;
+              h.x = x3::tf32_rna(v.x); l.x = __fsub_rn(v.x, h.x);
+              h.y = x3::tf32_rna(v.y); l.y = __fsub_rn(v.y, h.y);
+              h.z = x3::tf32_rna(v.z); l.z = __fsub_rn(v.z, h.z);
+              h.w = x3::tf32_rna(v.w); l.w = __fsub_rn(v.w, h.w);
+              x[i] = h;
+              lo[i] = l;
+            }
+          } else {
+#pragma unroll 2
+            for (int i = t; i < LO_OFF / 16; i += WORK_THREADS) {
+              const float4 v = x[i];
+              float4 l;
+              l.x = __fsub_rn(v.x, __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u));
+              l.y = __fsub_rn(v.y, __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u));
+              l.z = __fsub_rn(v.z, __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u));
+              l.w = __fsub_rn(v.w, __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u));
+              lo[i] = l;
+            }
+          }
+          x3::fence_proxy_async_smem();
+          asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cbar0 + stage * 8) : "memory");
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        if (pc >= 0) fold(pc, pmt, pnt);
+        pc = c; pmt = mt; pnt = nt;
+      }
+    }
+    if (pc >= 0) fold(pc, pmt, pnt);
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+  }
+}
+
+}  // namespace x3r
+
 // ------------------------------------------------------------ host side ----
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -1861,8 +2094,16 @@ static int gemm_core_3x(const float* A, const float* B, float* C, const GemmShap
   if (g.a_kmajor) rc = make_map(&ma, A, g.K, g.M, g.lda, BK, x3::HALF_M, true);
   else rc = make_map(&ma, A, g.M, g.K, g.lda, 32, BK, false);
   if (rc) return rc;
-  // wide form (256x256 pair tiles, default) or the 256x128 form with two chunk accumulators
-  static const bool wide = [] { const char* e = getenv("AOL_3XTF32_WIDE"); return !e || e[0] != '0'; }();
+  // form (read once per process): 2 = "regs" (256x256 pair tiles, two TMEM chunk accumulators,
+  // running sum in registers; default), 1 = "wide" (256x256, one accumulator + TMEM running
+  // sum), 0 = "narrow" (256x128, two 128-column accumulators + TMEM running sum) -- same bits
+  static const int form = [] {
+    const char* f = getenv("AOL_3XTF32_FORM");
+    const char* w = getenv("AOL_3XTF32_WIDE");
+    if (f) return !strcmp(f, "narrow") ? 0 : !strcmp(f, "wide") ? 1 : 2;
+    return (w && w[0] == '0') ? 0 : 2;
+  }();
+  const bool wide = form != 0;
   if (g.b_kmajor) rc = make_map(&mb, B, g.K, g.N, g.ldb, BK, wide ? x3w::HALF_N : x3::HALF_N, true);
   else rc = make_map(&mb, B, g.N, g.K, g.ldb, 32, BK, false);
   if (rc) return rc;
@@ -1886,14 +2127,17 @@ static int gemm_core_3x(const float* A, const float* B, float* C, const GemmShap
   const char* hr = getenv("AOL_3XTF32_HI");
   p.hi_round = hr ? (hr[0] != '0') : 0;
   void (*k)(const CUtensorMap, const CUtensorMap, Params);
-  if (wide) {
+  if (form == 2) {
+    if (g.a_kmajor) k = g.b_kmajor ? x3r::k_gemm_3xtf32_regs<true, true> : x3r::k_gemm_3xtf32_regs<true, false>;
+    else k = g.b_kmajor ? x3r::k_gemm_3xtf32_regs<false, true> : x3r::k_gemm_3xtf32_regs<false, false>;
+  } else if (wide) {
     if (g.a_kmajor) k = g.b_kmajor ? x3w::k_gemm_3xtf32_wide<true, true> : x3w::k_gemm_3xtf32_wide<true, false>;
     else k = g.b_kmajor ? x3w::k_gemm_3xtf32_wide<false, true> : x3w::k_gemm_3xtf32_wide<false, false>;
   } else {
     if (g.a_kmajor) k = g.b_kmajor ? x3::k_gemm_3xtf32_pair<true, true> : x3::k_gemm_3xtf32_pair<true, false>;
     else k = g.b_kmajor ? x3::k_gemm_3xtf32_pair<false, true> : x3::k_gemm_3xtf32_pair<false, false>;
   }
-  const int smem = (int)(wide ? x3w::SMEM_BYTES : x3::SMEM_BYTES);
+  const int smem = (int)(form == 2 ? x3r::SMEM_BYTES : wide ? x3w::SMEM_BYTES : x3::SMEM_BYTES);
   AOL_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int sms = kNumSMs;
   int dev = 0;
@@ -1901,7 +2145,7 @@ static int gemm_core_3x(const float* A, const float* B, float* C, const GemmShap
   const int pairs = p.num_tiles < sms / 2 ? p.num_tiles : sms / 2;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * pairs);
-  cfg.blockDim = dim3(wide ? x3w::NUM_THREADS : x3::NUM_THREADS);
+  cfg.blockDim = dim3(form == 2 ? x3r::NUM_THREADS : wide ? x3w::NUM_THREADS : x3::NUM_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
@@ -1912,7 +2156,7 @@ static int gemm_core_3x(const float* A, const float* B, float* C, const GemmShap
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   AOL_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k, ma, mb, p));
-  AOL_LAUNCH_CHECK(wide ? "k_gemm_3xtf32_wide" : "k_gemm_3xtf32_pair");
+  AOL_LAUNCH_CHECK(form == 2 ? "k_gemm_3xtf32_regs" : wide ? "k_gemm_3xtf32_wide" : "k_gemm_3xtf32_pair");
   return AOL_OK;
 }
 

@@ -501,20 +501,23 @@ np.save(sys.argv[2], execute_schedule(model, build_schedule(model, D), bind, D, 
 """
 
 
-def test_matmul_3xtf32_wide_equals_narrow_form(tmp_path):
-    """The 256x256-tile 3xTF32 kernel (default) and the 256x128 form (AOL_3XTF32_WIDE=0, read once
-    per process) use the same 64-deep chunks and add order: bit-identical C on unaligned shards."""
+def test_matmul_3xtf32_forms_are_bit_identical(tmp_path):
+    """The three fused 3xTF32 kernels -- regs (default: 256x256 tiles, running sum in registers),
+    wide (256x256, one accumulator + running sum in TMEM) and narrow (256x128) -- use the same
+    64-deep chunks and add order: bit-identical C on unaligned shards (the form is read once per
+    process, so each runs in its own interpreter)."""
     import os
     import subprocess
     import sys
     from pathlib import Path
     root = str(Path(__file__).resolve().parent.parent)
     outs = {}
-    for form, env in (("wide", {}), ("narrow", {"AOL_3XTF32_WIDE": "0"})):
+    for form, env in (("regs", {}), ("wide", {"AOL_3XTF32_FORM": "wide"}), ("narrow", {"AOL_3XTF32_WIDE": "0"})):
         out = tmp_path / f"{form}.npy"
         subprocess.run([sys.executable, "-c", _X3_FORM_SCRIPT, root, str(out)],
                        env={**os.environ, **env}, check=True, timeout=300)
         outs[form] = np.load(out)
+    assert np.array_equal(outs["regs"], outs["narrow"])
     assert np.array_equal(outs["wide"], outs["narrow"])
 
 
