@@ -1629,12 +1629,123 @@ __global__ void __launch_bounds__(256) k_gemm_exact(const T* __restrict__ A, con
   }
 }
 
+// 128 x 128 output tile per CTA (256 threads, 8 x 8 outputs each: rows ty*4 + {0..3} and
+// 64 + ty*4 + {0..3}, columns likewise), K through a double-buffered shared-memory slab 8 deep;
+// the next slab's global loads are issued before the current slab's products.  Each output
+// still accumulates k ascending with a separate rounding per product and per add: the same
+// bits as k_gemm_exact (and the oracle).  4x fewer shared-memory operand loads per product
+// than the 4 x 4 form, which was bound by them.
+constexpr int EX2_T = 128, EX2_K = 8;
+
+template <typename T>
+__device__ __forceinline__ void ex_ld4(const T* p, T (&v)[4]) {
+  if constexpr (sizeof(T) == 4) {
+    const float4 q = *reinterpret_cast<const float4*>(p);
+    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+  } else {
+    const double2 q0 = reinterpret_cast<const double2*>(p)[0], q1 = reinterpret_cast<const double2*>(p)[1];
+    v[0] = q0.x; v[1] = q0.y; v[2] = q1.x; v[3] = q1.y;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_gemm_exact128(const T* __restrict__ A, const T* __restrict__ B,
+                                                       T* __restrict__ C, GemmStrides g, int64_t m_lo, int64_t first,
+                                                       int64_t last, int n_tiles) {
+  __shared__ __align__(16) T As[2][EX2_K][EX2_T];
+  __shared__ __align__(16) T Bs[2][EX2_K][EX2_T];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int64_t mt = blockIdx.x / n_tiles, nt = blockIdx.x - mt * n_tiles;
+  const int64_t m0 = m_lo + mt * EX2_T, n0 = nt * EX2_T;
+  const bool a_k_fast = g.sak == 1, b_n_fast = g.sbn == 1;
+  T ra[4], rb[4];
+  // slab element e = threadIdx.x + 256 u (u < 4) -> (row/col, k) with the unit-stride axis fastest
+  auto load = [&](int64_t k0) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = threadIdx.x + 256 * u;
+      const int r = a_k_fast ? e >> 3 : e & 127, kk = a_k_fast ? e & 7 : e >> 7;
+      const int64_t m = m0 + r, k = k0 + kk;
+      ra[u] = (m < g.M && k < g.K) ? A[g.ca + g.sam * m + g.sak * k] : T(0);
+      const int c = b_n_fast ? e & 127 : e >> 3, kb = b_n_fast ? e >> 7 : e & 7;
+      const int64_t n = n0 + c, k2 = k0 + kb;
+      rb[u] = (n < g.N && k2 < g.K) ? B[g.cb + g.sbk * k2 + g.sbn * n] : T(0);
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = threadIdx.x + 256 * u;
+      As[buf][a_k_fast ? e & 7 : e >> 7][a_k_fast ? e >> 3 : e & 127] = ra[u];
+      Bs[buf][b_n_fast ? e >> 7 : e & 7][b_n_fast ? e & 127 : e >> 3] = rb[u];
+    }
+  };
+  T acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = T(0);
+  load(0);
+  store(0);
+  __syncthreads();
+  int buf = 0;
+  for (int64_t k0 = 0; k0 < g.K; k0 += EX2_K) {
+    const bool more = k0 + EX2_K < g.K;
+    if (more) load(k0 + EX2_K);
+    const int kn = (int)(g.K - k0 < EX2_K ? g.K - k0 : EX2_K);
+    for (int kk = 0; kk < kn; ++kk) {
+      T a[8], b[8];
+      ex_ld4(&As[buf][kk][ty * 4], *reinterpret_cast<T(*)[4]>(a));
+      ex_ld4(&As[buf][kk][64 + ty * 4], *reinterpret_cast<T(*)[4]>(a + 4));
+      ex_ld4(&Bs[buf][kk][tx * 4], *reinterpret_cast<T(*)[4]>(b));
+      ex_ld4(&Bs[buf][kk][64 + tx * 4], *reinterpret_cast<T(*)[4]>(b + 4));
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = ex_mac(acc[i][j], a[i], b[j]);
+    }
+    if (more) {
+      store(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t m = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+    if (m >= g.M) continue;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int64_t n = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
+      const int64_t lin = m * g.N + n;
+      if (n < g.N && lin >= first && lin <= last) C[g.cc + g.scm * m + g.scn * n] = acc[i][j];
+    }
+  }
+}
+
 int launch_gemm_exact(const aol_task& t, int64_t first, int64_t count, void* const* ports, cudaStream_t stream) {
   GemmStrides g;
   if (!recognise_gemm_strides(t, g)) return AOL_EUNSUPPORTED;
   if (count <= 0) return AOL_OK;
   const int64_t last = first + count - 1;
   const int64_t m_lo = first / g.N, m_hi = last / g.N;
+  // 128 x 128 tiles once there is one per SM (the double-buffered 8 x 8-per-thread form); small
+  // products keep 64 x 64 tiles for more CTAs.  AOL_GEMM_EXACT64=1 forces the 64 x 64 form.
+  static const bool force64 = getenv("AOL_GEMM_EXACT64") != nullptr;
+  const int64_t m_big = (m_hi - m_lo + EX2_T) / EX2_T, n_big = (g.N + EX2_T - 1) / EX2_T;
+  int dev = 0, sms = kNumSMs;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (!force64 && m_big * n_big >= sms && m_big * n_big < (1ll << 31)) {
+    const unsigned grid = (unsigned)(m_big * n_big);
+    if (t.dtype == AOL_F32)
+      k_gemm_exact128<float><<<grid, 256, 0, stream>>>((const float*)ports[0], (const float*)ports[1],
+                                                        (float*)ports[2], g, m_lo, first, last, (int)n_big);
+    else
+      k_gemm_exact128<double><<<grid, 256, 0, stream>>>((const double*)ports[0], (const double*)ports[1],
+                                                         (double*)ports[2], g, m_lo, first, last, (int)n_big);
+    AOL_LAUNCH_CHECK("k_gemm_exact128");
+    return AOL_OK;
+  }
   const int64_t m_tiles = (m_hi - m_lo + EX_T) / EX_T, n_tiles = (g.N + EX_T - 1) / EX_T;
   if (m_tiles * n_tiles >= (1ll << 31)) return AOL_EUNSUPPORTED;
   const unsigned grid = (unsigned)(m_tiles * n_tiles);

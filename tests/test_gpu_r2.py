@@ -582,3 +582,26 @@ def test_prepared_executor_busy_entry_is_bypassed():
         lock.release()
     assert np.array_equal(first, again)
     exm.clear_prepared()
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+@pytest.mark.parametrize("a_mn,b_k", [(False, False), (True, True), (False, True)])
+def test_matmul_exact_128_tiles_bit_exact(dtype, a_mn, b_k):
+    """precision="exact" at sizes that take the 128 x 128 double-buffered kernel (>= 2 tiles per
+    SM), K not a multiple of the 8-deep slab, unaligned shards: every output equals the k-ascending
+    product with a rounding per product and per add (numpy elementwise arithmetic in that order)."""
+    from paper_1105_4424_b200 import builders
+    from paper_1105_4424_b200.executor import execute_schedule
+    from paper_1105_4424_b200.partition import build_schedule
+    M, N, K, D = 2200, 2100, 45, 3
+    t, ports, bind, A, B = _gemm_case(M, N, K, a_mn, b_k, 17)
+    ports = {k: v.replace("float32", dtype) for k, v in ports.items()}
+    bind = {k: np.asarray(v).astype(dtype) for k, v in bind.items()}
+    model = builders.tile_task_model("matmul", ports, {k: _tiler(v) for k, v in t.items()}, (M, N))
+    sched = build_schedule(model, D)
+    c = execute_schedule(model, sched, bind, D, precision="exact").outputs["p_c"].reshape(M, N)
+    A, B = A.astype(dtype), B.astype(dtype)
+    want = np.zeros((M, N), dtype=dtype)
+    for k in range(K):
+        want = want + A[:, k:k + 1] * B[k:k + 1, :]
+    assert c.dtype == want.dtype and np.array_equal(c, want)
