@@ -211,7 +211,7 @@ int aol_loop_destroy(aol_loop* loop);
  * max_iter iterations, like refexec.py:525-541, with results bit-identical to launching
  * the same ops one by one.  Returns AOL_EUNSUPPORTED (nothing launched) for bodies
  * outside its op set (copy/sub/scale/axpy/spmv_csr/dot_partial/div/neg/rel_residual),
- * > 40 ops or > 32 ports; callers then fall back to aol_loop_begin/end/run. */
+ * > 128 ops, > 96 op groups or > 32 ports; callers then fall back to aol_loop_begin/end/run. */
 typedef struct aol_loop_op {
   int32_t op;
   int32_t n_scalars;       /* axpy: 1 -> y += a*x, 0 -> y += x */

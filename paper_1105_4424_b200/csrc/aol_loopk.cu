@@ -34,8 +34,8 @@ namespace cg = cooperative_groups;
 
 namespace aol {
 
-constexpr int kLoopMaxOps = 40;
-constexpr int kLoopMaxGroups = 40;
+constexpr int kLoopMaxOps = 128;
+constexpr int kLoopMaxGroups = 96;
 constexpr int kLoopMaxPorts = 32;
 constexpr int kLoopMaxParts = 8;
 constexpr int kLoopSub = 4;                   // 256-thread sub-blocks per CTA

@@ -1118,17 +1118,23 @@ class Executor:
             relres = self.storage.array(step.relres_port)
             torch.cuda.synchronize(self.device)
             handle = None
-            with torch.cuda.stream(stream):
-                handle = _capi.loop_begin(stream.cuda_stream, relres.data_ptr(),
-                                          str(relres.dtype).replace("torch.", ""), tol, max(1, int(max_iter)))
-                try:
-                    self._run_body_device(step.body)
-                finally:
+            # the body's launches go to the capture stream, also when the caller passed stream=:
+            # launched on the caller's stream they would run once, eagerly, outside the graph
+            caller_stream, self.stream = self.stream, stream
+            try:
+                with torch.cuda.stream(stream):
+                    handle = _capi.loop_begin(stream.cuda_stream, relres.data_ptr(),
+                                              str(relres.dtype).replace("torch.", ""), tol, max(1, int(max_iter)))
                     try:
-                        _capi.loop_end(handle)
-                    except Exception:
-                        _capi.loop_destroy(handle)
-                        raise
+                        self._run_body_device(step.body)
+                    finally:
+                        try:
+                            _capi.loop_end(handle)
+                        except Exception:
+                            _capi.loop_destroy(handle)
+                            raise
+            finally:
+                self.stream = caller_stream
             entry = (handle, stream)
             self._loops[key] = entry
         handle, stream = entry

@@ -605,3 +605,32 @@ def test_matmul_exact_128_tiles_bit_exact(dtype, a_mn, b_k):
     for k in range(K):
         want = want + A[:, k:k + 1] * B[k:k + 1, :]
     assert c.dtype == want.dtype and np.array_equal(c, want)
+
+
+@pytest.mark.parametrize("persistent", ["1", "0"])
+@pytest.mark.parametrize("D", [1, 5, 8])
+def test_cg_with_caller_stream_matches_default(golden, persistent, D, monkeypatch):
+    """A LoopStep run with execute_schedule(stream=...) equals the default-stream run bit for bit,
+    on the persistent interpreter (D up to 8 now fits it) and on the CUDA-graph WHILE path
+    (AOL_LOOP_PERSISTENT=0), whose capture must take the body's launches even when the caller
+    named a stream (they used to run once, eagerly, outside the graph: 400 iterations, no
+    convergence)."""
+    import torch
+    from paper_1105_4424_b200.executor import Executor, execute_schedule
+    from paper_1105_4424_b200.model import model_from_dict
+    from paper_1105_4424_b200.partition import build_schedule
+    monkeypatch.setenv("AOL_LOOP_PERSISTENT", persistent)
+    data, meta = golden
+    model = model_from_dict(meta["cg_k20"]["model"])
+    bind = {k: data[f"cg_k20/{k}"] for k in ("rowptr", "colidx", "values", "b")}
+    sched = build_schedule(model, D)
+    plain = execute_schedule(model, sched, bind, D)
+    s = torch.cuda.Stream()
+    res = execute_schedule(model, sched, bind, D, stream=s)
+    torch.cuda.synchronize()
+    assert res.iterations == plain.iterations
+    assert np.array_equal(np.asarray(res.outputs["x"]), np.asarray(plain.outputs["x"]))
+    if persistent == "1":
+        ex = Executor(model, sched, bind, D)
+        ex.run()
+        assert ex.persistent_loops == 1
