@@ -37,15 +37,18 @@ plain_cache = {}
 for case in range(int(os.environ.get("CASES", "120"))):
     name = names[int(rng.integers(0, len(names)))]
     model, bind, out_port, _ = cases[name]()
-    D = int(rng.integers(1, 6))
+    D = int(rng.integers(1, 9))
     sched = build_schedule(model, D)
-    prec = "exact" if name == "matmul" else "default"
-    key = (name, D)
+    prec = str(rng.choice(["exact", "default", "3xtf32"])) if name == "matmul" else "default"
+    loop_kw = {}
+    if name == "cg" and rng.random() < 0.3:
+        loop_kw = {"tol": float(rng.choice([1e-4, 1e-8])), "max_iter": int(rng.integers(3, 60))}
+    key = (name, D, prec, tuple(sorted(loop_kw.items())))
     if key not in plain_cache:
-        plain_cache[key] = execute_schedule(model, sched, bind, D, precision=prec).outputs
+        plain_cache[key] = execute_schedule(model, sched, bind, D, precision=prec, **loop_kw).outputs
     plain = plain_cache[key]
-    kw = {"precision": prec}
-    combo = []
+    kw = {"precision": prec, **loop_kw}
+    combo = [f"prec={prec}"] + [f"{k}={v}" for k, v in loop_kw.items()]
     if rng.random() < 0.4:
         kw["pipeline"] = int(rng.integers(2, 9))
         combo.append(f"pipeline={kw['pipeline']}")
