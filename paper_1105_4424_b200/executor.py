@@ -1282,6 +1282,7 @@ class Executor:
 # schedules of device steps, arenas up to AOL_PREPARED_ARENA_MB (default 64), at most
 # AOL_PREPARED_MAX entries (default 8, 0 disables); a busy entry (another thread) is bypassed.
 _PREPARED: dict = {}
+_PREPARED_LOCK = __import__("threading").Lock()   # guards the dict; each entry has its own lock
 _PREPARED_MAX = int(os.environ.get("AOL_PREPARED_MAX", "8"))
 _PREPARED_ARENA = int(os.environ.get("AOL_PREPARED_ARENA_MB", "64")) << 20
 
@@ -1297,10 +1298,16 @@ def _prepared_executor(model, schedule, bindings, device_count, precision, devic
     if sum(storage_layout(model).arenas.values()) > _PREPARED_ARENA:
         return None
     key = (id(model), id(schedule), device_count, precision, str(dev), fuse, graphs)
-    ent = _PREPARED.get(key)
-    if ent is not None and (ent[0]() is not model or ent[1]() is not schedule):
-        _PREPARED.pop(key, None)                 # ids reused by new objects
-        ent = None
+    with _PREPARED_LOCK:
+        ent = _PREPARED.get(key)
+        if ent is not None and (ent[0]() is not model or ent[1]() is not schedule):
+            _PREPARED.pop(key, None)             # ids reused by new objects
+            ent = None
+        if ent is not None:
+            _, _, ex, lock = ent
+            if not lock.acquire(blocking=False):
+                return None                      # busy (another thread): build a fresh executor
+            _PREPARED[key] = _PREPARED.pop(key)  # most recently used last
     if ent is None:
         try:
             mref, sref = weakref.ref(model), weakref.ref(schedule)
@@ -1310,25 +1317,25 @@ def _prepared_executor(model, schedule, bindings, device_count, precision, devic
                       graphs=graphs)
         lock = threading.Lock()
         lock.acquire()
-        if len(_PREPARED) >= _PREPARED_MAX:
-            _PREPARED.pop(next(iter(_PREPARED)))
-        _PREPARED[key] = (mref, sref, ex, lock)
+        with _PREPARED_LOCK:
+            if key in _PREPARED:                 # another thread cached one meanwhile: ours runs once
+                return ex, lock
+            while len(_PREPARED) >= _PREPARED_MAX:
+                _PREPARED.pop(next(iter(_PREPARED)))
+            _PREPARED[key] = (mref, sref, ex, lock)
         return ex, lock
-    _, _, ex, lock = ent
-    if not lock.acquire(blocking=False):
-        return None
     try:
         ex.rebind(bindings)
     except BaseException:
         lock.release()
         raise
-    _PREPARED[key] = _PREPARED.pop(key)          # most recently used last
     return ex, lock
 
 
 def clear_prepared() -> None:
     """Drop every cached prepared executor (frees their HBM arenas)."""
-    _PREPARED.clear()
+    with _PREPARED_LOCK:
+        _PREPARED.clear()
 
 
 def _default_devices(device_count: int, device, pipeline: int):

@@ -634,3 +634,44 @@ def test_cg_with_caller_stream_matches_default(golden, persistent, D, monkeypatc
         ex = Executor(model, sched, bind, D)
         ex.run()
         assert ex.persistent_loops == 1
+
+
+def test_concurrent_calls_from_threads():
+    """Four host threads calling execute_schedule on shared (model, schedule) objects at once --
+    two of them on their own streams -- all get the single-threaded results (the prepared-executor
+    cache's dict is locked; a busy entry is bypassed)."""
+    import threading
+    import torch
+    from paper_1105_4424_b200 import builders
+    from paper_1105_4424_b200 import executor as exm
+    from paper_1105_4424_b200.partition import build_schedule
+    rng = np.random.default_rng(4)
+    cases = []
+    for n, D in ((96, 1), (160, 3)):
+        model = builders.matmul_model(n, n, n)
+        sched = build_schedule(model, D)
+        bind = {"p_a": rng.standard_normal(n * n, dtype=np.float32), "p_b": rng.standard_normal(n * n, dtype=np.float32)}
+        want = exm.execute_schedule(model, sched, bind, D, precision="exact").outputs["p_c"]
+        cases.append((model, sched, bind, D, want))
+    exm.clear_prepared()
+    errors = []
+
+    def work(tid):
+        s = torch.cuda.Stream() if tid % 2 else None
+        for c in range(30):
+            model, sched, bind, D, want = cases[(tid + c) % len(cases)]
+            kw = {"stream": s} if s is not None else {}
+            try:
+                got = exm.execute_schedule(model, sched, bind, D, precision="exact", **kw).outputs["p_c"]
+                if not np.array_equal(got, want):
+                    errors.append((tid, c, "mismatch"))
+            except Exception as e:  # noqa: BLE001
+                errors.append((tid, c, repr(e)))
+
+    ts = [threading.Thread(target=work, args=(t,)) for t in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    exm.clear_prepared()
+    assert not errors, errors[:5]
