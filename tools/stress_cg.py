@@ -53,7 +53,7 @@ for case in range(int(os.environ.get("CASES", "40"))):
     rowptr, colidx, values = random_spd(n)
     nnz = int(rowptr[-1])
     model = model_from_dict(bench._resize_model_dict(base, 400, 1920, n, nnz))
-    D = int(rng.integers(1, 5))
+    D = int(rng.integers(1, 9))
     sched = build_schedule(model, D)
     bind = {"rowptr": rowptr, "colidx": colidx, "values": values, "b": rng.standard_normal(n)}
     eager = execute_schedule(model, sched, bind, D, graphs=False)
