@@ -134,6 +134,29 @@ int aol_device_count(int* n) {
 
 int aol_validate(const aol_task* task) { return validate(task); }
 
+// Ports every launch of `t` dereferences (aol_op's port lists; device scalars appended after the
+// vectors); 0 where the count is data-dependent (scalar_seq).
+static int required_ports(const aol_task* t) {
+  const int dev_scalar = (t->flags & AOL_FLAG_DEVICE_SCALARS) && t->n_scalars > 0 ? 1 : 0;
+  switch (t->op) {
+    case AOL_OP_COPY: return 2;
+    case AOL_OP_SUB: return 3;
+    case AOL_OP_SCALE: return 1 + dev_scalar;
+    case AOL_OP_AXPY: return 2 + dev_scalar;
+    case AOL_OP_SPMV_CSR: return 5;
+    case AOL_OP_DOT_PARTIAL: return 3;
+    case AOL_OP_SCALAR_DIV: return 3;
+    case AOL_OP_SCALAR_NEG: return 2;
+    case AOL_OP_REL_RESIDUAL: return 3;
+    case AOL_OP_PARTIALS_SUM: return 2;
+    case AOL_OP_TILE_COPY: return 2;
+    case AOL_OP_MATMUL: return 3;
+    case AOL_OP_TILE_FILTER: return 3;
+    case AOL_OP_TILE_SUM: return 2;
+    default: return 0;
+  }
+}
+
 int aol_launch(const aol_task* t, int64_t first, int64_t count, void* const* ports, const double* scalars,
                void* stream) {
   int rc = validate(t);
@@ -143,6 +166,8 @@ int aol_launch(const aol_task* t, int64_t first, int64_t count, void* const* por
   if (R >= 0 && first + count > R) return fail(AOL_EINVAL, "repetition range outside the repetition space");
   if (!ports) return fail(AOL_EINVAL, "null port array");
   if (count == 0) return AOL_OK;
+  for (int p = 0, n = required_ports(t); p < n; ++p)      // a null port would fault the kernel
+    if (!ports[p]) return fail(AOL_EINVAL, "null port " + std::to_string(p));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   switch (t->op) {
     case AOL_OP_TILE_COPY: return launch_tile_copy(*t, first, count, ports, s);

@@ -326,3 +326,18 @@ def test_config_builders_equal_the_oracle_tilers():
     assert np.array_equal(builders.downscaler_weights(14, 4), orc.vfilter_weights())
     m = builders.downscaler_model(2, 18, 64)
     assert set(m.application_components) >= {"HT", "VT", "m"}
+
+
+def test_launch_rejects_null_ports_without_gpu():
+    """aol_launch refuses a null pointer in any port the op dereferences (AOL_EINVAL, nothing
+    launched) -- checked before any CUDA call, so it runs here."""
+    cp = dict(array=(100,), rep=(25,), pattern=(4,), origin=(0,), paving=((4,),), fitting=((1,),))
+    t = _capi.make_task("tile_copy", "float32", [_bt(cp), _bt(cp)])
+    with pytest.raises(_capi.AolError, match="null port 1"):
+        _capi.launch(t, 0, 25, [0x1000, 0], (), 0)
+    g = orc.gemm_tilers(64, 64, 32)
+    mm = _capi.make_task("matmul", "float32", [_bt(g[k]) for k in "abc"])
+    with pytest.raises(_capi.AolError, match="null port 0"):
+        _capi.launch(mm, 0, 64 * 64, [0, 0x1000, 0x2000], (), 0)
+    with pytest.raises(_capi.AolError, match="outside the repetition space"):
+        _capi.launch(mm, 0, 64 * 64 + 1, [0x1000, 0x1000, 0x2000], (), 0)
