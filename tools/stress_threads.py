@@ -62,6 +62,8 @@ def worker(tid):
         kw = {"precision": k[2]}
         if stream is not None:
             kw["stream"] = stream
+        if rng.random() < 0.3:
+            kw["pipeline"] = int(rng.integers(2, 6))    # streamed paths: shared side streams + staging ring
         try:
             got = execute_schedule(model, sched, bind, k[1], **kw).outputs[out]
             if not np.array_equal(np.asarray(got), np.asarray(want)):
