@@ -30,8 +30,34 @@ def cg_case():
     return model, {k: data[f"cg_k20/{k}"] for k in ("rowptr", "colidx", "values", "b")}, "x", None
 
 
+def ref_op_case(op):
+    """A reference elementwise op (refexec.py:504-514) on n elements: y inout for axpy / scale,
+    a host-resident scalar `a` where the op takes one."""
+    from paper_1105_4424_b200 import builders
+    n = 4999 if op == "axpy" else 6007             # fixed per op: the plain results are cached per name
+    r = np.random.default_rng(n)
+    if op == "axpy":
+        tp = ["y inout float64 [%d]" % n, "x in float64 [%d]" % n, "a in float64 [1]"]
+        rp = ["i in float64 [%d]" % n, "v in float64 [%d]" % n, "s in float64 [1]", "o out float64 [%d]" % n]
+        cn = ["i -> t.y", "v -> t.x", "s -> t.a", "t.y -> o"]
+        al = ["allocate data i onto dev.gmem", "allocate data v onto dev.gmem", "allocate data s onto host.ram",
+              "allocate task t onto dev.cu"]
+        bind = {"i": r.standard_normal(n), "v": r.standard_normal(n), "s": np.array([0.75])}
+    else:                                          # sub: z = x - y
+        tp = ["x in float64 [%d]" % n, "y in float64 [%d]" % n, "z out float64 [%d]" % n]
+        rp = ["p in float64 [%d]" % n, "q in float64 [%d]" % n, "o out float64 [%d]" % n]
+        cn = ["p -> t.x", "q -> t.y", "t.z -> o"]
+        al = ["allocate data p onto dev.gmem", "allocate data q onto dev.gmem", "allocate data t.z onto dev.gmem",
+              "allocate task t onto dev.cu"]
+        bind = {"p": r.standard_normal(n), "q": r.standard_normal(n)}
+    model = builders.single_task_model(op, tp, rp, cn, al, n)
+    return model, bind, "o", None
+
+
 cases = dict(CASES)
 cases["cg"] = cg_case
+cases["axpy"] = lambda: ref_op_case("axpy")
+cases["sub"] = lambda: ref_op_case("sub")
 names = sorted(cases)
 plain_cache = {}
 for case in range(int(os.environ.get("CASES", "120"))):
