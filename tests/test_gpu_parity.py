@@ -1540,3 +1540,44 @@ def test_random_long_rows_batched_filters_vs_oracle(seed, dtype):
         got = _run_tile("tile_filter", {"x": tx, "y": ty}, ports, {"x": x, "w": w}, d).outputs["p_y"]
         ref = orc.run_tile_task("tile_filter", {"x": tx, "y": ty}, {"x": x, "w": w}, {"y": (R * py, np_dt)}, R, d)
         assert np.array_equal(got.view(np.uint8), ref["y"].view(np.uint8)), (tx, ty)
+
+
+def _special_values(n, seed):
+    """float32 data in three bands: subnormals and signed zeros, overflow-prone magnitudes
+    (1e38-3.3e38), ordinary values -- all non-negative, so every product and sum has one IEEE
+    answer (no inf - inf, no 0 * inf) and the comparison can be bit for bit."""
+    rng = np.random.default_rng(seed)
+    tiny = np.array([0.0, -0.0, 1e-45, 3e-42, 1e-40, 5e-39], dtype=np.float32)
+    huge = np.array([1e38, 2e38, 3.3e38], dtype=np.float32)
+    v = np.abs(rng.standard_normal(n)).astype(np.float32)
+    third = n // 3
+    v[:third] = tiny[rng.integers(0, tiny.size, third)]
+    v[third:2 * third] = huge[rng.integers(0, huge.size, third)]
+    v[:third] = np.where(v[:third] == 0, v[:third], np.abs(v[:third]))
+    return v
+
+
+@pytest.mark.parametrize("devices", [1, 3])
+def test_special_values_bit_exact(devices):
+    """Stencil, line filter, tile sum and exact-order matmul on subnormals, signed zeros and
+    overflowing magnitudes: no flush-to-zero (the library is built without fast math), the same
+    IEEE rounding per product and per add as the oracle, +inf where the oracle overflows."""
+    H, W = 48, 64
+    t = orc.stencil_tilers(H, W)
+    x = _special_values(H * W, 1)
+    w = (16 * np.abs(orc.stencil_weights())).astype(np.float32)     # 1 2 1 / 2 4 2 / 1 2 1: overflows
+    res = _run_tile("stencil", t, {"x": _spec(t["x"], "in", "float32"), "w": "in float32 [9]",
+                                   "y": _spec(t["y"], "out", "float32")}, {"x": x, "w": w}, devices)
+    with np.errstate(over="ignore"):
+        want = orc.run_tile_task("stencil", t, {"x": x, "w": w}, {"y": (H * W, np.float32)}, H * W, devices)["y"]
+    got = res.outputs["p_y"]
+    assert np.isinf(want).any() and (np.abs(want[want != 0]) < 1.2e-38).any()
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    M, N, K = 40, 36, 24
+    g = orc.gemm_tilers(M, N, K)
+    a, b = _special_values(M * K, 2), _special_values(K * N, 3)
+    res = _run_tile("matmul", g, {"a": _spec(g["a"], "in", "float32"), "b": _spec(g["b"], "in", "float32"),
+                                  "c": _spec(g["c"], "out", "float32")}, {"a": a, "b": b}, devices, precision="exact")
+    with np.errstate(over="ignore"):
+        want = orc.run_tile_task("matmul", g, {"a": a, "b": b}, {"c": (M * N, np.float32)}, M * N, devices)["c"]
+    assert np.array_equal(res.outputs["p_c"].view(np.uint32), want.view(np.uint32))
