@@ -219,3 +219,30 @@ def test_c2_matmul_8192_3xtf32_fp32_faithful():
     finally:
         torch.backends.cuda.matmul.allow_tf32 = prev
     assert ours <= 1e-6 and ours <= simt, (ours, simt)
+
+
+@pytest.mark.parametrize("precision", ["default", "3xtf32"])
+def test_matmul_output_beyond_2_31_elements(precision):
+    """C with 65536 x 36864 = 2.4e9 elements (9.7 GB): every tile's store offset passes 2^31, on
+    three unaligned shards; sampled rows at both ends against fp64 (TF32 bound / 3xTF32 1e-6)."""
+    from paper_1105_4424_b200 import builders
+    from paper_1105_4424_b200.executor import execute_schedule
+    from paper_1105_4424_b200.partition import build_schedule
+    M, N, K, D = 65536, 36864, 32, 3
+    g = torch.Generator(device="cuda").manual_seed(11)
+    a = torch.randn(M * K, device="cuda", generator=g)
+    b = torch.randn(K * N, device="cuda", generator=g)
+    model = builders.matmul_model(M, N, K)
+    c = execute_schedule(model, build_schedule(model, D), {"p_a": a, "p_b": b}, D, precision=precision,
+                         device_outputs=True).outputs["p_c"].view(M, N)
+    rows = torch.tensor([0, 1, 21845, 21846, 43690, 43691, M - 2, M - 1], device="cuda")
+    A, B = a.view(M, K), b.view(K, N)
+    ref = A[rows].double() @ B.double()
+    got = c[rows].double()
+    if precision == "default":
+        bound = (2.0 ** -9 + K * 2.0 ** -23) * (A[rows].double().abs() @ B.double().abs())
+        assert bool(((got - ref).abs() <= bound).all())
+    else:
+        assert float(torch.linalg.norm(got - ref) / torch.linalg.norm(ref)) <= 1e-6
+    del c, a, b
+    torch.cuda.empty_cache()
