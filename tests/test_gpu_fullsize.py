@@ -221,7 +221,7 @@ def test_c2_matmul_8192_3xtf32_fp32_faithful():
     assert ours <= 1e-6 and ours <= simt, (ours, simt)
 
 
-@pytest.mark.parametrize("precision", ["default", "3xtf32"])
+@pytest.mark.parametrize("precision", ["default", "3xtf32", "exact"])
 def test_matmul_output_beyond_2_31_elements(precision):
     """C with 65536 x 36864 = 2.4e9 elements (9.7 GB): every tile's store offset passes 2^31, on
     three unaligned shards; sampled rows at both ends against fp64 (TF32 bound / 3xTF32 1e-6)."""
@@ -242,6 +242,12 @@ def test_matmul_output_beyond_2_31_elements(precision):
     if precision == "default":
         bound = (2.0 ** -9 + K * 2.0 ** -23) * (A[rows].double().abs() @ B.double().abs())
         assert bool(((got - ref).abs() <= bound).all())
+    elif precision == "exact":                       # k ascending, a rounding per product and per add
+        an, bn = A[rows].cpu().numpy(), B.cpu().numpy()
+        want = np.zeros((len(rows), N), dtype=np.float32)
+        for k in range(K):
+            want = want + an[:, k:k + 1] * bn[k:k + 1, :]
+        assert np.array_equal(c[rows].cpu().numpy(), want)
     else:
         assert float(torch.linalg.norm(got - ref) / torch.linalg.norm(ref)) <= 1e-6
     del c, a, b
