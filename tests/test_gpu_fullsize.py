@@ -252,3 +252,38 @@ def test_matmul_output_beyond_2_31_elements(precision):
         assert float(torch.linalg.norm(got - ref) / torch.linalg.norm(ref)) <= 1e-6
     del c, a, b
     torch.cuda.empty_cache()
+
+
+def test_stencil_beyond_2_31_elements_sampled_rows():
+    """A 65536 x 36864 torus (2.4e9 elements, 9.7 GB each way) on three shards: offsets past 2^31
+    in the stencil kernel; the wrap rows, the shard seams and the middle against the oracle order
+    (`_stencil_rows_np`, equal to oracle/aol_oracle.c stencil_rows on a small torus)."""
+    from paper_1105_4424_b200 import builders
+    H, W, D = 65536, 36864, 3
+    t = orc.stencil_tilers(H, W)
+    w = orc.stencil_weights()
+    model = builders.tile_task_model(
+        "stencil", {"x": _spec(t["x"], "in"), "w": "in float32 [9]", "y": _spec(t["y"], "out")},
+        {k: _tiler(v) for k, v in t.items()}, (H, W))
+    xd = torch.randn(H * W, device="cuda", generator=torch.Generator(device="cuda").manual_seed(13))
+    ex = _executor(model, {"p_x": xd, "p_w": torch.from_numpy(w).cuda()}, D)
+    got = ex.outputs(on_device=True)["p_y"].view(H, W)
+    del ex
+    x = xd.cpu().numpy()
+    for lo in (0, H // 3 - 1, H // 2, 2 * H // 3, H - 2):
+        want = _stencil_rows_np(x, w, H, W, lo, lo + 2)
+        assert np.array_equal(got[lo:lo + 2].cpu().numpy().view(np.uint32), want.view(np.uint32)), lo
+    del got, xd
+    torch.cuda.empty_cache()
+
+
+def _stencil_rows_np(x, w, H, W, lo, hi):
+    """Oracle rows lo..hi-1 of the toroidal 3x3 stencil, taps row-major, each product and each
+    add rounded in float32 (the order orc.stencil_tilers' pattern walks)."""
+    x2 = x.reshape(H, W)
+    acc = np.zeros((hi - lo, W), dtype=np.float32)
+    for i in range(3):
+        rows = x2[[(r + i - 1) % H for r in range(lo, hi)]]
+        for j in range(3):
+            acc = acc + np.float32(w[i * 3 + j]) * np.roll(rows, 1 - j, axis=1)
+    return acc
