@@ -138,3 +138,22 @@ def test_c_oracle_matches_numpy_oracle_and_reference(golden):
     y = np.zeros_like(x)
     co.stencil_rows(x, data["stencil_32x48/w"], y, 32, 48, 0, 32)
     assert np.array_equal(y, data["stencil_32x48/out"])
+
+
+def test_fullsize_stencil_row_restatement_equals_c_oracle():
+    """tests/test_gpu_fullsize.py checks a 2.4e9-element torus on sampled rows with a numpy
+    restatement (`_stencil_rows_np`); pin it to the C oracle's stencil_rows on a small torus,
+    including the wrap rows and columns."""
+    from pathlib import Path
+    from oracle import c_oracle as co
+    path = Path(__file__).resolve().parent / "test_gpu_fullsize.py"
+    src = path.read_text()
+    ns = {}
+    exec(src[src.index("def _stencil_rows_np"):], {"np": np}, ns)
+    H, W = 37, 52
+    x = np.random.default_rng(2).standard_normal(H * W).astype(np.float32)
+    w = orc.stencil_weights()
+    want = np.zeros(H * W, np.float32)
+    co.stencil_rows(x, w, want, H, W, 0, H)
+    got = ns["_stencil_rows_np"](x, w, H, W, 0, H)
+    assert np.array_equal(got.ravel().view(np.uint32), want.view(np.uint32))
