@@ -1107,7 +1107,8 @@ class C1Workload(Workload):
         execute_schedule(self.model, self.schedule, self.dbind, 1, device_outputs=True)
 
     e2e_path = ("execute_schedule(model, schedule, pinned host bindings, 1, out={p_c: pinned buffer}): H2D of "
-                "A and B from pinned memory, the GEMM, C back into the caller's pinned buffer")
+                "A and B from pinned memory, the GEMM, C back into the caller's pinned buffer (steps back to back, "
+                "no L2 flush between them, unlike `value`: hence e2e can exceed value at this size)")
 
     def e2e_setup(self):
         self.e2e_bytes = (2 * self.n * self.n * 4, self.n * self.n * 4)
