@@ -675,3 +675,26 @@ def test_concurrent_calls_from_threads():
         t.join()
     exm.clear_prepared()
     assert not errors, errors[:5]
+
+
+def test_prepared_executor_survives_a_failed_call():
+    """A call whose binding is the wrong size raises MissingBinding from the prepared executor's
+    rebind; the entry's lock is released, and the next good call on the same cached executor
+    returns the right result."""
+    from paper_1105_4424_b200 import builders
+    from paper_1105_4424_b200 import executor as exm
+    from paper_1105_4424_b200.partition import build_schedule
+    n = 80
+    model = builders.matmul_model(n, n, n)
+    sched = build_schedule(model, 2)
+    rng = np.random.default_rng(6)
+    bind = {"p_a": rng.standard_normal(n * n, dtype=np.float32), "p_b": rng.standard_normal(n * n, dtype=np.float32)}
+    exm.clear_prepared()
+    want = exm.execute_schedule(model, sched, bind, 2, precision="exact").outputs["p_c"]
+    with pytest.raises(exm.MissingBinding):
+        exm.execute_schedule(model, sched, {"p_a": bind["p_a"][:-1], "p_b": bind["p_b"]}, 2, precision="exact")
+    (_, _, _, lock), = exm._PREPARED.values()
+    assert not lock.locked()
+    again = exm.execute_schedule(model, sched, bind, 2, precision="exact").outputs["p_c"]
+    assert np.array_equal(again, want)
+    exm.clear_prepared()
